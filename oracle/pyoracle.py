@@ -1,0 +1,299 @@
+"""ctypes front-end for the CHECKER libraries — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+arm may import this module.  It wraps:
+
+* ``oracle/liboracle.so``          — the C restatement (marsit_oracle.c), and
+* ``oracle/_ref/libmarsit_ref.so`` — the unmodified reference headers compiled
+  in place (ref_driver.cpp); present only where it was built from
+  /root/reference (it travels to the GPU box as a prebuilt file).
+
+All arrays are numpy; schedules are flat tables (phase, send_to, recv_from,
+segment) exactly like the product's C-ABI takes them.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libmarsit_ref.so")
+
+STATUS = {0: "ok", 1: "parameter_error", 2: "non_finite_error", 3: "protocol_error",
+          4: "unsupported_error", 9: "other"}
+
+_u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+_u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+_u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+
+
+def build() -> None:
+    """Compile the checker libraries (make -C oracle)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+_lib = None
+_ref = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(ORACLE_SO):
+            build()
+        L = C.CDLL(ORACLE_SO)
+        L.orc_mix.restype = C.c_uint64
+        L.orc_mix.argtypes = [C.c_uint64]
+        L.orc_stream_key.restype = C.c_uint64
+        L.orc_stream_key.argtypes = [C.c_uint64] * 5
+        L.orc_draw.restype = C.c_uint64
+        L.orc_draw.argtypes = [C.c_uint64, C.c_uint64]
+        for f in (L.orc_ring_schedule,):
+            f.restype = C.c_int
+            f.argtypes = [C.c_uint32, _u8p, _u32p, _u32p, _u32p]
+        L.orc_torus_schedule.restype = C.c_int
+        L.orc_torus_schedule.argtypes = [C.c_uint32, C.c_uint32, _u8p, _u32p, _u32p, _u32p]
+        L.orc_pack_signs.restype = None
+        L.orc_pack_signs.argtypes = [_f64p, C.c_size_t, _u64p]
+        L.orc_merge_signs.restype = C.c_int
+        L.orc_merge_signs.argtypes = [_u64p, C.c_uint32, _u64p, C.c_uint32, C.c_size_t,
+                                      C.c_uint64, C.POINTER(C.c_uint64), _u64p]
+        L.orc_allreduce_sign.restype = C.c_int
+        L.orc_allreduce_sign.argtypes = [C.c_uint32, C.c_uint32, C.c_size_t, _u64p, C.c_uint32,
+                                         _u8p, _u32p, _u32p, _u32p, C.c_uint64, C.c_uint64,
+                                         _u64p, _u32p, _u64p, C.POINTER(C.c_uint64),
+                                         C.POINTER(C.c_uint64)]
+        L.orc_allreduce_dense.restype = C.c_int
+        L.orc_allreduce_dense.argtypes = [C.c_uint32, C.c_uint32, C.c_size_t, _f64p,
+                                          C.c_uint32, _u8p, _u32p, _u32p, _u32p, _f64p, _u64p,
+                                          C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.orc_marsit_round.restype = C.c_int
+        L.orc_marsit_round.argtypes = [C.c_uint64, C.c_int, C.c_uint64, C.c_double, C.c_uint32,
+                                       C.c_uint32, C.c_size_t, _f64p, _f64p, C.c_uint32, _u8p,
+                                       _u32p, _u32p, _u32p, C.c_uint64, _f64p, _f64p, _u64p,
+                                       C.POINTER(C.c_int), _u64p, C.POINTER(C.c_uint64),
+                                       C.POINTER(C.c_uint64)]
+        L.orc_gen_dyadic.restype = None
+        L.orc_gen_dyadic.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_size_t, _f64p]
+        L.orc_gen_correlated.restype = None
+        L.orc_gen_correlated.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_size_t, _f64p]
+        _lib = L
+    return _lib
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref():
+    """The reference compiled from its own headers (None when not built)."""
+    global _ref
+    if _ref is None:
+        if not ref_available():
+            return None
+        R = C.CDLL(REF_SO)
+        R.ref_build_schedule.restype = C.c_int
+        R.ref_build_schedule.argtypes = [C.c_int, C.c_uint32, C.c_uint32, _u8p, _u32p, _u32p,
+                                         _u32p]
+        R.ref_stream_draws.restype = None
+        R.ref_stream_draws.argtypes = [C.c_uint64] * 5 + [C.c_size_t, _u64p]
+        R.ref_pack_signs.restype = C.c_int
+        R.ref_pack_signs.argtypes = [_f64p, C.c_size_t, _u64p]
+        R.ref_merge_signs.restype = C.c_int
+        R.ref_merge_signs.argtypes = [_u64p, C.c_uint32, _u64p, C.c_uint32, C.c_size_t,
+                                      C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                      C.c_uint64, _u64p, C.POINTER(C.c_uint64)]
+        R.ref_allreduce_sign.restype = C.c_int
+        R.ref_allreduce_sign.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_size_t, _u64p,
+                                         C.c_uint64, C.c_uint64, _u64p, _u32p, _u64p,
+                                         C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        R.ref_marsit_round.restype = C.c_int
+        R.ref_marsit_round.argtypes = [C.c_uint64, C.c_int, C.c_uint64, C.c_double, C.c_int,
+                                       C.c_uint32, C.c_uint32, C.c_size_t, _f64p, _f64p,
+                                       C.c_uint64, _f64p, _f64p, _u64p, C.POINTER(C.c_int),
+                                       _u64p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        R.ref_bench_create.restype = C.c_void_p
+        R.ref_bench_create.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_size_t, C.c_uint64]
+        R.ref_bench_round.restype = C.c_double
+        R.ref_bench_round.argtypes = [C.c_void_p, C.c_uint64]
+        R.ref_bench_destroy.restype = None
+        R.ref_bench_destroy.argtypes = [C.c_void_p]
+        _ref = R
+    return _ref
+
+
+# ----------------------------------------------------------------------------
+# Schedules
+# ----------------------------------------------------------------------------
+@dataclass
+class Tables:
+    topology: int  # 0 ring, 1 torus
+    a: int
+    b: int
+    workers: int
+    segments: int
+    phase: np.ndarray      # [steps] uint8 (0 reduce, 1 gather)
+    send_to: np.ndarray    # [steps, workers] uint32
+    recv_from: np.ndarray
+    segment: np.ndarray
+
+    @property
+    def steps(self) -> int:
+        return int(self.phase.shape[0])
+
+
+def schedule(topology: str, a: int, b: int = 0, use_ref: bool = False) -> Tables:
+    m = a if topology == "ring" else a * b
+    n = max(2 * (m - 1), 1)
+    ph = np.zeros(n, np.uint8)
+    st = np.zeros(n * m, np.uint32)
+    rf = np.zeros(n * m, np.uint32)
+    sg = np.zeros(n * m, np.uint32)
+    if use_ref:
+        k = ref().ref_build_schedule(0 if topology == "ring" else 1, a, b, ph, st, rf, sg)
+    elif topology == "ring":
+        k = lib().orc_ring_schedule(a, ph, st, rf, sg)
+    else:
+        k = lib().orc_torus_schedule(a, b, ph, st, rf, sg)
+    if k < 0:
+        raise ValueError(STATUS[-k])
+    return Tables(0 if topology == "ring" else 1, a, b, m, m, ph[:k].copy(),
+                  st[:k * m].reshape(k, m).copy(), rf[:k * m].reshape(k, m).copy(),
+                  sg[:k * m].reshape(k, m).copy())
+
+
+def _flat(t: Tables):
+    return (np.ascontiguousarray(t.phase), np.ascontiguousarray(t.send_to.ravel()),
+            np.ascontiguousarray(t.recv_from.ravel()), np.ascontiguousarray(t.segment.ravel()))
+
+
+# ----------------------------------------------------------------------------
+# Primitives
+# ----------------------------------------------------------------------------
+def words64(n_bits: int) -> int:
+    return (n_bits + 63) // 64
+
+
+def stream_key(seed, purpose, w, t, s) -> int:
+    return lib().orc_stream_key(seed, purpose, w, t, s)
+
+
+def draw(key: int, n: int) -> int:
+    return lib().orc_draw(key, n)
+
+
+def pack_signs(v: np.ndarray) -> np.ndarray:
+    v = np.ascontiguousarray(v, np.float64)
+    out = np.zeros(max(words64(v.size), 1), np.uint64)
+    lib().orc_pack_signs(v, v.size, out)
+    return out[:words64(v.size)]
+
+
+def merge_signs(recv, c_recv, local, c_local, length, key, used=0):
+    out = np.zeros(max(words64(length), 1), np.uint64)
+    u = C.c_uint64(used)
+    rc = lib().orc_merge_signs(np.ascontiguousarray(recv, np.uint64), c_recv,
+                               np.ascontiguousarray(local, np.uint64), c_local, length, key,
+                               C.byref(u), out)
+    if rc:
+        raise RuntimeError(STATUS[rc])
+    return out[:words64(length)], u.value
+
+
+def gen_dyadic(seed, w, t, dim) -> np.ndarray:
+    out = np.zeros(dim, np.float64)
+    lib().orc_gen_dyadic(seed, w, t, dim, out)
+    return out
+
+
+def gen_correlated(seed, w, t, dim) -> np.ndarray:
+    out = np.zeros(dim, np.float64)
+    lib().orc_gen_correlated(seed, w, t, dim, out)
+    return out
+
+
+@dataclass
+class SignResult:
+    state: np.ndarray      # [workers, segments, words] uint64
+    counts: np.ndarray     # [workers, segments] uint32
+    bits_per_worker: np.ndarray
+    reduce_bits: int
+    gather_bits: int
+
+
+def allreduce_sign(tables: Tables, signs: np.ndarray, seg_len: int, seed: int, rnd: int,
+                   use_ref: bool = False) -> SignResult:
+    W, S = tables.workers, tables.segments
+    nw = words64(seg_len)
+    signs = np.ascontiguousarray(signs, np.uint64).reshape(W * S * nw)
+    state = np.zeros(W * S * nw + 1, np.uint64)
+    counts = np.zeros(W * S, np.uint32)
+    bpw = np.zeros(W, np.uint64)
+    rb, gb = C.c_uint64(), C.c_uint64()
+    if use_ref:
+        rc = ref().ref_allreduce_sign(tables.topology, tables.a, tables.b, seg_len, signs, seed,
+                                      rnd, state, counts, bpw, C.byref(rb), C.byref(gb))
+    else:
+        ph, st, rf, sg = _flat(tables)
+        rc = lib().orc_allreduce_sign(W, S, seg_len, signs, tables.steps, ph, st, rf, sg, seed,
+                                      rnd, state, counts, bpw, C.byref(rb), C.byref(gb))
+    if rc:
+        raise RuntimeError(STATUS[rc])
+    return SignResult(state[:W * S * nw].reshape(W, S, nw), counts.reshape(W, S), bpw,
+                      rb.value, gb.value)
+
+
+@dataclass
+class RoundResult:
+    status: int
+    update: np.ndarray
+    comp: np.ndarray
+    agg_bits: np.ndarray
+    full_precision: bool
+    bits_per_worker: np.ndarray
+    reduce_bits: int
+    gather_bits: int
+
+
+def marsit_round(tables: Tables, t: int, period, eta_s: float, grads: np.ndarray,
+                 comp: np.ndarray, seed: int, use_ref: bool = False) -> RoundResult:
+    """grads/comp: [workers, dim] float64.  period None = never."""
+    W = tables.workers
+    grads = np.ascontiguousarray(grads, np.float64)
+    comp = np.ascontiguousarray(comp, np.float64)
+    dim = grads.shape[1]
+    upd = np.zeros(dim, np.float64)
+    cout = np.zeros((W, dim), np.float64)
+    agg = np.zeros(words64(dim) + 1, np.uint64)
+    fp = C.c_int(0)
+    bpw = np.zeros(W, np.uint64)
+    rb, gb = C.c_uint64(), C.c_uint64()
+    hp = 0 if period is None else 1
+    K = 0 if period is None else int(period)
+    if use_ref:
+        rc = ref().ref_marsit_round(t, hp, K, eta_s, tables.topology, tables.a, tables.b, dim,
+                                    grads.ravel(), comp.ravel(), seed, upd, cout.ravel(), agg,
+                                    C.byref(fp), bpw, C.byref(rb), C.byref(gb))
+    else:
+        ph, st, rf, sg = _flat(tables)
+        rc = lib().orc_marsit_round(t, hp, K, eta_s, W, tables.segments, dim, grads.ravel(),
+                                    comp.ravel(), tables.steps, ph, st, rf, sg, seed, upd,
+                                    cout.ravel(), agg, C.byref(fp), bpw, C.byref(rb),
+                                    C.byref(gb))
+    return RoundResult(rc, upd, cout, agg[:words64(dim)], bool(fp.value), bpw, rb.value,
+                       gb.value)
+
+
+def fnv1a64(words: np.ndarray) -> int:
+    """FNV-1a-64 over the little-endian bytes of u64 words (SURVEY §8c anchors)."""
+    h = 0xcbf29ce484222325
+    for byte in np.ascontiguousarray(words, "<u8").tobytes():
+        h ^= byte
+        h = (h * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return h
