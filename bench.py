@@ -1,0 +1,416 @@
+#!/usr/bin/env python3
+"""Marsit sign all-reduce round on B200 — the driver's benchmark.
+
+Default (N=1): BASELINE config C3 — ring all-reduce of a 25.6M-element fp32
+gradient over M=8 workers (all simulated on the one GPU), with the global
+compensation update, one step = one marsit_round sign round (t >= 1).
+Under torchrun with N ranks the same M=8 workers are split 8/N per GPU
+(strong scaling: total work fixed) and the path exchanges packed segments
+with NCCL.
+
+Metric: sign-allreduce Gelem/s = D / step time (all-reduce algbw convention).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sign-allreduce Gelem/s (25.6M grad, 1/2/4/8 B200) + % HBM/NVLink roofline"
+ETA = 2.0 ** -10
+SEED = 2026
+
+CONFIGS = {
+    # id: (D, topology, a, b)
+    "c1": (1_000_000, "ring", 4, 0),
+    "c2": (61_000_000, "ring", 8, 0),
+    "c3": (25_600_000, "ring", 8, 0),
+    "c4": (60_200_000, "torus", 2, 4),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    ap.add_argument("--recipe", type=int, default=0, help="0 dyadic (independent), 1 correlated")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--min-busy-s", type=float, default=1.5,
+                    help="keep the GPU busy at least this long before timing (clock sampling)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,utilization.gpu,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        rows = []
+        for ts, line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 10:
+                continue
+            rows.append((ts, parts))
+        sel = [p for ts, p in rows if t0 - 0.15 <= ts <= t1 + 0.15] or [p for _, p in rows]
+        if not sel:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        busy = [p for p in sel if p[4].isdigit() and int(p[4]) > 0] or sel
+        sm = [float(p[1]) for p in busy if p[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for p in busy:
+            for n, v in zip(names, p[6:10]):
+                if "Active" in v and "Not" not in v:
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(busy[0][2]) if busy[0][2].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(busy)}
+
+
+# ----------------------------------------------------------------------------
+# CPU baselines
+# ----------------------------------------------------------------------------
+def cpu_baseline(cfg_id: str, sample_dim: int, rounds: int = 3):
+    """The reference's own marsit_round (oracle/_ref, compiled from the unmodified
+    headers) or, where it was not built, the C restatement; 1 thread."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    import pyoracle as O
+    D, topo, a, b = CONFIGS[cfg_id]
+    cores = 1
+    if O.ref_available():
+        R = O.ref()
+        h = R.ref_bench_create(0 if topo == "ring" else 1, a, b, sample_dim, SEED)
+        R.ref_bench_round(h, 1)  # warm-up round
+        times = [R.ref_bench_round(h, t) for t in range(2, 2 + rounds)]
+        R.ref_bench_destroy(h)
+        kind = "reference"
+    else:
+        O.build() if not os.path.exists(O.ORACLE_SO) else None
+        T = O.schedule(topo, a, b)
+        g = np.stack([O.gen_dyadic(SEED, w, 1, sample_dim) for w in range(T.workers)])
+        comp = np.zeros_like(g)
+        times = []
+        for t in range(1, 2 + rounds):
+            t0 = time.perf_counter()
+            r = O.marsit_round(T, t, None, ETA, g, comp, SEED)
+            dt = (time.perf_counter() - t0) * 1e3
+            comp = r.comp
+            if t > 1:
+                times.append(dt)
+        kind = "port"
+    ms = min(times)
+    return {"value": sample_dim / (ms * 1e-3) / 1e9, "unit": "Gelem/s", "cores": cores,
+            "kind": kind, "ms_per_round": ms,
+            "sample": f"{topo} M={a * (b or 1)} D={sample_dim} sign round (t>=1, K=never), "
+                      f"best of {rounds} warm rounds, 1 thread",
+            "host_cpu": _cpu_model(), "nproc": os.cpu_count()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    D = CONFIGS[args.config][0]
+    sample = max(D // 10, 1000)
+    steps = []
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+    _, topo, a, b = CONFIGS[args.config]
+    if O.ref_available():
+        R = O.ref()
+        h = R.ref_bench_create(0 if topo == "ring" else 1, a, b, sample, SEED)
+        for t in range(1, args.warmup + 1):
+            R.ref_bench_round(h, t)
+        for t in range(args.warmup + 1, args.warmup + args.steps + 1):
+            steps.append(R.ref_bench_round(h, t))
+        R.ref_bench_destroy(h)
+        kind = "reference"
+    else:
+        cb = cpu_baseline(args.config, sample, rounds=max(args.steps, 1))
+        steps = [cb["ms_per_round"]]
+        kind = "port"
+    ms = sum(steps) / len(steps)
+    val = sample / (ms * 1e-3) / 1e9
+    line = {"metric": METRIC, "value": val, "unit": "Gelem/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SURVEY §8c dyadic recipe)", "impl": "reference",
+            "config": {"workload": f"{args.config}: {topo} M={a * (b or 1)} D={D} "
+                                   f"(timed on a D={sample} sample)",
+                       "sample_dim": sample},
+            "cpu_baseline": {"value": val, "unit": "Gelem/s", "cores": 1, "kind": kind,
+                             "sample": f"D={sample} (1/10 of D), one marsit_round per step, "
+                                       "1 thread (the reference is single-threaded)"},
+            "e2e": {"value": val, "unit": "Gelem/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2204_06787_b200 as mb
+
+    D, topo, a, b = CONFIGS[args.config]
+    sched = mb.build_ring_schedule(a) if topo == "ring" else mb.build_torus_schedule(a, b)
+    M = sched.workers
+    nccl_id = None
+    if world > 1:
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(mb.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().tolist())
+    ctx = mb.Context(D, sched, torch.float32, local_rank, nranks=world, rank=rank,
+                     nccl_id=nccl_id)
+    ml, w0 = ctx.local_workers, ctx.first_worker
+    grads = [torch.empty(D, device=dev) for _ in range(ml)]
+    for i in range(ml):
+        mb.fill_recipe(grads[i], args.recipe, SEED, w0 + i, 1)
+    comp = [torch.zeros(D, device=dev) for _ in range(ml)]
+    stream = torch.cuda.current_stream(dev)
+
+    def step(t):
+        ctx.sign_round(t, ETA, SEED, grads, comp)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    # warm-up: at least W steps and at least min_busy_s of GPU work (clock sampling)
+    t = 1
+    t_busy0 = time.time()
+    n_warm = 0
+    while n_warm < max(args.warmup, 3) or time.time() - t_busy0 < args.min_busy_s:
+        step(t)
+        t += 1
+        n_warm += 1
+        if n_warm % 20 == 0:
+            torch.cuda.synchronize(dev)
+    torch.cuda.synchronize(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    ctx.set_timing(True)
+    ctx.timing(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    wall0 = time.time()
+    e0.record(stream)
+    for k in range(args.steps):
+        step(t)
+        t += 1
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    wall1 = time.time()
+    phases = ctx.timing(reset=True)
+    ctx.set_timing(False)
+    ctx.check()
+    ms = e0.elapsed_time(e1) / args.steps
+    sampler.stop()
+    clocks = sampler.summary(wall0, wall1)
+    if world > 1:
+        tm = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        ms = float(tm.item())
+
+    # e2e through the public API with host buffers (pinned), copies inside the region
+    host_g = [torch.empty(D, dtype=torch.float32, pin_memory=True) for _ in range(ml)]
+    for i in range(ml):
+        host_g[i].copy_(grads[i])
+    nwords = (D + 63) // 64
+    agg_dev = torch.empty(nwords, dtype=torch.int64, device=dev)
+    agg_host = torch.empty(nwords, dtype=torch.int64, pin_memory=True)
+    dev_g = [torch.empty_like(x) for x in grads]
+
+    def e2e_step(t):
+        for i in range(ml):
+            dev_g[i].copy_(host_g[i], non_blocking=True)
+        ctx.sign_round(t, ETA, SEED, dev_g, comp, agg_bits=agg_dev)
+        agg_host.copy_(agg_dev, non_blocking=True)
+
+    e2e_step(t)
+    t += 1
+    torch.cuda.synchronize(dev)
+    barrier()
+    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    x0.record(stream)
+    for k in range(args.e2e_steps):
+        e2e_step(t)
+        t += 1
+    x1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    e2e_ms = x0.elapsed_time(x1) / args.e2e_steps
+    if world > 1:
+        tm = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tm.item())
+
+    # roofline: dominant kernel = decode+compensation (K3/K4), 12.125 B per
+    # worker-element (read g, c; write c'; read 1/8 B of aggregate bits)
+    hbm, hbm_kind = peaks()
+    per_launch = {}
+    for name, (pms, nl) in phases.items():
+        if nl:
+            per_launch[name] = pms / nl
+    dec_ms = per_launch.get("decode_comp", float("nan"))
+    ext_ms = per_launch.get("sign_extract", float("nan"))
+    dec_bytes = ml * D * 12.125
+    ext_bytes = ml * D * 8.125
+    dec_gbs = dec_bytes / (dec_ms * 1e-3) / 1e9
+    step_bytes = ml * D * 20.25
+    step_gbs = step_bytes / (ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        traffic = tr.get(f"{args.config}_g{world}_decode_bytes")
+    except Exception:
+        pass
+    launches = sum(nl for _, nl in phases.values())
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": D / (ms * 1e-3) / 1e9,
+            "unit": "Gelem/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": n_warm,
+            "ms_per_step": ms,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (SURVEY §8c dyadic recipe, on-device generation)"
+                    if args.recipe == 0 else "synthetic (SURVEY §8d correlated recipe)",
+            "config": {"workload": f"{args.config}: {topo} all-reduce M={M} workers "
+                                   f"({ml} per GPU), D={D}, sign round + compensation",
+                       "D": D, "workers": M, "topology": topo,
+                       "parallelism": f"{world} rank(s) x {ml} workers",
+                       "l2": "inputs (%.1f GB) > L2 (126 MB): no flush needed"
+                             % (2 * ml * D * 4 / 1e9)},
+            "worker_gelem_s": M * D / (ms * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "kernel": "decode_comp (K3+K4)",
+                         "achieved": dec_gbs, "peak": hbm, "unit": "GB/s",
+                         "frac": dec_gbs / hbm, "traffic": traffic,
+                         "peak_kind": hbm_kind,
+                         "algorithmic_bytes_per_launch": dec_bytes,
+                         "avg_launch_ms": dec_ms},
+            "step_roofline": {"bytes_per_step": step_bytes, "achieved": step_gbs,
+                              "frac": step_gbs / hbm,
+                              "note": "20.25 B per worker-element two-pass floor (SURVEY §8d)"},
+            "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items() if v[1]},
+            "sign_extract_gbs": ext_bytes / (ext_ms * 1e-3) / 1e9,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "e2e": {"value": D / (e2e_ms * 1e-3) / 1e9, "unit": "Gelem/s",
+                    "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": ml * D * 4,
+                    "d2h_bytes_per_step": nwords * 8,
+                    "path": "Context.sign_round (C-ABI marsit_sign_round) with pinned host "
+                            "gradients copied in and aggregate bits copied out every step"},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = cpu_baseline(args.config, D // 10)
+            except Exception as e:  # pragma: no cover
+                line["cpu_baseline"] = {"value": None, "error": str(e)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,193 @@
+/*
+ * marsit_b200.h — C-ABI of the B200-native Marsit sign-round path.
+ *
+ * This is the drop-in boundary for the reference's synchronisation path
+ * (/root/reference/proj/include/marsit/, header-only C++20).  The reference
+ * has no FFI; its public interface is a set of C++ functions, each of which
+ * an entry point below replaces (file:line cited per function).  The C++
+ * shim in include/marsit_b200/drop_in.hpp re-exposes the reference's exact
+ * C++ signatures on top of this ABI; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "d_" pointers are CUDA device pointers,
+ *    everything else is host memory.  `stream` is a cudaStream_t (NULL = the
+ *    legacy default stream).
+ *  - Every entry point returns a marsit_status; on failure the thread-local
+ *    message is available from marsit_last_error().  Status codes map 1:1 to
+ *    the reference exception taxonomy (errors.hpp:10-42).
+ *  - Round entry points are asynchronous on `stream`.  Data-dependent errors
+ *    that the reference raises mid-round (non_finite_error from
+ *    DenseVector's constructor, dense_vector.hpp:25-29) are latched on the
+ *    device and reported by marsit_ctx_check() (which synchronises the
+ *    stream).  Validation errors are returned immediately.
+ *  - One host thread per context; no global mutable state.
+ *  - There is no CPU fallback: without a CUDA device every compute entry
+ *    point returns MARSIT_ECUDA.
+ */
+#ifndef MARSIT_B200_H
+#define MARSIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MARSIT_B200_ABI_VERSION 1
+
+typedef enum marsit_status {
+    MARSIT_OK = 0,
+    MARSIT_EPARAM = 1,       /* marsit::parameter_error   errors.hpp:11-14 */
+    MARSIT_ENONFINITE = 2,   /* marsit::non_finite_error  errors.hpp:19-22 */
+    MARSIT_EPROTOCOL = 3,    /* marsit::protocol_error    errors.hpp:26-29 */
+    MARSIT_EUNSUPPORTED = 4, /* marsit::unsupported_error errors.hpp:33-36 */
+    MARSIT_ECUDA = 5,        /* CUDA runtime failure / no device        */
+    MARSIT_ENCCL = 6         /* NCCL failure (multi-GPU contexts)       */
+} marsit_status;
+
+typedef enum marsit_dtype { MARSIT_F32 = 0, MARSIT_F64 = 1 } marsit_dtype;
+
+/* schedule.hpp:12 Phase */
+typedef enum marsit_phase { MARSIT_REDUCE = 0, MARSIT_GATHER = 1 } marsit_phase;
+
+/* ------------------------------------------------------------------------
+ * Schedules (host objects).  Replace marsit::Schedule and its builders.
+ * ---------------------------------------------------------------------- */
+typedef struct marsit_schedule marsit_schedule;
+
+/* build_ring_schedule (schedule.hpp:61-94): m >= 2 else EPARAM. */
+marsit_status marsit_schedule_ring(uint32_t m, marsit_schedule** out);
+/* build_torus_schedule (schedule.hpp:110-196): rows, cols >= 2 else EPARAM. */
+marsit_status marsit_schedule_torus(uint32_t rows, uint32_t cols, marsit_schedule** out);
+/* An arbitrary Schedule given as flat tables (phase[steps];
+ * send_to/recv_from/segment[steps*workers]); validated like
+ * Schedule::validate (schedule.hpp:38-54) -> EPROTOCOL. */
+marsit_status marsit_schedule_from_tables(uint32_t workers, uint32_t segments, uint32_t steps,
+                                          const uint8_t* phase, const uint32_t* send_to,
+                                          const uint32_t* recv_from, const uint32_t* segment,
+                                          marsit_schedule** out);
+marsit_status marsit_schedule_info(const marsit_schedule* s, uint32_t* workers,
+                                   uint32_t* segments, uint32_t* steps);
+marsit_status marsit_schedule_tables(const marsit_schedule* s, uint8_t* phase,
+                                     uint32_t* send_to, uint32_t* recv_from, uint32_t* segment);
+void marsit_schedule_destroy(marsit_schedule* s);
+
+/* The compiled merge plan of one segment (host introspection, no device
+ * needed).  Node ids 0..workers-1 are the workers' own packed segments;
+ * node workers+k is the output of merge k.  offset_src is the index of the
+ * previous merge of the same (receiver, segment) stream, whose draws this
+ * merge continues (allreduce.hpp:167-177), or -1. */
+typedef struct marsit_merge_info {
+    uint32_t recv_node, local_node, receiver, c_recv, c_local;
+    int32_t offset_src;
+    uint32_t stage;
+} marsit_merge_info;
+marsit_status marsit_schedule_plan(const marsit_schedule* s, uint32_t segment,
+                                   uint32_t capacity, marsit_merge_info* merges,
+                                   uint32_t* n_merges, uint32_t* final_node,
+                                   uint32_t* final_count);
+
+/* ------------------------------------------------------------------------
+ * Contexts.  A context binds (D, schedule, dtype, device, rank layout) and
+ * owns all device scratch: per-segment packed-sign buffers, the compiled
+ * merge plan, look-back flags, the NCCL communicator.
+ * ---------------------------------------------------------------------- */
+typedef struct marsit_ctx marsit_ctx;
+
+typedef struct marsit_ctx_desc {
+    uint64_t dim;                     /* D >= 1                                   */
+    const marsit_schedule* schedule;  /* M workers, M segments                    */
+    marsit_dtype dtype;               /* element type of grads / compensation      */
+    int device;                       /* CUDA device ordinal                       */
+    uint32_t nranks;                  /* processes sharing the M workers (>= 1)    */
+    uint32_t rank;                    /* this process: workers [rank*M/nranks, ..) */
+    const void* nccl_id;              /* 128-byte ncclUniqueId when nranks > 1     */
+} marsit_ctx_desc;
+
+marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out);
+void marsit_ctx_destroy(marsit_ctx* ctx);
+/* The worker ids resident on this rank: [*first, *first + *count). */
+marsit_status marsit_ctx_local_workers(const marsit_ctx* ctx, uint32_t* first, uint32_t* count);
+
+/* Sign round: the sign branch of marsit_round (sync.hpp:60-120, 91-118).
+ *  d_grads[i], d_comp[i]: the i-th LOCAL worker's scaled gradient and
+ *    compensation (D elements of dtype).
+ *  d_comp_out[i]: receives c' = (g + c) - g_t; may equal d_comp[i] (in place).
+ *  d_agg_bits (optional): aggregate_bits in the reference layout, ceil(D/64)
+ *    little-endian u64 words, truncated to D (sync.hpp:103-112).
+ *  d_update (optional): global_update g_t = +-eta_s (D elements of dtype). */
+marsit_status marsit_sign_round(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_t global_seed,
+                                const void* const* d_grads, const void* const* d_comp,
+                                void* const* d_comp_out, uint64_t* d_agg_bits, void* d_update,
+                                void* stream);
+
+/* Dense round (sync.hpp:78-87 -> allreduce_dense, allreduce.hpp:98-130):
+ * d_mean = mean of (g + c) summed in schedule order; d_comp_out set to 0. */
+marsit_status marsit_dense_round(marsit_ctx* ctx, uint64_t t, const void* const* d_grads,
+                                 const void* const* d_comp, void* const* d_comp_out, void* d_mean,
+                                 void* stream);
+
+/* marsit_round (sync.hpp:60-120): dense iff period != 0 && t % period == 0,
+ * else sign.  period == 0 means "never" (SyncConfig with no K).  d_update
+ * receives g_t for both kinds of round (required for dense rounds).
+ * *full_precision (optional, host) reports which branch ran. */
+marsit_status marsit_round(marsit_ctx* ctx, uint64_t t, uint64_t period, double eta_s,
+                           uint64_t global_seed, const void* const* d_grads,
+                           const void* const* d_comp, void* const* d_comp_out,
+                           uint64_t* d_agg_bits, void* d_update, int* full_precision,
+                           void* stream);
+
+/* allreduce_sign (allreduce.hpp:148-189) on already packed signs.
+ *  d_signs: the LOCAL workers' packed segments, [local worker][segment][ceil(L/64)] u64
+ *    with L = ceil(D/M) (the reference's PackedSignVector words).
+ *  d_out: the consensus aggregate, [segment][ceil(L/64)] u64.
+ *  counts (optional, host): [segment] contribution counts (all M for ring/torus). */
+marsit_status marsit_allreduce_sign(marsit_ctx* ctx, uint64_t round, uint64_t global_seed,
+                                    const uint64_t* d_signs, uint64_t* d_out, uint32_t* counts,
+                                    void* stream);
+
+/* Error-compensated sign extraction alone (sync.hpp:71-76 + segmentation.hpp:32-53
+ * + sign_vector.hpp:67-73): d_signs_out as in marsit_allreduce_sign's input. */
+marsit_status marsit_sign_extract(marsit_ctx* ctx, const void* const* d_grads,
+                                  const void* const* d_comp, uint64_t* d_signs_out,
+                                  void* stream);
+
+/* One merge_signs (merge.hpp:34-58) on the device, synchronous.  `key` is the
+ * stream's constructor state (rng.hpp:30-38), `used` the draws it has already
+ * produced; *consumed (host) receives the draws this merge consumed. */
+marsit_status marsit_merge_signs(const uint64_t* d_recv, uint32_t c_recv, const uint64_t* d_local,
+                                 uint32_t c_local, uint64_t len, uint64_t key, uint64_t used,
+                                 uint64_t* d_out, uint64_t* consumed, int device, void* stream);
+
+/* BitsAccount of one round (bits_account.hpp:15-40; allreduce.hpp:113, 182).
+ * per_worker: [M] (optional). */
+marsit_status marsit_bits_account(const marsit_ctx* ctx, int dense, uint64_t* per_worker,
+                                  uint64_t* reduce_bits, uint64_t* gather_bits, uint64_t* total);
+
+/* Synchronise `stream` and report latched device errors (non-finite values,
+ * missing contributions).  Clears the latch. */
+marsit_status marsit_ctx_check(marsit_ctx* ctx, void* stream);
+
+/* Per-phase device timing (CUDA events on the launching stream).
+ * Phases: 0 sign_extract, 1 exchange, 2 merge, 3 allgather, 4 decode_comp,
+ * 5 export, 6 dense.  ms[i] accumulates; launches[i] counts kernel launches. */
+#define MARSIT_N_PHASES 7
+marsit_status marsit_ctx_set_timing(marsit_ctx* ctx, int enable);
+marsit_status marsit_ctx_timing(marsit_ctx* ctx, float* ms, uint64_t* launches, int reset);
+
+/* Synthetic input recipes generated on the device:
+ * recipe 0 = dyadic, 1 = correlated.  d_out: D elements of dtype. */
+marsit_status marsit_fill_recipe(int recipe, uint64_t seed, uint64_t worker, uint64_t round,
+                                 uint64_t dim, marsit_dtype dtype, void* d_out, void* stream);
+
+/* ncclGetUniqueId for multi-rank contexts (128 bytes). */
+marsit_status marsit_nccl_unique_id(void* out128);
+
+const char* marsit_last_error(void);
+int marsit_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MARSIT_B200_H */

@@ -1,0 +1,752 @@
+// kernels.cu — sm_100a kernels of the Marsit sign round.
+//
+//   K1 extract_kernel   u = g + c, bit = (u >= 0), packed per segment
+//                       (sync.hpp:71-76, segmentation.hpp:32-53, sign_vector.hpp:67-73)
+//   K2 merge_kernel     the segment's whole merge DAG, tile by tile, with one
+//                       decoupled look-back scan of popcount(r ^ l) per merge
+//                       for the coin stream offsets (merge.hpp:34-58,
+//                       allreduce.hpp:148-189, rng.hpp:28-54)
+//   K3/K4 decode_kernel g_t = +-eta_s from the aggregate bits and the
+//                       compensation update c' = u - g_t fused in one pass
+//                       (sync.hpp:103-118, sign_vector.hpp:77-89)
+//   export_bits_kernel  aggregate bits in the reference's whole-vector layout
+//   dense kernels       allreduce_dense in schedule order (allreduce.hpp:98-130)
+//
+// All of it is HBM / integer-ALU work: no tensor cores are involved.  The
+// streaming kernels use 128-bit coalesced loads, warp ballots for packing and
+// grids sized to the SM count; the merge kernel keeps every segment in L2.
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace marsit_b200 {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// Counter-based RNG (rng.hpp:28-73).  Draw n of a stream = mix(key + (n+1)γ).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint64_t stream_key(uint64_t seed, uint64_t purpose, uint64_t w,
+                                               uint64_t t, uint64_t s) {
+    uint64_t h = mix64(seed ^ 0x6a09e667f3bcc909ull);
+    h = mix64(h ^ (purpose * kGamma));
+    h = mix64(h ^ ((w + 1) * kGamma));
+    h = mix64(h ^ ((t + 1) * kGamma));
+    return mix64(h ^ ((s + 1) * kGamma));
+}
+
+// ---------------------------------------------------------------------------
+// Memory helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Streaming 128-bit loads that do not allocate in L1 (each byte is read once).
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p));
+    return v;
+}
+
+// Coherent variant for data the same kernel overwrites (in-place compensation).
+__device__ __forceinline__ float4 ld_stream_rw(const float4* p) {
+    float4 v;
+    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double2 ld_stream_rw(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p));
+    return v;
+}
+
+template <typename T>
+struct Quad {
+    T v[4];
+};
+
+// Four consecutive elements; `p` is 4-element aligned (16 B for float, 32 B for double).
+__device__ __forceinline__ Quad<float> load4(const float* p) {
+    float4 a = ld_stream(reinterpret_cast<const float4*>(p));
+    return {{a.x, a.y, a.z, a.w}};
+}
+__device__ __forceinline__ Quad<double> load4(const double* p) {
+    double2 a = ld_stream(reinterpret_cast<const double2*>(p));
+    double2 b = ld_stream(reinterpret_cast<const double2*>(p) + 1);
+    return {{a.x, a.y, b.x, b.y}};
+}
+__device__ __forceinline__ Quad<float> load4_rw(const float* p) {
+    float4 a = ld_stream_rw(reinterpret_cast<const float4*>(p));
+    return {{a.x, a.y, a.z, a.w}};
+}
+__device__ __forceinline__ Quad<double> load4_rw(const double* p) {
+    double2 a = ld_stream_rw(reinterpret_cast<const double2*>(p));
+    double2 b = ld_stream_rw(reinterpret_cast<const double2*>(p) + 1);
+    return {{a.x, a.y, b.x, b.y}};
+}
+__device__ __forceinline__ void store4(float* p, const Quad<float>& q) {
+    *reinterpret_cast<float4*>(p) = make_float4(q.v[0], q.v[1], q.v[2], q.v[3]);
+}
+__device__ __forceinline__ void store4(double* p, const Quad<double>& q) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(q.v[0], q.v[1]);
+    reinterpret_cast<double2*>(p)[1] = make_double2(q.v[2], q.v[3]);
+}
+
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+template <typename T>
+__device__ __forceinline__ bool finite(T x) {
+    return isfinite(x);
+}
+
+// bit j of a byte -> bit 4j of a word (Morton spread by 4)
+__device__ __forceinline__ uint32_t spread4(uint32_t x) {
+    x &= 0xffu;
+    x = (x | (x << 12)) & 0x000F000Fu;
+    x = (x | (x << 6)) & 0x03030303u;
+    x = (x | (x << 3)) & 0x11111111u;
+    return x;
+}
+
+// ---------------------------------------------------------------------------
+// K1: error-compensated sign extraction.
+//
+// A warp task is 512 consecutive coordinates of one (worker, segment):
+// 16 packed u32 words.  Vector path (L % 4 == 0): lane l holds coordinates
+// 4l..4l+3 of each 128-coordinate sub-chunk, so ballot k collects bit
+// (4l + k); word q of the sub-chunk is the 4-way bit interleave of byte q of
+// the four ballots.  Scalar path: lane l holds coordinate 32t + l of word t
+// and the ballot is the word.  Coordinates j >= L are storage padding (bit
+// 0, sign_vector.hpp:15-18); s*L + j >= D is value padding, 0.0, bit 1
+// (segmentation.hpp:45-49 + sign_vector.hpp:70).
+// ---------------------------------------------------------------------------
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kStreamThreads) extract_kernel(const StreamParams<T> p) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t warps = gridDim.x * (kStreamThreads / 32);
+    const uint32_t tasks_per_seg = (p.words_proc + kTaskWords - 1) / kTaskWords;
+    const uint64_t n_tasks = uint64_t(tasks_per_seg) * p.n_seg * p.ml;
+    bool bad = false;
+    for (uint64_t task = blockIdx.x * (kStreamThreads / 32) + (threadIdx.x >> 5); task < n_tasks;
+         task += warps) {
+        const uint32_t q = uint32_t(task % tasks_per_seg);
+        const uint64_t rest = task / tasks_per_seg;
+        const uint32_t s = uint32_t(rest % p.n_seg);
+        const uint32_t wl = uint32_t(rest / p.n_seg);
+        const T* __restrict__ g = p.g[wl];
+        const T* __restrict__ c = p.c[wl];
+        const uint64_t seg0 = uint64_t(s) * p.seg_len;  // first global coordinate
+        const uint64_t j0 = uint64_t(q) * (kTaskWords * 32);
+        uint32_t word = 0;  // lane t < 16 ends up holding word t of the task
+        if (VEC) {
+            Quad<T> gv[4], cv[4];
+#pragma unroll
+            for (int sub = 0; sub < 4; ++sub) {
+                const uint64_t j = j0 + sub * 128 + lane * 4;
+                const uint64_t gi = seg0 + j;
+                if (j < p.seg_len && gi + 3 < p.dim) {
+                    gv[sub] = load4(g + gi);
+                    cv[sub] = load4(c + gi);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const bool in = (j + k < p.seg_len) && (gi + k < p.dim);
+                        gv[sub].v[k] = in ? g[gi + k] : T(0);
+                        cv[sub].v[k] = in ? c[gi + k] : T(0);
+                    }
+                }
+            }
+#pragma unroll
+            for (int sub = 0; sub < 4; ++sub) {
+                const uint64_t j = j0 + sub * 128 + lane * 4;
+                uint32_t b[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const T u = add_rn(gv[sub].v[k], cv[sub].v[k]);
+                    bad |= !(finite(gv[sub].v[k]) && finite(cv[sub].v[k]) && finite(u));
+                    const bool bit = (j + k < p.seg_len) && (u >= T(0));  // -0.0 -> 1
+                    b[k] = __ballot_sync(kFull, bit);
+                }
+                const int qb = (lane & 3) * 8;
+                const uint32_t w = spread4(b[0] >> qb) | (spread4(b[1] >> qb) << 1) |
+                                   (spread4(b[2] >> qb) << 2) | (spread4(b[3] >> qb) << 3);
+                if ((lane >> 2) == sub) word = w;
+            }
+        } else {
+#pragma unroll 4
+            for (int t = 0; t < kTaskWords; ++t) {
+                const uint64_t j = j0 + t * 32 + lane;
+                const uint64_t gi = seg0 + j;
+                bool bit = false;
+                if (j < p.seg_len) {
+                    if (gi < p.dim) {
+                        const T gg = g[gi], cc = c[gi];
+                        const T u = add_rn(gg, cc);
+                        bad |= !(finite(gg) && finite(cc) && finite(u));
+                        bit = u >= T(0);
+                    } else {
+                        bit = true;  // value padding 0.0 packs to 1
+                    }
+                }
+                const uint32_t w = __ballot_sync(kFull, bit);
+                if (lane == t) word = w;
+            }
+        }
+        const uint32_t wi = q * kTaskWords + lane;
+        if (lane < kTaskWords && wi < p.words_proc)
+            p.bits[(uint64_t(s) * p.ml + wl) * p.wst + wi] = word;
+    }
+    if (__any_sync(kFull, bad) && lane == 0) atomicOr(p.err, 1);
+}
+
+// ---------------------------------------------------------------------------
+// K3+K4: decode the aggregate to +-eta_s and update the compensation,
+// c' = (g + c) - g_t, in the same pass (sync.hpp:113-118).  Same task
+// decomposition as K1, so each sub-chunk's bits are 4 aligned words.
+// ---------------------------------------------------------------------------
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kStreamThreads) decode_kernel(const StreamParams<T> p) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t warps = gridDim.x * (kStreamThreads / 32);
+    const uint32_t tasks_per_seg = (p.words_proc + kTaskWords - 1) / kTaskWords;
+    const uint64_t n_tasks = uint64_t(tasks_per_seg) * p.n_seg * p.ml;
+    const T eta = p.eta;
+    for (uint64_t task = blockIdx.x * (kStreamThreads / 32) + (threadIdx.x >> 5); task < n_tasks;
+         task += warps) {
+        const uint32_t q = uint32_t(task % tasks_per_seg);
+        const uint64_t rest = task / tasks_per_seg;
+        const uint32_t s = uint32_t(rest % p.n_seg);
+        const uint32_t wl = uint32_t(rest / p.n_seg);
+        const T* __restrict__ g = p.g[wl];
+        const T* c = p.c[wl];  // may alias c_out (in-place update): no __restrict__
+        T* co = p.c_out[wl];
+        T* upd = (wl == 0) ? p.update : nullptr;
+        const uint64_t seg0 = uint64_t(s) * p.seg_len;
+        const uint64_t j0 = uint64_t(q) * (kTaskWords * 32);
+        const uint32_t* aw = p.agg + uint64_t(s) * p.wst + q * kTaskWords;
+        if (VEC) {
+            Quad<T> gv[4], cv[4];
+            uint32_t nib[4];
+#pragma unroll
+            for (int sub = 0; sub < 4; ++sub) {
+                const uint64_t j = j0 + sub * 128 + lane * 4;
+                const uint64_t gi = seg0 + j;
+                const uint32_t wi = q * kTaskWords + sub * 4 + (lane >> 3);
+                const uint32_t word = (wi < p.words_proc) ? __ldg(aw + sub * 4 + (lane >> 3)) : 0u;
+                nib[sub] = (word >> ((lane & 7) * 4)) & 0xFu;
+                if (j < p.seg_len && gi + 3 < p.dim) {
+                    gv[sub] = load4(g + gi);
+                    cv[sub] = load4_rw(c + gi);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const bool in = (j + k < p.seg_len) && (gi + k < p.dim);
+                        gv[sub].v[k] = in ? g[gi + k] : T(0);
+                        cv[sub].v[k] = in ? c[gi + k] : T(0);
+                    }
+                }
+            }
+#pragma unroll
+            for (int sub = 0; sub < 4; ++sub) {
+                const uint64_t j = j0 + sub * 128 + lane * 4;
+                const uint64_t gi = seg0 + j;
+                Quad<T> out, up;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const T gt = ((nib[sub] >> k) & 1u) ? eta : -eta;
+                    out.v[k] = sub_rn(add_rn(gv[sub].v[k], cv[sub].v[k]), gt);
+                    up.v[k] = gt;
+                }
+                if (j < p.seg_len && gi + 3 < p.dim) {
+                    store4(co + gi, out);
+                    if (upd) store4(upd + gi, up);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if ((j + k < p.seg_len) && (gi + k < p.dim)) {
+                            co[gi + k] = out.v[k];
+                            if (upd) upd[gi + k] = up.v[k];
+                        }
+                }
+            }
+        } else {
+#pragma unroll 4
+            for (int t = 0; t < kTaskWords; ++t) {
+                const uint64_t j = j0 + t * 32 + lane;
+                const uint64_t gi = seg0 + j;
+                if (j < p.seg_len && gi < p.dim) {
+                    const uint32_t word = __ldg(aw + t);
+                    const T gt = ((word >> lane) & 1u) ? eta : -eta;
+                    co[gi] = sub_rn(add_rn(g[gi], c[gi]), gt);
+                    if (upd) upd[gi] = gt;
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: the merge DAG of every owned segment.
+//
+// A CTA takes a 1024-word tile (32768 coordinates) of one segment and runs
+// every merge of the current stage over it; thread t always owns words
+// 4t..4t+3 of the tile, so intermediate nodes never leave the thread (they
+// live in a shared-memory slot only because their index is dynamic).  Per
+// merge: d = r ^ l; the draw index of every disagreeing coordinate is
+//   base(stream) + exclusive_prefix(popcount(d)) over the segment,
+// obtained with a block scan plus a decoupled look-back across tiles; the
+// coin is (mix(key + (n+1)γ) >> 11) < ceil(p·2^53); out = r ^ (d & ~coin).
+// Tiles are handed out by an atomic counter in segment order, so every
+// look-back only waits on CTAs that are already running.
+// ---------------------------------------------------------------------------
+constexpr uint64_t kValMask = (1ull << 38) - 1;
+constexpr uint32_t kAgg = 1, kPrefix = 2;
+
+__device__ __forceinline__ uint64_t pack_flag(uint32_t epoch, uint32_t st, uint64_t v) {
+    return (uint64_t(epoch) << 40) | (uint64_t(st) << 38) | v;
+}
+
+// Warp-wide decoupled look-back; returns the exclusive prefix of `agg`.
+__device__ __forceinline__ uint64_t lookback(uint64_t* f, uint32_t tile, uint32_t epoch,
+                                             uint64_t agg, int lane) {
+    if (tile == 0) {
+        if (lane == 0) st_relaxed(f, pack_flag(epoch, kPrefix, agg));
+        return 0;
+    }
+    if (lane == 0) st_relaxed(f + tile, pack_flag(epoch, kAgg, agg));
+    uint64_t excl = 0;
+    int64_t pos = int64_t(tile) - 1;
+    while (true) {
+        const int64_t idx = pos - lane;
+        uint64_t v = 0;
+        bool valid = true, is_p = true;
+        if (idx >= 0) {
+            v = ld_relaxed(f + idx);
+            const uint32_t st = uint32_t(v >> 38) & 3u;
+            valid = uint32_t(v >> 40) == epoch && st != 0;
+            is_p = valid && st == kPrefix;
+        }
+        const unsigned pm = __ballot_sync(kFull, is_p);
+        const unsigned vm = __ballot_sync(kFull, valid);
+        const int fp = pm ? __ffs(pm) - 1 : 31;
+        const unsigned need = fp == 31 ? kFull : ((2u << fp) - 1u);
+        if ((vm & need) != need) {
+            __nanosleep(32);
+            continue;
+        }
+        uint64_t mine = (lane <= fp && idx >= 0) ? (v & kValMask) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(kFull, mine, o);
+        excl += mine;
+        if (pm) break;
+        pos -= 32;
+    }
+    if (lane == 0) st_relaxed(f + tile, pack_flag(epoch, kPrefix, excl + agg));
+    return excl;
+}
+
+__global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams p) {
+    extern __shared__ uint4 slots[];  // [max_slots][kMergeThreads]
+    __shared__ uint32_t s_tile;
+    __shared__ uint32_t s_warp[kMergeThreads / 32];
+    __shared__ uint64_t s_base;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t total_tiles = p.n_seg * p.tiles_per_seg;
+    while (true) {
+        if (tid == 0) s_tile = atomicAdd(p.tile_counter, 1u) - p.tile_base;
+        __syncthreads();
+        const uint32_t gt = s_tile;
+        __syncthreads();
+        if (gt >= total_tiles) break;
+        const uint32_t sl = gt % p.n_seg, tile = gt / p.n_seg;
+        const uint32_t w0 = tile * kTileWords + tid * kMergeWordsPerThread;
+        const bool active = w0 < p.words_proc;
+        // valid-bit masks of the four words (bits beyond L stay 0)
+        uint32_t vmask[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t rem = int64_t(p.seg_bits) - int64_t(w0 + k) * 32;
+            vmask[k] = rem >= 32 ? kFull : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+        }
+        const uint32_t mb = p.seg_begin[sl];
+        const uint32_t kb = p.stage_begin[sl * (p.n_stages + 1) + p.stage];
+        const uint32_t ke = p.stage_begin[sl * (p.n_stages + 1) + p.stage + 1];
+        const uint32_t sg = p.s_first + sl;
+        for (uint32_t k = kb; k < ke; ++k) {
+            const DevMerge m = p.merges[mb + k];
+            auto load_src = [&](uint16_t src) -> uint4 {
+                if (!active) return make_uint4(0, 0, 0, 0);
+                const uint32_t idx = src & 0x3FFFu;
+                switch (src & 0xC000u) {
+                    case kSrcLeaf: {
+                        const uint64_t off =
+                            (uint64_t((idx / p.ml) * p.n_seg + sl) * p.ml + idx % p.ml) * p.wst;
+                        return __ldcg(reinterpret_cast<const uint4*>(p.leaves + off + w0));
+                    }
+                    case kSrcSlot:
+                        return slots[idx * kMergeThreads + tid];
+                    default:
+                        return __ldcg(reinterpret_cast<const uint4*>(
+                            p.gnodes + (uint64_t(sl) * p.gmax + idx) * p.wst + w0));
+                }
+            };
+            const uint4 r4 = load_src(m.recv_src);
+            const uint4 l4 = load_src(m.local_src);
+            const uint32_t r[4] = {r4.x, r4.y, r4.z, r4.w};
+            const uint32_t l[4] = {l4.x, l4.y, l4.z, l4.w};
+            uint32_t d[4];
+            uint32_t cnt = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                d[j] = (r[j] ^ l[j]) & vmask[j];
+                cnt += __popc(d[j]);
+            }
+            // block exclusive scan of cnt
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) s_warp[wid] = incl;
+            __syncthreads();
+            if (wid == 0) {
+                const uint32_t ws = lane < kMergeThreads / 32 ? s_warp[lane] : 0u;
+                uint32_t wincl = ws;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(kFull, wincl, o);
+                    if (lane >= o) wincl += y;
+                }
+                const uint32_t tile_total = __shfl_sync(kFull, wincl, 31);
+                // draws this stream produced before this merge (continuations)
+                uint64_t base = 0;
+                if (lane == 0) {
+                    base = m.base_add;
+                    int32_t src = m.offset_src;
+                    while (src >= 0) {
+                        const DevMerge& pm = p.merges[mb + src];
+                        base += p.totals[mb + src] + pm.base_add;
+                        src = pm.offset_src;
+                    }
+                }
+                const uint64_t excl = lookback(p.flags + uint64_t(mb + k) * p.tiles_per_seg, tile,
+                                               p.epoch, tile_total, lane);
+                __syncwarp();
+                if (lane < kMergeThreads / 32) s_warp[lane] = wincl - ws;
+                if (lane == 0) {
+                    s_base = base + excl;
+                    if (tile == p.tiles_per_seg - 1) p.totals[mb + k] = excl + tile_total;
+                }
+            }
+            __syncthreads();
+            uint64_t n = s_base + s_warp[wid] + (incl - cnt);  // draw index of my first coin
+            const uint64_t key =
+                m.key_mode ? m.key : stream_key(p.seed, 5, m.receiver, p.round, sg);
+            uint64_t z = key + (n + 1) * kGamma;
+            const uint64_t th = m.thresh11;
+            uint32_t out[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t dd = d[j], keep = 0;
+                while (dd) {
+                    const int b = __ffs(dd) - 1;
+                    dd &= dd - 1;
+                    const uint64_t x = mix64(z);
+                    z += kGamma;
+                    keep |= uint32_t(x < th) << b;
+                }
+                out[j] = (r[j] ^ (d[j] & ~keep)) & vmask[j];
+            }
+            if (active) {
+                const uint4 o4 = make_uint4(out[0], out[1], out[2], out[3]);
+                if (m.out_slot != kNone) slots[m.out_slot * kMergeThreads + tid] = o4;
+                if (m.out_global == kFinal)
+                    *reinterpret_cast<uint4*>(p.agg + uint64_t(sg) * p.wst + w0) = o4;
+                else if (m.out_global != kNone)
+                    __stcg(reinterpret_cast<uint4*>(
+                               p.gnodes + (uint64_t(sl) * p.gmax + m.out_global) * p.wst + w0),
+                           o4);
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Aggregate bits in the reference layout: bit j of the whole vector lives in
+// segment j / L at offset j % L (sync.hpp:103-112).  One thread per output
+// u32 word (two of them form one little-endian u64 word).
+// ---------------------------------------------------------------------------
+__global__ void export_bits_kernel(const uint32_t* __restrict__ agg, uint32_t wst, uint64_t dim,
+                                   uint64_t seg_len, uint64_t n_out, uint32_t* __restrict__ out) {
+    for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n_out;
+         k += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t j0 = k * 32;
+        uint32_t val = 0;
+        if (j0 < dim) {
+            const uint32_t n = uint32_t(dim - j0 < 32 ? dim - j0 : 32);
+            uint32_t pos = 0;
+            while (pos < n) {
+                const uint64_t j = j0 + pos;
+                const uint64_t s = j / seg_len;
+                const uint64_t o = j - s * seg_len;
+                uint32_t take = n - pos;
+                if (seg_len - o < take) take = uint32_t(seg_len - o);
+                const uint32_t* a = agg + s * wst;
+                const uint32_t wi = uint32_t(o >> 5), sh = uint32_t(o & 31);
+                uint64_t window = a[wi];
+                if (sh + take > 32) window |= uint64_t(a[wi + 1]) << 32;
+                uint32_t bits = uint32_t(window >> sh);
+                if (take < 32) bits &= (1u << take) - 1u;
+                val |= bits << pos;
+                pos += take;
+            }
+        }
+        out[k] = val;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Synthetic inputs: g_j from draw j of RngStream(seed,
+// trial, w, t, 0).  recipe 0: ((x>>51) - 4096)·2^-20; recipe 1 (correlated):
+// shared ((x_a>>52) - 2048) + per-worker ((x_b>>53) - 1024), ·2^-20.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void fill_recipe_kernel(int recipe, uint64_t seed, uint64_t worker, uint64_t round,
+                                   uint64_t dim, T* __restrict__ out) {
+    const uint64_t kb = stream_key(seed, 6, worker, round, 0);
+    const uint64_t ka = stream_key(seed, 6, 0xFFFF, round, 0);
+    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < dim;
+         j += uint64_t(gridDim.x) * blockDim.x) {
+        int64_t q;
+        if (recipe == 0) {
+            q = int64_t(mix64(kb + (j + 1) * kGamma) >> 51) - 4096;
+        } else {
+            q = (int64_t(mix64(ka + (j + 1) * kGamma) >> 52) - 2048) +
+                (int64_t(mix64(kb + (j + 1) * kGamma) >> 53) - 1024);
+        }
+        out[j] = T(double(q) * 0x1.0p-20);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Dense round.  dense_leaf_kernel (multi-rank): u = g + c of the local
+// workers, laid out per destination rank for the exchange:
+// u_send[q][sl][wl][L] (segment q*s_own + sl).  dense_reduce_kernel: per
+// coordinate of an owned segment, evaluate the schedule's reduction tree in
+// double (state[to][s] = add(state[to][s], p), allreduce.hpp:114-116),
+// scale by 1/M (120-126).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void dense_leaf_kernel(const DenseParams<T> p, uint32_t s_own, uint32_t n_seg_total,
+                                  T* __restrict__ u_send) {
+    const uint64_t per_w = uint64_t(n_seg_total) * p.seg_len;
+    const uint64_t n = per_w * p.ml;
+    bool bad = false;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t wl = uint32_t(i / per_w);
+        const uint64_t jj = i - uint64_t(wl) * per_w;  // padded coordinate
+        const uint32_t s = uint32_t(jj / p.seg_len);
+        const uint64_t o = jj - uint64_t(s) * p.seg_len;
+        T u = T(0);
+        if (jj < p.dim) {
+            const T gg = p.src[2 * wl][jj], cc = p.src[2 * wl + 1][jj];
+            u = add_rn(gg, cc);
+            bad |= !(finite(gg) && finite(cc) && finite(u));
+        }
+        const uint32_t q = s / s_own, sl = s % s_own;
+        u_send[((uint64_t(q) * s_own + sl) * p.ml + wl) * p.seg_len + o] = u;
+    }
+    if (bad) atomicOr(p.err, 1);
+}
+
+template <typename T>
+__global__ void dense_reduce_kernel(const DenseParams<T> p) {
+    const uint64_t n = uint64_t(p.n_seg) * p.seg_len;
+    double val[2 * kMaxLocalWorkers];
+    bool bad = false;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t sl = uint32_t(i / p.seg_len);
+        const uint64_t o = i - uint64_t(sl) * p.seg_len;
+        const uint64_t j = uint64_t(p.s_first + sl) * p.seg_len + o;  // global coordinate
+        for (uint32_t w = 0; w < p.workers; ++w) {
+            double u;
+            if (p.mode == 0) {
+                if (j < p.dim) {
+                    const T gg = p.src[2 * w][j], cc = p.src[2 * w + 1][j];
+                    const T uu = add_rn(gg, cc);
+                    bad |= !(finite(gg) && finite(cc) && finite(uu));
+                    u = double(uu);
+                } else {
+                    u = 0.0;  // value padding
+                }
+            } else {
+                const uint32_t src_rank = w / p.ml, wl = w % p.ml;
+                u = double(p.u_buf[((uint64_t(src_rank) * p.n_seg + sl) * p.ml + wl) * p.seg_len + o]);
+            }
+            val[w] = u;
+        }
+        const DenseOp* ops = p.ops + uint64_t(sl) * p.n_ops;
+        for (uint32_t k = 0; k < p.n_ops; ++k) {
+            const double v = __dadd_rn(val[ops[k].a], val[ops[k].b]);
+            bad |= !isfinite(v);
+            val[p.workers + k] = v;
+        }
+        if (j < p.dim) p.mean[j] = T(__dmul_rn(val[p.final_node[sl]], p.inv_m));
+    }
+    if (bad) atomicOr(p.err, 1);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Launch wrappers
+// ---------------------------------------------------------------------------
+template <typename T>
+cudaError_t launch_extract(const StreamParams<T>& p, bool vec, int grid, cudaStream_t st) {
+    if (vec)
+        extract_kernel<T, true><<<grid, kStreamThreads, 0, st>>>(p);
+    else
+        extract_kernel<T, false><<<grid, kStreamThreads, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_decode(const StreamParams<T>& p, bool vec, int grid, cudaStream_t st) {
+    if (vec)
+        decode_kernel<T, true><<<grid, kStreamThreads, 0, st>>>(p);
+    else
+        decode_kernel<T, false><<<grid, kStreamThreads, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_merge(const MergeParams& p, int grid, size_t smem, cudaStream_t st) {
+    merge_kernel<<<grid, kMergeThreads, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t merge_kernel_set_smem(size_t smem) {
+    // The attribute is per function and process-wide: only ever raise it.
+    static size_t current = 48 * 1024;
+    if (smem <= current) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem));
+    if (e == cudaSuccess) current = smem;
+    return e;
+}
+
+cudaError_t stream_occupancy(bool f64, int* extract_blocks, int* decode_blocks) {
+    cudaError_t e;
+    if (f64) {
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(extract_blocks,
+                                                          extract_kernel<double, true>,
+                                                          kStreamThreads, 0);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(decode_blocks,
+                                                              decode_kernel<double, true>,
+                                                              kStreamThreads, 0);
+    } else {
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(extract_blocks,
+                                                          extract_kernel<float, true>,
+                                                          kStreamThreads, 0);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(decode_blocks,
+                                                              decode_kernel<float, true>,
+                                                              kStreamThreads, 0);
+    }
+    return e;
+}
+
+cudaError_t merge_kernel_occupancy(size_t smem, int* blocks_per_sm) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, merge_kernel,
+                                                         kMergeThreads, smem);
+}
+
+cudaError_t launch_export_bits(const uint32_t* agg, uint32_t wst, uint64_t dim, uint64_t seg_len,
+                               uint32_t* out_u32, cudaStream_t st) {
+    const uint64_t n_out = ((dim + 63) / 64) * 2;
+    const int threads = 256;
+    uint64_t blocks = (n_out + threads - 1) / threads;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    export_bits_kernel<<<int(blocks), threads, 0, st>>>(agg, wst, dim, seg_len, n_out, out_u32);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_fill_recipe(int recipe, uint64_t seed, uint64_t worker, uint64_t round,
+                               uint64_t dim, T* out, cudaStream_t st) {
+    uint64_t blocks = (dim + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks == 0) blocks = 1;
+    fill_recipe_kernel<T><<<int(blocks), 256, 0, st>>>(recipe, seed, worker, round, dim, out);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_dense_reduce(const DenseParams<T>& p, int grid, cudaStream_t st) {
+    dense_reduce_kernel<T><<<grid, 256, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_dense_leaf(const T* const* g, const T* const* c, uint32_t ml, uint64_t dim,
+                              uint64_t seg_len, uint32_t n_seg_total, uint32_t s_own, T* u_send,
+                              int* err, int grid, cudaStream_t st) {
+    DenseParams<T> p{};
+    for (uint32_t w = 0; w < ml; ++w) {
+        p.src[2 * w] = g[w];
+        p.src[2 * w + 1] = c[w];
+    }
+    p.ml = ml;
+    p.dim = dim;
+    p.seg_len = seg_len;
+    p.err = err;
+    dense_leaf_kernel<T><<<grid, 256, 0, st>>>(p, s_own, n_seg_total, u_send);
+    return cudaGetLastError();
+}
+
+#define MARSIT_INSTANTIATE(T)                                                                    \
+    template cudaError_t launch_extract<T>(const StreamParams<T>&, bool, int, cudaStream_t);    \
+    template cudaError_t launch_decode<T>(const StreamParams<T>&, bool, int, cudaStream_t);     \
+    template cudaError_t launch_fill_recipe<T>(int, uint64_t, uint64_t, uint64_t, uint64_t, T*, \
+                                               cudaStream_t);                                   \
+    template cudaError_t launch_dense_reduce<T>(const DenseParams<T>&, int, cudaStream_t);      \
+    template cudaError_t launch_dense_leaf<T>(const T* const*, const T* const*, uint32_t,       \
+                                              uint64_t, uint64_t, uint32_t, uint32_t, T*, int*,  \
+                                              int, cudaStream_t);
+MARSIT_INSTANTIATE(float)
+MARSIT_INSTANTIATE(double)
+
+}  // namespace marsit_b200

@@ -1,0 +1,114 @@
+// kernels.cuh — device-side data structures shared between the host runtime
+// (runtime.cu) and the sm_100a kernels (kernels.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace marsit_b200 {
+
+constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ull;  // rng.hpp:64
+constexpr uint32_t kMaxLocalWorkers = 64;           // workers resident on one rank
+constexpr int kMergeThreads = 256;
+constexpr int kMergeWordsPerThread = 4;              // one uint4 of packed signs
+constexpr int kTileWords = kMergeThreads * kMergeWordsPerThread;  // 1024 u32 = 32768 bits
+constexpr int kStreamThreads = 256;                  // sign_extract / decode
+constexpr int kTaskWords = 16;                       // u32 words per warp task (512 elements)
+
+// Source of a merge operand (16-bit code): [15:14] kind, [13:0] index.
+enum : uint16_t { kSrcLeaf = 0u << 14, kSrcSlot = 1u << 14, kSrcGlobal = 2u << 14 };
+constexpr uint16_t kNone = 0xFFFF;
+constexpr uint16_t kFinal = 0xFFFE;
+
+// One merge of a segment's compiled DAG (merge.hpp:34-58 applied by the
+// receiver of a reduce step, allreduce.hpp:183-185).
+struct DevMerge {
+    uint64_t thresh11;   // ceil(p * 2^53) << 11: coin <=> mix(..) < thresh11
+    uint64_t key;        // explicit stream key (key_mode == 1)
+    uint64_t base_add;   // draws the stream had produced before this round's merges
+    uint32_t receiver;   // stream owner; key = K(seed, merge, receiver, t, segment)
+    uint16_t recv_src, local_src;
+    uint16_t out_slot;   // shared-memory slot for same-stage consumers, or kNone
+    uint16_t out_global; // global node index, kFinal (aggregate) or kNone
+    int16_t offset_src;  // previous merge of the same stream (draw continuation) or -1
+    uint8_t key_mode;    // 0: derive key from (seed, round); 1: explicit `key`
+    uint8_t pad_;
+};
+static_assert(sizeof(DevMerge) == 40, "DevMerge layout");
+
+struct MergeParams {
+    const DevMerge* merges;      // all owned segments' merges, segment-major
+    const uint32_t* seg_begin;   // [n_seg] first merge of each owned segment
+    const uint32_t* stage_begin; // [n_seg][n_stages+1] merge-index ranges per stage
+    uint32_t n_stages, stage;
+    uint32_t n_seg, s_first;     // owned segments and the global id of the first
+    uint32_t tiles_per_seg, words_proc, wst, ml;
+    uint64_t seg_bits;           // L
+    const uint32_t* leaves;      // leaf(w, sl) = leaves + ((w/ml*n_seg + sl)*ml + w%ml)*wst
+    uint32_t* gnodes;            // [n_seg][gmax][wst]
+    uint32_t gmax;
+    uint32_t* agg;               // [S][wst]; owned segment sl at s_first + sl
+    uint64_t* flags;             // [merges][tiles_per_seg] decoupled look-back
+    uint64_t* totals;            // [merges] draws consumed by each merge (last tile)
+    uint32_t* tile_counter;
+    uint32_t tile_base, epoch;
+    uint64_t seed, round;
+};
+
+template <typename T>
+struct StreamParams {
+    const T* g[kMaxLocalWorkers];
+    const T* c[kMaxLocalWorkers];
+    T* c_out[kMaxLocalWorkers];
+    uint32_t ml, n_seg;          // local workers, segments (all S)
+    uint64_t dim, seg_len;       // D, L
+    uint32_t words_proc, wst;
+    uint32_t* bits;              // extract output: [S][ml][wst]
+    const uint32_t* agg;         // decode input: [S][wst]
+    T* update;                   // optional g_t (written by local worker 0)
+    T eta;
+    int* err;
+};
+
+// Launch wrappers (kernels.cu).
+template <typename T>
+cudaError_t launch_extract(const StreamParams<T>& p, bool vec, int grid, cudaStream_t st);
+template <typename T>
+cudaError_t launch_decode(const StreamParams<T>& p, bool vec, int grid, cudaStream_t st);
+cudaError_t launch_merge(const MergeParams& p, int grid, size_t smem, cudaStream_t st);
+cudaError_t merge_kernel_occupancy(size_t smem, int* blocks_per_sm);
+cudaError_t merge_kernel_set_smem(size_t smem);
+cudaError_t stream_occupancy(bool f64, int* extract_blocks, int* decode_blocks);
+cudaError_t launch_export_bits(const uint32_t* agg, uint32_t wst, uint64_t dim, uint64_t seg_len,
+                               uint32_t* out_u32, cudaStream_t st);
+template <typename T>
+cudaError_t launch_fill_recipe(int recipe, uint64_t seed, uint64_t worker, uint64_t round,
+                               uint64_t dim, T* out, cudaStream_t st);
+
+// Dense round (allreduce_dense, allreduce.hpp:98-130): per coordinate, the
+// schedule's reduction tree of u = g + c evaluated in double.
+struct DenseOp {
+    uint16_t a, b;     // operand node ids (leaf w < M, else M + k)
+    uint16_t pad0, pad1;
+};
+template <typename T>
+struct DenseParams {
+    const T* src[kMaxLocalWorkers * 2];  // leaves: g,c pairs (1 GPU) or exchanged u (multi)
+    uint32_t mode;                       // 0: leaf w = g[w] + c[w]; 1: leaf w = u buffer
+    const T* u_buf;                      // mode 1: [G][s_own][ml][L] u values
+    const DenseOp* ops;                  // [n_seg][n_ops]
+    const uint16_t* final_node;          // [n_seg]
+    uint32_t n_ops, n_seg, s_first, ml, workers;
+    uint64_t dim, seg_len;
+    double inv_m;
+    T* mean;                              // [D] (full vector; owned segments written)
+    int* err;
+};
+template <typename T>
+cudaError_t launch_dense_reduce(const DenseParams<T>& p, int grid, cudaStream_t st);
+template <typename T>
+cudaError_t launch_dense_leaf(const T* const* g, const T* const* c, uint32_t ml, uint64_t dim,
+                              uint64_t seg_len, uint32_t n_seg_total, uint32_t s_own,
+                              T* u_send, int* err, int grid, cudaStream_t st);
+
+}  // namespace marsit_b200

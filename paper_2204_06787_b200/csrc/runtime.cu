@@ -1,0 +1,987 @@
+// runtime.cu — host runtime behind the C-ABI (include/marsit_b200.h).
+//
+// A marsit_ctx owns every device buffer of the path and the compiled merge
+// plan; a round is a fixed sequence of launches on the caller's stream:
+//
+//   G == 1:  extract -> merge (1 launch per plan stage) -> decode [-> export]
+//   G  > 1:  extract -> NCCL exchange of packed segments to their owners ->
+//            merge (owned segments) -> NCCL all-gather of the aggregates ->
+//            decode [-> export]
+//
+// Segments are owned by ranks in contiguous blocks (rank q owns segments
+// [q*S/G, (q+1)*S/G)), so the exchange is a plain all-to-all of contiguous
+// per-destination blocks and the all-gather is in place.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/marsit_b200.h"
+#include "kernels.cuh"
+#include "plan.hpp"
+
+using namespace marsit_b200;
+
+struct marsit_schedule {
+    HostSchedule s;
+    Plan plan;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+marsit_status fail(marsit_status st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+    do {                                                                                  \
+        cudaError_t e_ = (expr);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(MARSIT_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define NCCL_TRY(expr)                                                                      \
+    do {                                                                                    \
+        ncclResult_t r_ = (expr);                                                           \
+        if (r_ != ncclSuccess)                                                              \
+            return fail(MARSIT_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
+uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+uint64_t round_up(uint64_t a, uint64_t b) { return ceil_div(a, b) * b; }
+
+// Device-side plan of the merge DAGs (see DevMerge in kernels.cuh).
+struct DevicePlan {
+    std::vector<DevMerge> merges;
+    std::vector<uint32_t> seg_begin, stage_begin;
+    uint32_t max_slots = 0, gmax = 0, n_stages = 1, n_merges = 0;
+};
+
+// Lower one segment's merge DAG: assign same-stage consumers to shared-memory
+// slots (liveness-based reuse) and cross-stage / final outputs to global nodes.
+marsit_status lower_plan(const Plan& plan, uint32_t s_first, uint32_t n_seg, DevicePlan& dp) {
+    const uint32_t W = plan.workers;
+    dp.n_stages = plan.n_stages;
+    dp.seg_begin.resize(n_seg);
+    dp.stage_begin.assign(size_t(n_seg) * (plan.n_stages + 1), 0);
+    for (uint32_t sl = 0; sl < n_seg; ++sl) {
+        const SegmentPlan& sp = plan.seg[s_first + sl];
+        const size_t n = sp.merges.size();
+        if (sp.final_node < W) return fail(MARSIT_EUNSUPPORTED, "schedule performs no reduction");
+        // execution order: by stage, then schedule order
+        std::vector<uint32_t> order(n);
+        for (size_t k = 0; k < n; ++k) order[k] = uint32_t(k);
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+            return sp.merges[a].stage < sp.merges[b].stage;
+        });
+        std::vector<uint32_t> pos(n);  // original index -> execution index
+        for (size_t e = 0; e < n; ++e) pos[order[e]] = uint32_t(e);
+        // consumers
+        std::vector<int> last_same(n, -1);
+        std::vector<bool> cross(n, false);
+        for (size_t e = 0; e < n; ++e) {
+            const MergeNode& m = sp.merges[order[e]];
+            for (uint32_t in : {m.recv_node, m.local_node}) {
+                if (in < W) continue;
+                const uint32_t src = in - W;
+                if (sp.merges[src].stage == m.stage)
+                    last_same[src] = std::max(last_same[src], int(e));
+                else
+                    cross[src] = true;
+            }
+        }
+        std::vector<uint16_t> slot_of(n, kNone), gidx_of(n, kNone);
+        std::vector<bool> slot_busy;
+        uint32_t gnext = 0;
+        dp.seg_begin[sl] = uint32_t(dp.merges.size());
+        for (size_t e = 0; e < n; ++e) {
+            const uint32_t k = order[e];
+            const MergeNode& m = sp.merges[k];
+            DevMerge d{};
+            d.thresh11 = coin_threshold(m.c_recv, m.c_local) << 11;
+            d.receiver = m.receiver;
+            d.key_mode = 0;
+            d.offset_src = m.offset_src < 0 ? int16_t(-1) : int16_t(pos[m.offset_src]);
+            auto encode = [&](uint32_t node) -> uint16_t {
+                if (node < W) return uint16_t(kSrcLeaf | node);
+                const uint32_t src = node - W;
+                if (sp.merges[src].stage == m.stage) return uint16_t(kSrcSlot | slot_of[src]);
+                return uint16_t(kSrcGlobal | gidx_of[src]);
+            };
+            d.recv_src = encode(m.recv_node);
+            d.local_src = encode(m.local_node);
+            // free slots whose last same-stage use is this merge (read before write)
+            for (uint32_t in : {m.recv_node, m.local_node})
+                if (in >= W && last_same[in - W] == int(e) && slot_of[in - W] != kNone)
+                    slot_busy[slot_of[in - W]] = false;
+            if (last_same[k] >= 0) {
+                uint32_t s = 0;
+                while (s < slot_busy.size() && slot_busy[s]) ++s;
+                if (s == slot_busy.size()) slot_busy.push_back(false);
+                slot_busy[s] = true;
+                slot_of[k] = uint16_t(s);
+                dp.max_slots = std::max<uint32_t>(dp.max_slots, uint32_t(slot_busy.size()));
+            }
+            d.out_slot = slot_of[k];
+            if (W + k == sp.final_node) {
+                d.out_global = kFinal;
+            } else if (cross[k]) {
+                gidx_of[k] = uint16_t(gnext++);
+                d.out_global = gidx_of[k];
+            } else {
+                d.out_global = kNone;
+            }
+            dp.merges.push_back(d);
+        }
+        dp.gmax = std::max(dp.gmax, gnext);
+        // stage ranges (execution order is stage-sorted)
+        for (uint32_t st = 0; st <= plan.n_stages; ++st) {
+            uint32_t c = 0;
+            for (size_t e = 0; e < n; ++e)
+                if (sp.merges[order[e]].stage < st) ++c;
+            dp.stage_begin[size_t(sl) * (plan.n_stages + 1) + st] = c;
+        }
+        if (slot_busy.size() > 64 || gnext > 0x3FFF)
+            return fail(MARSIT_EUNSUPPORTED, "merge plan too large");
+    }
+    dp.n_merges = uint32_t(dp.merges.size());
+    return MARSIT_OK;
+}
+
+struct TimedPair {
+    int phase;
+    cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct marsit_ctx {
+    int device = 0;
+    marsit_dtype dtype = MARSIT_F32;
+    size_t esize = 4;
+    uint64_t D = 0, L = 0;
+    uint32_t M = 0, S = 0, G = 1, rank = 0, ml = 0, s_own = 0, s_first = 0;
+    uint32_t words64 = 0, words_proc = 0, wst = 0, tiles_per_seg = 0;
+    int sm_count = 148;
+    bool vec_ok = false;
+    HostSchedule sched;
+    Plan plan;
+    DevicePlan dp;
+    // device buffers
+    uint32_t* bits = nullptr;   // [S][ml][wst]
+    uint32_t* recv = nullptr;   // [G][s_own][ml][wst]   (G > 1)
+    uint32_t* agg = nullptr;    // [S][wst]
+    uint32_t* gnodes = nullptr; // [s_own][gmax][wst]
+    DevMerge* d_merges = nullptr;
+    uint32_t* d_seg_begin = nullptr;
+    uint32_t* d_stage_begin = nullptr;
+    uint64_t* flags = nullptr;  // [n_merges][tiles_per_seg]
+    uint64_t* totals = nullptr; // [n_merges]
+    uint32_t* counter = nullptr;
+    int* err = nullptr;
+    uint32_t tile_base = 0, epoch = 0;
+    int merge_grid = 0;
+    size_t merge_smem = 0;
+    int stream_grid = 0;
+    // dense round scratch
+    void* dense_send = nullptr;  // [G][s_own][ml][L] of dtype
+    void* dense_recv = nullptr;
+    void* dense_mean = nullptr;  // [S*L] of dtype (G > 1)
+    DenseOp* d_dense_ops = nullptr;
+    uint16_t* d_dense_final = nullptr;
+    uint32_t dense_n_ops = 0;
+    // NCCL
+    ncclComm_t comm = nullptr;
+    // timing
+    bool timing = false;
+    std::vector<TimedPair> pending;
+    std::vector<cudaEvent_t> event_pool;
+    float ms[MARSIT_N_PHASES] = {};
+    uint64_t launches[MARSIT_N_PHASES] = {};
+
+    ~marsit_ctx();
+    marsit_status begin_phase(int phase, cudaStream_t st, cudaEvent_t* a);
+    marsit_status end_phase(int phase, cudaStream_t st, cudaEvent_t a, uint64_t n_launch);
+    marsit_status next_epoch();
+};
+
+marsit_ctx::~marsit_ctx() {
+    if (device >= 0) cudaSetDevice(device);
+    for (void* p : {(void*)bits, (void*)recv, (void*)agg, (void*)gnodes, (void*)d_merges,
+                    (void*)d_seg_begin, (void*)d_stage_begin, (void*)flags, (void*)totals,
+                    (void*)counter, (void*)err, dense_send, dense_recv, dense_mean,
+                    (void*)d_dense_ops, (void*)d_dense_final})
+        if (p) cudaFree(p);
+    for (auto& tp : pending) {
+        cudaEventDestroy(tp.a);
+        cudaEventDestroy(tp.b);
+    }
+    for (auto e : event_pool) cudaEventDestroy(e);
+    if (comm) ncclCommDestroy(comm);
+}
+
+marsit_status marsit_ctx::begin_phase(int, cudaStream_t st, cudaEvent_t* a) {
+    *a = nullptr;
+    if (!timing) return MARSIT_OK;
+    if (event_pool.empty()) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreate(&e));
+        event_pool.push_back(e);
+    }
+    *a = event_pool.back();
+    event_pool.pop_back();
+    CUDA_TRY(cudaEventRecord(*a, st));
+    return MARSIT_OK;
+}
+
+marsit_status marsit_ctx::end_phase(int phase, cudaStream_t st, cudaEvent_t a, uint64_t n_launch) {
+    launches[phase] += n_launch;
+    if (!timing || !a) return MARSIT_OK;
+    cudaEvent_t b;
+    if (event_pool.empty()) {
+        CUDA_TRY(cudaEventCreate(&b));
+    } else {
+        b = event_pool.back();
+        event_pool.pop_back();
+    }
+    CUDA_TRY(cudaEventRecord(b, st));
+    pending.push_back({phase, a, b});
+    return MARSIT_OK;
+}
+
+marsit_status marsit_ctx::next_epoch() {
+    if (++epoch >= (1u << 24)) {
+        CUDA_TRY(cudaMemset(flags, 0, sizeof(uint64_t) * size_t(dp.n_merges + 1) * tiles_per_seg));
+        epoch = 1;
+    }
+    return MARSIT_OK;
+}
+
+namespace {
+
+template <typename T>
+StreamParams<T> stream_params(marsit_ctx* ctx, const void* const* g, const void* const* c,
+                              void* const* c_out, void* update, double eta) {
+    StreamParams<T> p{};
+    for (uint32_t w = 0; w < ctx->ml; ++w) {
+        p.g[w] = static_cast<const T*>(g[w]);
+        p.c[w] = static_cast<const T*>(c[w]);
+        p.c_out[w] = c_out ? static_cast<T*>(c_out[w]) : nullptr;
+    }
+    p.ml = ctx->ml;
+    p.n_seg = ctx->S;
+    p.dim = ctx->D;
+    p.seg_len = ctx->L;
+    p.words_proc = ctx->words_proc;
+    p.wst = ctx->wst;
+    p.bits = ctx->bits;
+    p.agg = ctx->agg;
+    p.update = static_cast<T*>(update);
+    p.eta = T(eta);
+    p.err = ctx->err;
+    return p;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+bool vec_ok_ptrs(const marsit_ctx* ctx, const void* const* a, const void* const* b) {
+    if (!ctx->vec_ok) return false;
+    for (uint32_t w = 0; w < ctx->ml; ++w)
+        if (!aligned16(a[w]) || !aligned16(b[w])) return false;
+    return true;
+}
+
+marsit_status check_ptrs(const marsit_ctx* ctx, const void* const* a, const char* what) {
+    if (!a) return fail(MARSIT_EPARAM, std::string(what) + " is null");
+    for (uint32_t w = 0; w < ctx->ml; ++w)
+        if (!a[w]) return fail(MARSIT_EPARAM, std::string(what) + " has a null worker pointer");
+    return MARSIT_OK;
+}
+
+marsit_status run_extract(marsit_ctx* ctx, const void* const* g, const void* const* c,
+                          cudaStream_t st) {
+    cudaEvent_t ev;
+    marsit_status s = ctx->begin_phase(0, st, &ev);
+    if (s) return s;
+    const bool vec = vec_ok_ptrs(ctx, g, c);
+    if (ctx->dtype == MARSIT_F32)
+        CUDA_TRY(launch_extract(stream_params<float>(ctx, g, c, nullptr, nullptr, 0.0), vec,
+                                ctx->stream_grid, st));
+    else
+        CUDA_TRY(launch_extract(stream_params<double>(ctx, g, c, nullptr, nullptr, 0.0), vec,
+                                ctx->stream_grid, st));
+    return ctx->end_phase(0, st, ev, 1);
+}
+
+marsit_status run_exchange(marsit_ctx* ctx, cudaStream_t st) {
+    if (ctx->G == 1) return MARSIT_OK;
+    cudaEvent_t ev;
+    marsit_status s = ctx->begin_phase(1, st, &ev);
+    if (s) return s;
+    const size_t block = size_t(ctx->s_own) * ctx->ml * ctx->wst;  // u32 words per destination
+    NCCL_TRY(ncclGroupStart());
+    for (uint32_t q = 0; q < ctx->G; ++q) {
+        NCCL_TRY(ncclSend(ctx->bits + q * block, block, ncclUint32, int(q), ctx->comm, st));
+        NCCL_TRY(ncclRecv(ctx->recv + q * block, block, ncclUint32, int(q), ctx->comm, st));
+    }
+    NCCL_TRY(ncclGroupEnd());
+    return ctx->end_phase(1, st, ev, 0);
+}
+
+marsit_status run_merge(marsit_ctx* ctx, uint64_t seed, uint64_t round, cudaStream_t st) {
+    cudaEvent_t ev;
+    marsit_status s = ctx->begin_phase(2, st, &ev);
+    if (s) return s;
+    MergeParams p{};
+    p.merges = ctx->d_merges;
+    p.seg_begin = ctx->d_seg_begin;
+    p.stage_begin = ctx->d_stage_begin;
+    p.n_stages = ctx->dp.n_stages;
+    p.n_seg = ctx->s_own;
+    p.s_first = ctx->s_first;
+    p.tiles_per_seg = ctx->tiles_per_seg;
+    p.words_proc = ctx->words_proc;
+    p.wst = ctx->wst;
+    p.ml = ctx->ml;
+    p.seg_bits = ctx->L;
+    p.leaves = ctx->G == 1 ? ctx->bits : ctx->recv;
+    p.gnodes = ctx->gnodes;
+    p.gmax = std::max<uint32_t>(ctx->dp.gmax, 1);
+    p.agg = ctx->agg;
+    p.flags = ctx->flags;
+    p.totals = ctx->totals;
+    p.tile_counter = ctx->counter;
+    p.seed = seed;
+    p.round = round;
+    const uint32_t total_tiles = ctx->s_own * ctx->tiles_per_seg;
+    const int grid = int(std::min<uint64_t>(total_tiles, uint64_t(ctx->merge_grid)));
+    for (uint32_t stage = 0; stage < ctx->dp.n_stages; ++stage) {
+        s = ctx->next_epoch();
+        if (s) return s;
+        p.stage = stage;
+        p.epoch = ctx->epoch;
+        p.tile_base = ctx->tile_base;
+        CUDA_TRY(launch_merge(p, grid, ctx->merge_smem, st));
+        ctx->tile_base += total_tiles + uint32_t(grid);
+    }
+    return ctx->end_phase(2, st, ev, ctx->dp.n_stages);
+}
+
+marsit_status run_allgather(marsit_ctx* ctx, cudaStream_t st) {
+    if (ctx->G == 1) return MARSIT_OK;
+    cudaEvent_t ev;
+    marsit_status s = ctx->begin_phase(3, st, &ev);
+    if (s) return s;
+    const size_t block = size_t(ctx->s_own) * ctx->wst;
+    NCCL_TRY(ncclAllGather(ctx->agg + ctx->rank * block, ctx->agg, block, ncclUint32, ctx->comm, st));
+    return ctx->end_phase(3, st, ev, 0);
+}
+
+marsit_status run_decode(marsit_ctx* ctx, const void* const* g, const void* const* c,
+                         void* const* c_out, void* update, double eta, cudaStream_t st) {
+    cudaEvent_t ev;
+    marsit_status s = ctx->begin_phase(4, st, &ev);
+    if (s) return s;
+    const bool vec = vec_ok_ptrs(ctx, g, c) && vec_ok_ptrs(ctx, (const void* const*)c_out, c) &&
+                     (!update || aligned16(update));
+    if (ctx->dtype == MARSIT_F32)
+        CUDA_TRY(launch_decode(stream_params<float>(ctx, g, c, c_out, update, eta), vec,
+                               ctx->stream_grid, st));
+    else
+        CUDA_TRY(launch_decode(stream_params<double>(ctx, g, c, c_out, update, eta), vec,
+                               ctx->stream_grid, st));
+    return ctx->end_phase(4, st, ev, 1);
+}
+
+marsit_status run_export(marsit_ctx* ctx, uint64_t* out, cudaStream_t st) {
+    if (!out) return MARSIT_OK;
+    cudaEvent_t ev;
+    marsit_status s = ctx->begin_phase(5, st, &ev);
+    if (s) return s;
+    CUDA_TRY(launch_export_bits(ctx->agg, ctx->wst, ctx->D, ctx->L,
+                                reinterpret_cast<uint32_t*>(out), st));
+    return ctx->end_phase(5, st, ev, 1);
+}
+
+marsit_status check_consensus(const marsit_ctx* ctx, bool need_full_count) {
+    for (uint32_t s = 0; s < ctx->S; ++s) {
+        const SegmentPlan& sp = ctx->plan.seg[s];
+        if (!sp.consensus) return fail(MARSIT_EPROTOCOL, "consensus: workers disagree");
+        if (need_full_count && sp.final_count != ctx->M)
+            return fail(MARSIT_EPROTOCOL, "marsit_round: aggregate is missing contributions");
+    }
+    return MARSIT_OK;
+}
+
+template <typename T>
+marsit_status dense_round_impl(marsit_ctx* ctx, const void* const* g, const void* const* c,
+                               void* const* c_out, void* mean, cudaStream_t st) {
+    cudaEvent_t ev;
+    marsit_status s = ctx->begin_phase(6, st, &ev);
+    if (s) return s;
+    DenseParams<T> p{};
+    p.ops = ctx->d_dense_ops;
+    p.final_node = ctx->d_dense_final;
+    p.n_ops = ctx->dense_n_ops;
+    p.n_seg = ctx->s_own;
+    p.s_first = ctx->s_first;
+    p.ml = ctx->ml;
+    p.workers = ctx->M;
+    p.dim = ctx->D;
+    p.seg_len = ctx->L;
+    p.inv_m = 1.0 / double(ctx->M);
+    p.err = ctx->err;
+    uint64_t launches = 0;
+    if (ctx->G == 1) {
+        p.mode = 0;
+        for (uint32_t w = 0; w < ctx->ml; ++w) {
+            p.src[2 * w] = static_cast<const T*>(g[w]);
+            p.src[2 * w + 1] = static_cast<const T*>(c[w]);
+        }
+        p.mean = static_cast<T*>(mean);
+        CUDA_TRY(launch_dense_reduce(p, ctx->stream_grid, st));
+        ++launches;
+    } else {
+        std::vector<const T*> gg(ctx->ml), cc(ctx->ml);
+        for (uint32_t w = 0; w < ctx->ml; ++w) {
+            gg[w] = static_cast<const T*>(g[w]);
+            cc[w] = static_cast<const T*>(c[w]);
+        }
+        CUDA_TRY(launch_dense_leaf<T>(gg.data(), cc.data(), ctx->ml, ctx->D, ctx->L, ctx->S,
+                                      ctx->s_own, static_cast<T*>(ctx->dense_send), ctx->err,
+                                      ctx->stream_grid, st));
+        const size_t block = size_t(ctx->s_own) * ctx->ml * ctx->L;
+        const ncclDataType_t dt = sizeof(T) == 4 ? ncclFloat32 : ncclFloat64;
+        NCCL_TRY(ncclGroupStart());
+        for (uint32_t q = 0; q < ctx->G; ++q) {
+            NCCL_TRY(ncclSend(static_cast<T*>(ctx->dense_send) + q * block, block, dt, int(q),
+                              ctx->comm, st));
+            NCCL_TRY(ncclRecv(static_cast<T*>(ctx->dense_recv) + q * block, block, dt, int(q),
+                              ctx->comm, st));
+        }
+        NCCL_TRY(ncclGroupEnd());
+        p.mode = 1;
+        p.u_buf = static_cast<const T*>(ctx->dense_recv);
+        T* full = static_cast<T*>(ctx->dense_mean);
+        p.mean = full;  // padded [S*L] buffer; owned coordinates written at global index
+        p.dim = uint64_t(ctx->S) * ctx->L;
+        CUDA_TRY(launch_dense_reduce(p, ctx->stream_grid, st));
+        const size_t seg_block = size_t(ctx->s_own) * ctx->L;
+        NCCL_TRY(ncclAllGather(full + ctx->rank * seg_block, full, seg_block, dt, ctx->comm, st));
+        CUDA_TRY(cudaMemcpyAsync(mean, full, ctx->D * sizeof(T), cudaMemcpyDeviceToDevice, st));
+        launches += 2;
+    }
+    for (uint32_t w = 0; w < ctx->ml; ++w)
+        CUDA_TRY(cudaMemsetAsync(c_out[w], 0, ctx->D * sizeof(T), st));  // sync.hpp:83-85
+    return ctx->end_phase(6, st, ev, launches);
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+const char* marsit_last_error(void) { return g_last_error.c_str(); }
+int marsit_abi_version(void) { return MARSIT_B200_ABI_VERSION; }
+
+static marsit_status finish_schedule(marsit_schedule* s, marsit_schedule** out) {
+    s->plan = compile_plan(s->s);
+    *out = s;
+    return MARSIT_OK;
+}
+
+marsit_status marsit_schedule_ring(uint32_t m, marsit_schedule** out) {
+    if (!out) return fail(MARSIT_EPARAM, "out is null");
+    auto s = std::make_unique<marsit_schedule>();
+    std::string msg;
+    if (int rc = build_ring(m, s->s, &msg)) return fail(marsit_status(rc), msg);
+    return finish_schedule(s.release(), out);
+}
+
+marsit_status marsit_schedule_torus(uint32_t rows, uint32_t cols, marsit_schedule** out) {
+    if (!out) return fail(MARSIT_EPARAM, "out is null");
+    auto s = std::make_unique<marsit_schedule>();
+    std::string msg;
+    if (int rc = build_torus(rows, cols, s->s, &msg)) return fail(marsit_status(rc), msg);
+    return finish_schedule(s.release(), out);
+}
+
+marsit_status marsit_schedule_from_tables(uint32_t workers, uint32_t segments, uint32_t steps,
+                                          const uint8_t* phase, const uint32_t* send_to,
+                                          const uint32_t* recv_from, const uint32_t* segment,
+                                          marsit_schedule** out) {
+    if (!out) return fail(MARSIT_EPARAM, "out is null");
+    if (workers == 0 || segments == 0) return fail(MARSIT_EPARAM, "empty schedule");
+    if (steps && (!phase || !send_to || !recv_from || !segment))
+        return fail(MARSIT_EPARAM, "null schedule table");
+    auto s = std::make_unique<marsit_schedule>();
+    s->s.topology = 2;
+    s->s.workers = workers;
+    s->s.segments = segments;
+    const size_t n = size_t(steps) * workers;
+    s->s.phase.assign(phase, phase + steps);
+    s->s.send_to.assign(send_to, send_to + n);
+    s->s.recv_from.assign(recv_from, recv_from + n);
+    s->s.segment.assign(segment, segment + n);
+    std::string msg;
+    if (int rc = validate(s->s, &msg)) return fail(marsit_status(rc), msg);
+    return finish_schedule(s.release(), out);
+}
+
+marsit_status marsit_schedule_info(const marsit_schedule* s, uint32_t* workers,
+                                   uint32_t* segments, uint32_t* steps) {
+    if (!s) return fail(MARSIT_EPARAM, "schedule is null");
+    if (workers) *workers = s->s.workers;
+    if (segments) *segments = s->s.segments;
+    if (steps) *steps = s->s.steps();
+    return MARSIT_OK;
+}
+
+marsit_status marsit_schedule_tables(const marsit_schedule* s, uint8_t* phase,
+                                     uint32_t* send_to, uint32_t* recv_from, uint32_t* segment) {
+    if (!s) return fail(MARSIT_EPARAM, "schedule is null");
+    if (phase) std::copy(s->s.phase.begin(), s->s.phase.end(), phase);
+    if (send_to) std::copy(s->s.send_to.begin(), s->s.send_to.end(), send_to);
+    if (recv_from) std::copy(s->s.recv_from.begin(), s->s.recv_from.end(), recv_from);
+    if (segment) std::copy(s->s.segment.begin(), s->s.segment.end(), segment);
+    return MARSIT_OK;
+}
+
+void marsit_schedule_destroy(marsit_schedule* s) { delete s; }
+
+marsit_status marsit_schedule_plan(const marsit_schedule* s, uint32_t segment, uint32_t capacity,
+                                   marsit_merge_info* merges, uint32_t* n_merges,
+                                   uint32_t* final_node, uint32_t* final_count) {
+    if (!s) return fail(MARSIT_EPARAM, "schedule is null");
+    if (segment >= s->plan.segments) return fail(MARSIT_EPARAM, "segment out of range");
+    const SegmentPlan& sp = s->plan.seg[segment];
+    if (n_merges) *n_merges = uint32_t(sp.merges.size());
+    if (final_node) *final_node = sp.final_node;
+    if (final_count) *final_count = sp.final_count;
+    if (merges)
+        for (size_t k = 0; k < sp.merges.size() && k < capacity; ++k) {
+            const MergeNode& m = sp.merges[k];
+            merges[k] = {m.recv_node, m.local_node, m.receiver, m.c_recv,
+                         m.c_local,   m.offset_src, m.stage};
+        }
+    return MARSIT_OK;
+}
+
+marsit_status marsit_nccl_unique_id(void* out128) {
+    if (!out128) return fail(MARSIT_EPARAM, "out is null");
+    ncclUniqueId id;
+    NCCL_TRY(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(out128, &id, sizeof(id));
+    return MARSIT_OK;
+}
+
+marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out) {
+    if (!desc || !out) return fail(MARSIT_EPARAM, "null argument");
+    *out = nullptr;
+    if (!desc->schedule) return fail(MARSIT_EPARAM, "schedule is null");
+    if (desc->dim == 0) return fail(MARSIT_EPARAM, "DenseVector: dimension must be >= 1");
+    if (desc->dtype != MARSIT_F32 && desc->dtype != MARSIT_F64)
+        return fail(MARSIT_EPARAM, "unknown dtype");
+    const uint32_t G = desc->nranks ? desc->nranks : 1;
+    const HostSchedule& hs = desc->schedule->s;
+    if (hs.workers % G || hs.segments % G)
+        return fail(MARSIT_EUNSUPPORTED, "workers and segments must be divisible by nranks");
+    if (desc->rank >= G) return fail(MARSIT_EPARAM, "rank out of range");
+    if (hs.workers / G > kMaxLocalWorkers)
+        return fail(MARSIT_EUNSUPPORTED, "too many workers per rank (max 64)");
+    if (G > 1 && !desc->nccl_id) return fail(MARSIT_EPARAM, "nccl_id required for nranks > 1");
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(MARSIT_ECUDA, "no CUDA device available (this library has no CPU path)");
+    auto ctx = std::make_unique<marsit_ctx>();
+    ctx->device = desc->device;
+    CUDA_TRY(cudaSetDevice(desc->device));
+    CUDA_TRY(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, desc->device));
+    ctx->dtype = desc->dtype;
+    ctx->esize = desc->dtype == MARSIT_F32 ? 4 : 8;
+    ctx->sched = hs;
+    ctx->plan = desc->schedule->plan;
+    ctx->D = desc->dim;
+    ctx->M = hs.workers;
+    ctx->S = hs.segments;
+    ctx->G = G;
+    ctx->rank = desc->rank;
+    ctx->ml = ctx->M / G;
+    ctx->s_own = ctx->S / G;
+    ctx->s_first = ctx->rank * ctx->s_own;
+    ctx->L = ceil_div(ctx->D, ctx->S);  // segmentation.hpp:32-39
+    if (ctx->L >= (1ull << 37)) return fail(MARSIT_EUNSUPPORTED, "segment too long");
+    ctx->words64 = uint32_t(ceil_div(ctx->L, 64));
+    ctx->words_proc = uint32_t(round_up(2ull * ctx->words64, 4));
+    ctx->wst = uint32_t(round_up(ctx->words_proc, 32));
+    ctx->tiles_per_seg = uint32_t(ceil_div(ctx->words_proc, kTileWords));
+    ctx->vec_ok = (ctx->L % 4) == 0;
+
+    marsit_status st = lower_plan(ctx->plan, ctx->s_first, ctx->s_own, ctx->dp);
+    if (st) return st;
+
+    const size_t wst = ctx->wst;
+    CUDA_TRY(cudaMalloc(&ctx->bits, sizeof(uint32_t) * ctx->S * ctx->ml * wst));
+    CUDA_TRY(cudaMemset(ctx->bits, 0, sizeof(uint32_t) * ctx->S * ctx->ml * wst));
+    CUDA_TRY(cudaMalloc(&ctx->agg, sizeof(uint32_t) * ctx->S * wst));
+    CUDA_TRY(cudaMemset(ctx->agg, 0, sizeof(uint32_t) * ctx->S * wst));
+    if (G > 1) {
+        CUDA_TRY(cudaMalloc(&ctx->recv, sizeof(uint32_t) * ctx->S * ctx->ml * wst));
+        CUDA_TRY(cudaMemset(ctx->recv, 0, sizeof(uint32_t) * ctx->S * ctx->ml * wst));
+    }
+    const uint32_t gmax = std::max<uint32_t>(ctx->dp.gmax, 1);
+    CUDA_TRY(cudaMalloc(&ctx->gnodes, sizeof(uint32_t) * ctx->s_own * gmax * wst));
+    CUDA_TRY(cudaMalloc(&ctx->d_merges, sizeof(DevMerge) * std::max<size_t>(ctx->dp.n_merges, 1)));
+    CUDA_TRY(cudaMemcpy(ctx->d_merges, ctx->dp.merges.data(), sizeof(DevMerge) * ctx->dp.n_merges,
+                        cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMalloc(&ctx->d_seg_begin, sizeof(uint32_t) * ctx->dp.seg_begin.size()));
+    CUDA_TRY(cudaMemcpy(ctx->d_seg_begin, ctx->dp.seg_begin.data(),
+                        sizeof(uint32_t) * ctx->dp.seg_begin.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMalloc(&ctx->d_stage_begin, sizeof(uint32_t) * ctx->dp.stage_begin.size()));
+    CUDA_TRY(cudaMemcpy(ctx->d_stage_begin, ctx->dp.stage_begin.data(),
+                        sizeof(uint32_t) * ctx->dp.stage_begin.size(), cudaMemcpyHostToDevice));
+    const size_t nflags = size_t(ctx->dp.n_merges + 1) * ctx->tiles_per_seg;
+    CUDA_TRY(cudaMalloc(&ctx->flags, sizeof(uint64_t) * nflags));
+    CUDA_TRY(cudaMemset(ctx->flags, 0, sizeof(uint64_t) * nflags));
+    CUDA_TRY(cudaMalloc(&ctx->totals, sizeof(uint64_t) * (ctx->dp.n_merges + 1)));
+    CUDA_TRY(cudaMemset(ctx->totals, 0, sizeof(uint64_t) * (ctx->dp.n_merges + 1)));
+    CUDA_TRY(cudaMalloc(&ctx->counter, sizeof(uint32_t)));
+    CUDA_TRY(cudaMemset(ctx->counter, 0, sizeof(uint32_t)));
+    CUDA_TRY(cudaMalloc(&ctx->err, sizeof(int)));
+    CUDA_TRY(cudaMemset(ctx->err, 0, sizeof(int)));
+
+    ctx->merge_smem = size_t(std::max<uint32_t>(ctx->dp.max_slots, 1)) * kMergeThreads * 16;
+    CUDA_TRY(merge_kernel_set_smem(ctx->merge_smem));
+    int occ = 0;
+    CUDA_TRY(merge_kernel_occupancy(ctx->merge_smem, &occ));
+    ctx->merge_grid = std::max(1, occ) * ctx->sm_count;
+    {
+        // persistent grid-stride launch: exactly the resident CTAs, one wave
+        int ob_extract = 0, ob_decode = 0;
+        CUDA_TRY(stream_occupancy(ctx->dtype == MARSIT_F64, &ob_extract, &ob_decode));
+        ctx->stream_grid = std::max(1, std::min(ob_extract, ob_decode)) * ctx->sm_count;
+    }
+
+    // dense-round plan: per owned segment, the reduction tree (local + received)
+    {
+        std::vector<DenseOp> ops;
+        std::vector<uint16_t> fin(ctx->s_own);
+        uint32_t n_ops = 0;
+        for (uint32_t sl = 0; sl < ctx->s_own; ++sl)
+            n_ops = std::max<uint32_t>(n_ops, uint32_t(ctx->plan.seg[ctx->s_first + sl].merges.size()));
+        if (ctx->M + n_ops > 2 * kMaxLocalWorkers)
+            return fail(MARSIT_EUNSUPPORTED, "dense reduction tree too large");
+        ops.resize(size_t(ctx->s_own) * std::max<uint32_t>(n_ops, 1));
+        for (uint32_t sl = 0; sl < ctx->s_own; ++sl) {
+            const SegmentPlan& sp = ctx->plan.seg[ctx->s_first + sl];
+            for (uint32_t k = 0; k < n_ops; ++k) {
+                DenseOp o{};
+                if (k < sp.merges.size()) {
+                    o.a = uint16_t(sp.merges[k].local_node);
+                    o.b = uint16_t(sp.merges[k].recv_node);
+                } else {  // pad with a harmless op (result unused)
+                    o.a = 0;
+                    o.b = 0;
+                }
+                ops[size_t(sl) * n_ops + k] = o;
+            }
+            fin[sl] = uint16_t(sp.final_node);
+        }
+        ctx->dense_n_ops = n_ops;
+        CUDA_TRY(cudaMalloc(&ctx->d_dense_ops, sizeof(DenseOp) * ops.size()));
+        CUDA_TRY(cudaMemcpy(ctx->d_dense_ops, ops.data(), sizeof(DenseOp) * ops.size(),
+                            cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMalloc(&ctx->d_dense_final, sizeof(uint16_t) * fin.size()));
+        CUDA_TRY(cudaMemcpy(ctx->d_dense_final, fin.data(), sizeof(uint16_t) * fin.size(),
+                            cudaMemcpyHostToDevice));
+    }
+    if (G > 1) {
+        const size_t dense_elems = size_t(ctx->S) * ctx->ml * ctx->L;
+        CUDA_TRY(cudaMalloc(&ctx->dense_send, ctx->esize * dense_elems));
+        CUDA_TRY(cudaMalloc(&ctx->dense_recv, ctx->esize * dense_elems));
+        CUDA_TRY(cudaMalloc(&ctx->dense_mean, ctx->esize * size_t(ctx->S) * ctx->L));
+        ncclUniqueId id;
+        std::memcpy(&id, desc->nccl_id, sizeof(id));
+        NCCL_TRY(ncclCommInitRank(&ctx->comm, int(G), id, int(desc->rank)));
+    }
+    *out = ctx.release();
+    return MARSIT_OK;
+}
+
+void marsit_ctx_destroy(marsit_ctx* ctx) { delete ctx; }
+
+marsit_status marsit_ctx_local_workers(const marsit_ctx* ctx, uint32_t* first, uint32_t* count) {
+    if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
+    if (first) *first = ctx->rank * ctx->ml;
+    if (count) *count = ctx->ml;
+    return MARSIT_OK;
+}
+
+marsit_status marsit_sign_round(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_t seed,
+                                const void* const* d_grads, const void* const* d_comp,
+                                void* const* d_comp_out, uint64_t* d_agg_bits, void* d_update,
+                                void* stream) {
+    if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
+    if (!(eta_s > 0.0)) return fail(MARSIT_EPARAM, "SyncConfig: eta_s must be > 0");
+    marsit_status s;
+    if ((s = check_ptrs(ctx, d_grads, "grads")) || (s = check_ptrs(ctx, d_comp, "comp")) ||
+        (s = check_ptrs(ctx, (const void* const*)d_comp_out, "comp_out")))
+        return s;
+    if ((s = check_consensus(ctx, true))) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    if ((s = run_extract(ctx, d_grads, d_comp, st))) return s;
+    if ((s = run_exchange(ctx, st))) return s;
+    if ((s = run_merge(ctx, seed, t, st))) return s;
+    if ((s = run_allgather(ctx, st))) return s;
+    if ((s = run_decode(ctx, d_grads, d_comp, d_comp_out, d_update, eta_s, st))) return s;
+    return run_export(ctx, d_agg_bits, st);
+}
+
+marsit_status marsit_dense_round(marsit_ctx* ctx, uint64_t, const void* const* d_grads,
+                                 const void* const* d_comp, void* const* d_comp_out, void* d_mean,
+                                 void* stream) {
+    if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
+    if (!d_mean) return fail(MARSIT_EPARAM, "mean is null");
+    marsit_status s;
+    if ((s = check_ptrs(ctx, d_grads, "grads")) || (s = check_ptrs(ctx, d_comp, "comp")) ||
+        (s = check_ptrs(ctx, (const void* const*)d_comp_out, "comp_out")))
+        return s;
+    if ((s = check_consensus(ctx, false))) return s;
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (ctx->dtype == MARSIT_F32)
+        return dense_round_impl<float>(ctx, d_grads, d_comp, d_comp_out, d_mean, st);
+    return dense_round_impl<double>(ctx, d_grads, d_comp, d_comp_out, d_mean, st);
+}
+
+marsit_status marsit_round(marsit_ctx* ctx, uint64_t t, uint64_t period, double eta_s,
+                           uint64_t seed, const void* const* d_grads, const void* const* d_comp,
+                           void* const* d_comp_out, uint64_t* d_agg_bits, void* d_update,
+                           int* full_precision, void* stream) {
+    if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
+    // SyncConfig::validate (sync.hpp:27-34); "never" is period == 0 here.
+    if (!(eta_s > 0.0)) return fail(MARSIT_EPARAM, "SyncConfig: eta_s must be > 0");
+    const bool dense = period != 0 && (t % period == 0);  // sync.hpp:78
+    if (full_precision) *full_precision = dense ? 1 : 0;
+    if (dense) {
+        if (!d_update) return fail(MARSIT_EPARAM, "dense round needs d_update for the mean");
+        return marsit_dense_round(ctx, t, d_grads, d_comp, d_comp_out, d_update, stream);
+    }
+    return marsit_sign_round(ctx, t, eta_s, seed, d_grads, d_comp, d_comp_out, d_agg_bits,
+                             d_update, stream);
+}
+
+marsit_status marsit_sign_extract(marsit_ctx* ctx, const void* const* d_grads,
+                                  const void* const* d_comp, uint64_t* d_signs_out, void* stream) {
+    if (!ctx || !d_signs_out) return fail(MARSIT_EPARAM, "null argument");
+    marsit_status s;
+    if ((s = check_ptrs(ctx, d_grads, "grads")) || (s = check_ptrs(ctx, d_comp, "comp"))) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    if ((s = run_extract(ctx, d_grads, d_comp, st))) return s;
+    const size_t row = size_t(ctx->words64) * 8;
+    for (uint32_t w = 0; w < ctx->ml; ++w)
+        CUDA_TRY(cudaMemcpy2DAsync(d_signs_out + size_t(w) * ctx->S * ctx->words64, row,
+                                   ctx->bits + size_t(w) * ctx->wst, size_t(ctx->ml) * ctx->wst * 4,
+                                   row, ctx->S, cudaMemcpyDeviceToDevice, st));
+    return MARSIT_OK;
+}
+
+marsit_status marsit_allreduce_sign(marsit_ctx* ctx, uint64_t round, uint64_t seed,
+                                    const uint64_t* d_signs, uint64_t* d_out, uint32_t* counts,
+                                    void* stream) {
+    if (!ctx || !d_signs || !d_out) return fail(MARSIT_EPARAM, "null argument");
+    marsit_status s;
+    if ((s = check_consensus(ctx, false))) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    const size_t row = size_t(ctx->words64) * 8;
+    for (uint32_t w = 0; w < ctx->ml; ++w)
+        CUDA_TRY(cudaMemcpy2DAsync(ctx->bits + size_t(w) * ctx->wst, size_t(ctx->ml) * ctx->wst * 4,
+                                   d_signs + size_t(w) * ctx->S * ctx->words64, row, row, ctx->S,
+                                   cudaMemcpyDeviceToDevice, st));
+    if ((s = run_exchange(ctx, st))) return s;
+    if ((s = run_merge(ctx, seed, round, st))) return s;
+    if ((s = run_allgather(ctx, st))) return s;
+    CUDA_TRY(cudaMemcpy2DAsync(d_out, row, ctx->agg, size_t(ctx->wst) * 4, row, ctx->S,
+                               cudaMemcpyDeviceToDevice, st));
+    if (counts)
+        for (uint32_t sg = 0; sg < ctx->S; ++sg) counts[sg] = ctx->plan.seg[sg].final_count;
+    return MARSIT_OK;
+}
+
+marsit_status marsit_merge_signs(const uint64_t* d_recv, uint32_t c_recv, const uint64_t* d_local,
+                                 uint32_t c_local, uint64_t len, uint64_t key, uint64_t used,
+                                 uint64_t* d_out, uint64_t* consumed, int device, void* stream) {
+    // merge.hpp:42-47 validation order: length is implied equal here.
+    if (c_recv == 0 || c_local == 0)
+        return fail(MARSIT_EPARAM, "merge_signs: aggregate count must be >= 1");
+    if (!d_recv || !d_local || !d_out) return fail(MARSIT_EPARAM, "null argument");
+    if (len == 0) return MARSIT_OK;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(MARSIT_ECUDA, "no CUDA device available (this library has no CPU path)");
+    CUDA_TRY(cudaSetDevice(device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint64_t words64 = ceil_div(len, 64);
+    const uint32_t words_proc = uint32_t(round_up(2 * words64, 4));
+    const uint32_t wst = uint32_t(round_up(words_proc, 32));
+    const uint32_t tiles = uint32_t(ceil_div(words_proc, kTileWords));
+    // scratch: leaves [2][wst], agg [wst], flags [tiles], totals, counter, plan
+    struct Scratch {
+        void* p = nullptr;
+        ~Scratch() {
+            if (p) cudaFree(p);
+        }
+    } scratch;
+    const size_t leaves_b = sizeof(uint32_t) * 2 * wst, agg_b = sizeof(uint32_t) * wst;
+    const size_t flags_b = sizeof(uint64_t) * tiles;
+    const size_t total_b = leaves_b + agg_b + flags_b + 64 + sizeof(DevMerge) + 64;
+    CUDA_TRY(cudaMalloc(&scratch.p, total_b));
+    char* base = static_cast<char*>(scratch.p);
+    CUDA_TRY(cudaMemsetAsync(base, 0, total_b, st));
+    uint32_t* leaves = reinterpret_cast<uint32_t*>(base);
+    uint32_t* agg = reinterpret_cast<uint32_t*>(base + leaves_b);
+    uint64_t* flags = reinterpret_cast<uint64_t*>(base + leaves_b + agg_b);
+    uint64_t* totals = reinterpret_cast<uint64_t*>(base + leaves_b + agg_b + flags_b);
+    uint32_t* counter = reinterpret_cast<uint32_t*>(base + leaves_b + agg_b + flags_b + 16);
+    uint32_t* meta = reinterpret_cast<uint32_t*>(base + leaves_b + agg_b + flags_b + 32);
+    DevMerge* dm = reinterpret_cast<DevMerge*>(base + leaves_b + agg_b + flags_b + 64);
+    CUDA_TRY(cudaMemcpyAsync(leaves, d_recv, words64 * 8, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(leaves + wst, d_local, words64 * 8, cudaMemcpyDeviceToDevice, st));
+    DevMerge m{};
+    m.thresh11 = coin_threshold(c_recv, c_local) << 11;
+    m.key = key;
+    m.base_add = used;
+    m.key_mode = 1;
+    m.recv_src = uint16_t(kSrcLeaf | 0);
+    m.local_src = uint16_t(kSrcLeaf | 1);
+    m.out_slot = kNone;
+    m.out_global = kFinal;
+    m.offset_src = -1;
+    const uint32_t host_meta[3] = {0, 0, 1};  // seg_begin[0]; stage_begin[0..1]
+    CUDA_TRY(cudaMemcpyAsync(dm, &m, sizeof(m), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(meta, host_meta, sizeof(host_meta), cudaMemcpyHostToDevice, st));
+    MergeParams p{};
+    p.merges = dm;
+    p.seg_begin = meta;
+    p.stage_begin = meta + 1;
+    p.n_stages = 1;
+    p.stage = 0;
+    p.n_seg = 1;
+    p.s_first = 0;
+    p.tiles_per_seg = tiles;
+    p.words_proc = words_proc;
+    p.wst = wst;
+    p.ml = 2;
+    p.seg_bits = len;
+    p.leaves = leaves;
+    p.gnodes = agg;
+    p.gmax = 1;
+    p.agg = agg;
+    p.flags = flags;
+    p.totals = totals;
+    p.tile_counter = counter;
+    p.tile_base = 0;
+    p.epoch = 1;
+    const size_t smem = kMergeThreads * 16;
+    CUDA_TRY(merge_kernel_set_smem(smem));
+    CUDA_TRY(launch_merge(p, int(std::min<uint32_t>(tiles, 148 * 4)), smem, st));
+    CUDA_TRY(cudaMemcpyAsync(d_out, agg, words64 * 8, cudaMemcpyDeviceToDevice, st));
+    uint64_t tot = 0;
+    CUDA_TRY(cudaMemcpyAsync(&tot, totals, sizeof(tot), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (consumed) *consumed = tot;
+    return MARSIT_OK;
+}
+
+marsit_status marsit_bits_account(const marsit_ctx* ctx, int dense, uint64_t* per_worker,
+                                  uint64_t* reduce_bits, uint64_t* gather_bits, uint64_t* total) {
+    if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
+    const uint64_t unit = dense ? 32ull * ctx->L : ctx->L;  // allreduce.hpp:113, 182
+    uint64_t t = 0;
+    for (uint32_t w = 0; w < ctx->M; ++w) {
+        const uint64_t b = ctx->plan.sends_per_worker[w] * unit;
+        if (per_worker) per_worker[w] = b;
+        t += b;
+    }
+    if (reduce_bits) *reduce_bits = ctx->plan.reduce_sends * unit;
+    if (gather_bits) *gather_bits = ctx->plan.gather_sends * unit;
+    if (total) *total = t;
+    return MARSIT_OK;
+}
+
+marsit_status marsit_ctx_check(marsit_ctx* ctx, void* stream) {
+    if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int flag = 0;
+    CUDA_TRY(cudaMemcpyAsync(&flag, ctx->err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    CUDA_TRY(cudaGetLastError());
+    if (flag) {
+        CUDA_TRY(cudaMemsetAsync(ctx->err, 0, sizeof(int), st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        return fail(MARSIT_ENONFINITE, "DenseVector: non-finite entry");
+    }
+    return MARSIT_OK;
+}
+
+marsit_status marsit_ctx_set_timing(marsit_ctx* ctx, int enable) {
+    if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
+    ctx->timing = enable != 0;
+    return MARSIT_OK;
+}
+
+marsit_status marsit_ctx_timing(marsit_ctx* ctx, float* ms, uint64_t* launches, int reset) {
+    if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    for (auto& tp : ctx->pending) {
+        CUDA_TRY(cudaEventSynchronize(tp.b));
+        float e = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&e, tp.a, tp.b));
+        ctx->ms[tp.phase] += e;
+        ctx->event_pool.push_back(tp.a);
+        ctx->event_pool.push_back(tp.b);
+    }
+    ctx->pending.clear();
+    for (int i = 0; i < MARSIT_N_PHASES; ++i) {
+        if (ms) ms[i] = ctx->ms[i];
+        if (launches) launches[i] = ctx->launches[i];
+        if (reset) {
+            ctx->ms[i] = 0.f;
+            ctx->launches[i] = 0;
+        }
+    }
+    return MARSIT_OK;
+}
+
+marsit_status marsit_fill_recipe(int recipe, uint64_t seed, uint64_t worker, uint64_t round,
+                                 uint64_t dim, marsit_dtype dtype, void* d_out, void* stream) {
+    if (!d_out) return fail(MARSIT_EPARAM, "out is null");
+    if (recipe != 0 && recipe != 1) return fail(MARSIT_EPARAM, "unknown recipe");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (dtype == MARSIT_F32)
+        CUDA_TRY(launch_fill_recipe<float>(recipe, seed, worker, round, dim,
+                                           static_cast<float*>(d_out), st));
+    else
+        CUDA_TRY(launch_fill_recipe<double>(recipe, seed, worker, round, dim,
+                                            static_cast<double*>(d_out), st));
+    return MARSIT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,276 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's golden
+fixtures and the C oracle, bit-exact for sign words / aggregate bits, exact
+for compensation when the inputs are fp32-exact (dyadic recipe) and within
+1e-6 relative (+ tiny absolute floor) for Gaussian fp32 inputs."""
+import hashlib
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2204_06787_b200 as mb  # noqa: E402
+import pyoracle as O  # noqa: E402
+from conftest import load_golden  # noqa: E402
+
+DEV = "cuda:0"
+ETA = 2.0 ** -10
+
+
+def fx(lst):
+    return np.array([float.fromhex(x) for x in lst], np.float64)
+
+
+def wx(lst):
+    return np.array([int(x, 16) for x in lst], np.uint64)
+
+
+def sched_of(topo, a, b):
+    return mb.build_ring_schedule(a) if topo == "ring" else mb.build_torus_schedule(a, b)
+
+
+def to_dev(arr, dtype):
+    return [torch.tensor(x, dtype=dtype, device=DEV) for x in arr]
+
+
+def u64(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, "<f8").tobytes()).hexdigest()
+
+
+def golden_inputs(case, rnd, W):
+    if "grads" in rnd:
+        return fx(rnd["grads"]).reshape(W, case["dim"])
+    gen = O.gen_dyadic if case["recipe"] == "dyadic" else O.gen_correlated
+    return np.stack([gen(case["seed"], w, rnd["t"], case["dim"]) for w in range(W)])
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_rounds_match_reference_golden(dtype):
+    for case in load_golden("rounds"):
+        exact_inputs = case["recipe"] in ("dyadic", "correlated")
+        if dtype == torch.float32 and case["recipe"] == "special":
+            continue  # its subnormal doubles are not fp32-representable
+        sched = sched_of(case["topology"], case["a"], case["b"])
+        W, D = sched.workers, case["dim"]
+        cfg = mb.SyncConfig(case["period"], case["eta_s"])
+        comp = [torch.zeros(D, dtype=dtype, device=DEV) for _ in range(W)]
+        for rnd in case["rounds"]:
+            g = golden_inputs(case, rnd, W)
+            res = mb.marsit_round(rnd["t"], cfg, to_dev(g, dtype), comp, sched, case["seed"])
+            assert res.full_precision == rnd["full_precision"]
+            assert res.bits.per_worker == rnd["bits_per_worker"]
+            assert (res.bits.reduce_bits, res.bits.gather_bits) == (rnd["reduce_bits"],
+                                                                   rnd["gather_bits"])
+            if not rnd["full_precision"]:
+                assert u64(res.aggregate_bits).tolist() == wx(rnd["agg_bits"]).tolist(), case
+            got_c = np.stack([c.c.double().cpu().numpy() for c in res.compensation])
+            got_u = res.global_update.double().cpu().numpy()
+            exact = dtype == torch.float64 or (exact_inputs and not rnd["full_precision"])
+            if "comp" in rnd:
+                want_c = fx(rnd["comp"]).reshape(W, D)
+                want_u = fx(rnd["update"])
+                if exact:
+                    assert np.array_equal(got_c, want_c), case
+                    assert np.array_equal(got_u, want_u), case
+                else:
+                    # fp32 arithmetic vs the reference's fp64: 1e-6 relative with an
+                    # absolute floor of 1e-6 * eta_s (SURVEY §7 hard part 3c)
+                    np.testing.assert_allclose(got_c, want_c, rtol=1e-6,
+                                               atol=1e-6 * max(case["eta_s"], np.abs(g).max()))
+                    np.testing.assert_allclose(got_u, want_u, rtol=1e-6,
+                                               atol=1e-6 * max(case["eta_s"], np.abs(g).max()))
+            else:
+                assert exact
+                assert sha(got_c) == rnd["comp_sha256"], case
+                assert sha(got_u) == rnd["update_sha256"], case
+            comp = [c.c for c in res.compensation]
+
+
+def test_survey_anchors_c1():
+    """SURVEY §8c known answers for C1 (ring D=1M, M=4, rounds 1..3, fp32)."""
+    sched = mb.build_ring_schedule(4)
+    D = 1_000_000
+    cfg = mb.SyncConfig(None, ETA)
+    comp = [torch.zeros(D, device=DEV) for _ in range(4)]
+    gold = [g for g in load_golden("anchors") if g["dim"] == D]
+    for gd in gold:
+        t = gd["t"]
+        g = [torch.empty(D, device=DEV) for _ in range(4)]
+        for w in range(4):
+            mb.fill_recipe(g[w], 0, 2026, w, t)
+        res = mb.marsit_round(t, cfg, g, comp, sched, 2026, inplace=True)
+        bits = u64(res.aggregate_bits)
+        assert int(sum(bin(int(x)).count("1") for x in bits)) == gd["popcount"]
+        assert "%016x" % O.fnv1a64(bits) == gd["fnv1a64"]
+        assert float(comp[0][0]) == float.fromhex(gd["c00"])
+        assert float(comp[0].double().sum()) == pytest.approx(float.fromhex(gd["sum_c0"]),
+                                                              abs=1e-12)
+
+
+def test_device_recipe_matches_oracle_recipe():
+    out = torch.empty(10_007, device=DEV)
+    for recipe, gen in ((0, O.gen_dyadic), (1, O.gen_correlated)):
+        mb.fill_recipe(out, recipe, 2026, 3, 7)
+        assert np.array_equal(out.double().cpu().numpy(), gen(2026, 3, 7, 10_007))
+
+
+@pytest.mark.parametrize("topo,a,b,D,rounds", [
+    ("ring", 4, 0, 1_000_000, 3),        # C1
+    ("ring", 8, 0, 1_000_003, 2),        # odd D: L % 4 != 0 -> scalar path
+    ("torus", 2, 4, 602_001, 2),         # torus with stream continuation
+    ("ring", 2, 0, 64 * 1024 * 3 + 17, 2),
+    ("ring", 3, 0, 5, 3),
+    ("ring", 4, 0, 3, 2),                # one segment is pure padding
+])
+def test_multi_round_vs_oracle(topo, a, b, D, rounds):
+    sched = sched_of(topo, a, b)
+    T = O.schedule(topo, a, b)
+    W = sched.workers
+    cfg = mb.SyncConfig(None, ETA)
+    comp_d = [torch.zeros(D, device=DEV) for _ in range(W)]
+    comp_h = np.zeros((W, D))
+    for t in range(1, rounds + 1):
+        gh = np.stack([O.gen_correlated(77, w, t, D) if t % 2 else O.gen_dyadic(77, w, t, D)
+                       for w in range(W)])
+        res = mb.marsit_round(t, cfg, to_dev(gh, torch.float32), comp_d, sched, 77, inplace=True)
+        want = O.marsit_round(T, t, None, ETA, gh, comp_h, 77)
+        assert want.status == 0
+        assert np.array_equal(u64(res.aggregate_bits), want.agg_bits)
+        got = np.stack([c.double().cpu().numpy() for c in comp_d])
+        assert np.array_equal(got, want.comp)
+        assert np.array_equal(res.global_update.double().cpu().numpy(), want.update)
+        comp_h = want.comp
+
+
+@pytest.mark.slow
+def test_c3_full_size_round_vs_oracle():
+    """The bench workload (ring M=8, D=25.6M): one round bit-exact vs the oracle."""
+    D, W = 25_600_000, 8
+    sched = mb.build_ring_schedule(W)
+    g = [torch.empty(D, device=DEV) for _ in range(W)]
+    for w in range(W):
+        mb.fill_recipe(g[w], 0, 2026, w, 1)
+    comp = [torch.zeros(D, device=DEV) for _ in range(W)]
+    res = mb.marsit_round(1, mb.SyncConfig(None, ETA), g, comp, sched, 2026, want_update=False)
+    gh = np.stack([O.gen_dyadic(2026, w, 1, D) for w in range(W)])
+    want = O.marsit_round(O.schedule("ring", W), 1, None, ETA, gh, np.zeros((W, D)), 2026)
+    assert np.array_equal(u64(res.aggregate_bits), want.agg_bits)
+    for w in (0, W - 1):
+        assert np.array_equal(res.compensation[w].c.double().cpu().numpy(), want.comp[w])
+
+
+def test_merge_signs_matches_reference_golden():
+    for rec in load_golden("merges"):
+        L = rec["length"]
+        key = mb.stream_key(rec["seed"], 5, rec["w"], rec["t"], rec["s"])
+        r = torch.tensor(wx(rec["recv"]).view(np.int64), device=DEV)
+        l_ = torch.tensor(wx(rec["local"]).view(np.int64), device=DEV)
+        out, used = mb.merge_signs(mb.AggregateSign(r, rec["c_recv"], L),
+                                   mb.AggregateSign(l_, rec["c_local"], L), key, rec["skip"])
+        assert u64(out.bits).tolist() == wx(rec["out"]).tolist()
+        assert used == rec["consumed"]
+        assert out.count == rec["c_recv"] + rec["c_local"]
+
+
+def test_merge_signs_large_multi_tile_vs_oracle():
+    rng = np.random.default_rng(1)
+    for L in (32768 * 3 + 5, 200_000):
+        nw = (L + 63) // 64
+        r = rng.integers(0, 2**63, nw, dtype=np.uint64) * 2 + rng.integers(0, 2, nw, dtype=np.uint64)
+        l_ = rng.integers(0, 2**63, nw, dtype=np.uint64)
+        r[-1] &= np.uint64((1 << (L % 64)) - 1)
+        l_[-1] &= np.uint64((1 << (L % 64)) - 1)
+        key = O.stream_key(5, 5, 1, 2, 3)
+        want, used = O.merge_signs(r, 3, l_, 2, L, key, 17)
+        out, consumed = mb.merge_signs(
+            mb.AggregateSign(torch.tensor(r.view(np.int64), device=DEV), 3, L),
+            mb.AggregateSign(torch.tensor(l_.view(np.int64), device=DEV), 2, L), key, 17)
+        assert np.array_equal(u64(out.bits), want)
+        assert consumed == used - 17
+
+
+def test_allreduce_sign_matches_reference_golden():
+    for rec in load_golden("allreduce"):
+        sched = sched_of(rec["topology"], rec["a"], rec["b"])
+        L = rec["seg_len"]
+        nw = (L + 63) // 64
+        signs = torch.tensor(wx(rec["signs"]).view(np.int64).reshape(sched.workers,
+                                                                    sched.segments, nw),
+                             device=DEV)
+        out, counts = mb.allreduce_sign(signs, sched, rec["seed"], rec["round"], L)
+        state = wx(rec["state"]).reshape(sched.workers, sched.segments, nw)
+        assert u64(out).reshape(sched.segments, nw).tolist() == state[0].tolist()
+        assert counts == rec["counts"][:sched.segments]
+
+
+def test_pack_signs_matches_oracle_with_zeros_and_subnormals():
+    rng = np.random.default_rng(2)
+    W, D = 5, 10_001
+    sched = mb.build_ring_schedule(W)
+    g = rng.standard_normal((W, D)).astype(np.float32)
+    c = rng.standard_normal((W, D)).astype(np.float32)
+    g[:, ::5] = 0.0
+    g[:, 1::5] = -0.0
+    c[:, ::5] = 0.0
+    c[:, 1::5] = -0.0  # -0.0 + -0.0 = -0.0 -> bit 1
+    g[:, 2::5] = np.float32(1e-45)
+    c[:, 2::5] = 0.0
+    g[:, 3::5] = np.float32(-1e-45)
+    c[:, 3::5] = 0.0
+    out = mb.pack_signs(to_dev(g, torch.float32), to_dev(c, torch.float32), sched)
+    L = -(-D // W)
+    u = g.astype(np.float64) + c.astype(np.float64)
+    for w in range(W):
+        for s in range(W):
+            part = np.zeros(L)
+            lo, hi = s * L, min((s + 1) * L, D)
+            part[:hi - lo] = u[w, lo:hi]
+            assert u64(out[w, s]).tolist() == O.pack_signs(part).tolist()
+
+
+def test_errors_map_to_reference_exceptions():
+    sched = mb.build_ring_schedule(2)
+    g = [torch.ones(8, device=DEV), torch.ones(8, device=DEV)]
+    c = [torch.zeros(8, device=DEV), torch.zeros(8, device=DEV)]
+    with pytest.raises(mb.ParameterError):
+        mb.marsit_round(1, mb.SyncConfig(0, 0.1), g, c, sched, 1)
+    with pytest.raises(mb.ParameterError):
+        mb.marsit_round(1, mb.SyncConfig(None, 0.0), g, c, sched, 1)
+    with pytest.raises(mb.ParameterError):
+        mb.marsit_round(1, mb.SyncConfig(None, 0.1), g[:1], c, sched, 1)
+    bad = [torch.ones(8, device=DEV), torch.tensor([1.0] * 7 + [float("nan")], device=DEV)]
+    with pytest.raises(mb.NonFiniteError):
+        mb.marsit_round(1, mb.SyncConfig(None, 0.1), bad, c, sched, 1)
+    big = [torch.full((8,), 3e38, device=DEV)] * 2
+    with pytest.raises(mb.NonFiniteError):  # u = g + c overflows
+        mb.marsit_round(1, mb.SyncConfig(None, 0.1), big, big, sched, 1)
+    # the latch is cleared: the next good round succeeds
+    mb.marsit_round(2, mb.SyncConfig(None, 0.1), g, c, sched, 1)
+    with pytest.raises(mb.ParameterError):
+        mb.build_ring_schedule(1)
+    with pytest.raises(mb.ParameterError):
+        mb.build_torus_schedule(1, 3)
+
+
+def test_value_semantics_and_inplace_agree():
+    sched = mb.build_torus_schedule(2, 3)
+    D = 4099
+    g = [torch.empty(D, device=DEV) for _ in range(6)]
+    for w in range(6):
+        mb.fill_recipe(g[w], 0, 9, w, 1)
+    c0 = [torch.zeros(D, device=DEV) for _ in range(6)]
+    a = mb.marsit_round(1, mb.SyncConfig(None, ETA), g, c0, sched, 9)
+    assert all(float(c.abs().sum()) == 0.0 for c in c0)  # inputs untouched
+    c1 = [torch.zeros(D, device=DEV) for _ in range(6)]
+    b = mb.marsit_round(1, mb.SyncConfig(None, ETA), g, c1, sched, 9, inplace=True)
+    for x, y in zip(a.compensation, c1):
+        assert torch.equal(x.c, y)
+    assert torch.equal(a.aggregate_bits, b.aggregate_bits)
