@@ -171,8 +171,9 @@ marsit_status marsit_ctx_check(marsit_ctx* ctx, void* stream);
 
 /* Per-phase device timing (CUDA events on the launching stream).
  * Phases: 0 sign_extract, 1 exchange, 2 merge, 3 allgather, 4 decode_comp,
- * 5 export, 6 dense.  ms[i] accumulates; launches[i] counts kernel launches. */
-#define MARSIT_N_PHASES 7
+ * 5 export, 6 dense, 7 coins (coin precompute, on the context's side stream,
+ * overlapping phase 0).  ms[i] accumulates; launches[i] counts kernel launches. */
+#define MARSIT_N_PHASES 8
 marsit_status marsit_ctx_set_timing(marsit_ctx* ctx, int enable);
 marsit_status marsit_ctx_timing(marsit_ctx* ctx, float* ms, uint64_t* launches, int reset);
 

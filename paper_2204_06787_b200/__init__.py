@@ -74,9 +74,12 @@ class Schedule:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and N._lib is not None:
-            N.lib().marsit_schedule_destroy(h)
-            self._h = None
+        try:
+            if h is not None and h.value and N._lib is not None:
+                N._lib.marsit_schedule_destroy(h)
+        except Exception:  # interpreter shutdown
+            pass
+        self._h = None
 
     @staticmethod
     def from_tables(workers, segments, phase, send_to, recv_from, segment) -> "Schedule":
@@ -239,9 +242,12 @@ class Context:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and N._lib is not None:
-            N.lib().marsit_ctx_destroy(h)
-            self._h = None
+        try:
+            if h is not None and h.value and N._lib is not None:
+                N._lib.marsit_ctx_destroy(h)
+        except Exception:  # interpreter shutdown
+            pass
+        self._h = None
 
     # raw entry points ------------------------------------------------------
     def sign_round(self, t, eta_s, seed, grads, comp, comp_out=None, agg_bits=None,

@@ -10,12 +10,13 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libmarsit_b200.so")
+SO_PATH = os.environ.get("MARSIT_SO") or os.path.join(HERE, "libmarsit_b200.so")
 
 # status codes (include/marsit_b200.h)
 OK, EPARAM, ENONFINITE, EPROTOCOL, EUNSUPPORTED, ECUDA, ENCCL = range(7)
-N_PHASES = 7
-PHASES = ("sign_extract", "exchange", "merge", "allgather", "decode_comp", "export", "dense")
+N_PHASES = 8
+PHASES = ("sign_extract", "exchange", "merge", "allgather", "decode_comp", "export", "dense",
+          "coins")
 
 F32, F64 = 0, 1
 

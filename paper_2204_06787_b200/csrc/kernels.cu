@@ -33,6 +33,34 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
+// The same finalizer with the 64-bit shifts of the xor-shifts moved onto the
+// FMA pipe: for the low word, (lo >> s) == mulhi(lo, 2^(32-s)) and the bits
+// carried in from the high word are hi * 2^(32-s).  Bit-identical to mix64;
+// it only balances the ALU / FMA pipes (each issues every other cycle).
+__device__ __forceinline__ uint32_t mulhi32(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ void xorshr_fma(uint32_t& lo, uint32_t& hi, uint32_t m) {
+    const uint32_t nlo = lo ^ mulhi32(lo, m) ^ (hi * m);
+    hi ^= mulhi32(hi, m);
+    lo = nlo;
+}
+__device__ __forceinline__ uint64_t mix64f(uint64_t z) {
+    uint32_t lo = uint32_t(z), hi = uint32_t(z >> 32);
+    xorshr_fma(lo, hi, 1u << 2);  // >> 30
+    uint64_t t = ((uint64_t(hi) << 32) | lo) * 0xbf58476d1ce4e5b9ull;
+    lo = uint32_t(t);
+    hi = uint32_t(t >> 32);
+    xorshr_fma(lo, hi, 1u << 5);  // >> 27
+    t = ((uint64_t(hi) << 32) | lo) * 0x94d049bb133111ebull;
+    lo = uint32_t(t);
+    hi = uint32_t(t >> 32);
+    xorshr_fma(lo, hi, 1u << 1);  // >> 31
+    return (uint64_t(hi) << 32) | lo;
+}
+
 __device__ __forceinline__ uint64_t stream_key(uint64_t seed, uint64_t purpose, uint64_t w,
                                                uint64_t t, uint64_t s) {
     uint64_t h = mix64(seed ^ 0x6a09e667f3bcc909ull);
@@ -123,57 +151,70 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
 
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+
 template <typename T>
 __device__ __forceinline__ bool finite(T x) {
     return isfinite(x);
 }
 
-// bit j of a byte -> bit 4j of a word (Morton spread by 4)
-__device__ __forceinline__ uint32_t spread4(uint32_t x) {
-    x &= 0xffu;
-    x = (x | (x << 12)) & 0x000F000Fu;
-    x = (x | (x << 6)) & 0x03030303u;
-    x = (x | (x << 3)) & 0x11111111u;
-    return x;
+// Word holding the sign bit in its top byte.
+__device__ __forceinline__ uint32_t sign_word(float x) { return __float_as_uint(x); }
+__device__ __forceinline__ uint32_t sign_word(double x) { return uint32_t(__double2hiint(x)); }
+
+// bit k = (v_k >= 0) for values whose -0.0 has been folded to +0.0: the four
+// sign bytes are gathered with byte permutes, inverted, and compacted to a
+// nibble by one multiply-high (bits 7/15/23/31 -> 32/33/34/35).
+template <typename T>
+__device__ __forceinline__ uint32_t sign_nibble(T a, T b, T c, T d) {
+    const uint32_t r1 = __byte_perm(sign_word(a), sign_word(b), 0x0073);
+    const uint32_t r2 = __byte_perm(sign_word(c), sign_word(d), 0x7300);
+    const uint32_t r = __byte_perm(r1, r2, 0x7610);
+    return __umulhi(~r & 0x80808080u, 0x02040810u) & 0xFu;
 }
+
 
 // ---------------------------------------------------------------------------
 // K1: error-compensated sign extraction.
 //
 // A warp task is 512 consecutive coordinates of one (worker, segment):
 // 16 packed u32 words.  Vector path (L % 4 == 0): lane l holds coordinates
-// 4l..4l+3 of each 128-coordinate sub-chunk, so ballot k collects bit
-// (4l + k); word q of the sub-chunk is the 4-way bit interleave of byte q of
-// the four ballots.  Scalar path: lane l holds coordinate 32t + l of word t
-// and the ballot is the word.  Coordinates j >= L are storage padding (bit
+// 4l..4l+3 of each 128-coordinate sub-chunk (one 128-bit load per operand),
+// packs them into a nibble, and 8-lane OR-shuffles assemble the words.
+// Scalar path: lane l holds coordinate 32t + l of word t and a ballot is the
+// word.  Coordinates j >= L are storage padding (bit
 // 0, sign_vector.hpp:15-18); s*L + j >= D is value padding, 0.0, bit 1
 // (segmentation.hpp:45-49 + sign_vector.hpp:70).
 // ---------------------------------------------------------------------------
 template <typename T, bool VEC>
-__global__ void __launch_bounds__(kStreamThreads) extract_kernel(const StreamParams<T> p) {
+__global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 4 : 2) extract_kernel(const StreamParams<T> p) {
     const int lane = threadIdx.x & 31;
     const uint32_t warps = gridDim.x * (kStreamThreads / 32);
     const uint32_t tasks_per_seg = (p.words_proc + kTaskWords - 1) / kTaskWords;
-    const uint64_t n_tasks = uint64_t(tasks_per_seg) * p.n_seg * p.ml;
+    const uint64_t n_tasks = uint64_t(tasks_per_seg) * p.n_proc * p.ml;
     bool bad = false;
+    T fin = T(0);  // stays 0 unless some u = g + c is not finite
     for (uint64_t task = blockIdx.x * (kStreamThreads / 32) + (threadIdx.x >> 5); task < n_tasks;
          task += warps) {
         const uint32_t q = uint32_t(task % tasks_per_seg);
         const uint64_t rest = task / tasks_per_seg;
-        const uint32_t s = uint32_t(rest % p.n_seg);
-        const uint32_t wl = uint32_t(rest / p.n_seg);
+        const uint32_t s = p.seg0 + uint32_t(rest % p.n_proc);
+        const uint32_t wl = uint32_t(rest / p.n_proc);
         const T* __restrict__ g = p.g[wl];
         const T* __restrict__ c = p.c[wl];
         const uint64_t seg0 = uint64_t(s) * p.seg_len;  // first global coordinate
         const uint64_t j0 = uint64_t(q) * (kTaskWords * 32);
-        uint32_t word = 0;  // lane t < 16 ends up holding word t of the task
+        uint32_t word = 0;  // scalar path: lane t < 16 ends up holding word t of the task
         if (VEC) {
+            // full task: every coordinate is real (no storage or value padding)
+            const bool full = j0 + kTaskWords * 32 <= p.seg_len && seg0 + j0 + kTaskWords * 32 <= p.dim;
             Quad<T> gv[4], cv[4];
 #pragma unroll
             for (int sub = 0; sub < 4; ++sub) {
                 const uint64_t j = j0 + sub * 128 + lane * 4;
                 const uint64_t gi = seg0 + j;
-                if (j < p.seg_len && gi + 3 < p.dim) {
+                if (full || (j < p.seg_len && gi + 3 < p.dim)) {
                     gv[sub] = load4(g + gi);
                     cv[sub] = load4(c + gi);
                 } else {
@@ -185,21 +226,32 @@ __global__ void __launch_bounds__(kStreamThreads) extract_kernel(const StreamPar
                     }
                 }
             }
+            // lane l's nibble = bits of coordinates 4l..4l+3; word q of the
+            // sub-chunk is the concatenation of lanes 8q..8q+7's nibbles: an
+            // OR-reduction over aligned groups of 8 lanes (3 shuffles).
 #pragma unroll
             for (int sub = 0; sub < 4; ++sub) {
-                const uint64_t j = j0 + sub * 128 + lane * 4;
-                uint32_t b[4];
+                T u[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const T u = add_rn(gv[sub].v[k], cv[sub].v[k]);
-                    bad |= !(finite(gv[sub].v[k]) && finite(cv[sub].v[k]) && finite(u));
-                    const bool bit = (j + k < p.seg_len) && (u >= T(0));  // -0.0 -> 1
-                    b[k] = __ballot_sync(kFull, bit);
+                    // + 0 turns -0.0 (only from -0.0 + -0.0) into +0.0, so the
+                    // sign bit alone decides (u >= 0), sign_vector.hpp:70
+                    u[k] = add_rn(add_rn(gv[sub].v[k], cv[sub].v[k]), T(0));
+                    fin = fma_rn(u[k], T(0), fin);  // NaN iff some u is inf/NaN
                 }
-                const int qb = (lane & 3) * 8;
-                const uint32_t w = spread4(b[0] >> qb) | (spread4(b[1] >> qb) << 1) |
-                                   (spread4(b[2] >> qb) << 2) | (spread4(b[3] >> qb) << 3);
-                if ((lane >> 2) == sub) word = w;
+                uint32_t nib = sign_nibble(u[0], u[1], u[2], u[3]);
+                if (!full) {
+                    const uint64_t j = j0 + sub * 128 + lane * 4;
+                    const uint64_t valid = j >= p.seg_len ? 0 : p.seg_len - j;  // storage padding -> 0
+                    if (valid < 4) nib &= (1u << valid) - 1u;
+                }
+                uint32_t v = nib << ((lane & 7) * 4);
+                v |= __shfl_xor_sync(kFull, v, 1);
+                v |= __shfl_xor_sync(kFull, v, 2);
+                v |= __shfl_xor_sync(kFull, v, 4);
+                const uint32_t wi = q * kTaskWords + sub * 4 + (lane >> 3);
+                if ((lane & 7) == 0 && wi < p.words_proc)
+                    p.bits[(uint64_t(s) * p.ml + wl) * p.wst + wi] = v;
             }
         } else {
 #pragma unroll 4
@@ -221,10 +273,13 @@ __global__ void __launch_bounds__(kStreamThreads) extract_kernel(const StreamPar
                 if (lane == t) word = w;
             }
         }
-        const uint32_t wi = q * kTaskWords + lane;
-        if (lane < kTaskWords && wi < p.words_proc)
-            p.bits[(uint64_t(s) * p.ml + wl) * p.wst + wi] = word;
+        if (!VEC) {
+            const uint32_t wi = q * kTaskWords + lane;
+            if (lane < kTaskWords && wi < p.words_proc)
+                p.bits[(uint64_t(s) * p.ml + wl) * p.wst + wi] = word;
+        }
     }
+    bad |= !(fin == fin);
     if (__any_sync(kFull, bad) && lane == 0) atomicOr(p.err, 1);
 }
 
@@ -234,18 +289,18 @@ __global__ void __launch_bounds__(kStreamThreads) extract_kernel(const StreamPar
 // decomposition as K1, so each sub-chunk's bits are 4 aligned words.
 // ---------------------------------------------------------------------------
 template <typename T, bool VEC>
-__global__ void __launch_bounds__(kStreamThreads) decode_kernel(const StreamParams<T> p) {
+__global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode_kernel(const StreamParams<T> p) {
     const int lane = threadIdx.x & 31;
     const uint32_t warps = gridDim.x * (kStreamThreads / 32);
     const uint32_t tasks_per_seg = (p.words_proc + kTaskWords - 1) / kTaskWords;
-    const uint64_t n_tasks = uint64_t(tasks_per_seg) * p.n_seg * p.ml;
+    const uint64_t n_tasks = uint64_t(tasks_per_seg) * p.n_proc * p.ml;
     const T eta = p.eta;
     for (uint64_t task = blockIdx.x * (kStreamThreads / 32) + (threadIdx.x >> 5); task < n_tasks;
          task += warps) {
         const uint32_t q = uint32_t(task % tasks_per_seg);
         const uint64_t rest = task / tasks_per_seg;
-        const uint32_t s = uint32_t(rest % p.n_seg);
-        const uint32_t wl = uint32_t(rest / p.n_seg);
+        const uint32_t s = p.seg0 + uint32_t(rest % p.n_proc);
+        const uint32_t wl = uint32_t(rest / p.n_proc);
         const T* __restrict__ g = p.g[wl];
         const T* c = p.c[wl];  // may alias c_out (in-place update): no __restrict__
         T* co = p.c_out[wl];
@@ -335,102 +390,202 @@ __device__ __forceinline__ uint64_t pack_flag(uint32_t epoch, uint32_t st, uint6
     return (uint64_t(epoch) << 40) | (uint64_t(st) << 38) | v;
 }
 
-// Warp-wide decoupled look-back; returns the exclusive prefix of `agg`.
-__device__ __forceinline__ uint64_t lookback(uint64_t* f, uint32_t tile, uint32_t epoch,
+// Warp-wide decoupled look-back.  Lane l inspects the F predecessors
+// pos - l*F - f (order o = l*F + f), so one round trip to L2 covers 32*F
+// tiles.  The warp sums the published prefix of that window up to the first
+// inclusive prefix (done) or the first unpublished flag (it then polls that
+// single flag with backoff and resumes there: resolved flags are never
+// re-read).  Returns the exclusive prefix and publishes the inclusive one.
+template <int F>
+__device__ __forceinline__ uint64_t lookback(uint64_t* fl, uint32_t tile, uint32_t epoch,
                                              uint64_t agg, int lane) {
     if (tile == 0) {
-        if (lane == 0) st_relaxed(f, pack_flag(epoch, kPrefix, agg));
+        if (lane == 0) st_relaxed(fl, pack_flag(epoch, kPrefix, agg));
         return 0;
     }
-    if (lane == 0) st_relaxed(f + tile, pack_flag(epoch, kAgg, agg));
+    if (lane == 0) st_relaxed(fl + tile, pack_flag(epoch, kAgg, agg));
     uint64_t excl = 0;
     int64_t pos = int64_t(tile) - 1;
     while (true) {
-        const int64_t idx = pos - lane;
-        uint64_t v = 0;
-        bool valid = true, is_p = true;
-        if (idx >= 0) {
-            v = ld_relaxed(f + idx);
-            const uint32_t st = uint32_t(v >> 38) & 3u;
-            valid = uint32_t(v >> 40) == epoch && st != 0;
-            is_p = valid && st == kPrefix;
+        uint64_t v[F];
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+            const int64_t idx = pos - int64_t(lane) * F - f;
+            v[f] = idx >= 0 ? ld_relaxed(fl + idx) : pack_flag(epoch, kPrefix, 0);
         }
-        const unsigned pm = __ballot_sync(kFull, is_p);
-        const unsigned vm = __ballot_sync(kFull, valid);
-        const int fp = pm ? __ffs(pm) - 1 : 31;
-        const unsigned need = fp == 31 ? kFull : ((2u << fp) - 1u);
-        if ((vm & need) != need) {
-            __nanosleep(32);
-            continue;
+        uint32_t my_p = 0xffffffffu, my_inv = 0xffffffffu;
+#pragma unroll
+        for (int f = F - 1; f >= 0; --f) {
+            const uint32_t st = uint32_t(v[f] >> 38) & 3u;
+            const bool valid = uint32_t(v[f] >> 40) == epoch && st != 0;
+            if (!valid) my_inv = uint32_t(lane * F + f);
+            else if (st == kPrefix) my_p = uint32_t(lane * F + f);
         }
-        uint64_t mine = (lane <= fp && idx >= 0) ? (v & kValMask) : 0;
+        const uint32_t gp = __reduce_min_sync(kFull, my_p);
+        const uint32_t gi = __reduce_min_sync(kFull, my_inv);
+        // orders [0, bound) are summed: through the first inclusive prefix, else
+        // up to the first unpublished flag, else the whole window
+        const uint32_t bound = gp < gi ? gp + 1 : (gi < 32u * F ? gi : 32u * F);
+        uint64_t mine = 0;
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+            if (uint32_t(lane * F + f) < bound) mine += v[f] & kValMask;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(kFull, mine, o);
         excl += mine;
-        if (pm) break;
-        pos -= 32;
+        if (gp < gi) break;
+        pos -= bound;
+        if (bound == 0 && lane == 0) {  // wait for the nearest predecessor to publish
+            uint32_t ns = 32;
+            while (true) {
+                const uint64_t w = ld_relaxed(fl + pos);
+                if (uint32_t(w >> 40) == epoch && ((w >> 38) & 3u) != 0) break;
+                __nanosleep(ns);
+                ns = ns < 1024 ? ns * 2 : ns;
+            }
+        }
+        __syncwarp();
     }
-    if (lane == 0) st_relaxed(f + tile, pack_flag(epoch, kPrefix, excl + agg));
+    if (lane == 0) st_relaxed(fl + tile, pack_flag(epoch, kPrefix, excl + agg));
     return excl;
 }
 
+template <int WPT>
+__device__ __forceinline__ uint64_t load_bits(const uint32_t* p) {
+    if (WPT == 2) {
+        const uint2 v = __ldcg(reinterpret_cast<const uint2*>(p));
+        return uint64_t(v.x) | (uint64_t(v.y) << 32);
+    }
+    return __ldcg(p);
+}
+template <int WPT>
+__device__ __forceinline__ void store_bits(uint32_t* p, uint64_t v, bool streaming) {
+    if (WPT == 2) {
+        const uint2 u = make_uint2(uint32_t(v), uint32_t(v >> 32));
+        if (streaming)
+            __stcg(reinterpret_cast<uint2*>(p), u);
+        else
+            *reinterpret_cast<uint2*>(p) = u;
+    } else {
+        if (streaming)
+            __stcg(p, uint32_t(v));
+        else
+            *p = uint32_t(v);
+    }
+}
+
+// Coins of one packed word: for each set bit of `d` (ascending), draw
+// mix(z), z += gamma; keep the received bit where the draw is below th.
+__device__ __forceinline__ uint32_t coin_word(uint32_t d, uint64_t& z, uint64_t th) {
+    uint32_t keep = 0;
+    while (d) {
+        const uint32_t lsb = d & (0u - d);
+        d ^= lsb;
+        const uint64_t x = mix64f(z);
+        z += kGamma;
+        if (x < th) keep |= lsb;
+    }
+    return keep;
+}
+
+// Deposit consecutive coin bits (bit 0 first) onto the set bits of d, in
+// ascending order; returns the keep mask (coin -> received bit).
+__device__ __forceinline__ uint32_t deposit_word(uint32_t d, uint64_t& cb) {
+    uint32_t keep = 0;
+    while (d) {
+        const uint32_t lsb = d & (0u - d);
+        d ^= lsb;
+        if (uint32_t(cb) & 1u) keep |= lsb;
+        cb >>= 1;
+    }
+    return keep;
+}
+
+// Merge kernel.  A CTA takes a tile of 256 x WPT packed words of one owned
+// segment and runs every merge of the current plan stage over it; thread t
+// always owns words t*WPT.. of the tile, so DAG intermediates never leave
+// the thread (shared-memory slots only because their index is dynamic).
+// Per merge: d = r ^ l; a block scan of popcount(d) plus one decoupled
+// look-back (warp 0) give each thread the stream index of its first coin;
+// the coins are the precomputed bits [n, n + popc) deposited onto the set
+// bits of d (inline SplitMix64 draws beyond the precomputed budget);
+// out = r ^ (d & ~coin).  Leaf operands of the next merge are prefetched
+// before the look-back.  Tiles are handed out by an atomic counter in
+// segment order, so a look-back only ever waits on running CTAs.
+#ifdef MARSIT_MERGE_PROF
+}  // namespace
+__device__ unsigned long long g_merge_prof[8];
+namespace {
+__device__ __forceinline__ uint64_t gtime() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define PROF_T(var) const uint64_t var = (tid == 0) ? gtime() : 0
+#define PROF_ADD(i, v) if (tid == 0) atomicAdd(&g_merge_prof[i], (unsigned long long)(v))
+#else
+#define PROF_T(var)
+#define PROF_ADD(i, v)
+#endif
+
+template <int WPT>
 __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams p) {
-    extern __shared__ uint4 slots[];  // [max_slots][kMergeThreads]
+    extern __shared__ uint64_t slots[];  // [max_slots][kMergeThreads]
     __shared__ uint32_t s_tile;
     __shared__ uint32_t s_warp[kMergeThreads / 32];
     __shared__ uint64_t s_base;
+    constexpr uint32_t kTW = kMergeThreads * WPT;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t total_tiles = p.n_seg * p.tiles_per_seg;
+    const uint32_t total_tiles = p.n_proc * p.tiles_per_seg;
     while (true) {
         if (tid == 0) s_tile = atomicAdd(p.tile_counter, 1u) - p.tile_base;
         __syncthreads();
         const uint32_t gt = s_tile;
         __syncthreads();
         if (gt >= total_tiles) break;
-        const uint32_t sl = gt % p.n_seg, tile = gt / p.n_seg;
-        const uint32_t w0 = tile * kTileWords + tid * kMergeWordsPerThread;
+        const uint32_t sl = p.seg0 + gt % p.n_proc, tile = gt / p.n_proc;
+        const uint32_t w0 = tile * kTW + tid * WPT;
         const bool active = w0 < p.words_proc;
-        // valid-bit masks of the four words (bits beyond L stay 0)
-        uint32_t vmask[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int64_t rem = int64_t(p.seg_bits) - int64_t(w0 + k) * 32;
-            vmask[k] = rem >= 32 ? kFull : (rem <= 0 ? 0u : ((1u << rem) - 1u));
-        }
+        const int64_t rem = int64_t(p.seg_bits) - int64_t(w0) * 32;
+        const uint64_t vmask =
+            rem >= WPT * 32 ? (WPT == 2 ? ~0ull : 0xffffffffull)
+                            : (rem <= 0 ? 0ull : ((1ull << rem) - 1ull));
         const uint32_t mb = p.seg_begin[sl];
         const uint32_t kb = p.stage_begin[sl * (p.n_stages + 1) + p.stage];
         const uint32_t ke = p.stage_begin[sl * (p.n_stages + 1) + p.stage + 1];
         const uint32_t sg = p.s_first + sl;
-        for (uint32_t k = kb; k < ke; ++k) {
-            const DevMerge m = p.merges[mb + k];
-            auto load_src = [&](uint16_t src) -> uint4 {
-                if (!active) return make_uint4(0, 0, 0, 0);
-                const uint32_t idx = src & 0x3FFFu;
-                switch (src & 0xC000u) {
-                    case kSrcLeaf: {
-                        const uint64_t off =
-                            (uint64_t((idx / p.ml) * p.n_seg + sl) * p.ml + idx % p.ml) * p.wst;
-                        return __ldcg(reinterpret_cast<const uint4*>(p.leaves + off + w0));
-                    }
-                    case kSrcSlot:
-                        return slots[idx * kMergeThreads + tid];
-                    default:
-                        return __ldcg(reinterpret_cast<const uint4*>(
-                            p.gnodes + (uint64_t(sl) * p.gmax + idx) * p.wst + w0));
-                }
-            };
-            const uint4 r4 = load_src(m.recv_src);
-            const uint4 l4 = load_src(m.local_src);
-            const uint32_t r[4] = {r4.x, r4.y, r4.z, r4.w};
-            const uint32_t l[4] = {l4.x, l4.y, l4.z, l4.w};
-            uint32_t d[4];
-            uint32_t cnt = 0;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                d[j] = (r[j] ^ l[j]) & vmask[j];
-                cnt += __popc(d[j]);
+        auto load_src = [&](uint16_t src) -> uint64_t {
+            if (!active) return 0ull;
+            const uint32_t idx = src & 0x3FFFu;
+            switch (src & 0xC000u) {
+                case kSrcLeaf:
+                    return load_bits<WPT>(
+                        p.leaves +
+                        (uint64_t((idx / p.ml) * p.n_seg + sl) * p.ml + idx % p.ml) * p.wst + w0);
+                case kSrcSlot:
+                    return slots[idx * kMergeThreads + tid];
+                default:
+                    return load_bits<WPT>(p.gnodes + (uint64_t(sl) * p.gmax + idx) * p.wst + w0);
             }
-            // block exclusive scan of cnt
+        };
+        uint64_t pf_r = 0, pf_l = 0;
+        if (kb < ke) {
+            const DevMerge m0 = p.merges[mb + kb];
+            if ((m0.recv_src & 0xC000u) == kSrcLeaf) pf_r = load_src(m0.recv_src);
+            if ((m0.local_src & 0xC000u) == kSrcLeaf) pf_l = load_src(m0.local_src);
+        }
+        for (uint32_t k = kb; k < ke; ++k) {
+            PROF_T(t0);
+            const DevMerge m = p.merges[mb + k];
+            const uint64_t r = (m.recv_src & 0xC000u) == kSrcLeaf ? pf_r : load_src(m.recv_src);
+            const uint64_t l = (m.local_src & 0xC000u) == kSrcLeaf ? pf_l : load_src(m.local_src);
+            if (k + 1 < ke) {
+                const DevMerge mn = p.merges[mb + k + 1];
+                if ((mn.recv_src & 0xC000u) == kSrcLeaf) pf_r = load_src(mn.recv_src);
+                if ((mn.local_src & 0xC000u) == kSrcLeaf) pf_l = load_src(mn.local_src);
+            }
+            const uint64_t d = (r ^ l) & vmask;
+            const uint32_t cnt = __popcll(d);
             uint32_t incl = cnt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -439,6 +594,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
             }
             if (lane == 31) s_warp[wid] = incl;
             __syncthreads();
+            PROF_T(t1);
             if (wid == 0) {
                 const uint32_t ws = lane < kMergeThreads / 32 ? s_warp[lane] : 0u;
                 uint32_t wincl = ws;
@@ -448,20 +604,16 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
                     if (lane >= o) wincl += y;
                 }
                 const uint32_t tile_total = __shfl_sync(kFull, wincl, 31);
-                // draws this stream produced before this merge (continuations)
-                uint64_t base = 0;
-                if (lane == 0) {
-                    base = m.base_add;
-                    int32_t src = m.offset_src;
-                    while (src >= 0) {
+                uint64_t base = m.base_add;  // draws of this stream before this merge
+                if (m.offset_src >= 0 && lane == 0) {
+                    for (int32_t src = m.offset_src; src >= 0;) {
                         const DevMerge& pm = p.merges[mb + src];
                         base += p.totals[mb + src] + pm.base_add;
                         src = pm.offset_src;
                     }
                 }
-                const uint64_t excl = lookback(p.flags + uint64_t(mb + k) * p.tiles_per_seg, tile,
-                                               p.epoch, tile_total, lane);
-                __syncwarp();
+                const uint64_t excl = lookback<4>(p.flags + uint64_t(mb + k) * p.tiles_per_seg,
+                                                  tile, p.epoch, tile_total, lane);
                 if (lane < kMergeThreads / 32) s_warp[lane] = wincl - ws;
                 if (lane == 0) {
                     s_base = base + excl;
@@ -469,36 +621,98 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
                 }
             }
             __syncthreads();
-            uint64_t n = s_base + s_warp[wid] + (incl - cnt);  // draw index of my first coin
-            const uint64_t key =
-                m.key_mode ? m.key : stream_key(p.seed, 5, m.receiver, p.round, sg);
-            uint64_t z = key + (n + 1) * kGamma;
-            const uint64_t th = m.thresh11;
-            uint32_t out[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                uint32_t dd = d[j], keep = 0;
-                while (dd) {
-                    const int b = __ffs(dd) - 1;
-                    dd &= dd - 1;
-                    const uint64_t x = mix64(z);
-                    z += kGamma;
-                    keep |= uint32_t(x < th) << b;
-                }
-                out[j] = (r[j] ^ (d[j] & ~keep)) & vmask[j];
+            PROF_T(t2);
+            const uint64_t n0 = s_base + s_warp[wid] + (incl - cnt);  // my first coin's draw
+            uint64_t keep;
+            if (n0 + cnt <= uint64_t(m.coin_words) * 32) {
+                // precomputed coin bits [n0, n0 + cnt): at most 64 of them
+                const uint32_t* cw = p.coins + m.coin_off + (n0 >> 5);
+                const uint32_t sh = uint32_t(n0 & 31);
+                const uint64_t last = (n0 + cnt + 31) >> 5;  // one past the last word needed
+                const uint32_t c0 = cnt ? __ldg(cw) : 0u;
+                const uint32_t c1 = ((n0 >> 5) + 1 < last) ? __ldg(cw + 1) : 0u;
+                const uint32_t c2 = ((n0 >> 5) + 2 < last) ? __ldg(cw + 2) : 0u;
+                uint64_t cb = uint64_t(__funnelshift_r(c0, c1, sh)) |
+                              (uint64_t(__funnelshift_r(c1, c2, sh)) << 32);
+                keep = deposit_word(uint32_t(d), cb);
+                if (WPT == 2) keep |= uint64_t(deposit_word(uint32_t(d >> 32), cb)) << 32;
+            } else {
+                // beyond the precomputed budget (unusually many disagreements): draw inline
+                const uint64_t key =
+                    m.key_mode ? m.key : stream_key(p.seed, 5, m.receiver, p.round, sg);
+                uint64_t z = key + (n0 + 1) * kGamma;
+                keep = coin_word(uint32_t(d), z, m.thresh11);
+                if (WPT == 2) keep |= uint64_t(coin_word(uint32_t(d >> 32), z, m.thresh11)) << 32;
             }
+            const uint64_t out = (r ^ (d & ~keep)) & vmask;
+            PROF_T(t3);
             if (active) {
-                const uint4 o4 = make_uint4(out[0], out[1], out[2], out[3]);
-                if (m.out_slot != kNone) slots[m.out_slot * kMergeThreads + tid] = o4;
+                if (m.out_slot != kNone) slots[m.out_slot * kMergeThreads + tid] = out;
                 if (m.out_global == kFinal)
-                    *reinterpret_cast<uint4*>(p.agg + uint64_t(sg) * p.wst + w0) = o4;
+                    store_bits<WPT>(p.agg + uint64_t(sg) * p.wst + w0, out, false);
                 else if (m.out_global != kNone)
-                    __stcg(reinterpret_cast<uint4*>(
-                               p.gnodes + (uint64_t(sl) * p.gmax + m.out_global) * p.wst + w0),
-                           o4);
+                    store_bits<WPT>(p.gnodes + (uint64_t(sl) * p.gmax + m.out_global) * p.wst + w0,
+                                    out, true);
             }
-            __syncthreads();
+            __syncthreads();  // s_warp / s_base are rewritten by the next merge
+            PROF_T(t4);
+            PROF_ADD(0, t1 - t0);
+            PROF_ADD(1, t2 - t1);
+            PROF_ADD(2, t3 - t2);
+            PROF_ADD(3, t4 - t3);
+            PROF_ADD(4, 1);
         }
+    }
+}
+
+
+
+// ---------------------------------------------------------------------------
+// Coin precompute: blockIdx.y = merge, warps stride over the merge's words;
+// lane l draws n = 32*w + l and the warp ballot is coin word w.
+// ---------------------------------------------------------------------------
+// Coin of draw z: (mix64(z) < th) evaluated on the high word only (exact
+// unless the high words tie, probability 2^-32, which takes the full path).
+// The first xor-shift stays on the ALU pipe, the second goes through the
+// FMA pipe, and only the high word of the last product is formed.
+__device__ __forceinline__ bool coin_hi(uint64_t z, uint64_t th) {
+    uint64_t y = z ^ (z >> 30);
+    y *= 0xbf58476d1ce4e5b9ull;
+    uint32_t lo = uint32_t(y), hi = uint32_t(y >> 32);
+    xorshr_fma(lo, hi, 1u << 5);  // >> 27
+    const uint32_t h2 = mulhi32(lo, 0x133111ebu) + lo * 0x94d049bbu + hi * 0x133111ebu;
+    const uint32_t xh = h2 ^ (h2 >> 31);
+    const uint32_t thh = uint32_t(th >> 32);
+    bool c = xh < thh;
+    if (xh == thh) c = mix64(z) < th;
+    return c;
+}
+
+__global__ void __launch_bounds__(256) coins_kernel(const DevMerge* __restrict__ merges,
+                                                    uint64_t seed, uint64_t round,
+                                                    uint32_t* __restrict__ coins) {
+    const DevMerge m = merges[blockIdx.y];
+    const uint32_t chunks = (m.coin_words + 63) / 64;  // 64 words = 2048 draws per chunk
+    if (chunks == 0) return;
+    const int lane = threadIdx.x & 31;
+    const uint64_t key = m.key_mode ? m.key : stream_key(seed, 5, m.receiver, round, m.segment);
+    const uint64_t th = m.thresh11;
+    uint32_t* out = coins + m.coin_off;
+    for (uint32_t c = blockIdx.x * 8 + (threadIdx.x >> 5); c < chunks; c += gridDim.x * 8) {
+        // lane l builds words l and l + 32 of the chunk bit by bit (two
+        // independent draw streams for ILP), then both are stored coalesced
+        uint64_t za = key + (uint64_t(c) * 2048 + uint64_t(lane) * 32 + 1) * kGamma;
+        uint64_t zb = za + 1024 * kGamma;
+        uint32_t wa = 0, wb = 0;
+#pragma unroll 8
+        for (int i = 0; i < 32; ++i) {
+            if (coin_hi(za, th)) wa |= 1u << i;
+            if (coin_hi(zb, th)) wb |= 1u << i;
+            za += kGamma;
+            zb += kGamma;
+        }
+        __stcg(out + uint64_t(c) * 64 + lane, wa);
+        __stcg(out + uint64_t(c) * 64 + 32 + lane, wb);
     }
 }
 
@@ -652,8 +866,11 @@ cudaError_t launch_decode(const StreamParams<T>& p, bool vec, int grid, cudaStre
     return cudaGetLastError();
 }
 
-cudaError_t launch_merge(const MergeParams& p, int grid, size_t smem, cudaStream_t st) {
-    merge_kernel<<<grid, kMergeThreads, smem, st>>>(p);
+cudaError_t launch_merge(const MergeParams& p, int wpt, int grid, size_t smem, cudaStream_t st) {
+    if (wpt == 2)
+        merge_kernel<2><<<grid, kMergeThreads, smem, st>>>(p);
+    else
+        merge_kernel<1><<<grid, kMergeThreads, smem, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -661,8 +878,11 @@ cudaError_t merge_kernel_set_smem(size_t smem) {
     // The attribute is per function and process-wide: only ever raise it.
     static size_t current = 48 * 1024;
     if (smem <= current) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem));
+    cudaError_t e = cudaFuncSetAttribute(merge_kernel<1>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(merge_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem));
     if (e == cudaSuccess) current = smem;
     return e;
 }
@@ -690,8 +910,15 @@ cudaError_t stream_occupancy(bool f64, int* extract_blocks, int* decode_blocks) 
 }
 
 cudaError_t merge_kernel_occupancy(size_t smem, int* blocks_per_sm) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, merge_kernel,
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, merge_kernel<2>,
                                                          kMergeThreads, smem);
+}
+
+cudaError_t launch_coins(const DevMerge* merges, uint32_t n_merges, uint64_t seed, uint64_t round,
+                         uint32_t* coins, int grid_x, cudaStream_t st) {
+    if (n_merges == 0) return cudaSuccess;
+    coins_kernel<<<dim3(grid_x, n_merges), 256, 0, st>>>(merges, seed, round, coins);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_export_bits(const uint32_t* agg, uint32_t wst, uint64_t dim, uint64_t seg_len,
@@ -750,3 +977,13 @@ MARSIT_INSTANTIATE(float)
 MARSIT_INSTANTIATE(double)
 
 }  // namespace marsit_b200
+
+#ifdef MARSIT_MERGE_PROF
+extern "C" void marsit_debug_merge_prof(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, marsit_b200::g_merge_prof, sizeof(marsit_b200::g_merge_prof));
+    if (reset) {
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(marsit_b200::g_merge_prof, z, sizeof(z));
+    }
+}
+#endif

@@ -9,9 +9,8 @@ namespace marsit_b200 {
 
 constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ull;  // rng.hpp:64
 constexpr uint32_t kMaxLocalWorkers = 64;           // workers resident on one rank
-constexpr int kMergeThreads = 256;
-constexpr int kMergeWordsPerThread = 4;              // one uint4 of packed signs
-constexpr int kTileWords = kMergeThreads * kMergeWordsPerThread;  // 1024 u32 = 32768 bits
+constexpr int kMergeThreads = 256;                   // 8 warps; a warp tile is 32 x WPT packed
+                                                     // words, WPT in {1, 2} chosen per context
 constexpr int kStreamThreads = 256;                  // sign_extract / decode
 constexpr int kTaskWords = 16;                       // u32 words per warp task (512 elements)
 
@@ -33,8 +32,11 @@ struct DevMerge {
     int16_t offset_src;  // previous merge of the same stream (draw continuation) or -1
     uint8_t key_mode;    // 0: derive key from (seed, round); 1: explicit `key`
     uint8_t pad_;
+    uint32_t segment;    // global segment id (stream key)
+    uint32_t coin_words; // precomputed coin bits of this merge: draws [0, 32*coin_words)
+    uint64_t coin_off;   // u32-word offset of those bits in the coin buffer
 };
-static_assert(sizeof(DevMerge) == 40, "DevMerge layout");
+static_assert(sizeof(DevMerge) == 56, "DevMerge layout");
 
 struct MergeParams {
     const DevMerge* merges;      // all owned segments' merges, segment-major
@@ -42,12 +44,15 @@ struct MergeParams {
     const uint32_t* stage_begin; // [n_seg][n_stages+1] merge-index ranges per stage
     uint32_t n_stages, stage;
     uint32_t n_seg, s_first;     // owned segments and the global id of the first
+    uint32_t seg0, n_proc;       // this launch: owned segments [seg0, seg0 + n_proc)
     uint32_t tiles_per_seg, words_proc, wst, ml;
+    uint32_t max_slots;          // shared-memory node slots per warp
     uint64_t seg_bits;           // L
     const uint32_t* leaves;      // leaf(w, sl) = leaves + ((w/ml*n_seg + sl)*ml + w%ml)*wst
     uint32_t* gnodes;            // [n_seg][gmax][wst]
     uint32_t gmax;
     uint32_t* agg;               // [S][wst]; owned segment sl at s_first + sl
+    const uint32_t* coins;       // precomputed coin bitstreams (see launch_coins)
     uint64_t* flags;             // [merges][tiles_per_seg] decoupled look-back
     uint64_t* totals;            // [merges] draws consumed by each merge (last tile)
     uint32_t* tile_counter;
@@ -61,6 +66,7 @@ struct StreamParams {
     const T* c[kMaxLocalWorkers];
     T* c_out[kMaxLocalWorkers];
     uint32_t ml, n_seg;          // local workers, segments (all S)
+    uint32_t seg0, n_proc;       // this launch: segments [seg0, seg0 + n_proc)
     uint64_t dim, seg_len;       // D, L
     uint32_t words_proc, wst;
     uint32_t* bits;              // extract output: [S][ml][wst]
@@ -75,10 +81,15 @@ template <typename T>
 cudaError_t launch_extract(const StreamParams<T>& p, bool vec, int grid, cudaStream_t st);
 template <typename T>
 cudaError_t launch_decode(const StreamParams<T>& p, bool vec, int grid, cudaStream_t st);
-cudaError_t launch_merge(const MergeParams& p, int grid, size_t smem, cudaStream_t st);
+cudaError_t launch_merge(const MergeParams& p, int wpt, int grid, size_t smem, cudaStream_t st);
 cudaError_t merge_kernel_occupancy(size_t smem, int* blocks_per_sm);
 cudaError_t merge_kernel_set_smem(size_t smem);
 cudaError_t stream_occupancy(bool f64, int* extract_blocks, int* decode_blocks);
+// Precompute the coin bits of every merge: bit n of merge m's stream is
+// (mix(key_m + (n+1)γ) < thresh11_m) for n < 32 * coin_words.  Data
+// independent, so it runs concurrently with the HBM-bound extract.
+cudaError_t launch_coins(const DevMerge* merges, uint32_t n_merges, uint64_t seed, uint64_t round,
+                         uint32_t* coins, int grid_x, cudaStream_t st);
 cudaError_t launch_export_bits(const uint32_t* agg, uint32_t wst, uint64_t dim, uint64_t seg_len,
                                uint32_t* out_u32, cudaStream_t st);
 template <typename T>

@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -109,6 +110,7 @@ marsit_status lower_plan(const Plan& plan, uint32_t s_first, uint32_t n_seg, Dev
             DevMerge d{};
             d.thresh11 = coin_threshold(m.c_recv, m.c_local) << 11;
             d.receiver = m.receiver;
+            d.segment = s_first + sl;
             d.key_mode = 0;
             d.offset_src = m.offset_src < 0 ? int16_t(-1) : int16_t(pos[m.offset_src]);
             auto encode = [&](uint32_t node) -> uint16_t {
@@ -190,8 +192,11 @@ struct marsit_ctx {
     int* err = nullptr;
     uint32_t tile_base = 0, epoch = 0;
     int merge_grid = 0;
+    int merge_wpt = 2;      // packed u32 words per merge thread (tile = 256 * wpt words)
     size_t merge_smem = 0;
-    int stream_grid = 0;
+    int stream_grid = 0;   // generic grid-stride kernels
+    int extract_grid = 0;  // persistent, one wave of resident CTAs
+    int decode_grid = 0;
     // dense round scratch
     void* dense_send = nullptr;  // [G][s_own][ml][L] of dtype
     void* dense_recv = nullptr;
@@ -199,6 +204,17 @@ struct marsit_ctx {
     DenseOp* d_dense_ops = nullptr;
     uint16_t* d_dense_final = nullptr;
     uint32_t dense_n_ops = 0;
+    // coin precompute (aux stream, overlapped with the extract)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_coins = nullptr;
+    uint32_t* coins = nullptr;
+    uint64_t coin_total_words = 0;
+    int coin_grid_x = 1;
+    bool coins_pending = false;
+    // single GPU: merge of segment s (aux) pipelined with decode (caller stream)
+    bool pipeline = false;
+    cudaEvent_t ev_extract = nullptr;
+    std::vector<cudaEvent_t> ev_merge;
     // NCCL
     ncclComm_t comm = nullptr;
     // timing
@@ -226,6 +242,12 @@ marsit_ctx::~marsit_ctx() {
         cudaEventDestroy(tp.b);
     }
     for (auto e : event_pool) cudaEventDestroy(e);
+    if (ev_extract) cudaEventDestroy(ev_extract);
+    for (auto e : ev_merge) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_coins) cudaEventDestroy(ev_coins);
+    if (coins) cudaFree(coins);
+    if (aux) cudaStreamDestroy(aux);
     if (comm) ncclCommDestroy(comm);
 }
 
@@ -308,17 +330,22 @@ marsit_status check_ptrs(const marsit_ctx* ctx, const void* const* a, const char
 }
 
 marsit_status run_extract(marsit_ctx* ctx, const void* const* g, const void* const* c,
-                          cudaStream_t st) {
+                          uint32_t seg0, uint32_t n, cudaStream_t st) {
     cudaEvent_t ev;
     marsit_status s = ctx->begin_phase(0, st, &ev);
     if (s) return s;
     const bool vec = vec_ok_ptrs(ctx, g, c);
-    if (ctx->dtype == MARSIT_F32)
-        CUDA_TRY(launch_extract(stream_params<float>(ctx, g, c, nullptr, nullptr, 0.0), vec,
-                                ctx->stream_grid, st));
-    else
-        CUDA_TRY(launch_extract(stream_params<double>(ctx, g, c, nullptr, nullptr, 0.0), vec,
-                                ctx->stream_grid, st));
+    if (ctx->dtype == MARSIT_F32) {
+        auto p = stream_params<float>(ctx, g, c, nullptr, nullptr, 0.0);
+        p.seg0 = seg0;
+        p.n_proc = n;
+        CUDA_TRY(launch_extract(p, vec, ctx->extract_grid, st));
+    } else {
+        auto p = stream_params<double>(ctx, g, c, nullptr, nullptr, 0.0);
+        p.seg0 = seg0;
+        p.n_proc = n;
+        CUDA_TRY(launch_extract(p, vec, ctx->extract_grid, st));
+    }
     return ctx->end_phase(0, st, ev, 1);
 }
 
@@ -337,7 +364,14 @@ marsit_status run_exchange(marsit_ctx* ctx, cudaStream_t st) {
     return ctx->end_phase(1, st, ev, 0);
 }
 
-marsit_status run_merge(marsit_ctx* ctx, uint64_t seed, uint64_t round, cudaStream_t st) {
+// Merge owned segments [seg0, seg0 + n) (indices relative to the rank's
+// first owned segment): one launch per plan stage.
+marsit_status run_merge(marsit_ctx* ctx, uint64_t seed, uint64_t round, uint32_t seg0, uint32_t n,
+                        cudaStream_t st) {
+    if (ctx->coins_pending) {
+        CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_coins, 0));
+        ctx->coins_pending = false;
+    }
     cudaEvent_t ev;
     marsit_status s = ctx->begin_phase(2, st, &ev);
     if (s) return s;
@@ -348,6 +382,8 @@ marsit_status run_merge(marsit_ctx* ctx, uint64_t seed, uint64_t round, cudaStre
     p.n_stages = ctx->dp.n_stages;
     p.n_seg = ctx->s_own;
     p.s_first = ctx->s_first;
+    p.seg0 = seg0;
+    p.n_proc = n;
     p.tiles_per_seg = ctx->tiles_per_seg;
     p.words_proc = ctx->words_proc;
     p.wst = ctx->wst;
@@ -359,10 +395,12 @@ marsit_status run_merge(marsit_ctx* ctx, uint64_t seed, uint64_t round, cudaStre
     p.agg = ctx->agg;
     p.flags = ctx->flags;
     p.totals = ctx->totals;
+    p.coins = ctx->coins;
     p.tile_counter = ctx->counter;
     p.seed = seed;
     p.round = round;
-    const uint32_t total_tiles = ctx->s_own * ctx->tiles_per_seg;
+    p.max_slots = std::max<uint32_t>(ctx->dp.max_slots, 1);
+    const uint32_t total_tiles = n * ctx->tiles_per_seg;
     const int grid = int(std::min<uint64_t>(total_tiles, uint64_t(ctx->merge_grid)));
     for (uint32_t stage = 0; stage < ctx->dp.n_stages; ++stage) {
         s = ctx->next_epoch();
@@ -370,7 +408,7 @@ marsit_status run_merge(marsit_ctx* ctx, uint64_t seed, uint64_t round, cudaStre
         p.stage = stage;
         p.epoch = ctx->epoch;
         p.tile_base = ctx->tile_base;
-        CUDA_TRY(launch_merge(p, grid, ctx->merge_smem, st));
+        CUDA_TRY(launch_merge(p, ctx->merge_wpt, grid, ctx->merge_smem, st));
         ctx->tile_base += total_tiles + uint32_t(grid);
     }
     return ctx->end_phase(2, st, ev, ctx->dp.n_stages);
@@ -387,19 +425,42 @@ marsit_status run_allgather(marsit_ctx* ctx, cudaStream_t st) {
 }
 
 marsit_status run_decode(marsit_ctx* ctx, const void* const* g, const void* const* c,
-                         void* const* c_out, void* update, double eta, cudaStream_t st) {
+                         void* const* c_out, void* update, double eta, uint32_t seg0, uint32_t n,
+                         cudaStream_t st) {
     cudaEvent_t ev;
     marsit_status s = ctx->begin_phase(4, st, &ev);
     if (s) return s;
     const bool vec = vec_ok_ptrs(ctx, g, c) && vec_ok_ptrs(ctx, (const void* const*)c_out, c) &&
                      (!update || aligned16(update));
-    if (ctx->dtype == MARSIT_F32)
-        CUDA_TRY(launch_decode(stream_params<float>(ctx, g, c, c_out, update, eta), vec,
-                               ctx->stream_grid, st));
-    else
-        CUDA_TRY(launch_decode(stream_params<double>(ctx, g, c, c_out, update, eta), vec,
-                               ctx->stream_grid, st));
+    if (ctx->dtype == MARSIT_F32) {
+        auto p = stream_params<float>(ctx, g, c, c_out, update, eta);
+        p.seg0 = seg0;
+        p.n_proc = n;
+        CUDA_TRY(launch_decode(p, vec, ctx->decode_grid, st));
+    } else {
+        auto p = stream_params<double>(ctx, g, c, c_out, update, eta);
+        p.seg0 = seg0;
+        p.n_proc = n;
+        CUDA_TRY(launch_decode(p, vec, ctx->decode_grid, st));
+    }
     return ctx->end_phase(4, st, ev, 1);
+}
+
+// Coin precompute on the aux stream, forked from `st` so it overlaps the
+// (HBM-bound) sign extraction; run_merge joins it.
+marsit_status run_coins(marsit_ctx* ctx, uint64_t seed, uint64_t round, cudaStream_t st) {
+    if (ctx->coin_total_words == 0) return MARSIT_OK;
+    CUDA_TRY(cudaEventRecord(ctx->ev_fork, st));
+    CUDA_TRY(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+    cudaEvent_t ev;
+    marsit_status s = ctx->begin_phase(7, ctx->aux, &ev);
+    if (s) return s;
+    CUDA_TRY(launch_coins(ctx->d_merges, ctx->dp.n_merges, seed, round, ctx->coins,
+                          ctx->coin_grid_x, ctx->aux));
+    if ((s = ctx->end_phase(7, ctx->aux, ev, 1))) return s;
+    CUDA_TRY(cudaEventRecord(ctx->ev_coins, ctx->aux));
+    ctx->coins_pending = true;
+    return MARSIT_OK;
 }
 
 marsit_status run_export(marsit_ctx* ctx, uint64_t* out, cudaStream_t st) {
@@ -627,11 +688,26 @@ marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out) {
     ctx->words64 = uint32_t(ceil_div(ctx->L, 64));
     ctx->words_proc = uint32_t(round_up(2ull * ctx->words64, 4));
     ctx->wst = uint32_t(round_up(ctx->words_proc, 32));
-    ctx->tiles_per_seg = uint32_t(ceil_div(ctx->words_proc, kTileWords));
     ctx->vec_ok = (ctx->L % 4) == 0;
 
     marsit_status st = lower_plan(ctx->plan, ctx->s_first, ctx->s_own, ctx->dp);
     if (st) return st;
+
+    // merge tiling: one CTA tile = 256 threads x WPT packed words; WPT = 2
+    // unless that leaves fewer tiles than resident CTA slots (small segments,
+    // e.g. one segment per GPU at 8 GPUs), then WPT = 1
+    ctx->merge_smem = size_t(std::max<uint32_t>(ctx->dp.max_slots, 1)) * kMergeThreads * 8;
+    CUDA_TRY(merge_kernel_set_smem(ctx->merge_smem));
+    {
+        int occ = 0;
+        CUDA_TRY(merge_kernel_occupancy(ctx->merge_smem, &occ));
+        if (const char* e = std::getenv("MARSIT_MERGE_CTAS")) occ = std::min(occ, std::atoi(e));
+        ctx->merge_grid = std::max(1, occ) * ctx->sm_count;
+        const uint64_t tiles2 = ceil_div(ctx->words_proc, 2 * kMergeThreads) * ctx->s_own;
+        ctx->merge_wpt = tiles2 >= uint64_t(ctx->merge_grid) ? 2 : 1;
+        ctx->tiles_per_seg =
+            uint32_t(ceil_div(ctx->words_proc, uint64_t(ctx->merge_wpt) * kMergeThreads));
+    }
 
     const size_t wst = ctx->wst;
     CUDA_TRY(cudaMalloc(&ctx->bits, sizeof(uint32_t) * ctx->S * ctx->ml * wst));
@@ -644,6 +720,52 @@ marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out) {
     }
     const uint32_t gmax = std::max<uint32_t>(ctx->dp.gmax, 1);
     CUDA_TRY(cudaMalloc(&ctx->gnodes, sizeof(uint32_t) * ctx->s_own * gmax * wst));
+    {
+        // Coin precompute budget per merge: frac * L draws per use of its
+        // (receiver, segment) stream (a continuation merge starts after the
+        // earlier merges' draws).  Draws beyond it are computed inline, so
+        // the budget only trades memory/ALU for the rare over-budget case.
+        double frac = 0.53;
+        if (const char* e = std::getenv("MARSIT_COIN_FRAC")) frac = std::atof(e);
+        uint64_t off = 0;
+        for (uint32_t sl = 0; sl < ctx->s_own; ++sl) {
+            const uint32_t mb = ctx->dp.seg_begin[sl];
+            const uint32_t me = sl + 1 < ctx->s_own ? ctx->dp.seg_begin[sl + 1] : ctx->dp.n_merges;
+            for (uint32_t k = mb; k < me; ++k) {
+                DevMerge& d = ctx->dp.merges[k];
+                uint32_t depth = 0;
+                for (int32_t src = d.offset_src; src >= 0; src = ctx->dp.merges[mb + src].offset_src)
+                    ++depth;
+                const double want = frac * double(ctx->L) * (depth + 1);
+                uint64_t words = frac > 0 ? ceil_div(uint64_t(want) + 1, 32) : 0;
+                words = std::min<uint64_t>(words, ceil_div(ctx->L * (depth + 1), 32));
+                d.coin_words = uint32_t(words);
+                d.coin_off = off;
+                off += round_up(words, 64);  // whole 64-word chunks (coins_kernel)
+            }
+        }
+        ctx->coin_total_words = off;
+        if (off) CUDA_TRY(cudaMalloc(&ctx->coins, sizeof(uint32_t) * off));
+        uint64_t max_words = 0;
+        for (auto& d : ctx->dp.merges) max_words = std::max<uint64_t>(max_words, d.coin_words);
+        // MARSIT_COIN_CTAS (default 4) CTAs per SM in total, split across the
+        // merges (one warp per 64-word chunk)
+        const char* ce = std::getenv("MARSIT_COIN_CTAS");
+        const uint64_t coin_ctas = ce ? std::max(1, std::atoi(ce)) : 4;
+        ctx->coin_grid_x = int(std::max<uint64_t>(
+            1, std::min<uint64_t>(ceil_div(max_words, 64 * 8),
+                                  ceil_div(coin_ctas * ctx->sm_count,
+                                           std::max<uint32_t>(ctx->dp.n_merges, 1)))));
+        CUDA_TRY(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_coins, cudaEventDisableTiming));
+    }
+    if (G == 1 && ctx->S >= 2 && std::getenv("MARSIT_PIPELINE") != nullptr) {
+        ctx->pipeline = true;
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_extract, cudaEventDisableTiming));
+        ctx->ev_merge.resize(ctx->S);
+        for (auto& e : ctx->ev_merge) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     CUDA_TRY(cudaMalloc(&ctx->d_merges, sizeof(DevMerge) * std::max<size_t>(ctx->dp.n_merges, 1)));
     CUDA_TRY(cudaMemcpy(ctx->d_merges, ctx->dp.merges.data(), sizeof(DevMerge) * ctx->dp.n_merges,
                         cudaMemcpyHostToDevice));
@@ -663,16 +785,21 @@ marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out) {
     CUDA_TRY(cudaMalloc(&ctx->err, sizeof(int)));
     CUDA_TRY(cudaMemset(ctx->err, 0, sizeof(int)));
 
-    ctx->merge_smem = size_t(std::max<uint32_t>(ctx->dp.max_slots, 1)) * kMergeThreads * 16;
-    CUDA_TRY(merge_kernel_set_smem(ctx->merge_smem));
-    int occ = 0;
-    CUDA_TRY(merge_kernel_occupancy(ctx->merge_smem, &occ));
-    ctx->merge_grid = std::max(1, occ) * ctx->sm_count;
     {
-        // persistent grid-stride launch: exactly the resident CTAs, one wave
+        // persistent grid-stride launches.  The HBM-bound kernels deliberately
+        // leave SM room (threads/registers) for the concurrently running coin
+        // and merge kernels; MARSIT_{EXTRACT,DECODE}_CTAS override per SM.
         int ob_extract = 0, ob_decode = 0;
         CUDA_TRY(stream_occupancy(ctx->dtype == MARSIT_F64, &ob_extract, &ob_decode));
-        ctx->stream_grid = std::max(1, std::min(ob_extract, ob_decode)) * ctx->sm_count;
+        auto env_int = [](const char* name, int dflt) {
+            const char* e = std::getenv(name);
+            return e ? std::atoi(e) : dflt;
+        };
+        const int want_e = env_int("MARSIT_EXTRACT_CTAS", 2);
+        const int want_d = env_int("MARSIT_DECODE_CTAS", 2);
+        ctx->extract_grid = std::max(1, std::min(ob_extract, want_e)) * ctx->sm_count;
+        ctx->decode_grid = std::max(1, std::min(ob_decode, want_d)) * ctx->sm_count;
+        ctx->stream_grid = 4 * ctx->sm_count;
     }
 
     // dense-round plan: per owned segment, the reduction tree (local + received)
@@ -743,11 +870,31 @@ marsit_status marsit_sign_round(marsit_ctx* ctx, uint64_t t, double eta_s, uint6
     if ((s = check_consensus(ctx, true))) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     CUDA_TRY(cudaSetDevice(ctx->device));
-    if ((s = run_extract(ctx, d_grads, d_comp, st))) return s;
-    if ((s = run_exchange(ctx, st))) return s;
-    if ((s = run_merge(ctx, seed, t, st))) return s;
-    if ((s = run_allgather(ctx, st))) return s;
-    if ((s = run_decode(ctx, d_grads, d_comp, d_comp_out, d_update, eta_s, st))) return s;
+    if ((s = run_coins(ctx, seed, t, st))) return s;
+    if ((s = run_extract(ctx, d_grads, d_comp, 0, ctx->S, st))) return s;
+    if (ctx->pipeline) {
+        // aux: M_0 M_1 ... (after the extract and the coins); st: D_s after M_s, so
+        // the ALU/latency-bound merges hide under the HBM-bound decode
+        CUDA_TRY(cudaEventRecord(ctx->ev_extract, st));
+        CUDA_TRY(cudaStreamWaitEvent(ctx->aux, ctx->ev_extract, 0));
+        if (ctx->coins_pending) ctx->coins_pending = false;  // aux is already ordered after them
+        for (uint32_t sg = 0; sg < ctx->S; ++sg) {
+            if ((s = run_merge(ctx, seed, t, sg, 1, ctx->aux))) return s;
+            CUDA_TRY(cudaEventRecord(ctx->ev_merge[sg], ctx->aux));
+        }
+        for (uint32_t sg = 0; sg < ctx->S; ++sg) {
+            CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_merge[sg], 0));
+            if ((s = run_decode(ctx, d_grads, d_comp, d_comp_out, d_update, eta_s, sg, 1, st)))
+                return s;
+        }
+        // st has now joined aux (it waited on the last merge event)
+    } else {
+        if ((s = run_exchange(ctx, st))) return s;
+        if ((s = run_merge(ctx, seed, t, 0, ctx->s_own, st))) return s;
+        if ((s = run_allgather(ctx, st))) return s;
+        if ((s = run_decode(ctx, d_grads, d_comp, d_comp_out, d_update, eta_s, 0, ctx->S, st)))
+            return s;
+    }
     return run_export(ctx, d_agg_bits, st);
 }
 
@@ -792,7 +939,7 @@ marsit_status marsit_sign_extract(marsit_ctx* ctx, const void* const* d_grads,
     if ((s = check_ptrs(ctx, d_grads, "grads")) || (s = check_ptrs(ctx, d_comp, "comp"))) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     CUDA_TRY(cudaSetDevice(ctx->device));
-    if ((s = run_extract(ctx, d_grads, d_comp, st))) return s;
+    if ((s = run_extract(ctx, d_grads, d_comp, 0, ctx->S, st))) return s;
     const size_t row = size_t(ctx->words64) * 8;
     for (uint32_t w = 0; w < ctx->ml; ++w)
         CUDA_TRY(cudaMemcpy2DAsync(d_signs_out + size_t(w) * ctx->S * ctx->words64, row,
@@ -814,8 +961,9 @@ marsit_status marsit_allreduce_sign(marsit_ctx* ctx, uint64_t round, uint64_t se
         CUDA_TRY(cudaMemcpy2DAsync(ctx->bits + size_t(w) * ctx->wst, size_t(ctx->ml) * ctx->wst * 4,
                                    d_signs + size_t(w) * ctx->S * ctx->words64, row, row, ctx->S,
                                    cudaMemcpyDeviceToDevice, st));
+    if ((s = run_coins(ctx, seed, round, st))) return s;
     if ((s = run_exchange(ctx, st))) return s;
-    if ((s = run_merge(ctx, seed, round, st))) return s;
+    if ((s = run_merge(ctx, seed, round, 0, ctx->s_own, st))) return s;
     if ((s = run_allgather(ctx, st))) return s;
     CUDA_TRY(cudaMemcpy2DAsync(d_out, row, ctx->agg, size_t(ctx->wst) * 4, row, ctx->S,
                                cudaMemcpyDeviceToDevice, st));
@@ -840,7 +988,7 @@ marsit_status marsit_merge_signs(const uint64_t* d_recv, uint32_t c_recv, const 
     const uint64_t words64 = ceil_div(len, 64);
     const uint32_t words_proc = uint32_t(round_up(2 * words64, 4));
     const uint32_t wst = uint32_t(round_up(words_proc, 32));
-    const uint32_t tiles = uint32_t(ceil_div(words_proc, kTileWords));
+    const uint32_t tiles = uint32_t(ceil_div(words_proc, 2 * kMergeThreads));
     // scratch: leaves [2][wst], agg [wst], flags [tiles], totals, counter, plan
     struct Scratch {
         void* p = nullptr;
@@ -884,6 +1032,8 @@ marsit_status marsit_merge_signs(const uint64_t* d_recv, uint32_t c_recv, const 
     p.stage = 0;
     p.n_seg = 1;
     p.s_first = 0;
+    p.seg0 = 0;
+    p.n_proc = 1;
     p.tiles_per_seg = tiles;
     p.words_proc = words_proc;
     p.wst = wst;
@@ -898,9 +1048,10 @@ marsit_status marsit_merge_signs(const uint64_t* d_recv, uint32_t c_recv, const 
     p.tile_counter = counter;
     p.tile_base = 0;
     p.epoch = 1;
-    const size_t smem = kMergeThreads * 16;
-    CUDA_TRY(merge_kernel_set_smem(smem));
-    CUDA_TRY(launch_merge(p, int(std::min<uint32_t>(tiles, 148 * 4)), smem, st));
+    p.max_slots = 1;
+    const size_t smem = kMergeThreads * 8;
+    const int grid = int(std::min<uint64_t>(tiles, 148 * 4));
+    CUDA_TRY(launch_merge(p, 2, grid, smem, st));
     CUDA_TRY(cudaMemcpyAsync(d_out, agg, words64 * 8, cudaMemcpyDeviceToDevice, st));
     uint64_t tot = 0;
     CUDA_TRY(cudaMemcpyAsync(&tot, totals, sizeof(tot), cudaMemcpyDeviceToHost, st));

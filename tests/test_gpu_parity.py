@@ -274,3 +274,26 @@ def test_value_semantics_and_inplace_agree():
     for x, y in zip(a.compensation, c1):
         assert torch.equal(x.c, y)
     assert torch.equal(a.aggregate_bits, b.aggregate_bits)
+
+
+@pytest.mark.parametrize("frac", ["0", "0.2", "0.5", "2"])
+@pytest.mark.parametrize("topo,a,b", [("ring", 8, 0), ("torus", 2, 4)])
+def test_coin_precompute_budget_and_inline_fallback(frac, topo, a, b, monkeypatch):
+    """Precomputed coin bits, the inline-draw fallback beyond the budget, and
+    mixtures of both must give identical results (the budget is a tuning knob)."""
+    monkeypatch.setenv("MARSIT_COIN_FRAC", frac)
+    sched = sched_of(topo, a, b)
+    W, D = sched.workers, 300_001
+    ctx = mb.Context(D, sched, torch.float32, 0)
+    T = O.schedule(topo, a, b)
+    comp_d = [torch.zeros(D, device=DEV) for _ in range(W)]
+    comp_h = np.zeros((W, D))
+    agg = torch.empty((D + 63) // 64, dtype=torch.int64, device=DEV)
+    for t in (1, 2):
+        gh = np.stack([O.gen_dyadic(5, w, t, D) for w in range(W)])
+        ctx.sign_round(t, ETA, 5, to_dev(gh, torch.float32), comp_d, agg_bits=agg)
+        ctx.check()
+        want = O.marsit_round(T, t, None, ETA, gh, comp_h, 5)
+        assert np.array_equal(u64(agg), want.agg_bits)
+        assert np.array_equal(np.stack([c.double().cpu().numpy() for c in comp_d]), want.comp)
+        comp_h = want.comp
