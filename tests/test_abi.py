@@ -114,3 +114,29 @@ def test_no_cpu_fallback_without_device():
         pytest.skip("a device is present")
     with pytest.raises(mb.CudaError):
         mb.Context(1000, mb.build_ring_schedule(4))
+
+
+REF_INC = "/root/reference/proj/include"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_INC), reason="reference headers absent")
+def test_dropin_shim_compiles_against_reference_headers():
+    """include/marsit_b200/drop_in.hpp builds inside the reference's own type
+    system (marsit::MarsitRoundResult etc.) and links the C-ABI library."""
+    import subprocess
+    r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tools"), "dropin"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert os.path.exists(os.path.join(ROOT, "build", "dropin_parity"))
+
+
+def test_dropin_binary_fails_loudly_without_gpu():
+    import subprocess
+    exe = os.path.join(ROOT, "build", "dropin_parity")
+    if not os.path.exists(exe):
+        pytest.skip("dropin_parity not built here")
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+    assert r.returncode != 0 and "no CUDA device" in r.stdout

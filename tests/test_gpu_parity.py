@@ -297,3 +297,18 @@ def test_coin_precompute_budget_and_inline_fallback(frac, topo, a, b, monkeypatc
         assert np.array_equal(u64(agg), want.agg_bits)
         assert np.array_equal(np.stack([c.double().cpu().numpy() for c in comp_d]), want.comp)
         comp_h = want.comp
+
+
+def test_cpp_dropin_bit_identical_to_reference_in_process():
+    """build/dropin_parity (built where the reference headers exist) runs the
+    reference's marsit_round/allreduce_sign and marsit::gpu:: versions on the
+    same inputs in one process and requires bit-identical results."""
+    import os
+    import subprocess
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "build", "dropin_parity")
+    if not os.path.exists(exe):
+        pytest.skip("dropin_parity binary not shipped")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "DROP-IN PARITY OK" in r.stdout

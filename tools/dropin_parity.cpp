@@ -1,0 +1,137 @@
+// dropin_parity.cpp — runs the REFERENCE's marsit::marsit_round /
+// marsit::allreduce_sign and the drop-in marsit::gpu:: versions (B200 path via
+// the C-ABI) on identical inputs in one process and requires bit-identical
+// results (compensation, global update, aggregate bits, bit accounting).
+//
+// Built here by `make -C tools dropin` against the read-only reference headers
+// (test infrastructure: the binary carries the reference code, it does not
+// read /root/reference at run time).  Exit status 0 = all cases identical.
+#include <marsit/allreduce.hpp>
+#include <marsit/rng.hpp>
+#include <marsit/sync.hpp>
+
+#include <marsit_b200/drop_in.hpp>
+
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+using namespace marsit;
+
+static int failures = 0;
+
+static void expect(bool ok, const char* what, const char* tag) {
+    if (!ok) {
+        std::printf("MISMATCH %s: %s\n", tag, what);
+        ++failures;
+    }
+}
+
+static bool same(const DenseVector& a, const DenseVector& b) {
+    return a.size() == b.size() &&
+           std::memcmp(a.values().data(), b.values().data(), a.size() * sizeof(double)) == 0;
+}
+
+static std::vector<DenseVector> inputs(uint32_t W, size_t D, uint64_t seed, uint64_t t, int kind) {
+    std::vector<DenseVector> out;
+    for (uint32_t w = 0; w < W; ++w) {
+        RngStream rng(seed, RngPurpose::trial, w, t, 0);
+        std::vector<double> v(D);
+        for (size_t j = 0; j < D; ++j) {
+            if (kind == 0)
+                v[j] = double(int64_t(rng.next_u64() >> 51) - 4096) * 0x1.0p-20;  // dyadic
+            else
+                v[j] = rng.next_gaussian() * 1e-3;                               // arbitrary doubles
+            if (kind == 2 && j % 7 == 0) v[j] = (j % 14 == 0) ? 0.0 : -0.0;     // zeros
+        }
+        out.emplace_back(std::move(v));
+    }
+    return out;
+}
+
+static void run_case(const char* tag, const Schedule& sched, size_t D, std::optional<uint64_t> K,
+                     int kind, int rounds) {
+    SyncConfig cfg{K, 0x1.0p-10};
+    std::vector<CompensationState> comp_ref(sched.workers, CompensationState{DenseVector::zeros(D)});
+    std::vector<CompensationState> comp_gpu = comp_ref;
+    for (int r = 0; r < rounds; ++r) {
+        const uint64_t t = K ? uint64_t(r) : uint64_t(r + 1);
+        auto g = inputs(sched.workers, D, 77, t, kind);
+        MarsitRoundResult a = marsit::marsit_round(t, cfg, g, comp_ref, sched, 2026);
+        MarsitRoundResult b = marsit::gpu::marsit_round(t, cfg, g, comp_gpu, sched, 2026);
+        expect(a.full_precision == b.full_precision, "full_precision", tag);
+        expect(same(a.global_update, b.global_update), "global_update", tag);
+        for (uint32_t w = 0; w < sched.workers; ++w)
+            expect(same(a.compensation[w].c, b.compensation[w].c), "compensation", tag);
+        expect(a.aggregate_bits.has_value() == b.aggregate_bits.has_value(), "aggregate presence", tag);
+        if (a.aggregate_bits && b.aggregate_bits)
+            expect(*a.aggregate_bits == *b.aggregate_bits, "aggregate_bits", tag);
+        expect(a.bits.per_worker == b.bits.per_worker && a.bits.total == b.bits.total &&
+                   a.bits.reduce_bits == b.bits.reduce_bits && a.bits.gather_bits == b.bits.gather_bits,
+               "BitsAccount", tag);
+        comp_ref = a.compensation;
+        comp_gpu = b.compensation;
+    }
+    std::printf("case %-28s D=%zu rounds=%d %s\n", tag, D, rounds, failures ? "" : "ok");
+}
+
+static void run_allreduce(const char* tag, const Schedule& sched, size_t L) {
+    std::vector<std::vector<PackedSignVector>> signs(sched.workers);
+    for (uint32_t w = 0; w < sched.workers; ++w) {
+        RngStream rng(9, RngPurpose::trial, w, 3, 1);
+        for (uint32_t s = 0; s < sched.segments; ++s) {
+            PackedSignVector v = PackedSignVector::zeros(L);
+            for (size_t j = 0; j < L; ++j)
+                if (rng.next_u64() & 1u) v.set_bit(j, true);
+            signs[w].push_back(std::move(v));
+        }
+    }
+    RoundContext rc{31, 4};
+    SignAllreduceResult a = marsit::allreduce_sign(signs, sched, rc);
+    SignAllreduceResult b = marsit::gpu::allreduce_sign(signs, sched, rc);
+    for (uint32_t w = 0; w < sched.workers; ++w)
+        for (uint32_t s = 0; s < sched.segments; ++s)
+            expect(a.per_worker[w][s] == b.per_worker[w][s], "AggregateSign", tag);
+    expect(a.bits.total == b.bits.total && a.bits.per_worker == b.bits.per_worker, "bits", tag);
+    std::printf("allreduce %-23s L=%zu %s\n", tag, L, failures ? "" : "ok");
+}
+
+int main() {
+    try {
+        run_case("ring5 dyadic", build_ring_schedule(5), 37, std::nullopt, 0, 4);
+        run_case("ring4 C1 dyadic", build_ring_schedule(4), 1000000, std::nullopt, 0, 2);
+        run_case("ring8 gaussian", build_ring_schedule(8), 100003, std::nullopt, 1, 3);
+        run_case("torus2x4 gaussian", build_torus_schedule(2, 4), 60201, std::nullopt, 1, 3);
+        run_case("torus3x3 zeros", build_torus_schedule(3, 3), 5000, std::nullopt, 2, 2);
+        run_case("ring4 dense K=3", build_ring_schedule(4), 777, uint64_t{3}, 1, 5);
+        run_case("torus2x3 dense K=2", build_torus_schedule(2, 3), 61, uint64_t{2}, 1, 4);
+        run_case("ring4 D<M", build_ring_schedule(4), 3, std::nullopt, 1, 2);
+        run_allreduce("ring6", build_ring_schedule(6), 97);
+        run_allreduce("torus2x3", build_torus_schedule(2, 3), 1000);
+        run_allreduce("torus4x2", build_torus_schedule(4, 2), 65537);
+        // error mapping: non-finite u (overflow) raises non_finite_error like the reference
+        bool threw = false;
+        try {
+            std::vector<DenseVector> big(2, DenseVector(std::vector<double>(4, 1.5e308)));
+            std::vector<CompensationState> c(2, CompensationState{DenseVector(std::vector<double>(4, 1.5e308))});
+            marsit::gpu::marsit_round(1, SyncConfig{std::nullopt, 0.1}, big, c, build_ring_schedule(2), 1);
+        } catch (const non_finite_error&) {
+            threw = true;
+        }
+        expect(threw, "non_finite_error on overflow", "errors");
+        threw = false;
+        try {
+            std::vector<DenseVector> g(2, DenseVector(std::vector<double>(4, 1.0)));
+            std::vector<CompensationState> c(2, CompensationState{DenseVector::zeros(4)});
+            marsit::gpu::marsit_round(1, SyncConfig{std::nullopt, 0.0}, g, c, build_ring_schedule(2), 1);
+        } catch (const parameter_error&) {
+            threw = true;
+        }
+        expect(threw, "parameter_error on eta_s <= 0", "errors");
+    } catch (const std::exception& e) {
+        std::printf("EXCEPTION %s\n", e.what());
+        return 2;
+    }
+    std::printf("%s\n", failures ? "DROP-IN PARITY FAILED" : "DROP-IN PARITY OK (bit-identical)");
+    return failures ? 1 : 0;
+}
