@@ -15,6 +15,8 @@
 // All of it is HBM / integer-ALU work: no tensor cores are involved.  The
 // streaming kernels use 128-bit coalesced loads, warp ballots for packing and
 // grids sized to the SM count; the merge kernel keeps every segment in L2.
+#include <cooperative_groups.h>
+
 #include <cstdint>
 
 #include "kernels.cuh"
@@ -667,6 +669,201 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
 
 
 
+// Cooperative merge.  One CTA per tile of 256 x WPT packed words, every tile
+// of every owned segment resident at once (cooperative launch).  Merge step
+// k: each tile publishes popcount(r ^ l) of its k-th merge, one grid-wide
+// barrier, then every tile sums the published counts of the tiles before it
+// (its exclusive draw offset), reads its precomputed coin bits and deposits
+// them.  No look-back chains, no per-stage launches: a continuation merge
+// (torus) reads the finished total of the merge whose stream it continues.
+__device__ __forceinline__ uint32_t deposit32(uint32_t d, uint32_t cb) {
+    uint32_t keep = 0;
+    while (d) {
+        const uint32_t lsb = d & (0u - d);
+        d ^= lsb;
+        if (cb & 1u) keep |= lsb;
+        cb >>= 1;
+    }
+    return keep;
+}
+
+template <int WPT>
+__device__ __forceinline__ void load_words(const uint32_t* p, uint32_t (&v)[WPT]) {
+    if constexpr (WPT >= 4) {
+#pragma unroll
+        for (int q = 0; q < WPT / 4; ++q) {
+            const uint4 x = __ldcg(reinterpret_cast<const uint4*>(p) + q);
+            v[4 * q] = x.x;
+            v[4 * q + 1] = x.y;
+            v[4 * q + 2] = x.z;
+            v[4 * q + 3] = x.w;
+        }
+    } else if constexpr (WPT == 2) {
+        const uint2 x = __ldcg(reinterpret_cast<const uint2*>(p));
+        v[0] = x.x;
+        v[1] = x.y;
+    } else {
+        v[0] = __ldcg(p);
+    }
+}
+
+template <int WPT>
+__global__ void __launch_bounds__(kMergeThreads) merge_coop_kernel(const CoopParams p) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ uint32_t cslots[];  // [max_slots][WPT][kMergeThreads]
+    __shared__ uint32_t s_warp[kMergeThreads / 32];
+    __shared__ uint64_t s_base;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t T = p.n_seg * p.tiles_per_seg;
+    const uint32_t tg = blockIdx.x;          // segment-major tile id
+    const uint32_t sl = tg / p.tiles_per_seg, tile = tg % p.tiles_per_seg;
+    const uint32_t w0 = tile * (kMergeThreads * WPT) + tid * WPT;
+    const bool active = w0 < p.words_proc;
+    // valid bits of my words: all 32 while rem >= 32 (bits beyond L stay 0)
+    const int64_t rem0 = int64_t(p.seg_bits) - int64_t(w0) * 32;
+    auto vmask = [&](int j) -> uint32_t {
+        const int64_t rem = rem0 - 32 * j;
+        return rem >= 32 ? kFull : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+    };
+    const uint32_t mb = p.seg_begin[sl], nm = p.seg_count[sl];
+    const uint32_t sg = p.s_first + sl;
+    auto load_src = [&](uint16_t src, uint32_t (&v)[WPT]) {
+        const uint32_t idx = src & 0x3FFFu;
+        if (!active) {
+#pragma unroll
+            for (int j = 0; j < WPT; ++j) v[j] = 0;
+        } else if ((src & 0xC000u) == kSrcLeaf) {
+            load_words<WPT>(p.leaves +
+                                (uint64_t((idx / p.ml) * p.n_seg + sl) * p.ml + idx % p.ml) * p.wst +
+                                w0,
+                            v);
+        } else {
+#pragma unroll
+            for (int j = 0; j < WPT; ++j) v[j] = cslots[(idx * WPT + j) * kMergeThreads + tid];
+        }
+    };
+    // the local operand of the next merge is prefetched when it is a leaf
+    // (the ring / torus case: the received operand is the running aggregate)
+    uint32_t pl[WPT];
+    if (nm > 0) {
+        const DevMerge m0 = p.merges[mb];
+        if ((m0.local_src & 0xC000u) == kSrcLeaf) load_src(m0.local_src, pl);
+    }
+    uint32_t r[WPT], d[WPT];
+    for (uint32_t k = 0; k < p.k_max; ++k) {
+        const bool live = k < nm;
+        DevMerge m{};
+        uint32_t cnt = 0;
+        if (live) {
+            m = p.merges[mb + k];
+            load_src(m.recv_src, r);
+            if ((m.local_src & 0xC000u) == kSrcLeaf) {
+#pragma unroll
+                for (int j = 0; j < WPT; ++j) d[j] = (r[j] ^ pl[j]) & vmask(j);
+            } else {
+                load_src(m.local_src, d);
+#pragma unroll
+                for (int j = 0; j < WPT; ++j) d[j] = (r[j] ^ d[j]) & vmask(j);
+            }
+            if (k + 1 < nm) {
+                const DevMerge mn = p.merges[mb + k + 1];
+                if ((mn.local_src & 0xC000u) == kSrcLeaf) load_src(mn.local_src, pl);
+            }
+#pragma unroll
+            for (int j = 0; j < WPT; ++j) cnt += __popc(d[j]);
+        }
+        // block scan: thread offset within the tile, tile total
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_warp[wid] = incl;
+        __syncthreads();
+        uint32_t warp_off = 0, tile_total = 0;
+#pragma unroll
+        for (int w = 0; w < kMergeThreads / 32; ++w) {
+            const uint32_t v = s_warp[w];
+            warp_off += w < wid ? v : 0u;
+            tile_total += v;
+        }
+        if (tid == 0) p.counts[uint64_t(k) * T + tg] = tile_total;
+        grid.sync();
+        if (live && wid == 0) {
+            // exclusive prefix over the earlier tiles of this segment
+            const uint32_t* cs = p.counts + uint64_t(k) * T + uint64_t(sl) * p.tiles_per_seg;
+            uint64_t acc = 0, all = 0;
+            for (uint32_t i = lane; i < p.tiles_per_seg; i += 32) {
+                const uint32_t v = __ldcg(cs + i);
+                acc += i < tile ? v : 0u;
+                all += v;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                acc += __shfl_xor_sync(kFull, acc, o);
+                all += __shfl_xor_sync(kFull, all, o);
+            }
+            uint64_t base = m.base_add;  // draws of this stream before this merge
+            for (int32_t src = m.offset_src; src >= 0;) {
+                const DevMerge& pm = p.merges[mb + src];
+                base += __ldcg(p.totals + mb + src) + pm.base_add;
+                src = pm.offset_src;
+            }
+            if (lane == 0) {
+                s_base = base + acc;
+                if (tile == 0) p.totals[mb + k] = all;
+            }
+        }
+        __syncthreads();
+        if (live) {
+            const uint64_t n0 = s_base + warp_off + (incl - cnt);  // my first coin's draw
+            if (n0 + cnt <= uint64_t(m.coin_words) * 32) {
+                const uint32_t* cw = p.coins + m.coin_off;
+                uint64_t n = n0;
+#pragma unroll
+                for (int j = 0; j < WPT; ++j) {
+                    const uint32_t pc = __popc(d[j]);
+                    uint32_t window = 0;
+                    if (pc) {
+                        const uint64_t wi = n >> 5;
+                        const uint32_t sh = uint32_t(n & 31);
+                        const uint32_t c0 = __ldg(cw + wi);
+                        const uint32_t c1 = (sh + pc > 32) ? __ldg(cw + wi + 1) : 0u;
+                        window = __funnelshift_r(c0, c1, sh);
+                    }
+                    r[j] = (r[j] ^ (d[j] & ~deposit32(d[j], window))) & vmask(j);
+                    n += pc;
+                }
+            } else {
+                // beyond the precomputed budget: draw inline (same stream, same indices)
+                const uint64_t key =
+                    m.key_mode ? m.key : stream_key(p.seed, 5, m.receiver, p.round, sg);
+                uint64_t z = key + (n0 + 1) * kGamma;
+#pragma unroll
+                for (int j = 0; j < WPT; ++j)
+                    r[j] = (r[j] ^ (d[j] & ~coin_word(d[j], z, m.thresh11))) & vmask(j);
+            }
+            if (active) {
+                if (m.out_slot != kNone) {
+#pragma unroll
+                    for (int j = 0; j < WPT; ++j)
+                        cslots[(m.out_slot * WPT + j) * kMergeThreads + tid] = r[j];
+                }
+                if (m.out_global == kFinal) {
+                    uint32_t* dst = p.agg + uint64_t(sg) * p.wst + w0;
+#pragma unroll
+                    for (int j = 0; j < WPT; ++j) dst[j] = r[j];
+                }
+            }
+        }
+        // s_warp / s_base are rewritten next step; slots written above are read
+        // by the same thread only
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Coin precompute: blockIdx.y = merge, warps stride over the merge's words;
 // lane l draws n = 32*w + l and the warp ballot is coin word w.
@@ -885,6 +1082,44 @@ cudaError_t merge_kernel_set_smem(size_t smem) {
                                  int(smem));
     if (e == cudaSuccess) current = smem;
     return e;
+}
+
+template <int WPT>
+static cudaError_t coop_launch_t(const CoopParams& p, size_t smem, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(merge_coop_kernel<WPT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    CoopParams q = p;
+    void* args[] = {&q};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(merge_coop_kernel<WPT>),
+                                       dim3(p.n_seg * p.tiles_per_seg), dim3(kMergeThreads), args,
+                                       smem, st);
+}
+
+cudaError_t launch_merge_coop(const CoopParams& p, int wpt, size_t smem, cudaStream_t st) {
+    switch (wpt) {
+        case 1: return coop_launch_t<1>(p, smem, st);
+        case 2: return coop_launch_t<2>(p, smem, st);
+        case 4: return coop_launch_t<4>(p, smem, st);
+        case 8: return coop_launch_t<8>(p, smem, st);
+        case 16: return coop_launch_t<16>(p, smem, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t merge_coop_occupancy(int wpt, size_t smem, int* blocks) {
+    switch (wpt) {
+        case 1: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<1>, kMergeThreads, smem);
+        case 2: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<2>, kMergeThreads, smem);
+        case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<4>, kMergeThreads, smem);
+        case 8: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<8>, kMergeThreads, smem);
+        case 16: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<16>, kMergeThreads, smem);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 cudaError_t stream_occupancy(bool f64, int* extract_blocks, int* decode_blocks) {

@@ -60,6 +60,23 @@ struct MergeParams {
     uint64_t seed, round;
 };
 
+// Cooperative merge (all tiles co-resident, one grid barrier per merge step).
+struct CoopParams {
+    const DevMerge* merges;      // owned segments' merges in schedule order
+    const uint32_t* seg_begin;   // [n_seg] first merge of each owned segment
+    const uint32_t* seg_count;   // [n_seg] merges of each owned segment
+    uint32_t n_seg, s_first, tiles_per_seg, words_proc, wst, ml, max_slots, k_max;
+    uint64_t seg_bits;           // L
+    const uint32_t* leaves;      // as MergeParams
+    uint32_t* agg;               // [S][wst]
+    const uint32_t* coins;
+    uint32_t* counts;            // [k_max][n_seg * tiles_per_seg] popcount of each tile
+    uint64_t* totals;            // [n_merges] draws consumed by each merge (whole segment)
+    uint64_t seed, round;
+};
+cudaError_t launch_merge_coop(const CoopParams& p, int wpt, size_t smem, cudaStream_t st);
+cudaError_t merge_coop_occupancy(int wpt, size_t smem, int* blocks_per_sm);
+
 template <typename T>
 struct StreamParams {
     const T* g[kMaxLocalWorkers];

@@ -193,6 +193,10 @@ struct marsit_ctx {
     uint32_t tile_base = 0, epoch = 0;
     int merge_grid = 0;
     int merge_wpt = 2;      // packed u32 words per merge thread (tile = 256 * wpt words)
+    bool coop = false;      // cooperative merge kernel (flat plan) vs look-back (staged plan)
+    uint32_t coop_kmax = 0;
+    uint32_t* d_seg_count = nullptr;
+    uint32_t* coop_counts = nullptr;  // [kmax][s_own * tiles_per_seg]
     size_t merge_smem = 0;
     int stream_grid = 0;   // generic grid-stride kernels
     int extract_grid = 0;  // persistent, one wave of resident CTAs
@@ -206,8 +210,17 @@ struct marsit_ctx {
     uint32_t dense_n_ops = 0;
     // coin precompute (aux stream, overlapped with the extract)
     cudaStream_t aux = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_coins = nullptr;
-    uint32_t* coins = nullptr;
+    cudaEvent_t ev_fork = nullptr;
+    // two coin buffers: the current round's, and the next round's computed
+    // speculatively for (seed, t + 1) while this round's decode streams HBM
+    uint32_t* coin_buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev_coin_done[2] = {nullptr, nullptr};
+    struct CoinTag {
+        bool valid = false;
+        uint64_t seed = 0, round = 0;
+    } coin_tag[2];
+    int cur_coin = 0;
+    bool coin_prefetch = true;
     uint64_t coin_total_words = 0;
     int coin_grid_x = 1;
     bool coins_pending = false;
@@ -235,6 +248,7 @@ marsit_ctx::~marsit_ctx() {
     for (void* p : {(void*)bits, (void*)recv, (void*)agg, (void*)gnodes, (void*)d_merges,
                     (void*)d_seg_begin, (void*)d_stage_begin, (void*)flags, (void*)totals,
                     (void*)counter, (void*)err, dense_send, dense_recv, dense_mean,
+                    (void*)d_seg_count, (void*)coop_counts,
                     (void*)d_dense_ops, (void*)d_dense_final})
         if (p) cudaFree(p);
     for (auto& tp : pending) {
@@ -245,8 +259,10 @@ marsit_ctx::~marsit_ctx() {
     if (ev_extract) cudaEventDestroy(ev_extract);
     for (auto e : ev_merge) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_coins) cudaEventDestroy(ev_coins);
-    if (coins) cudaFree(coins);
+    for (int b = 0; b < 2; ++b) {
+        if (ev_coin_done[b]) cudaEventDestroy(ev_coin_done[b]);
+        if (coin_buf[b]) cudaFree(coin_buf[b]);
+    }
     if (aux) cudaStreamDestroy(aux);
     if (comm) ncclCommDestroy(comm);
 }
@@ -369,12 +385,38 @@ marsit_status run_exchange(marsit_ctx* ctx, cudaStream_t st) {
 marsit_status run_merge(marsit_ctx* ctx, uint64_t seed, uint64_t round, uint32_t seg0, uint32_t n,
                         cudaStream_t st) {
     if (ctx->coins_pending) {
-        CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_coins, 0));
+        CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_coin_done[ctx->cur_coin], 0));
         ctx->coins_pending = false;
     }
     cudaEvent_t ev;
     marsit_status s = ctx->begin_phase(2, st, &ev);
     if (s) return s;
+    if (ctx->coop) {
+        CoopParams c{};
+        c.merges = ctx->d_merges;
+        c.seg_begin = ctx->d_seg_begin;
+        c.seg_count = ctx->d_seg_count;
+        c.n_seg = ctx->s_own;
+        c.s_first = ctx->s_first;
+        c.tiles_per_seg = ctx->tiles_per_seg;
+        c.words_proc = ctx->words_proc;
+        c.wst = ctx->wst;
+        c.ml = ctx->ml;
+        c.max_slots = std::max<uint32_t>(ctx->dp.max_slots, 1);
+        c.k_max = ctx->coop_kmax;
+        c.seg_bits = ctx->L;
+        c.leaves = ctx->G == 1 ? ctx->bits : ctx->recv;
+        c.agg = ctx->agg;
+        c.coins = ctx->coin_buf[ctx->cur_coin];
+        c.counts = ctx->coop_counts;
+        c.totals = ctx->totals;
+        c.seed = seed;
+        c.round = round;
+        (void)seg0;
+        (void)n;
+        CUDA_TRY(launch_merge_coop(c, ctx->merge_wpt, ctx->merge_smem, st));
+        return ctx->end_phase(2, st, ev, 1);
+    }
     MergeParams p{};
     p.merges = ctx->d_merges;
     p.seg_begin = ctx->d_seg_begin;
@@ -395,7 +437,7 @@ marsit_status run_merge(marsit_ctx* ctx, uint64_t seed, uint64_t round, uint32_t
     p.agg = ctx->agg;
     p.flags = ctx->flags;
     p.totals = ctx->totals;
-    p.coins = ctx->coins;
+    p.coins = ctx->coin_buf[ctx->cur_coin];
     p.tile_counter = ctx->counter;
     p.seed = seed;
     p.round = round;
@@ -448,19 +490,48 @@ marsit_status run_decode(marsit_ctx* ctx, const void* const* g, const void* cons
 
 // Coin precompute on the aux stream, forked from `st` so it overlaps the
 // (HBM-bound) sign extraction; run_merge joins it.
-marsit_status run_coins(marsit_ctx* ctx, uint64_t seed, uint64_t round, cudaStream_t st) {
-    if (ctx->coin_total_words == 0) return MARSIT_OK;
+// Launch the coin kernel for (seed, round) into buffer b on the aux stream,
+// forked from `st` at this point of its work.
+marsit_status launch_coin_buffer(marsit_ctx* ctx, int b, uint64_t seed, uint64_t round,
+                                 cudaStream_t st) {
     CUDA_TRY(cudaEventRecord(ctx->ev_fork, st));
     CUDA_TRY(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
     cudaEvent_t ev;
     marsit_status s = ctx->begin_phase(7, ctx->aux, &ev);
     if (s) return s;
-    CUDA_TRY(launch_coins(ctx->d_merges, ctx->dp.n_merges, seed, round, ctx->coins,
+    CUDA_TRY(launch_coins(ctx->d_merges, ctx->dp.n_merges, seed, round, ctx->coin_buf[b],
                           ctx->coin_grid_x, ctx->aux));
     if ((s = ctx->end_phase(7, ctx->aux, ev, 1))) return s;
-    CUDA_TRY(cudaEventRecord(ctx->ev_coins, ctx->aux));
+    CUDA_TRY(cudaEventRecord(ctx->ev_coin_done[b], ctx->aux));
+    ctx->coin_tag[b] = {true, seed, round};
+    return MARSIT_OK;
+}
+
+// Coins of this round: reuse the speculatively prefetched buffer when its tag
+// matches (seed, round); otherwise compute them now, overlapping the extract.
+// run_merge joins them.
+marsit_status run_coins(marsit_ctx* ctx, uint64_t seed, uint64_t round, cudaStream_t st) {
+    if (ctx->coin_total_words == 0) return MARSIT_OK;
+    for (int b = 0; b < 2; ++b)
+        if (ctx->coin_tag[b].valid && ctx->coin_tag[b].seed == seed &&
+            ctx->coin_tag[b].round == round) {
+            ctx->cur_coin = b;
+            ctx->coins_pending = true;
+            return MARSIT_OK;
+        }
+    const int b = 1 - ctx->cur_coin;
+    marsit_status s = launch_coin_buffer(ctx, b, seed, round, st);
+    if (s) return s;
+    ctx->cur_coin = b;
     ctx->coins_pending = true;
     return MARSIT_OK;
+}
+
+// After this round's merge is enqueued: precompute (seed, round + 1) into the
+// other buffer; it runs underneath the HBM-bound decode.
+marsit_status prefetch_coins(marsit_ctx* ctx, uint64_t seed, uint64_t round, cudaStream_t st) {
+    if (ctx->coin_total_words == 0 || !ctx->coin_prefetch) return MARSIT_OK;
+    return launch_coin_buffer(ctx, 1 - ctx->cur_coin, seed, round + 1, st);
 }
 
 marsit_status run_export(marsit_ctx* ctx, uint64_t* out, cudaStream_t st) {
@@ -690,23 +761,55 @@ marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out) {
     ctx->wst = uint32_t(round_up(ctx->words_proc, 32));
     ctx->vec_ok = (ctx->L % 4) == 0;
 
-    marsit_status st = lower_plan(ctx->plan, ctx->s_first, ctx->s_own, ctx->dp);
-    if (st) return st;
-
-    // merge tiling: one CTA tile = 256 threads x WPT packed words; WPT = 2
-    // unless that leaves fewer tiles than resident CTA slots (small segments,
-    // e.g. one segment per GPU at 8 GPUs), then WPT = 1
-    ctx->merge_smem = size_t(std::max<uint32_t>(ctx->dp.max_slots, 1)) * kMergeThreads * 8;
-    CUDA_TRY(merge_kernel_set_smem(ctx->merge_smem));
+    // Merge kernel choice.  Preferred: the cooperative kernel (all tiles of
+    // all owned segments co-resident, one grid barrier per merge step) with
+    // the smallest words-per-thread that fits the GPU; it runs the flat
+    // (single-stage) plan.  Otherwise (huge segments, or MARSIT_MERGE=lookback)
+    // the decoupled look-back kernel with the staged plan.
+    marsit_status st;
     {
-        int occ = 0;
-        CUDA_TRY(merge_kernel_occupancy(ctx->merge_smem, &occ));
-        if (const char* e = std::getenv("MARSIT_MERGE_CTAS")) occ = std::min(occ, std::atoi(e));
-        ctx->merge_grid = std::max(1, occ) * ctx->sm_count;
-        const uint64_t tiles2 = ceil_div(ctx->words_proc, 2 * kMergeThreads) * ctx->s_own;
-        ctx->merge_wpt = tiles2 >= uint64_t(ctx->merge_grid) ? 2 : 1;
-        ctx->tiles_per_seg =
-            uint32_t(ceil_div(ctx->words_proc, uint64_t(ctx->merge_wpt) * kMergeThreads));
+        const char* mode = std::getenv("MARSIT_MERGE");
+        const bool want_coop = !(mode && std::string(mode) == "lookback");
+        if (want_coop) {
+            Plan flat = ctx->plan;
+            flat.n_stages = 1;
+            for (auto& sp : flat.seg)
+                for (auto& m : sp.merges) m.stage = 0;
+            DevicePlan dpf;
+            if ((st = lower_plan(flat, ctx->s_first, ctx->s_own, dpf))) return st;
+            for (int wpt : {1, 2, 4, 8, 16}) {
+                const uint64_t tps = ceil_div(ctx->words_proc, uint64_t(wpt) * kMergeThreads);
+                const uint64_t tiles = tps * ctx->s_own;
+                const size_t smem = size_t(std::max<uint32_t>(dpf.max_slots, 1)) * wpt *
+                                    kMergeThreads * sizeof(uint32_t);
+                if (smem > 160 * 1024) break;
+                int occ = 0;
+                CUDA_TRY(merge_coop_occupancy(wpt, smem, &occ));
+                if (tiles <= uint64_t(occ) * ctx->sm_count) {
+                    ctx->coop = true;
+                    ctx->merge_wpt = wpt;
+                    ctx->merge_smem = smem;
+                    ctx->tiles_per_seg = uint32_t(tps);
+                    ctx->dp = std::move(dpf);
+                    break;
+                }
+            }
+        }
+        if (!ctx->coop) {
+            if ((st = lower_plan(ctx->plan, ctx->s_first, ctx->s_own, ctx->dp))) return st;
+            // look-back kernel: one CTA tile = 256 threads x WPT packed words; WPT = 2
+            // unless that leaves fewer tiles than resident CTA slots, then WPT = 1
+            ctx->merge_smem = size_t(std::max<uint32_t>(ctx->dp.max_slots, 1)) * kMergeThreads * 8;
+            CUDA_TRY(merge_kernel_set_smem(ctx->merge_smem));
+            int occ = 0;
+            CUDA_TRY(merge_kernel_occupancy(ctx->merge_smem, &occ));
+            if (const char* e = std::getenv("MARSIT_MERGE_CTAS")) occ = std::min(occ, std::atoi(e));
+            ctx->merge_grid = std::max(1, occ) * ctx->sm_count;
+            const uint64_t tiles2 = ceil_div(ctx->words_proc, 2 * kMergeThreads) * ctx->s_own;
+            ctx->merge_wpt = tiles2 >= uint64_t(ctx->merge_grid) ? 2 : 1;
+            ctx->tiles_per_seg =
+                uint32_t(ceil_div(ctx->words_proc, uint64_t(ctx->merge_wpt) * kMergeThreads));
+        }
     }
 
     const size_t wst = ctx->wst;
@@ -745,7 +848,12 @@ marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out) {
             }
         }
         ctx->coin_total_words = off;
-        if (off) CUDA_TRY(cudaMalloc(&ctx->coins, sizeof(uint32_t) * off));
+        if (off)
+            for (int b = 0; b < 2; ++b) {
+                CUDA_TRY(cudaMalloc(&ctx->coin_buf[b], sizeof(uint32_t) * off));
+                CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_coin_done[b], cudaEventDisableTiming));
+            }
+        if (const char* e = std::getenv("MARSIT_COIN_PREFETCH")) ctx->coin_prefetch = std::atoi(e) != 0;
         uint64_t max_words = 0;
         for (auto& d : ctx->dp.merges) max_words = std::max<uint64_t>(max_words, d.coin_words);
         // MARSIT_COIN_CTAS (default 4) CTAs per SM in total, split across the
@@ -758,9 +866,9 @@ marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out) {
                                            std::max<uint32_t>(ctx->dp.n_merges, 1)))));
         CUDA_TRY(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
         CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
-        CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_coins, cudaEventDisableTiming));
+
     }
-    if (G == 1 && ctx->S >= 2 && std::getenv("MARSIT_PIPELINE") != nullptr) {
+    if (G == 1 && ctx->S >= 2 && !ctx->coop && std::getenv("MARSIT_PIPELINE") != nullptr) {
         ctx->pipeline = true;
         CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_extract, cudaEventDisableTiming));
         ctx->ev_merge.resize(ctx->S);
@@ -775,6 +883,20 @@ marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out) {
     CUDA_TRY(cudaMalloc(&ctx->d_stage_begin, sizeof(uint32_t) * ctx->dp.stage_begin.size()));
     CUDA_TRY(cudaMemcpy(ctx->d_stage_begin, ctx->dp.stage_begin.data(),
                         sizeof(uint32_t) * ctx->dp.stage_begin.size(), cudaMemcpyHostToDevice));
+    if (ctx->coop) {
+        std::vector<uint32_t> cnt(ctx->s_own);
+        for (uint32_t sl = 0; sl < ctx->s_own; ++sl) {
+            const uint32_t mb = ctx->dp.seg_begin[sl];
+            const uint32_t me = sl + 1 < ctx->s_own ? ctx->dp.seg_begin[sl + 1] : ctx->dp.n_merges;
+            cnt[sl] = me - mb;
+            ctx->coop_kmax = std::max(ctx->coop_kmax, cnt[sl]);
+        }
+        CUDA_TRY(cudaMalloc(&ctx->d_seg_count, sizeof(uint32_t) * cnt.size()));
+        CUDA_TRY(cudaMemcpy(ctx->d_seg_count, cnt.data(), sizeof(uint32_t) * cnt.size(),
+                            cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMalloc(&ctx->coop_counts, sizeof(uint32_t) * std::max<uint64_t>(1, ctx->coop_kmax) *
+                                                   ctx->s_own * ctx->tiles_per_seg));
+    }
     const size_t nflags = size_t(ctx->dp.n_merges + 1) * ctx->tiles_per_seg;
     CUDA_TRY(cudaMalloc(&ctx->flags, sizeof(uint64_t) * nflags));
     CUDA_TRY(cudaMemset(ctx->flags, 0, sizeof(uint64_t) * nflags));
@@ -795,7 +917,7 @@ marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out) {
             const char* e = std::getenv(name);
             return e ? std::atoi(e) : dflt;
         };
-        const int want_e = env_int("MARSIT_EXTRACT_CTAS", 2);
+        const int want_e = env_int("MARSIT_EXTRACT_CTAS", 4);
         const int want_d = env_int("MARSIT_DECODE_CTAS", 2);
         ctx->extract_grid = std::max(1, std::min(ob_extract, want_e)) * ctx->sm_count;
         ctx->decode_grid = std::max(1, std::min(ob_decode, want_d)) * ctx->sm_count;
@@ -891,6 +1013,7 @@ marsit_status marsit_sign_round(marsit_ctx* ctx, uint64_t t, double eta_s, uint6
     } else {
         if ((s = run_exchange(ctx, st))) return s;
         if ((s = run_merge(ctx, seed, t, 0, ctx->s_own, st))) return s;
+        if ((s = prefetch_coins(ctx, seed, t, st))) return s;
         if ((s = run_allgather(ctx, st))) return s;
         if ((s = run_decode(ctx, d_grads, d_comp, d_comp_out, d_update, eta_s, 0, ctx->S, st)))
             return s;

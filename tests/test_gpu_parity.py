@@ -312,3 +312,23 @@ def test_cpp_dropin_bit_identical_to_reference_in_process():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "DROP-IN PARITY OK" in r.stdout
+
+
+def test_coin_prefetch_speculation_is_safe():
+    """Round t+1's coins are precomputed during round t; rounds that do not
+    follow that guess (jumps in t, a new seed) must still be bit-exact."""
+    sched = mb.build_ring_schedule(4)
+    D = 100_003
+    T = O.schedule("ring", 4)
+    ctx = mb.Context(D, sched, torch.float32, 0)
+    comp_d = [torch.zeros(D, device=DEV) for _ in range(4)]
+    comp_h = np.zeros((4, D))
+    agg = torch.empty((D + 63) // 64, dtype=torch.int64, device=DEV)
+    for t, seed in [(1, 7), (2, 7), (5, 7), (3, 7), (4, 7), (4, 8), (5, 8), (6, 9)]:
+        gh = np.stack([O.gen_dyadic(seed, w, t, D) for w in range(4)])
+        ctx.sign_round(t, ETA, seed, to_dev(gh, torch.float32), comp_d, agg_bits=agg)
+        ctx.check()
+        want = O.marsit_round(T, t, None, ETA, gh, comp_h, seed)
+        assert np.array_equal(u64(agg), want.agg_bits), (t, seed)
+        comp_h = want.comp
+    assert np.array_equal(np.stack([c.double().cpu().numpy() for c in comp_d]), comp_h)

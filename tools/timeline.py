@@ -52,5 +52,9 @@ for e in step:
     name = e["name"].split("::")[-1].split("(")[0]
     print(f"{name:28s} stream {e['args'].get('stream', '?'):>4}  "
           f"{e['ts'] - t0:9.1f} .. {e['ts'] + e['dur'] - t0:9.1f} us  ({e['dur']:.1f})")
-print("step span:", round(step[-1]["ts"] + step[-1]["dur"] - t0, 1), "us; steps:",
-      [round(s[-1]["ts"] + s[-1]["dur"] - s[0]["ts"], 1) for s in steps])
+def span(st):
+    return round(max(e["ts"] + e["dur"] for e in st) - st[0]["ts"], 1)
+
+
+print("step span:", span(step), "us; steps:", [span(s) for s in steps],
+      "; extract-to-extract:", [round(b[0]["ts"] - a[0]["ts"], 1) for a, b in zip(steps, steps[1:])])
