@@ -676,15 +676,38 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
 // (its exclusive draw offset), reads its precomputed coin bits and deposits
 // them.  No look-back chains, no per-stage launches: a continuation merge
 // (torus) reads the finished total of the merge whose stream it continues.
-__device__ __forceinline__ uint32_t deposit32(uint32_t d, uint32_t cb) {
-    uint32_t keep = 0;
-    while (d) {
-        const uint32_t lsb = d & (0u - d);
-        d ^= lsb;
-        if (cb & 1u) keep |= lsb;
-        cb >>= 1;
+// Parallel bit deposit (PDEP): the low popcount(m) bits of x are placed,
+// in order, at the set bits of m.  Branch-free "expand" of Hacker's Delight
+// §7-6 (five parallel-suffix rounds); left shifts are written as multiplies
+// so they can issue on the FMA pipe next to the ALU-pipe logic ops.
+__device__ __forceinline__ uint32_t shl_fma(uint32_t x, uint32_t s) { return x * (1u << s); }
+__device__ __forceinline__ uint32_t deposit32(uint32_t m, uint32_t x) {
+    const uint32_t m0 = m;
+    uint32_t mk = ~m << 1;
+    uint32_t mv0, mv1, mv2, mv3, mv4;
+#define MARSIT_EXPAND_ROUND(I, MV)                        \
+    {                                                     \
+        uint32_t mp = mk ^ shl_fma(mk, 1);                \
+        mp ^= shl_fma(mp, 2);                             \
+        mp ^= shl_fma(mp, 4);                             \
+        mp ^= shl_fma(mp, 8);                             \
+        mp ^= shl_fma(mp, 16);                            \
+        MV = mp & m;                                      \
+        m = (m ^ MV) | (MV >> (1 << I));                  \
+        mk &= ~mp;                                        \
     }
-    return keep;
+    MARSIT_EXPAND_ROUND(0, mv0)
+    MARSIT_EXPAND_ROUND(1, mv1)
+    MARSIT_EXPAND_ROUND(2, mv2)
+    MARSIT_EXPAND_ROUND(3, mv3)
+    MARSIT_EXPAND_ROUND(4, mv4)
+#undef MARSIT_EXPAND_ROUND
+    x = (x & ~mv4) | (shl_fma(x, 16) & mv4);
+    x = (x & ~mv3) | (shl_fma(x, 8) & mv3);
+    x = (x & ~mv2) | (shl_fma(x, 4) & mv2);
+    x = (x & ~mv1) | (shl_fma(x, 2) & mv1);
+    x = (x & ~mv0) | (shl_fma(x, 1) & mv0);
+    return x & m0;
 }
 
 template <int WPT>
