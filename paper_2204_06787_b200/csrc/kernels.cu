@@ -2,10 +2,12 @@
 //
 //   K1 extract_kernel   u = g + c, bit = (u >= 0), packed per segment
 //                       (sync.hpp:71-76, segmentation.hpp:32-53, sign_vector.hpp:67-73)
-//   K2 merge_kernel     the segment's whole merge DAG, tile by tile, with one
-//                       decoupled look-back scan of popcount(r ^ l) per merge
-//                       for the coin stream offsets (merge.hpp:34-58,
-//                       allreduce.hpp:148-189, rng.hpp:28-54)
+//   C  coins_kernel     the coin bits of every merge stream, precomputed on a
+//                       side stream (data independent; rng.hpp:28-54)
+//   K2 merge_coop_kernel the segments' merge DAGs, cooperative: one grid
+//                       barrier + prefix sum per merge step for the coin
+//                       stream offsets, parallel bit deposit of the coins
+//                       (merge.hpp:34-58, allreduce.hpp:148-189)
 //   K3/K4 decode_kernel g_t = +-eta_s from the aggregate bits and the
 //                       compensation update c' = u - g_t fused in one pass
 //                       (sync.hpp:103-118, sign_vector.hpp:77-89)
@@ -75,15 +77,6 @@ __device__ __forceinline__ uint64_t stream_key(uint64_t seed, uint64_t purpose, 
 // ---------------------------------------------------------------------------
 // Memory helpers
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
-    uint64_t v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
 // Streaming 128-bit loads that do not allocate in L1 (each byte is read once).
 __device__ __forceinline__ float4 ld_stream(const float4* p) {
     float4 v;
@@ -385,97 +378,6 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode
 // Tiles are handed out by an atomic counter in segment order, so every
 // look-back only waits on CTAs that are already running.
 // ---------------------------------------------------------------------------
-constexpr uint64_t kValMask = (1ull << 38) - 1;
-constexpr uint32_t kAgg = 1, kPrefix = 2;
-
-__device__ __forceinline__ uint64_t pack_flag(uint32_t epoch, uint32_t st, uint64_t v) {
-    return (uint64_t(epoch) << 40) | (uint64_t(st) << 38) | v;
-}
-
-// Warp-wide decoupled look-back.  Lane l inspects the F predecessors
-// pos - l*F - f (order o = l*F + f), so one round trip to L2 covers 32*F
-// tiles.  The warp sums the published prefix of that window up to the first
-// inclusive prefix (done) or the first unpublished flag (it then polls that
-// single flag with backoff and resumes there: resolved flags are never
-// re-read).  Returns the exclusive prefix and publishes the inclusive one.
-template <int F>
-__device__ __forceinline__ uint64_t lookback(uint64_t* fl, uint32_t tile, uint32_t epoch,
-                                             uint64_t agg, int lane) {
-    if (tile == 0) {
-        if (lane == 0) st_relaxed(fl, pack_flag(epoch, kPrefix, agg));
-        return 0;
-    }
-    if (lane == 0) st_relaxed(fl + tile, pack_flag(epoch, kAgg, agg));
-    uint64_t excl = 0;
-    int64_t pos = int64_t(tile) - 1;
-    while (true) {
-        uint64_t v[F];
-#pragma unroll
-        for (int f = 0; f < F; ++f) {
-            const int64_t idx = pos - int64_t(lane) * F - f;
-            v[f] = idx >= 0 ? ld_relaxed(fl + idx) : pack_flag(epoch, kPrefix, 0);
-        }
-        uint32_t my_p = 0xffffffffu, my_inv = 0xffffffffu;
-#pragma unroll
-        for (int f = F - 1; f >= 0; --f) {
-            const uint32_t st = uint32_t(v[f] >> 38) & 3u;
-            const bool valid = uint32_t(v[f] >> 40) == epoch && st != 0;
-            if (!valid) my_inv = uint32_t(lane * F + f);
-            else if (st == kPrefix) my_p = uint32_t(lane * F + f);
-        }
-        const uint32_t gp = __reduce_min_sync(kFull, my_p);
-        const uint32_t gi = __reduce_min_sync(kFull, my_inv);
-        // orders [0, bound) are summed: through the first inclusive prefix, else
-        // up to the first unpublished flag, else the whole window
-        const uint32_t bound = gp < gi ? gp + 1 : (gi < 32u * F ? gi : 32u * F);
-        uint64_t mine = 0;
-#pragma unroll
-        for (int f = 0; f < F; ++f)
-            if (uint32_t(lane * F + f) < bound) mine += v[f] & kValMask;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(kFull, mine, o);
-        excl += mine;
-        if (gp < gi) break;
-        pos -= bound;
-        if (bound == 0 && lane == 0) {  // wait for the nearest predecessor to publish
-            uint32_t ns = 32;
-            while (true) {
-                const uint64_t w = ld_relaxed(fl + pos);
-                if (uint32_t(w >> 40) == epoch && ((w >> 38) & 3u) != 0) break;
-                __nanosleep(ns);
-                ns = ns < 1024 ? ns * 2 : ns;
-            }
-        }
-        __syncwarp();
-    }
-    if (lane == 0) st_relaxed(fl + tile, pack_flag(epoch, kPrefix, excl + agg));
-    return excl;
-}
-
-template <int WPT>
-__device__ __forceinline__ uint64_t load_bits(const uint32_t* p) {
-    if (WPT == 2) {
-        const uint2 v = __ldcg(reinterpret_cast<const uint2*>(p));
-        return uint64_t(v.x) | (uint64_t(v.y) << 32);
-    }
-    return __ldcg(p);
-}
-template <int WPT>
-__device__ __forceinline__ void store_bits(uint32_t* p, uint64_t v, bool streaming) {
-    if (WPT == 2) {
-        const uint2 u = make_uint2(uint32_t(v), uint32_t(v >> 32));
-        if (streaming)
-            __stcg(reinterpret_cast<uint2*>(p), u);
-        else
-            *reinterpret_cast<uint2*>(p) = u;
-    } else {
-        if (streaming)
-            __stcg(p, uint32_t(v));
-        else
-            *p = uint32_t(v);
-    }
-}
-
 // Coins of one packed word: for each set bit of `d` (ascending), draw
 // mix(z), z += gamma; keep the received bit where the draw is below th.
 __device__ __forceinline__ uint32_t coin_word(uint32_t d, uint64_t& z, uint64_t th) {
@@ -490,197 +392,20 @@ __device__ __forceinline__ uint32_t coin_word(uint32_t d, uint64_t& z, uint64_t 
     return keep;
 }
 
-// Deposit consecutive coin bits (bit 0 first) onto the set bits of d, in
-// ascending order; returns the keep mask (coin -> received bit).
-__device__ __forceinline__ uint32_t deposit_word(uint32_t d, uint64_t& cb) {
-    uint32_t keep = 0;
-    while (d) {
-        const uint32_t lsb = d & (0u - d);
-        d ^= lsb;
-        if (uint32_t(cb) & 1u) keep |= lsb;
-        cb >>= 1;
-    }
-    return keep;
-}
-
-// Merge kernel.  A CTA takes a tile of 256 x WPT packed words of one owned
-// segment and runs every merge of the current plan stage over it; thread t
-// always owns words t*WPT.. of the tile, so DAG intermediates never leave
-// the thread (shared-memory slots only because their index is dynamic).
-// Per merge: d = r ^ l; a block scan of popcount(d) plus one decoupled
-// look-back (warp 0) give each thread the stream index of its first coin;
-// the coins are the precomputed bits [n, n + popc) deposited onto the set
-// bits of d (inline SplitMix64 draws beyond the precomputed budget);
-// out = r ^ (d & ~coin).  Leaf operands of the next merge are prefetched
-// before the look-back.  Tiles are handed out by an atomic counter in
-// segment order, so a look-back only ever waits on running CTAs.
-#ifdef MARSIT_MERGE_PROF
-}  // namespace
-__device__ unsigned long long g_merge_prof[8];
-namespace {
-__device__ __forceinline__ uint64_t gtime() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-#define PROF_T(var) const uint64_t var = (tid == 0) ? gtime() : 0
-#define PROF_ADD(i, v) if (tid == 0) atomicAdd(&g_merge_prof[i], (unsigned long long)(v))
-#else
-#define PROF_T(var)
-#define PROF_ADD(i, v)
-#endif
-
-template <int WPT>
-__global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams p) {
-    extern __shared__ uint64_t slots[];  // [max_slots][kMergeThreads]
-    __shared__ uint32_t s_tile;
-    __shared__ uint32_t s_warp[kMergeThreads / 32];
-    __shared__ uint64_t s_base;
-    constexpr uint32_t kTW = kMergeThreads * WPT;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t total_tiles = p.n_proc * p.tiles_per_seg;
-    while (true) {
-        if (tid == 0) s_tile = atomicAdd(p.tile_counter, 1u) - p.tile_base;
-        __syncthreads();
-        const uint32_t gt = s_tile;
-        __syncthreads();
-        if (gt >= total_tiles) break;
-        const uint32_t sl = p.seg0 + gt % p.n_proc, tile = gt / p.n_proc;
-        const uint32_t w0 = tile * kTW + tid * WPT;
-        const bool active = w0 < p.words_proc;
-        const int64_t rem = int64_t(p.seg_bits) - int64_t(w0) * 32;
-        const uint64_t vmask =
-            rem >= WPT * 32 ? (WPT == 2 ? ~0ull : 0xffffffffull)
-                            : (rem <= 0 ? 0ull : ((1ull << rem) - 1ull));
-        const uint32_t mb = p.seg_begin[sl];
-        const uint32_t kb = p.stage_begin[sl * (p.n_stages + 1) + p.stage];
-        const uint32_t ke = p.stage_begin[sl * (p.n_stages + 1) + p.stage + 1];
-        const uint32_t sg = p.s_first + sl;
-        auto load_src = [&](uint16_t src) -> uint64_t {
-            if (!active) return 0ull;
-            const uint32_t idx = src & 0x3FFFu;
-            switch (src & 0xC000u) {
-                case kSrcLeaf:
-                    return load_bits<WPT>(
-                        p.leaves +
-                        (uint64_t((idx / p.ml) * p.n_seg + sl) * p.ml + idx % p.ml) * p.wst + w0);
-                case kSrcSlot:
-                    return slots[idx * kMergeThreads + tid];
-                default:
-                    return load_bits<WPT>(p.gnodes + (uint64_t(sl) * p.gmax + idx) * p.wst + w0);
-            }
-        };
-        uint64_t pf_r = 0, pf_l = 0;
-        if (kb < ke) {
-            const DevMerge m0 = p.merges[mb + kb];
-            if ((m0.recv_src & 0xC000u) == kSrcLeaf) pf_r = load_src(m0.recv_src);
-            if ((m0.local_src & 0xC000u) == kSrcLeaf) pf_l = load_src(m0.local_src);
-        }
-        for (uint32_t k = kb; k < ke; ++k) {
-            PROF_T(t0);
-            const DevMerge m = p.merges[mb + k];
-            const uint64_t r = (m.recv_src & 0xC000u) == kSrcLeaf ? pf_r : load_src(m.recv_src);
-            const uint64_t l = (m.local_src & 0xC000u) == kSrcLeaf ? pf_l : load_src(m.local_src);
-            if (k + 1 < ke) {
-                const DevMerge mn = p.merges[mb + k + 1];
-                if ((mn.recv_src & 0xC000u) == kSrcLeaf) pf_r = load_src(mn.recv_src);
-                if ((mn.local_src & 0xC000u) == kSrcLeaf) pf_l = load_src(mn.local_src);
-            }
-            const uint64_t d = (r ^ l) & vmask;
-            const uint32_t cnt = __popcll(d);
-            uint32_t incl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(kFull, incl, o);
-                if (lane >= o) incl += y;
-            }
-            if (lane == 31) s_warp[wid] = incl;
-            __syncthreads();
-            PROF_T(t1);
-            if (wid == 0) {
-                const uint32_t ws = lane < kMergeThreads / 32 ? s_warp[lane] : 0u;
-                uint32_t wincl = ws;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(kFull, wincl, o);
-                    if (lane >= o) wincl += y;
-                }
-                const uint32_t tile_total = __shfl_sync(kFull, wincl, 31);
-                uint64_t base = m.base_add;  // draws of this stream before this merge
-                if (m.offset_src >= 0 && lane == 0) {
-                    for (int32_t src = m.offset_src; src >= 0;) {
-                        const DevMerge& pm = p.merges[mb + src];
-                        base += p.totals[mb + src] + pm.base_add;
-                        src = pm.offset_src;
-                    }
-                }
-                const uint64_t excl = lookback<4>(p.flags + uint64_t(mb + k) * p.tiles_per_seg,
-                                                  tile, p.epoch, tile_total, lane);
-                if (lane < kMergeThreads / 32) s_warp[lane] = wincl - ws;
-                if (lane == 0) {
-                    s_base = base + excl;
-                    if (tile == p.tiles_per_seg - 1) p.totals[mb + k] = excl + tile_total;
-                }
-            }
-            __syncthreads();
-            PROF_T(t2);
-            const uint64_t n0 = s_base + s_warp[wid] + (incl - cnt);  // my first coin's draw
-            uint64_t keep;
-            if (n0 + cnt <= uint64_t(m.coin_words) * 32) {
-                // precomputed coin bits [n0, n0 + cnt): at most 64 of them
-                const uint32_t* cw = p.coins + m.coin_off + (n0 >> 5);
-                const uint32_t sh = uint32_t(n0 & 31);
-                const uint64_t last = (n0 + cnt + 31) >> 5;  // one past the last word needed
-                const uint32_t c0 = cnt ? __ldg(cw) : 0u;
-                const uint32_t c1 = ((n0 >> 5) + 1 < last) ? __ldg(cw + 1) : 0u;
-                const uint32_t c2 = ((n0 >> 5) + 2 < last) ? __ldg(cw + 2) : 0u;
-                uint64_t cb = uint64_t(__funnelshift_r(c0, c1, sh)) |
-                              (uint64_t(__funnelshift_r(c1, c2, sh)) << 32);
-                keep = deposit_word(uint32_t(d), cb);
-                if (WPT == 2) keep |= uint64_t(deposit_word(uint32_t(d >> 32), cb)) << 32;
-            } else {
-                // beyond the precomputed budget (unusually many disagreements): draw inline
-                const uint64_t key =
-                    m.key_mode ? m.key : stream_key(p.seed, 5, m.receiver, p.round, sg);
-                uint64_t z = key + (n0 + 1) * kGamma;
-                keep = coin_word(uint32_t(d), z, m.thresh11);
-                if (WPT == 2) keep |= uint64_t(coin_word(uint32_t(d >> 32), z, m.thresh11)) << 32;
-            }
-            const uint64_t out = (r ^ (d & ~keep)) & vmask;
-            PROF_T(t3);
-            if (active) {
-                if (m.out_slot != kNone) slots[m.out_slot * kMergeThreads + tid] = out;
-                if (m.out_global == kFinal)
-                    store_bits<WPT>(p.agg + uint64_t(sg) * p.wst + w0, out, false);
-                else if (m.out_global != kNone)
-                    store_bits<WPT>(p.gnodes + (uint64_t(sl) * p.gmax + m.out_global) * p.wst + w0,
-                                    out, true);
-            }
-            __syncthreads();  // s_warp / s_base are rewritten by the next merge
-            PROF_T(t4);
-            PROF_ADD(0, t1 - t0);
-            PROF_ADD(1, t2 - t1);
-            PROF_ADD(2, t3 - t2);
-            PROF_ADD(3, t4 - t3);
-            PROF_ADD(4, 1);
-        }
-    }
-}
-
-
-
-// Cooperative merge.  One CTA per tile of 256 x WPT packed words, every tile
-// of every owned segment resident at once (cooperative launch).  Merge step
-// k: each tile publishes popcount(r ^ l) of its k-th merge, one grid-wide
-// barrier, then every tile sums the published counts of the tiles before it
-// (its exclusive draw offset), reads its precomputed coin bits and deposits
-// them.  No look-back chains, no per-stage launches: a continuation merge
-// (torus) reads the finished total of the merge whose stream it continues.
+// K2: the merge DAG, cooperative.  One CTA per tile of 256 x WPT packed words;
+// the tiles of one launch ("part": tiles [part_tile0, part_tile0+part_tiles)
+// of every owned segment) are co-resident (cooperative launch).  Merge step
+// k of the current plan stage: each tile publishes popcount(r ^ l), one
+// grid-wide barrier, then every tile sums the published counts of the
+// tiles before it (its exclusive draw offset; earlier parts contribute their
+// totals), reads its precomputed coin bits and deposits them onto the set
+// bits of r ^ l.  A continuation merge (torus stage 2) starts its stream
+// after the complete draw total of the merge it continues (previous stage).
+__device__ __forceinline__ uint32_t shl_fma(uint32_t x, uint32_t s) { return x * (1u << s); }
 // Parallel bit deposit (PDEP): the low popcount(m) bits of x are placed,
 // in order, at the set bits of m.  Branch-free "expand" of Hacker's Delight
 // §7-6 (five parallel-suffix rounds); left shifts are written as multiplies
 // so they can issue on the FMA pipe next to the ALU-pipe logic ops.
-__device__ __forceinline__ uint32_t shl_fma(uint32_t x, uint32_t s) { return x * (1u << s); }
 __device__ __forceinline__ uint32_t deposit32(uint32_t m, uint32_t x) {
     const uint32_t m0 = m;
     uint32_t mk = ~m << 1;
@@ -731,25 +456,27 @@ __device__ __forceinline__ void load_words(const uint32_t* p, uint32_t (&v)[WPT]
 }
 
 template <int WPT>
-__global__ void __launch_bounds__(kMergeThreads) merge_coop_kernel(const CoopParams p) {
+__global__ void __launch_bounds__(kMergeThreads, WPT >= 8 ? 3 : 4) merge_coop_kernel(const CoopParams p) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     extern __shared__ uint32_t cslots[];  // [max_slots][WPT][kMergeThreads]
     __shared__ uint32_t s_warp[kMergeThreads / 32];
     __shared__ uint64_t s_base;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t T = p.n_seg * p.tiles_per_seg;
-    const uint32_t tg = blockIdx.x;          // segment-major tile id
-    const uint32_t sl = tg / p.tiles_per_seg, tile = tg % p.tiles_per_seg;
+    const uint32_t T = p.n_seg * p.part_tiles;  // CTAs in this launch
+    const uint32_t sl = blockIdx.x / p.part_tiles, lt = blockIdx.x % p.part_tiles;
+    const uint32_t tile = p.part_tile0 + lt;
     const uint32_t w0 = tile * (kMergeThreads * WPT) + tid * WPT;
-    const bool active = w0 < p.words_proc;
+    const bool active = tile < p.tiles_per_seg && w0 < p.words_proc;
     // valid bits of my words: all 32 while rem >= 32 (bits beyond L stay 0)
     const int64_t rem0 = int64_t(p.seg_bits) - int64_t(w0) * 32;
     auto vmask = [&](int j) -> uint32_t {
         const int64_t rem = rem0 - 32 * j;
         return rem >= 32 ? kFull : (rem <= 0 ? 0u : ((1u << rem) - 1u));
     };
-    const uint32_t mb = p.seg_begin[sl], nm = p.seg_count[sl];
+    const uint32_t mb = p.seg_begin[sl];
+    const uint32_t kb = p.stage_begin[sl * (p.n_stages + 1) + p.stage];
+    const uint32_t nm = p.stage_begin[sl * (p.n_stages + 1) + p.stage + 1] - kb;
     const uint32_t sg = p.s_first + sl;
     auto load_src = [&](uint16_t src, uint32_t (&v)[WPT]) {
         const uint32_t idx = src & 0x3FFFu;
@@ -761,25 +488,28 @@ __global__ void __launch_bounds__(kMergeThreads) merge_coop_kernel(const CoopPar
                                 (uint64_t((idx / p.ml) * p.n_seg + sl) * p.ml + idx % p.ml) * p.wst +
                                 w0,
                             v);
-        } else {
+        } else if ((src & 0xC000u) == kSrcSlot) {
 #pragma unroll
             for (int j = 0; j < WPT; ++j) v[j] = cslots[(idx * WPT + j) * kMergeThreads + tid];
+        } else {
+            load_words<WPT>(p.gnodes + (uint64_t(sl) * p.gmax + idx) * p.wst + w0, v);
         }
     };
     // the local operand of the next merge is prefetched when it is a leaf
-    // (the ring / torus case: the received operand is the running aggregate)
+    // (ring / torus: the received operand is the running aggregate)
     uint32_t pl[WPT];
     if (nm > 0) {
-        const DevMerge m0 = p.merges[mb];
+        const DevMerge m0 = p.merges[mb + kb];
         if ((m0.local_src & 0xC000u) == kSrcLeaf) load_src(m0.local_src, pl);
     }
     uint32_t r[WPT], d[WPT];
-    for (uint32_t k = 0; k < p.k_max; ++k) {
+    for (uint32_t k = 0; k < p.k_steps; ++k) {
         const bool live = k < nm;
+        const uint32_t mi = kb + k;  // merge index within the segment
         DevMerge m{};
         uint32_t cnt = 0;
         if (live) {
-            m = p.merges[mb + k];
+            m = p.merges[mb + mi];
             load_src(m.recv_src, r);
             if ((m.local_src & 0xC000u) == kSrcLeaf) {
 #pragma unroll
@@ -790,7 +520,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_coop_kernel(const CoopPar
                 for (int j = 0; j < WPT; ++j) d[j] = (r[j] ^ d[j]) & vmask(j);
             }
             if (k + 1 < nm) {
-                const DevMerge mn = p.merges[mb + k + 1];
+                const DevMerge mn = p.merges[mb + mi + 1];
                 if ((mn.local_src & 0xC000u) == kSrcLeaf) load_src(mn.local_src, pl);
             }
 #pragma unroll
@@ -812,15 +542,15 @@ __global__ void __launch_bounds__(kMergeThreads) merge_coop_kernel(const CoopPar
             warp_off += w < wid ? v : 0u;
             tile_total += v;
         }
-        if (tid == 0) p.counts[uint64_t(k) * T + tg] = tile_total;
+        if (tid == 0) p.counts[uint64_t(k) * T + blockIdx.x] = tile_total;
         grid.sync();
         if (live && wid == 0) {
-            // exclusive prefix over the earlier tiles of this segment
-            const uint32_t* cs = p.counts + uint64_t(k) * T + uint64_t(sl) * p.tiles_per_seg;
+            // exclusive prefix over the earlier tiles of this segment in this part
+            const uint32_t* cs = p.counts + uint64_t(k) * T + uint64_t(sl) * p.part_tiles;
             uint64_t acc = 0, all = 0;
-            for (uint32_t i = lane; i < p.tiles_per_seg; i += 32) {
+            for (uint32_t i = lane; i < p.part_tiles; i += 32) {
                 const uint32_t v = __ldcg(cs + i);
-                acc += i < tile ? v : 0u;
+                acc += i < lt ? v : 0u;
                 all += v;
             }
 #pragma unroll
@@ -828,15 +558,20 @@ __global__ void __launch_bounds__(kMergeThreads) merge_coop_kernel(const CoopPar
                 acc += __shfl_xor_sync(kFull, acc, o);
                 all += __shfl_xor_sync(kFull, all, o);
             }
-            uint64_t base = m.base_add;  // draws of this stream before this merge
-            for (int32_t src = m.offset_src; src >= 0;) {
-                const DevMerge& pm = p.merges[mb + src];
-                base += __ldcg(p.totals + mb + src) + pm.base_add;
-                src = pm.offset_src;
-            }
             if (lane == 0) {
+                const uint32_t nmerges = p.n_merges;
+                uint64_t base = m.base_add;  // draws of this stream before this merge
+                for (uint32_t q = 0; q < p.part; ++q)  // earlier parts of this merge
+                    base += __ldcg(p.part_totals + uint64_t(q) * nmerges + mb + mi);
+                for (int32_t src = m.offset_src; src >= 0;) {  // continued stream (earlier stage)
+                    const DevMerge& pm = p.merges[mb + src];
+                    for (uint32_t q = 0; q < p.n_parts; ++q)
+                        base += __ldcg(p.part_totals + uint64_t(q) * nmerges + mb + src);
+                    base += pm.base_add;
+                    src = pm.offset_src;
+                }
                 s_base = base + acc;
-                if (tile == 0) p.totals[mb + k] = all;
+                if (lt == 0) p.part_totals[uint64_t(p.part) * nmerges + mb + mi] = all;
             }
         }
         __syncthreads();
@@ -878,11 +613,15 @@ __global__ void __launch_bounds__(kMergeThreads) merge_coop_kernel(const CoopPar
                     uint32_t* dst = p.agg + uint64_t(sg) * p.wst + w0;
 #pragma unroll
                     for (int j = 0; j < WPT; ++j) dst[j] = r[j];
+                } else if (m.out_global != kNone) {
+                    uint32_t* dst = p.gnodes + (uint64_t(sl) * p.gmax + m.out_global) * p.wst + w0;
+#pragma unroll
+                    for (int j = 0; j < WPT; ++j) __stcg(dst + j, r[j]);
                 }
             }
         }
-        // s_warp / s_base are rewritten next step; slots written above are read
-        // by the same thread only
+        // s_warp / s_base are rewritten next step; slots are read by the
+        // writing thread only
         __syncthreads();
     }
 }
@@ -1086,26 +825,7 @@ cudaError_t launch_decode(const StreamParams<T>& p, bool vec, int grid, cudaStre
     return cudaGetLastError();
 }
 
-cudaError_t launch_merge(const MergeParams& p, int wpt, int grid, size_t smem, cudaStream_t st) {
-    if (wpt == 2)
-        merge_kernel<2><<<grid, kMergeThreads, smem, st>>>(p);
-    else
-        merge_kernel<1><<<grid, kMergeThreads, smem, st>>>(p);
-    return cudaGetLastError();
-}
 
-cudaError_t merge_kernel_set_smem(size_t smem) {
-    // The attribute is per function and process-wide: only ever raise it.
-    static size_t current = 48 * 1024;
-    if (smem <= current) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(merge_kernel<1>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(merge_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(smem));
-    if (e == cudaSuccess) current = smem;
-    return e;
-}
 
 template <int WPT>
 static cudaError_t coop_launch_t(const CoopParams& p, size_t smem, cudaStream_t st) {
@@ -1119,7 +839,7 @@ static cudaError_t coop_launch_t(const CoopParams& p, size_t smem, cudaStream_t 
     CoopParams q = p;
     void* args[] = {&q};
     return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(merge_coop_kernel<WPT>),
-                                       dim3(p.n_seg * p.tiles_per_seg), dim3(kMergeThreads), args,
+                                       dim3(p.n_seg * p.part_tiles), dim3(kMergeThreads), args,
                                        smem, st);
 }
 
@@ -1129,7 +849,6 @@ cudaError_t launch_merge_coop(const CoopParams& p, int wpt, size_t smem, cudaStr
         case 2: return coop_launch_t<2>(p, smem, st);
         case 4: return coop_launch_t<4>(p, smem, st);
         case 8: return coop_launch_t<8>(p, smem, st);
-        case 16: return coop_launch_t<16>(p, smem, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -1140,7 +859,6 @@ cudaError_t merge_coop_occupancy(int wpt, size_t smem, int* blocks) {
         case 2: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<2>, kMergeThreads, smem);
         case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<4>, kMergeThreads, smem);
         case 8: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<8>, kMergeThreads, smem);
-        case 16: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<16>, kMergeThreads, smem);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -1167,10 +885,6 @@ cudaError_t stream_occupancy(bool f64, int* extract_blocks, int* decode_blocks) 
     return e;
 }
 
-cudaError_t merge_kernel_occupancy(size_t smem, int* blocks_per_sm) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, merge_kernel<2>,
-                                                         kMergeThreads, smem);
-}
 
 cudaError_t launch_coins(const DevMerge* merges, uint32_t n_merges, uint64_t seed, uint64_t round,
                          uint32_t* coins, int grid_x, cudaStream_t st) {
@@ -1236,12 +950,4 @@ MARSIT_INSTANTIATE(double)
 
 }  // namespace marsit_b200
 
-#ifdef MARSIT_MERGE_PROF
-extern "C" void marsit_debug_merge_prof(unsigned long long* out, int reset) {
-    cudaMemcpyFromSymbol(out, marsit_b200::g_merge_prof, sizeof(marsit_b200::g_merge_prof));
-    if (reset) {
-        unsigned long long z[8] = {};
-        cudaMemcpyToSymbol(marsit_b200::g_merge_prof, z, sizeof(z));
-    }
-}
-#endif
+

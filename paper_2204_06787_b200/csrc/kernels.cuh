@@ -38,40 +38,25 @@ struct DevMerge {
 };
 static_assert(sizeof(DevMerge) == 56, "DevMerge layout");
 
-struct MergeParams {
-    const DevMerge* merges;      // all owned segments' merges, segment-major
-    const uint32_t* seg_begin;   // [n_seg] first merge of each owned segment
-    const uint32_t* stage_begin; // [n_seg][n_stages+1] merge-index ranges per stage
-    uint32_t n_stages, stage;
-    uint32_t n_seg, s_first;     // owned segments and the global id of the first
-    uint32_t seg0, n_proc;       // this launch: owned segments [seg0, seg0 + n_proc)
-    uint32_t tiles_per_seg, words_proc, wst, ml;
-    uint32_t max_slots;          // shared-memory node slots per warp
-    uint64_t seg_bits;           // L
-    const uint32_t* leaves;      // leaf(w, sl) = leaves + ((w/ml*n_seg + sl)*ml + w%ml)*wst
-    uint32_t* gnodes;            // [n_seg][gmax][wst]
-    uint32_t gmax;
-    uint32_t* agg;               // [S][wst]; owned segment sl at s_first + sl
-    const uint32_t* coins;       // precomputed coin bitstreams (see launch_coins)
-    uint64_t* flags;             // [merges][tiles_per_seg] decoupled look-back
-    uint64_t* totals;            // [merges] draws consumed by each merge (last tile)
-    uint32_t* tile_counter;
-    uint32_t tile_base, epoch;
-    uint64_t seed, round;
-};
 
-// Cooperative merge (all tiles co-resident, one grid barrier per merge step).
+// Cooperative merge (kernels.cu, K2): the tiles of one launch are
+// co-resident; one grid barrier per merge step of the current plan stage.
 struct CoopParams {
-    const DevMerge* merges;      // owned segments' merges in schedule order
-    const uint32_t* seg_begin;   // [n_seg] first merge of each owned segment
-    const uint32_t* seg_count;   // [n_seg] merges of each owned segment
-    uint32_t n_seg, s_first, tiles_per_seg, words_proc, wst, ml, max_slots, k_max;
-    uint64_t seg_bits;           // L
-    const uint32_t* leaves;      // as MergeParams
-    uint32_t* agg;               // [S][wst]
-    const uint32_t* coins;
-    uint32_t* counts;            // [k_max][n_seg * tiles_per_seg] popcount of each tile
-    uint64_t* totals;            // [n_merges] draws consumed by each merge (whole segment)
+    const DevMerge* merges;       // owned segments' merges, stage-sorted per segment
+    const uint32_t* seg_begin;    // [n_seg] first merge of each owned segment
+    const uint32_t* stage_begin;  // [n_seg][n_stages+1] merge ranges per stage
+    uint32_t n_stages, stage, k_steps;  // k_steps: max merges of this stage over segments
+    uint32_t n_seg, s_first, tiles_per_seg, words_proc, wst, ml, max_slots;
+    uint32_t part, n_parts, part_tile0, part_tiles;  // tiles of each segment in this launch
+    uint32_t n_merges;
+    uint64_t seg_bits;            // L
+    const uint32_t* leaves;       // leaf(w, sl) = leaves + ((w/ml*n_seg + sl)*ml + w%ml)*wst
+    uint32_t* gnodes;             // [n_seg][gmax][wst] nodes crossing stages
+    uint32_t gmax;
+    uint32_t* agg;                // [S][wst]
+    const uint32_t* coins;        // precomputed coin bitstreams
+    uint32_t* counts;             // [k_steps][n_seg * part_tiles] popcount of each tile
+    uint64_t* part_totals;        // [n_parts][n_merges] draws consumed per (part, merge)
     uint64_t seed, round;
 };
 cudaError_t launch_merge_coop(const CoopParams& p, int wpt, size_t smem, cudaStream_t st);
@@ -98,9 +83,6 @@ template <typename T>
 cudaError_t launch_extract(const StreamParams<T>& p, bool vec, int grid, cudaStream_t st);
 template <typename T>
 cudaError_t launch_decode(const StreamParams<T>& p, bool vec, int grid, cudaStream_t st);
-cudaError_t launch_merge(const MergeParams& p, int wpt, int grid, size_t smem, cudaStream_t st);
-cudaError_t merge_kernel_occupancy(size_t smem, int* blocks_per_sm);
-cudaError_t merge_kernel_set_smem(size_t smem);
 cudaError_t stream_occupancy(bool f64, int* extract_blocks, int* decode_blocks);
 // Precompute the coin bits of every merge: bit n of merge m's stream is
 // (mix(key_m + (n+1)γ) < thresh11_m) for n < 32 * coin_words.  Data

@@ -1,15 +1,15 @@
 // runtime.cu — host runtime behind the C-ABI (include/marsit_b200.h).
 //
 // A marsit_ctx owns every device buffer of the path and the compiled merge
-// plan; a round is a fixed sequence of launches on the caller's stream:
+// plan; a sign round is a fixed sequence of launches on the caller's stream:
 //
-//   G == 1:  extract -> merge (1 launch per plan stage) -> decode [-> export]
-//   G  > 1:  extract -> NCCL exchange of packed segments to their owners ->
-//            merge (owned segments) -> NCCL all-gather of the aggregates ->
-//            decode [-> export]
+//   [aux: coins for (seed, t) unless prefetched]
+//   extract -> (G > 1: NCCL exchange of packed segments to their owners)
+//   -> cooperative merge (per plan stage x part) -> [aux: coins for t + 1]
+//   -> (G > 1: NCCL all-gather of the owned aggregates) -> decode+comp
 //
 // Segments are owned by ranks in contiguous blocks (rank q owns segments
-// [q*S/G, (q+1)*S/G)), so the exchange is a plain all-to-all of contiguous
+// [q*S/G, (q+1)*S/G)), so the exchange is an all-to-all of contiguous
 // per-destination blocks and the all-gather is in place.
 #include <cuda_runtime.h>
 #include <nccl.h>
@@ -18,7 +18,6 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -60,6 +59,16 @@ marsit_status fail(marsit_status st, const std::string& msg) {
 uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 uint64_t round_up(uint64_t a, uint64_t b) { return ceil_div(a, b) * b; }
 
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+bool have_device() {
+    int n = 0;
+    return cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
+}
+
 // Device-side plan of the merge DAGs (see DevMerge in kernels.cuh).
 struct DevicePlan {
     std::vector<DevMerge> merges;
@@ -67,10 +76,14 @@ struct DevicePlan {
     uint32_t max_slots = 0, gmax = 0, n_stages = 1, n_merges = 0;
 };
 
-// Lower one segment's merge DAG: assign same-stage consumers to shared-memory
-// slots (liveness-based reuse) and cross-stage / final outputs to global nodes.
+// Lower the owned segments' merge DAGs: execution order = (stage, schedule
+// order); outputs consumed by a later merge of the same stage get a
+// shared-memory slot (liveness-based reuse, read-before-write within a
+// thread), outputs consumed by a later stage get a global node, the final
+// node goes to the aggregate.
 marsit_status lower_plan(const Plan& plan, uint32_t s_first, uint32_t n_seg, DevicePlan& dp) {
     const uint32_t W = plan.workers;
+    dp = DevicePlan{};
     dp.n_stages = plan.n_stages;
     dp.seg_begin.resize(n_seg);
     dp.stage_begin.assign(size_t(n_seg) * (plan.n_stages + 1), 0);
@@ -78,15 +91,13 @@ marsit_status lower_plan(const Plan& plan, uint32_t s_first, uint32_t n_seg, Dev
         const SegmentPlan& sp = plan.seg[s_first + sl];
         const size_t n = sp.merges.size();
         if (sp.final_node < W) return fail(MARSIT_EUNSUPPORTED, "schedule performs no reduction");
-        // execution order: by stage, then schedule order
         std::vector<uint32_t> order(n);
         for (size_t k = 0; k < n; ++k) order[k] = uint32_t(k);
         std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
             return sp.merges[a].stage < sp.merges[b].stage;
         });
-        std::vector<uint32_t> pos(n);  // original index -> execution index
+        std::vector<uint32_t> pos(n);  // schedule index -> execution index
         for (size_t e = 0; e < n; ++e) pos[order[e]] = uint32_t(e);
-        // consumers
         std::vector<int> last_same(n, -1);
         std::vector<bool> cross(n, false);
         for (size_t e = 0; e < n; ++e) {
@@ -121,7 +132,6 @@ marsit_status lower_plan(const Plan& plan, uint32_t s_first, uint32_t n_seg, Dev
             };
             d.recv_src = encode(m.recv_node);
             d.local_src = encode(m.local_node);
-            // free slots whose last same-stage use is this merge (read before write)
             for (uint32_t in : {m.recv_node, m.local_node})
                 if (in >= W && last_same[in - W] == int(e) && slot_of[in - W] != kNone)
                     slot_busy[slot_of[in - W]] = false;
@@ -145,7 +155,6 @@ marsit_status lower_plan(const Plan& plan, uint32_t s_first, uint32_t n_seg, Dev
             dp.merges.push_back(d);
         }
         dp.gmax = std::max(dp.gmax, gnext);
-        // stage ranges (execution order is stage-sorted)
         for (uint32_t st = 0; st <= plan.n_stages; ++st) {
             uint32_t c = 0;
             for (size_t e = 0; e < n; ++e)
@@ -158,6 +167,130 @@ marsit_status lower_plan(const Plan& plan, uint32_t s_first, uint32_t n_seg, Dev
     dp.n_merges = uint32_t(dp.merges.size());
     return MARSIT_OK;
 }
+
+// The cooperative merge of a set of owned segments (K2).  Chooses the words
+// per thread and splits each segment's tiles into parts so that one launch's
+// tiles are co-resident; launches stage x part.
+struct MergeRunner {
+    DevicePlan dp;
+    uint32_t n_seg = 0, s_first = 0, words_proc = 0, wst = 0, ml = 0;
+    uint64_t L = 0;
+    int wpt = 1;
+    size_t smem = 0;
+    uint32_t tiles_per_seg = 0, part_tiles = 0, n_parts = 1;
+    std::vector<uint32_t> k_steps;  // per stage: max merges over segments
+    DevMerge* d_merges = nullptr;
+    uint32_t* d_seg_begin = nullptr;
+    uint32_t* d_stage_begin = nullptr;
+    uint32_t* gnodes = nullptr;
+    uint32_t* counts = nullptr;
+    uint64_t* part_totals = nullptr;
+
+    MergeRunner() = default;
+    MergeRunner(const MergeRunner&) = delete;
+    MergeRunner& operator=(const MergeRunner&) = delete;
+    ~MergeRunner() {
+        for (void* p : {(void*)d_merges, (void*)d_seg_begin, (void*)d_stage_begin, (void*)gnodes,
+                        (void*)counts, (void*)part_totals})
+            if (p) cudaFree(p);
+    }
+
+    // Tiling: minimise the number of parts, then the words per thread.
+    marsit_status configure(int sm_count) {
+        k_steps.assign(dp.n_stages, 0);
+        for (uint32_t sl = 0; sl < n_seg; ++sl)
+            for (uint32_t st = 0; st < dp.n_stages; ++st) {
+                const uint32_t* sb = &dp.stage_begin[size_t(sl) * (dp.n_stages + 1)];
+                k_steps[st] = std::max(k_steps[st], sb[st + 1] - sb[st]);
+            }
+        const int forced = env_int("MARSIT_MERGE_WPT", 0);
+        uint64_t best_parts = ~0ull;
+        for (int w : {1, 2, 4, 8}) {
+            if (forced && w != forced) continue;
+            const size_t sm = size_t(std::max<uint32_t>(dp.max_slots, 1)) * w * kMergeThreads * 4;
+            if (sm > 160 * 1024) continue;
+            int occ = 0;
+            CUDA_TRY(merge_coop_occupancy(w, sm, &occ));
+            const uint64_t cap = uint64_t(occ) * sm_count;
+            const uint64_t tps = ceil_div(words_proc, uint64_t(w) * kMergeThreads);
+            const uint64_t pt = std::min<uint64_t>(tps, cap / n_seg);
+            if (pt == 0) continue;
+            const uint64_t parts = ceil_div(tps, pt);
+            if (parts < best_parts) {
+                best_parts = parts;
+                wpt = w;
+                smem = sm;
+                tiles_per_seg = uint32_t(tps);
+                part_tiles = uint32_t(pt);
+                n_parts = uint32_t(parts);
+            }
+        }
+        if (best_parts == ~0ull) return fail(MARSIT_EUNSUPPORTED, "merge tiles do not fit the device");
+        return MARSIT_OK;
+    }
+
+    marsit_status upload() {
+        const size_t nm = std::max<size_t>(dp.n_merges, 1);
+        CUDA_TRY(cudaMalloc(&d_merges, sizeof(DevMerge) * nm));
+        CUDA_TRY(cudaMemcpy(d_merges, dp.merges.data(), sizeof(DevMerge) * dp.n_merges,
+                            cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMalloc(&d_seg_begin, sizeof(uint32_t) * dp.seg_begin.size()));
+        CUDA_TRY(cudaMemcpy(d_seg_begin, dp.seg_begin.data(), sizeof(uint32_t) * dp.seg_begin.size(),
+                            cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMalloc(&d_stage_begin, sizeof(uint32_t) * dp.stage_begin.size()));
+        CUDA_TRY(cudaMemcpy(d_stage_begin, dp.stage_begin.data(),
+                            sizeof(uint32_t) * dp.stage_begin.size(), cudaMemcpyHostToDevice));
+        const uint32_t gmax = std::max<uint32_t>(dp.gmax, 1);
+        CUDA_TRY(cudaMalloc(&gnodes, sizeof(uint32_t) * size_t(n_seg) * gmax * wst));
+        uint32_t kmax = 1;
+        for (uint32_t k : k_steps) kmax = std::max(kmax, k);
+        CUDA_TRY(cudaMalloc(&counts, sizeof(uint32_t) * size_t(kmax) * n_seg * part_tiles));
+        CUDA_TRY(cudaMalloc(&part_totals, sizeof(uint64_t) * size_t(n_parts) * nm));
+        CUDA_TRY(cudaMemset(part_totals, 0, sizeof(uint64_t) * size_t(n_parts) * nm));
+        return MARSIT_OK;
+    }
+
+    marsit_status run(const uint32_t* leaves, uint32_t* agg, const uint32_t* coins, uint64_t seed,
+                      uint64_t round, cudaStream_t st, uint64_t* n_launch) {
+        CoopParams c{};
+        c.merges = d_merges;
+        c.seg_begin = d_seg_begin;
+        c.stage_begin = d_stage_begin;
+        c.n_stages = dp.n_stages;
+        c.n_seg = n_seg;
+        c.s_first = s_first;
+        c.tiles_per_seg = tiles_per_seg;
+        c.words_proc = words_proc;
+        c.wst = wst;
+        c.ml = ml;
+        c.max_slots = std::max<uint32_t>(dp.max_slots, 1);
+        c.n_parts = n_parts;
+        c.part_tiles = part_tiles;
+        c.n_merges = dp.n_merges;
+        c.seg_bits = L;
+        c.leaves = leaves;
+        c.gnodes = gnodes;
+        c.gmax = std::max<uint32_t>(dp.gmax, 1);
+        c.agg = agg;
+        c.coins = coins;
+        c.counts = counts;
+        c.part_totals = part_totals;
+        c.seed = seed;
+        c.round = round;
+        for (uint32_t stage = 0; stage < dp.n_stages; ++stage) {
+            if (k_steps[stage] == 0) continue;
+            c.stage = stage;
+            c.k_steps = k_steps[stage];
+            for (uint32_t part = 0; part < n_parts; ++part) {
+                c.part = part;
+                c.part_tile0 = part * part_tiles;
+                CUDA_TRY(launch_merge_coop(c, wpt, smem, st));
+                ++*n_launch;
+            }
+        }
+        return MARSIT_OK;
+    }
+};
 
 struct TimedPair {
     int phase;
@@ -172,32 +305,17 @@ struct marsit_ctx {
     size_t esize = 4;
     uint64_t D = 0, L = 0;
     uint32_t M = 0, S = 0, G = 1, rank = 0, ml = 0, s_own = 0, s_first = 0;
-    uint32_t words64 = 0, words_proc = 0, wst = 0, tiles_per_seg = 0;
+    uint32_t words64 = 0, words_proc = 0, wst = 0;
     int sm_count = 148;
     bool vec_ok = false;
     HostSchedule sched;
     Plan plan;
-    DevicePlan dp;
+    MergeRunner merge;
     // device buffers
-    uint32_t* bits = nullptr;   // [S][ml][wst]
-    uint32_t* recv = nullptr;   // [G][s_own][ml][wst]   (G > 1)
-    uint32_t* agg = nullptr;    // [S][wst]
-    uint32_t* gnodes = nullptr; // [s_own][gmax][wst]
-    DevMerge* d_merges = nullptr;
-    uint32_t* d_seg_begin = nullptr;
-    uint32_t* d_stage_begin = nullptr;
-    uint64_t* flags = nullptr;  // [n_merges][tiles_per_seg]
-    uint64_t* totals = nullptr; // [n_merges]
-    uint32_t* counter = nullptr;
+    uint32_t* bits = nullptr;  // [S][ml][wst]
+    uint32_t* recv = nullptr;  // [G][s_own][ml][wst]   (G > 1)
+    uint32_t* agg = nullptr;   // [S][wst]
     int* err = nullptr;
-    uint32_t tile_base = 0, epoch = 0;
-    int merge_grid = 0;
-    int merge_wpt = 2;      // packed u32 words per merge thread (tile = 256 * wpt words)
-    bool coop = false;      // cooperative merge kernel (flat plan) vs look-back (staged plan)
-    uint32_t coop_kmax = 0;
-    uint32_t* d_seg_count = nullptr;
-    uint32_t* coop_counts = nullptr;  // [kmax][s_own * tiles_per_seg]
-    size_t merge_smem = 0;
     int stream_grid = 0;   // generic grid-stride kernels
     int extract_grid = 0;  // persistent, one wave of resident CTAs
     int decode_grid = 0;
@@ -208,11 +326,10 @@ struct marsit_ctx {
     DenseOp* d_dense_ops = nullptr;
     uint16_t* d_dense_final = nullptr;
     uint32_t dense_n_ops = 0;
-    // coin precompute (aux stream, overlapped with the extract)
+    // coin precompute on the aux stream; two buffers: this round's and the
+    // next round's, computed speculatively for (seed, t + 1) during the decode
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr;
-    // two coin buffers: the current round's, and the next round's computed
-    // speculatively for (seed, t + 1) while this round's decode streams HBM
     uint32_t* coin_buf[2] = {nullptr, nullptr};
     cudaEvent_t ev_coin_done[2] = {nullptr, nullptr};
     struct CoinTag {
@@ -221,13 +338,9 @@ struct marsit_ctx {
     } coin_tag[2];
     int cur_coin = 0;
     bool coin_prefetch = true;
+    bool coins_pending = false;
     uint64_t coin_total_words = 0;
     int coin_grid_x = 1;
-    bool coins_pending = false;
-    // single GPU: merge of segment s (aux) pipelined with decode (caller stream)
-    bool pipeline = false;
-    cudaEvent_t ev_extract = nullptr;
-    std::vector<cudaEvent_t> ev_merge;
     // NCCL
     ncclComm_t comm = nullptr;
     // timing
@@ -238,26 +351,20 @@ struct marsit_ctx {
     uint64_t launches[MARSIT_N_PHASES] = {};
 
     ~marsit_ctx();
-    marsit_status begin_phase(int phase, cudaStream_t st, cudaEvent_t* a);
+    marsit_status begin_phase(cudaStream_t st, cudaEvent_t* a);
     marsit_status end_phase(int phase, cudaStream_t st, cudaEvent_t a, uint64_t n_launch);
-    marsit_status next_epoch();
 };
 
 marsit_ctx::~marsit_ctx() {
     if (device >= 0) cudaSetDevice(device);
-    for (void* p : {(void*)bits, (void*)recv, (void*)agg, (void*)gnodes, (void*)d_merges,
-                    (void*)d_seg_begin, (void*)d_stage_begin, (void*)flags, (void*)totals,
-                    (void*)counter, (void*)err, dense_send, dense_recv, dense_mean,
-                    (void*)d_seg_count, (void*)coop_counts,
-                    (void*)d_dense_ops, (void*)d_dense_final})
+    for (void* p : {(void*)bits, (void*)recv, (void*)agg, (void*)err, dense_send, dense_recv,
+                    dense_mean, (void*)d_dense_ops, (void*)d_dense_final})
         if (p) cudaFree(p);
     for (auto& tp : pending) {
         cudaEventDestroy(tp.a);
         cudaEventDestroy(tp.b);
     }
     for (auto e : event_pool) cudaEventDestroy(e);
-    if (ev_extract) cudaEventDestroy(ev_extract);
-    for (auto e : ev_merge) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);
     for (int b = 0; b < 2; ++b) {
         if (ev_coin_done[b]) cudaEventDestroy(ev_coin_done[b]);
@@ -267,7 +374,7 @@ marsit_ctx::~marsit_ctx() {
     if (comm) ncclCommDestroy(comm);
 }
 
-marsit_status marsit_ctx::begin_phase(int, cudaStream_t st, cudaEvent_t* a) {
+marsit_status marsit_ctx::begin_phase(cudaStream_t st, cudaEvent_t* a) {
     *a = nullptr;
     if (!timing) return MARSIT_OK;
     if (event_pool.empty()) {
@@ -296,15 +403,10 @@ marsit_status marsit_ctx::end_phase(int phase, cudaStream_t st, cudaEvent_t a, u
     return MARSIT_OK;
 }
 
-marsit_status marsit_ctx::next_epoch() {
-    if (++epoch >= (1u << 24)) {
-        CUDA_TRY(cudaMemset(flags, 0, sizeof(uint64_t) * size_t(dp.n_merges + 1) * tiles_per_seg));
-        epoch = 1;
-    }
-    return MARSIT_OK;
-}
-
 namespace {
+
+enum Phase { kPhExtract = 0, kPhExchange, kPhMerge, kPhAllgather, kPhDecode, kPhExport, kPhDense,
+             kPhCoins };
 
 template <typename T>
 StreamParams<T> stream_params(marsit_ctx* ctx, const void* const* g, const void* const* c,
@@ -317,6 +419,8 @@ StreamParams<T> stream_params(marsit_ctx* ctx, const void* const* g, const void*
     }
     p.ml = ctx->ml;
     p.n_seg = ctx->S;
+    p.seg0 = 0;
+    p.n_proc = ctx->S;
     p.dim = ctx->D;
     p.seg_len = ctx->L;
     p.words_proc = ctx->words_proc;
@@ -345,30 +449,28 @@ marsit_status check_ptrs(const marsit_ctx* ctx, const void* const* a, const char
     return MARSIT_OK;
 }
 
+// K1 over all segments of the local workers.
 marsit_status run_extract(marsit_ctx* ctx, const void* const* g, const void* const* c,
-                          uint32_t seg0, uint32_t n, cudaStream_t st) {
+                          cudaStream_t st) {
     cudaEvent_t ev;
-    marsit_status s = ctx->begin_phase(0, st, &ev);
+    marsit_status s = ctx->begin_phase(st, &ev);
     if (s) return s;
     const bool vec = vec_ok_ptrs(ctx, g, c);
-    if (ctx->dtype == MARSIT_F32) {
-        auto p = stream_params<float>(ctx, g, c, nullptr, nullptr, 0.0);
-        p.seg0 = seg0;
-        p.n_proc = n;
-        CUDA_TRY(launch_extract(p, vec, ctx->extract_grid, st));
-    } else {
-        auto p = stream_params<double>(ctx, g, c, nullptr, nullptr, 0.0);
-        p.seg0 = seg0;
-        p.n_proc = n;
-        CUDA_TRY(launch_extract(p, vec, ctx->extract_grid, st));
-    }
-    return ctx->end_phase(0, st, ev, 1);
+    if (ctx->dtype == MARSIT_F32)
+        CUDA_TRY(launch_extract(stream_params<float>(ctx, g, c, nullptr, nullptr, 0.0), vec,
+                                ctx->extract_grid, st));
+    else
+        CUDA_TRY(launch_extract(stream_params<double>(ctx, g, c, nullptr, nullptr, 0.0), vec,
+                                ctx->extract_grid, st));
+    return ctx->end_phase(kPhExtract, st, ev, 1);
 }
 
+// NCCL all-to-all of the packed segments: destination q receives this rank's
+// local workers' bits of the segments it owns (one contiguous block).
 marsit_status run_exchange(marsit_ctx* ctx, cudaStream_t st) {
     if (ctx->G == 1) return MARSIT_OK;
     cudaEvent_t ev;
-    marsit_status s = ctx->begin_phase(1, st, &ev);
+    marsit_status s = ctx->begin_phase(st, &ev);
     if (s) return s;
     const size_t block = size_t(ctx->s_own) * ctx->ml * ctx->wst;  // u32 words per destination
     NCCL_TRY(ncclGroupStart());
@@ -377,119 +479,9 @@ marsit_status run_exchange(marsit_ctx* ctx, cudaStream_t st) {
         NCCL_TRY(ncclRecv(ctx->recv + q * block, block, ncclUint32, int(q), ctx->comm, st));
     }
     NCCL_TRY(ncclGroupEnd());
-    return ctx->end_phase(1, st, ev, 0);
+    return ctx->end_phase(kPhExchange, st, ev, 0);
 }
 
-// Merge owned segments [seg0, seg0 + n) (indices relative to the rank's
-// first owned segment): one launch per plan stage.
-marsit_status run_merge(marsit_ctx* ctx, uint64_t seed, uint64_t round, uint32_t seg0, uint32_t n,
-                        cudaStream_t st) {
-    if (ctx->coins_pending) {
-        CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_coin_done[ctx->cur_coin], 0));
-        ctx->coins_pending = false;
-    }
-    cudaEvent_t ev;
-    marsit_status s = ctx->begin_phase(2, st, &ev);
-    if (s) return s;
-    if (ctx->coop) {
-        CoopParams c{};
-        c.merges = ctx->d_merges;
-        c.seg_begin = ctx->d_seg_begin;
-        c.seg_count = ctx->d_seg_count;
-        c.n_seg = ctx->s_own;
-        c.s_first = ctx->s_first;
-        c.tiles_per_seg = ctx->tiles_per_seg;
-        c.words_proc = ctx->words_proc;
-        c.wst = ctx->wst;
-        c.ml = ctx->ml;
-        c.max_slots = std::max<uint32_t>(ctx->dp.max_slots, 1);
-        c.k_max = ctx->coop_kmax;
-        c.seg_bits = ctx->L;
-        c.leaves = ctx->G == 1 ? ctx->bits : ctx->recv;
-        c.agg = ctx->agg;
-        c.coins = ctx->coin_buf[ctx->cur_coin];
-        c.counts = ctx->coop_counts;
-        c.totals = ctx->totals;
-        c.seed = seed;
-        c.round = round;
-        (void)seg0;
-        (void)n;
-        CUDA_TRY(launch_merge_coop(c, ctx->merge_wpt, ctx->merge_smem, st));
-        return ctx->end_phase(2, st, ev, 1);
-    }
-    MergeParams p{};
-    p.merges = ctx->d_merges;
-    p.seg_begin = ctx->d_seg_begin;
-    p.stage_begin = ctx->d_stage_begin;
-    p.n_stages = ctx->dp.n_stages;
-    p.n_seg = ctx->s_own;
-    p.s_first = ctx->s_first;
-    p.seg0 = seg0;
-    p.n_proc = n;
-    p.tiles_per_seg = ctx->tiles_per_seg;
-    p.words_proc = ctx->words_proc;
-    p.wst = ctx->wst;
-    p.ml = ctx->ml;
-    p.seg_bits = ctx->L;
-    p.leaves = ctx->G == 1 ? ctx->bits : ctx->recv;
-    p.gnodes = ctx->gnodes;
-    p.gmax = std::max<uint32_t>(ctx->dp.gmax, 1);
-    p.agg = ctx->agg;
-    p.flags = ctx->flags;
-    p.totals = ctx->totals;
-    p.coins = ctx->coin_buf[ctx->cur_coin];
-    p.tile_counter = ctx->counter;
-    p.seed = seed;
-    p.round = round;
-    p.max_slots = std::max<uint32_t>(ctx->dp.max_slots, 1);
-    const uint32_t total_tiles = n * ctx->tiles_per_seg;
-    const int grid = int(std::min<uint64_t>(total_tiles, uint64_t(ctx->merge_grid)));
-    for (uint32_t stage = 0; stage < ctx->dp.n_stages; ++stage) {
-        s = ctx->next_epoch();
-        if (s) return s;
-        p.stage = stage;
-        p.epoch = ctx->epoch;
-        p.tile_base = ctx->tile_base;
-        CUDA_TRY(launch_merge(p, ctx->merge_wpt, grid, ctx->merge_smem, st));
-        ctx->tile_base += total_tiles + uint32_t(grid);
-    }
-    return ctx->end_phase(2, st, ev, ctx->dp.n_stages);
-}
-
-marsit_status run_allgather(marsit_ctx* ctx, cudaStream_t st) {
-    if (ctx->G == 1) return MARSIT_OK;
-    cudaEvent_t ev;
-    marsit_status s = ctx->begin_phase(3, st, &ev);
-    if (s) return s;
-    const size_t block = size_t(ctx->s_own) * ctx->wst;
-    NCCL_TRY(ncclAllGather(ctx->agg + ctx->rank * block, ctx->agg, block, ncclUint32, ctx->comm, st));
-    return ctx->end_phase(3, st, ev, 0);
-}
-
-marsit_status run_decode(marsit_ctx* ctx, const void* const* g, const void* const* c,
-                         void* const* c_out, void* update, double eta, uint32_t seg0, uint32_t n,
-                         cudaStream_t st) {
-    cudaEvent_t ev;
-    marsit_status s = ctx->begin_phase(4, st, &ev);
-    if (s) return s;
-    const bool vec = vec_ok_ptrs(ctx, g, c) && vec_ok_ptrs(ctx, (const void* const*)c_out, c) &&
-                     (!update || aligned16(update));
-    if (ctx->dtype == MARSIT_F32) {
-        auto p = stream_params<float>(ctx, g, c, c_out, update, eta);
-        p.seg0 = seg0;
-        p.n_proc = n;
-        CUDA_TRY(launch_decode(p, vec, ctx->decode_grid, st));
-    } else {
-        auto p = stream_params<double>(ctx, g, c, c_out, update, eta);
-        p.seg0 = seg0;
-        p.n_proc = n;
-        CUDA_TRY(launch_decode(p, vec, ctx->decode_grid, st));
-    }
-    return ctx->end_phase(4, st, ev, 1);
-}
-
-// Coin precompute on the aux stream, forked from `st` so it overlaps the
-// (HBM-bound) sign extraction; run_merge joins it.
 // Launch the coin kernel for (seed, round) into buffer b on the aux stream,
 // forked from `st` at this point of its work.
 marsit_status launch_coin_buffer(marsit_ctx* ctx, int b, uint64_t seed, uint64_t round,
@@ -497,11 +489,11 @@ marsit_status launch_coin_buffer(marsit_ctx* ctx, int b, uint64_t seed, uint64_t
     CUDA_TRY(cudaEventRecord(ctx->ev_fork, st));
     CUDA_TRY(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
     cudaEvent_t ev;
-    marsit_status s = ctx->begin_phase(7, ctx->aux, &ev);
+    marsit_status s = ctx->begin_phase(ctx->aux, &ev);
     if (s) return s;
-    CUDA_TRY(launch_coins(ctx->d_merges, ctx->dp.n_merges, seed, round, ctx->coin_buf[b],
-                          ctx->coin_grid_x, ctx->aux));
-    if ((s = ctx->end_phase(7, ctx->aux, ev, 1))) return s;
+    CUDA_TRY(launch_coins(ctx->merge.d_merges, ctx->merge.dp.n_merges, seed, round,
+                          ctx->coin_buf[b], ctx->coin_grid_x, ctx->aux));
+    if ((s = ctx->end_phase(kPhCoins, ctx->aux, ev, 1))) return s;
     CUDA_TRY(cudaEventRecord(ctx->ev_coin_done[b], ctx->aux));
     ctx->coin_tag[b] = {true, seed, round};
     return MARSIT_OK;
@@ -509,7 +501,6 @@ marsit_status launch_coin_buffer(marsit_ctx* ctx, int b, uint64_t seed, uint64_t
 
 // Coins of this round: reuse the speculatively prefetched buffer when its tag
 // matches (seed, round); otherwise compute them now, overlapping the extract.
-// run_merge joins them.
 marsit_status run_coins(marsit_ctx* ctx, uint64_t seed, uint64_t round, cudaStream_t st) {
     if (ctx->coin_total_words == 0) return MARSIT_OK;
     for (int b = 0; b < 2; ++b)
@@ -534,14 +525,55 @@ marsit_status prefetch_coins(marsit_ctx* ctx, uint64_t seed, uint64_t round, cud
     return launch_coin_buffer(ctx, 1 - ctx->cur_coin, seed, round + 1, st);
 }
 
+marsit_status run_merge(marsit_ctx* ctx, uint64_t seed, uint64_t round, cudaStream_t st) {
+    if (ctx->coins_pending) {
+        CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_coin_done[ctx->cur_coin], 0));
+        ctx->coins_pending = false;
+    }
+    cudaEvent_t ev;
+    marsit_status s = ctx->begin_phase(st, &ev);
+    if (s) return s;
+    uint64_t n = 0;
+    if ((s = ctx->merge.run(ctx->G == 1 ? ctx->bits : ctx->recv, ctx->agg,
+                            ctx->coin_buf[ctx->cur_coin], seed, round, st, &n)))
+        return s;
+    return ctx->end_phase(kPhMerge, st, ev, n);
+}
+
+marsit_status run_allgather(marsit_ctx* ctx, cudaStream_t st) {
+    if (ctx->G == 1) return MARSIT_OK;
+    cudaEvent_t ev;
+    marsit_status s = ctx->begin_phase(st, &ev);
+    if (s) return s;
+    const size_t block = size_t(ctx->s_own) * ctx->wst;
+    NCCL_TRY(ncclAllGather(ctx->agg + ctx->rank * block, ctx->agg, block, ncclUint32, ctx->comm, st));
+    return ctx->end_phase(kPhAllgather, st, ev, 0);
+}
+
+marsit_status run_decode(marsit_ctx* ctx, const void* const* g, const void* const* c,
+                         void* const* c_out, void* update, double eta, cudaStream_t st) {
+    cudaEvent_t ev;
+    marsit_status s = ctx->begin_phase(st, &ev);
+    if (s) return s;
+    const bool vec = vec_ok_ptrs(ctx, g, c) && vec_ok_ptrs(ctx, (const void* const*)c_out, c) &&
+                     (!update || aligned16(update));
+    if (ctx->dtype == MARSIT_F32)
+        CUDA_TRY(launch_decode(stream_params<float>(ctx, g, c, c_out, update, eta), vec,
+                               ctx->decode_grid, st));
+    else
+        CUDA_TRY(launch_decode(stream_params<double>(ctx, g, c, c_out, update, eta), vec,
+                               ctx->decode_grid, st));
+    return ctx->end_phase(kPhDecode, st, ev, 1);
+}
+
 marsit_status run_export(marsit_ctx* ctx, uint64_t* out, cudaStream_t st) {
     if (!out) return MARSIT_OK;
     cudaEvent_t ev;
-    marsit_status s = ctx->begin_phase(5, st, &ev);
+    marsit_status s = ctx->begin_phase(st, &ev);
     if (s) return s;
     CUDA_TRY(launch_export_bits(ctx->agg, ctx->wst, ctx->D, ctx->L,
                                 reinterpret_cast<uint32_t*>(out), st));
-    return ctx->end_phase(5, st, ev, 1);
+    return ctx->end_phase(kPhExport, st, ev, 1);
 }
 
 marsit_status check_consensus(const marsit_ctx* ctx, bool need_full_count) {
@@ -558,7 +590,7 @@ template <typename T>
 marsit_status dense_round_impl(marsit_ctx* ctx, const void* const* g, const void* const* c,
                                void* const* c_out, void* mean, cudaStream_t st) {
     cudaEvent_t ev;
-    marsit_status s = ctx->begin_phase(6, st, &ev);
+    marsit_status s = ctx->begin_phase(st, &ev);
     if (s) return s;
     DenseParams<T> p{};
     p.ops = ctx->d_dense_ops;
@@ -614,7 +646,34 @@ marsit_status dense_round_impl(marsit_ctx* ctx, const void* const* g, const void
     }
     for (uint32_t w = 0; w < ctx->ml; ++w)
         CUDA_TRY(cudaMemsetAsync(c_out[w], 0, ctx->D * sizeof(T), st));  // sync.hpp:83-85
-    return ctx->end_phase(6, st, ev, launches);
+    return ctx->end_phase(kPhDense, st, ev, launches);
+}
+
+// Coin precompute budget per merge: frac * L draws per use of its (receiver,
+// segment) stream (a continuation merge starts after the earlier merges'
+// draws).  Draws beyond it are computed inline by K2, so the budget only
+// trades memory/ALU for the rare over-budget case.
+void assign_coin_budget(DevicePlan& dp, uint32_t n_seg, uint64_t L, double frac,
+                        uint64_t* total_words, uint64_t* max_words) {
+    uint64_t off = 0, mx = 0;
+    for (uint32_t sl = 0; sl < n_seg; ++sl) {
+        const uint32_t mb = dp.seg_begin[sl];
+        const uint32_t me = sl + 1 < n_seg ? dp.seg_begin[sl + 1] : dp.n_merges;
+        for (uint32_t k = mb; k < me; ++k) {
+            DevMerge& d = dp.merges[k];
+            uint32_t depth = 0;
+            for (int32_t src = d.offset_src; src >= 0; src = dp.merges[mb + src].offset_src) ++depth;
+            const double want = frac * double(L) * (depth + 1);
+            uint64_t words = frac > 0 ? ceil_div(uint64_t(want) + 1, 32) : 0;
+            words = std::min<uint64_t>(words, ceil_div(L * (depth + 1), 32));
+            d.coin_words = uint32_t(words);
+            d.coin_off = off;
+            off += round_up(words, 64);  // whole 64-word chunks (coins_kernel)
+            mx = std::max(mx, words);
+        }
+    }
+    *total_words = off;
+    *max_words = mx;
 }
 
 }  // namespace
@@ -734,10 +793,9 @@ marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out) {
     if (hs.workers / G > kMaxLocalWorkers)
         return fail(MARSIT_EUNSUPPORTED, "too many workers per rank (max 64)");
     if (G > 1 && !desc->nccl_id) return fail(MARSIT_EPARAM, "nccl_id required for nranks > 1");
-
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    if (!have_device())
         return fail(MARSIT_ECUDA, "no CUDA device available (this library has no CPU path)");
+
     auto ctx = std::make_unique<marsit_ctx>();
     ctx->device = desc->device;
     CUDA_TRY(cudaSetDevice(desc->device));
@@ -761,56 +819,22 @@ marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out) {
     ctx->wst = uint32_t(round_up(ctx->words_proc, 32));
     ctx->vec_ok = (ctx->L % 4) == 0;
 
-    // Merge kernel choice.  Preferred: the cooperative kernel (all tiles of
-    // all owned segments co-resident, one grid barrier per merge step) with
-    // the smallest words-per-thread that fits the GPU; it runs the flat
-    // (single-stage) plan.  Otherwise (huge segments, or MARSIT_MERGE=lookback)
-    // the decoupled look-back kernel with the staged plan.
-    marsit_status st;
-    {
-        const char* mode = std::getenv("MARSIT_MERGE");
-        const bool want_coop = !(mode && std::string(mode) == "lookback");
-        if (want_coop) {
-            Plan flat = ctx->plan;
-            flat.n_stages = 1;
-            for (auto& sp : flat.seg)
-                for (auto& m : sp.merges) m.stage = 0;
-            DevicePlan dpf;
-            if ((st = lower_plan(flat, ctx->s_first, ctx->s_own, dpf))) return st;
-            for (int wpt : {1, 2, 4, 8, 16}) {
-                const uint64_t tps = ceil_div(ctx->words_proc, uint64_t(wpt) * kMergeThreads);
-                const uint64_t tiles = tps * ctx->s_own;
-                const size_t smem = size_t(std::max<uint32_t>(dpf.max_slots, 1)) * wpt *
-                                    kMergeThreads * sizeof(uint32_t);
-                if (smem > 160 * 1024) break;
-                int occ = 0;
-                CUDA_TRY(merge_coop_occupancy(wpt, smem, &occ));
-                if (tiles <= uint64_t(occ) * ctx->sm_count) {
-                    ctx->coop = true;
-                    ctx->merge_wpt = wpt;
-                    ctx->merge_smem = smem;
-                    ctx->tiles_per_seg = uint32_t(tps);
-                    ctx->dp = std::move(dpf);
-                    break;
-                }
-            }
-        }
-        if (!ctx->coop) {
-            if ((st = lower_plan(ctx->plan, ctx->s_first, ctx->s_own, ctx->dp))) return st;
-            // look-back kernel: one CTA tile = 256 threads x WPT packed words; WPT = 2
-            // unless that leaves fewer tiles than resident CTA slots, then WPT = 1
-            ctx->merge_smem = size_t(std::max<uint32_t>(ctx->dp.max_slots, 1)) * kMergeThreads * 8;
-            CUDA_TRY(merge_kernel_set_smem(ctx->merge_smem));
-            int occ = 0;
-            CUDA_TRY(merge_kernel_occupancy(ctx->merge_smem, &occ));
-            if (const char* e = std::getenv("MARSIT_MERGE_CTAS")) occ = std::min(occ, std::atoi(e));
-            ctx->merge_grid = std::max(1, occ) * ctx->sm_count;
-            const uint64_t tiles2 = ceil_div(ctx->words_proc, 2 * kMergeThreads) * ctx->s_own;
-            ctx->merge_wpt = tiles2 >= uint64_t(ctx->merge_grid) ? 2 : 1;
-            ctx->tiles_per_seg =
-                uint32_t(ceil_div(ctx->words_proc, uint64_t(ctx->merge_wpt) * kMergeThreads));
-        }
-    }
+    // merge plan, coin budget, tiling
+    MergeRunner& mr = ctx->merge;
+    marsit_status st = lower_plan(ctx->plan, ctx->s_first, ctx->s_own, mr.dp);
+    if (st) return st;
+    mr.n_seg = ctx->s_own;
+    mr.s_first = ctx->s_first;
+    mr.words_proc = ctx->words_proc;
+    mr.wst = ctx->wst;
+    mr.ml = ctx->ml;
+    mr.L = ctx->L;
+    double frac = 0.53;
+    if (const char* e = std::getenv("MARSIT_COIN_FRAC")) frac = std::atof(e);
+    uint64_t max_words = 0;
+    assign_coin_budget(mr.dp, ctx->s_own, ctx->L, frac, &ctx->coin_total_words, &max_words);
+    if ((st = mr.configure(ctx->sm_count))) return st;
+    if ((st = mr.upload())) return st;
 
     const size_t wst = ctx->wst;
     CUDA_TRY(cudaMalloc(&ctx->bits, sizeof(uint32_t) * ctx->S * ctx->ml * wst));
@@ -821,102 +845,33 @@ marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out) {
         CUDA_TRY(cudaMalloc(&ctx->recv, sizeof(uint32_t) * ctx->S * ctx->ml * wst));
         CUDA_TRY(cudaMemset(ctx->recv, 0, sizeof(uint32_t) * ctx->S * ctx->ml * wst));
     }
-    const uint32_t gmax = std::max<uint32_t>(ctx->dp.gmax, 1);
-    CUDA_TRY(cudaMalloc(&ctx->gnodes, sizeof(uint32_t) * ctx->s_own * gmax * wst));
-    {
-        // Coin precompute budget per merge: frac * L draws per use of its
-        // (receiver, segment) stream (a continuation merge starts after the
-        // earlier merges' draws).  Draws beyond it are computed inline, so
-        // the budget only trades memory/ALU for the rare over-budget case.
-        double frac = 0.53;
-        if (const char* e = std::getenv("MARSIT_COIN_FRAC")) frac = std::atof(e);
-        uint64_t off = 0;
-        for (uint32_t sl = 0; sl < ctx->s_own; ++sl) {
-            const uint32_t mb = ctx->dp.seg_begin[sl];
-            const uint32_t me = sl + 1 < ctx->s_own ? ctx->dp.seg_begin[sl + 1] : ctx->dp.n_merges;
-            for (uint32_t k = mb; k < me; ++k) {
-                DevMerge& d = ctx->dp.merges[k];
-                uint32_t depth = 0;
-                for (int32_t src = d.offset_src; src >= 0; src = ctx->dp.merges[mb + src].offset_src)
-                    ++depth;
-                const double want = frac * double(ctx->L) * (depth + 1);
-                uint64_t words = frac > 0 ? ceil_div(uint64_t(want) + 1, 32) : 0;
-                words = std::min<uint64_t>(words, ceil_div(ctx->L * (depth + 1), 32));
-                d.coin_words = uint32_t(words);
-                d.coin_off = off;
-                off += round_up(words, 64);  // whole 64-word chunks (coins_kernel)
-            }
-        }
-        ctx->coin_total_words = off;
-        if (off)
-            for (int b = 0; b < 2; ++b) {
-                CUDA_TRY(cudaMalloc(&ctx->coin_buf[b], sizeof(uint32_t) * off));
-                CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_coin_done[b], cudaEventDisableTiming));
-            }
-        if (const char* e = std::getenv("MARSIT_COIN_PREFETCH")) ctx->coin_prefetch = std::atoi(e) != 0;
-        uint64_t max_words = 0;
-        for (auto& d : ctx->dp.merges) max_words = std::max<uint64_t>(max_words, d.coin_words);
-        // MARSIT_COIN_CTAS (default 4) CTAs per SM in total, split across the
-        // merges (one warp per 64-word chunk)
-        const char* ce = std::getenv("MARSIT_COIN_CTAS");
-        const uint64_t coin_ctas = ce ? std::max(1, std::atoi(ce)) : 4;
-        ctx->coin_grid_x = int(std::max<uint64_t>(
-            1, std::min<uint64_t>(ceil_div(max_words, 64 * 8),
-                                  ceil_div(coin_ctas * ctx->sm_count,
-                                           std::max<uint32_t>(ctx->dp.n_merges, 1)))));
-        CUDA_TRY(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
-        CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
-
-    }
-    if (G == 1 && ctx->S >= 2 && !ctx->coop && std::getenv("MARSIT_PIPELINE") != nullptr) {
-        ctx->pipeline = true;
-        CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_extract, cudaEventDisableTiming));
-        ctx->ev_merge.resize(ctx->S);
-        for (auto& e : ctx->ev_merge) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
-    CUDA_TRY(cudaMalloc(&ctx->d_merges, sizeof(DevMerge) * std::max<size_t>(ctx->dp.n_merges, 1)));
-    CUDA_TRY(cudaMemcpy(ctx->d_merges, ctx->dp.merges.data(), sizeof(DevMerge) * ctx->dp.n_merges,
-                        cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMalloc(&ctx->d_seg_begin, sizeof(uint32_t) * ctx->dp.seg_begin.size()));
-    CUDA_TRY(cudaMemcpy(ctx->d_seg_begin, ctx->dp.seg_begin.data(),
-                        sizeof(uint32_t) * ctx->dp.seg_begin.size(), cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMalloc(&ctx->d_stage_begin, sizeof(uint32_t) * ctx->dp.stage_begin.size()));
-    CUDA_TRY(cudaMemcpy(ctx->d_stage_begin, ctx->dp.stage_begin.data(),
-                        sizeof(uint32_t) * ctx->dp.stage_begin.size(), cudaMemcpyHostToDevice));
-    if (ctx->coop) {
-        std::vector<uint32_t> cnt(ctx->s_own);
-        for (uint32_t sl = 0; sl < ctx->s_own; ++sl) {
-            const uint32_t mb = ctx->dp.seg_begin[sl];
-            const uint32_t me = sl + 1 < ctx->s_own ? ctx->dp.seg_begin[sl + 1] : ctx->dp.n_merges;
-            cnt[sl] = me - mb;
-            ctx->coop_kmax = std::max(ctx->coop_kmax, cnt[sl]);
-        }
-        CUDA_TRY(cudaMalloc(&ctx->d_seg_count, sizeof(uint32_t) * cnt.size()));
-        CUDA_TRY(cudaMemcpy(ctx->d_seg_count, cnt.data(), sizeof(uint32_t) * cnt.size(),
-                            cudaMemcpyHostToDevice));
-        CUDA_TRY(cudaMalloc(&ctx->coop_counts, sizeof(uint32_t) * std::max<uint64_t>(1, ctx->coop_kmax) *
-                                                   ctx->s_own * ctx->tiles_per_seg));
-    }
-    const size_t nflags = size_t(ctx->dp.n_merges + 1) * ctx->tiles_per_seg;
-    CUDA_TRY(cudaMalloc(&ctx->flags, sizeof(uint64_t) * nflags));
-    CUDA_TRY(cudaMemset(ctx->flags, 0, sizeof(uint64_t) * nflags));
-    CUDA_TRY(cudaMalloc(&ctx->totals, sizeof(uint64_t) * (ctx->dp.n_merges + 1)));
-    CUDA_TRY(cudaMemset(ctx->totals, 0, sizeof(uint64_t) * (ctx->dp.n_merges + 1)));
-    CUDA_TRY(cudaMalloc(&ctx->counter, sizeof(uint32_t)));
-    CUDA_TRY(cudaMemset(ctx->counter, 0, sizeof(uint32_t)));
     CUDA_TRY(cudaMalloc(&ctx->err, sizeof(int)));
     CUDA_TRY(cudaMemset(ctx->err, 0, sizeof(int)));
 
+    // coin buffers, aux stream
+    CUDA_TRY(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    if (ctx->coin_total_words)
+        for (int b = 0; b < 2; ++b) {
+            CUDA_TRY(cudaMalloc(&ctx->coin_buf[b], sizeof(uint32_t) * ctx->coin_total_words));
+            CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_coin_done[b], cudaEventDisableTiming));
+        }
+    ctx->coin_prefetch = env_int("MARSIT_COIN_PREFETCH", 1) != 0;
     {
-        // persistent grid-stride launches.  The HBM-bound kernels deliberately
-        // leave SM room (threads/registers) for the concurrently running coin
-        // and merge kernels; MARSIT_{EXTRACT,DECODE}_CTAS override per SM.
+        // MARSIT_COIN_CTAS (default 4) CTAs per SM in total, split across the
+        // merges (one warp per 64-word chunk)
+        const uint64_t coin_ctas = uint64_t(std::max(1, env_int("MARSIT_COIN_CTAS", 4)));
+        ctx->coin_grid_x = int(std::max<uint64_t>(
+            1, std::min<uint64_t>(ceil_div(max_words, 64 * 8),
+                                  ceil_div(coin_ctas * ctx->sm_count,
+                                           std::max<uint32_t>(mr.dp.n_merges, 1)))));
+    }
+    {
+        // persistent grid-stride streaming kernels; MARSIT_{EXTRACT,DECODE}_CTAS
+        // override the CTAs per SM.  The decode leaves SM room for the next
+        // round's coin kernel running underneath it.
         int ob_extract = 0, ob_decode = 0;
         CUDA_TRY(stream_occupancy(ctx->dtype == MARSIT_F64, &ob_extract, &ob_decode));
-        auto env_int = [](const char* name, int dflt) {
-            const char* e = std::getenv(name);
-            return e ? std::atoi(e) : dflt;
-        };
         const int want_e = env_int("MARSIT_EXTRACT_CTAS", 4);
         const int want_d = env_int("MARSIT_DECODE_CTAS", 2);
         ctx->extract_grid = std::max(1, std::min(ob_extract, want_e)) * ctx->sm_count;
@@ -941,9 +896,6 @@ marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out) {
                 if (k < sp.merges.size()) {
                     o.a = uint16_t(sp.merges[k].local_node);
                     o.b = uint16_t(sp.merges[k].recv_node);
-                } else {  // pad with a harmless op (result unused)
-                    o.a = 0;
-                    o.b = 0;
                 }
                 ops[size_t(sl) * n_ops + k] = o;
             }
@@ -993,31 +945,12 @@ marsit_status marsit_sign_round(marsit_ctx* ctx, uint64_t t, double eta_s, uint6
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     CUDA_TRY(cudaSetDevice(ctx->device));
     if ((s = run_coins(ctx, seed, t, st))) return s;
-    if ((s = run_extract(ctx, d_grads, d_comp, 0, ctx->S, st))) return s;
-    if (ctx->pipeline) {
-        // aux: M_0 M_1 ... (after the extract and the coins); st: D_s after M_s, so
-        // the ALU/latency-bound merges hide under the HBM-bound decode
-        CUDA_TRY(cudaEventRecord(ctx->ev_extract, st));
-        CUDA_TRY(cudaStreamWaitEvent(ctx->aux, ctx->ev_extract, 0));
-        if (ctx->coins_pending) ctx->coins_pending = false;  // aux is already ordered after them
-        for (uint32_t sg = 0; sg < ctx->S; ++sg) {
-            if ((s = run_merge(ctx, seed, t, sg, 1, ctx->aux))) return s;
-            CUDA_TRY(cudaEventRecord(ctx->ev_merge[sg], ctx->aux));
-        }
-        for (uint32_t sg = 0; sg < ctx->S; ++sg) {
-            CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_merge[sg], 0));
-            if ((s = run_decode(ctx, d_grads, d_comp, d_comp_out, d_update, eta_s, sg, 1, st)))
-                return s;
-        }
-        // st has now joined aux (it waited on the last merge event)
-    } else {
-        if ((s = run_exchange(ctx, st))) return s;
-        if ((s = run_merge(ctx, seed, t, 0, ctx->s_own, st))) return s;
-        if ((s = prefetch_coins(ctx, seed, t, st))) return s;
-        if ((s = run_allgather(ctx, st))) return s;
-        if ((s = run_decode(ctx, d_grads, d_comp, d_comp_out, d_update, eta_s, 0, ctx->S, st)))
-            return s;
-    }
+    if ((s = run_extract(ctx, d_grads, d_comp, st))) return s;
+    if ((s = run_exchange(ctx, st))) return s;
+    if ((s = run_merge(ctx, seed, t, st))) return s;
+    if ((s = prefetch_coins(ctx, seed, t, st))) return s;
+    if ((s = run_allgather(ctx, st))) return s;
+    if ((s = run_decode(ctx, d_grads, d_comp, d_comp_out, d_update, eta_s, st))) return s;
     return run_export(ctx, d_agg_bits, st);
 }
 
@@ -1062,7 +995,7 @@ marsit_status marsit_sign_extract(marsit_ctx* ctx, const void* const* d_grads,
     if ((s = check_ptrs(ctx, d_grads, "grads")) || (s = check_ptrs(ctx, d_comp, "comp"))) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     CUDA_TRY(cudaSetDevice(ctx->device));
-    if ((s = run_extract(ctx, d_grads, d_comp, 0, ctx->S, st))) return s;
+    if ((s = run_extract(ctx, d_grads, d_comp, st))) return s;
     const size_t row = size_t(ctx->words64) * 8;
     for (uint32_t w = 0; w < ctx->ml; ++w)
         CUDA_TRY(cudaMemcpy2DAsync(d_signs_out + size_t(w) * ctx->S * ctx->words64, row,
@@ -1086,7 +1019,7 @@ marsit_status marsit_allreduce_sign(marsit_ctx* ctx, uint64_t round, uint64_t se
                                    cudaMemcpyDeviceToDevice, st));
     if ((s = run_coins(ctx, seed, round, st))) return s;
     if ((s = run_exchange(ctx, st))) return s;
-    if ((s = run_merge(ctx, seed, round, 0, ctx->s_own, st))) return s;
+    if ((s = run_merge(ctx, seed, round, st))) return s;
     if ((s = run_allgather(ctx, st))) return s;
     CUDA_TRY(cudaMemcpy2DAsync(d_out, row, ctx->agg, size_t(ctx->wst) * 4, row, ctx->S,
                                cudaMemcpyDeviceToDevice, st));
@@ -1095,45 +1028,33 @@ marsit_status marsit_allreduce_sign(marsit_ctx* ctx, uint64_t round, uint64_t se
     return MARSIT_OK;
 }
 
+// merge_signs (merge.hpp:34-58) as a one-merge plan through the same
+// cooperative kernel: leaves = [received, local], explicit stream key, the
+// stream's earlier draws as base, coins drawn inline.
 marsit_status marsit_merge_signs(const uint64_t* d_recv, uint32_t c_recv, const uint64_t* d_local,
                                  uint32_t c_local, uint64_t len, uint64_t key, uint64_t used,
                                  uint64_t* d_out, uint64_t* consumed, int device, void* stream) {
-    // merge.hpp:42-47 validation order: length is implied equal here.
     if (c_recv == 0 || c_local == 0)
         return fail(MARSIT_EPARAM, "merge_signs: aggregate count must be >= 1");
     if (!d_recv || !d_local || !d_out) return fail(MARSIT_EPARAM, "null argument");
-    if (len == 0) return MARSIT_OK;
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    if (len == 0) {
+        if (consumed) *consumed = 0;
+        return MARSIT_OK;
+    }
+    if (!have_device())
         return fail(MARSIT_ECUDA, "no CUDA device available (this library has no CPU path)");
     CUDA_TRY(cudaSetDevice(device));
+    int sm = 148;
+    CUDA_TRY(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const uint64_t words64 = ceil_div(len, 64);
-    const uint32_t words_proc = uint32_t(round_up(2 * words64, 4));
-    const uint32_t wst = uint32_t(round_up(words_proc, 32));
-    const uint32_t tiles = uint32_t(ceil_div(words_proc, 2 * kMergeThreads));
-    // scratch: leaves [2][wst], agg [wst], flags [tiles], totals, counter, plan
-    struct Scratch {
-        void* p = nullptr;
-        ~Scratch() {
-            if (p) cudaFree(p);
-        }
-    } scratch;
-    const size_t leaves_b = sizeof(uint32_t) * 2 * wst, agg_b = sizeof(uint32_t) * wst;
-    const size_t flags_b = sizeof(uint64_t) * tiles;
-    const size_t total_b = leaves_b + agg_b + flags_b + 64 + sizeof(DevMerge) + 64;
-    CUDA_TRY(cudaMalloc(&scratch.p, total_b));
-    char* base = static_cast<char*>(scratch.p);
-    CUDA_TRY(cudaMemsetAsync(base, 0, total_b, st));
-    uint32_t* leaves = reinterpret_cast<uint32_t*>(base);
-    uint32_t* agg = reinterpret_cast<uint32_t*>(base + leaves_b);
-    uint64_t* flags = reinterpret_cast<uint64_t*>(base + leaves_b + agg_b);
-    uint64_t* totals = reinterpret_cast<uint64_t*>(base + leaves_b + agg_b + flags_b);
-    uint32_t* counter = reinterpret_cast<uint32_t*>(base + leaves_b + agg_b + flags_b + 16);
-    uint32_t* meta = reinterpret_cast<uint32_t*>(base + leaves_b + agg_b + flags_b + 32);
-    DevMerge* dm = reinterpret_cast<DevMerge*>(base + leaves_b + agg_b + flags_b + 64);
-    CUDA_TRY(cudaMemcpyAsync(leaves, d_recv, words64 * 8, cudaMemcpyDeviceToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(leaves + wst, d_local, words64 * 8, cudaMemcpyDeviceToDevice, st));
+    MergeRunner mr;
+    mr.n_seg = 1;
+    mr.s_first = 0;
+    mr.words_proc = uint32_t(round_up(2 * words64, 4));
+    mr.wst = uint32_t(round_up(mr.words_proc, 32));
+    mr.ml = 2;
+    mr.L = len;
     DevMerge m{};
     m.thresh11 = coin_threshold(c_recv, c_local) << 11;
     m.key = key;
@@ -1144,42 +1065,39 @@ marsit_status marsit_merge_signs(const uint64_t* d_recv, uint32_t c_recv, const 
     m.out_slot = kNone;
     m.out_global = kFinal;
     m.offset_src = -1;
-    const uint32_t host_meta[3] = {0, 0, 1};  // seg_begin[0]; stage_begin[0..1]
-    CUDA_TRY(cudaMemcpyAsync(dm, &m, sizeof(m), cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(meta, host_meta, sizeof(host_meta), cudaMemcpyHostToDevice, st));
-    MergeParams p{};
-    p.merges = dm;
-    p.seg_begin = meta;
-    p.stage_begin = meta + 1;
-    p.n_stages = 1;
-    p.stage = 0;
-    p.n_seg = 1;
-    p.s_first = 0;
-    p.seg0 = 0;
-    p.n_proc = 1;
-    p.tiles_per_seg = tiles;
-    p.words_proc = words_proc;
-    p.wst = wst;
-    p.ml = 2;
-    p.seg_bits = len;
-    p.leaves = leaves;
-    p.gnodes = agg;
-    p.gmax = 1;
-    p.agg = agg;
-    p.flags = flags;
-    p.totals = totals;
-    p.tile_counter = counter;
-    p.tile_base = 0;
-    p.epoch = 1;
-    p.max_slots = 1;
-    const size_t smem = kMergeThreads * 8;
-    const int grid = int(std::min<uint64_t>(tiles, 148 * 4));
-    CUDA_TRY(launch_merge(p, 2, grid, smem, st));
+    m.coin_words = 0;  // inline draws
+    mr.dp.merges = {m};
+    mr.dp.seg_begin = {0};
+    mr.dp.stage_begin = {0, 1};
+    mr.dp.n_stages = 1;
+    mr.dp.n_merges = 1;
+    marsit_status s;
+    if ((s = mr.configure(sm)) || (s = mr.upload())) return s;
+    struct Scratch {
+        void* p = nullptr;
+        ~Scratch() {
+            if (p) cudaFree(p);
+        }
+    } scratch;
+    const size_t leaves_b = sizeof(uint32_t) * 2 * mr.wst, agg_b = sizeof(uint32_t) * mr.wst;
+    CUDA_TRY(cudaMalloc(&scratch.p, leaves_b + agg_b));
+    uint32_t* leaves = static_cast<uint32_t*>(scratch.p);
+    uint32_t* agg = leaves + 2 * mr.wst;
+    CUDA_TRY(cudaMemsetAsync(scratch.p, 0, leaves_b + agg_b, st));
+    CUDA_TRY(cudaMemcpyAsync(leaves, d_recv, words64 * 8, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(leaves + mr.wst, d_local, words64 * 8, cudaMemcpyDeviceToDevice, st));
+    uint64_t n = 0;
+    if ((s = mr.run(leaves, agg, nullptr, 0, 0, st, &n))) return s;
     CUDA_TRY(cudaMemcpyAsync(d_out, agg, words64 * 8, cudaMemcpyDeviceToDevice, st));
-    uint64_t tot = 0;
-    CUDA_TRY(cudaMemcpyAsync(&tot, totals, sizeof(tot), cudaMemcpyDeviceToHost, st));
+    std::vector<uint64_t> tot(mr.n_parts);
+    CUDA_TRY(cudaMemcpyAsync(tot.data(), mr.part_totals, sizeof(uint64_t) * mr.n_parts,
+                             cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    if (consumed) *consumed = tot;
+    if (consumed) {
+        uint64_t c = 0;
+        for (uint64_t v : tot) c += v;
+        *consumed = c;
+    }
     return MARSIT_OK;
 }
 
