@@ -182,6 +182,66 @@ marsit_status marsit_ctx_timing(marsit_ctx* ctx, float* ms, uint64_t* launches, 
 marsit_status marsit_fill_recipe(int recipe, uint64_t seed, uint64_t worker, uint64_t round,
                                  uint64_t dim, marsit_dtype dtype, void* d_out, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Multi-step sync driver: the per-round synchronisation part of the
+ * reference trainer (trainer.hpp:184-307, Alg. 2) around marsit_round —
+ * compensation state owned on the device and carried across rounds
+ * (trainer.hpp:252), the round counter t, the dense cadence K, the identical
+ * parameter update x_w -= g_t on every replica fused into the decode
+ * (trainer.hpp:285-288), cumulative payload bits (trainer.hpp:278-279), and
+ * bucketing for large models.
+ *
+ * Buckets: coordinates [b*bucket_elems, min((b+1)*bucket_elems, D)) form an
+ * independent marsit_round with global seed
+ *     seed_b = seed                                   if there is one bucket
+ *     seed_b = mix(seed ^ ((b + 1) * 0x9e3779b97f4a7c15))  otherwise
+ * where mix is the SplitMix64 finalizer of rng.hpp:66-70.  The reference
+ * reproduces a bucketed round bucket by bucket with marsit_round(t, cfg,
+ * grads[b], comp[b], sched, seed_b).
+ * ---------------------------------------------------------------------- */
+typedef struct marsit_driver marsit_driver;
+
+typedef struct marsit_driver_desc {
+    uint64_t dim;                     /* D                                         */
+    const marsit_schedule* schedule;  /* M workers                                 */
+    marsit_dtype dtype;
+    int device;
+    uint32_t nranks, rank;            /* as marsit_ctx_desc                        */
+    const void* nccl_id;
+    uint64_t bucket_elems;            /* 0 = one bucket of D                       */
+    uint64_t period;                  /* K: dense every K-th round; 0 = never      */
+    double eta_s;                     /* > 0                                       */
+    uint64_t global_seed;
+    uint64_t first_round;             /* t of the first step (trainer starts at 0) */
+} marsit_driver_desc;
+
+marsit_status marsit_driver_create(const marsit_driver_desc* desc, marsit_driver** out);
+void marsit_driver_destroy(marsit_driver* drv);
+/* One round t (then t += 1): d_grads[i] = local worker i's scaled gradient
+ * (D elements).  d_params (optional): replica parameters, x -= g_t.
+ * d_update (optional): receives g_t.  *full_precision (optional). */
+marsit_status marsit_driver_step(marsit_driver* drv, const void* const* d_grads,
+                                 void* const* d_params, void* d_update, int* full_precision,
+                                 void* stream);
+/* Device pointer to local worker i's compensation (D elements). */
+marsit_status marsit_driver_compensation(marsit_driver* drv, uint32_t local_worker, void** d_comp);
+/* Next round index, cumulative payload bits, number of buckets. */
+marsit_status marsit_driver_state(const marsit_driver* drv, uint64_t* next_round,
+                                  uint64_t* cum_bits, uint32_t* n_buckets);
+/* Checkpoint / resume of the sync state (t, cumulative bits, every local
+ * worker's compensation) — state the reference's params-only checkpoint
+ * (checkpoint.hpp:18-91) does not keep.  Synchronises `stream`. */
+marsit_status marsit_driver_save(marsit_driver* drv, const char* path, void* stream);
+marsit_status marsit_driver_load(marsit_driver* drv, const char* path, void* stream);
+
+/* Parameters in the reference's checkpoint format (checkpoint.hpp:18-91:
+ * "marsit-ckpt\0", u32 version 1, u64 D, D little-endian doubles), from / to
+ * a device vector of dtype. */
+marsit_status marsit_write_params_checkpoint(const char* path, const void* d_params, uint64_t dim,
+                                             marsit_dtype dtype, void* stream);
+marsit_status marsit_read_params_checkpoint(const char* path, void* d_params, uint64_t dim,
+                                            marsit_dtype dtype, void* stream);
+
 /* ncclGetUniqueId for multi-rank contexts (128 bytes). */
 marsit_status marsit_nccl_unique_id(void* out128);
 

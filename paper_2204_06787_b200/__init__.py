@@ -19,7 +19,8 @@ __all__ = [
     "ParameterError", "NonFiniteError", "ProtocolError", "UnsupportedError", "CudaError",
     "NcclError", "Schedule", "build_ring_schedule", "build_torus_schedule", "SyncConfig",
     "CompensationState", "BitsAccount", "MarsitRoundResult", "AggregateSign", "Context",
-    "marsit_round", "allreduce_sign", "pack_signs", "merge_signs", "stream_key",
+    "marsit_round", "allreduce_sign", "pack_signs", "merge_signs", "stream_key", "Driver",
+    "write_params_checkpoint", "read_params_checkpoint",
 ]
 
 
@@ -415,6 +416,105 @@ def fill_recipe(out, recipe: int, seed: int, worker: int, round_: int) -> None:
     _check(N.lib().marsit_fill_recipe(recipe, seed, worker, round_, out.numel(),
                                       _dtype_code(out), C.c_void_p(out.data_ptr()),
                                       _stream_ptr(out.device.index or 0)))
+
+
+class Driver:
+    """Multi-step sync driver (marsit_driver_*): the per-round sync part of the
+    reference trainer (trainer.hpp:184-307) — device-resident compensation
+    carried across rounds, dense cadence K, fused replica update x -= g_t,
+    cumulative bits, buckets (seed_b = mix(seed ^ (b+1)*gamma) when > 1), and
+    checkpoint/resume of (t, cum_bits, compensation)."""
+
+    def __init__(self, dim: int, schedule: Schedule, *, eta_s: float, global_seed: int,
+                 period: Optional[int] = None, bucket_elems: int = 0, dtype=None,
+                 device: int = 0, first_round: int = 0, nranks: int = 1, rank: int = 0,
+                 nccl_id: Optional[bytes] = None):
+        import torch
+        dtype = dtype or torch.float32
+        if period == 0:
+            raise ParameterError("SyncConfig: full-precision period must be >= 1")
+        self.dim, self.schedule, self.device, self.dtype = int(dim), schedule, device, dtype
+        d = N.DriverDesc()
+        d.dim = self.dim
+        d.schedule = schedule._h
+        d.dtype = N.F32 if dtype == torch.float32 else N.F64
+        d.device = device
+        d.nranks = nranks
+        d.rank = rank
+        self._id_buf = None
+        if nccl_id is not None:
+            self._id_buf = C.create_string_buffer(bytes(nccl_id), 128)
+            d.nccl_id = C.cast(self._id_buf, C.c_void_p)
+        d.bucket_elems = bucket_elems
+        d.period = 0 if period is None else int(period)
+        d.eta_s = float(eta_s)
+        d.global_seed = global_seed
+        d.first_round = first_round
+        out = C.c_void_p()
+        _check(N.lib().marsit_driver_create(C.byref(d), C.byref(out)))
+        self._h = out
+        self.local_workers = schedule.workers // nranks
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        try:
+            if h is not None and h.value and N._lib is not None:
+                N._lib.marsit_driver_destroy(h)
+        except Exception:
+            pass
+        self._h = None
+
+    def step(self, grads, params=None, update=None):
+        g = N.ptr_array([x.data_ptr() for x in grads])
+        pp = N.ptr_array([x.data_ptr() for x in params]) if params is not None else None
+        full = C.c_int()
+        _check(N.lib().marsit_driver_step(
+            self._h, g, pp, C.c_void_p(update.data_ptr() if update is not None else None),
+            C.byref(full), _stream_ptr(self.device)))
+        return bool(full.value)
+
+    def compensation(self, i: int):
+        """A torch view of local worker i's device compensation (D elements)."""
+        import torch
+        ptr = C.c_void_p()
+        _check(N.lib().marsit_driver_compensation(self._h, i, C.byref(ptr)))
+        esize = 4 if self.dtype == torch.float32 else 8
+        return _device_view(ptr.value, self.dim, self.dtype, self.device, esize)
+
+    def state(self):
+        t, bits, nb = C.c_uint64(), C.c_uint64(), C.c_uint32()
+        _check(N.lib().marsit_driver_state(self._h, C.byref(t), C.byref(bits), C.byref(nb)))
+        return {"next_round": t.value, "cum_bits": bits.value, "buckets": nb.value}
+
+    def save(self, path: str):
+        _check(N.lib().marsit_driver_save(self._h, path.encode(), _stream_ptr(self.device)))
+
+    def load(self, path: str):
+        _check(N.lib().marsit_driver_load(self._h, path.encode(), _stream_ptr(self.device)))
+
+
+def _device_view(ptr: int, n: int, dtype, device: int, esize: int):
+    """Zero-copy torch tensor over device memory owned by the library."""
+    import torch
+
+    class _Holder:
+        __cuda_array_interface__ = {
+            "shape": (n,), "typestr": "<f4" if esize == 4 else "<f8",
+            "data": (ptr, False), "version": 3, "strides": None}
+    return torch.as_tensor(_Holder(), device=f"cuda:{device}")
+
+
+def write_params_checkpoint(path: str, params) -> None:
+    """Reference checkpoint format (checkpoint.hpp:18-91) from a device vector."""
+    _check(N.lib().marsit_write_params_checkpoint(path.encode(), C.c_void_p(params.data_ptr()),
+                                                  params.numel(), _dtype_code(params),
+                                                  _stream_ptr(params.device.index or 0)))
+
+
+def read_params_checkpoint(path: str, params) -> None:
+    _check(N.lib().marsit_read_params_checkpoint(path.encode(), C.c_void_p(params.data_ptr()),
+                                                 params.numel(), _dtype_code(params),
+                                                 _stream_ptr(params.device.index or 0)))
 
 
 def nccl_unique_id() -> bytes:

@@ -27,6 +27,13 @@ class MergeInfo(C.Structure):
                 ("stage", C.c_uint32)]
 
 
+class DriverDesc(C.Structure):
+    _fields_ = [("dim", C.c_uint64), ("schedule", C.c_void_p), ("dtype", C.c_int),
+                ("device", C.c_int), ("nranks", C.c_uint32), ("rank", C.c_uint32),
+                ("nccl_id", C.c_void_p), ("bucket_elems", C.c_uint64), ("period", C.c_uint64),
+                ("eta_s", C.c_double), ("global_seed", C.c_uint64), ("first_round", C.c_uint64)]
+
+
 class CtxDesc(C.Structure):
     _fields_ = [("dim", C.c_uint64), ("schedule", C.c_void_p), ("dtype", C.c_int),
                 ("device", C.c_int), ("nranks", C.c_uint32), ("rank", C.c_uint32),
@@ -63,6 +70,15 @@ SIGNATURES = {
     "marsit_ctx_timing": (_i32, [_vp, _vp, _vp, _i32]),
     "marsit_fill_recipe": (_i32, [_i32, _u64, _u64, _u64, _u64, _i32, _vp, _vp]),
     "marsit_nccl_unique_id": (_i32, [_vp]),
+    "marsit_driver_create": (_i32, [C.POINTER(DriverDesc), _pvp]),
+    "marsit_driver_destroy": (None, [_vp]),
+    "marsit_driver_step": (_i32, [_vp, _vp, _vp, _vp, C.POINTER(_i32), _vp]),
+    "marsit_driver_compensation": (_i32, [_vp, _u32, _pvp]),
+    "marsit_driver_state": (_i32, [_vp, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u32)]),
+    "marsit_driver_save": (_i32, [_vp, C.c_char_p, _vp]),
+    "marsit_driver_load": (_i32, [_vp, C.c_char_p, _vp]),
+    "marsit_write_params_checkpoint": (_i32, [C.c_char_p, _vp, _u64, _i32, _vp]),
+    "marsit_read_params_checkpoint": (_i32, [C.c_char_p, _vp, _u64, _i32, _vp]),
     "marsit_last_error": (C.c_char_p, []),
     "marsit_abi_version": (_i32, []),
 }

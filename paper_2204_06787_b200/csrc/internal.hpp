@@ -1,0 +1,275 @@
+// internal.hpp — private runtime structures shared by runtime.cu (the
+// C-ABI) and driver.cu (the multi-step sync driver).  Not installed.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/marsit_b200.h"
+#include "kernels.cuh"
+#include "plan.hpp"
+
+struct marsit_schedule {
+    marsit_b200::HostSchedule s;
+    marsit_b200::Plan plan;
+};
+
+namespace marsit_b200 {
+
+// Record the thread-local error message and return the status.
+marsit_status fail(marsit_status st, const std::string& msg);
+
+
+#define CUDA_TRY(expr)                                                                    \
+    do {                                                                                  \
+        cudaError_t e_ = (expr);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(MARSIT_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define NCCL_TRY(expr)                                                                      \
+    do {                                                                                    \
+        ncclResult_t r_ = (expr);                                                           \
+        if (r_ != ncclSuccess)                                                              \
+            return fail(MARSIT_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
+inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+inline uint64_t round_up(uint64_t a, uint64_t b) { return ceil_div(a, b) * b; }
+
+inline int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+inline bool have_device() {
+    int n = 0;
+    return cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
+}
+
+// Device-side plan of the merge DAGs (see DevMerge in kernels.cuh).
+struct DevicePlan {
+    std::vector<DevMerge> merges;
+    std::vector<uint32_t> seg_begin, stage_begin;
+    uint32_t max_slots = 0, gmax = 0, n_stages = 1, n_merges = 0;
+};
+
+// Lower the owned segments' merge DAGs into the device plan (runtime.cu).
+marsit_status lower_plan(const Plan& plan, uint32_t s_first, uint32_t n_seg, DevicePlan& dp);
+
+// The cooperative merge of a set of owned segments (K2).  Chooses the words
+// per thread and splits each segment's tiles into parts so that one launch's
+// tiles are co-resident; launches stage x part.
+struct MergeRunner {
+    DevicePlan dp;
+    uint32_t n_seg = 0, s_first = 0, words_proc = 0, wst = 0, ml = 0;
+    uint64_t L = 0;
+    int wpt = 1;
+    size_t smem = 0;
+    uint32_t tiles_per_seg = 0, part_tiles = 0, n_parts = 1;
+    std::vector<uint32_t> k_steps;  // per stage: max merges over segments
+    DevMerge* d_merges = nullptr;
+    uint32_t* d_seg_begin = nullptr;
+    uint32_t* d_stage_begin = nullptr;
+    uint32_t* gnodes = nullptr;
+    uint32_t* counts = nullptr;
+    uint64_t* part_totals = nullptr;
+
+    MergeRunner() = default;
+    MergeRunner(const MergeRunner&) = delete;
+    MergeRunner& operator=(const MergeRunner&) = delete;
+    ~MergeRunner() {
+        for (void* p : {(void*)d_merges, (void*)d_seg_begin, (void*)d_stage_begin, (void*)gnodes,
+                        (void*)counts, (void*)part_totals})
+            if (p) cudaFree(p);
+    }
+
+    // Tiling: minimise the number of parts, then the words per thread.
+    marsit_status configure(int sm_count) {
+        k_steps.assign(dp.n_stages, 0);
+        for (uint32_t sl = 0; sl < n_seg; ++sl)
+            for (uint32_t st = 0; st < dp.n_stages; ++st) {
+                const uint32_t* sb = &dp.stage_begin[size_t(sl) * (dp.n_stages + 1)];
+                k_steps[st] = std::max(k_steps[st], sb[st + 1] - sb[st]);
+            }
+        const int forced = env_int("MARSIT_MERGE_WPT", 0);
+        uint64_t best_parts = ~0ull;
+        for (int w : {1, 2, 4, 8}) {
+            if (forced && w != forced) continue;
+            const size_t sm = size_t(std::max<uint32_t>(dp.max_slots, 1)) * w * kMergeThreads * 4;
+            if (sm > 160 * 1024) continue;
+            int occ = 0;
+            CUDA_TRY(merge_coop_occupancy(w, sm, &occ));
+            const uint64_t cap = uint64_t(occ) * sm_count;
+            const uint64_t tps = ceil_div(words_proc, uint64_t(w) * kMergeThreads);
+            const uint64_t pt = std::min<uint64_t>(tps, cap / n_seg);
+            if (pt == 0) continue;
+            const uint64_t parts = ceil_div(tps, pt);
+            if (parts < best_parts) {
+                best_parts = parts;
+                wpt = w;
+                smem = sm;
+                tiles_per_seg = uint32_t(tps);
+                part_tiles = uint32_t(pt);
+                n_parts = uint32_t(parts);
+            }
+        }
+        if (best_parts == ~0ull) return fail(MARSIT_EUNSUPPORTED, "merge tiles do not fit the device");
+        return MARSIT_OK;
+    }
+
+    marsit_status upload() {
+        const size_t nm = std::max<size_t>(dp.n_merges, 1);
+        CUDA_TRY(cudaMalloc(&d_merges, sizeof(DevMerge) * nm));
+        CUDA_TRY(cudaMemcpy(d_merges, dp.merges.data(), sizeof(DevMerge) * dp.n_merges,
+                            cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMalloc(&d_seg_begin, sizeof(uint32_t) * dp.seg_begin.size()));
+        CUDA_TRY(cudaMemcpy(d_seg_begin, dp.seg_begin.data(), sizeof(uint32_t) * dp.seg_begin.size(),
+                            cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMalloc(&d_stage_begin, sizeof(uint32_t) * dp.stage_begin.size()));
+        CUDA_TRY(cudaMemcpy(d_stage_begin, dp.stage_begin.data(),
+                            sizeof(uint32_t) * dp.stage_begin.size(), cudaMemcpyHostToDevice));
+        const uint32_t gmax = std::max<uint32_t>(dp.gmax, 1);
+        CUDA_TRY(cudaMalloc(&gnodes, sizeof(uint32_t) * size_t(n_seg) * gmax * wst));
+        uint32_t kmax = 1;
+        for (uint32_t k : k_steps) kmax = std::max(kmax, k);
+        CUDA_TRY(cudaMalloc(&counts, sizeof(uint32_t) * size_t(kmax) * n_seg * part_tiles));
+        CUDA_TRY(cudaMalloc(&part_totals, sizeof(uint64_t) * size_t(n_parts) * nm));
+        CUDA_TRY(cudaMemset(part_totals, 0, sizeof(uint64_t) * size_t(n_parts) * nm));
+        return MARSIT_OK;
+    }
+
+    marsit_status run(const uint32_t* leaves, uint32_t* agg, const uint32_t* coins, uint64_t seed,
+                      uint64_t round, cudaStream_t st, uint64_t* n_launch) {
+        CoopParams c{};
+        c.merges = d_merges;
+        c.seg_begin = d_seg_begin;
+        c.stage_begin = d_stage_begin;
+        c.n_stages = dp.n_stages;
+        c.n_seg = n_seg;
+        c.s_first = s_first;
+        c.tiles_per_seg = tiles_per_seg;
+        c.words_proc = words_proc;
+        c.wst = wst;
+        c.ml = ml;
+        c.max_slots = std::max<uint32_t>(dp.max_slots, 1);
+        c.n_parts = n_parts;
+        c.part_tiles = part_tiles;
+        c.n_merges = dp.n_merges;
+        c.seg_bits = L;
+        c.leaves = leaves;
+        c.gnodes = gnodes;
+        c.gmax = std::max<uint32_t>(dp.gmax, 1);
+        c.agg = agg;
+        c.coins = coins;
+        c.counts = counts;
+        c.part_totals = part_totals;
+        c.seed = seed;
+        c.round = round;
+        for (uint32_t stage = 0; stage < dp.n_stages; ++stage) {
+            if (k_steps[stage] == 0) continue;
+            c.stage = stage;
+            c.k_steps = k_steps[stage];
+            for (uint32_t part = 0; part < n_parts; ++part) {
+                c.part = part;
+                c.part_tile0 = part * part_tiles;
+                CUDA_TRY(launch_merge_coop(c, wpt, smem, st));
+                ++*n_launch;
+            }
+        }
+        return MARSIT_OK;
+    }
+};
+
+struct TimedPair {
+    int phase;
+    cudaEvent_t a, b;
+};
+
+
+}  // namespace marsit_b200
+
+struct marsit_ctx {
+    int device = 0;
+    marsit_dtype dtype = MARSIT_F32;
+    size_t esize = 4;
+    uint64_t D = 0, L = 0;
+    uint32_t M = 0, S = 0, G = 1, rank = 0, ml = 0, s_own = 0, s_first = 0;
+    uint32_t words64 = 0, words_proc = 0, wst = 0;
+    int sm_count = 148;
+    bool vec_ok = false;
+    marsit_b200::HostSchedule sched;
+    marsit_b200::Plan plan;
+    marsit_b200::MergeRunner merge;
+    // device buffers
+    uint32_t* bits = nullptr;  // [S][ml][wst]
+    uint32_t* recv = nullptr;  // [G][s_own][ml][wst]   (G > 1)
+    uint32_t* agg = nullptr;   // [S][wst]
+    int* err = nullptr;
+    int stream_grid = 0;   // generic grid-stride kernels
+    int extract_grid = 0;  // persistent, one wave of resident CTAs
+    int decode_grid = 0;
+    // dense round scratch
+    void* dense_send = nullptr;  // [G][s_own][ml][L] of dtype
+    void* dense_recv = nullptr;
+    void* dense_mean = nullptr;  // [S*L] of dtype (G > 1)
+    marsit_b200::DenseOp* d_dense_ops = nullptr;
+    uint16_t* d_dense_final = nullptr;
+    uint32_t dense_n_ops = 0;
+    // coin precompute on the aux stream; two buffers: this round's and the
+    // next round's, computed speculatively for (seed, t + 1) during the decode
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_fork = nullptr;
+    uint32_t* coin_buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev_coin_done[2] = {nullptr, nullptr};
+    struct CoinTag {
+        bool valid = false;
+        uint64_t seed = 0, round = 0;
+    } coin_tag[2];
+    int cur_coin = 0;
+    bool coin_prefetch = true;
+    bool coins_pending = false;
+    uint64_t coin_total_words = 0;
+    int coin_grid_x = 1;
+    // NCCL
+    ncclComm_t comm = nullptr;
+    bool owns_comm = true;
+    // timing
+    bool timing = false;
+    std::vector<marsit_b200::TimedPair> pending;
+    std::vector<cudaEvent_t> event_pool;
+    float ms[MARSIT_N_PHASES] = {};
+    uint64_t launches[MARSIT_N_PHASES] = {};
+
+    ~marsit_ctx();
+    marsit_status begin_phase(cudaStream_t st, cudaEvent_t* a);
+    marsit_status end_phase(int phase, cudaStream_t st, cudaEvent_t a, uint64_t n_launch);
+};
+
+
+namespace marsit_b200 {
+
+// One sign round (sync.hpp:91-118) with the optional fused parameter update
+// x_w -= g_t (params may be null).
+marsit_status sign_round_impl(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_t seed,
+                              const void* const* grads, const void* const* comp,
+                              void* const* comp_out, void* const* params, uint64_t* agg_bits,
+                              void* update, cudaStream_t st);
+// One dense round (sync.hpp:78-87); mean is required; params may be null.
+marsit_status dense_round_any(marsit_ctx* ctx, const void* const* grads, const void* const* comp,
+                              void* const* comp_out, void* const* params, void* mean,
+                              cudaStream_t st);
+// marsit_ctx_create, optionally sharing an existing communicator (driver buckets).
+marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared_comm,
+                                  marsit_ctx** out);
+// Payload bits of one round (allreduce.hpp:113, 182).
+uint64_t round_bits_total(const marsit_ctx* ctx, bool dense);
+
+}  // namespace marsit_b200

@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode
         const T* c = p.c[wl];  // may alias c_out (in-place update): no __restrict__
         T* co = p.c_out[wl];
         T* upd = (wl == 0) ? p.update : nullptr;
+        T* xp = p.x[wl];  // replica parameters (optional)
         const uint64_t seg0 = uint64_t(s) * p.seg_len;
         const uint64_t j0 = uint64_t(q) * (kTaskWords * 32);
         const uint32_t* aw = p.agg + uint64_t(s) * p.wst + q * kTaskWords;
@@ -339,12 +340,19 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode
                 if (j < p.seg_len && gi + 3 < p.dim) {
                     store4(co + gi, out);
                     if (upd) store4(upd + gi, up);
+                    if (xp) {
+                        Quad<T> xv = load4_rw(xp + gi);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) xv.v[k] = sub_rn(xv.v[k], up.v[k]);
+                        store4(xp + gi, xv);
+                    }
                 } else {
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
                         if ((j + k < p.seg_len) && (gi + k < p.dim)) {
                             co[gi + k] = out.v[k];
                             if (upd) upd[gi + k] = up.v[k];
+                            if (xp) xp[gi + k] = sub_rn(xp[gi + k], up.v[k]);
                         }
                 }
             }
@@ -358,6 +366,7 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode
                     const T gt = ((word >> lane) & 1u) ? eta : -eta;
                     co[gi] = sub_rn(add_rn(g[gi], c[gi]), gt);
                     if (upd) upd[gi] = gt;
+                    if (xp) xp[gi] = sub_rn(xp[gi], gt);
                 }
             }
         }
@@ -709,6 +718,18 @@ __global__ void export_bits_kernel(const uint32_t* __restrict__ agg, uint32_t ws
     }
 }
 
+// x_w -= v (dense-round parameter update, trainer.hpp:285-288)
+template <typename T>
+__global__ void sub_update_kernel(StreamParams<T> p, const T* __restrict__ v) {
+    const uint64_t n = p.dim * p.ml;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t w = uint32_t(i / p.dim);
+        const uint64_t j = i - uint64_t(w) * p.dim;
+        p.x[w][j] = sub_rn(p.x[w][j], v[j]);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Synthetic inputs: g_j from draw j of RngStream(seed,
 // trial, w, t, 0).  recipe 0: ((x>>51) - 4096)·2^-20; recipe 1 (correlated):
@@ -914,6 +935,17 @@ cudaError_t launch_fill_recipe(int recipe, uint64_t seed, uint64_t worker, uint6
 }
 
 template <typename T>
+cudaError_t launch_sub_update(T* const* x, uint32_t ml, const T* v, uint64_t dim, int grid,
+                              cudaStream_t st) {
+    StreamParams<T> p{};
+    for (uint32_t w = 0; w < ml; ++w) p.x[w] = x[w];
+    p.ml = ml;
+    p.dim = dim;
+    sub_update_kernel<T><<<grid, 256, 0, st>>>(p, v);
+    return cudaGetLastError();
+}
+
+template <typename T>
 cudaError_t launch_dense_reduce(const DenseParams<T>& p, int grid, cudaStream_t st) {
     dense_reduce_kernel<T><<<grid, 256, 0, st>>>(p);
     return cudaGetLastError();
@@ -942,6 +974,8 @@ cudaError_t launch_dense_leaf(const T* const* g, const T* const* c, uint32_t ml,
     template cudaError_t launch_fill_recipe<T>(int, uint64_t, uint64_t, uint64_t, uint64_t, T*, \
                                                cudaStream_t);                                   \
     template cudaError_t launch_dense_reduce<T>(const DenseParams<T>&, int, cudaStream_t);      \
+    template cudaError_t launch_sub_update<T>(T* const*, uint32_t, const T*, uint64_t, int,     \
+                                              cudaStream_t);                                    \
     template cudaError_t launch_dense_leaf<T>(const T* const*, const T* const*, uint32_t,       \
                                               uint64_t, uint64_t, uint32_t, uint32_t, T*, int*,  \
                                               int, cudaStream_t);

@@ -74,6 +74,7 @@ struct StreamParams {
     uint32_t* bits;              // extract output: [S][ml][wst]
     const uint32_t* agg;         // decode input: [S][wst]
     T* update;                   // optional g_t (written by local worker 0)
+    T* x[kMaxLocalWorkers];      // optional replica parameters: x -= g_t (trainer.hpp:285-288)
     T eta;
     int* err;
 };
@@ -91,6 +92,10 @@ cudaError_t launch_coins(const DevMerge* merges, uint32_t n_merges, uint64_t see
                          uint32_t* coins, int grid_x, cudaStream_t st);
 cudaError_t launch_export_bits(const uint32_t* agg, uint32_t wst, uint64_t dim, uint64_t seg_len,
                                uint32_t* out_u32, cudaStream_t st);
+// x_w -= v for the local workers' parameter replicas (dense-round update).
+template <typename T>
+cudaError_t launch_sub_update(T* const* x, uint32_t ml, const T* v, uint64_t dim, int grid,
+                              cudaStream_t st);
 template <typename T>
 cudaError_t launch_fill_recipe(int recipe, uint64_t seed, uint64_t worker, uint64_t round,
                                uint64_t dim, T* out, cudaStream_t st);

@@ -22,59 +22,20 @@
 #include <string>
 #include <vector>
 
-#include "../../include/marsit_b200.h"
-#include "kernels.cuh"
-#include "plan.hpp"
+#include "internal.hpp"
 
 using namespace marsit_b200;
 
-struct marsit_schedule {
-    HostSchedule s;
-    Plan plan;
-};
+namespace marsit_b200 {
 
 namespace {
-
 thread_local std::string g_last_error;
+}  // namespace
 
 marsit_status fail(marsit_status st, const std::string& msg) {
     g_last_error = msg;
     return st;
 }
-
-#define CUDA_TRY(expr)                                                                    \
-    do {                                                                                  \
-        cudaError_t e_ = (expr);                                                          \
-        if (e_ != cudaSuccess)                                                            \
-            return fail(MARSIT_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
-    } while (0)
-
-#define NCCL_TRY(expr)                                                                      \
-    do {                                                                                    \
-        ncclResult_t r_ = (expr);                                                           \
-        if (r_ != ncclSuccess)                                                              \
-            return fail(MARSIT_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
-    } while (0)
-
-uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
-uint64_t round_up(uint64_t a, uint64_t b) { return ceil_div(a, b) * b; }
-
-int env_int(const char* name, int dflt) {
-    const char* e = std::getenv(name);
-    return e ? std::atoi(e) : dflt;
-}
-
-bool have_device() {
-    int n = 0;
-    return cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
-}
-
-// Device-side plan of the merge DAGs (see DevMerge in kernels.cuh).
-struct DevicePlan {
-    std::vector<DevMerge> merges;
-    std::vector<uint32_t> seg_begin, stage_begin;
-    uint32_t max_slots = 0, gmax = 0, n_stages = 1, n_merges = 0;
-};
 
 // Lower the owned segments' merge DAGs: execution order = (stage, schedule
 // order); outputs consumed by a later merge of the same stage get a
@@ -168,192 +129,7 @@ marsit_status lower_plan(const Plan& plan, uint32_t s_first, uint32_t n_seg, Dev
     return MARSIT_OK;
 }
 
-// The cooperative merge of a set of owned segments (K2).  Chooses the words
-// per thread and splits each segment's tiles into parts so that one launch's
-// tiles are co-resident; launches stage x part.
-struct MergeRunner {
-    DevicePlan dp;
-    uint32_t n_seg = 0, s_first = 0, words_proc = 0, wst = 0, ml = 0;
-    uint64_t L = 0;
-    int wpt = 1;
-    size_t smem = 0;
-    uint32_t tiles_per_seg = 0, part_tiles = 0, n_parts = 1;
-    std::vector<uint32_t> k_steps;  // per stage: max merges over segments
-    DevMerge* d_merges = nullptr;
-    uint32_t* d_seg_begin = nullptr;
-    uint32_t* d_stage_begin = nullptr;
-    uint32_t* gnodes = nullptr;
-    uint32_t* counts = nullptr;
-    uint64_t* part_totals = nullptr;
-
-    MergeRunner() = default;
-    MergeRunner(const MergeRunner&) = delete;
-    MergeRunner& operator=(const MergeRunner&) = delete;
-    ~MergeRunner() {
-        for (void* p : {(void*)d_merges, (void*)d_seg_begin, (void*)d_stage_begin, (void*)gnodes,
-                        (void*)counts, (void*)part_totals})
-            if (p) cudaFree(p);
-    }
-
-    // Tiling: minimise the number of parts, then the words per thread.
-    marsit_status configure(int sm_count) {
-        k_steps.assign(dp.n_stages, 0);
-        for (uint32_t sl = 0; sl < n_seg; ++sl)
-            for (uint32_t st = 0; st < dp.n_stages; ++st) {
-                const uint32_t* sb = &dp.stage_begin[size_t(sl) * (dp.n_stages + 1)];
-                k_steps[st] = std::max(k_steps[st], sb[st + 1] - sb[st]);
-            }
-        const int forced = env_int("MARSIT_MERGE_WPT", 0);
-        uint64_t best_parts = ~0ull;
-        for (int w : {1, 2, 4, 8}) {
-            if (forced && w != forced) continue;
-            const size_t sm = size_t(std::max<uint32_t>(dp.max_slots, 1)) * w * kMergeThreads * 4;
-            if (sm > 160 * 1024) continue;
-            int occ = 0;
-            CUDA_TRY(merge_coop_occupancy(w, sm, &occ));
-            const uint64_t cap = uint64_t(occ) * sm_count;
-            const uint64_t tps = ceil_div(words_proc, uint64_t(w) * kMergeThreads);
-            const uint64_t pt = std::min<uint64_t>(tps, cap / n_seg);
-            if (pt == 0) continue;
-            const uint64_t parts = ceil_div(tps, pt);
-            if (parts < best_parts) {
-                best_parts = parts;
-                wpt = w;
-                smem = sm;
-                tiles_per_seg = uint32_t(tps);
-                part_tiles = uint32_t(pt);
-                n_parts = uint32_t(parts);
-            }
-        }
-        if (best_parts == ~0ull) return fail(MARSIT_EUNSUPPORTED, "merge tiles do not fit the device");
-        return MARSIT_OK;
-    }
-
-    marsit_status upload() {
-        const size_t nm = std::max<size_t>(dp.n_merges, 1);
-        CUDA_TRY(cudaMalloc(&d_merges, sizeof(DevMerge) * nm));
-        CUDA_TRY(cudaMemcpy(d_merges, dp.merges.data(), sizeof(DevMerge) * dp.n_merges,
-                            cudaMemcpyHostToDevice));
-        CUDA_TRY(cudaMalloc(&d_seg_begin, sizeof(uint32_t) * dp.seg_begin.size()));
-        CUDA_TRY(cudaMemcpy(d_seg_begin, dp.seg_begin.data(), sizeof(uint32_t) * dp.seg_begin.size(),
-                            cudaMemcpyHostToDevice));
-        CUDA_TRY(cudaMalloc(&d_stage_begin, sizeof(uint32_t) * dp.stage_begin.size()));
-        CUDA_TRY(cudaMemcpy(d_stage_begin, dp.stage_begin.data(),
-                            sizeof(uint32_t) * dp.stage_begin.size(), cudaMemcpyHostToDevice));
-        const uint32_t gmax = std::max<uint32_t>(dp.gmax, 1);
-        CUDA_TRY(cudaMalloc(&gnodes, sizeof(uint32_t) * size_t(n_seg) * gmax * wst));
-        uint32_t kmax = 1;
-        for (uint32_t k : k_steps) kmax = std::max(kmax, k);
-        CUDA_TRY(cudaMalloc(&counts, sizeof(uint32_t) * size_t(kmax) * n_seg * part_tiles));
-        CUDA_TRY(cudaMalloc(&part_totals, sizeof(uint64_t) * size_t(n_parts) * nm));
-        CUDA_TRY(cudaMemset(part_totals, 0, sizeof(uint64_t) * size_t(n_parts) * nm));
-        return MARSIT_OK;
-    }
-
-    marsit_status run(const uint32_t* leaves, uint32_t* agg, const uint32_t* coins, uint64_t seed,
-                      uint64_t round, cudaStream_t st, uint64_t* n_launch) {
-        CoopParams c{};
-        c.merges = d_merges;
-        c.seg_begin = d_seg_begin;
-        c.stage_begin = d_stage_begin;
-        c.n_stages = dp.n_stages;
-        c.n_seg = n_seg;
-        c.s_first = s_first;
-        c.tiles_per_seg = tiles_per_seg;
-        c.words_proc = words_proc;
-        c.wst = wst;
-        c.ml = ml;
-        c.max_slots = std::max<uint32_t>(dp.max_slots, 1);
-        c.n_parts = n_parts;
-        c.part_tiles = part_tiles;
-        c.n_merges = dp.n_merges;
-        c.seg_bits = L;
-        c.leaves = leaves;
-        c.gnodes = gnodes;
-        c.gmax = std::max<uint32_t>(dp.gmax, 1);
-        c.agg = agg;
-        c.coins = coins;
-        c.counts = counts;
-        c.part_totals = part_totals;
-        c.seed = seed;
-        c.round = round;
-        for (uint32_t stage = 0; stage < dp.n_stages; ++stage) {
-            if (k_steps[stage] == 0) continue;
-            c.stage = stage;
-            c.k_steps = k_steps[stage];
-            for (uint32_t part = 0; part < n_parts; ++part) {
-                c.part = part;
-                c.part_tile0 = part * part_tiles;
-                CUDA_TRY(launch_merge_coop(c, wpt, smem, st));
-                ++*n_launch;
-            }
-        }
-        return MARSIT_OK;
-    }
-};
-
-struct TimedPair {
-    int phase;
-    cudaEvent_t a, b;
-};
-
-}  // namespace
-
-struct marsit_ctx {
-    int device = 0;
-    marsit_dtype dtype = MARSIT_F32;
-    size_t esize = 4;
-    uint64_t D = 0, L = 0;
-    uint32_t M = 0, S = 0, G = 1, rank = 0, ml = 0, s_own = 0, s_first = 0;
-    uint32_t words64 = 0, words_proc = 0, wst = 0;
-    int sm_count = 148;
-    bool vec_ok = false;
-    HostSchedule sched;
-    Plan plan;
-    MergeRunner merge;
-    // device buffers
-    uint32_t* bits = nullptr;  // [S][ml][wst]
-    uint32_t* recv = nullptr;  // [G][s_own][ml][wst]   (G > 1)
-    uint32_t* agg = nullptr;   // [S][wst]
-    int* err = nullptr;
-    int stream_grid = 0;   // generic grid-stride kernels
-    int extract_grid = 0;  // persistent, one wave of resident CTAs
-    int decode_grid = 0;
-    // dense round scratch
-    void* dense_send = nullptr;  // [G][s_own][ml][L] of dtype
-    void* dense_recv = nullptr;
-    void* dense_mean = nullptr;  // [S*L] of dtype (G > 1)
-    DenseOp* d_dense_ops = nullptr;
-    uint16_t* d_dense_final = nullptr;
-    uint32_t dense_n_ops = 0;
-    // coin precompute on the aux stream; two buffers: this round's and the
-    // next round's, computed speculatively for (seed, t + 1) during the decode
-    cudaStream_t aux = nullptr;
-    cudaEvent_t ev_fork = nullptr;
-    uint32_t* coin_buf[2] = {nullptr, nullptr};
-    cudaEvent_t ev_coin_done[2] = {nullptr, nullptr};
-    struct CoinTag {
-        bool valid = false;
-        uint64_t seed = 0, round = 0;
-    } coin_tag[2];
-    int cur_coin = 0;
-    bool coin_prefetch = true;
-    bool coins_pending = false;
-    uint64_t coin_total_words = 0;
-    int coin_grid_x = 1;
-    // NCCL
-    ncclComm_t comm = nullptr;
-    // timing
-    bool timing = false;
-    std::vector<TimedPair> pending;
-    std::vector<cudaEvent_t> event_pool;
-    float ms[MARSIT_N_PHASES] = {};
-    uint64_t launches[MARSIT_N_PHASES] = {};
-
-    ~marsit_ctx();
-    marsit_status begin_phase(cudaStream_t st, cudaEvent_t* a);
-    marsit_status end_phase(int phase, cudaStream_t st, cudaEvent_t a, uint64_t n_launch);
-};
+}  // namespace marsit_b200
 
 marsit_ctx::~marsit_ctx() {
     if (device >= 0) cudaSetDevice(device);
@@ -371,7 +147,7 @@ marsit_ctx::~marsit_ctx() {
         if (coin_buf[b]) cudaFree(coin_buf[b]);
     }
     if (aux) cudaStreamDestroy(aux);
-    if (comm) ncclCommDestroy(comm);
+    if (comm && owns_comm) ncclCommDestroy(comm);
 }
 
 marsit_status marsit_ctx::begin_phase(cudaStream_t st, cudaEvent_t* a) {
@@ -410,12 +186,14 @@ enum Phase { kPhExtract = 0, kPhExchange, kPhMerge, kPhAllgather, kPhDecode, kPh
 
 template <typename T>
 StreamParams<T> stream_params(marsit_ctx* ctx, const void* const* g, const void* const* c,
-                              void* const* c_out, void* update, double eta) {
+                              void* const* c_out, void* update, double eta,
+                              void* const* params = nullptr) {
     StreamParams<T> p{};
     for (uint32_t w = 0; w < ctx->ml; ++w) {
         p.g[w] = static_cast<const T*>(g[w]);
         p.c[w] = static_cast<const T*>(c[w]);
         p.c_out[w] = c_out ? static_cast<T*>(c_out[w]) : nullptr;
+        p.x[w] = params ? static_cast<T*>(params[w]) : nullptr;
     }
     p.ml = ctx->ml;
     p.n_seg = ctx->S;
@@ -551,17 +329,19 @@ marsit_status run_allgather(marsit_ctx* ctx, cudaStream_t st) {
 }
 
 marsit_status run_decode(marsit_ctx* ctx, const void* const* g, const void* const* c,
-                         void* const* c_out, void* update, double eta, cudaStream_t st) {
+                         void* const* c_out, void* const* params, void* update, double eta,
+                         cudaStream_t st) {
     cudaEvent_t ev;
     marsit_status s = ctx->begin_phase(st, &ev);
     if (s) return s;
     const bool vec = vec_ok_ptrs(ctx, g, c) && vec_ok_ptrs(ctx, (const void* const*)c_out, c) &&
+                     (!params || vec_ok_ptrs(ctx, (const void* const*)params, c)) &&
                      (!update || aligned16(update));
     if (ctx->dtype == MARSIT_F32)
-        CUDA_TRY(launch_decode(stream_params<float>(ctx, g, c, c_out, update, eta), vec,
+        CUDA_TRY(launch_decode(stream_params<float>(ctx, g, c, c_out, update, eta, params), vec,
                                ctx->decode_grid, st));
     else
-        CUDA_TRY(launch_decode(stream_params<double>(ctx, g, c, c_out, update, eta), vec,
+        CUDA_TRY(launch_decode(stream_params<double>(ctx, g, c, c_out, update, eta, params), vec,
                                ctx->decode_grid, st));
     return ctx->end_phase(kPhDecode, st, ev, 1);
 }
@@ -588,7 +368,8 @@ marsit_status check_consensus(const marsit_ctx* ctx, bool need_full_count) {
 
 template <typename T>
 marsit_status dense_round_impl(marsit_ctx* ctx, const void* const* g, const void* const* c,
-                               void* const* c_out, void* mean, cudaStream_t st) {
+                               void* const* c_out, void* const* params, void* mean,
+                               cudaStream_t st) {
     cudaEvent_t ev;
     marsit_status s = ctx->begin_phase(st, &ev);
     if (s) return s;
@@ -646,6 +427,13 @@ marsit_status dense_round_impl(marsit_ctx* ctx, const void* const* g, const void
     }
     for (uint32_t w = 0; w < ctx->ml; ++w)
         CUDA_TRY(cudaMemsetAsync(c_out[w], 0, ctx->D * sizeof(T), st));  // sync.hpp:83-85
+    if (params) {  // x_w -= mean (trainer.hpp:285-288)
+        std::vector<T*> xs(ctx->ml);
+        for (uint32_t w = 0; w < ctx->ml; ++w) xs[w] = static_cast<T*>(params[w]);
+        CUDA_TRY(launch_sub_update<T>(xs.data(), ctx->ml, static_cast<const T*>(mean), ctx->D,
+                                      ctx->stream_grid, st));
+        ++launches;
+    }
     return ctx->end_phase(kPhDense, st, ev, launches);
 }
 
@@ -677,6 +465,57 @@ void assign_coin_budget(DevicePlan& dp, uint32_t n_seg, uint64_t L, double frac,
 }
 
 }  // namespace
+
+namespace marsit_b200 {
+
+marsit_status sign_round_impl(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_t seed,
+                              const void* const* d_grads, const void* const* d_comp,
+                              void* const* d_comp_out, void* const* params, uint64_t* d_agg_bits,
+                              void* d_update, cudaStream_t st) {
+    if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
+    if (!(eta_s > 0.0)) return fail(MARSIT_EPARAM, "SyncConfig: eta_s must be > 0");
+    marsit_status s;
+    if ((s = check_ptrs(ctx, d_grads, "grads")) || (s = check_ptrs(ctx, d_comp, "comp")) ||
+        (s = check_ptrs(ctx, (const void* const*)d_comp_out, "comp_out")) ||
+        (params && (s = check_ptrs(ctx, (const void* const*)params, "params"))))
+        return s;
+    if ((s = check_consensus(ctx, true))) return s;
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    if ((s = run_coins(ctx, seed, t, st))) return s;
+    if ((s = run_extract(ctx, d_grads, d_comp, st))) return s;
+    if ((s = run_exchange(ctx, st))) return s;
+    if ((s = run_merge(ctx, seed, t, st))) return s;
+    if ((s = prefetch_coins(ctx, seed, t, st))) return s;
+    if ((s = run_allgather(ctx, st))) return s;
+    if ((s = run_decode(ctx, d_grads, d_comp, d_comp_out, params, d_update, eta_s, st))) return s;
+    return run_export(ctx, d_agg_bits, st);
+}
+
+marsit_status dense_round_any(marsit_ctx* ctx, const void* const* d_grads,
+                              const void* const* d_comp, void* const* d_comp_out,
+                              void* const* params, void* d_mean, cudaStream_t st) {
+    if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
+    if (!d_mean) return fail(MARSIT_EPARAM, "mean is null");
+    marsit_status s;
+    if ((s = check_ptrs(ctx, d_grads, "grads")) || (s = check_ptrs(ctx, d_comp, "comp")) ||
+        (s = check_ptrs(ctx, (const void* const*)d_comp_out, "comp_out")) ||
+        (params && (s = check_ptrs(ctx, (const void* const*)params, "params"))))
+        return s;
+    if ((s = check_consensus(ctx, false))) return s;
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    if (ctx->dtype == MARSIT_F32)
+        return dense_round_impl<float>(ctx, d_grads, d_comp, d_comp_out, params, d_mean, st);
+    return dense_round_impl<double>(ctx, d_grads, d_comp, d_comp_out, params, d_mean, st);
+}
+
+uint64_t round_bits_total(const marsit_ctx* ctx, bool dense) {
+    const uint64_t unit = dense ? 32ull * ctx->L : ctx->L;
+    uint64_t t = 0;
+    for (uint32_t w = 0; w < ctx->M; ++w) t += ctx->plan.sends_per_worker[w] * unit;
+    return t;
+}
+
+}  // namespace marsit_b200
 
 // ===========================================================================
 // C-ABI
@@ -779,6 +618,15 @@ marsit_status marsit_nccl_unique_id(void* out128) {
 }
 
 marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out) {
+    return ctx_create_internal(desc, nullptr, out);
+}
+
+}  // extern "C"
+
+namespace marsit_b200 {
+
+marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared_comm,
+                                  marsit_ctx** out) {
     if (!desc || !out) return fail(MARSIT_EPARAM, "null argument");
     *out = nullptr;
     if (!desc->schedule) return fail(MARSIT_EPARAM, "schedule is null");
@@ -792,7 +640,8 @@ marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out) {
     if (desc->rank >= G) return fail(MARSIT_EPARAM, "rank out of range");
     if (hs.workers / G > kMaxLocalWorkers)
         return fail(MARSIT_EUNSUPPORTED, "too many workers per rank (max 64)");
-    if (G > 1 && !desc->nccl_id) return fail(MARSIT_EPARAM, "nccl_id required for nranks > 1");
+    if (G > 1 && !desc->nccl_id && !shared_comm)
+        return fail(MARSIT_EPARAM, "nccl_id required for nranks > 1");
     if (!have_device())
         return fail(MARSIT_ECUDA, "no CUDA device available (this library has no CPU path)");
 
@@ -914,13 +763,22 @@ marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out) {
         CUDA_TRY(cudaMalloc(&ctx->dense_send, ctx->esize * dense_elems));
         CUDA_TRY(cudaMalloc(&ctx->dense_recv, ctx->esize * dense_elems));
         CUDA_TRY(cudaMalloc(&ctx->dense_mean, ctx->esize * size_t(ctx->S) * ctx->L));
-        ncclUniqueId id;
-        std::memcpy(&id, desc->nccl_id, sizeof(id));
-        NCCL_TRY(ncclCommInitRank(&ctx->comm, int(G), id, int(desc->rank)));
+        if (shared_comm) {
+            ctx->comm = shared_comm;
+            ctx->owns_comm = false;
+        } else {
+            ncclUniqueId id;
+            std::memcpy(&id, desc->nccl_id, sizeof(id));
+            NCCL_TRY(ncclCommInitRank(&ctx->comm, int(G), id, int(desc->rank)));
+        }
     }
     *out = ctx.release();
     return MARSIT_OK;
 }
+
+}  // namespace marsit_b200
+
+extern "C" {
 
 void marsit_ctx_destroy(marsit_ctx* ctx) { delete ctx; }
 
@@ -935,40 +793,15 @@ marsit_status marsit_sign_round(marsit_ctx* ctx, uint64_t t, double eta_s, uint6
                                 const void* const* d_grads, const void* const* d_comp,
                                 void* const* d_comp_out, uint64_t* d_agg_bits, void* d_update,
                                 void* stream) {
-    if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
-    if (!(eta_s > 0.0)) return fail(MARSIT_EPARAM, "SyncConfig: eta_s must be > 0");
-    marsit_status s;
-    if ((s = check_ptrs(ctx, d_grads, "grads")) || (s = check_ptrs(ctx, d_comp, "comp")) ||
-        (s = check_ptrs(ctx, (const void* const*)d_comp_out, "comp_out")))
-        return s;
-    if ((s = check_consensus(ctx, true))) return s;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    CUDA_TRY(cudaSetDevice(ctx->device));
-    if ((s = run_coins(ctx, seed, t, st))) return s;
-    if ((s = run_extract(ctx, d_grads, d_comp, st))) return s;
-    if ((s = run_exchange(ctx, st))) return s;
-    if ((s = run_merge(ctx, seed, t, st))) return s;
-    if ((s = prefetch_coins(ctx, seed, t, st))) return s;
-    if ((s = run_allgather(ctx, st))) return s;
-    if ((s = run_decode(ctx, d_grads, d_comp, d_comp_out, d_update, eta_s, st))) return s;
-    return run_export(ctx, d_agg_bits, st);
+    return sign_round_impl(ctx, t, eta_s, seed, d_grads, d_comp, d_comp_out, nullptr, d_agg_bits,
+                           d_update, static_cast<cudaStream_t>(stream));
 }
 
 marsit_status marsit_dense_round(marsit_ctx* ctx, uint64_t, const void* const* d_grads,
                                  const void* const* d_comp, void* const* d_comp_out, void* d_mean,
                                  void* stream) {
-    if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
-    if (!d_mean) return fail(MARSIT_EPARAM, "mean is null");
-    marsit_status s;
-    if ((s = check_ptrs(ctx, d_grads, "grads")) || (s = check_ptrs(ctx, d_comp, "comp")) ||
-        (s = check_ptrs(ctx, (const void* const*)d_comp_out, "comp_out")))
-        return s;
-    if ((s = check_consensus(ctx, false))) return s;
-    CUDA_TRY(cudaSetDevice(ctx->device));
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (ctx->dtype == MARSIT_F32)
-        return dense_round_impl<float>(ctx, d_grads, d_comp, d_comp_out, d_mean, st);
-    return dense_round_impl<double>(ctx, d_grads, d_comp, d_comp_out, d_mean, st);
+    return dense_round_any(ctx, d_grads, d_comp, d_comp_out, nullptr, d_mean,
+                           static_cast<cudaStream_t>(stream));
 }
 
 marsit_status marsit_round(marsit_ctx* ctx, uint64_t t, uint64_t period, double eta_s,
