@@ -785,40 +785,56 @@ __global__ void dense_leaf_kernel(const DenseParams<T> p, uint32_t s_own, uint32
     if (bad) atomicOr(p.err, 1);
 }
 
+// Node values of the reduction tree live in shared memory
+// ([node][kDenseThreads], conflict-free); a node index is data, so a
+// register array would spill to local memory.
+constexpr int kDenseThreads = 128;
 template <typename T>
-__global__ void dense_reduce_kernel(const DenseParams<T> p) {
+__global__ void __launch_bounds__(kDenseThreads) dense_reduce_kernel(const DenseParams<T> p) {
+    extern __shared__ double dval[];  // [workers + n_ops][kDenseThreads]
+    const int tid = threadIdx.x;
     const uint64_t n = uint64_t(p.n_seg) * p.seg_len;
-    double val[2 * kMaxLocalWorkers];
     bool bad = false;
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + tid; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t sl = uint32_t(i / p.seg_len);
         const uint64_t o = i - uint64_t(sl) * p.seg_len;
         const uint64_t j = uint64_t(p.s_first + sl) * p.seg_len + o;  // global coordinate
-        for (uint32_t w = 0; w < p.workers; ++w) {
-            double u;
-            if (p.mode == 0) {
-                if (j < p.dim) {
-                    const T gg = p.src[2 * w][j], cc = p.src[2 * w + 1][j];
-                    const T uu = add_rn(gg, cc);
-                    bad |= !(finite(gg) && finite(cc) && finite(uu));
-                    u = double(uu);
-                } else {
-                    u = 0.0;  // value padding
+        if (p.mode == 0) {
+            // loads in groups of 8 workers (16 independent loads in flight)
+            const bool in = j < p.dim;
+            for (uint32_t w0 = 0; w0 < p.workers; w0 += 8) {
+                T gg[8], cc[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const bool ok = in && w0 + k < p.workers;
+                    gg[k] = ok ? p.src[2 * (w0 + k)][j] : T(0);
+                    cc[k] = ok ? p.src[2 * (w0 + k) + 1][j] : T(0);
                 }
-            } else {
-                const uint32_t src_rank = w / p.ml, wl = w % p.ml;
-                u = double(p.u_buf[((uint64_t(src_rank) * p.n_seg + sl) * p.ml + wl) * p.seg_len + o]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (w0 + k >= p.workers) break;
+                    const T uu = add_rn(gg[k], cc[k]);  // value padding: 0 + 0
+                    bad |= !(finite(gg[k]) && finite(cc[k]) && finite(uu));
+                    dval[(w0 + k) * kDenseThreads + tid] = double(uu);
+                }
             }
-            val[w] = u;
+        } else {
+            for (uint32_t w = 0; w < p.workers; ++w) {
+                const uint32_t src_rank = w / p.ml, wl = w % p.ml;
+                dval[w * kDenseThreads + tid] = double(
+                    p.u_buf[((uint64_t(src_rank) * p.n_seg + sl) * p.ml + wl) * p.seg_len + o]);
+            }
         }
         const DenseOp* ops = p.ops + uint64_t(sl) * p.n_ops;
         for (uint32_t k = 0; k < p.n_ops; ++k) {
-            const double v = __dadd_rn(val[ops[k].a], val[ops[k].b]);
+            const double v = __dadd_rn(dval[ops[k].a * kDenseThreads + tid],
+                                       dval[ops[k].b * kDenseThreads + tid]);
             bad |= !isfinite(v);
-            val[p.workers + k] = v;
+            dval[(p.workers + k) * kDenseThreads + tid] = v;
         }
-        if (j < p.dim) p.mean[j] = T(__dmul_rn(val[p.final_node[sl]], p.inv_m));
+        if (j < p.dim)
+            p.mean[j] = T(__dmul_rn(dval[p.final_node[sl] * kDenseThreads + tid], p.inv_m));
     }
     if (bad) atomicOr(p.err, 1);
 }
@@ -947,7 +963,13 @@ cudaError_t launch_sub_update(T* const* x, uint32_t ml, const T* v, uint64_t dim
 
 template <typename T>
 cudaError_t launch_dense_reduce(const DenseParams<T>& p, int grid, cudaStream_t st) {
-    dense_reduce_kernel<T><<<grid, 256, 0, st>>>(p);
+    const size_t smem = size_t(p.workers + p.n_ops) * kDenseThreads * sizeof(double);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(dense_reduce_kernel<T>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+    }
+    dense_reduce_kernel<T><<<grid * 2, kDenseThreads, smem, st>>>(p);
     return cudaGetLastError();
 }
 
