@@ -95,6 +95,12 @@ marsit_status marsit_schedule_plan(const marsit_schedule* s, uint32_t segment,
  * ---------------------------------------------------------------------- */
 typedef struct marsit_ctx marsit_ctx;
 
+/* How the packed segments move between ranks (nranks > 1). */
+typedef enum marsit_transport {
+    MARSIT_TRANSPORT_NCCL = 0,     /* built in: grouped send/recv + all-gather     */
+    MARSIT_TRANSPORT_EXTERNAL = 1  /* the caller moves the blocks between phases   */
+} marsit_transport;
+
 typedef struct marsit_ctx_desc {
     uint64_t dim;                     /* D >= 1                                   */
     const marsit_schedule* schedule;  /* M workers, M segments                    */
@@ -102,7 +108,8 @@ typedef struct marsit_ctx_desc {
     int device;                       /* CUDA device ordinal                       */
     uint32_t nranks;                  /* processes sharing the M workers (>= 1)    */
     uint32_t rank;                    /* this process: workers [rank*M/nranks, ..) */
-    const void* nccl_id;              /* 128-byte ncclUniqueId when nranks > 1     */
+    const void* nccl_id;              /* 128-byte ncclUniqueId (NCCL, nranks > 1) */
+    marsit_transport transport;
 } marsit_ctx_desc;
 
 marsit_status marsit_ctx_create(const marsit_ctx_desc* desc, marsit_ctx** out);
@@ -146,6 +153,28 @@ marsit_status marsit_round(marsit_ctx* ctx, uint64_t t, uint64_t period, double 
 marsit_status marsit_allreduce_sign(marsit_ctx* ctx, uint64_t round, uint64_t global_seed,
                                     const uint64_t* d_signs, uint64_t* d_out, uint32_t* counts,
                                     void* stream);
+
+/* External transport (or manual staging): a round split at its two exchange
+ * points.  phase 0: sign extraction (or, for a dense round, u = g + c per
+ * destination); the caller then moves block q of layout.send to rank q's
+ * layout.recv (block r of recv comes from rank r).  phase 1: merge (dense:
+ * sum) of this rank's owned segments into its own block of layout.gather;
+ * the caller all-gathers the gather blocks.  phase 2: decode + compensation
+ * (dense: mean out, compensation = 0).  Arguments as marsit_round. */
+typedef struct marsit_exchange_layout {
+    void* send;
+    void* recv;
+    uint64_t block_bytes;         /* per destination / source rank              */
+    void* gather;
+    uint64_t gather_block_bytes;  /* this rank's block is at rank*gather_block_bytes */
+} marsit_exchange_layout;
+marsit_status marsit_ctx_exchange_layout(const marsit_ctx* ctx, int dense,
+                                         marsit_exchange_layout* out);
+marsit_status marsit_round_phase(marsit_ctx* ctx, int phase, uint64_t t, uint64_t period,
+                                 double eta_s, uint64_t global_seed, const void* const* d_grads,
+                                 const void* const* d_comp, void* const* d_comp_out,
+                                 uint64_t* d_agg_bits, void* d_update, int* full_precision,
+                                 void* stream);
 
 /* Error-compensated sign extraction alone (sync.hpp:71-76 + segmentation.hpp:32-53
  * + sign_vector.hpp:67-73): d_signs_out as in marsit_allreduce_sign's input. */

@@ -217,7 +217,8 @@ class Context:
     """Owns a marsit_ctx (device scratch + compiled plan + optional NCCL comm)."""
 
     def __init__(self, dim: int, schedule: Schedule, dtype=None, device: int = 0,
-                 nranks: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None):
+                 nranks: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
+                 external_transport: bool = False):
         import torch
         dtype = dtype or torch.float32
         self.dim, self.schedule, self.device = int(dim), schedule, int(device)
@@ -230,6 +231,7 @@ class Context:
         desc.device = self.device
         desc.nranks = nranks
         desc.rank = rank
+        desc.transport = 1 if external_transport else 0
         self._id_buf = None
         if nccl_id is not None:
             self._id_buf = C.create_string_buffer(bytes(nccl_id), 128)
@@ -269,6 +271,24 @@ class Context:
         _check(N.lib().marsit_dense_round(self._h, t, g, c, co, C.c_void_p(mean.data_ptr()),
                                           stream if stream is not None
                                           else _stream_ptr(self.device)))
+
+    def exchange_layout(self, dense: bool = False):
+        lay = N.ExchangeLayout()
+        _check(N.lib().marsit_ctx_exchange_layout(self._h, int(dense), C.byref(lay)))
+        return lay
+
+    def round_phase(self, phase, t, period, eta_s, seed, grads, comp, comp_out=None,
+                    agg_bits=None, update=None, stream=None):
+        g = N.ptr_array([x.data_ptr() for x in grads])
+        c = N.ptr_array([x.data_ptr() for x in comp])
+        co = N.ptr_array([x.data_ptr() for x in (comp_out if comp_out is not None else comp)])
+        full = C.c_int()
+        _check(N.lib().marsit_round_phase(
+            self._h, phase, t, 0 if period is None else period, float(eta_s), seed, g, c, co,
+            C.c_void_p(agg_bits.data_ptr() if agg_bits is not None else None),
+            C.c_void_p(update.data_ptr() if update is not None else None), C.byref(full),
+            stream if stream is not None else _stream_ptr(self.device)))
+        return bool(full.value)
 
     def check(self, stream=None):
         _check(N.lib().marsit_ctx_check(self._h, stream if stream is not None

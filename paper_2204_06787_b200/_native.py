@@ -37,7 +37,12 @@ class DriverDesc(C.Structure):
 class CtxDesc(C.Structure):
     _fields_ = [("dim", C.c_uint64), ("schedule", C.c_void_p), ("dtype", C.c_int),
                 ("device", C.c_int), ("nranks", C.c_uint32), ("rank", C.c_uint32),
-                ("nccl_id", C.c_void_p)]
+                ("nccl_id", C.c_void_p), ("transport", C.c_int)]
+
+
+class ExchangeLayout(C.Structure):
+    _fields_ = [("send", C.c_void_p), ("recv", C.c_void_p), ("block_bytes", C.c_uint64),
+                ("gather", C.c_void_p), ("gather_block_bytes", C.c_uint64)]
 
 
 # Every symbol include/marsit_b200.h declares: name -> (restype, argtypes)
@@ -61,6 +66,9 @@ SIGNATURES = {
                             C.POINTER(_i32), _vp]),
     "marsit_allreduce_sign": (_i32, [_vp, _u64, _u64, _vp, _vp, _vp, _vp]),
     "marsit_sign_extract": (_i32, [_vp, _vp, _vp, _vp, _vp]),
+    "marsit_ctx_exchange_layout": (_i32, [_vp, _i32, C.POINTER(ExchangeLayout)]),
+    "marsit_round_phase": (_i32, [_vp, _i32, _u64, _u64, _dbl, _u64, _vp, _vp, _vp, _vp, _vp,
+                                  C.POINTER(_i32), _vp]),
     "marsit_merge_signs": (_i32, [_vp, _u32, _vp, _u32, _u64, _u64, _u64, _vp,
                                   C.POINTER(_u64), _i32, _vp]),
     "marsit_bits_account": (_i32, [_vp, _i32, _vp, C.POINTER(_u64), C.POINTER(_u64),

@@ -246,7 +246,7 @@ marsit_status run_extract(marsit_ctx* ctx, const void* const* g, const void* con
 // NCCL all-to-all of the packed segments: destination q receives this rank's
 // local workers' bits of the segments it owns (one contiguous block).
 marsit_status run_exchange(marsit_ctx* ctx, cudaStream_t st) {
-    if (ctx->G == 1) return MARSIT_OK;
+    if (ctx->G == 1 || !ctx->comm) return MARSIT_OK;  // external transport: the caller's
     cudaEvent_t ev;
     marsit_status s = ctx->begin_phase(st, &ev);
     if (s) return s;
@@ -319,7 +319,7 @@ marsit_status run_merge(marsit_ctx* ctx, uint64_t seed, uint64_t round, cudaStre
 }
 
 marsit_status run_allgather(marsit_ctx* ctx, cudaStream_t st) {
-    if (ctx->G == 1) return MARSIT_OK;
+    if (ctx->G == 1 || !ctx->comm) return MARSIT_OK;
     cudaEvent_t ev;
     marsit_status s = ctx->begin_phase(st, &ev);
     if (s) return s;
@@ -366,10 +366,16 @@ marsit_status check_consensus(const marsit_ctx* ctx, bool need_full_count) {
     return MARSIT_OK;
 }
 
+// Dense round in three phases around the two exchange points (G > 1):
+//   0: u = g + c of the local workers, laid out per destination rank
+//   [exchange of u blocks]
+//   1: owner-side schedule-order sum of the owned segments, x 1/M
+//   [all-gather of the owned mean blocks]
+//   2: mean out, compensation = 0 (sync.hpp:83-85), optional x -= mean
+// With G == 1 phase 1 reads g and c directly and writes `mean`.
 template <typename T>
-marsit_status dense_round_impl(marsit_ctx* ctx, const void* const* g, const void* const* c,
-                               void* const* c_out, void* const* params, void* mean,
-                               cudaStream_t st) {
+marsit_status dense_phase(marsit_ctx* ctx, int phase, const void* const* g, const void* const* c,
+                          void* const* c_out, void* const* params, void* mean, cudaStream_t st) {
     cudaEvent_t ev;
     marsit_status s = ctx->begin_phase(st, &ev);
     if (s) return s;
@@ -386,16 +392,7 @@ marsit_status dense_round_impl(marsit_ctx* ctx, const void* const* g, const void
     p.inv_m = 1.0 / double(ctx->M);
     p.err = ctx->err;
     uint64_t launches = 0;
-    if (ctx->G == 1) {
-        p.mode = 0;
-        for (uint32_t w = 0; w < ctx->ml; ++w) {
-            p.src[2 * w] = static_cast<const T*>(g[w]);
-            p.src[2 * w + 1] = static_cast<const T*>(c[w]);
-        }
-        p.mean = static_cast<T*>(mean);
-        CUDA_TRY(launch_dense_reduce(p, ctx->stream_grid, st));
-        ++launches;
-    } else {
+    if (phase == 0 && ctx->G > 1) {
         std::vector<const T*> gg(ctx->ml), cc(ctx->ml);
         for (uint32_t w = 0; w < ctx->ml; ++w) {
             gg[w] = static_cast<const T*>(g[w]);
@@ -404,37 +401,70 @@ marsit_status dense_round_impl(marsit_ctx* ctx, const void* const* g, const void
         CUDA_TRY(launch_dense_leaf<T>(gg.data(), cc.data(), ctx->ml, ctx->D, ctx->L, ctx->S,
                                       ctx->s_own, static_cast<T*>(ctx->dense_send), ctx->err,
                                       ctx->stream_grid, st));
-        const size_t block = size_t(ctx->s_own) * ctx->ml * ctx->L;
-        const ncclDataType_t dt = sizeof(T) == 4 ? ncclFloat32 : ncclFloat64;
-        NCCL_TRY(ncclGroupStart());
-        for (uint32_t q = 0; q < ctx->G; ++q) {
-            NCCL_TRY(ncclSend(static_cast<T*>(ctx->dense_send) + q * block, block, dt, int(q),
-                              ctx->comm, st));
-            NCCL_TRY(ncclRecv(static_cast<T*>(ctx->dense_recv) + q * block, block, dt, int(q),
-                              ctx->comm, st));
-        }
-        NCCL_TRY(ncclGroupEnd());
-        p.mode = 1;
-        p.u_buf = static_cast<const T*>(ctx->dense_recv);
-        T* full = static_cast<T*>(ctx->dense_mean);
-        p.mean = full;  // padded [S*L] buffer; owned coordinates written at global index
-        p.dim = uint64_t(ctx->S) * ctx->L;
-        CUDA_TRY(launch_dense_reduce(p, ctx->stream_grid, st));
-        const size_t seg_block = size_t(ctx->s_own) * ctx->L;
-        NCCL_TRY(ncclAllGather(full + ctx->rank * seg_block, full, seg_block, dt, ctx->comm, st));
-        CUDA_TRY(cudaMemcpyAsync(mean, full, ctx->D * sizeof(T), cudaMemcpyDeviceToDevice, st));
-        launches += 2;
-    }
-    for (uint32_t w = 0; w < ctx->ml; ++w)
-        CUDA_TRY(cudaMemsetAsync(c_out[w], 0, ctx->D * sizeof(T), st));  // sync.hpp:83-85
-    if (params) {  // x_w -= mean (trainer.hpp:285-288)
-        std::vector<T*> xs(ctx->ml);
-        for (uint32_t w = 0; w < ctx->ml; ++w) xs[w] = static_cast<T*>(params[w]);
-        CUDA_TRY(launch_sub_update<T>(xs.data(), ctx->ml, static_cast<const T*>(mean), ctx->D,
-                                      ctx->stream_grid, st));
         ++launches;
+    } else if (phase == 1) {
+        if (ctx->G == 1) {
+            p.mode = 0;
+            for (uint32_t w = 0; w < ctx->ml; ++w) {
+                p.src[2 * w] = static_cast<const T*>(g[w]);
+                p.src[2 * w + 1] = static_cast<const T*>(c[w]);
+            }
+            p.mean = static_cast<T*>(mean);
+        } else {
+            p.mode = 1;
+            p.u_buf = static_cast<const T*>(ctx->dense_recv);
+            p.mean = static_cast<T*>(ctx->dense_mean);  // padded [S*L]; owned block written
+            p.dim = uint64_t(ctx->S) * ctx->L;
+        }
+        CUDA_TRY(launch_dense_reduce(p, ctx->stream_grid, st));
+        ++launches;
+    } else if (phase == 2) {
+        if (ctx->G > 1)
+            CUDA_TRY(cudaMemcpyAsync(mean, ctx->dense_mean, ctx->D * sizeof(T),
+                                     cudaMemcpyDeviceToDevice, st));
+        for (uint32_t w = 0; w < ctx->ml; ++w)
+            CUDA_TRY(cudaMemsetAsync(c_out[w], 0, ctx->D * sizeof(T), st));  // sync.hpp:83-85
+        if (params) {  // x_w -= mean (trainer.hpp:285-288)
+            std::vector<T*> xs(ctx->ml);
+            for (uint32_t w = 0; w < ctx->ml; ++w) xs[w] = static_cast<T*>(params[w]);
+            CUDA_TRY(launch_sub_update<T>(xs.data(), ctx->ml, static_cast<const T*>(mean),
+                                          ctx->D, ctx->stream_grid, st));
+            ++launches;
+        }
     }
     return ctx->end_phase(kPhDense, st, ev, launches);
+}
+
+marsit_status dense_exchange(marsit_ctx* ctx, cudaStream_t st) {
+    if (ctx->G == 1 || !ctx->comm) return MARSIT_OK;  // external transport: the caller's
+    const size_t block = size_t(ctx->s_own) * ctx->ml * ctx->L;
+    const ncclDataType_t dt = ctx->esize == 4 ? ncclFloat32 : ncclFloat64;
+    NCCL_TRY(ncclGroupStart());
+    for (uint32_t q = 0; q < ctx->G; ++q) {
+        NCCL_TRY(ncclSend(static_cast<char*>(ctx->dense_send) + q * block * ctx->esize, block, dt,
+                          int(q), ctx->comm, st));
+        NCCL_TRY(ncclRecv(static_cast<char*>(ctx->dense_recv) + q * block * ctx->esize, block, dt,
+                          int(q), ctx->comm, st));
+    }
+    NCCL_TRY(ncclGroupEnd());
+    return MARSIT_OK;
+}
+
+marsit_status dense_allgather(marsit_ctx* ctx, cudaStream_t st) {
+    if (ctx->G == 1 || !ctx->comm) return MARSIT_OK;
+    const size_t seg_block = size_t(ctx->s_own) * ctx->L;
+    const ncclDataType_t dt = ctx->esize == 4 ? ncclFloat32 : ncclFloat64;
+    char* full = static_cast<char*>(ctx->dense_mean);
+    NCCL_TRY(ncclAllGather(full + ctx->rank * seg_block * ctx->esize, full, seg_block, dt,
+                           ctx->comm, st));
+    return MARSIT_OK;
+}
+
+marsit_status dense_phase_any(marsit_ctx* ctx, int phase, const void* const* g,
+                              const void* const* c, void* const* c_out, void* const* params,
+                              void* mean, cudaStream_t st) {
+    if (ctx->dtype == MARSIT_F32) return dense_phase<float>(ctx, phase, g, c, c_out, params, mean, st);
+    return dense_phase<double>(ctx, phase, g, c, c_out, params, mean, st);
 }
 
 // Coin precompute budget per merge: frac * L draws per use of its (receiver,
@@ -468,44 +498,76 @@ void assign_coin_budget(DevicePlan& dp, uint32_t n_seg, uint64_t L, double frac,
 
 namespace marsit_b200 {
 
-marsit_status sign_round_impl(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_t seed,
-                              const void* const* d_grads, const void* const* d_comp,
-                              void* const* d_comp_out, void* const* params, uint64_t* d_agg_bits,
-                              void* d_update, cudaStream_t st) {
+// Sign round phases around the two exchange points:
+//   0: coins (aux) + extract  ->  [exchange of packed segments]
+//   1: merge of the owned segments (+ next round's coin prefetch)
+//      ->  [all-gather of the owned aggregates]
+//   2: decode + compensation (+ fused replica update) + export
+marsit_status sign_phase(marsit_ctx* ctx, int phase, uint64_t t, double eta_s, uint64_t seed,
+                         const void* const* d_grads, const void* const* d_comp,
+                         void* const* d_comp_out, void* const* params, uint64_t* d_agg_bits,
+                         void* d_update, cudaStream_t st) {
+    marsit_status s = MARSIT_OK;
+    if (phase == 0) {
+        if ((s = run_coins(ctx, seed, t, st))) return s;
+        return run_extract(ctx, d_grads, d_comp, st);
+    }
+    if (phase == 1) {
+        if ((s = run_merge(ctx, seed, t, st))) return s;
+        return prefetch_coins(ctx, seed, t, st);
+    }
+    if ((s = run_decode(ctx, d_grads, d_comp, d_comp_out, params, d_update, eta_s, st))) return s;
+    return run_export(ctx, d_agg_bits, st);
+}
+
+marsit_status check_round_args(marsit_ctx* ctx, double eta_s, const void* const* d_grads,
+                               const void* const* d_comp, void* const* d_comp_out,
+                               void* const* params, bool sign) {
     if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
-    if (!(eta_s > 0.0)) return fail(MARSIT_EPARAM, "SyncConfig: eta_s must be > 0");
+    if (sign && !(eta_s > 0.0)) return fail(MARSIT_EPARAM, "SyncConfig: eta_s must be > 0");
     marsit_status s;
     if ((s = check_ptrs(ctx, d_grads, "grads")) || (s = check_ptrs(ctx, d_comp, "comp")) ||
         (s = check_ptrs(ctx, (const void* const*)d_comp_out, "comp_out")) ||
         (params && (s = check_ptrs(ctx, (const void* const*)params, "params"))))
         return s;
-    if ((s = check_consensus(ctx, true))) return s;
+    if ((s = check_consensus(ctx, sign))) return s;
     CUDA_TRY(cudaSetDevice(ctx->device));
-    if ((s = run_coins(ctx, seed, t, st))) return s;
-    if ((s = run_extract(ctx, d_grads, d_comp, st))) return s;
+    return MARSIT_OK;
+}
+
+marsit_status sign_round_impl(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_t seed,
+                              const void* const* d_grads, const void* const* d_comp,
+                              void* const* d_comp_out, void* const* params, uint64_t* d_agg_bits,
+                              void* d_update, cudaStream_t st) {
+    marsit_status s = check_round_args(ctx, eta_s, d_grads, d_comp, d_comp_out, params, true);
+    if (s) return s;
+    if (ctx->G > 1 && !ctx->comm)
+        return fail(MARSIT_EUNSUPPORTED, "external-transport context: use marsit_round_phase");
+    if ((s = sign_phase(ctx, 0, t, eta_s, seed, d_grads, d_comp, d_comp_out, params, d_agg_bits,
+                        d_update, st)))
+        return s;
     if ((s = run_exchange(ctx, st))) return s;
-    if ((s = run_merge(ctx, seed, t, st))) return s;
-    if ((s = prefetch_coins(ctx, seed, t, st))) return s;
+    if ((s = sign_phase(ctx, 1, t, eta_s, seed, d_grads, d_comp, d_comp_out, params, d_agg_bits,
+                        d_update, st)))
+        return s;
     if ((s = run_allgather(ctx, st))) return s;
-    if ((s = run_decode(ctx, d_grads, d_comp, d_comp_out, params, d_update, eta_s, st))) return s;
-    return run_export(ctx, d_agg_bits, st);
+    return sign_phase(ctx, 2, t, eta_s, seed, d_grads, d_comp, d_comp_out, params, d_agg_bits,
+                      d_update, st);
 }
 
 marsit_status dense_round_any(marsit_ctx* ctx, const void* const* d_grads,
                               const void* const* d_comp, void* const* d_comp_out,
                               void* const* params, void* d_mean, cudaStream_t st) {
-    if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
+    marsit_status s = check_round_args(ctx, 1.0, d_grads, d_comp, d_comp_out, params, false);
+    if (s) return s;
     if (!d_mean) return fail(MARSIT_EPARAM, "mean is null");
-    marsit_status s;
-    if ((s = check_ptrs(ctx, d_grads, "grads")) || (s = check_ptrs(ctx, d_comp, "comp")) ||
-        (s = check_ptrs(ctx, (const void* const*)d_comp_out, "comp_out")) ||
-        (params && (s = check_ptrs(ctx, (const void* const*)params, "params"))))
-        return s;
-    if ((s = check_consensus(ctx, false))) return s;
-    CUDA_TRY(cudaSetDevice(ctx->device));
-    if (ctx->dtype == MARSIT_F32)
-        return dense_round_impl<float>(ctx, d_grads, d_comp, d_comp_out, params, d_mean, st);
-    return dense_round_impl<double>(ctx, d_grads, d_comp, d_comp_out, params, d_mean, st);
+    if (ctx->G > 1 && !ctx->comm)
+        return fail(MARSIT_EUNSUPPORTED, "external-transport context: use marsit_round_phase");
+    if ((s = dense_phase_any(ctx, 0, d_grads, d_comp, d_comp_out, params, d_mean, st))) return s;
+    if ((s = dense_exchange(ctx, st))) return s;
+    if ((s = dense_phase_any(ctx, 1, d_grads, d_comp, d_comp_out, params, d_mean, st))) return s;
+    if ((s = dense_allgather(ctx, st))) return s;
+    return dense_phase_any(ctx, 2, d_grads, d_comp, d_comp_out, params, d_mean, st);
 }
 
 uint64_t round_bits_total(const marsit_ctx* ctx, bool dense) {
@@ -640,7 +702,8 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     if (desc->rank >= G) return fail(MARSIT_EPARAM, "rank out of range");
     if (hs.workers / G > kMaxLocalWorkers)
         return fail(MARSIT_EUNSUPPORTED, "too many workers per rank (max 64)");
-    if (G > 1 && !desc->nccl_id && !shared_comm)
+    const bool external = desc->transport == MARSIT_TRANSPORT_EXTERNAL;
+    if (G > 1 && !external && !desc->nccl_id && !shared_comm)
         return fail(MARSIT_EPARAM, "nccl_id required for nranks > 1");
     if (!have_device())
         return fail(MARSIT_ECUDA, "no CUDA device available (this library has no CPU path)");
@@ -763,7 +826,9 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
         CUDA_TRY(cudaMalloc(&ctx->dense_send, ctx->esize * dense_elems));
         CUDA_TRY(cudaMalloc(&ctx->dense_recv, ctx->esize * dense_elems));
         CUDA_TRY(cudaMalloc(&ctx->dense_mean, ctx->esize * size_t(ctx->S) * ctx->L));
-        if (shared_comm) {
+        if (external) {
+            ctx->comm = nullptr;  // the caller moves the blocks (marsit_round_phase)
+        } else if (shared_comm) {
             ctx->comm = shared_comm;
             ctx->owns_comm = false;
         } else {
@@ -819,6 +884,45 @@ marsit_status marsit_round(marsit_ctx* ctx, uint64_t t, uint64_t period, double 
     }
     return marsit_sign_round(ctx, t, eta_s, seed, d_grads, d_comp, d_comp_out, d_agg_bits,
                              d_update, stream);
+}
+
+marsit_status marsit_ctx_exchange_layout(const marsit_ctx* ctx, int dense,
+                                         marsit_exchange_layout* out) {
+    if (!ctx || !out) return fail(MARSIT_EPARAM, "null argument");
+    if (dense) {
+        out->send = ctx->G > 1 ? ctx->dense_send : nullptr;
+        out->recv = ctx->G > 1 ? ctx->dense_recv : nullptr;
+        out->block_bytes = uint64_t(ctx->s_own) * ctx->ml * ctx->L * ctx->esize;
+        out->gather = ctx->G > 1 ? ctx->dense_mean : nullptr;
+        out->gather_block_bytes = uint64_t(ctx->s_own) * ctx->L * ctx->esize;
+    } else {
+        out->send = ctx->bits;
+        out->recv = ctx->G > 1 ? ctx->recv : ctx->bits;
+        out->block_bytes = uint64_t(ctx->s_own) * ctx->ml * ctx->wst * 4;
+        out->gather = ctx->agg;
+        out->gather_block_bytes = uint64_t(ctx->s_own) * ctx->wst * 4;
+    }
+    return MARSIT_OK;
+}
+
+marsit_status marsit_round_phase(marsit_ctx* ctx, int phase, uint64_t t, uint64_t period,
+                                 double eta_s, uint64_t seed, const void* const* d_grads,
+                                 const void* const* d_comp, void* const* d_comp_out,
+                                 uint64_t* d_agg_bits, void* d_update, int* full_precision,
+                                 void* stream) {
+    if (phase < 0 || phase > 2) return fail(MARSIT_EPARAM, "phase must be 0, 1 or 2");
+    if (!(eta_s > 0.0)) return fail(MARSIT_EPARAM, "SyncConfig: eta_s must be > 0");
+    const bool dense = period != 0 && (t % period == 0);  // sync.hpp:78
+    if (full_precision) *full_precision = dense ? 1 : 0;
+    marsit_status s = check_round_args(ctx, eta_s, d_grads, d_comp, d_comp_out, nullptr, !dense);
+    if (s) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (dense) {
+        if (!d_update) return fail(MARSIT_EPARAM, "dense round needs d_update for the mean");
+        return dense_phase_any(ctx, phase, d_grads, d_comp, d_comp_out, nullptr, d_update, st);
+    }
+    return sign_phase(ctx, phase, t, eta_s, seed, d_grads, d_comp, d_comp_out, nullptr,
+                      d_agg_bits, d_update, st);
 }
 
 marsit_status marsit_sign_extract(marsit_ctx* ctx, const void* const* d_grads,
