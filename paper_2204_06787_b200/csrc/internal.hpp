@@ -73,6 +73,7 @@ struct MergeRunner {
     uint64_t L = 0;
     int wpt = 1;
     size_t smem = 0;
+    uint32_t seg_per_launch = 1;  // owned segments per cooperative launch
     uint32_t tiles_per_seg = 0, part_tiles = 0, n_parts = 1;
     std::vector<uint32_t> k_steps;  // per stage: max merges over segments
     DevMerge* d_merges = nullptr;
@@ -92,7 +93,10 @@ struct MergeRunner {
     }
 
     // Tiling: minimise the number of parts, then the words per thread.
-    marsit_status configure(int sm_count) {
+    // seg_launch: owned segments per launch (1: per-segment pipeline);
+    // cta_limit: CTAs per SM left to the merge (0: all it can get).
+    marsit_status configure(int sm_count, uint32_t seg_launch = 0, int cta_limit = 0) {
+        seg_per_launch = seg_launch ? seg_launch : n_seg;
         k_steps.assign(dp.n_stages, 0);
         for (uint32_t sl = 0; sl < n_seg; ++sl)
             for (uint32_t st = 0; st < dp.n_stages; ++st) {
@@ -107,9 +111,10 @@ struct MergeRunner {
             if (sm > 160 * 1024) continue;
             int occ = 0;
             CUDA_TRY(merge_coop_occupancy(w, sm, &occ));
+            if (cta_limit > 0) occ = std::min(occ, cta_limit);
             const uint64_t cap = uint64_t(occ) * sm_count;
             const uint64_t tps = ceil_div(words_proc, uint64_t(w) * kMergeThreads);
-            const uint64_t pt = std::min<uint64_t>(tps, cap / n_seg);
+            const uint64_t pt = std::min<uint64_t>(tps, cap / seg_per_launch);
             if (pt == 0) continue;
             const uint64_t parts = ceil_div(tps, pt);
             if (parts < best_parts) {
@@ -140,14 +145,18 @@ struct MergeRunner {
         CUDA_TRY(cudaMalloc(&gnodes, sizeof(uint32_t) * size_t(n_seg) * gmax * wst));
         uint32_t kmax = 1;
         for (uint32_t k : k_steps) kmax = std::max(kmax, k);
-        CUDA_TRY(cudaMalloc(&counts, sizeof(uint32_t) * size_t(kmax) * n_seg * part_tiles));
+        CUDA_TRY(cudaMalloc(&counts, sizeof(uint32_t) * size_t(kmax) * seg_per_launch * part_tiles));
         CUDA_TRY(cudaMalloc(&part_totals, sizeof(uint64_t) * size_t(n_parts) * nm));
         CUDA_TRY(cudaMemset(part_totals, 0, sizeof(uint64_t) * size_t(n_parts) * nm));
         return MARSIT_OK;
     }
 
+    // Merge owned segments [seg_lo, seg_lo + seg_cnt) (seg_cnt <= seg_per_launch
+    // per launch; more segments run as consecutive launches).
     marsit_status run(const uint32_t* leaves, uint32_t* agg, const uint32_t* coins, uint64_t seed,
-                      uint64_t round, cudaStream_t st, uint64_t* n_launch) {
+                      uint64_t round, cudaStream_t st, uint64_t* n_launch, uint32_t seg_lo = 0,
+                      uint32_t seg_cnt = ~0u) {
+        if (seg_cnt == ~0u) seg_cnt = n_seg - seg_lo;
         CoopParams c{};
         c.merges = d_merges;
         c.seg_begin = d_seg_begin;
@@ -173,15 +182,19 @@ struct MergeRunner {
         c.part_totals = part_totals;
         c.seed = seed;
         c.round = round;
-        for (uint32_t stage = 0; stage < dp.n_stages; ++stage) {
-            if (k_steps[stage] == 0) continue;
-            c.stage = stage;
-            c.k_steps = k_steps[stage];
-            for (uint32_t part = 0; part < n_parts; ++part) {
-                c.part = part;
-                c.part_tile0 = part * part_tiles;
-                CUDA_TRY(launch_merge_coop(c, wpt, smem, st));
-                ++*n_launch;
+        for (uint32_t s0 = seg_lo; s0 < seg_lo + seg_cnt; s0 += seg_per_launch) {
+            c.seg_lo = s0;
+            c.seg_cnt = std::min(seg_per_launch, seg_lo + seg_cnt - s0);
+            for (uint32_t stage = 0; stage < dp.n_stages; ++stage) {
+                if (k_steps[stage] == 0) continue;
+                c.stage = stage;
+                c.k_steps = k_steps[stage];
+                for (uint32_t part = 0; part < n_parts; ++part) {
+                    c.part = part;
+                    c.part_tile0 = part * part_tiles;
+                    CUDA_TRY(launch_merge_coop(c, wpt, smem, st));
+                    ++*n_launch;
+                }
             }
         }
         return MARSIT_OK;
@@ -237,6 +250,10 @@ struct marsit_ctx {
     bool coin_prefetch = true;
     bool coins_pending = false;
     uint64_t coin_total_words = 0;
+    // single GPU: per-segment merges (aux) pipelined with per-segment decodes
+    bool pipeline = false;
+    cudaEvent_t ev_extract = nullptr;
+    std::vector<cudaEvent_t> ev_merge;
     int coin_grid_x = 1;
     // NCCL
     ncclComm_t comm = nullptr;

@@ -472,8 +472,8 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 8 ? 3 : 4) merge_coop_ke
     __shared__ uint32_t s_warp[kMergeThreads / 32];
     __shared__ uint64_t s_base;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t T = p.n_seg * p.part_tiles;  // CTAs in this launch
-    const uint32_t sl = blockIdx.x / p.part_tiles, lt = blockIdx.x % p.part_tiles;
+    const uint32_t T = gridDim.x;  // CTAs in this launch
+    const uint32_t sl = p.seg_lo + blockIdx.x / p.part_tiles, lt = blockIdx.x % p.part_tiles;
     const uint32_t tile = p.part_tile0 + lt;
     const uint32_t w0 = tile * (kMergeThreads * WPT) + tid * WPT;
     const bool active = tile < p.tiles_per_seg && w0 < p.words_proc;
@@ -555,7 +555,8 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 8 ? 3 : 4) merge_coop_ke
         grid.sync();
         if (live && wid == 0) {
             // exclusive prefix over the earlier tiles of this segment in this part
-            const uint32_t* cs = p.counts + uint64_t(k) * T + uint64_t(sl) * p.part_tiles;
+            const uint32_t* cs =
+                p.counts + uint64_t(k) * T + uint64_t(sl - p.seg_lo) * p.part_tiles;
             uint64_t acc = 0, all = 0;
             for (uint32_t i = lane; i < p.part_tiles; i += 32) {
                 const uint32_t v = __ldcg(cs + i);
@@ -876,7 +877,7 @@ static cudaError_t coop_launch_t(const CoopParams& p, size_t smem, cudaStream_t 
     CoopParams q = p;
     void* args[] = {&q};
     return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(merge_coop_kernel<WPT>),
-                                       dim3(p.n_seg * p.part_tiles), dim3(kMergeThreads), args,
+                                       dim3(p.seg_cnt * p.part_tiles), dim3(kMergeThreads), args,
                                        smem, st);
 }
 

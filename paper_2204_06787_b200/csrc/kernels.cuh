@@ -48,6 +48,7 @@ struct CoopParams {
     uint32_t n_stages, stage, k_steps;  // k_steps: max merges of this stage over segments
     uint32_t n_seg, s_first, tiles_per_seg, words_proc, wst, ml, max_slots;
     uint32_t part, n_parts, part_tile0, part_tiles;  // tiles of each segment in this launch
+    uint32_t seg_lo, seg_cnt;     // owned segments [seg_lo, seg_lo + seg_cnt) in this launch
     uint32_t n_merges;
     uint64_t seg_bits;            // L
     const uint32_t* leaves;       // leaf(w, sl) = leaves + ((w/ml*n_seg + sl)*ml + w%ml)*wst

@@ -142,6 +142,8 @@ marsit_ctx::~marsit_ctx() {
     }
     for (auto e : event_pool) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_extract) cudaEventDestroy(ev_extract);
+    for (auto e : ev_merge) cudaEventDestroy(e);
     for (int b = 0; b < 2; ++b) {
         if (ev_coin_done[b]) cudaEventDestroy(ev_coin_done[b]);
         if (coin_buf[b]) cudaFree(coin_buf[b]);
@@ -330,19 +332,25 @@ marsit_status run_allgather(marsit_ctx* ctx, cudaStream_t st) {
 
 marsit_status run_decode(marsit_ctx* ctx, const void* const* g, const void* const* c,
                          void* const* c_out, void* const* params, void* update, double eta,
-                         cudaStream_t st) {
+                         cudaStream_t st, uint32_t seg0 = 0, uint32_t n = 0) {
     cudaEvent_t ev;
     marsit_status s = ctx->begin_phase(st, &ev);
     if (s) return s;
     const bool vec = vec_ok_ptrs(ctx, g, c) && vec_ok_ptrs(ctx, (const void* const*)c_out, c) &&
                      (!params || vec_ok_ptrs(ctx, (const void* const*)params, c)) &&
                      (!update || aligned16(update));
-    if (ctx->dtype == MARSIT_F32)
-        CUDA_TRY(launch_decode(stream_params<float>(ctx, g, c, c_out, update, eta, params), vec,
-                               ctx->decode_grid, st));
-    else
-        CUDA_TRY(launch_decode(stream_params<double>(ctx, g, c, c_out, update, eta, params), vec,
-                               ctx->decode_grid, st));
+    if (!n) n = ctx->S;
+    if (ctx->dtype == MARSIT_F32) {
+        auto p = stream_params<float>(ctx, g, c, c_out, update, eta, params);
+        p.seg0 = seg0;
+        p.n_proc = n;
+        CUDA_TRY(launch_decode(p, vec, ctx->decode_grid, st));
+    } else {
+        auto p = stream_params<double>(ctx, g, c, c_out, update, eta, params);
+        p.seg0 = seg0;
+        p.n_proc = n;
+        CUDA_TRY(launch_decode(p, vec, ctx->decode_grid, st));
+    }
     return ctx->end_phase(kPhDecode, st, ev, 1);
 }
 
@@ -543,6 +551,42 @@ marsit_status sign_round_impl(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_
     if (s) return s;
     if (ctx->G > 1 && !ctx->comm)
         return fail(MARSIT_EUNSUPPORTED, "external-transport context: use marsit_round_phase");
+    if (ctx->pipeline) {
+        // st : coins? E ............ D0 D1 ... D(S-1)   (D_s waits M_s)
+        // aux:           M0 M1 ... M(S-1) coins(t+1)      (after E)
+        if ((s = run_coins(ctx, seed, t, st))) return s;
+        if ((s = run_extract(ctx, d_grads, d_comp, st))) return s;
+        CUDA_TRY(cudaEventRecord(ctx->ev_extract, st));
+        CUDA_TRY(cudaStreamWaitEvent(ctx->aux, ctx->ev_extract, 0));
+        ctx->coins_pending = false;  // aux is ordered after this round's coin kernel
+        for (uint32_t sg = 0; sg < ctx->S; ++sg) {
+            cudaEvent_t ev;
+            if ((s = ctx->begin_phase(ctx->aux, &ev))) return s;
+            uint64_t nl = 0;
+            if ((s = ctx->merge.run(ctx->bits, ctx->agg, ctx->coin_buf[ctx->cur_coin], seed, t,
+                                    ctx->aux, &nl, sg, 1)))
+                return s;
+            if ((s = ctx->end_phase(kPhMerge, ctx->aux, ev, nl))) return s;
+            CUDA_TRY(cudaEventRecord(ctx->ev_merge[sg], ctx->aux));
+        }
+        if (ctx->coin_total_words && ctx->coin_prefetch) {  // aux is ordered after the merges
+            const int b = 1 - ctx->cur_coin;
+            cudaEvent_t ev;
+            if ((s = ctx->begin_phase(ctx->aux, &ev))) return s;
+            CUDA_TRY(launch_coins(ctx->merge.d_merges, ctx->merge.dp.n_merges, seed, t + 1,
+                                  ctx->coin_buf[b], ctx->coin_grid_x, ctx->aux));
+            if ((s = ctx->end_phase(kPhCoins, ctx->aux, ev, 1))) return s;
+            CUDA_TRY(cudaEventRecord(ctx->ev_coin_done[b], ctx->aux));
+            ctx->coin_tag[b] = {true, seed, t + 1};
+        }
+        for (uint32_t sg = 0; sg < ctx->S; ++sg) {
+            CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_merge[sg], 0));
+            if ((s = run_decode(ctx, d_grads, d_comp, d_comp_out, params, d_update, eta_s, st, sg,
+                                1)))
+                return s;
+        }
+        return run_export(ctx, d_agg_bits, st);  // st waited on the last merge
+    }
     if ((s = sign_phase(ctx, 0, t, eta_s, seed, d_grads, d_comp, d_comp_out, params, d_agg_bits,
                         d_update, st)))
         return s;
@@ -745,7 +789,15 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     if (const char* e = std::getenv("MARSIT_COIN_FRAC")) frac = std::atof(e);
     uint64_t max_words = 0;
     assign_coin_budget(mr.dp, ctx->s_own, ctx->L, frac, &ctx->coin_total_words, &max_words);
-    if ((st = mr.configure(ctx->sm_count))) return st;
+    // single GPU with several segments: per-segment merge launches sized to
+    // co-reside with the decode (MARSIT_PIPELINE=0 disables)
+    ctx->pipeline = G == 1 && ctx->S >= 2 && env_int("MARSIT_PIPELINE", 0) != 0 &&
+                    desc->transport != MARSIT_TRANSPORT_EXTERNAL;
+    if (ctx->pipeline) {
+        if ((st = mr.configure(ctx->sm_count, 1, env_int("MARSIT_PIPE_MERGE_CTAS", 1)))) return st;
+    } else {
+        if ((st = mr.configure(ctx->sm_count))) return st;
+    }
     if ((st = mr.upload())) return st;
 
     const size_t wst = ctx->wst;
@@ -769,6 +821,11 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
             CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_coin_done[b], cudaEventDisableTiming));
         }
     ctx->coin_prefetch = env_int("MARSIT_COIN_PREFETCH", 1) != 0;
+    if (ctx->pipeline) {
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_extract, cudaEventDisableTiming));
+        ctx->ev_merge.resize(ctx->S);
+        for (auto& e : ctx->ev_merge) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     {
         // MARSIT_COIN_CTAS (default 4) CTAs per SM in total, split across the
         // merges (one warp per 64-word chunk)
