@@ -74,25 +74,25 @@ struct MergeRunner {
     int wpt = 1;
     size_t smem = 0;
     uint32_t seg_per_launch = 1;  // owned segments per cooperative launch
-    uint32_t tiles_per_seg = 0, part_tiles = 0, n_parts = 1;
+    uint32_t tiles_per_seg = 0, part_tiles = 0, n_parts = 1, tile_words = 0;
     std::vector<uint32_t> k_steps;  // per stage: max merges over segments
     DevMerge* d_merges = nullptr;
     uint32_t* d_seg_begin = nullptr;
     uint32_t* d_stage_begin = nullptr;
     uint32_t* gnodes = nullptr;
-    uint32_t* counts = nullptr;
+    uint64_t* flags = nullptr;  // [kmax][seg_per_launch * part_tiles]
     uint64_t* part_totals = nullptr;
+    uint32_t epoch = 0;
 
     MergeRunner() = default;
     MergeRunner(const MergeRunner&) = delete;
     MergeRunner& operator=(const MergeRunner&) = delete;
     ~MergeRunner() {
         for (void* p : {(void*)d_merges, (void*)d_seg_begin, (void*)d_stage_begin, (void*)gnodes,
-                        (void*)counts, (void*)part_totals})
+                        (void*)flags, (void*)part_totals})
             if (p) cudaFree(p);
     }
 
-    // Tiling: minimise the number of parts, then the words per thread.
     // seg_launch: owned segments per launch (1: per-segment pipeline);
     // cta_limit: CTAs per SM left to the merge (0: all it can get).
     marsit_status configure(int sm_count, uint32_t seg_launch = 0, int cta_limit = 0) {
@@ -103,8 +103,15 @@ struct MergeRunner {
                 const uint32_t* sb = &dp.stage_begin[size_t(sl) * (dp.n_stages + 1)];
                 k_steps[st] = std::max(k_steps[st], sb[st + 1] - sb[st]);
             }
+        // Tiling (measured on B200, tools/sweep_merge.sh): fewest parts (launches)
+        // first; among those, the smallest words per thread whose grid stays
+        // within 2 CTAs per SM — each step is a chain of latencies (scan, grid
+        // barrier, prefix, coin loads) whose cost grows with both the words per
+        // thread and the number of CTAs meeting at the barrier.  Optionally
+        // (MARSIT_MERGE_BALANCE=k) the grid is k CTAs per SM exactly.
         const int forced = env_int("MARSIT_MERGE_WPT", 0);
-        uint64_t best_parts = ~0ull;
+        const int balance = env_int("MARSIT_MERGE_BALANCE", 0);
+        uint64_t best_parts = ~0ull, best_ctas = 0;
         for (int w : {1, 2, 4, 8}) {
             if (forced && w != forced) continue;
             const size_t sm = size_t(std::max<uint32_t>(dp.max_slots, 1)) * w * kMergeThreads * 4;
@@ -113,14 +120,32 @@ struct MergeRunner {
             CUDA_TRY(merge_coop_occupancy(w, sm, &occ));
             if (cta_limit > 0) occ = std::min(occ, cta_limit);
             const uint64_t cap = uint64_t(occ) * sm_count;
-            const uint64_t tps = ceil_div(words_proc, uint64_t(w) * kMergeThreads);
+            const uint64_t tw_max = uint64_t(w) * kMergeThreads;
+            const uint64_t gran = std::max(w, 4);  // a thread's words never straddle tiles
+            const uint64_t tps_min = ceil_div(words_proc, tw_max);
+            uint64_t tps = tps_min, tw = round_up(ceil_div(words_proc, tps), gran);
+            if (balance > 0 && balance <= occ && seg_per_launch == 1) {
+                // trailing tiles may be empty: they only take part in the barriers
+                const uint64_t t = uint64_t(balance) * sm_count;
+                const uint64_t tww = round_up(ceil_div(words_proc, t), gran);
+                if (t >= tps_min && tww <= tw_max) {
+                    tps = t;
+                    tw = tww;
+                }
+            }
             const uint64_t pt = std::min<uint64_t>(tps, cap / seg_per_launch);
             if (pt == 0) continue;
             const uint64_t parts = ceil_div(tps, pt);
-            if (parts < best_parts) {
+            const uint64_t ctas = pt * seg_per_launch;
+            const uint64_t lim = 2ull * sm_count;
+            bool better = parts < best_parts;
+            if (parts == best_parts && best_ctas > lim && ctas <= lim) better = true;
+            if (better) {
                 best_parts = parts;
+                best_ctas = ctas;
                 wpt = w;
                 smem = sm;
+                tile_words = uint32_t(tw);
                 tiles_per_seg = uint32_t(tps);
                 part_tiles = uint32_t(pt);
                 n_parts = uint32_t(parts);
@@ -145,7 +170,9 @@ struct MergeRunner {
         CUDA_TRY(cudaMalloc(&gnodes, sizeof(uint32_t) * size_t(n_seg) * gmax * wst));
         uint32_t kmax = 1;
         for (uint32_t k : k_steps) kmax = std::max(kmax, k);
-        CUDA_TRY(cudaMalloc(&counts, sizeof(uint32_t) * size_t(kmax) * seg_per_launch * part_tiles));
+        const size_t nflags = size_t(kmax) * seg_per_launch * part_tiles;
+        CUDA_TRY(cudaMalloc(&flags, sizeof(uint64_t) * nflags));
+        CUDA_TRY(cudaMemset(flags, 0, sizeof(uint64_t) * nflags));
         CUDA_TRY(cudaMalloc(&part_totals, sizeof(uint64_t) * size_t(n_parts) * nm));
         CUDA_TRY(cudaMemset(part_totals, 0, sizeof(uint64_t) * size_t(n_parts) * nm));
         return MARSIT_OK;
@@ -165,6 +192,7 @@ struct MergeRunner {
         c.n_seg = n_seg;
         c.s_first = s_first;
         c.tiles_per_seg = tiles_per_seg;
+        c.tile_words = tile_words;
         c.words_proc = words_proc;
         c.wst = wst;
         c.ml = ml;
@@ -178,7 +206,7 @@ struct MergeRunner {
         c.gmax = std::max<uint32_t>(dp.gmax, 1);
         c.agg = agg;
         c.coins = coins;
-        c.counts = counts;
+        c.flags = flags;
         c.part_totals = part_totals;
         c.seed = seed;
         c.round = round;
@@ -192,6 +220,13 @@ struct MergeRunner {
                 for (uint32_t part = 0; part < n_parts; ++part) {
                     c.part = part;
                     c.part_tile0 = part * part_tiles;
+                    if (++epoch == 0) {  // 2^32 launches: clear the tags once
+                        const size_t nflags = size_t(*std::max_element(k_steps.begin(), k_steps.end())) *
+                                              seg_per_launch * part_tiles;
+                        CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(uint64_t) * std::max<size_t>(nflags, 1), st));
+                        epoch = 1;
+                    }
+                    c.epoch = epoch;
                     CUDA_TRY(launch_merge_coop(c, wpt, smem, st));
                     ++*n_launch;
                 }

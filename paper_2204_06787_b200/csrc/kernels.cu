@@ -464,19 +464,37 @@ __device__ __forceinline__ void load_words(const uint32_t* p, uint32_t (&v)[WPT]
     }
 }
 
+#ifdef MARSIT_COOP_PROF
+}  // namespace
+__device__ unsigned long long g_coop_prof[8];
+namespace {
+__device__ __forceinline__ uint64_t gtime_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define COOP_T(v) const uint64_t v = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0
+#define COOP_ADD(slot_, val_) if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&g_coop_prof[slot_], (unsigned long long)(val_))
+#else
+#define COOP_T(v)
+#define COOP_ADD(i, x)
+#endif
+
 template <int WPT>
 __global__ void __launch_bounds__(kMergeThreads, WPT >= 8 ? 3 : 4) merge_coop_kernel(const CoopParams p) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     extern __shared__ uint32_t cslots[];  // [max_slots][WPT][kMergeThreads]
     __shared__ uint32_t s_warp[kMergeThreads / 32];
+    __shared__ uint64_t s_acc[kMergeThreads / 32];
     __shared__ uint64_t s_base;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t T = gridDim.x;  // CTAs in this launch
     const uint32_t sl = p.seg_lo + blockIdx.x / p.part_tiles, lt = blockIdx.x % p.part_tiles;
     const uint32_t tile = p.part_tile0 + lt;
-    const uint32_t w0 = tile * (kMergeThreads * WPT) + tid * WPT;
-    const bool active = tile < p.tiles_per_seg && w0 < p.words_proc;
+    // a tile is tile_words (<= 256 * WPT, multiple of 4) consecutive words
+    const uint32_t w0 = tile * p.tile_words + tid * WPT;
+    const bool active = tile < p.tiles_per_seg && tid * WPT < p.tile_words && w0 < p.words_proc;
     // valid bits of my words: all 32 while rem >= 32 (bits beyond L stay 0)
     const int64_t rem0 = int64_t(p.seg_bits) - int64_t(w0) * 32;
     auto vmask = [&](int j) -> uint32_t {
@@ -513,6 +531,7 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 8 ? 3 : 4) merge_coop_ke
     }
     uint32_t r[WPT], d[WPT];
     for (uint32_t k = 0; k < p.k_steps; ++k) {
+        COOP_T(t0);
         const bool live = k < nm;
         const uint32_t mi = kb + k;  // merge index within the segment
         DevMerge m{};
@@ -551,40 +570,45 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 8 ? 3 : 4) merge_coop_ke
             warp_off += w < wid ? v : 0u;
             tile_total += v;
         }
-        if (tid == 0) p.counts[uint64_t(k) * T + blockIdx.x] = tile_total;
+        // publish this tile's count for step k, then one grid-wide barrier
+        uint64_t* flags = p.flags + uint64_t(k) * T;
+        if (tid == 0) __stcg(reinterpret_cast<unsigned long long*>(flags + blockIdx.x),
+                             (unsigned long long)tile_total);
+        COOP_T(t1);
         grid.sync();
-        if (live && wid == 0) {
-            // exclusive prefix over the earlier tiles of this segment in this part
-            const uint32_t* cs =
-                p.counts + uint64_t(k) * T + uint64_t(sl - p.seg_lo) * p.part_tiles;
-            uint64_t acc = 0, all = 0;
-            for (uint32_t i = lane; i < p.part_tiles; i += 32) {
-                const uint32_t v = __ldcg(cs + i);
-                acc += i < lt ? v : 0u;
-                all += v;
-            }
+        // exclusive draw offset: the counts of this segment's earlier tiles in
+        // this launch, read block-wide (all loads in flight at once)
+        const uint32_t seg_base = blockIdx.x - lt;
+        uint64_t acc = 0;
+        if (live)
+            for (uint32_t i = tid; i < lt; i += kMergeThreads) acc += __ldcg(flags + seg_base + i);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                acc += __shfl_xor_sync(kFull, acc, o);
-                all += __shfl_xor_sync(kFull, all, o);
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+        if (lane == 0) s_acc[wid] = acc;
+        __syncthreads();
+        COOP_T(t2);
+        if (live && tid == 0) {
+            uint64_t pre = 0;
+#pragma unroll
+            for (int w = 0; w < kMergeThreads / 32; ++w) pre += s_acc[w];
+            const uint32_t nmerges = p.n_merges;
+            uint64_t base = m.base_add;  // draws of this stream before this merge
+            for (uint32_t q = 0; q < p.part; ++q)  // earlier parts (earlier launches)
+                base += __ldcg(p.part_totals + uint64_t(q) * nmerges + mb + mi);
+            for (int32_t src = m.offset_src; src >= 0;) {  // continued stream (earlier stage)
+                const DevMerge& pm = p.merges[mb + src];
+                for (uint32_t q = 0; q < p.n_parts; ++q)
+                    base += __ldcg(p.part_totals + uint64_t(q) * nmerges + mb + src);
+                base += pm.base_add;
+                src = pm.offset_src;
             }
-            if (lane == 0) {
-                const uint32_t nmerges = p.n_merges;
-                uint64_t base = m.base_add;  // draws of this stream before this merge
-                for (uint32_t q = 0; q < p.part; ++q)  // earlier parts of this merge
-                    base += __ldcg(p.part_totals + uint64_t(q) * nmerges + mb + mi);
-                for (int32_t src = m.offset_src; src >= 0;) {  // continued stream (earlier stage)
-                    const DevMerge& pm = p.merges[mb + src];
-                    for (uint32_t q = 0; q < p.n_parts; ++q)
-                        base += __ldcg(p.part_totals + uint64_t(q) * nmerges + mb + src);
-                    base += pm.base_add;
-                    src = pm.offset_src;
-                }
-                s_base = base + acc;
-                if (lt == 0) p.part_totals[uint64_t(p.part) * nmerges + mb + mi] = all;
-            }
+            s_base = base + pre;
+            // the last tile of the part knows the part's total for this merge
+            if (lt == p.part_tiles - 1 || tile + 1 == p.tiles_per_seg)
+                p.part_totals[uint64_t(p.part) * nmerges + mb + mi] = pre + tile_total;
         }
         __syncthreads();
+        COOP_T(t3);
         if (live) {
             const uint64_t n0 = s_base + warp_off + (incl - cnt);  // my first coin's draw
             if (n0 + cnt <= uint64_t(m.coin_words) * 32) {
@@ -633,6 +657,12 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 8 ? 3 : 4) merge_coop_ke
         // s_warp / s_base are rewritten next step; slots are read by the
         // writing thread only
         __syncthreads();
+        COOP_T(t4);
+        COOP_ADD(0, t1 - t0);
+        COOP_ADD(1, t2 - t1);
+        COOP_ADD(2, t3 - t2);
+        COOP_ADD(3, t4 - t3);
+        COOP_ADD(4, 1);
     }
 }
 
@@ -1007,4 +1037,12 @@ MARSIT_INSTANTIATE(double)
 
 }  // namespace marsit_b200
 
-
+#ifdef MARSIT_COOP_PROF
+extern "C" void marsit_debug_coop_prof(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, marsit_b200::g_coop_prof, sizeof(marsit_b200::g_coop_prof));
+    if (reset) {
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(marsit_b200::g_coop_prof, z, sizeof(z));
+    }
+}
+#endif

@@ -47,6 +47,7 @@ struct CoopParams {
     const uint32_t* stage_begin;  // [n_seg][n_stages+1] merge ranges per stage
     uint32_t n_stages, stage, k_steps;  // k_steps: max merges of this stage over segments
     uint32_t n_seg, s_first, tiles_per_seg, words_proc, wst, ml, max_slots;
+    uint32_t tile_words;          // words per tile (<= 256 * WPT, multiple of max(WPT, 4))
     uint32_t part, n_parts, part_tile0, part_tiles;  // tiles of each segment in this launch
     uint32_t seg_lo, seg_cnt;     // owned segments [seg_lo, seg_lo + seg_cnt) in this launch
     uint32_t n_merges;
@@ -56,7 +57,8 @@ struct CoopParams {
     uint32_t gmax;
     uint32_t* agg;                // [S][wst]
     const uint32_t* coins;        // precomputed coin bitstreams
-    uint32_t* counts;             // [k_steps][n_seg * part_tiles] popcount of each tile
+    uint64_t* flags;              // [k_steps][CTAs] popcount of each tile
+    uint32_t epoch;               // launch counter (unused by the barrier version)
     uint64_t* part_totals;        // [n_parts][n_merges] draws consumed per (part, merge)
     uint64_t seed, round;
 };
