@@ -206,6 +206,36 @@ marsit_status marsit_ctx_check(marsit_ctx* ctx, void* stream);
 marsit_status marsit_ctx_set_timing(marsit_ctx* ctx, int enable);
 marsit_status marsit_ctx_timing(marsit_ctx* ctx, float* ms, uint64_t* launches, int reset);
 
+/* On-device round metrics.  Replaces the trainer's
+ * per-round figures: matching_rate (analysis.hpp:244-253 against the mean of
+ * u_w = g_w + c_w, trainer.hpp:241-251, 280-281), the round's BitsAccount
+ * (bits_account.hpp:15-40) and the merge disagreement counters (coins drawn,
+ * merge.hpp:44-53).  When enabled, the decode kernel forms the fp64 mean of u
+ * over the workers and counts matches in the same pass (no extra HBM
+ * traffic); the merge kernel's per-merge draw totals give the disagreements.
+ * Matching needs every worker of the job on this context (G == 1); with an
+ * NCCL communicator the disagreement counters are summed over the ranks
+ * (marsit_ctx_metrics is then collective); with the external transport they
+ * cover this rank's owned segments (rank_local = 1). */
+typedef struct marsit_round_metrics {
+    uint64_t round;             /* t of the last round run on the context */
+    int32_t valid;              /* 0: no round has run yet */
+    int32_t full_precision;     /* 1: the last round was dense (no sign metrics) */
+    int32_t has_matching;       /* 1: matches / matching_rate are set */
+    int32_t rank_local;         /* 1: disagreement counters cover this rank only */
+    uint64_t dim;
+    uint64_t matches;           /* coordinates with bit == (mean(u) >= 0) */
+    double matching_rate;       /* matches / dim */
+    uint64_t merges;            /* merges evaluated (one per reduce delivery) */
+    uint64_t compared_bits;     /* merges * L */
+    uint64_t disagreements;     /* coins drawn = sum over merges of popcount(r ^ l) */
+    double disagreement_rate;   /* disagreements / compared_bits */
+    uint64_t round_bits;        /* BitsAccount total of the last round */
+} marsit_round_metrics;
+marsit_status marsit_ctx_set_metrics(marsit_ctx* ctx, int enable);
+/* Waits for `stream`, then reports the last round's metrics. */
+marsit_status marsit_ctx_metrics(marsit_ctx* ctx, marsit_round_metrics* out, void* stream);
+
 /* Synthetic input recipes generated on the device:
  * recipe 0 = dyadic, 1 = correlated.  d_out: D elements of dtype. */
 marsit_status marsit_fill_recipe(int recipe, uint64_t seed, uint64_t worker, uint64_t round,
@@ -262,6 +292,10 @@ marsit_status marsit_driver_state(const marsit_driver* drv, uint64_t* next_round
  * (checkpoint.hpp:18-91) does not keep.  Synchronises `stream`. */
 marsit_status marsit_driver_save(marsit_driver* drv, const char* path, void* stream);
 marsit_status marsit_driver_load(marsit_driver* drv, const char* path, void* stream);
+/* Round metrics of the last step summed over the buckets (matching over all D
+ * coordinates, as trainer.hpp:280-281 records it per round). */
+marsit_status marsit_driver_set_metrics(marsit_driver* drv, int enable);
+marsit_status marsit_driver_metrics(marsit_driver* drv, marsit_round_metrics* out, void* stream);
 
 /* Parameters in the reference's checkpoint format (checkpoint.hpp:18-91:
  * "marsit-ckpt\0", u32 version 1, u64 D, D little-endian doubles), from / to

@@ -170,6 +170,14 @@ int orc_merge_signs(const uint64_t* recv, uint32_t c_recv, const uint64_t* local
 /* allreduce.hpp:148-189 driving detail::run_schedule (51-73) and the lock-step
  * Transport (transport.hpp:18-47): every sender's payload is snapshotted
  * before any delivery of the step; deliveries happen in ascending sender order. */
+/* statistics of the most recent orc_allreduce_sign call (orc_last_sign_stats) */
+static uint64_t g_last_draws, g_last_merges;
+
+void orc_last_sign_stats(uint64_t* draws, uint64_t* merges) {
+    *draws = g_last_draws;
+    *merges = g_last_merges;
+}
+
 int orc_allreduce_sign(uint32_t workers, uint32_t segments, size_t seg_len,
                        const uint64_t* signs, uint32_t steps, const uint8_t* phase,
                        const uint32_t* send_to, const uint32_t* recv_from,
@@ -188,6 +196,7 @@ int orc_allreduce_sign(uint32_t workers, uint32_t segments, size_t seg_len,
     for (size_t i = 0; i < (size_t)workers * segments; ++i) out_counts[i] = 1;
     for (uint32_t w = 0; w < workers; ++w) bits_per_worker[w] = 0;
     *reduce_bits = *gather_bits = 0;
+    g_last_draws = g_last_merges = 0;
 
     for (uint32_t k = 0; k < steps; ++k) {
         const uint32_t* st_ = send_to + (size_t)k * workers;
@@ -214,6 +223,7 @@ int orc_allreduce_sign(uint32_t workers, uint32_t segments, size_t seg_len,
                                          seg_len, key, &used[(size_t)to * segments + s], dst);
                 if (rc) { st = rc; goto done; }
                 *cnt = inbox_count[from] + *cnt;
+                ++g_last_merges;
             } else {
                 memcpy(dst, inbox + (size_t)from * nw, nw * sizeof(uint64_t));
                 *cnt = inbox_count[from];
@@ -221,6 +231,8 @@ int orc_allreduce_sign(uint32_t workers, uint32_t segments, size_t seg_len,
         }
     }
 done:
+    /* every draw of a (receiver, segment) stream is one disagreeing coordinate */
+    for (size_t i = 0; i < (size_t)workers * segments; ++i) g_last_draws += used[i];
     free(used);
     free(inbox);
     free(inbox_count);

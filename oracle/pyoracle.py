@@ -83,6 +83,8 @@ def lib():
         L.orc_gen_dyadic.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_size_t, _f64p]
         L.orc_gen_correlated.restype = None
         L.orc_gen_correlated.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_size_t, _f64p]
+        L.orc_last_sign_stats.argtypes = [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.orc_last_sign_stats.restype = None
         _lib = L
     return _lib
 
@@ -259,6 +261,8 @@ class RoundResult:
     bits_per_worker: np.ndarray
     reduce_bits: int
     gather_bits: int
+    draws: int = 0    # coins drawn over all merges (sign rounds, oracle path)
+    merges: int = 0   # merges evaluated
 
 
 def marsit_round(tables: Tables, t: int, period, eta_s: float, grads: np.ndarray,
@@ -286,8 +290,29 @@ def marsit_round(tables: Tables, t: int, period, eta_s: float, grads: np.ndarray
                                     comp.ravel(), tables.steps, ph, st, rf, sg, seed, upd,
                                     cout.ravel(), agg, C.byref(fp), bpw, C.byref(rb),
                                     C.byref(gb))
+    draws = merges = 0
+    if not use_ref and not fp.value:
+        d, m = C.c_uint64(), C.c_uint64()
+        lib().orc_last_sign_stats(C.byref(d), C.byref(m))
+        draws, merges = d.value, m.value
     return RoundResult(rc, upd, cout, agg[:words64(dim)], bool(fp.value), bpw, rb.value,
-                       gb.value)
+                       gb.value, draws, merges)
+
+
+def matching_count(agg_bits: np.ndarray, grads: np.ndarray, comp: np.ndarray) -> int:
+    """analysis.hpp:244-253 on the input mean of trainer.hpp:241-251: the number
+    of coordinates whose aggregate bit equals (mean_w(g_w + c_w) >= 0), the mean
+    summed in fp64 in worker order from 0.0 and divided by M."""
+    grads = np.asarray(grads, np.float64)
+    comp = np.asarray(comp, np.float64)
+    W, dim = grads.shape
+    mean = np.zeros(dim)
+    for w in range(W):
+        mean += grads[w] + comp[w]
+    mean /= float(W)
+    bits = np.unpackbits(np.ascontiguousarray(agg_bits, "<u8").view(np.uint8),
+                         bitorder="little")[:dim].astype(bool)
+    return int(np.count_nonzero(bits == (mean >= 0.0)))
 
 
 def fnv1a64(words: np.ndarray) -> int:

@@ -213,6 +213,35 @@ def _stream_ptr(device):
     return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
+@dataclass
+class RoundMetrics:
+    """Per-round figures of merit computed on the device:
+    matching_rate as analysis.hpp:244-253 against the mean of u = g + c
+    (trainer.hpp:241-251), the round's BitsAccount total, and the merge
+    disagreement counters (coins drawn / bits compared)."""
+    round: int
+    valid: bool
+    full_precision: bool
+    has_matching: bool
+    rank_local: bool
+    dim: int
+    matches: int
+    matching_rate: Optional[float]
+    merges: int
+    compared_bits: int
+    disagreements: int
+    disagreement_rate: float
+    round_bits: int
+
+    @classmethod
+    def from_c(cls, m) -> "RoundMetrics":
+        return cls(int(m.round), bool(m.valid), bool(m.full_precision), bool(m.has_matching),
+                   bool(m.rank_local), int(m.dim), int(m.matches),
+                   float(m.matching_rate) if m.has_matching else None, int(m.merges),
+                   int(m.compared_bits), int(m.disagreements), float(m.disagreement_rate),
+                   int(m.round_bits))
+
+
 class Context:
     """Owns a marsit_ctx (device scratch + compiled plan + optional NCCL comm)."""
 
@@ -303,6 +332,18 @@ class Context:
 
     def set_timing(self, on: bool):
         _check(N.lib().marsit_ctx_set_timing(self._h, int(on)))
+
+    def set_metrics(self, on: bool):
+        """Fused on-device round metrics (matching count in the decode,
+        per-merge disagreement totals from the merge)."""
+        _check(N.lib().marsit_ctx_set_metrics(self._h, int(on)))
+
+    def metrics(self, stream=None) -> RoundMetrics:
+        """The last round's metrics (waits for the stream)."""
+        m = N.RoundMetrics()
+        _check(N.lib().marsit_ctx_metrics(self._h, C.byref(m), stream if stream is not None
+                                          else _stream_ptr(self.device)))
+        return RoundMetrics.from_c(m)
 
     def timing(self, reset: bool = False):
         ms = (C.c_float * N.N_PHASES)()
@@ -505,6 +546,15 @@ class Driver:
         t, bits, nb = C.c_uint64(), C.c_uint64(), C.c_uint32()
         _check(N.lib().marsit_driver_state(self._h, C.byref(t), C.byref(bits), C.byref(nb)))
         return {"next_round": t.value, "cum_bits": bits.value, "buckets": nb.value}
+
+    def set_metrics(self, on: bool):
+        _check(N.lib().marsit_driver_set_metrics(self._h, int(on)))
+
+    def metrics(self) -> "RoundMetrics":
+        """Last step's metrics summed over the buckets (trainer.hpp:278-281)."""
+        m = N.RoundMetrics()
+        _check(N.lib().marsit_driver_metrics(self._h, C.byref(m), _stream_ptr(self.device)))
+        return RoundMetrics.from_c(m)
 
     def save(self, path: str):
         _check(N.lib().marsit_driver_save(self._h, path.encode(), _stream_ptr(self.device)))

@@ -48,6 +48,16 @@ class ExchangeLayout(C.Structure):
 # Every symbol include/marsit_b200.h declares: name -> (restype, argtypes)
 _vp, _u32, _u64, _i32, _dbl = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int, C.c_double
 _pvp = C.POINTER(C.c_void_p)
+class RoundMetrics(C.Structure):
+    """marsit_round_metrics (include/marsit_b200.h)."""
+    _fields_ = [("round", C.c_uint64), ("valid", C.c_int32), ("full_precision", C.c_int32),
+                ("has_matching", C.c_int32), ("rank_local", C.c_int32), ("dim", C.c_uint64),
+                ("matches", C.c_uint64), ("matching_rate", C.c_double),
+                ("merges", C.c_uint64), ("compared_bits", C.c_uint64),
+                ("disagreements", C.c_uint64), ("disagreement_rate", C.c_double),
+                ("round_bits", C.c_uint64)]
+
+
 SIGNATURES = {
     "marsit_schedule_ring": (_i32, [_u32, _pvp]),
     "marsit_schedule_torus": (_i32, [_u32, _u32, _pvp]),
@@ -75,6 +85,10 @@ SIGNATURES = {
                                    C.POINTER(_u64)]),
     "marsit_ctx_check": (_i32, [_vp, _vp]),
     "marsit_ctx_set_timing": (_i32, [_vp, _i32]),
+    "marsit_ctx_set_metrics": (_i32, [_vp, _i32]),
+    "marsit_ctx_metrics": (_i32, [_vp, C.POINTER(RoundMetrics), _vp]),
+    "marsit_driver_set_metrics": (_i32, [_vp, _i32]),
+    "marsit_driver_metrics": (_i32, [_vp, C.POINTER(RoundMetrics), _vp]),
     "marsit_ctx_timing": (_i32, [_vp, _vp, _vp, _i32]),
     "marsit_fill_recipe": (_i32, [_i32, _u64, _u64, _u64, _u64, _i32, _vp, _vp]),
     "marsit_nccl_unique_id": (_i32, [_vp]),

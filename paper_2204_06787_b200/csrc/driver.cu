@@ -151,7 +151,7 @@ marsit_status marsit_driver_step(marsit_driver* drv, const void* const* d_grads,
         marsit_status s;
         if (dense) {
             void* mean = upd ? upd : static_cast<char*>(drv->scratch) + boff;
-            s = dense_round_any(b.ctx, g.data(), (const void* const*)c.data(), c.data(),
+            s = dense_round_any(b.ctx, drv->t, g.data(), (const void* const*)c.data(), c.data(),
                                 d_params ? x.data() : nullptr, mean, st);
         } else {
             s = sign_round_impl(b.ctx, drv->t, drv->eta, bucket_seed(drv->seed, bi, nb), g.data(),
@@ -179,6 +179,42 @@ marsit_status marsit_driver_state(const marsit_driver* drv, uint64_t* next_round
     if (next_round) *next_round = drv->t;
     if (cum_bits) *cum_bits = drv->cum_bits;
     if (n_buckets) *n_buckets = uint32_t(drv->buckets.size());
+    return MARSIT_OK;
+}
+
+marsit_status marsit_driver_set_metrics(marsit_driver* drv, int enable) {
+    if (!drv) return fail(MARSIT_EPARAM, "driver is null");
+    marsit_status s;
+    for (auto& b : drv->buckets)
+        if ((s = marsit_ctx_set_metrics(b.ctx, enable))) return s;
+    return MARSIT_OK;
+}
+
+marsit_status marsit_driver_metrics(marsit_driver* drv, marsit_round_metrics* out, void* stream) {
+    if (!drv || !out) return fail(MARSIT_EPARAM, "null argument");
+    *out = marsit_round_metrics{};
+    out->has_matching = 1;
+    marsit_status s;
+    for (auto& b : drv->buckets) {
+        marsit_round_metrics m{};
+        if ((s = marsit_ctx_metrics(b.ctx, &m, stream))) return s;
+        out->round = m.round;
+        out->valid = m.valid;
+        out->full_precision = m.full_precision;
+        out->has_matching &= m.has_matching;
+        out->rank_local |= m.rank_local;
+        out->dim += m.dim;
+        out->matches += m.matches;
+        out->merges += m.merges;
+        out->compared_bits += m.compared_bits;
+        out->disagreements += m.disagreements;
+        out->round_bits += m.round_bits;
+    }
+    if (!out->valid || out->full_precision) out->has_matching = 0;
+    if (!out->has_matching) out->matches = 0;
+    out->matching_rate = out->has_matching ? double(out->matches) / double(out->dim) : 0.0;
+    out->disagreement_rate =
+        out->compared_bits ? double(out->disagreements) / double(out->compared_bits) : 0.0;
     return MARSIT_OK;
 }
 

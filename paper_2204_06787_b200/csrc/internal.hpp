@@ -293,6 +293,11 @@ struct marsit_ctx {
     // NCCL
     ncclComm_t comm = nullptr;
     bool owns_comm = true;
+    // on-device round metrics (marsit_ctx_set_metrics)
+    bool metrics = false;
+    unsigned long long* d_metrics = nullptr;  // [0] matches, [1..2] NCCL sum scratch
+    bool last_valid = false, last_dense = false, last_matching = false;
+    uint64_t last_t = 0;
     // timing
     bool timing = false;
     std::vector<marsit_b200::TimedPair> pending;
@@ -315,7 +320,7 @@ marsit_status sign_round_impl(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_
                               void* const* comp_out, void* const* params, uint64_t* agg_bits,
                               void* update, cudaStream_t st);
 // One dense round (sync.hpp:78-87); mean is required; params may be null.
-marsit_status dense_round_any(marsit_ctx* ctx, const void* const* grads, const void* const* comp,
+marsit_status dense_round_any(marsit_ctx* ctx, uint64_t t, const void* const* grads, const void* const* comp,
                               void* const* comp_out, void* const* params, void* mean,
                               cudaStream_t st);
 // marsit_ctx_create, optionally sharing an existing communicator (driver buckets).

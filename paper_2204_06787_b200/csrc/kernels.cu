@@ -374,6 +374,135 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode
 }
 
 // ---------------------------------------------------------------------------
+// K3/K4 with the round's matching count fused in (analysis.hpp:244-253 on the
+// input mean of trainer.hpp:241-251): every local worker of one coordinate
+// block in the same task, so the fp64 sum of u_w = g_w + c_w in worker order
+// is formed in registers while the decode reads g and c anyway — no extra
+// HBM traffic.  matches += [aggregate bit == (sum / M >= 0)] over the D
+// coordinates.  Needs every worker of the job local (p.ml == M).
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void decode_one(const StreamParams<T>& p, uint32_t wl, uint64_t gi,
+                                           T gt, T& u) {
+    u = add_rn(p.g[wl][gi], p.c[wl][gi]);
+    p.c_out[wl][gi] = sub_rn(u, gt);
+    if (wl == 0 && p.update) p.update[gi] = gt;
+    if (p.x[wl]) p.x[wl][gi] = sub_rn(p.x[wl][gi], gt);
+}
+
+template <typename T, bool VEC>
+// register cap: two CTAs per SM leave room for the coin precompute
+// of the next round, which runs beside the decode on the side stream
+__global__ void __maxnreg__(sizeof(T) == 4 ? 80 : 128) decode_stats_kernel(const StreamParams<T> p) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t warps = gridDim.x * (kStreamThreads / 32);
+    const uint32_t tasks_per_seg = (p.words_proc + kTaskWords - 1) / kTaskWords;
+    const uint64_t n_tasks = uint64_t(tasks_per_seg) * p.n_proc;
+    const T eta = p.eta;
+    const double wm = double(p.n_workers);  // the mean divides by M (trainer.hpp:249)
+    uint64_t matches = 0;
+    for (uint64_t task = blockIdx.x * (kStreamThreads / 32) + (threadIdx.x >> 5); task < n_tasks;
+         task += warps) {
+        const uint32_t q = uint32_t(task % tasks_per_seg);
+        const uint32_t s = p.seg0 + uint32_t(task / tasks_per_seg);
+        const uint64_t seg0 = uint64_t(s) * p.seg_len;
+        const uint64_t j0 = uint64_t(q) * (kTaskWords * 32);
+        const uint32_t* aw = p.agg + uint64_t(s) * p.wst + q * kTaskWords;
+        // full task: all 512 coordinates real, 16-byte aligned quads
+        const bool full = VEC && j0 + kTaskWords * 32 <= p.seg_len &&
+                          seg0 + j0 + kTaskWords * 32 <= p.dim;
+        if (full) {
+            // two passes of two sub-chunks: 8 fp64 sums, and worker w + 1's
+            // loads in flight while worker w is computed (the buffers of
+            // different workers never overlap)
+#pragma unroll 1
+            for (int half = 0; half < 2; ++half) {
+                uint32_t nib[2];
+                double sum[2][4];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int sub = 2 * half + h;
+                    const uint32_t word = __ldg(aw + sub * 4 + (lane >> 3));
+                    nib[h] = (word >> ((lane & 7) * 4)) & 0xFu;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) sum[h][k] = 0.0;
+                }
+                const uint64_t gb = seg0 + j0 + half * 256 + lane * 4;  // + h * 128
+                Quad<T> gv[2], cv[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    gv[h] = load4(p.g[0] + gb + h * 128);
+                    cv[h] = load4_rw(p.c[0] + gb + h * 128);
+                }
+                for (uint32_t wl = 0; wl < p.ml; ++wl) {
+                    Quad<T> gn[2], cn[2];
+                    if (wl + 1 < p.ml) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            gn[h] = load4(p.g[wl + 1] + gb + h * 128);
+                            cn[h] = load4_rw(p.c[wl + 1] + gb + h * 128);
+                        }
+                    }
+                    T* xp = p.x[wl];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint64_t gi = gb + h * 128;
+                        Quad<T> out, up;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const T gt = ((nib[h] >> k) & 1u) ? eta : -eta;
+                            const T u = add_rn(gv[h].v[k], cv[h].v[k]);
+                            sum[h][k] = __dadd_rn(sum[h][k], double(u));
+                            out.v[k] = sub_rn(u, gt);
+                            up.v[k] = gt;
+                        }
+                        store4(p.c_out[wl] + gi, out);
+                        if (wl == 0 && p.update) store4(p.update + gi, up);
+                        if (xp) {
+                            Quad<T> xv = load4_rw(xp + gi);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) xv.v[k] = sub_rn(xv.v[k], up.v[k]);
+                            store4(xp + gi, xv);
+                        }
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        gv[h] = gn[h];
+                        cv[h] = cn[h];
+                    }
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        matches += (((nib[h] >> k) & 1u) != 0) == (__ddiv_rn(sum[h][k], wm) >= 0.0);
+            }
+        } else {
+            // ragged task (segment / vector tail or unaligned buffers): per coordinate
+#pragma unroll 1
+            for (int t = 0; t < kTaskWords; ++t) {
+                const uint64_t j = j0 + t * 32 + lane;
+                const uint64_t gi = seg0 + j;
+                if (j < p.seg_len && gi < p.dim) {
+                    const uint32_t bit = (__ldg(aw + t) >> lane) & 1u;
+                    const T gt = bit ? eta : -eta;
+                    double sum = 0.0;
+                    for (uint32_t wl = 0; wl < p.ml; ++wl) {
+                        T u;
+                        decode_one(p, wl, gi, gt, u);
+                        sum = __dadd_rn(sum, double(u));
+                    }
+                    matches += (bit != 0) == (__ddiv_rn(sum, wm) >= 0.0);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) matches += __shfl_xor_sync(kFull, matches, o);
+    if (lane == 0 && matches) atomicAdd(p.matches, (unsigned long long)matches);
+}
+
+// ---------------------------------------------------------------------------
 // K2: the merge DAG of every owned segment.
 //
 // A CTA takes a 1024-word tile (32768 coordinates) of one segment and runs
@@ -886,7 +1015,12 @@ cudaError_t launch_extract(const StreamParams<T>& p, bool vec, int grid, cudaStr
 
 template <typename T>
 cudaError_t launch_decode(const StreamParams<T>& p, bool vec, int grid, cudaStream_t st) {
-    if (vec)
+    if (p.matches) {
+        if (vec)
+            decode_stats_kernel<T, true><<<grid, kStreamThreads, 0, st>>>(p);
+        else
+            decode_stats_kernel<T, false><<<grid, kStreamThreads, 0, st>>>(p);
+    } else if (vec)
         decode_kernel<T, true><<<grid, kStreamThreads, 0, st>>>(p);
     else
         decode_kernel<T, false><<<grid, kStreamThreads, 0, st>>>(p);

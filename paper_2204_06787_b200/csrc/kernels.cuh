@@ -80,6 +80,10 @@ struct StreamParams {
     T* x[kMaxLocalWorkers];      // optional replica parameters: x -= g_t (trainer.hpp:285-288)
     T eta;
     int* err;
+    // decode only: when set, the decode also counts the coordinates whose
+    // aggregate bit equals (mean of u over the n_workers workers >= 0)
+    unsigned long long* matches;
+    uint32_t n_workers;
 };
 
 // Launch wrappers (kernels.cu).

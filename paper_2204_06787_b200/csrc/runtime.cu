@@ -134,7 +134,7 @@ marsit_status lower_plan(const Plan& plan, uint32_t s_first, uint32_t n_seg, Dev
 marsit_ctx::~marsit_ctx() {
     if (device >= 0) cudaSetDevice(device);
     for (void* p : {(void*)bits, (void*)recv, (void*)agg, (void*)err, dense_send, dense_recv,
-                    dense_mean, (void*)d_dense_ops, (void*)d_dense_final})
+                    dense_mean, (void*)d_dense_ops, (void*)d_dense_final, (void*)d_metrics})
         if (p) cudaFree(p);
     for (auto& tp : pending) {
         cudaEventDestroy(tp.a);
@@ -340,15 +340,26 @@ marsit_status run_decode(marsit_ctx* ctx, const void* const* g, const void* cons
                      (!params || vec_ok_ptrs(ctx, (const void* const*)params, c)) &&
                      (!update || aligned16(update));
     if (!n) n = ctx->S;
+    // matching count fused into the decode (needs every worker local)
+    unsigned long long* matches = nullptr;
+    if (ctx->metrics && ctx->ml == ctx->M) {
+        if (seg0 == 0) CUDA_TRY(cudaMemsetAsync(ctx->d_metrics, 0, sizeof(unsigned long long), st));
+        matches = ctx->d_metrics;
+        ctx->last_matching = true;
+    }
     if (ctx->dtype == MARSIT_F32) {
         auto p = stream_params<float>(ctx, g, c, c_out, update, eta, params);
         p.seg0 = seg0;
         p.n_proc = n;
+        p.matches = matches;
+        p.n_workers = ctx->M;
         CUDA_TRY(launch_decode(p, vec, ctx->decode_grid, st));
     } else {
         auto p = stream_params<double>(ctx, g, c, c_out, update, eta, params);
         p.seg0 = seg0;
         p.n_proc = n;
+        p.matches = matches;
+        p.n_workers = ctx->M;
         CUDA_TRY(launch_decode(p, vec, ctx->decode_grid, st));
     }
     return ctx->end_phase(kPhDecode, st, ev, 1);
@@ -528,6 +539,13 @@ marsit_status sign_phase(marsit_ctx* ctx, int phase, uint64_t t, double eta_s, u
     return run_export(ctx, d_agg_bits, st);
 }
 
+void note_round(marsit_ctx* ctx, uint64_t t, bool dense) {
+    ctx->last_valid = true;
+    ctx->last_t = t;
+    ctx->last_dense = dense;
+    ctx->last_matching = false;  // set by the decode when it counts
+}
+
 marsit_status check_round_args(marsit_ctx* ctx, double eta_s, const void* const* d_grads,
                                const void* const* d_comp, void* const* d_comp_out,
                                void* const* params, bool sign) {
@@ -551,6 +569,7 @@ marsit_status sign_round_impl(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_
     if (s) return s;
     if (ctx->G > 1 && !ctx->comm)
         return fail(MARSIT_EUNSUPPORTED, "external-transport context: use marsit_round_phase");
+    note_round(ctx, t, false);
     if (ctx->pipeline) {
         // st : coins? E ............ D0 D1 ... D(S-1)   (D_s waits M_s)
         // aux:           M0 M1 ... M(S-1) coins(t+1)      (after E)
@@ -599,7 +618,7 @@ marsit_status sign_round_impl(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_
                       d_update, st);
 }
 
-marsit_status dense_round_any(marsit_ctx* ctx, const void* const* d_grads,
+marsit_status dense_round_any(marsit_ctx* ctx, uint64_t t, const void* const* d_grads,
                               const void* const* d_comp, void* const* d_comp_out,
                               void* const* params, void* d_mean, cudaStream_t st) {
     marsit_status s = check_round_args(ctx, 1.0, d_grads, d_comp, d_comp_out, params, false);
@@ -607,6 +626,7 @@ marsit_status dense_round_any(marsit_ctx* ctx, const void* const* d_grads,
     if (!d_mean) return fail(MARSIT_EPARAM, "mean is null");
     if (ctx->G > 1 && !ctx->comm)
         return fail(MARSIT_EUNSUPPORTED, "external-transport context: use marsit_round_phase");
+    note_round(ctx, t, true);
     if ((s = dense_phase_any(ctx, 0, d_grads, d_comp, d_comp_out, params, d_mean, st))) return s;
     if ((s = dense_exchange(ctx, st))) return s;
     if ((s = dense_phase_any(ctx, 1, d_grads, d_comp, d_comp_out, params, d_mean, st))) return s;
@@ -919,10 +939,10 @@ marsit_status marsit_sign_round(marsit_ctx* ctx, uint64_t t, double eta_s, uint6
                            d_update, static_cast<cudaStream_t>(stream));
 }
 
-marsit_status marsit_dense_round(marsit_ctx* ctx, uint64_t, const void* const* d_grads,
+marsit_status marsit_dense_round(marsit_ctx* ctx, uint64_t t, const void* const* d_grads,
                                  const void* const* d_comp, void* const* d_comp_out, void* d_mean,
                                  void* stream) {
-    return dense_round_any(ctx, d_grads, d_comp, d_comp_out, nullptr, d_mean,
+    return dense_round_any(ctx, t, d_grads, d_comp, d_comp_out, nullptr, d_mean,
                            static_cast<cudaStream_t>(stream));
 }
 
@@ -974,6 +994,7 @@ marsit_status marsit_round_phase(marsit_ctx* ctx, int phase, uint64_t t, uint64_
     marsit_status s = check_round_args(ctx, eta_s, d_grads, d_comp, d_comp_out, nullptr, !dense);
     if (s) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (phase == 0) note_round(ctx, t, dense);
     if (dense) {
         if (!d_update) return fail(MARSIT_EPARAM, "dense round needs d_update for the mean");
         return dense_phase_any(ctx, phase, d_grads, d_comp, d_comp_out, nullptr, d_update, st);
@@ -1124,6 +1145,62 @@ marsit_status marsit_ctx_check(marsit_ctx* ctx, void* stream) {
         CUDA_TRY(cudaStreamSynchronize(st));
         return fail(MARSIT_ENONFINITE, "DenseVector: non-finite entry");
     }
+    return MARSIT_OK;
+}
+
+marsit_status marsit_ctx_set_metrics(marsit_ctx* ctx, int enable) {
+    if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    if (enable && !ctx->d_metrics) {
+        CUDA_TRY(cudaMalloc(&ctx->d_metrics, 4 * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMemset(ctx->d_metrics, 0, 4 * sizeof(unsigned long long)));
+    }
+    ctx->metrics = enable != 0;
+    return MARSIT_OK;
+}
+
+marsit_status marsit_ctx_metrics(marsit_ctx* ctx, marsit_round_metrics* out, void* stream) {
+    if (!ctx || !out) return fail(MARSIT_EPARAM, "null argument");
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    *out = marsit_round_metrics{};
+    out->round = ctx->last_t;
+    out->valid = ctx->last_valid ? 1 : 0;
+    out->full_precision = ctx->last_dense ? 1 : 0;
+    out->dim = ctx->D;
+    marsit_bits_account(ctx, ctx->last_dense ? 1 : 0, nullptr, nullptr, nullptr, &out->round_bits);
+    if (!ctx->last_valid || ctx->last_dense) return MARSIT_OK;
+    if (ctx->last_matching) {
+        unsigned long long m = 0;
+        CUDA_TRY(cudaMemcpyAsync(&m, ctx->d_metrics, sizeof(m), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        out->has_matching = 1;
+        out->matches = m;
+        out->matching_rate = double(m) / double(ctx->D);
+    }
+    // per-merge draw totals of the owned segments, [part][merge]
+    const MergeRunner& mr = ctx->merge;
+    std::vector<uint64_t> tot(size_t(mr.n_parts) * mr.dp.n_merges);
+    if (!tot.empty())
+        CUDA_TRY(cudaMemcpyAsync(tot.data(), mr.part_totals, sizeof(uint64_t) * tot.size(),
+                                 cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    unsigned long long agg[2] = {0, mr.dp.n_merges};
+    for (uint64_t v : tot) agg[0] += v;
+    if (ctx->G > 1 && ctx->comm) {
+        if (!ctx->d_metrics) CUDA_TRY(cudaMalloc(&ctx->d_metrics, 4 * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMemcpyAsync(ctx->d_metrics + 1, agg, sizeof(agg), cudaMemcpyHostToDevice, st));
+        NCCL_TRY(ncclAllReduce(ctx->d_metrics + 1, ctx->d_metrics + 1, 2, ncclUint64, ncclSum,
+                               ctx->comm, st));
+        CUDA_TRY(cudaMemcpyAsync(agg, ctx->d_metrics + 1, sizeof(agg), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    out->rank_local = (ctx->G > 1 && !ctx->comm) ? 1 : 0;
+    out->disagreements = agg[0];
+    out->merges = agg[1];
+    out->compared_bits = agg[1] * ctx->L;
+    out->disagreement_rate =
+        out->compared_bits ? double(out->disagreements) / double(out->compared_bits) : 0.0;
     return MARSIT_OK;
 }
 
