@@ -236,6 +236,39 @@ marsit_status marsit_ctx_set_metrics(marsit_ctx* ctx, int enable);
 /* Waits for `stream`, then reports the last round's metrics. */
 marsit_status marsit_ctx_metrics(marsit_ctx* ctx, marsit_round_metrics* out, void* stream);
 
+/* ------------------------------------------------------------------------
+ * SSDM baseline collectives (the paper's comparison points).
+ *   marsit_ssdm_compress   = ssdm_compress (ssdm.hpp:29-40) of one vector with
+ *                            RngStream(seed, ssdm, worker, round, segment);
+ *                            d_bits: ceil(len/64) u64 words; *norm_out on the
+ *                            host (synchronises `stream`)
+ *   marsit_ssdm_decompress = ssdm_decompress (ssdm.hpp:44-56)
+ *   marsit_ssdm_allreduce  = cascading_allreduce (allreduce.hpp:205-262, mode
+ *                            MARSIT_SSDM_CASCADING) or sum_ssdm_allreduce
+ *                            (275-339, MARSIT_SSDM_SUM) over the context's
+ *                            schedule: d_vectors[w] = worker w's D elements,
+ *                            d_estimate = the D-element estimate every worker
+ *                            ends with.  Ring schedules only
+ *                            (MARSIT_EUNSUPPORTED otherwise, as the reference);
+ *                            every worker on this context (G == 1).  The
+ *                            BitsAccount outputs and max_abs_per_step[steps]
+ *                            (sum mode) are optional host outputs; asking for
+ *                            them in sum mode synchronises `stream`.
+ * The l2 norm is summed in a fixed parallel order: equal to the reference's
+ * sequential sum whenever that sum is exact, within a few ulps otherwise.
+ * ---------------------------------------------------------------------- */
+typedef enum marsit_ssdm_mode { MARSIT_SSDM_CASCADING = 0, MARSIT_SSDM_SUM = 1 } marsit_ssdm_mode;
+marsit_status marsit_ssdm_compress(const void* d_v, uint64_t len, marsit_dtype dtype, uint64_t seed,
+                                   uint64_t worker, uint64_t round, uint64_t segment,
+                                   uint64_t* d_bits, double* norm_out, void* stream);
+marsit_status marsit_ssdm_decompress(const uint64_t* d_bits, uint64_t len, double norm,
+                                     marsit_dtype dtype, void* d_out, void* stream);
+marsit_status marsit_ssdm_allreduce(marsit_ctx* ctx, int mode, uint64_t round, uint64_t seed,
+                                    const void* const* d_vectors, void* d_estimate,
+                                    uint64_t* bits_per_worker, uint64_t* reduce_bits,
+                                    uint64_t* gather_bits, int64_t* max_abs_per_step,
+                                    void* stream);
+
 /* Synthetic input recipes generated on the device:
  * recipe 0 = dyadic, 1 = correlated.  d_out: D elements of dtype. */
 marsit_status marsit_fill_recipe(int recipe, uint64_t seed, uint64_t worker, uint64_t round,

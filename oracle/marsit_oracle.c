@@ -384,6 +384,197 @@ done:
     return st;
 }
 
+/* ---- SSDM baselines ---------------------------------------------------- */
+
+#define ORC_PURPOSE_SSDM 4 /* rng.hpp:18 */
+
+/* rng.hpp:46-54: next_uniform = (x >> 11) * 2^-53; next_bernoulli(p) = u < p */
+static double uniform_of(uint64_t x) { return (double)(x >> 11) * 0x1.0p-53; }
+
+/* ssdm.hpp:29-40 (DenseVector::l2_norm, dense_vector.hpp:41-45: acc += v*v) */
+double orc_ssdm_compress(const double* v, size_t len, uint64_t key, uint64_t* bits) {
+    double acc = 0.0;
+    for (size_t j = 0; j < len; ++j) acc += v[j] * v[j];
+    const double norm = sqrt(acc);
+    memset(bits, 0, ((len + 63) / 64) * sizeof(uint64_t));
+    const double denom = norm > 0.0 ? 2.0 * norm : 0.0;
+    for (size_t j = 0; j < len; ++j) {
+        const double p = denom > 0.0 ? 0.5 + v[j] / denom : 0.5;
+        if (uniform_of(orc_draw(key, j)) < p) bits[j >> 6] |= (uint64_t)1 << (j & 63);
+    }
+    return norm;
+}
+
+/* ssdm.hpp:44-56 */
+void orc_ssdm_decompress(const uint64_t* bits, size_t len, double norm, double* out) {
+    for (size_t j = 0; j < len; ++j)
+        out[j] = norm == 0.0 ? 0.0 : (get_bit(bits, j) ? norm : -norm);
+}
+
+/* elias.hpp:14-31: gamma length of zigzag(s) + 1 */
+static uint64_t signed_sum_code_length(int64_t s) {
+    const uint64_t z = ((uint64_t)s << 1) ^ (uint64_t)(s >> 63);
+    uint64_t n = z + 1, width = 0;
+    while (n) { ++width; n >>= 1; }
+    return 2 * width - 1;
+}
+
+/* allreduce.hpp:205-262.  State per (worker, segment): the dense raw segment
+ * (segmentation.hpp:32-53, value padding 0.0) and an optional packet. */
+int orc_cascading_allreduce(uint32_t workers, uint32_t segments, size_t dim,
+                            const double* vectors, uint32_t steps, const uint8_t* phase,
+                            const uint32_t* send_to, const uint32_t* recv_from,
+                            const uint32_t* segment, int is_ring, uint64_t seed, uint64_t round,
+                            double* out_estimate, uint64_t* bits_per_worker,
+                            uint64_t* reduce_bits, uint64_t* gather_bits) {
+    if (!is_ring) return ORC_EUNSUPPORTED;
+    int st = orc_validate_schedule(workers, segments, steps, send_to, recv_from, segment);
+    if (st) return st;
+    if (dim == 0) return ORC_EPARAM;
+    const size_t L = (dim + segments - 1) / segments, nw = (L + 63) / 64;
+    const size_t n_ws = (size_t)workers * segments;
+    double* raw = (double*)calloc(n_ws * L, sizeof(double));
+    uint64_t* pk_bits = (uint64_t*)calloc(n_ws * nw, sizeof(uint64_t));
+    double* pk_norm = (double*)calloc(n_ws, sizeof(double));
+    uint8_t* has = (uint8_t*)calloc(n_ws, 1);
+    uint64_t* in_bits = (uint64_t*)malloc(((size_t)workers * nw + 1) * sizeof(uint64_t));
+    double* in_norm = (double*)malloc(workers * sizeof(double));
+    double* dec = (double*)malloc(L * sizeof(double));
+    for (uint32_t w = 0; w < workers; ++w)
+        for (size_t j = 0; j < dim; ++j)
+            raw[(size_t)w * segments * L + j] = vectors[(size_t)w * dim + j];
+    for (uint32_t w = 0; w < workers; ++w) bits_per_worker[w] = 0;
+    *reduce_bits = *gather_bits = 0;
+    for (uint32_t k = 0; k < steps; ++k) {
+        const uint32_t* st_ = send_to + (size_t)k * workers;
+        const uint32_t* sg = segment + (size_t)k * workers;
+        for (uint32_t w = 0; w < workers; ++w) { /* make_payload: compress lazily */
+            const size_t i = (size_t)w * segments + sg[w];
+            if (!has[i]) {
+                const uint64_t key = orc_stream_key(seed, ORC_PURPOSE_SSDM, w, round, sg[w]);
+                pk_norm[i] = orc_ssdm_compress(raw + i * L, L, key, pk_bits + i * nw);
+                has[i] = 1;
+            }
+            memcpy(in_bits + (size_t)w * nw, pk_bits + i * nw, nw * sizeof(uint64_t));
+            in_norm[w] = pk_norm[i];
+            bits_per_worker[w] += (uint64_t)L + 32u; /* bits.size() + 32 */
+            if (phase[k] == ORC_PHASE_REDUCE) *reduce_bits += (uint64_t)L + 32u;
+            else *gather_bits += (uint64_t)L + 32u;
+        }
+        for (uint32_t from = 0; from < workers; ++from) { /* deliver in sender order */
+            const size_t i = (size_t)st_[from] * segments + sg[from];
+            if (phase[k] == ORC_PHASE_REDUCE) {
+                /* raw = add(ssdm_decompress(p), raw) */
+                orc_ssdm_decompress(in_bits + (size_t)from * nw, L, in_norm[from], dec);
+                for (size_t j = 0; j < L; ++j) {
+                    raw[i * L + j] = dec[j] + raw[i * L + j];
+                    if (!isfinite(raw[i * L + j])) { st = ORC_ENONFINITE; goto done; }
+                }
+            } else {
+                memcpy(pk_bits + i * nw, in_bits + (size_t)from * nw, nw * sizeof(uint64_t));
+                pk_norm[i] = in_norm[from];
+                has[i] = 1;
+            }
+        }
+    }
+    {
+        /* per worker: reassemble(scaled(ssdm_decompress(packet), 1/M)); consensus */
+        const double inv_m = 1.0 / (double)workers;
+        for (uint32_t w = 0; w < workers; ++w)
+            for (uint32_t s = 0; s < segments; ++s) {
+                const size_t i = (size_t)w * segments + s;
+                if (!has[i]) { st = ORC_EPROTOCOL; goto done; }
+                orc_ssdm_decompress(pk_bits + i * nw, L, pk_norm[i], dec);
+                for (size_t j = 0; j < L && (size_t)s * L + j < dim; ++j) {
+                    const double v = dec[j] * inv_m;
+                    double* o = out_estimate + (size_t)s * L + j;
+                    if (w == 0) *o = v;
+                    else if (!(*o == v)) { st = ORC_EPROTOCOL; goto done; }
+                }
+            }
+    }
+done:
+    free(raw); free(pk_bits); free(pk_norm); free(has); free(in_bits); free(in_norm); free(dec);
+    return st;
+}
+
+/* allreduce.hpp:275-339 */
+int orc_sum_ssdm_allreduce(uint32_t workers, uint32_t segments, size_t dim,
+                           const double* vectors, uint32_t steps, const uint8_t* phase,
+                           const uint32_t* send_to, const uint32_t* recv_from,
+                           const uint32_t* segment, int is_ring, uint64_t seed, uint64_t round,
+                           double* out_estimate, uint64_t* bits_per_worker,
+                           uint64_t* reduce_bits, uint64_t* gather_bits,
+                           int64_t* max_abs_per_step) {
+    if (!is_ring) return ORC_EUNSUPPORTED;
+    int st = orc_validate_schedule(workers, segments, steps, send_to, recv_from, segment);
+    if (st) return st;
+    if (dim == 0) return ORC_EPARAM;
+    const size_t L = (dim + segments - 1) / segments, nw = (L + 63) / 64;
+    const size_t n_ws = (size_t)workers * segments;
+    uint64_t* pk_bits = (uint64_t*)calloc(n_ws * nw, sizeof(uint64_t));
+    double* pk_norm = (double*)calloc(n_ws, sizeof(double));
+    int64_t* sums = (int64_t*)malloc(n_ws * L * sizeof(int64_t));
+    int64_t* inbox = (int64_t*)malloc(((size_t)workers * L + 1) * sizeof(int64_t));
+    double* part = (double*)calloc(L, sizeof(double));
+    double* dec = (double*)malloc(L * sizeof(double));
+    for (uint32_t w = 0; w < workers; ++w)
+        for (uint32_t s = 0; s < segments; ++s) { /* compress once, sums = +-1 */
+            const size_t i = (size_t)w * segments + s;
+            for (size_t j = 0; j < L; ++j) {
+                const size_t src = (size_t)s * L + j;
+                part[j] = src < dim ? vectors[(size_t)w * dim + src] : 0.0;
+            }
+            pk_norm[i] = orc_ssdm_compress(
+                part, L, orc_stream_key(seed, ORC_PURPOSE_SSDM, w, round, s), pk_bits + i * nw);
+            for (size_t j = 0; j < L; ++j) sums[i * L + j] = get_bit(pk_bits + i * nw, j) ? 1 : -1;
+        }
+    for (uint32_t w = 0; w < workers; ++w) bits_per_worker[w] = 0;
+    *reduce_bits = *gather_bits = 0;
+    for (uint32_t k = 0; k < steps; ++k) {
+        const uint32_t* st_ = send_to + (size_t)k * workers;
+        const uint32_t* sg = segment + (size_t)k * workers;
+        int64_t step_max = 0;
+        for (uint32_t w = 0; w < workers; ++w) {
+            const size_t i = (size_t)w * segments + sg[w];
+            uint64_t total = 32; /* norm side channel */
+            for (size_t j = 0; j < L; ++j) {
+                const int64_t v = sums[i * L + j];
+                inbox[(size_t)w * L + j] = v;
+                total += signed_sum_code_length(v);
+                const int64_t mag = v < 0 ? -v : v;
+                if (mag > step_max) step_max = mag;
+            }
+            bits_per_worker[w] += total;
+            if (phase[k] == ORC_PHASE_REDUCE) *reduce_bits += total;
+            else *gather_bits += total;
+        }
+        if (max_abs_per_step) max_abs_per_step[k] = step_max;
+        for (uint32_t from = 0; from < workers; ++from) {
+            int64_t* dst = sums + ((size_t)st_[from] * segments + sg[from]) * L;
+            const int64_t* src = inbox + (size_t)from * L;
+            if (phase[k] == ORC_PHASE_REDUCE) for (size_t j = 0; j < L; ++j) dst[j] += src[j];
+            else memcpy(dst, src, L * sizeof(int64_t));
+        }
+    }
+    {
+        /* mean of the individually decompressed packets, worker order, * 1/M */
+        const double inv_m = 1.0 / (double)workers;
+        for (uint32_t s = 0; s < segments; ++s) {
+            for (size_t j = 0; j < L; ++j) part[j] = 0.0;
+            for (uint32_t w = 0; w < workers; ++w) {
+                const size_t i = (size_t)w * segments + s;
+                orc_ssdm_decompress(pk_bits + i * nw, L, pk_norm[i], dec);
+                for (size_t j = 0; j < L; ++j) part[j] += dec[j];
+            }
+            for (size_t j = 0; j < L && (size_t)s * L + j < dim; ++j)
+                out_estimate[(size_t)s * L + j] = part[j] * inv_m;
+        }
+    }
+    free(pk_bits); free(pk_norm); free(sums); free(inbox); free(part); free(dec);
+    return st;
+}
+
 void orc_gen_dyadic(uint64_t seed, uint64_t worker, uint64_t round, size_t dim, double* out) {
     uint64_t key = orc_stream_key(seed, ORC_PURPOSE_TRIAL, worker, round, 0);
     for (size_t j = 0; j < dim; ++j) {

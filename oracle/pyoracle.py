@@ -28,6 +28,7 @@ STATUS = {0: "ok", 1: "parameter_error", 2: "non_finite_error", 3: "protocol_err
           4: "unsupported_error", 9: "other"}
 
 _u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
 _u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 _u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
 _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
@@ -85,6 +86,17 @@ def lib():
         L.orc_gen_correlated.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_size_t, _f64p]
         L.orc_last_sign_stats.argtypes = [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.orc_last_sign_stats.restype = None
+        L.orc_ssdm_compress.restype = C.c_double
+        L.orc_ssdm_compress.argtypes = [_f64p, C.c_size_t, C.c_uint64, _u64p]
+        L.orc_ssdm_decompress.restype = None
+        L.orc_ssdm_decompress.argtypes = [_u64p, C.c_size_t, C.c_double, _f64p]
+        for f in (L.orc_cascading_allreduce, L.orc_sum_ssdm_allreduce):
+            f.restype = C.c_int
+        _ss = [C.c_uint32, C.c_uint32, C.c_size_t, _f64p, C.c_uint32, _u8p, _u32p, _u32p, _u32p,
+               C.c_int, C.c_uint64, C.c_uint64, _f64p, _u64p, C.POINTER(C.c_uint64),
+               C.POINTER(C.c_uint64)]
+        L.orc_cascading_allreduce.argtypes = _ss
+        L.orc_sum_ssdm_allreduce.argtypes = _ss + [_i64p]
         _lib = L
     return _lib
 
@@ -120,6 +132,13 @@ def ref():
                                        C.c_uint32, C.c_uint32, C.c_size_t, _f64p, _f64p,
                                        C.c_uint64, _f64p, _f64p, _u64p, C.POINTER(C.c_int),
                                        _u64p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        R.ref_ssdm_compress.restype = C.c_int
+        R.ref_ssdm_compress.argtypes = [_f64p, C.c_size_t] + [C.c_uint64] * 4 + [
+            _u64p, C.POINTER(C.c_double)]
+        R.ref_ssdm_allreduce.restype = C.c_int
+        R.ref_ssdm_allreduce.argtypes = [C.c_int, C.c_int, C.c_uint32, C.c_uint32, C.c_size_t,
+                                         _f64p, C.c_uint64, C.c_uint64, _f64p, _u64p,
+                                         C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), _i64p]
         R.ref_bench_create.restype = C.c_void_p
         R.ref_bench_create.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_size_t, C.c_uint64]
         R.ref_bench_round.restype = C.c_double
@@ -313,6 +332,65 @@ def matching_count(agg_bits: np.ndarray, grads: np.ndarray, comp: np.ndarray) ->
     bits = np.unpackbits(np.ascontiguousarray(agg_bits, "<u8").view(np.uint8),
                          bitorder="little")[:dim].astype(bool)
     return int(np.count_nonzero(bits == (mean >= 0.0)))
+
+
+# ----------------------------------------------------------------------------
+# SSDM baselines (ssdm.hpp:29-56, allreduce.hpp:198-339)
+# ----------------------------------------------------------------------------
+PURPOSE_SSDM = 4  # rng.hpp:18
+
+
+def ssdm_compress(v: np.ndarray, seed: int, w: int, t: int, s: int, use_ref: bool = False):
+    """(bits words, norm) of ssdm_compress(v, RngStream(seed, ssdm, w, t, s))."""
+    v = np.ascontiguousarray(v, np.float64)
+    bits = np.zeros(words64(len(v)) + 1, np.uint64)
+    if use_ref:
+        nrm = C.c_double()
+        rc = ref().ref_ssdm_compress(v, len(v), seed, w, t, s, bits, C.byref(nrm))
+        assert rc == 0
+        return bits[:words64(len(v))], nrm.value
+    key = stream_key(seed, PURPOSE_SSDM, w, t, s)
+    nrm = lib().orc_ssdm_compress(v, len(v), key, bits)
+    return bits[:words64(len(v))], nrm
+
+
+def ssdm_decompress(bits: np.ndarray, length: int, norm: float) -> np.ndarray:
+    out = np.zeros(length, np.float64)
+    lib().orc_ssdm_decompress(np.ascontiguousarray(bits, np.uint64), length, norm, out)
+    return out
+
+
+@dataclass
+class SsdmResult:
+    status: int
+    estimate: np.ndarray
+    bits_per_worker: np.ndarray
+    reduce_bits: int
+    gather_bits: int
+    max_abs_per_step: np.ndarray
+
+
+def ssdm_allreduce(mode: str, tables: Tables, vectors: np.ndarray, seed: int, rnd: int,
+                   use_ref: bool = False) -> SsdmResult:
+    """mode 'cascading' (allreduce.hpp:205-262) or 'sum' (275-339)."""
+    W = tables.workers
+    vectors = np.ascontiguousarray(vectors, np.float64)
+    dim = vectors.shape[1]
+    out = np.zeros(dim, np.float64)
+    bpw = np.zeros(W, np.uint64)
+    rb, gb = C.c_uint64(), C.c_uint64()
+    mx = np.zeros(max(tables.steps, 1), np.int64)
+    m = 0 if mode == "cascading" else 1
+    if use_ref:
+        rc = ref().ref_ssdm_allreduce(m, tables.topology, tables.a, tables.b, dim, vectors.ravel(),
+                                      seed, rnd, out, bpw, C.byref(rb), C.byref(gb), mx)
+    else:
+        ph, st, rf, sg = _flat(tables)
+        args = (W, tables.segments, dim, vectors.ravel(), tables.steps, ph, st, rf, sg,
+                int(tables.topology == 0), seed, rnd, out, bpw, C.byref(rb), C.byref(gb))
+        rc = (lib().orc_cascading_allreduce(*args) if m == 0
+              else lib().orc_sum_ssdm_allreduce(*args, mx))
+    return SsdmResult(rc, out, bpw, rb.value, gb.value, mx[:tables.steps])
 
 
 def fnv1a64(words: np.ndarray) -> int:

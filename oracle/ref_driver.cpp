@@ -14,6 +14,7 @@
 #include <marsit/merge.hpp>
 #include <marsit/rng.hpp>
 #include <marsit/schedule.hpp>
+#include <marsit/ssdm.hpp>
 #include <marsit/sync.hpp>
 
 #include <chrono>
@@ -177,6 +178,52 @@ int ref_marsit_round(std::uint64_t t, int has_period, std::uint64_t period, doub
             bits_per_worker[w] = res.bits.per_worker[w];
         *reduce_bits = res.bits.reduce_bits;
         *gather_bits = res.bits.gather_bits;
+    });
+}
+
+// ---------------------------------------------------------------------------
+// SSDM baselines (ssdm.hpp:29-56, allreduce.hpp:198-339).
+// ---------------------------------------------------------------------------
+// ssdm_compress of v with RngStream(seed, ssdm, w, t, s).
+int ref_ssdm_compress(const double* v, std::size_t len, std::uint64_t seed, std::uint64_t w,
+                      std::uint64_t t, std::uint64_t s, std::uint64_t* bits, double* norm) {
+    return guarded([&] {
+        RngStream rng(seed, RngPurpose::ssdm, w, t, s);
+        SsdmPacket p = ssdm_compress(DenseVector(std::vector<double>(v, v + len)), rng);
+        to_words(p.bits, bits);
+        *norm = p.norm;
+    });
+}
+
+// cascading_allreduce (mode 0) / sum_ssdm_allreduce (mode 1).  vectors:
+// [M][D]; out: the consensus estimate (D); max_abs_per_step: [steps] (mode 1).
+int ref_ssdm_allreduce(int mode, int topology, std::uint32_t a, std::uint32_t b, std::size_t dim,
+                       const double* vectors, std::uint64_t seed, std::uint64_t round,
+                       double* out, std::uint64_t* bits_per_worker, std::uint64_t* reduce_bits,
+                       std::uint64_t* gather_bits, std::int64_t* max_abs_per_step) {
+    return guarded([&] {
+        const Schedule sched = make_schedule(topology, a, b);
+        std::vector<DenseVector> in;
+        for (std::uint32_t w = 0; w < sched.workers; ++w)
+            in.emplace_back(std::vector<double>(vectors + w * dim, vectors + (w + 1) * dim));
+        std::vector<DenseVector> per_worker;
+        BitsAccount bits(sched.workers);
+        if (mode == 0) {
+            CascadingAllreduceResult r = cascading_allreduce(in, sched, RoundContext{seed, round});
+            per_worker = std::move(r.per_worker);
+            bits = r.bits;
+        } else {
+            SumSsdmAllreduceResult r = sum_ssdm_allreduce(in, sched, RoundContext{seed, round});
+            per_worker = std::move(r.per_worker);
+            bits = r.bits;
+            for (std::size_t k = 0; k < r.max_abs_per_step.size(); ++k)
+                max_abs_per_step[k] = r.max_abs_per_step[k];
+        }
+        const DenseVector& est = consensus(per_worker);
+        std::memcpy(out, est.values().data(), dim * sizeof(double));
+        for (std::uint32_t w = 0; w < sched.workers; ++w) bits_per_worker[w] = bits.per_worker[w];
+        *reduce_bits = bits.reduce_bits;
+        *gather_bits = bits.gather_bits;
     });
 }
 

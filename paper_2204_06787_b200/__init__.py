@@ -455,6 +455,96 @@ def pack_signs(grads: Sequence, comp: Sequence, sched: Schedule):
     return out
 
 
+# --------------------------------------------------------------------------
+# SSDM baselines (ssdm.hpp:29-56, allreduce.hpp:198-339)
+# --------------------------------------------------------------------------
+@dataclass
+class SsdmPacket:
+    """ssdm.hpp:21-24: one sign bit per coordinate + the l2 norm."""
+    norm: float
+    bits: object  # int64 CUDA tensor, ceil(len/64) u64 words
+    length: int
+
+
+@dataclass
+class CascadingAllreduceResult:
+    per_worker: list  # the chain estimate of the mean (identical at every worker)
+    bits: BitsAccount
+
+
+@dataclass
+class SumSsdmAllreduceResult:
+    per_worker: list
+    bits: BitsAccount
+    max_abs_per_step: list
+
+
+def ssdm_compress(v, global_seed: int, worker: int, round_: int, segment: int) -> SsdmPacket:
+    """ssdm_compress (ssdm.hpp:29-40) with RngStream(seed, ssdm, worker, round, segment)."""
+    import torch
+    n = v.numel()
+    bits = torch.zeros((n + 63) // 64, dtype=torch.int64, device=v.device)
+    norm = C.c_double()
+    dev = v.device.index or 0
+    _check(N.lib().marsit_ssdm_compress(C.c_void_p(v.data_ptr()), n, _dtype_code(v),
+                                        global_seed, worker, round_, segment,
+                                        C.c_void_p(bits.data_ptr()), C.byref(norm),
+                                        _stream_ptr(dev)))
+    return SsdmPacket(norm.value, bits, n)
+
+
+def ssdm_decompress(packet: SsdmPacket, dtype=None):
+    """ssdm_decompress (ssdm.hpp:44-56): +-norm per coordinate (0 for norm 0)."""
+    import torch
+    dtype = dtype or torch.float64
+    out = torch.empty(packet.length, dtype=dtype, device=packet.bits.device)
+    dev = packet.bits.device.index or 0
+    _check(N.lib().marsit_ssdm_decompress(C.c_void_p(packet.bits.data_ptr()), packet.length,
+                                          packet.norm, _dtype_code(out),
+                                          C.c_void_p(out.data_ptr()), _stream_ptr(dev)))
+    return out
+
+
+def _ssdm(mode: int, vectors: Sequence, sched: Schedule, global_seed: int, round_: int):
+    import torch
+    if len(vectors) != sched.workers:
+        raise ParameterError("allreduce: vector count != schedule workers")
+    dim = vectors[0].numel()
+    if any(v.numel() != dim for v in vectors):
+        raise ParameterError("allreduce: inconsistent dimensions")
+    dev = vectors[0].device.index or 0
+    ctx = _context_for(dim, sched, vectors[0].dtype, dev)
+    out = torch.empty(dim, dtype=vectors[0].dtype, device=vectors[0].device)
+    M = sched.workers
+    pw = (C.c_uint64 * M)()
+    rb, gb = C.c_uint64(), C.c_uint64()
+    steps = max(sched.n_steps, 1)
+    mx = (C.c_int64 * steps)()
+    _check(N.lib().marsit_ssdm_allreduce(ctx._h, mode, round_, global_seed,
+                                         N.ptr_array([v.data_ptr() for v in vectors]),
+                                         C.c_void_p(out.data_ptr()), pw, C.byref(rb),
+                                         C.byref(gb), mx, _stream_ptr(dev)))
+    ctx.check()
+    bits = BitsAccount(list(pw), rb.value, gb.value, rb.value + gb.value)
+    return out, bits, list(mx)[:sched.n_steps]
+
+
+def cascading_allreduce(vectors: Sequence, sched: Schedule, global_seed: int,
+                        round_: int) -> CascadingAllreduceResult:
+    """cascading_allreduce (allreduce.hpp:205-262): every hop decompresses,
+    adds its own segment and recompresses; ring schedules only."""
+    out, bits, _ = _ssdm(0, vectors, sched, global_seed, round_)
+    return CascadingAllreduceResult([out] * sched.workers, bits)
+
+
+def sum_ssdm_allreduce(vectors: Sequence, sched: Schedule, global_seed: int,
+                       round_: int) -> SumSsdmAllreduceResult:
+    """sum_ssdm_allreduce (allreduce.hpp:275-339): integer sums of the signs on
+    the wire (Elias-gamma accounting), estimate = mean of the packets."""
+    out, bits, mx = _ssdm(1, vectors, sched, global_seed, round_)
+    return SumSsdmAllreduceResult([out] * sched.workers, bits, mx)
+
+
 def merge_signs(received: AggregateSign, local: AggregateSign, key: int, used: int = 0):
     """merge.hpp:34-58 on the device: returns (AggregateSign, draws consumed)."""
     import torch

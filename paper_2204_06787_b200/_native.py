@@ -86,6 +86,11 @@ SIGNATURES = {
     "marsit_ctx_check": (_i32, [_vp, _vp]),
     "marsit_ctx_set_timing": (_i32, [_vp, _i32]),
     "marsit_ctx_set_metrics": (_i32, [_vp, _i32]),
+    "marsit_ssdm_compress": (_i32, [_vp, _u64, _i32, _u64, _u64, _u64, _u64, _vp,
+                                    C.POINTER(_dbl), _vp]),
+    "marsit_ssdm_decompress": (_i32, [_vp, _u64, _dbl, _i32, _vp, _vp]),
+    "marsit_ssdm_allreduce": (_i32, [_vp, _i32, _u64, _u64, _vp, _vp, _vp,
+                                     C.POINTER(_u64), C.POINTER(_u64), _vp, _vp]),
     "marsit_ctx_metrics": (_i32, [_vp, C.POINTER(RoundMetrics), _vp]),
     "marsit_driver_set_metrics": (_i32, [_vp, _i32]),
     "marsit_driver_metrics": (_i32, [_vp, C.POINTER(RoundMetrics), _vp]),

@@ -244,6 +244,19 @@ struct TimedPair {
 
 }  // namespace marsit_b200
 
+namespace marsit_b200 {
+// Device scratch of the SSDM baselines (ssdm.cu), allocated on first use.
+struct SsdmScratch {
+    double* acc = nullptr;       // cascading accumulators [S][L]
+    uint32_t* pk = nullptr;      // packets [M][S][wst]
+    double* norms = nullptr;     // [M * S]
+    double* partial = nullptr;   // [M * S][chunks]
+    unsigned long long* hist = nullptr;  // [S][M][M+1]
+    uint8_t* chain = nullptr;    // [S][M]
+    ~SsdmScratch();
+};
+}  // namespace marsit_b200
+
 struct marsit_ctx {
     int device = 0;
     marsit_dtype dtype = MARSIT_F32;
@@ -293,6 +306,8 @@ struct marsit_ctx {
     // NCCL
     ncclComm_t comm = nullptr;
     bool owns_comm = true;
+    // SSDM baselines (ssdm.cu)
+    std::unique_ptr<marsit_b200::SsdmScratch> ssdm;
     // on-device round metrics (marsit_ctx_set_metrics)
     bool metrics = false;
     unsigned long long* d_metrics = nullptr;  // [0] matches, [1..2] NCCL sum scratch
@@ -323,6 +338,12 @@ marsit_status sign_round_impl(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_
 marsit_status dense_round_any(marsit_ctx* ctx, uint64_t t, const void* const* grads, const void* const* comp,
                               void* const* comp_out, void* const* params, void* mean,
                               cudaStream_t st);
+// cascading_allreduce / sum_ssdm_allreduce on the device (ssdm.cu).
+marsit_status ssdm_allreduce_impl(marsit_ctx* ctx, int mode, uint64_t round, uint64_t seed,
+                                  const void* const* d_vectors, void* d_estimate,
+                                  uint64_t* bits_per_worker, uint64_t* reduce_bits,
+                                  uint64_t* gather_bits, int64_t* max_abs_per_step,
+                                  cudaStream_t st);
 // marsit_ctx_create, optionally sharing an existing communicator (driver buckets).
 marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared_comm,
                                   marsit_ctx** out);

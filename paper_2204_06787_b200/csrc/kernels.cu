@@ -22,20 +22,12 @@
 #include <cstdint>
 
 #include "kernels.cuh"
+#include "rng.cuh"
 
 namespace marsit_b200 {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-
-// ---------------------------------------------------------------------------
-// Counter-based RNG (rng.hpp:28-73).  Draw n of a stream = mix(key + (n+1)γ).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t mix64(uint64_t z) {
-    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-    return z ^ (z >> 31);
-}
 
 // The same finalizer with the 64-bit shifts of the xor-shifts moved onto the
 // FMA pipe: for the low word, (lo >> s) == mulhi(lo, 2^(32-s)) and the bits
@@ -63,15 +55,6 @@ __device__ __forceinline__ uint64_t mix64f(uint64_t z) {
     hi = uint32_t(t >> 32);
     xorshr_fma(lo, hi, 1u << 1);  // >> 31
     return (uint64_t(hi) << 32) | lo;
-}
-
-__device__ __forceinline__ uint64_t stream_key(uint64_t seed, uint64_t purpose, uint64_t w,
-                                               uint64_t t, uint64_t s) {
-    uint64_t h = mix64(seed ^ 0x6a09e667f3bcc909ull);
-    h = mix64(h ^ (purpose * kGamma));
-    h = mix64(h ^ ((w + 1) * kGamma));
-    h = mix64(h ^ ((t + 1) * kGamma));
-    return mix64(h ^ ((s + 1) * kGamma));
 }
 
 // ---------------------------------------------------------------------------

@@ -198,6 +198,46 @@ def allreduces():
     return out
 
 
+def ssdm_cases():
+    """ssdm_compress (ssdm.hpp:29-40) and the two baseline all-reduces
+    (allreduce.hpp:205-262, 275-339) from the reference."""
+    rng = np.random.default_rng(11)
+    comp, allr = [], []
+    for n, kind in [(1, "gauss"), (21, "gauss"), (64, "gauss"), (100, "dyadic"), (130, "zero"),
+                    (33, "onehot")]:
+        if kind == "gauss":
+            v = rng.standard_normal(n)
+        elif kind == "dyadic":
+            v = O.gen_dyadic(3, 0, 1, n)
+        elif kind == "zero":
+            v = np.zeros(n)
+        else:
+            v = np.zeros(n)
+            v[n // 2] = 2.5
+        bits, norm = O.ssdm_compress(v, 77, 2, 5, 1, use_ref=True)
+        comp.append(dict(v=hx(v), seed=77, worker=2, round=5, segment=1, bits=wx(bits),
+                         norm=float(norm).hex()))
+    for mode in ("cascading", "sum"):
+        for a, D, recipe in [(4, 21, "gauss"), (5, 40, "gauss"), (3, 3, "dyadic"),
+                             (8, 1001, "dyadic"), (6, 5, "gauss"), (4, 4096, "dyadic"),
+                             (2, 7, "gauss")]:
+            T = O.schedule("ring", a, 0, use_ref=True)
+            if recipe == "dyadic":
+                v = inputs("dyadic", 2026, a, 3, D)
+                vec = None
+            else:
+                v = rng.standard_normal((a, D))
+                vec = hx(v)
+            r = O.ssdm_allreduce(mode, T, v, 2026, 3, use_ref=True)
+            assert r.status == 0
+            allr.append(dict(mode=mode, a=a, dim=D, recipe=recipe, vectors=vec, seed=2026,
+                             round=3, estimate=hx(r.estimate),
+                             bits_per_worker=[int(x) for x in r.bits_per_worker],
+                             reduce_bits=r.reduce_bits, gather_bits=r.gather_bits,
+                             max_abs_per_step=[int(x) for x in r.max_abs_per_step]))
+    return dict(compress=comp, allreduce=allr)
+
+
 def schedules():
     out = []
     for topo, a, b in [("ring", 2, 0), ("ring", 3, 0), ("ring", 8, 0), ("torus", 2, 2),
@@ -214,7 +254,8 @@ def main():
         O.build()
     assert O.ref_available(), "oracle/_ref/libmarsit_ref.so not built (needs /root/reference)"
     blobs = dict(anchors=anchors(), streams=streams(), merges=merges(),
-                 allreduce=allreduces(), schedules=schedules(), rounds=round_cases())
+                 allreduce=allreduces(), schedules=schedules(), rounds=round_cases(),
+                 ssdm=ssdm_cases())
     for name, obj in blobs.items():
         with open(os.path.join(HERE, name + ".json"), "w") as f:
             json.dump(obj, f, separators=(",", ":"))
