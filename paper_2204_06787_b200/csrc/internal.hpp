@@ -103,16 +103,19 @@ struct MergeRunner {
                 const uint32_t* sb = &dp.stage_begin[size_t(sl) * (dp.n_stages + 1)];
                 k_steps[st] = std::max(k_steps[st], sb[st + 1] - sb[st]);
             }
-        // Tiling (measured on B200, tools/sweep_merge.sh): fewest parts (launches)
-        // first; among those, the smallest words per thread whose grid stays
-        // within 2 CTAs per SM — each step is a chain of latencies (scan, grid
-        // barrier, prefix, coin loads) whose cost grows with both the words per
-        // thread and the number of CTAs meeting at the barrier.  Optionally
-        // (MARSIT_MERGE_BALANCE=k) the grid is k CTAs per SM exactly.
+        // Tiling (measured on B200, tools/sweep_merge_balance.sh, merge alone):
+        // fewest launches ("parts") first, then the lowest estimated step cost
+        //   cost = WPT * (k + 1) + 6 * [k >= 3],   k = CTAs on the busiest SM.
+        // Each merge step is a latency chain per thread that grows with the
+        // words per thread (WPT), and the busiest SM's ALU work (coin deposit)
+        // and the grid barrier grow with k.  Measured picks: G = 8 rank (1
+        // segment) WPT 2, G = 2 rank (4 segments) WPT 4, one GPU C3 (8
+        // segments) WPT 12.  MARSIT_MERGE_WPT forces the words per thread;
+        // MARSIT_MERGE_BALANCE = k forces exactly k CTAs per SM when possible.
         const int forced = env_int("MARSIT_MERGE_WPT", 0);
         const int balance = env_int("MARSIT_MERGE_BALANCE", 0);
-        uint64_t best_parts = ~0ull, best_ctas = 0;
-        for (int w : {1, 2, 4, 8}) {
+        uint64_t best_parts = ~0ull, best_cost = ~0ull;
+        for (int w : {1, 2, 4, 8, 12, 16}) {
             if (forced && w != forced) continue;
             const size_t sm = size_t(std::max<uint32_t>(dp.max_slots, 1)) * w * kMergeThreads * 4;
             if (sm > 160 * 1024) continue;
@@ -124,9 +127,10 @@ struct MergeRunner {
             const uint64_t gran = std::max(w, 4);  // a thread's words never straddle tiles
             const uint64_t tps_min = ceil_div(words_proc, tw_max);
             uint64_t tps = tps_min, tw = round_up(ceil_div(words_proc, tps), gran);
-            if (balance > 0 && balance <= occ && seg_per_launch == 1) {
-                // trailing tiles may be empty: they only take part in the barriers
-                const uint64_t t = uint64_t(balance) * sm_count;
+            if (balance > 0 && balance <= occ && (uint64_t(balance) * sm_count) % seg_per_launch == 0) {
+                // exactly `balance` CTAs on every SM; trailing tiles may be
+                // empty: they only take part in the barriers
+                const uint64_t t = uint64_t(balance) * sm_count / seg_per_launch;
                 const uint64_t tww = round_up(ceil_div(words_proc, t), gran);
                 if (t >= tps_min && tww <= tw_max) {
                     tps = t;
@@ -137,12 +141,11 @@ struct MergeRunner {
             if (pt == 0) continue;
             const uint64_t parts = ceil_div(tps, pt);
             const uint64_t ctas = pt * seg_per_launch;
-            const uint64_t lim = 2ull * sm_count;
-            bool better = parts < best_parts;
-            if (parts == best_parts && best_ctas > lim && ctas <= lim) better = true;
-            if (better) {
+            const uint64_t k = ceil_div(ctas, uint64_t(sm_count));
+            const uint64_t cost = uint64_t(w) * (k + 1) + (k >= 3 ? 6 : 0);
+            if (parts < best_parts || (parts == best_parts && cost < best_cost)) {
                 best_parts = parts;
-                best_ctas = ctas;
+                best_cost = cost;
                 wpt = w;
                 smem = sm;
                 tile_words = uint32_t(tw);

@@ -593,7 +593,8 @@ __device__ __forceinline__ uint64_t gtime_ns() {
 #endif
 
 template <int WPT>
-__global__ void __launch_bounds__(kMergeThreads, WPT >= 8 ? 3 : 4) merge_coop_kernel(const CoopParams p) {
+__global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 : 4))
+    merge_coop_kernel(const CoopParams p) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     extern __shared__ uint32_t cslots[];  // [max_slots][WPT][kMergeThreads]
@@ -617,21 +618,29 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 8 ? 3 : 4) merge_coop_ke
     const uint32_t kb = p.stage_begin[sl * (p.n_stages + 1) + p.stage];
     const uint32_t nm = p.stage_begin[sl * (p.n_stages + 1) + p.stage + 1] - kb;
     const uint32_t sg = p.s_first + sl;
+    // a thread's last words may pass the segment's end (WPT = 12): those are
+    // loaded as 0 and never stored
+    const bool tail = w0 + WPT > p.words_proc;
+    auto load_row = [&](const uint32_t* row, uint32_t (&v)[WPT]) {
+        if (!tail) {
+            load_words<WPT>(row + w0, v);
+        } else {
+#pragma unroll
+            for (int j = 0; j < WPT; ++j) v[j] = (w0 + j < p.words_proc) ? __ldcg(row + w0 + j) : 0u;
+        }
+    };
     auto load_src = [&](uint16_t src, uint32_t (&v)[WPT]) {
         const uint32_t idx = src & 0x3FFFu;
         if (!active) {
 #pragma unroll
             for (int j = 0; j < WPT; ++j) v[j] = 0;
         } else if ((src & 0xC000u) == kSrcLeaf) {
-            load_words<WPT>(p.leaves +
-                                (uint64_t((idx / p.ml) * p.n_seg + sl) * p.ml + idx % p.ml) * p.wst +
-                                w0,
-                            v);
+            load_row(p.leaves + (uint64_t((idx / p.ml) * p.n_seg + sl) * p.ml + idx % p.ml) * p.wst, v);
         } else if ((src & 0xC000u) == kSrcSlot) {
 #pragma unroll
             for (int j = 0; j < WPT; ++j) v[j] = cslots[(idx * WPT + j) * kMergeThreads + tid];
         } else {
-            load_words<WPT>(p.gnodes + (uint64_t(sl) * p.gmax + idx) * p.wst + w0, v);
+            load_row(p.gnodes + (uint64_t(sl) * p.gmax + idx) * p.wst, v);
         }
     };
     // the local operand of the next merge is prefetched when it is a leaf
@@ -758,11 +767,13 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 8 ? 3 : 4) merge_coop_ke
                 if (m.out_global == kFinal) {
                     uint32_t* dst = p.agg + uint64_t(sg) * p.wst + w0;
 #pragma unroll
-                    for (int j = 0; j < WPT; ++j) dst[j] = r[j];
+                    for (int j = 0; j < WPT; ++j)
+                        if (!tail || w0 + j < p.words_proc) dst[j] = r[j];
                 } else if (m.out_global != kNone) {
                     uint32_t* dst = p.gnodes + (uint64_t(sl) * p.gmax + m.out_global) * p.wst + w0;
 #pragma unroll
-                    for (int j = 0; j < WPT; ++j) __stcg(dst + j, r[j]);
+                    for (int j = 0; j < WPT; ++j)
+                        if (!tail || w0 + j < p.words_proc) __stcg(dst + j, r[j]);
                 }
             }
         }
@@ -1034,6 +1045,8 @@ cudaError_t launch_merge_coop(const CoopParams& p, int wpt, size_t smem, cudaStr
         case 2: return coop_launch_t<2>(p, smem, st);
         case 4: return coop_launch_t<4>(p, smem, st);
         case 8: return coop_launch_t<8>(p, smem, st);
+        case 12: return coop_launch_t<12>(p, smem, st);
+        case 16: return coop_launch_t<16>(p, smem, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -1044,6 +1057,8 @@ cudaError_t merge_coop_occupancy(int wpt, size_t smem, int* blocks) {
         case 2: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<2>, kMergeThreads, smem);
         case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<4>, kMergeThreads, smem);
         case 8: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<8>, kMergeThreads, smem);
+        case 12: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<12>, kMergeThreads, smem);
+        case 16: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<16>, kMergeThreads, smem);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -332,3 +332,28 @@ def test_coin_prefetch_speculation_is_safe():
         assert np.array_equal(u64(agg), want.agg_bits), (t, seed)
         comp_h = want.comp
     assert np.array_equal(np.stack([c.double().cpu().numpy() for c in comp_d]), comp_h)
+
+
+@pytest.mark.parametrize("wpt", [1, 2, 4, 8, 12, 16])
+@pytest.mark.parametrize("topo,a,b,D", [("ring", 8, 0, 1_000_037), ("torus", 2, 4, 700_001),
+                                        ("ring", 3, 0, 4_001)])
+def test_merge_tilings_bit_exact(wpt, topo, a, b, D, monkeypatch):
+    """Every merge tiling (words per thread incl. the 12/16-word tails that
+    pass the segment end, balanced grids) gives the reference's bits."""
+    monkeypatch.setenv("MARSIT_MERGE_WPT", str(wpt))
+    monkeypatch.setenv("MARSIT_MERGE_BALANCE", "2" if wpt >= 12 else "0")
+    sched = sched_of(topo, a, b)
+    T = O.schedule(topo, a, b)
+    W, seed = sched.workers, 99
+    ctx = mb.Context(D, sched, torch.float32, 0)
+    comp_o = np.zeros((W, D))
+    comp = [torch.zeros(D, device=DEV) for _ in range(W)]
+    for t in (1, 2):
+        g = np.stack([O.gen_dyadic(seed, w, t, D) for w in range(W)])
+        agg = torch.empty((D + 63) // 64, dtype=torch.int64, device=DEV)
+        ctx.sign_round(t, ETA, seed, [torch.tensor(x, dtype=torch.float32, device=DEV) for x in g],
+                       comp, agg_bits=agg)
+        r = O.marsit_round(T, t, None, ETA, g, comp_o, seed)
+        assert u64(agg).tolist() == r.agg_bits.tolist(), (wpt, topo, t)
+        comp_o = r.comp
+    ctx.check()

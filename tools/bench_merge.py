@@ -7,6 +7,10 @@ import sys
 
 import torch
 
+# the next round's coin prefetch would co-run with the following merge here
+# (in a real round it runs underneath the decode): measure the merge alone
+os.environ.setdefault("MARSIT_COIN_PREFETCH", "0")
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2204_06787_b200 as mb  # noqa: E402
 
