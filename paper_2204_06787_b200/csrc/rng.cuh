@@ -27,4 +27,28 @@ __device__ __forceinline__ uint64_t stream_key(uint64_t seed, uint64_t purpose, 
     return mix64(h ^ ((s + 1) * kGamma));
 }
 
+// The finalizer with the 64-bit shifts of the xor-shifts moved onto the FMA
+// pipe: for the low word, (lo >> s) == mulhi(lo, 2^(32-s)) and the bits
+// carried in from the high word are hi * 2^(32-s).  Bit-identical to mix64;
+// it only balances the ALU / FMA pipes (each issues every other cycle).
+__device__ __forceinline__ uint32_t mulhi32(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ void xorshr_fma(uint32_t& lo, uint32_t& hi, uint32_t m) {
+    const uint32_t nlo = lo ^ mulhi32(lo, m) ^ (hi * m);
+    hi ^= mulhi32(hi, m);
+    lo = nlo;
+}
+// High 32 bits of mix64(z): only the high word of the last product is formed.
+__device__ __forceinline__ uint32_t mix64_hi(uint64_t z) {
+    uint64_t y = z ^ (z >> 30);
+    y *= 0xbf58476d1ce4e5b9ull;
+    uint32_t lo = uint32_t(y), hi = uint32_t(y >> 32);
+    xorshr_fma(lo, hi, 1u << 5);  // >> 27
+    const uint32_t h2 = mulhi32(lo, 0x133111ebu) + lo * 0x94d049bbu + hi * 0x133111ebu;
+    return h2 ^ (h2 >> 31);
+}
+
 }  // namespace marsit_b200

@@ -18,10 +18,11 @@
 //                     prefix (bit-sliced counters), from which the code
 //                     lengths of every partial sum follow exactly
 //
-// Norm: every CTA of a segment sums the per-chunk partial sums in the same
-// fixed order, so the norm is deterministic and identical across CTAs; it
-// equals the reference's sequential sum whenever that sum is exact (e.g. the
-// dyadic recipe inputs) and is within a few ulps otherwise.
+// Norm: per-chunk partial sums, then one warp per item sums them in a fixed
+// order, so the norm is deterministic; it equals the reference's sequential
+// sum whenever that sum is exact (e.g. the dyadic recipe inputs) and is
+// within a few ulps otherwise.  The Bernoulli draws avoid the division in
+// all but ~2^-21 of the coordinates (ssdm_bit) and stay exact.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -38,7 +39,6 @@ namespace {
 
 constexpr int kSsThreads = 256;
 constexpr uint32_t kSsChunk = kSsThreads * 32;  // coordinates per CTA in the norm passes
-constexpr uint32_t kSsWordsPerCta = 64;         // packet words per compress CTA
 constexpr uint64_t kPurposeSsdm = 4;            // rng.hpp:18
 constexpr uint32_t kSsMaxWorkers = 64;          // bit-sliced counters: 7 planes
 constexpr unsigned kAll = 0xffffffffu;
@@ -71,6 +71,10 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
     return t;  // valid in thread 0
 }
 
+__host__ __device__ __forceinline__ uint64_t ceil_div_d(uint64_t a, uint64_t b) {
+    return (a + b - 1) / b;
+}
+
 template <typename T>
 __device__ __forceinline__ double raw_at(const SsdmParams& p, uint32_t w, uint32_t s, uint64_t j) {
     const uint64_t gi = uint64_t(s) * p.L + j;
@@ -83,20 +87,51 @@ __device__ __forceinline__ double dec_at(const uint32_t* pk, uint64_t j, double 
     return ((pk[j >> 5] >> (j & 31)) & 1u) ? norm : -norm;
 }
 
-// Sum of squares of the raw segments (sum variant: item = w * S + s).
-template <typename T>
+// Four consecutive coordinates j..j+3 of worker w's segment s in the input
+// type (value padding beyond L / D reads 0).  VEC: quads fully inside both
+// bounds are one 16-byte aligned vector load.
+template <typename T, bool VEC>
+__device__ __forceinline__ void raw_quad(const SsdmParams& p, uint32_t w, uint32_t s, uint64_t j,
+                                         T (&v)[4]) {
+    const uint64_t gi = uint64_t(s) * p.L + j;
+    const T* src = static_cast<const T*>(p.vec[w]);
+    if (VEC && j + 3 < p.L && gi + 3 < p.D) {
+        if constexpr (sizeof(T) == 4) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(src + gi));
+            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+        } else {
+            const double2 a = __ldg(reinterpret_cast<const double2*>(src + gi));
+            const double2 b = __ldg(reinterpret_cast<const double2*>(src + gi) + 1);
+            v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = (j + k < p.L && gi + k < p.D) ? src[gi + k] : T(0);
+    }
+}
+
+// Sum of squares of the raw segments (sum variant: item = w * S + s).  A CTA
+// owns a fixed chunk of kSsChunk coordinates (the summation order does not
+// depend on the hardware); thread t takes quads t, t + 256, ... of it.
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(kSsThreads) ssdm_sumsq_raw_kernel(const SsdmParams p) {
     __shared__ double sh[kSsThreads / 32];
     const uint32_t item = blockIdx.y, w = item / p.S, s = item % p.S;
     const uint64_t base = uint64_t(blockIdx.x) * kSsChunk;
+    T v[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        raw_quad<T, VEC>(p, w, s, base + (uint64_t(i) * kSsThreads + threadIdx.x) * 4, v[i]);
     double ss = 0.0;
     bool bad = false;
-    for (int i = 0; i < 32; ++i) {
-        const uint64_t j = base + uint64_t(i) * kSsThreads + threadIdx.x;
-        const double v = raw_at<T>(p, w, s, j);
-        bad |= !isfinite(v);
-        ss = __dadd_rn(ss, __dmul_rn(v, v));
-    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double x = double(v[i][k]);
+            bad |= !isfinite(x);
+            ss = __dadd_rn(ss, __dmul_rn(x, x));
+        }
     if (bad) atomicExch(p.err, 1);  // DenseVector: non-finite entry (dense_vector.hpp:25-29)
     const double t = block_sum(ss, sh);
     if (threadIdx.x == 0) p.partial[uint64_t(item) * p.nb + blockIdx.x] = t;
@@ -105,7 +140,7 @@ __global__ void __launch_bounds__(kSsThreads) ssdm_sumsq_raw_kernel(const SsdmPa
 // Cascading hop k for every segment (item = s): acc = raw (k = 0) or
 // add(ssdm_decompress(packet of hop k-1), raw) (allreduce.hpp:240-242), and its
 // sum of squares.
-template <typename T>
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(kSsThreads) ssdm_hop_kernel(const SsdmParams p) {
     __shared__ double sh[kSsThreads / 32];
     const uint32_t s = blockIdx.y;
@@ -114,29 +149,88 @@ __global__ void __launch_bounds__(kSsThreads) ssdm_hop_kernel(const SsdmParams p
     const double nrm = p.k > 0 ? p.norms[s] : 0.0;
     double* acc = p.acc + uint64_t(s) * p.L;
     const uint64_t base = uint64_t(blockIdx.x) * kSsChunk;
+    T r[8][4];
+    uint32_t word[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint64_t j = base + (uint64_t(i) * kSsThreads + threadIdx.x) * 4;
+        raw_quad<T, VEC>(p, w, s, j, r[i]);
+        word[i] = (p.k > 0 && j < p.L) ? __ldg(pk + (j >> 5)) : 0u;
+    }
     double ss = 0.0;
     bool bad = false;
-    for (int i = 0; i < 32; ++i) {
-        const uint64_t j = base + uint64_t(i) * kSsThreads + threadIdx.x;
-        if (j >= p.L) break;
-        const double r = raw_at<T>(p, w, s, j);
-        const double v = p.k == 0 ? r : __dadd_rn(dec_at(pk, j, nrm), r);
-        bad |= !isfinite(v);
-        acc[j] = v;
-        ss = __dadd_rn(ss, __dmul_rn(v, v));
+    // acc rows start at s * L doubles: 16-byte aligned pairs iff L is even
+    const bool pairs = VEC && (p.L % 2 == 0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint64_t j = base + (uint64_t(i) * kSsThreads + threadIdx.x) * 4;
+        double v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            v[k] = double(r[i][k]);
+            if (p.k > 0) {
+                const double d = nrm == 0.0 ? 0.0 : (((word[i] >> ((j + k) & 31)) & 1u) ? nrm : -nrm);
+                v[k] = __dadd_rn(d, v[k]);
+            }
+        }
+        if (pairs && j + 3 < p.L) {
+            reinterpret_cast<double2*>(acc + j)[0] = make_double2(v[0], v[1]);
+            reinterpret_cast<double2*>(acc + j)[1] = make_double2(v[2], v[3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (j + k < p.L) acc[j + k] = v[k];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (j + k < p.L) {
+                bad |= !isfinite(v[k]);
+                ss = __dadd_rn(ss, __dmul_rn(v[k], v[k]));
+            }
     }
     if (bad) atomicExch(p.err, 1);
     const double t = block_sum(ss, sh);
     if (threadIdx.x == 0) p.partial[uint64_t(s) * p.nb + blockIdx.x] = t;
 }
 
-// ssdm_compress (ssdm.hpp:29-40) of every item: norm from the partial sums (same
-// order in every CTA), then one Bernoulli draw per coordinate, 32 per ballot.
-// SRC: T for raw inputs (sum variant / standalone), double for the cascading
-// accumulators.
+// The l2 norm of every item from its per-chunk partial sums, one warp per
+// item, always the same order (lane l takes chunks l, l+32, ...; then a fixed
+// butterfly), so every later use sees one deterministic value.
+__global__ void ssdm_norm_kernel(const SsdmParams p, uint32_t items) {
+    const uint32_t item = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (item >= items) return;
+    double t = 0.0;
+    for (uint32_t b = lane; b < p.nb; b += 32) t = __dadd_rn(t, p.partial[uint64_t(item) * p.nb + b]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t = __dadd_rn(t, __shfl_xor_sync(kAll, t, o));
+    if (lane == 0) p.norms[item] = __dsqrt_rn(t);
+}
+
+// Bernoulli draw of ssdm_compress (ssdm.hpp:33-37): bit = (u < p), u = (x >> 11)
+// * 2^-53, x = mix64(z), z = key + (j+1)γ, p = 1/2 + v / (2 norm).  Exact,
+// without a division in the common case: P = p * 2^53 is known to +-2 units
+// from one FMA (s53 = 2^52 / norm), and (x >> 11) < P is decided by the high
+// word xh of x alone (x lies in [xh, xh+1) * 2^32, i.e. x >> 11 in
+// [xh, xh+1) * 2^21) unless that interval is within 16 units of P — one
+// value of xh in 2^32 — in which case the literal formula runs.
+__device__ __forceinline__ bool ssdm_bit(uint64_t z, double v, double norm, double denom,
+                                         double s53) {
+    if (norm == 0.0) return mix64_hi(z) < 0x80000000u;  // p = 1/2 exactly
+    const double pd = fma(v, s53, 0x1p52);
+    const double lo = fma(double(mix64_hi(z)), 0x1p21, -pd);  // xh * 2^21 - P (exact)
+    if (lo + 0x1p21 <= -16.0) return true;                     // whole block below P
+    if (lo >= 16.0) return false;                              // whole block above P
+    const double u = double(mix64(z) >> 11) * 0x1.0p-53;
+    return u < __dadd_rn(0.5, __ddiv_rn(v, denom));
+}
+
+constexpr int kSsWordsPerWarp = 64;  // batches of 8 words, loads first
+
+// ssdm_compress (ssdm.hpp:29-40) of every item; SRC: T for raw inputs (sum
+// variant / standalone), double for the cascading accumulators.
 template <typename SRC, bool CASCADE>
 __global__ void __launch_bounds__(kSsThreads) ssdm_compress_kernel(const SsdmParams p) {
-    __shared__ double s_norm;
     const uint32_t item = blockIdx.y;
     uint32_t w, s;
     if (CASCADE) {
@@ -146,69 +240,95 @@ __global__ void __launch_bounds__(kSsThreads) ssdm_compress_kernel(const SsdmPar
         w = item / p.S;
         s = item % p.S;
     }
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (uint32_t b = 0; b < p.nb; ++b) t = __dadd_rn(t, p.partial[uint64_t(item) * p.nb + b]);
-        const double n = __dsqrt_rn(t);
-        s_norm = n;
-        if (blockIdx.x == 0) p.norms[item] = n;
-    }
-    __syncthreads();
-    const double norm = s_norm;
+    const double norm = p.norms[item];
     const double denom = norm > 0.0 ? __dmul_rn(2.0, norm) : 0.0;
+    const double s53 = norm > 0.0 ? __ddiv_rn(0x1p52, norm) : 0.0;
     const uint64_t key =
         p.key_w >= 0 ? stream_key(p.seed, kPurposeSsdm, uint64_t(p.key_w), p.round, uint64_t(p.key_s))
                      : stream_key(p.seed, kPurposeSsdm, w, p.round, s);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t warp = blockIdx.x * (kSsThreads / 32) + (threadIdx.x >> 5);
     uint32_t* out = p.pk + uint64_t(item) * p.wst;
-    for (uint32_t q = blockIdx.x * kSsWordsPerCta + wid; q < min(p.wst, (blockIdx.x + 1) * kSsWordsPerCta);
-         q += kSsThreads / 32) {
-        const uint64_t j = uint64_t(q) * 32 + lane;
-        bool bit = false;
-        if (j < p.L) {
-            double v;
-            if (CASCADE)
-                v = p.acc[uint64_t(s) * p.L + j];
+    const uint32_t q_end = min(p.wst, (warp + 1) * kSsWordsPerWarp);
+    for (uint32_t q0 = warp * kSsWordsPerWarp; q0 < q_end; q0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const uint64_t j = uint64_t(q0 + b) * 32 + lane;
+            if (j >= p.L)
+                v[b] = 0.0;
+            else if (CASCADE)
+                v[b] = p.acc[uint64_t(s) * p.L + j];
             else
-                v = raw_at<SRC>(p, w, s, j);
-            const uint64_t x = mix64(key + (j + 1) * kGamma);
-            const double u = double(x >> 11) * 0x1.0p-53;  // next_uniform (rng.hpp:46-48)
-            const double pr = denom > 0.0 ? __dadd_rn(0.5, __ddiv_rn(v, denom)) : 0.5;
-            bit = u < pr;
+                v[b] = raw_at<SRC>(p, w, s, j);
         }
-        const uint32_t word = __ballot_sync(kAll, bit);
-        if (lane == 0) out[q] = word;
+        uint64_t z = key + (uint64_t(q0) * 32 + lane + 1) * kGamma;  // draw j = 32 q + lane
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const uint64_t j = uint64_t(q0 + b) * 32 + lane;
+            const bool bit = j < p.L && ssdm_bit(z, v[b], norm, denom, s53);
+            z += 32 * kGamma;
+            const uint32_t word = __ballot_sync(kAll, bit);
+            if (lane == b && q0 + b < q_end) out[q0 + b] = word;
+        }
     }
 }
 
 // Cascading estimate: reassemble(scaled(ssdm_decompress(final packet), 1/M))
-// (allreduce.hpp:252-260).
+// (allreduce.hpp:252-260).  A warp per packed word: the word is broadcast,
+// lanes are coordinates (coalesced stores).
 template <typename T>
 __global__ void ssdm_out_cascade_kernel(const SsdmParams p, T* __restrict__ out) {
     const double inv_m = 1.0 / double(p.M);
-    for (uint64_t gi = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; gi < p.D;
-         gi += uint64_t(gridDim.x) * blockDim.x) {
-        const uint32_t s = uint32_t(gi / p.L);
-        const uint64_t j = gi - uint64_t(s) * p.L;
-        out[gi] = T(__dmul_rn(dec_at(p.pk + uint64_t(s) * p.wst, j, p.norms[s]), inv_m));
+    const uint32_t s = blockIdx.y;  // segment; warps stride over its packed words
+    const uint64_t wps = ceil_div_d(p.L, 32);
+    const int lane = threadIdx.x & 31;
+    const double nrm = p.norms[s];
+    const uint32_t* pk = p.pk + uint64_t(s) * p.wst;
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x / 32);
+    for (uint64_t q0 = (blockIdx.x * uint64_t(blockDim.x / 32) + (threadIdx.x >> 5)) * 4; q0 < wps;
+         q0 += warps * 4) {
+        uint32_t word[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) word[i] = q0 + i < wps ? __ldg(pk + q0 + i) : 0u;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint64_t j = (q0 + i) * 32 + lane, gi = uint64_t(s) * p.L + j;
+            const double d = nrm == 0.0 ? 0.0 : (((word[i] >> lane) & 1u) ? nrm : -nrm);
+            if (j < p.L && gi < p.D) out[gi] = T(__dmul_rn(d, inv_m));
+        }
     }
 }
 
 // Sum variant estimate: mean of the M decompressed packets, summed in worker
-// order from 0.0, times 1/M (allreduce.hpp:322-336).
+// order from 0.0, times 1/M (allreduce.hpp:322-336).  A warp per packed word
+// (lanes = coordinates); the packet words of 8 workers are loaded at once.
 template <typename T>
 __global__ void ssdm_out_sum_kernel(const SsdmParams p, T* __restrict__ out) {
+    __shared__ double s_norm[kSsMaxWorkers];
     const double inv_m = 1.0 / double(p.M);
-    for (uint64_t gi = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; gi < p.D;
-         gi += uint64_t(gridDim.x) * blockDim.x) {
-        const uint32_t s = uint32_t(gi / p.L);
-        const uint64_t j = gi - uint64_t(s) * p.L;
+    const uint32_t s = blockIdx.y;
+    for (uint32_t w = threadIdx.x; w < p.M; w += blockDim.x) s_norm[w] = p.norms[w * p.S + s];
+    __syncthreads();
+    const uint64_t wps = ceil_div_d(p.L, 32);
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x / 32);
+    for (uint64_t q = blockIdx.x * uint64_t(blockDim.x / 32) + (threadIdx.x >> 5); q < wps; q += warps) {
+        const uint64_t j = q * 32 + lane, gi = uint64_t(s) * p.L + j;
         double a = 0.0;
-        for (uint32_t w = 0; w < p.M; ++w) {
-            const uint32_t item = w * p.S + s;
-            a = __dadd_rn(a, dec_at(p.pk + uint64_t(item) * p.wst, j, p.norms[item]));
+        for (uint32_t w0 = 0; w0 < p.M; w0 += 8) {
+            uint32_t word[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                word[i] = w0 + i < p.M ? __ldg(p.pk + (uint64_t(w0 + i) * p.S + s) * p.wst + q) : 0u;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (w0 + i >= p.M) break;
+                const double nrm = s_norm[w0 + i];
+                a = __dadd_rn(a, nrm == 0.0 ? 0.0 : (((word[i] >> lane) & 1u) ? nrm : -nrm));
+            }
         }
-        out[gi] = T(__dmul_rn(a, inv_m));
+        if (j < p.L && gi < p.D) out[gi] = T(__dmul_rn(a, inv_m));
     }
 }
 
@@ -269,33 +389,50 @@ uint64_t signed_sum_code_length(int64_t v) {
     return 2 * width - 1;
 }
 
-int grid_for(uint64_t n, int sm_count) {
-    return int(std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(n, 256), uint64_t(sm_count) * 8)));
+
+uint32_t compress_grid_x(uint32_t wst) {
+    return uint32_t(ceil_div_d(wst, uint64_t(kSsThreads / 32) * kSsWordsPerWarp));
 }
+
 
 template <typename T>
 marsit_status launch_pipeline(marsit_ctx* ctx, SsdmScratch& sc, SsdmParams& p, int mode,
                               void* d_out, bool want_hist, cudaStream_t st) {
     const dim3 blk(kSsThreads);
-    const uint32_t cgx = ceil_div(p.wst, kSsWordsPerCta);
+    const uint32_t cgx = compress_grid_x(p.wst);
+    const uint32_t out_gx = uint32_t(std::max<uint64_t>(
+        1, std::min<uint64_t>(ceil_div_d(ceil_div_d(p.L, 32), 8), ceil_div_d(uint64_t(ctx->sm_count) * 16, p.S))));
+    // quads of a segment start at s * L: vector loads need L and D multiples
+    // of 4 and 16-byte aligned inputs
+    bool vec = p.L % 4 == 0;
+    for (uint32_t w = 0; w < p.M; ++w) vec = vec && (reinterpret_cast<uintptr_t>(p.vec[w]) % 16 == 0);
     if (mode == 0) {
         for (uint32_t k = 0; k < p.M; ++k) {
             p.k = int(k);
-            ssdm_hop_kernel<T><<<dim3(p.nb, p.S), blk, 0, st>>>(p);
+            if (vec)
+                ssdm_hop_kernel<T, true><<<dim3(p.nb, p.S), blk, 0, st>>>(p);
+            else
+                ssdm_hop_kernel<T, false><<<dim3(p.nb, p.S), blk, 0, st>>>(p);
+            ssdm_norm_kernel<<<ceil_div_d(p.S, 8), 256, 0, st>>>(p, p.S);
             ssdm_compress_kernel<double, true><<<dim3(cgx, p.S), blk, 0, st>>>(p);
         }
         ssdm_out_cascade_kernel<T>
-            <<<grid_for(p.D, ctx->sm_count), 256, 0, st>>>(p, static_cast<T*>(d_out));
+            <<<dim3(out_gx, p.S), 256, 0, st>>>(p, static_cast<T*>(d_out));
     } else {
-        ssdm_sumsq_raw_kernel<T><<<dim3(p.nb, p.M * p.S), blk, 0, st>>>(p);
-        ssdm_compress_kernel<T, false><<<dim3(cgx, p.M * p.S), blk, 0, st>>>(p);
-        ssdm_out_sum_kernel<T><<<grid_for(p.D, ctx->sm_count), 256, 0, st>>>(p, static_cast<T*>(d_out));
+        const uint32_t items = p.M * p.S;
+        if (vec)
+            ssdm_sumsq_raw_kernel<T, true><<<dim3(p.nb, items), blk, 0, st>>>(p);
+        else
+            ssdm_sumsq_raw_kernel<T, false><<<dim3(p.nb, items), blk, 0, st>>>(p);
+        ssdm_norm_kernel<<<ceil_div_d(items, 8), 256, 0, st>>>(p, items);
+        ssdm_compress_kernel<T, false><<<dim3(cgx, items), blk, 0, st>>>(p);
+        ssdm_out_sum_kernel<T><<<dim3(out_gx, p.S), 256, 0, st>>>(p, static_cast<T*>(d_out));
         if (want_hist) {
             const size_t H = size_t(p.M) * (p.M + 1);
             CUDA_TRY(cudaMemsetAsync(sc.hist, 0, sizeof(unsigned long long) * H * p.S, st));
-            const uint32_t n_words = uint32_t(ceil_div(p.L, 32));
+            const uint32_t n_w = uint32_t(ceil_div(p.L, 32));
             const uint32_t gx = std::max<uint32_t>(
-                1, std::min<uint32_t>(ceil_div(n_words, kSsThreads), ceil_div(4u * ctx->sm_count, p.S)));
+                1, std::min<uint32_t>(ceil_div(n_w, kSsThreads), ceil_div(4u * ctx->sm_count, p.S)));
             ssdm_hist_kernel<<<dim3(gx, p.S), blk, H * sizeof(uint32_t), st>>>(p, sc.hist);
         }
     }
@@ -498,14 +635,16 @@ marsit_status marsit_ssdm_compress(const void* d_v, uint64_t len, marsit_dtype d
     p.err = reinterpret_cast<int*>(p.partial + p.nb);
     CUDA_TRY(cudaMemsetAsync(p.err, 0, sizeof(int), st));
     const dim3 blk(kSsThreads);
-    const uint32_t cgx = ceil_div(p.wst, kSsWordsPerCta);
-    if (dtype == MARSIT_F32) {
-        ssdm_sumsq_raw_kernel<float><<<dim3(p.nb, 1), blk, 0, st>>>(p);
+    const uint32_t cgx = compress_grid_x(p.wst);
+    if (dtype == MARSIT_F32)
+        ssdm_sumsq_raw_kernel<float, false><<<dim3(p.nb, 1), blk, 0, st>>>(p);
+    else
+        ssdm_sumsq_raw_kernel<double, false><<<dim3(p.nb, 1), blk, 0, st>>>(p);
+    ssdm_norm_kernel<<<1, 32, 0, st>>>(p, 1);
+    if (dtype == MARSIT_F32)
         ssdm_compress_kernel<float, false><<<dim3(cgx, 1), blk, 0, st>>>(p);
-    } else {
-        ssdm_sumsq_raw_kernel<double><<<dim3(p.nb, 1), blk, 0, st>>>(p);
+    else
         ssdm_compress_kernel<double, false><<<dim3(cgx, 1), blk, 0, st>>>(p);
-    }
     CUDA_TRY(cudaGetLastError());
     int bad = 0;
     CUDA_TRY(cudaMemcpyAsync(norm_out, p.norms, sizeof(double), cudaMemcpyDeviceToHost, st));
