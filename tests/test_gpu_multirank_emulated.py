@@ -112,3 +112,33 @@ def test_external_transport_rejects_one_shot_rounds():
     g = [torch.zeros(1000, device=DEV) for _ in range(2)]
     with pytest.raises(mb.UnsupportedError):
         ctx.sign_round(1, ETA, 1, g, g)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("topo,a,b,D", [("ring", 8, 0, 61_000_000), ("torus", 2, 4, 60_200_000)])
+def test_full_size_c2_c4_ranks_bit_identical(topo, a, b, D):
+    """C2 (ring 8, D = 61M: 40-bit segment tail) and C4 (torus 2x4, D = 60.2M:
+    8-bit tail) at full size: the G = 8 rank decomposition reproduces the
+    single-context round bit for bit, g_t = +-eta and c' = (g + c) - g_t hold
+    exactly (fp32-exact dyadic inputs)."""
+    sched = mb.build_ring_schedule(a) if topo == "ring" else mb.build_torus_schedule(a, b)
+    W, G, seed, t = sched.workers, 8, 2026, 1
+    grads = [torch.empty(D, device=DEV) for _ in range(W)]
+    for w in range(W):
+        mb.fill_recipe(grads[w], 0, seed, w, t)
+    single = mb.Context(D, sched, torch.float32, 0)
+    comp_1 = [torch.zeros(D, device=DEV) for _ in range(W)]
+    upd = torch.empty(D, device=DEV)
+    single.sign_round(t, ETA, seed, grads, comp_1, update=upd)
+    torch.cuda.synchronize()
+    assert bool(((upd == ETA) | (upd == -ETA)).all())
+    for w in (0, W - 1):
+        assert torch.equal(comp_1[w], grads[w] - upd)  # c = 0: c' = g - g_t exactly
+    ctxs = [mb.Context(D, sched, torch.float32, 0, nranks=G, rank=r, external_transport=True)
+            for r in range(G)]
+    comp_g = [torch.zeros(D, device=DEV) for _ in range(W)]
+    run_ranks(ctxs, G, W // G, t, None, seed, grads, comp_g)
+    torch.cuda.synchronize()
+    for w in range(W):
+        assert torch.equal(comp_g[w], comp_1[w]), w
+    single.check()

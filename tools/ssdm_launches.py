@@ -22,4 +22,4 @@ for i, m in per.items():
     a[2] += (m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)) / 1e6
 for n, (c, us, mb) in agg.items():
     print(f"{n:42s} x{c:3d}  {us / c:9.1f} us/launch  {mb / c:9.1f} MB/launch  "
-          f"{mb / us / 1e3 if us else 0:6.2f} TB/s")
+          f"{mb / us if us else 0:6.2f} TB/s")
