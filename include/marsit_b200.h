@@ -97,8 +97,9 @@ typedef struct marsit_ctx marsit_ctx;
 
 /* How the packed segments move between ranks (nranks > 1). */
 typedef enum marsit_transport {
-    MARSIT_TRANSPORT_NCCL = 0,     /* built in: grouped send/recv + all-gather     */
-    MARSIT_TRANSPORT_EXTERNAL = 1  /* the caller moves the blocks between phases   */
+    MARSIT_TRANSPORT_NCCL = 0,      /* built in: grouped send/recv + all-gather     */
+    MARSIT_TRANSPORT_EXTERNAL = 1,  /* the caller moves the blocks between phases   */
+    MARSIT_TRANSPORT_P2P = 2        /* fused over peer memory (marsit_ctx_set_peers) */
 } marsit_transport;
 
 typedef struct marsit_ctx_desc {
@@ -175,6 +176,36 @@ marsit_status marsit_round_phase(marsit_ctx* ctx, int phase, uint64_t t, uint64_
                                  const void* const* d_comp, void* const* d_comp_out,
                                  uint64_t* d_agg_bits, void* d_update, int* full_precision,
                                  void* stream);
+
+/* P2P transport (NVLink / NVSwitch peer memory, one process per GPU): no
+ * exchange or all-gather phase.  The merge kernel reads its leaves straight
+ * out of the peer ranks' packed-sign buffers and the decode reads every
+ * aggregate segment from the rank that owns it; the dense round's owner sum
+ * reads the peers' u blocks the same way.  Ordering is stream-ordered: after
+ * each producing phase the stream writes this rank's epoch into its slot of
+ * every peer's flag array, and before each consuming phase it waits
+ * (cuStreamWaitValue64, on local memory) until every peer's slot reaches the
+ * epoch — no kernel ever waits on another.  Every rank runs the same
+ * sequence of rounds.
+ * Setup: export this rank's buffers (marsit_ctx_p2p_buffers), map the peers'
+ * (marsit_ipc_handle / marsit_ipc_open across processes), hand the table of
+ * all ranks' mapped buffers (indexed by rank) to marsit_ctx_set_peers.
+ * marsit_round_phase splits a round at the same points (0: extract + flag,
+ * 1: wait + merge + flag, 2: wait + decode). */
+typedef struct marsit_p2p_buffers {
+    void* bits;        /* packed signs [S][local workers][words]          */
+    void* agg;         /* aggregate bits [S][words] (owned segments)      */
+    void* dense_send;  /* dense round: u [S][local workers][L]            */
+    void* dense_mean;  /* dense round: mean [S * L] (owned segments)      */
+    void* flags;       /* [2][nranks] u64 epochs reported by each rank   */
+} marsit_p2p_buffers;
+marsit_status marsit_ctx_p2p_buffers(const marsit_ctx* ctx, marsit_p2p_buffers* out);
+marsit_status marsit_ctx_set_peers(marsit_ctx* ctx, const marsit_p2p_buffers* peers,
+                                   uint32_t nranks);
+/* CUDA IPC of one device allocation (64-byte handle) for the peer table. */
+marsit_status marsit_ipc_handle(const void* d_ptr, void* handle_out);
+marsit_status marsit_ipc_open(const void* handle, int device, void** d_ptr_out);
+marsit_status marsit_ipc_close(void* d_ptr);
 
 /* Error-compensated sign extraction alone (sync.hpp:71-76 + segmentation.hpp:32-53
  * + sign_vector.hpp:67-73): d_signs_out as in marsit_allreduce_sign's input. */

@@ -247,9 +247,15 @@ class Context:
 
     def __init__(self, dim: int, schedule: Schedule, dtype=None, device: int = 0,
                  nranks: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
-                 external_transport: bool = False):
+                 external_transport: bool = False, transport: Optional[str] = None):
+        """transport: "nccl" (default for nranks > 1), "external" (the caller
+        moves blocks between marsit_round_phase calls) or "p2p" (fused over
+        peer memory; call set_peers before the first round)."""
         import torch
         dtype = dtype or torch.float32
+        if transport is None:
+            transport = "external" if external_transport else "nccl"
+        self.transport = transport
         self.dim, self.schedule, self.device = int(dim), schedule, int(device)
         self.dtype = dtype
         self.nranks, self.rank = nranks, rank
@@ -260,7 +266,7 @@ class Context:
         desc.device = self.device
         desc.nranks = nranks
         desc.rank = rank
-        desc.transport = 1 if external_transport else 0
+        desc.transport = {"nccl": 0, "external": 1, "p2p": 2}[transport]
         self._id_buf = None
         if nccl_id is not None:
             self._id_buf = C.create_string_buffer(bytes(nccl_id), 128)
@@ -280,6 +286,18 @@ class Context:
         except Exception:  # interpreter shutdown
             pass
         self._h = None
+
+    # P2P transport -----------------------------------------------------------
+    def p2p_buffers(self) -> "N.P2PBuffers":
+        """This rank's buffers to export to its peers (marsit_ctx_p2p_buffers)."""
+        b = N.P2PBuffers()
+        _check(N.lib().marsit_ctx_p2p_buffers(self._h, C.byref(b)))
+        return b
+
+    def set_peers(self, peers: Sequence["N.P2PBuffers"]):
+        """All ranks' buffers as mapped in this process, indexed by rank."""
+        arr = (N.P2PBuffers * len(peers))(*peers)
+        _check(N.lib().marsit_ctx_set_peers(self._h, arr, len(peers)))
 
     # raw entry points ------------------------------------------------------
     def sign_round(self, t, eta_s, seed, grads, comp, comp_out=None, agg_bits=None,
@@ -543,6 +561,47 @@ def sum_ssdm_allreduce(vectors: Sequence, sched: Schedule, global_seed: int,
     the wire (Elias-gamma accounting), estimate = mean of the packets."""
     out, bits, mx = _ssdm(1, vectors, sched, global_seed, round_)
     return SumSsdmAllreduceResult([out] * sched.workers, bits, mx)
+
+
+def ipc_handle(ptr: int) -> bytes:
+    """64-byte CUDA IPC handle of a device allocation (marsit_ipc_handle)."""
+    buf = C.create_string_buffer(64)
+    _check(N.lib().marsit_ipc_handle(C.c_void_p(ptr), buf))
+    return buf.raw
+
+
+def ipc_open(handle: bytes, device: int) -> int:
+    """Map a peer allocation into this process (marsit_ipc_open)."""
+    out = C.c_void_p()
+    _check(N.lib().marsit_ipc_open(C.create_string_buffer(bytes(handle), 64), device,
+                                   C.byref(out)))
+    return out.value
+
+
+def exchange_p2p_buffers(ctx: "Context", group=None):
+    """Multi-process setup of a P2P-transport context over torch.distributed:
+    every rank exports its buffers as IPC handles, maps the others' and hands
+    the full table to ctx.set_peers.  Returns the mapped pointers (close them
+    with marsit_ipc_close when the context is gone)."""
+    import torch.distributed as dist
+    mine = ctx.p2p_buffers()
+    names = ("bits", "agg", "dense_send", "dense_mean", "flags")
+    handles = {k: ipc_handle(getattr(mine, k)) for k in names}
+    world = [None] * dist.get_world_size(group)
+    dist.all_gather_object(world, handles, group=group)
+    table, opened = [], []
+    for q, h in enumerate(world):
+        b = N.P2PBuffers()
+        for k in names:
+            if q == ctx.rank:
+                setattr(b, k, getattr(mine, k))
+            else:
+                ptr = ipc_open(h[k], ctx.device)
+                opened.append(ptr)
+                setattr(b, k, ptr)
+        table.append(b)
+    ctx.set_peers(table)
+    return opened
 
 
 def merge_signs(received: AggregateSign, local: AggregateSign, key: int, used: int = 0):

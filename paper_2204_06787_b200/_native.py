@@ -40,6 +40,12 @@ class CtxDesc(C.Structure):
                 ("nccl_id", C.c_void_p), ("transport", C.c_int)]
 
 
+class P2PBuffers(C.Structure):
+    """marsit_p2p_buffers (include/marsit_b200.h)."""
+    _fields_ = [("bits", C.c_void_p), ("agg", C.c_void_p), ("dense_send", C.c_void_p),
+                ("dense_mean", C.c_void_p), ("flags", C.c_void_p)]
+
+
 class ExchangeLayout(C.Structure):
     _fields_ = [("send", C.c_void_p), ("recv", C.c_void_p), ("block_bytes", C.c_uint64),
                 ("gather", C.c_void_p), ("gather_block_bytes", C.c_uint64)]
@@ -86,6 +92,11 @@ SIGNATURES = {
     "marsit_ctx_check": (_i32, [_vp, _vp]),
     "marsit_ctx_set_timing": (_i32, [_vp, _i32]),
     "marsit_ctx_set_metrics": (_i32, [_vp, _i32]),
+    "marsit_ctx_p2p_buffers": (_i32, [_vp, C.POINTER(P2PBuffers)]),
+    "marsit_ctx_set_peers": (_i32, [_vp, C.POINTER(P2PBuffers), _u32]),
+    "marsit_ipc_handle": (_i32, [_vp, _vp]),
+    "marsit_ipc_open": (_i32, [_vp, _i32, C.POINTER(_vp)]),
+    "marsit_ipc_close": (_i32, [_vp]),
     "marsit_ssdm_compress": (_i32, [_vp, _u64, _i32, _u64, _u64, _u64, _u64, _vp,
                                     C.POINTER(_dbl), _vp]),
     "marsit_ssdm_decompress": (_i32, [_vp, _u64, _dbl, _i32, _vp, _vp]),

@@ -83,6 +83,7 @@ struct MergeRunner {
     uint64_t* flags = nullptr;  // [kmax][seg_per_launch * part_tiles]
     uint64_t* part_totals = nullptr;
     uint32_t epoch = 0;
+    const uint32_t* const* peer_bits = nullptr;  // P2P transport: device table [G]
 
     MergeRunner() = default;
     MergeRunner(const MergeRunner&) = delete;
@@ -205,6 +206,7 @@ struct MergeRunner {
         c.n_merges = dp.n_merges;
         c.seg_bits = L;
         c.leaves = leaves;
+        c.peer_bits = peer_bits;
         c.gnodes = gnodes;
         c.gmax = std::max<uint32_t>(dp.gmax, 1);
         c.agg = agg;
@@ -306,6 +308,14 @@ struct marsit_ctx {
     cudaEvent_t ev_extract = nullptr;
     std::vector<cudaEvent_t> ev_merge;
     int coin_grid_x = 1;
+    // P2P transport (marsit_ctx_set_peers): device tables of the peers'
+    // buffers, host copies of their flag words, this rank's epoch flags
+    bool p2p = false, peers_set = false;
+    uint64_t* flags = nullptr;  // [2][G]: epoch each rank reported (data ready, results ready)
+    uint64_t epoch = 0;         // rounds (sign or dense) run so far
+    std::vector<const uint64_t*> peer_flags;
+    std::vector<void*> peer_dense_mean;
+    void** d_peer_tables = nullptr;  // [3][G]: bits, agg, dense_send
     // NCCL
     ncclComm_t comm = nullptr;
     bool owns_comm = true;

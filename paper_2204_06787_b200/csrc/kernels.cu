@@ -256,6 +256,13 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 4 : 2) extrac
 // c' = (g + c) - g_t, in the same pass (sync.hpp:113-118).  Same task
 // decomposition as K1, so each sub-chunk's bits are 4 aligned words.
 // ---------------------------------------------------------------------------
+// Aggregate row of segment s: local, or (P2P transport) the owner's buffer.
+template <typename T>
+__device__ __forceinline__ const uint32_t* agg_row(const StreamParams<T>& p, uint32_t s) {
+    const uint32_t* base = p.agg_peers ? p.agg_peers[s / p.s_own] : p.agg;
+    return base + uint64_t(s) * p.wst;
+}
+
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode_kernel(const StreamParams<T> p) {
     const int lane = threadIdx.x & 31;
@@ -276,7 +283,7 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode
         T* xp = p.x[wl];  // replica parameters (optional)
         const uint64_t seg0 = uint64_t(s) * p.seg_len;
         const uint64_t j0 = uint64_t(q) * (kTaskWords * 32);
-        const uint32_t* aw = p.agg + uint64_t(s) * p.wst + q * kTaskWords;
+        const uint32_t* aw = agg_row(p, s) + q * kTaskWords;
         if (VEC) {
             Quad<T> gv[4], cv[4];
             uint32_t nib[4];
@@ -380,7 +387,7 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 80 : 128) decode_stats_kernel(const
         const uint32_t s = p.seg0 + uint32_t(task / tasks_per_seg);
         const uint64_t seg0 = uint64_t(s) * p.seg_len;
         const uint64_t j0 = uint64_t(q) * (kTaskWords * 32);
-        const uint32_t* aw = p.agg + uint64_t(s) * p.wst + q * kTaskWords;
+        const uint32_t* aw = agg_row(p, s) + q * kTaskWords;
         // full task: all 512 coordinates real, 16-byte aligned quads
         const bool full = VEC && j0 + kTaskWords * 32 <= p.seg_len &&
                           seg0 + j0 + kTaskWords * 32 <= p.dim;
@@ -625,7 +632,11 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
 #pragma unroll
             for (int j = 0; j < WPT; ++j) v[j] = 0;
         } else if ((src & 0xC000u) == kSrcLeaf) {
-            load_row(p.leaves + (uint64_t((idx / p.ml) * p.n_seg + sl) * p.ml + idx % p.ml) * p.wst, v);
+            if (p.peer_bits)  // P2P: the source rank's buffer, over NVLink
+                load_row(p.peer_bits[idx / p.ml] + (uint64_t(sg) * p.ml + idx % p.ml) * p.wst, v);
+            else
+                load_row(p.leaves + (uint64_t((idx / p.ml) * p.n_seg + sl) * p.ml + idx % p.ml) * p.wst,
+                         v);
         } else if ((src & 0xC000u) == kSrcSlot) {
 #pragma unroll
             for (int j = 0; j < WPT; ++j) v[j] = cslots[(idx * WPT + j) * kMergeThreads + tid];
@@ -829,7 +840,8 @@ __global__ void __launch_bounds__(256) coins_kernel(const DevMerge* __restrict__
 // u32 word (two of them form one little-endian u64 word).
 // ---------------------------------------------------------------------------
 __global__ void export_bits_kernel(const uint32_t* __restrict__ agg, uint32_t wst, uint64_t dim,
-                                   uint64_t seg_len, uint64_t n_out, uint32_t* __restrict__ out) {
+                                   uint64_t seg_len, uint64_t n_out, uint32_t* __restrict__ out,
+                                   const uint32_t* const* agg_peers, uint32_t s_own) {
     for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n_out;
          k += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t j0 = k * 32;
@@ -843,7 +855,7 @@ __global__ void export_bits_kernel(const uint32_t* __restrict__ agg, uint32_t ws
                 const uint64_t o = j - s * seg_len;
                 uint32_t take = n - pos;
                 if (seg_len - o < take) take = uint32_t(seg_len - o);
-                const uint32_t* a = agg + s * wst;
+                const uint32_t* a = (agg_peers ? agg_peers[s / s_own] : agg) + s * wst;
                 const uint32_t wi = uint32_t(o >> 5), sh = uint32_t(o & 31);
                 uint64_t window = a[wi];
                 if (sh + take > 32) window |= uint64_t(a[wi + 1]) << 32;
@@ -958,11 +970,17 @@ __global__ void __launch_bounds__(kDenseThreads) dense_reduce_kernel(const Dense
                     dval[(w0 + k) * kDenseThreads + tid] = double(uu);
                 }
             }
-        } else {
+        } else if (p.mode == 1) {
             for (uint32_t w = 0; w < p.workers; ++w) {
                 const uint32_t src_rank = w / p.ml, wl = w % p.ml;
                 dval[w * kDenseThreads + tid] = double(
                     p.u_buf[((uint64_t(src_rank) * p.n_seg + sl) * p.ml + wl) * p.seg_len + o]);
+            }
+        } else {  // P2P: straight out of the source rank's [S][ml][L] buffer
+            for (uint32_t w = 0; w < p.workers; ++w) {
+                const uint32_t src_rank = w / p.ml, wl = w % p.ml;
+                dval[w * kDenseThreads + tid] = double(
+                    p.u_peers[src_rank][((uint64_t(p.s_first) + sl) * p.ml + wl) * p.seg_len + o]);
             }
         }
         const DenseOp* ops = p.ops + uint64_t(sl) * p.n_ops;
@@ -1079,12 +1097,14 @@ cudaError_t launch_coins(const DevMerge* merges, uint32_t n_merges, uint64_t see
 }
 
 cudaError_t launch_export_bits(const uint32_t* agg, uint32_t wst, uint64_t dim, uint64_t seg_len,
-                               uint32_t* out_u32, cudaStream_t st) {
+                               uint32_t* out_u32, cudaStream_t st,
+                               const uint32_t* const* agg_peers, uint32_t s_own) {
     const uint64_t n_out = ((dim + 63) / 64) * 2;
     const int threads = 256;
     uint64_t blocks = (n_out + threads - 1) / threads;
     if (blocks > 148 * 8) blocks = 148 * 8;
-    export_bits_kernel<<<int(blocks), threads, 0, st>>>(agg, wst, dim, seg_len, n_out, out_u32);
+    export_bits_kernel<<<int(blocks), threads, 0, st>>>(agg, wst, dim, seg_len, n_out, out_u32,
+                                                        agg_peers, s_own);
     return cudaGetLastError();
 }
 

@@ -53,6 +53,9 @@ struct CoopParams {
     uint32_t n_merges;
     uint64_t seg_bits;            // L
     const uint32_t* leaves;       // leaf(w, sl) = leaves + ((w/ml*n_seg + sl)*ml + w%ml)*wst
+    // P2P transport: leaf(w, sl) = peer_bits[w/ml] + ((s_first + sl)*ml + w%ml)*wst,
+    // i.e. straight out of the source rank's own [S][ml][wst] buffer
+    const uint32_t* const* peer_bits;
     uint32_t* gnodes;             // [n_seg][gmax][wst] nodes crossing stages
     uint32_t gmax;
     uint32_t* agg;                // [S][wst]
@@ -76,6 +79,9 @@ struct StreamParams {
     uint32_t words_proc, wst;
     uint32_t* bits;              // extract output: [S][ml][wst]
     const uint32_t* agg;         // decode input: [S][wst]
+    // P2P transport: segment s is read from its owner's buffer agg_peers[s / s_own]
+    const uint32_t* const* agg_peers;
+    uint32_t s_own;
     T* update;                   // optional g_t (written by local worker 0)
     T* x[kMaxLocalWorkers];      // optional replica parameters: x -= g_t (trainer.hpp:285-288)
     T eta;
@@ -98,7 +104,8 @@ cudaError_t stream_occupancy(bool f64, int* extract_blocks, int* decode_blocks);
 cudaError_t launch_coins(const DevMerge* merges, uint32_t n_merges, uint64_t seed, uint64_t round,
                          uint32_t* coins, int grid_x, cudaStream_t st);
 cudaError_t launch_export_bits(const uint32_t* agg, uint32_t wst, uint64_t dim, uint64_t seg_len,
-                               uint32_t* out_u32, cudaStream_t st);
+                               uint32_t* out_u32, cudaStream_t st,
+                               const uint32_t* const* agg_peers = nullptr, uint32_t s_own = 1);
 // x_w -= v for the local workers' parameter replicas (dense-round update).
 template <typename T>
 cudaError_t launch_sub_update(T* const* x, uint32_t ml, const T* v, uint64_t dim, int grid,
@@ -118,6 +125,7 @@ struct DenseParams {
     const T* src[kMaxLocalWorkers * 2];  // leaves: g,c pairs (1 GPU) or exchanged u (multi)
     uint32_t mode;                       // 0: leaf w = g[w] + c[w]; 1: leaf w = u buffer
     const T* u_buf;                      // mode 1: [G][s_own][ml][L] u values
+    const T* const* u_peers;             // mode 2 (P2P): rank q's own [S][ml][L] u buffer
     const DenseOp* ops;                  // [n_seg][n_ops]
     const uint16_t* final_node;          // [n_seg]
     uint32_t n_ops, n_seg, s_first, ml, workers;

@@ -11,6 +11,7 @@
 // Segments are owned by ranks in contiguous blocks (rank q owns segments
 // [q*S/G, (q+1)*S/G)), so the exchange is an all-to-all of contiguous
 // per-destination blocks and the all-gather is in place.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -19,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -134,7 +136,8 @@ marsit_status lower_plan(const Plan& plan, uint32_t s_first, uint32_t n_seg, Dev
 marsit_ctx::~marsit_ctx() {
     if (device >= 0) cudaSetDevice(device);
     for (void* p : {(void*)bits, (void*)recv, (void*)agg, (void*)err, dense_send, dense_recv,
-                    dense_mean, (void*)d_dense_ops, (void*)d_dense_final, (void*)d_metrics})
+                    dense_mean, (void*)d_dense_ops, (void*)d_dense_final, (void*)d_metrics,
+                    (void*)flags, (void*)d_peer_tables})
         if (p) cudaFree(p);
     for (auto& tp : pending) {
         cudaEventDestroy(tp.a);
@@ -281,6 +284,71 @@ marsit_status launch_coin_buffer(marsit_ctx* ctx, int b, uint64_t seed, uint64_t
 
 // Coins of this round: reuse the speculatively prefetched buffer when its tag
 // matches (seed, round); otherwise compute them now, overlapping the extract.
+// ---------------------------------------------------------------------------
+// P2P transport: stream-ordered epoch flags (driver stream memory operations,
+// resolved at run time so the library does not link libcuda).
+// ---------------------------------------------------------------------------
+using PfnStreamValue64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+struct StreamMemOps {
+    PfnStreamValue64 wait = nullptr, write = nullptr;
+};
+const StreamMemOps& stream_memops() {
+    static StreamMemOps ops;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            ops.wait = reinterpret_cast<PfnStreamValue64>(f);
+        f = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            ops.write = reinterpret_cast<PfnStreamValue64>(f);
+        cudaGetLastError();
+    });
+    return ops;
+}
+
+// Flags: every rank owns 2 x G u64 slots, flags[which * G + q] = the last
+// epoch rank q reported for `which` (0: phase-0 data ready, 1: owned results
+// ready).  A rank signals by writing its slot in every rank's array (remote
+// stream writes, each preceded by a system-wide fence) and waits only on its
+// own, local array — polling never crosses NVLink.
+marsit_status p2p_signal(marsit_ctx* ctx, int which, cudaStream_t st) {
+    if (!ctx->p2p) return MARSIT_OK;
+    const StreamMemOps& m = stream_memops();
+    if (!m.write) return fail(MARSIT_EUNSUPPORTED, "cuStreamWriteValue64 unavailable");
+    for (uint32_t q = 0; q < ctx->G; ++q) {
+        if (q == ctx->rank) continue;
+        uint64_t* slot = const_cast<uint64_t*>(ctx->peer_flags[q]) + size_t(which) * ctx->G + ctx->rank;
+        const CUresult r = m.write(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(slot),
+                                   ctx->epoch, 0);
+        if (r != CUDA_SUCCESS) return fail(MARSIT_ECUDA, "cuStreamWriteValue64 failed");
+    }
+    return MARSIT_OK;
+}
+
+// The stream waits until every peer has reported this epoch for `which`.
+marsit_status p2p_wait(marsit_ctx* ctx, int which, cudaStream_t st) {
+    if (!ctx->p2p) return MARSIT_OK;
+    const StreamMemOps& m = stream_memops();
+    if (!m.wait) return fail(MARSIT_EUNSUPPORTED, "cuStreamWaitValue64 unavailable");
+    for (uint32_t q = 0; q < ctx->G; ++q) {
+        if (q == ctx->rank) continue;  // own work: stream order already holds
+        const uint64_t* slot = ctx->flags + size_t(which) * ctx->G + q;
+        const CUresult r = m.wait(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(slot),
+                                  ctx->epoch, CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) return fail(MARSIT_ECUDA, "cuStreamWaitValue64 failed");
+    }
+    return MARSIT_OK;
+}
+
+const uint32_t* const* p2p_table(const marsit_ctx* ctx, int which) {
+    return ctx->p2p ? reinterpret_cast<const uint32_t* const*>(ctx->d_peer_tables + size_t(which) * ctx->G)
+                    : nullptr;
+}
+
 marsit_status run_coins(marsit_ctx* ctx, uint64_t seed, uint64_t round, cudaStream_t st) {
     if (ctx->coin_total_words == 0) return MARSIT_OK;
     for (int b = 0; b < 2; ++b)
@@ -353,6 +421,8 @@ marsit_status run_decode(marsit_ctx* ctx, const void* const* g, const void* cons
         p.n_proc = n;
         p.matches = matches;
         p.n_workers = ctx->M;
+        p.agg_peers = p2p_table(ctx, 1);
+        p.s_own = ctx->s_own;
         CUDA_TRY(launch_decode(p, vec, ctx->decode_grid, st));
     } else {
         auto p = stream_params<double>(ctx, g, c, c_out, update, eta, params);
@@ -360,6 +430,8 @@ marsit_status run_decode(marsit_ctx* ctx, const void* const* g, const void* cons
         p.n_proc = n;
         p.matches = matches;
         p.n_workers = ctx->M;
+        p.agg_peers = p2p_table(ctx, 1);
+        p.s_own = ctx->s_own;
         CUDA_TRY(launch_decode(p, vec, ctx->decode_grid, st));
     }
     return ctx->end_phase(kPhDecode, st, ev, 1);
@@ -371,7 +443,7 @@ marsit_status run_export(marsit_ctx* ctx, uint64_t* out, cudaStream_t st) {
     marsit_status s = ctx->begin_phase(st, &ev);
     if (s) return s;
     CUDA_TRY(launch_export_bits(ctx->agg, ctx->wst, ctx->D, ctx->L,
-                                reinterpret_cast<uint32_t*>(out), st));
+                                reinterpret_cast<uint32_t*>(out), st, p2p_table(ctx, 1), ctx->s_own));
     return ctx->end_phase(kPhExport, st, ev, 1);
 }
 
@@ -411,6 +483,9 @@ marsit_status dense_phase(marsit_ctx* ctx, int phase, const void* const* g, cons
     p.inv_m = 1.0 / double(ctx->M);
     p.err = ctx->err;
     uint64_t launches = 0;
+    if (phase == 0 && ctx->p2p) ++ctx->epoch;
+    if (phase == 1 && (s = p2p_wait(ctx, 0, st))) return s;
+    if (phase == 2 && (s = p2p_wait(ctx, 1, st))) return s;
     if (phase == 0 && ctx->G > 1) {
         std::vector<const T*> gg(ctx->ml), cc(ctx->ml);
         for (uint32_t w = 0; w < ctx->ml; ++w) {
@@ -430,17 +505,29 @@ marsit_status dense_phase(marsit_ctx* ctx, int phase, const void* const* g, cons
             }
             p.mean = static_cast<T*>(mean);
         } else {
-            p.mode = 1;
+            p.mode = ctx->p2p ? 2 : 1;
             p.u_buf = static_cast<const T*>(ctx->dense_recv);
+            p.u_peers = reinterpret_cast<const T* const*>(ctx->d_peer_tables + 2 * size_t(ctx->G));
             p.mean = static_cast<T*>(ctx->dense_mean);  // padded [S*L]; owned block written
             p.dim = uint64_t(ctx->S) * ctx->L;
         }
         CUDA_TRY(launch_dense_reduce(p, ctx->stream_grid, st));
         ++launches;
     } else if (phase == 2) {
-        if (ctx->G > 1)
+        if (ctx->p2p) {  // every owner's block straight from its buffer (peer copies)
+            const size_t block = size_t(ctx->s_own) * ctx->L;
+            for (uint32_t q = 0; q < ctx->G; ++q) {
+                const size_t off = q * block;
+                if (off >= ctx->D) break;
+                const size_t n = std::min<size_t>(block, ctx->D - off);
+                CUDA_TRY(cudaMemcpyAsync(static_cast<T*>(mean) + off,
+                                         static_cast<const T*>(ctx->peer_dense_mean[q]) + off,
+                                         n * sizeof(T), cudaMemcpyDefault, st));
+            }
+        } else if (ctx->G > 1) {
             CUDA_TRY(cudaMemcpyAsync(mean, ctx->dense_mean, ctx->D * sizeof(T),
                                      cudaMemcpyDeviceToDevice, st));
+        }
         for (uint32_t w = 0; w < ctx->ml; ++w)
             CUDA_TRY(cudaMemsetAsync(c_out[w], 0, ctx->D * sizeof(T), st));  // sync.hpp:83-85
         if (params) {  // x_w -= mean (trainer.hpp:285-288)
@@ -451,7 +538,10 @@ marsit_status dense_phase(marsit_ctx* ctx, int phase, const void* const* g, cons
             ++launches;
         }
     }
-    return ctx->end_phase(kPhDense, st, ev, launches);
+    if ((s = ctx->end_phase(kPhDense, st, ev, launches))) return s;
+    if (phase == 0) return p2p_signal(ctx, 0, st);  // my u blocks are ready
+    if (phase == 1) return p2p_signal(ctx, 1, st);  // my owned mean block is ready
+    return MARSIT_OK;
 }
 
 marsit_status dense_exchange(marsit_ctx* ctx, cudaStream_t st) {
@@ -528,13 +618,18 @@ marsit_status sign_phase(marsit_ctx* ctx, int phase, uint64_t t, double eta_s, u
                          void* d_update, cudaStream_t st) {
     marsit_status s = MARSIT_OK;
     if (phase == 0) {
+        if (ctx->p2p) ++ctx->epoch;
         if ((s = run_coins(ctx, seed, t, st))) return s;
-        return run_extract(ctx, d_grads, d_comp, st);
+        if ((s = run_extract(ctx, d_grads, d_comp, st))) return s;
+        return p2p_signal(ctx, 0, st);  // my packed signs are ready
     }
     if (phase == 1) {
+        if ((s = p2p_wait(ctx, 0, st))) return s;  // every rank's packed signs
         if ((s = run_merge(ctx, seed, t, st))) return s;
-        return prefetch_coins(ctx, seed, t, st);
+        if ((s = prefetch_coins(ctx, seed, t, st))) return s;
+        return p2p_signal(ctx, 1, st);  // my owned aggregates are ready
     }
+    if ((s = p2p_wait(ctx, 1, st))) return s;  // every owner's aggregates
     if ((s = run_decode(ctx, d_grads, d_comp, d_comp_out, params, d_update, eta_s, st))) return s;
     return run_export(ctx, d_agg_bits, st);
 }
@@ -567,8 +662,9 @@ marsit_status sign_round_impl(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_
                               void* d_update, cudaStream_t st) {
     marsit_status s = check_round_args(ctx, eta_s, d_grads, d_comp, d_comp_out, params, true);
     if (s) return s;
-    if (ctx->G > 1 && !ctx->comm)
+    if (ctx->G > 1 && !ctx->comm && !ctx->p2p)
         return fail(MARSIT_EUNSUPPORTED, "external-transport context: use marsit_round_phase");
+    if (ctx->p2p && !ctx->peers_set) return fail(MARSIT_EPARAM, "P2P transport: call marsit_ctx_set_peers");
     note_round(ctx, t, false);
     if (ctx->pipeline) {
         // st : coins? E ............ D0 D1 ... D(S-1)   (D_s waits M_s)
@@ -624,8 +720,9 @@ marsit_status dense_round_any(marsit_ctx* ctx, uint64_t t, const void* const* d_
     marsit_status s = check_round_args(ctx, 1.0, d_grads, d_comp, d_comp_out, params, false);
     if (s) return s;
     if (!d_mean) return fail(MARSIT_EPARAM, "mean is null");
-    if (ctx->G > 1 && !ctx->comm)
+    if (ctx->G > 1 && !ctx->comm && !ctx->p2p)
         return fail(MARSIT_EUNSUPPORTED, "external-transport context: use marsit_round_phase");
+    if (ctx->p2p && !ctx->peers_set) return fail(MARSIT_EPARAM, "P2P transport: call marsit_ctx_set_peers");
     note_round(ctx, t, true);
     if ((s = dense_phase_any(ctx, 0, d_grads, d_comp, d_comp_out, params, d_mean, st))) return s;
     if ((s = dense_exchange(ctx, st))) return s;
@@ -767,7 +864,11 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     if (hs.workers / G > kMaxLocalWorkers)
         return fail(MARSIT_EUNSUPPORTED, "too many workers per rank (max 64)");
     const bool external = desc->transport == MARSIT_TRANSPORT_EXTERNAL;
-    if (G > 1 && !external && !desc->nccl_id && !shared_comm)
+    const bool p2p = G > 1 && desc->transport == MARSIT_TRANSPORT_P2P;
+    if (desc->transport != MARSIT_TRANSPORT_NCCL && desc->transport != MARSIT_TRANSPORT_EXTERNAL &&
+        desc->transport != MARSIT_TRANSPORT_P2P)
+        return fail(MARSIT_EPARAM, "unknown transport");
+    if (G > 1 && !external && !p2p && !desc->nccl_id && !shared_comm)
         return fail(MARSIT_EPARAM, "nccl_id required for nranks > 1");
     if (!have_device())
         return fail(MARSIT_ECUDA, "no CUDA device available (this library has no CPU path)");
@@ -812,7 +913,7 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     // single GPU with several segments: per-segment merge launches sized to
     // co-reside with the decode (MARSIT_PIPELINE=0 disables)
     ctx->pipeline = G == 1 && ctx->S >= 2 && env_int("MARSIT_PIPELINE", 0) != 0 &&
-                    desc->transport != MARSIT_TRANSPORT_EXTERNAL;
+                    desc->transport == MARSIT_TRANSPORT_NCCL;
     if (ctx->pipeline) {
         if ((st = mr.configure(ctx->sm_count, 1, env_int("MARSIT_PIPE_MERGE_CTAS", 1)))) return st;
     } else {
@@ -825,9 +926,16 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     CUDA_TRY(cudaMemset(ctx->bits, 0, sizeof(uint32_t) * ctx->S * ctx->ml * wst));
     CUDA_TRY(cudaMalloc(&ctx->agg, sizeof(uint32_t) * ctx->S * wst));
     CUDA_TRY(cudaMemset(ctx->agg, 0, sizeof(uint32_t) * ctx->S * wst));
-    if (G > 1) {
+    if (G > 1 && !p2p) {
         CUDA_TRY(cudaMalloc(&ctx->recv, sizeof(uint32_t) * ctx->S * ctx->ml * wst));
         CUDA_TRY(cudaMemset(ctx->recv, 0, sizeof(uint32_t) * ctx->S * ctx->ml * wst));
+    }
+    if (p2p) {
+        ctx->p2p = true;
+        CUDA_TRY(cudaMalloc(&ctx->flags, 2 * size_t(G) * sizeof(uint64_t)));
+        CUDA_TRY(cudaMemset(ctx->flags, 0, 2 * size_t(G) * sizeof(uint64_t)));
+        CUDA_TRY(cudaMalloc(&ctx->d_peer_tables, 3 * size_t(G) * sizeof(void*)));
+        CUDA_TRY(cudaMemset(ctx->d_peer_tables, 0, 3 * size_t(G) * sizeof(void*)));
     }
     CUDA_TRY(cudaMalloc(&ctx->err, sizeof(int)));
     CUDA_TRY(cudaMemset(ctx->err, 0, sizeof(int)));
@@ -901,10 +1009,10 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     if (G > 1) {
         const size_t dense_elems = size_t(ctx->S) * ctx->ml * ctx->L;
         CUDA_TRY(cudaMalloc(&ctx->dense_send, ctx->esize * dense_elems));
-        CUDA_TRY(cudaMalloc(&ctx->dense_recv, ctx->esize * dense_elems));
+        if (!p2p) CUDA_TRY(cudaMalloc(&ctx->dense_recv, ctx->esize * dense_elems));
         CUDA_TRY(cudaMalloc(&ctx->dense_mean, ctx->esize * size_t(ctx->S) * ctx->L));
-        if (external) {
-            ctx->comm = nullptr;  // the caller moves the blocks (marsit_round_phase)
+        if (external || p2p) {
+            ctx->comm = nullptr;  // the caller moves the blocks / peer memory
         } else if (shared_comm) {
             ctx->comm = shared_comm;
             ctx->owns_comm = false;
@@ -994,6 +1102,7 @@ marsit_status marsit_round_phase(marsit_ctx* ctx, int phase, uint64_t t, uint64_
     marsit_status s = check_round_args(ctx, eta_s, d_grads, d_comp, d_comp_out, nullptr, !dense);
     if (s) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (ctx->p2p && !ctx->peers_set) return fail(MARSIT_EPARAM, "P2P transport: call marsit_ctx_set_peers");
     if (phase == 0) note_round(ctx, t, dense);
     if (dense) {
         if (!d_update) return fail(MARSIT_EPARAM, "dense round needs d_update for the mean");
@@ -1145,6 +1254,67 @@ marsit_status marsit_ctx_check(marsit_ctx* ctx, void* stream) {
         CUDA_TRY(cudaStreamSynchronize(st));
         return fail(MARSIT_ENONFINITE, "DenseVector: non-finite entry");
     }
+    return MARSIT_OK;
+}
+
+marsit_status marsit_ctx_p2p_buffers(const marsit_ctx* ctx, marsit_p2p_buffers* out) {
+    if (!ctx || !out) return fail(MARSIT_EPARAM, "null argument");
+    if (!ctx->p2p) return fail(MARSIT_EPARAM, "not a P2P-transport context (nranks > 1)");
+    out->bits = ctx->bits;
+    out->agg = ctx->agg;
+    out->dense_send = ctx->dense_send;
+    out->dense_mean = ctx->dense_mean;
+    out->flags = ctx->flags;
+    return MARSIT_OK;
+}
+
+marsit_status marsit_ctx_set_peers(marsit_ctx* ctx, const marsit_p2p_buffers* peers,
+                                   uint32_t nranks) {
+    if (!ctx || !peers) return fail(MARSIT_EPARAM, "null argument");
+    if (!ctx->p2p) return fail(MARSIT_EPARAM, "not a P2P-transport context (nranks > 1)");
+    if (nranks != ctx->G) return fail(MARSIT_EPARAM, "peer table must have one entry per rank");
+    std::vector<void*> tab(3 * size_t(ctx->G));
+    ctx->peer_flags.assign(ctx->G, nullptr);
+    ctx->peer_dense_mean.assign(ctx->G, nullptr);
+    for (uint32_t q = 0; q < ctx->G; ++q) {
+        const marsit_p2p_buffers& b = peers[q];
+        if (!b.bits || !b.agg || !b.dense_send || !b.dense_mean || !b.flags)
+            return fail(MARSIT_EPARAM, "peer table: null buffer");
+        tab[q] = b.bits;
+        tab[ctx->G + q] = b.agg;
+        tab[2 * size_t(ctx->G) + q] = b.dense_send;
+        ctx->peer_flags[q] = static_cast<const uint64_t*>(b.flags);
+        ctx->peer_dense_mean[q] = b.dense_mean;
+    }
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    CUDA_TRY(cudaMemcpy(ctx->d_peer_tables, tab.data(), tab.size() * sizeof(void*),
+                        cudaMemcpyHostToDevice));
+    ctx->merge.peer_bits = reinterpret_cast<const uint32_t* const*>(ctx->d_peer_tables);
+    ctx->peers_set = true;
+    return MARSIT_OK;
+}
+
+marsit_status marsit_ipc_handle(const void* d_ptr, void* handle_out) {
+    if (!d_ptr || !handle_out) return fail(MARSIT_EPARAM, "null argument");
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+    static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+    std::memcpy(handle_out, &h, sizeof(h));
+    return MARSIT_OK;
+}
+
+marsit_status marsit_ipc_open(const void* handle, int device, void** d_ptr_out) {
+    if (!handle || !d_ptr_out) return fail(MARSIT_EPARAM, "null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    CUDA_TRY(cudaSetDevice(device));
+    CUDA_TRY(cudaIpcOpenMemHandle(d_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+    return MARSIT_OK;
+}
+
+marsit_status marsit_ipc_close(void* d_ptr) {
+    if (!d_ptr) return fail(MARSIT_EPARAM, "null argument");
+    CUDA_TRY(cudaIpcCloseMemHandle(d_ptr));
     return MARSIT_OK;
 }
 

@@ -142,3 +142,103 @@ def test_full_size_c2_c4_ranks_bit_identical(topo, a, b, D):
     for w in range(W):
         assert torch.equal(comp_g[w], comp_1[w]), w
     single.check()
+
+
+# --------------------------------------------------------------------------
+# P2P transport (fused over peer memory): on one GPU the G rank contexts'
+# peer tables point at each other's buffers.  Phase-ordered on one stream,
+# every stream wait is already satisfied when it is reached; the concurrent
+# variant below runs each rank on its own stream so the waits really block.
+# --------------------------------------------------------------------------
+def p2p_contexts(D, sched, G, dtype=torch.float32):
+    ctxs = [mb.Context(D, sched, dtype, 0, nranks=G, rank=r, transport="p2p") for r in range(G)]
+    table = [c.p2p_buffers() for c in ctxs]
+    for c in ctxs:
+        c.set_peers(table)
+    return ctxs
+
+
+@pytest.mark.parametrize("topo,a,b,G,D", [
+    ("ring", 8, 0, 2, 100_003),
+    ("ring", 8, 0, 8, 25_601),
+    ("torus", 2, 4, 4, 60_211),
+    ("torus", 2, 4, 8, 1_000_003),
+    ("ring", 4, 0, 4, 1_000_000),
+])
+def test_p2p_transport_matches_single_context(topo, a, b, G, D):
+    sched = mb.build_ring_schedule(a) if topo == "ring" else mb.build_torus_schedule(a, b)
+    W = sched.workers
+    ml = W // G
+    seed, period = 2026, 3
+    single = mb.Context(D, sched, torch.float32, 0)
+    ctxs = p2p_contexts(D, sched, G)
+    comp_1 = [torch.zeros(D, device=DEV) for _ in range(W)]
+    comp_g = [torch.zeros(D, device=DEV) for _ in range(W)]
+    for t in range(0, 5):  # t = 0 and 3 are dense rounds (K = 3)
+        grads = [torch.empty(D, device=DEV) for _ in range(W)]
+        for w in range(W):
+            mb.fill_recipe(grads[w], t % 2, seed, w, t)
+        dense = t % period == 0
+        agg_1 = torch.empty((D + 63) // 64, dtype=torch.int64, device=DEV)
+        mean_1 = torch.empty(D, device=DEV)
+        if dense:
+            single.dense_round(t, grads, comp_1, mean_1)
+        else:
+            single.sign_round(t, ETA, seed, grads, comp_1, agg_bits=agg_1)
+        aggs = [torch.empty_like(agg_1) for _ in range(G)]
+        means = [torch.empty(D, device=DEV) for _ in range(G)]
+        for phase in range(3):
+            for r, ctx in enumerate(ctxs):
+                loc = slice(r * ml, (r + 1) * ml)
+                full = ctx.round_phase(phase, t, period, ETA, seed, grads[loc], comp_g[loc],
+                                       agg_bits=None if dense else aggs[r],
+                                       update=means[r] if dense else None)
+                assert full == dense
+        torch.cuda.synchronize()
+        for w in range(W):
+            assert torch.equal(comp_g[w], comp_1[w]), (t, w)
+        for r in range(G):
+            if dense:
+                assert torch.equal(means[r], mean_1), (t, r)
+            else:
+                assert torch.equal(aggs[r], agg_1), (t, r)  # every rank reads every owner
+    single.check()
+    for c in ctxs:
+        c.check()
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_p2p_transport_concurrent_streams(G):
+    """Each rank's whole round on its own stream, enqueued rank by rank: rank
+    0's stream blocks in its flag wait until the other ranks' extracts ran.
+    Small D, so every rank's cooperative merge grid fits the GPU at once."""
+    sched = mb.build_ring_schedule(8)
+    W, D, seed = 8, 50_003, 7
+    ml = W // G
+    single = mb.Context(D, sched, torch.float32, 0)
+    ctxs = p2p_contexts(D, sched, G)
+    streams = [torch.cuda.Stream() for _ in range(G)]
+    comp_1 = [torch.zeros(D, device=DEV) for _ in range(W)]
+    comp_g = [torch.zeros(D, device=DEV) for _ in range(W)]
+    for t in range(1, 4):
+        grads = [torch.empty(D, device=DEV) for _ in range(W)]
+        for w in range(W):
+            mb.fill_recipe(grads[w], 0, seed, w, t)
+        single.sign_round(t, ETA, seed, grads, comp_1)
+        torch.cuda.synchronize()
+        for r, ctx in enumerate(ctxs):
+            loc = slice(r * ml, (r + 1) * ml)
+            ctx.sign_round(t, ETA, seed, grads[loc], comp_g[loc], stream=streams[r].cuda_stream)
+        torch.cuda.synchronize()
+        for w in range(W):
+            assert torch.equal(comp_g[w], comp_1[w]), (t, w)
+
+
+def test_p2p_transport_requires_peers():
+    sched = mb.build_ring_schedule(4)
+    ctx = mb.Context(1000, sched, torch.float32, 0, nranks=2, rank=0, transport="p2p")
+    g = [torch.zeros(1000, device=DEV) for _ in range(2)]
+    with pytest.raises(mb.ParameterError):
+        ctx.sign_round(1, ETA, 1, g, g)
+    with pytest.raises(mb.ParameterError):
+        ctx.set_peers([ctx.p2p_buffers()])  # one entry per rank
