@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
+                    help="N > 1: fused over NVLink peer memory (p2p) or NCCL send/recv + all-gather")
     ap.add_argument("--recipe", type=int, default=0, help="0 dyadic (independent), 1 correlated")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -235,14 +237,16 @@ def run_ours(args):
     sched = mb.build_ring_schedule(a) if topo == "ring" else mb.build_torus_schedule(a, b)
     M = sched.workers
     nccl_id = None
-    if world > 1:
+    if world > 1 and args.transport == "nccl":
         idt = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
             idt.copy_(torch.frombuffer(bytearray(mb.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(idt, 0)
         nccl_id = bytes(idt.cpu().tolist())
     ctx = mb.Context(D, sched, torch.float32, local_rank, nranks=world, rank=rank,
-                     nccl_id=nccl_id)
+                     nccl_id=nccl_id, transport=args.transport if world > 1 else None)
+    if world > 1 and args.transport == "p2p":
+        mb.exchange_p2p_buffers(ctx)  # CUDA IPC handles over torch.distributed
     ml, w0 = ctx.local_workers, ctx.first_worker
     grads = [torch.empty(D, device=dev) for _ in range(ml)]
     for i in range(ml):
@@ -371,6 +375,7 @@ def run_ours(args):
                                    f"({ml} per GPU), D={D}, sign round + compensation",
                        "D": D, "workers": M, "topology": topo,
                        "parallelism": f"{world} rank(s) x {ml} workers",
+                       "transport": (args.transport if world > 1 else "none (1 rank)"),
                        "l2": "inputs (%.1f GB) > L2 (126 MB): no flush needed"
                              % (2 * ml * D * 4 / 1e9)},
             "worker_gelem_s": M * D / (ms * 1e-3) / 1e9,

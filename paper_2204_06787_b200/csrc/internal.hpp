@@ -311,6 +311,7 @@ struct marsit_ctx {
     // P2P transport (marsit_ctx_set_peers): device tables of the peers'
     // buffers, host copies of their flag words, this rank's epoch flags
     bool p2p = false, peers_set = false;
+    bool flag_kernel = false;   // signal with flag_write_kernel instead of stream writes
     uint64_t* flags = nullptr;  // [2][G]: epoch each rank reported (data ready, results ready)
     uint64_t epoch = 0;         // rounds (sign or dense) run so far
     std::vector<const uint64_t*> peer_flags;

@@ -1108,6 +1108,17 @@ cudaError_t launch_export_bits(const uint32_t* agg, uint32_t wst, uint64_t dim, 
     return cudaGetLastError();
 }
 
+__global__ void flag_write_kernel(const FlagSlots s, unsigned long long value) {
+    __threadfence_system();  // the stream's earlier writes are visible system-wide first
+    for (uint32_t i = threadIdx.x; i < s.n; i += blockDim.x)
+        *reinterpret_cast<volatile unsigned long long*>(s.slot[i]) = value;
+}
+
+cudaError_t launch_flag_write(const FlagSlots& s, unsigned long long value, cudaStream_t st) {
+    flag_write_kernel<<<1, 32, 0, st>>>(s, value);
+    return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_fill_recipe(int recipe, uint64_t seed, uint64_t worker, uint64_t round,
                                uint64_t dim, T* out, cudaStream_t st) {

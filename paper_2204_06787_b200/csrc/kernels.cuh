@@ -106,6 +106,14 @@ cudaError_t launch_coins(const DevMerge* merges, uint32_t n_merges, uint64_t see
 cudaError_t launch_export_bits(const uint32_t* agg, uint32_t wst, uint64_t dim, uint64_t seg_len,
                                uint32_t* out_u32, cudaStream_t st,
                                const uint32_t* const* agg_peers = nullptr, uint32_t s_own = 1);
+// P2P epoch flags: after everything before it on the stream, a system-wide
+// fence then slots[i] = value (peer memory stores; fallback when the driver's
+// stream write on peer memory is unavailable).
+struct FlagSlots {
+    unsigned long long* slot[kMaxLocalWorkers];
+    uint32_t n;
+};
+cudaError_t launch_flag_write(const FlagSlots& s, unsigned long long value, cudaStream_t st);
 // x_w -= v for the local workers' parameter replicas (dense-round update).
 template <typename T>
 cudaError_t launch_sub_update(T* const* x, uint32_t ml, const T* v, uint64_t dim, int grid,

@@ -318,14 +318,19 @@ const StreamMemOps& stream_memops() {
 marsit_status p2p_signal(marsit_ctx* ctx, int which, cudaStream_t st) {
     if (!ctx->p2p) return MARSIT_OK;
     const StreamMemOps& m = stream_memops();
-    if (!m.write) return fail(MARSIT_EUNSUPPORTED, "cuStreamWriteValue64 unavailable");
+    FlagSlots fs{};
     for (uint32_t q = 0; q < ctx->G; ++q) {
         if (q == ctx->rank) continue;
         uint64_t* slot = const_cast<uint64_t*>(ctx->peer_flags[q]) + size_t(which) * ctx->G + ctx->rank;
-        const CUresult r = m.write(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(slot),
-                                   ctx->epoch, 0);
-        if (r != CUDA_SUCCESS) return fail(MARSIT_ECUDA, "cuStreamWriteValue64 failed");
+        if (m.write && !ctx->flag_kernel) {
+            const CUresult r = m.write(reinterpret_cast<CUstream>(st),
+                                       reinterpret_cast<CUdeviceptr>(slot), ctx->epoch, 0);
+            if (r == CUDA_SUCCESS) continue;
+            ctx->flag_kernel = true;  // stream writes to peer memory unsupported: store from a kernel
+        }
+        fs.slot[fs.n++] = reinterpret_cast<unsigned long long*>(slot);
     }
+    if (fs.n) CUDA_TRY(launch_flag_write(fs, ctx->epoch, st));
     return MARSIT_OK;
 }
 
@@ -932,6 +937,7 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     }
     if (p2p) {
         ctx->p2p = true;
+        ctx->flag_kernel = env_int("MARSIT_P2P_FLAG_KERNEL", 0) != 0;
         CUDA_TRY(cudaMalloc(&ctx->flags, 2 * size_t(G) * sizeof(uint64_t)));
         CUDA_TRY(cudaMemset(ctx->flags, 0, 2 * size_t(G) * sizeof(uint64_t)));
         CUDA_TRY(cudaMalloc(&ctx->d_peer_tables, 3 * size_t(G) * sizeof(void*)));

@@ -207,11 +207,15 @@ def test_p2p_transport_matches_single_context(topo, a, b, G, D):
         c.check()
 
 
+@pytest.mark.parametrize("flag_kernel", ["0", "1"])
 @pytest.mark.parametrize("G", [2, 4])
-def test_p2p_transport_concurrent_streams(G):
+def test_p2p_transport_concurrent_streams(G, flag_kernel, monkeypatch):
     """Each rank's whole round on its own stream, enqueued rank by rank: rank
     0's stream blocks in its flag wait until the other ranks' extracts ran.
-    Small D, so every rank's cooperative merge grid fits the GPU at once."""
+    Small D, so every rank's cooperative merge grid fits the GPU at once.
+    flag_kernel = 1: the epoch flags are stored by a kernel (the fallback when
+    stream writes to peer memory are unavailable)."""
+    monkeypatch.setenv("MARSIT_P2P_FLAG_KERNEL", flag_kernel)
     sched = mb.build_ring_schedule(8)
     W, D, seed = 8, 50_003, 7
     ml = W // G
