@@ -336,6 +336,7 @@ typedef struct marsit_driver_desc {
     double eta_s;                     /* > 0                                       */
     uint64_t global_seed;
     uint64_t first_round;             /* t of the first step (trainer starts at 0) */
+    marsit_transport transport;       /* nranks > 1: NCCL (default) or P2P         */
 } marsit_driver_desc;
 
 marsit_status marsit_driver_create(const marsit_driver_desc* desc, marsit_driver** out);
@@ -356,6 +357,13 @@ marsit_status marsit_driver_state(const marsit_driver* drv, uint64_t* next_round
  * (checkpoint.hpp:18-91) does not keep.  Synchronises `stream`. */
 marsit_status marsit_driver_save(marsit_driver* drv, const char* path, void* stream);
 marsit_status marsit_driver_load(marsit_driver* drv, const char* path, void* stream);
+/* P2P transport (desc.transport = MARSIT_TRANSPORT_P2P): every bucket owns a
+ * context whose buffers the ranks exchange as for marsit_ctx_set_peers, once
+ * per bucket, before the first step. */
+marsit_status marsit_driver_p2p_buffers(const marsit_driver* drv, uint32_t bucket,
+                                        marsit_p2p_buffers* out);
+marsit_status marsit_driver_set_peers(marsit_driver* drv, uint32_t bucket,
+                                      const marsit_p2p_buffers* peers, uint32_t nranks);
 /* Round metrics of the last step summed over the buckets (matching over all D
  * coordinates, as trainer.hpp:280-281 records it per round). */
 marsit_status marsit_driver_set_metrics(marsit_driver* drv, int enable);

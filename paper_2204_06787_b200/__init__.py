@@ -578,13 +578,8 @@ def ipc_open(handle: bytes, device: int) -> int:
     return out.value
 
 
-def exchange_p2p_buffers(ctx: "Context", group=None):
-    """Multi-process setup of a P2P-transport context over torch.distributed:
-    every rank exports its buffers as IPC handles, maps the others' and hands
-    the full table to ctx.set_peers.  Returns the mapped pointers (close them
-    with marsit_ipc_close when the context is gone)."""
+def _exchange_tables(mine, rank: int, device: int, set_peers, group=None):
     import torch.distributed as dist
-    mine = ctx.p2p_buffers()
     names = ("bits", "agg", "dense_send", "dense_mean", "flags")
     handles = {k: ipc_handle(getattr(mine, k)) for k in names}
     world = [None] * dist.get_world_size(group)
@@ -593,15 +588,23 @@ def exchange_p2p_buffers(ctx: "Context", group=None):
     for q, h in enumerate(world):
         b = N.P2PBuffers()
         for k in names:
-            if q == ctx.rank:
+            if q == rank:
                 setattr(b, k, getattr(mine, k))
             else:
-                ptr = ipc_open(h[k], ctx.device)
+                ptr = ipc_open(h[k], device)
                 opened.append(ptr)
                 setattr(b, k, ptr)
         table.append(b)
-    ctx.set_peers(table)
+    set_peers(table)
     return opened
+
+
+def exchange_p2p_buffers(ctx: "Context", group=None):
+    """Multi-process setup of a P2P-transport context over torch.distributed:
+    every rank exports its buffers as IPC handles, maps the others' and hands
+    the full table to ctx.set_peers.  Returns the mapped pointers (close them
+    with marsit_ipc_close when the context is gone)."""
+    return _exchange_tables(ctx.p2p_buffers(), ctx.rank, ctx.device, ctx.set_peers, group)
 
 
 def merge_signs(received: AggregateSign, local: AggregateSign, key: int, used: int = 0):
@@ -638,7 +641,9 @@ class Driver:
     def __init__(self, dim: int, schedule: Schedule, *, eta_s: float, global_seed: int,
                  period: Optional[int] = None, bucket_elems: int = 0, dtype=None,
                  device: int = 0, first_round: int = 0, nranks: int = 1, rank: int = 0,
-                 nccl_id: Optional[bytes] = None):
+                 nccl_id: Optional[bytes] = None, transport: str = "nccl"):
+        """transport (nranks > 1): "nccl", or "p2p" (then exchange every
+        bucket's buffers with set_peers / exchange_p2p_buffers first)."""
         import torch
         dtype = dtype or torch.float32
         if period == 0:
@@ -660,10 +665,29 @@ class Driver:
         d.eta_s = float(eta_s)
         d.global_seed = global_seed
         d.first_round = first_round
+        d.transport = {"nccl": 0, "p2p": 2}[transport]
         out = C.c_void_p()
         _check(N.lib().marsit_driver_create(C.byref(d), C.byref(out)))
         self._h = out
         self.local_workers = schedule.workers // nranks
+        self.rank, self.nranks, self.transport = rank, nranks, transport
+
+    def p2p_buffers(self, bucket: int) -> "N.P2PBuffers":
+        b = N.P2PBuffers()
+        _check(N.lib().marsit_driver_p2p_buffers(self._h, bucket, C.byref(b)))
+        return b
+
+    def set_peers(self, bucket: int, peers: Sequence["N.P2PBuffers"]):
+        arr = (N.P2PBuffers * len(peers))(*peers)
+        _check(N.lib().marsit_driver_set_peers(self._h, bucket, arr, len(peers)))
+
+    def exchange_p2p_buffers(self, group=None):
+        """CUDA IPC exchange of every bucket's buffers over torch.distributed."""
+        opened = []
+        for b in range(self.state()["buckets"]):
+            opened += _exchange_tables(self.p2p_buffers(b), self.rank, self.device,
+                                       lambda tab, b=b: self.set_peers(b, tab), group)
+        return opened
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -674,13 +698,13 @@ class Driver:
             pass
         self._h = None
 
-    def step(self, grads, params=None, update=None):
+    def step(self, grads, params=None, update=None, stream=None):
         g = N.ptr_array([x.data_ptr() for x in grads])
         pp = N.ptr_array([x.data_ptr() for x in params]) if params is not None else None
         full = C.c_int()
         _check(N.lib().marsit_driver_step(
             self._h, g, pp, C.c_void_p(update.data_ptr() if update is not None else None),
-            C.byref(full), _stream_ptr(self.device)))
+            C.byref(full), stream if stream is not None else _stream_ptr(self.device)))
         return bool(full.value)
 
     def compensation(self, i: int):

@@ -31,7 +31,8 @@ class DriverDesc(C.Structure):
     _fields_ = [("dim", C.c_uint64), ("schedule", C.c_void_p), ("dtype", C.c_int),
                 ("device", C.c_int), ("nranks", C.c_uint32), ("rank", C.c_uint32),
                 ("nccl_id", C.c_void_p), ("bucket_elems", C.c_uint64), ("period", C.c_uint64),
-                ("eta_s", C.c_double), ("global_seed", C.c_uint64), ("first_round", C.c_uint64)]
+                ("eta_s", C.c_double), ("global_seed", C.c_uint64), ("first_round", C.c_uint64),
+                ("transport", C.c_int)]
 
 
 class CtxDesc(C.Structure):
@@ -94,6 +95,8 @@ SIGNATURES = {
     "marsit_ctx_set_metrics": (_i32, [_vp, _i32]),
     "marsit_ctx_p2p_buffers": (_i32, [_vp, C.POINTER(P2PBuffers)]),
     "marsit_ctx_set_peers": (_i32, [_vp, C.POINTER(P2PBuffers), _u32]),
+    "marsit_driver_p2p_buffers": (_i32, [_vp, _u32, C.POINTER(P2PBuffers)]),
+    "marsit_driver_set_peers": (_i32, [_vp, _u32, C.POINTER(P2PBuffers), _u32]),
     "marsit_ipc_handle": (_i32, [_vp, _vp]),
     "marsit_ipc_open": (_i32, [_vp, _i32, C.POINTER(_vp)]),
     "marsit_ipc_close": (_i32, [_vp]),

@@ -107,6 +107,8 @@ marsit_status marsit_driver_create(const marsit_driver_desc* desc, marsit_driver
         cd.nranks = desc->nranks;
         cd.rank = desc->rank;
         cd.nccl_id = desc->nccl_id;
+        cd.transport = desc->transport == MARSIT_TRANSPORT_P2P ? MARSIT_TRANSPORT_P2P
+                                                               : MARSIT_TRANSPORT_NCCL;
         // one NCCL communicator for all buckets (a unique id initialises one comm)
         marsit_status s = ctx_create_internal(
             &cd, drv->buckets.empty() ? nullptr : drv->buckets[0].ctx->comm, &b.ctx);
@@ -180,6 +182,20 @@ marsit_status marsit_driver_state(const marsit_driver* drv, uint64_t* next_round
     if (cum_bits) *cum_bits = drv->cum_bits;
     if (n_buckets) *n_buckets = uint32_t(drv->buckets.size());
     return MARSIT_OK;
+}
+
+marsit_status marsit_driver_p2p_buffers(const marsit_driver* drv, uint32_t bucket,
+                                        marsit_p2p_buffers* out) {
+    if (!drv) return fail(MARSIT_EPARAM, "driver is null");
+    if (bucket >= drv->buckets.size()) return fail(MARSIT_EPARAM, "bucket out of range");
+    return marsit_ctx_p2p_buffers(drv->buckets[bucket].ctx, out);
+}
+
+marsit_status marsit_driver_set_peers(marsit_driver* drv, uint32_t bucket,
+                                      const marsit_p2p_buffers* peers, uint32_t nranks) {
+    if (!drv) return fail(MARSIT_EPARAM, "driver is null");
+    if (bucket >= drv->buckets.size()) return fail(MARSIT_EPARAM, "bucket out of range");
+    return marsit_ctx_set_peers(drv->buckets[bucket].ctx, peers, nranks);
 }
 
 marsit_status marsit_driver_set_metrics(marsit_driver* drv, int enable) {

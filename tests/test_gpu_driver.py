@@ -170,3 +170,40 @@ def test_c5_bucketed_round_properties():
     assert bool((upd[pos] == eta).all()) and bool((upd[neg] == -eta).all())
     assert drv.state()["buckets"] == 4
     del x
+
+
+@pytest.mark.parametrize("G,bucket", [(2, 4000), (4, 0)])
+def test_driver_p2p_transport_matches_single_driver(G, bucket):
+    """G rank drivers with the P2P transport on one GPU (each rank's steps on
+    its own stream; the stream flag waits block until the other ranks'
+    phases ran) against one driver holding every worker: compensation and
+    replicas bit-identical over sign and dense rounds."""
+    sched = mb.build_ring_schedule(8)
+    W, D, seed, eta = 8, 10_007, 5, 2.0 ** -10
+    ml = W // G
+    kw = dict(eta_s=eta, global_seed=seed, period=3, bucket_elems=bucket, first_round=1)
+    one = mb.Driver(D, sched, **kw)
+    ranks = [mb.Driver(D, sched, nranks=G, rank=r, transport="p2p", **kw) for r in range(G)]
+    for b in range(ranks[0].state()["buckets"]):
+        table = [d.p2p_buffers(b) for d in ranks]
+        for d in ranks:
+            d.set_peers(b, table)
+    streams = [torch.cuda.Stream() for _ in range(G)]
+    x1 = [torch.zeros(D, device=DEV) for _ in range(W)]
+    xg = [torch.zeros(D, device=DEV) for _ in range(W)]
+    for t in range(1, 6):  # t = 3 dense
+        g = [torch.empty(D, device=DEV) for _ in range(W)]
+        for w in range(W):
+            mb.fill_recipe(g[w], 1, seed, w, t)
+        one.step(g, params=x1)
+        torch.cuda.synchronize()
+        for r, d in enumerate(ranks):
+            loc = slice(r * ml, (r + 1) * ml)
+            d.step(g[loc], params=xg[loc], stream=streams[r].cuda_stream)
+        torch.cuda.synchronize()
+    for r, d in enumerate(ranks):
+        for i in range(ml):
+            assert torch.equal(d.compensation(i), one.compensation(r * ml + i)), (r, i)
+    for w in range(W):
+        assert torch.equal(xg[w], x1[w])
+    assert all(d.state()["next_round"] == one.state()["next_round"] for d in ranks)
