@@ -82,7 +82,6 @@ struct MergeRunner {
     uint32_t* gnodes = nullptr;
     uint64_t* flags = nullptr;  // [kmax][seg_per_launch * part_tiles]
     uint64_t* part_totals = nullptr;
-    uint32_t epoch = 0;
     const uint32_t* const* peer_bits = nullptr;  // P2P transport: device table [G]
 
     MergeRunner() = default;
@@ -225,13 +224,6 @@ struct MergeRunner {
                 for (uint32_t part = 0; part < n_parts; ++part) {
                     c.part = part;
                     c.part_tile0 = part * part_tiles;
-                    if (++epoch == 0) {  // 2^32 launches: clear the tags once
-                        const size_t nflags = size_t(*std::max_element(k_steps.begin(), k_steps.end())) *
-                                              seg_per_launch * part_tiles;
-                        CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(uint64_t) * std::max<size_t>(nflags, 1), st));
-                        epoch = 1;
-                    }
-                    c.epoch = epoch;
                     CUDA_TRY(launch_merge_coop(c, wpt, smem, st));
                     ++*n_launch;
                 }

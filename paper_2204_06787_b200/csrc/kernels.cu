@@ -483,18 +483,12 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 80 : 128) decode_stats_kernel(const
 }
 
 // ---------------------------------------------------------------------------
-// K2: the merge DAG of every owned segment.
+// K2: the merge DAG of every owned segment (merge.hpp:34-58 per merge).
 //
-// A CTA takes a 1024-word tile (32768 coordinates) of one segment and runs
-// every merge of the current stage over it; thread t always owns words
-// 4t..4t+3 of the tile, so intermediate nodes never leave the thread (they
-// live in a shared-memory slot only because their index is dynamic).  Per
-// merge: d = r ^ l; the draw index of every disagreeing coordinate is
-//   base(stream) + exclusive_prefix(popcount(d)) over the segment,
-// obtained with a block scan plus a decoupled look-back across tiles; the
-// coin is (mix(key + (n+1)γ) >> 11) < ceil(p·2^53); out = r ^ (d & ~coin).
-// Tiles are handed out by an atomic counter in segment order, so every
-// look-back only waits on CTAs that are already running.
+// Per merge: d = r ^ l; the draw index of every disagreeing coordinate is
+//   base(stream) + exclusive_prefix(popcount(d)) over the segment;
+// the coin is (mix(key + (n+1)γ) >> 11) < ceil(p·2^53) (precomputed bit
+// streams, coins_kernel) and out = r ^ (d & ~coin).  See merge_coop_kernel.
 // ---------------------------------------------------------------------------
 // Coins of one packed word: for each set bit of `d` (ascending), draw
 // mix(z), z += gamma; keep the received bit where the draw is below th.

@@ -61,7 +61,6 @@ struct CoopParams {
     uint32_t* agg;                // [S][wst]
     const uint32_t* coins;        // precomputed coin bitstreams
     uint64_t* flags;              // [k_steps][CTAs] popcount of each tile
-    uint32_t epoch;               // launch counter (unused by the barrier version)
     uint64_t* part_totals;        // [n_parts][n_merges] draws consumed per (part, merge)
     uint64_t seed, round;
 };
