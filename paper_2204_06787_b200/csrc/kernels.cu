@@ -1021,19 +1021,30 @@ cudaError_t launch_decode(const StreamParams<T>& p, bool vec, int grid, cudaStre
 
 
 template <int WPT>
+static cudaError_t coop_attr() {  // dynamic shared memory beyond 48 KB (slots)
+    static cudaError_t e = cudaFuncSetAttribute(merge_coop_kernel<WPT>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                200 * 1024);
+    return e;
+}
+
+template <int WPT>
 static cudaError_t coop_launch_t(const CoopParams& p, size_t smem, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(merge_coop_kernel<WPT>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    cudaError_t e = coop_attr<WPT>();
+    if (e != cudaSuccess) return e;
     CoopParams q = p;
     void* args[] = {&q};
     return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(merge_coop_kernel<WPT>),
                                        dim3(p.seg_cnt * p.part_tiles), dim3(kMergeThreads), args,
                                        smem, st);
+}
+
+template <int WPT>
+static cudaError_t coop_occ_t(size_t smem, int* blocks) {
+    cudaError_t e = coop_attr<WPT>();
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<WPT>,
+                                                         kMergeThreads, smem);
 }
 
 cudaError_t launch_merge_coop(const CoopParams& p, int wpt, size_t smem, cudaStream_t st) {
@@ -1050,12 +1061,12 @@ cudaError_t launch_merge_coop(const CoopParams& p, int wpt, size_t smem, cudaStr
 
 cudaError_t merge_coop_occupancy(int wpt, size_t smem, int* blocks) {
     switch (wpt) {
-        case 1: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<1>, kMergeThreads, smem);
-        case 2: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<2>, kMergeThreads, smem);
-        case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<4>, kMergeThreads, smem);
-        case 8: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<8>, kMergeThreads, smem);
-        case 12: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<12>, kMergeThreads, smem);
-        case 16: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_coop_kernel<16>, kMergeThreads, smem);
+        case 1: return coop_occ_t<1>(smem, blocks);
+        case 2: return coop_occ_t<2>(smem, blocks);
+        case 4: return coop_occ_t<4>(smem, blocks);
+        case 8: return coop_occ_t<8>(smem, blocks);
+        case 12: return coop_occ_t<12>(smem, blocks);
+        case 16: return coop_occ_t<16>(smem, blocks);
         default: return cudaErrorInvalidValue;
     }
 }

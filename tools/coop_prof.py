@@ -24,5 +24,5 @@ def run(G, D):
     n = buf[4]
     print(f"G={G} D={D}: steps {n}  avg ns: load+scan {buf[0]/n:.0f}  grid.sync {buf[1]/n:.0f}  "
           f"prefix {buf[2]/n:.0f}  coins+deposit+store {buf[3]/n:.0f}")
-for G in (8, 2):
+for G in (8, 2, 1):
     run(G, 25_600_000)
