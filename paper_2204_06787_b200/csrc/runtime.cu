@@ -972,10 +972,12 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     {
         // persistent grid-stride streaming kernels; MARSIT_{EXTRACT,DECODE}_CTAS
         // override the CTAs per SM.  The decode leaves SM room for the next
-        // round's coin kernel running underneath it.
+        // round's coin kernel running underneath it.  Measured (CUPTI, C3):
+        // extract 247 us at 3 CTAs/SM vs 255 us at 4 and 274 us at 2
+        // (tools/sweep_stream_ctas.sh, tools/ab_extract_ctas.sh).
         int ob_extract = 0, ob_decode = 0;
         CUDA_TRY(stream_occupancy(ctx->dtype == MARSIT_F64, &ob_extract, &ob_decode));
-        const int want_e = env_int("MARSIT_EXTRACT_CTAS", 4);
+        const int want_e = env_int("MARSIT_EXTRACT_CTAS", 3);
         const int want_d = env_int("MARSIT_DECODE_CTAS", 2);
         ctx->extract_grid = std::max(1, std::min(ob_extract, want_e)) * ctx->sm_count;
         ctx->decode_grid = std::max(1, std::min(ob_decode, want_d)) * ctx->sm_count;
