@@ -923,6 +923,7 @@ __global__ void dense_leaf_kernel(const DenseParams<T> p, uint32_t s_own, uint32
             const T gg = p.src[2 * wl][jj], cc = p.src[2 * wl + 1][jj];
             u = add_rn(gg, cc);
             bad |= !(finite(gg) && finite(cc) && finite(u));
+            if (p.c_zero[wl]) p.c_zero[wl][jj] = T(0);  // after the read (c may alias)
         }
         const uint32_t q = s / s_own, sl = s % s_own;
         u_send[((uint64_t(q) * s_own + sl) * p.ml + wl) * p.seg_len + o] = u;
@@ -962,6 +963,7 @@ __global__ void __launch_bounds__(kDenseThreads) dense_reduce_kernel(const Dense
                     const T uu = add_rn(gg[k], cc[k]);  // value padding: 0 + 0
                     bad |= !(finite(gg[k]) && finite(cc[k]) && finite(uu));
                     dval[(w0 + k) * kDenseThreads + tid] = double(uu);
+                    if (in && p.c_zero[w0 + k]) p.c_zero[w0 + k][j] = T(0);  // after the read
                 }
             }
         } else if (p.mode == 1) {
@@ -986,6 +988,71 @@ __global__ void __launch_bounds__(kDenseThreads) dense_reduce_kernel(const Dense
         }
         if (j < p.dim)
             p.mean[j] = T(__dmul_rn(dval[p.final_node[sl] * kDenseThreads + tid], p.inv_m));
+    }
+    if (bad) atomicOr(p.err, 1);
+}
+
+// Ring plans: every owned segment's reduction is one linear chain,
+// v_0 = u[c_1] + u[c_0], v_k = u[c_{k+1}] + v_{k-1} (the receiver's state plus
+// the received partial, allreduce.hpp:114-116), so the leaves are loaded in
+// chain order straight into registers (static indices) — no shared-memory
+// staging — 16 loads in flight per group of 8 workers.  MODE 0: leaves
+// g + c (one GPU), with the compensation reset fused; 1: exchanged u buffer;
+// 2: peers' u buffers (P2P).
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) dense_chain_kernel(const DenseParams<T> p) {
+    const uint64_t n = uint64_t(p.n_seg) * p.seg_len;
+    bool bad = false;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t sl = uint32_t(i / p.seg_len);
+        const uint64_t o = i - uint64_t(sl) * p.seg_len;
+        const uint64_t j = uint64_t(p.s_first + sl) * p.seg_len + o;  // global coordinate
+        if (j >= p.dim) continue;  // value padding never reaches the output
+        const uint16_t* ch = p.chain + uint64_t(sl) * p.workers;
+        double acc = 0.0;
+        for (uint32_t k0 = 0; k0 < p.workers; k0 += 8) {
+            T u[8];
+            if (MODE == 0) {
+                T gg[8], cc[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const bool ok = k0 + k < p.workers;
+                    const uint32_t w = ok ? ch[k0 + k] : 0u;
+                    gg[k] = ok ? p.src[2 * w][j] : T(0);
+                    cc[k] = ok ? p.src[2 * w + 1][j] : T(0);
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    u[k] = add_rn(gg[k], cc[k]);
+                    bad |= !(finite(gg[k]) && finite(cc[k]) && finite(u[k]));
+                    if (k0 + k < p.workers) {
+                        T* z = p.c_zero[ch[k0 + k]];
+                        if (z) z[j] = T(0);  // after the read (c may alias)
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const bool ok = k0 + k < p.workers;
+                    const uint32_t w = ok ? ch[k0 + k] : 0u;
+                    const uint32_t src_rank = w / p.ml, wl = w % p.ml;
+                    if (!ok)
+                        u[k] = T(0);
+                    else if (MODE == 1)
+                        u[k] = p.u_buf[((uint64_t(src_rank) * p.n_seg + sl) * p.ml + wl) * p.seg_len + o];
+                    else
+                        u[k] = p.u_peers[src_rank][((uint64_t(p.s_first) + sl) * p.ml + wl) * p.seg_len + o];
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (k0 + k >= p.workers) break;
+                acc = (k0 + k == 0) ? double(u[k]) : __dadd_rn(double(u[k]), acc);
+                bad |= !isfinite(acc);
+            }
+        }
+        p.mean[j] = T(__dmul_rn(acc, p.inv_m));
     }
     if (bad) atomicOr(p.err, 1);
 }
@@ -1147,6 +1214,15 @@ cudaError_t launch_sub_update(T* const* x, uint32_t ml, const T* v, uint64_t dim
 
 template <typename T>
 cudaError_t launch_dense_reduce(const DenseParams<T>& p, int grid, cudaStream_t st) {
+    if (p.chain) {
+        if (p.mode == 0)
+            dense_chain_kernel<T, 0><<<grid, 256, 0, st>>>(p);
+        else if (p.mode == 1)
+            dense_chain_kernel<T, 1><<<grid, 256, 0, st>>>(p);
+        else
+            dense_chain_kernel<T, 2><<<grid, 256, 0, st>>>(p);
+        return cudaGetLastError();
+    }
     const size_t smem = size_t(p.workers + p.n_ops) * kDenseThreads * sizeof(double);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(dense_reduce_kernel<T>,
@@ -1160,11 +1236,12 @@ cudaError_t launch_dense_reduce(const DenseParams<T>& p, int grid, cudaStream_t 
 template <typename T>
 cudaError_t launch_dense_leaf(const T* const* g, const T* const* c, uint32_t ml, uint64_t dim,
                               uint64_t seg_len, uint32_t n_seg_total, uint32_t s_own, T* u_send,
-                              int* err, int grid, cudaStream_t st) {
+                              int* err, int grid, cudaStream_t st, T* const* c_zero) {
     DenseParams<T> p{};
     for (uint32_t w = 0; w < ml; ++w) {
         p.src[2 * w] = g[w];
         p.src[2 * w + 1] = c[w];
+        p.c_zero[w] = c_zero ? c_zero[w] : nullptr;
     }
     p.ml = ml;
     p.dim = dim;
@@ -1172,6 +1249,57 @@ cudaError_t launch_dense_leaf(const T* const* g, const T* const* c, uint32_t ml,
     p.err = err;
     dense_leaf_kernel<T><<<grid, 256, 0, st>>>(p, s_own, n_seg_total, u_send);
     return cudaGetLastError();
+}
+
+// Load every kernel of this library now (CUDA's default lazy loading would
+// do it at first launch, which must wait for the device to go quiet — with
+// P2P ranks whose streams wait on each other's flags inside one process, a
+// first launch after such a wait was enqueued could never return).
+cudaError_t preload_kernels() {
+    static cudaError_t result = [] {
+        const void* fns[] = {
+            reinterpret_cast<const void*>(extract_kernel<float, true>),
+            reinterpret_cast<const void*>(extract_kernel<float, false>),
+            reinterpret_cast<const void*>(extract_kernel<double, true>),
+            reinterpret_cast<const void*>(extract_kernel<double, false>),
+            reinterpret_cast<const void*>(decode_kernel<float, true>),
+            reinterpret_cast<const void*>(decode_kernel<float, false>),
+            reinterpret_cast<const void*>(decode_kernel<double, true>),
+            reinterpret_cast<const void*>(decode_kernel<double, false>),
+            reinterpret_cast<const void*>(decode_stats_kernel<float, true>),
+            reinterpret_cast<const void*>(decode_stats_kernel<float, false>),
+            reinterpret_cast<const void*>(decode_stats_kernel<double, true>),
+            reinterpret_cast<const void*>(decode_stats_kernel<double, false>),
+            reinterpret_cast<const void*>(merge_coop_kernel<1>),
+            reinterpret_cast<const void*>(merge_coop_kernel<2>),
+            reinterpret_cast<const void*>(merge_coop_kernel<4>),
+            reinterpret_cast<const void*>(merge_coop_kernel<8>),
+            reinterpret_cast<const void*>(merge_coop_kernel<12>),
+            reinterpret_cast<const void*>(merge_coop_kernel<16>),
+            reinterpret_cast<const void*>(coins_kernel),
+            reinterpret_cast<const void*>(export_bits_kernel),
+            reinterpret_cast<const void*>(flag_write_kernel),
+            reinterpret_cast<const void*>(dense_leaf_kernel<float>),
+            reinterpret_cast<const void*>(dense_leaf_kernel<double>),
+            reinterpret_cast<const void*>(dense_reduce_kernel<float>),
+            reinterpret_cast<const void*>(dense_reduce_kernel<double>),
+            reinterpret_cast<const void*>(dense_chain_kernel<float, 0>),
+            reinterpret_cast<const void*>(dense_chain_kernel<float, 1>),
+            reinterpret_cast<const void*>(dense_chain_kernel<float, 2>),
+            reinterpret_cast<const void*>(dense_chain_kernel<double, 0>),
+            reinterpret_cast<const void*>(dense_chain_kernel<double, 1>),
+            reinterpret_cast<const void*>(dense_chain_kernel<double, 2>),
+            reinterpret_cast<const void*>(sub_update_kernel<float>),
+            reinterpret_cast<const void*>(sub_update_kernel<double>),
+        };
+        cudaFuncAttributes a;
+        for (const void* f : fns) {
+            const cudaError_t e = cudaFuncGetAttributes(&a, f);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }();
+    return result;
 }
 
 #define MARSIT_INSTANTIATE(T)                                                                    \
@@ -1184,7 +1312,7 @@ cudaError_t launch_dense_leaf(const T* const* g, const T* const* c, uint32_t ml,
                                               cudaStream_t);                                    \
     template cudaError_t launch_dense_leaf<T>(const T* const*, const T* const*, uint32_t,       \
                                               uint64_t, uint64_t, uint32_t, uint32_t, T*, int*,  \
-                                              int, cudaStream_t);
+                                              int, cudaStream_t, T* const*);
 MARSIT_INSTANTIATE(float)
 MARSIT_INSTANTIATE(double)
 

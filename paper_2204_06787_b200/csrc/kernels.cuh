@@ -113,6 +113,8 @@ struct FlagSlots {
     uint32_t n;
 };
 cudaError_t launch_flag_write(const FlagSlots& s, unsigned long long value, cudaStream_t st);
+// Loads every kernel of the library (instead of lazily at first launch).
+cudaError_t preload_kernels();
 // x_w -= v for the local workers' parameter replicas (dense-round update).
 template <typename T>
 cudaError_t launch_sub_update(T* const* x, uint32_t ml, const T* v, uint64_t dim, int grid,
@@ -133,6 +135,10 @@ struct DenseParams {
     uint32_t mode;                       // 0: leaf w = g[w] + c[w]; 1: leaf w = u buffer
     const T* u_buf;                      // mode 1: [G][s_own][ml][L] u values
     const T* const* u_peers;             // mode 2 (P2P): rank q's own [S][ml][L] u buffer
+    const uint16_t* chain;               // ring plans: [n_seg][workers] leaf order of the
+                                         // linear reduction chain (null: general DAG)
+    T* c_zero[kMaxLocalWorkers];         // compensation reset c' = 0 fused into the pass
+                                         // that reads g, c (sync.hpp:83-85); may alias c
     const DenseOp* ops;                  // [n_seg][n_ops]
     const uint16_t* final_node;          // [n_seg]
     uint32_t n_ops, n_seg, s_first, ml, workers;
@@ -146,6 +152,7 @@ cudaError_t launch_dense_reduce(const DenseParams<T>& p, int grid, cudaStream_t 
 template <typename T>
 cudaError_t launch_dense_leaf(const T* const* g, const T* const* c, uint32_t ml, uint64_t dim,
                               uint64_t seg_len, uint32_t n_seg_total, uint32_t s_own,
-                              T* u_send, int* err, int grid, cudaStream_t st);
+                              T* u_send, int* err, int grid, cudaStream_t st,
+                              T* const* c_zero = nullptr);
 
 }  // namespace marsit_b200

@@ -137,6 +137,7 @@ marsit_ctx::~marsit_ctx() {
     if (device >= 0) cudaSetDevice(device);
     for (void* p : {(void*)bits, (void*)recv, (void*)agg, (void*)err, dense_send, dense_recv,
                     dense_mean, (void*)d_dense_ops, (void*)d_dense_final, (void*)d_metrics,
+                    (void*)d_dense_chain,
                     (void*)flags, (void*)d_peer_tables})
         if (p) cudaFree(p);
     for (auto& tp : pending) {
@@ -476,6 +477,7 @@ marsit_status dense_phase(marsit_ctx* ctx, int phase, const void* const* g, cons
     marsit_status s = ctx->begin_phase(st, &ev);
     if (s) return s;
     DenseParams<T> p{};
+    p.chain = ctx->d_dense_chain;
     p.ops = ctx->d_dense_ops;
     p.final_node = ctx->d_dense_final;
     p.n_ops = ctx->dense_n_ops;
@@ -493,13 +495,15 @@ marsit_status dense_phase(marsit_ctx* ctx, int phase, const void* const* g, cons
     if (phase == 2 && (s = p2p_wait(ctx, 1, st))) return s;
     if (phase == 0 && ctx->G > 1) {
         std::vector<const T*> gg(ctx->ml), cc(ctx->ml);
+        std::vector<T*> zz(ctx->ml);
         for (uint32_t w = 0; w < ctx->ml; ++w) {
             gg[w] = static_cast<const T*>(g[w]);
             cc[w] = static_cast<const T*>(c[w]);
+            zz[w] = static_cast<T*>(c_out[w]);  // c' = 0 (sync.hpp:83-85), fused
         }
         CUDA_TRY(launch_dense_leaf<T>(gg.data(), cc.data(), ctx->ml, ctx->D, ctx->L, ctx->S,
                                       ctx->s_own, static_cast<T*>(ctx->dense_send), ctx->err,
-                                      ctx->stream_grid, st));
+                                      ctx->stream_grid, st, zz.data()));
         ++launches;
     } else if (phase == 1) {
         if (ctx->G == 1) {
@@ -507,6 +511,7 @@ marsit_status dense_phase(marsit_ctx* ctx, int phase, const void* const* g, cons
             for (uint32_t w = 0; w < ctx->ml; ++w) {
                 p.src[2 * w] = static_cast<const T*>(g[w]);
                 p.src[2 * w + 1] = static_cast<const T*>(c[w]);
+                p.c_zero[w] = static_cast<T*>(c_out[w]);  // c' = 0 (sync.hpp:83-85), fused
             }
             p.mean = static_cast<T*>(mean);
         } else {
@@ -533,8 +538,6 @@ marsit_status dense_phase(marsit_ctx* ctx, int phase, const void* const* g, cons
             CUDA_TRY(cudaMemcpyAsync(mean, ctx->dense_mean, ctx->D * sizeof(T),
                                      cudaMemcpyDeviceToDevice, st));
         }
-        for (uint32_t w = 0; w < ctx->ml; ++w)
-            CUDA_TRY(cudaMemsetAsync(c_out[w], 0, ctx->D * sizeof(T), st));  // sync.hpp:83-85
         if (params) {  // x_w -= mean (trainer.hpp:285-288)
             std::vector<T*> xs(ctx->ml);
             for (uint32_t w = 0; w < ctx->ml; ++w) xs[w] = static_cast<T*>(params[w]);
@@ -881,6 +884,7 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     auto ctx = std::make_unique<marsit_ctx>();
     ctx->device = desc->device;
     CUDA_TRY(cudaSetDevice(desc->device));
+    CUDA_TRY(preload_kernels());
     CUDA_TRY(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, desc->device));
     ctx->dtype = desc->dtype;
     ctx->esize = desc->dtype == MARSIT_F32 ? 4 : 8;
@@ -1007,6 +1011,24 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
             fin[sl] = uint16_t(sp.final_node);
         }
         ctx->dense_n_ops = n_ops;
+        // linear chains (ring): v_0 = leaf a_0 + leaf b_0, v_k = leaf a_k + v_{k-1}
+        bool chain = n_ops + 1 == ctx->M && env_int("MARSIT_DENSE_DAG", 0) == 0;
+        std::vector<uint16_t> order(size_t(ctx->s_own) * ctx->M);
+        for (uint32_t sl = 0; sl < ctx->s_own && chain; ++sl) {
+            const DenseOp* o = &ops[size_t(sl) * n_ops];
+            chain = o[0].a < ctx->M && o[0].b < ctx->M && fin[sl] == ctx->M + n_ops - 1;
+            order[size_t(sl) * ctx->M] = o[0].b;
+            order[size_t(sl) * ctx->M + 1] = o[0].a;
+            for (uint32_t k = 1; k < n_ops && chain; ++k) {
+                chain = o[k].a < ctx->M && o[k].b == ctx->M + k - 1;
+                order[size_t(sl) * ctx->M + k + 1] = o[k].a;
+            }
+        }
+        if (chain && n_ops > 0) {
+            CUDA_TRY(cudaMalloc(&ctx->d_dense_chain, sizeof(uint16_t) * order.size()));
+            CUDA_TRY(cudaMemcpy(ctx->d_dense_chain, order.data(), sizeof(uint16_t) * order.size(),
+                                cudaMemcpyHostToDevice));
+        }
         CUDA_TRY(cudaMalloc(&ctx->d_dense_ops, sizeof(DenseOp) * ops.size()));
         CUDA_TRY(cudaMemcpy(ctx->d_dense_ops, ops.data(), sizeof(DenseOp) * ops.size(),
                             cudaMemcpyHostToDevice));
