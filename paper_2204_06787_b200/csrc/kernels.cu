@@ -1057,6 +1057,58 @@ __global__ void __launch_bounds__(256) dense_chain_kernel(const DenseParams<T> p
     if (bad) atomicOr(p.err, 1);
 }
 
+// dense_chain_kernel, one-GPU leaves, 4 consecutive coordinates per thread
+// (16-byte loads; needs L and D multiples of 4 and aligned g, c, c', mean).
+template <typename T>
+__global__ void __launch_bounds__(256) dense_chain4_kernel(const DenseParams<T> p) {
+    const uint64_t n4 = uint64_t(p.n_seg) * p.seg_len / 4;
+    bool bad = false;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n4;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i0 = i * 4;
+        const uint32_t sl = uint32_t(i0 / p.seg_len);
+        const uint64_t o = i0 - uint64_t(sl) * p.seg_len;
+        const uint64_t j = uint64_t(p.s_first + sl) * p.seg_len + o;
+        if (j >= p.dim) continue;
+        const uint16_t* ch = p.chain + uint64_t(sl) * p.workers;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (uint32_t k0 = 0; k0 < p.workers; k0 += 8) {
+            Quad<T> gq[8], cq[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (k0 + k < p.workers) {
+                    const uint32_t w = ch[k0 + k];
+                    gq[k] = load4(p.src[2 * w] + j);
+                    cq[k] = load4_rw(p.src[2 * w + 1] + j);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) gq[k].v[e] = cq[k].v[e] = T(0);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (k0 + k >= p.workers) break;
+                Quad<T> zero;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const T u = add_rn(gq[k].v[e], cq[k].v[e]);
+                    bad |= !(finite(gq[k].v[e]) && finite(cq[k].v[e]) && finite(u));
+                    acc[e] = (k0 + k == 0) ? double(u) : __dadd_rn(double(u), acc[e]);
+                    bad |= !isfinite(acc[e]);
+                    zero.v[e] = T(0);
+                }
+                T* z = p.c_zero[ch[k0 + k]];
+                if (z) store4(z + j, zero);  // after the read (c may alias)
+            }
+        }
+        Quad<T> m;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) m.v[e] = T(__dmul_rn(acc[e], p.inv_m));
+        store4(p.mean + j, m);
+    }
+    if (bad) atomicOr(p.err, 1);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -1215,7 +1267,9 @@ cudaError_t launch_sub_update(T* const* x, uint32_t ml, const T* v, uint64_t dim
 template <typename T>
 cudaError_t launch_dense_reduce(const DenseParams<T>& p, int grid, cudaStream_t st) {
     if (p.chain) {
-        if (p.mode == 0)
+        if (p.mode == 0 && p.vec4)
+            dense_chain4_kernel<T><<<grid, 256, 0, st>>>(p);
+        else if (p.mode == 0)
             dense_chain_kernel<T, 0><<<grid, 256, 0, st>>>(p);
         else if (p.mode == 1)
             dense_chain_kernel<T, 1><<<grid, 256, 0, st>>>(p);
@@ -1289,6 +1343,8 @@ cudaError_t preload_kernels() {
             reinterpret_cast<const void*>(dense_chain_kernel<double, 0>),
             reinterpret_cast<const void*>(dense_chain_kernel<double, 1>),
             reinterpret_cast<const void*>(dense_chain_kernel<double, 2>),
+            reinterpret_cast<const void*>(dense_chain4_kernel<float>),
+            reinterpret_cast<const void*>(dense_chain4_kernel<double>),
             reinterpret_cast<const void*>(sub_update_kernel<float>),
             reinterpret_cast<const void*>(sub_update_kernel<double>),
         };

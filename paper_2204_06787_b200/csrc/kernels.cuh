@@ -135,6 +135,7 @@ struct DenseParams {
     uint32_t mode;                       // 0: leaf w = g[w] + c[w]; 1: leaf w = u buffer
     const T* u_buf;                      // mode 1: [G][s_own][ml][L] u values
     const T* const* u_peers;             // mode 2 (P2P): rank q's own [S][ml][L] u buffer
+    bool vec4;                           // mode 0 chain: 16-byte aligned quads throughout
     const uint16_t* chain;               // ring plans: [n_seg][workers] leaf order of the
                                          // linear reduction chain (null: general DAG)
     T* c_zero[kMaxLocalWorkers];         // compensation reset c' = 0 fused into the pass

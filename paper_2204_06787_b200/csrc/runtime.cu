@@ -514,6 +514,8 @@ marsit_status dense_phase(marsit_ctx* ctx, int phase, const void* const* g, cons
                 p.c_zero[w] = static_cast<T*>(c_out[w]);  // c' = 0 (sync.hpp:83-85), fused
             }
             p.mean = static_cast<T*>(mean);
+            p.vec4 = ctx->L % 4 == 0 && ctx->D % 4 == 0 && aligned16(mean) &&
+                     vec_ok_ptrs(ctx, g, c) && vec_ok_ptrs(ctx, (const void* const*)c_out, c);
         } else {
             p.mode = ctx->p2p ? 2 : 1;
             p.u_buf = static_cast<const T*>(ctx->dense_recv);

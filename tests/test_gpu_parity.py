@@ -357,3 +357,30 @@ def test_merge_tilings_bit_exact(wpt, topo, a, b, D, monkeypatch):
         assert u64(agg).tolist() == r.agg_bits.tolist(), (wpt, topo, t)
         comp_o = r.comp
     ctx.check()
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("M,D", [(8, 8192), (4, 1_000_000), (8, 8196)])
+def test_dense_round_vector_path_vs_oracle(dtype, M, D):
+    """Dense rounds on ring plans whose L and D are multiples of 4 take the
+    16-byte chain kernel (and a ragged D the scalar one): exact vs the oracle,
+    compensation reset to 0."""
+    sched = mb.build_ring_schedule(M)
+    T = O.schedule("ring", M)
+    rng = np.random.default_rng(D + M)
+    if dtype == torch.float64:
+        g = rng.standard_normal((M, D))
+    else:
+        g = np.stack([O.gen_dyadic(3, w, 1, D) for w in range(M)])
+    comp_o = rng.standard_normal((M, D)) * 1e-3 if dtype == torch.float64 else np.zeros((M, D))
+    r = O.marsit_round(T, 2, 2, ETA, g, comp_o, 5)
+    assert r.status == 0 and r.full_precision
+    ctx = mb.Context(D, sched, dtype, 0)
+    comp = [torch.tensor(x, dtype=dtype, device=DEV) for x in comp_o]
+    mean = torch.empty(D, dtype=dtype, device=DEV)
+    ctx.dense_round(2, [torch.tensor(x, dtype=dtype, device=DEV) for x in g], comp, mean)
+    torch.cuda.synchronize()
+    want = r.update if dtype == torch.float64 else r.update.astype(np.float32).astype(np.float64)
+    assert np.array_equal(mean.double().cpu().numpy(), want)
+    assert all(bool((c == 0).all()) for c in comp)
+    ctx.check()
