@@ -19,7 +19,10 @@
 // grids sized to the SM count; the merge kernel keeps every segment in L2.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <mutex>
+#include <vector>
 
 #include "kernels.cuh"
 #include "rng.cuh"
@@ -1310,7 +1313,15 @@ cudaError_t launch_dense_leaf(const T* const* g, const T* const* c, uint32_t ml,
 // P2P ranks whose streams wait on each other's flags inside one process, a
 // first launch after such a wait was enqueued could never return).
 cudaError_t preload_kernels() {
-    static cudaError_t result = [] {
+    // modules load per device: once for every device this process uses
+    static std::mutex mu;
+    static std::vector<int> done;
+    int dev = 0;
+    cudaError_t e0 = cudaGetDevice(&dev);
+    if (e0 != cudaSuccess) return e0;
+    std::lock_guard<std::mutex> lock(mu);
+    if (std::find(done.begin(), done.end(), dev) != done.end()) return cudaSuccess;
+    const cudaError_t result = [] {
         const void* fns[] = {
             reinterpret_cast<const void*>(extract_kernel<float, true>),
             reinterpret_cast<const void*>(extract_kernel<float, false>),
@@ -1355,6 +1366,7 @@ cudaError_t preload_kernels() {
         }
         return cudaSuccess;
     }();
+    if (result == cudaSuccess) done.push_back(dev);
     return result;
 }
 
