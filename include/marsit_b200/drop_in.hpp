@@ -5,7 +5,9 @@
 //     marsit::marsit_round(t, cfg, grads, comp, sched, seed)        // sync.hpp:60-63
 //     marsit::allreduce_sign(signs, sched, RoundContext{seed, t})   // allreduce.hpp:148-149
 // to marsit::gpu::marsit_round / marsit::gpu::allreduce_sign with the SAME
-// arguments and result types.  This header includes the reference's own
+// arguments and result types; likewise allreduce_dense (allreduce.hpp:98-130)
+// and the SSDM baselines cascading_allreduce / sum_ssdm_allreduce
+// (allreduce.hpp:205-339).  This header includes the reference's own
 // headers for those types (marsit/sync.hpp), so it compiles inside the
 // reference tree with -I<b200 repo>/include and links against
 // libmarsit_b200.so and libcudart.
@@ -22,6 +24,7 @@
 
 #include <marsit/allreduce.hpp>
 #include <marsit/schedule.hpp>
+#include <marsit/ssdm.hpp>
 #include <marsit/sync.hpp>
 
 #include <cuda_runtime.h>
@@ -234,6 +237,103 @@ inline SignAllreduceResult allreduce_sign(const std::vector<std::vector<PackedSi
                             detail::bits_account(ctx, W, false)};
     // BitsAccount of allreduce_sign counts L bits per send (allreduce.hpp:182)
     return out;
+}
+
+namespace detail {
+
+inline void check_vectors(const std::vector<DenseVector>& v, const Schedule& sched) {
+    // allreduce.hpp:75-84
+    if (v.size() != sched.workers) throw parameter_error("allreduce: vector count != schedule workers");
+    for (const DenseVector& x : v)
+        if (x.size() != v[0].size()) throw parameter_error("allreduce: inconsistent dimensions");
+}
+
+// Upload M host vectors into one device buffer; returns the per-worker pointers.
+inline std::vector<const void*> upload(const std::vector<DenseVector>& v, DeviceBuffer& buf) {
+    const size_t bytes = v[0].size() * sizeof(double);
+    std::vector<const void*> ptrs(v.size());
+    for (size_t w = 0; w < v.size(); ++w) {
+        char* d = static_cast<char*>(buf.p) + w * bytes;
+        cuda_check(cudaMemcpy(d, v[w].values().data(), bytes, cudaMemcpyHostToDevice), "H2D");
+        ptrs[w] = d;
+    }
+    return ptrs;
+}
+
+inline DenseVector download(const void* d, size_t n) {
+    std::vector<double> h(n);
+    cuda_check(cudaMemcpy(h.data(), d, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    return DenseVector(std::move(h));
+}
+
+}  // namespace detail
+
+// allreduce.hpp:98-130, same signature and result: the schedule-order sum
+// scaled by 1/M at every worker.  Runs as a dense round whose compensation is
+// -0.0 (x + -0.0 == x bit for bit, including x = -0.0).
+inline DenseAllreduceResult allreduce_dense(const std::vector<DenseVector>& vectors,
+                                            const Schedule& sched) {
+    detail::check_vectors(vectors, sched);
+    const size_t dim = vectors[0].size();
+    const uint32_t W = sched.workers;
+    marsit_ctx* ctx = detail::context_for(dim, sched);
+    const size_t bytes = dim * sizeof(double);
+    detail::DeviceBuffer dv(W * bytes), dz(bytes), dscr(W * bytes), dmean(bytes);
+    std::vector<const void*> vp = detail::upload(vectors, dv);
+    std::vector<double> negzero(dim, -0.0);
+    detail::cuda_check(cudaMemcpy(dz.p, negzero.data(), bytes, cudaMemcpyHostToDevice), "H2D");
+    std::vector<const void*> zp(W, dz.p);
+    std::vector<void*> sp(W);
+    for (uint32_t w = 0; w < W; ++w) sp[w] = static_cast<char*>(dscr.p) + w * bytes;
+    detail::check(marsit_dense_round(ctx, 0, vp.data(), zp.data(), sp.data(), dmean.p, nullptr));
+    detail::check(marsit_ctx_check(ctx, nullptr));
+    DenseVector mean = detail::download(dmean.p, dim);
+    return DenseAllreduceResult{std::vector<DenseVector>(W, mean), detail::bits_account(ctx, W, true)};
+}
+
+namespace detail {
+inline std::pair<DenseVector, BitsAccount> ssdm(int mode, const std::vector<DenseVector>& vectors,
+                                                const Schedule& sched, const RoundContext& rc,
+                                                std::vector<std::int64_t>* max_abs) {
+    if (sched.topology != Topology::ring)
+        throw unsupported_error(mode == MARSIT_SSDM_CASCADING
+                                    ? "cascading_allreduce: only ring schedules are supported"
+                                    : "sum_ssdm_allreduce: only ring schedules are supported");
+    check_vectors(vectors, sched);
+    const size_t dim = vectors[0].size();
+    const uint32_t W = sched.workers;
+    marsit_ctx* ctx = context_for(dim, sched);
+    DeviceBuffer dv(W * dim * sizeof(double)), dout(dim * sizeof(double));
+    std::vector<const void*> vp = upload(vectors, dv);
+    BitsAccount bits(W);
+    std::vector<std::int64_t> mx(sched.steps.size() + 1);
+    check(marsit_ssdm_allreduce(ctx, mode, rc.round, rc.global_seed, vp.data(), dout.p,
+                                bits.per_worker.data(), &bits.reduce_bits, &bits.gather_bits,
+                                mx.data(), nullptr));
+    check(marsit_ctx_check(ctx, nullptr));
+    bits.total = bits.reduce_bits + bits.gather_bits;
+    if (max_abs) *max_abs = std::vector<std::int64_t>(mx.begin(), mx.begin() + sched.steps.size());
+    return {download(dout.p, dim), std::move(bits)};
+}
+}  // namespace detail
+
+// allreduce.hpp:205-262, same signature and result.  The l2 norms are summed
+// in a fixed parallel order: bit-identical whenever the reference's
+// sequential sums are exact, within its own rounding otherwise.
+inline CascadingAllreduceResult cascading_allreduce(const std::vector<DenseVector>& vectors,
+                                                    const Schedule& sched, const RoundContext& rc) {
+    auto r = detail::ssdm(MARSIT_SSDM_CASCADING, vectors, sched, rc, nullptr);
+    return CascadingAllreduceResult{std::vector<DenseVector>(sched.workers, r.first),
+                                    std::move(r.second)};
+}
+
+// allreduce.hpp:275-339, same signature and result.
+inline SumSsdmAllreduceResult sum_ssdm_allreduce(const std::vector<DenseVector>& vectors,
+                                                 const Schedule& sched, const RoundContext& rc) {
+    std::vector<std::int64_t> mx;
+    auto r = detail::ssdm(MARSIT_SSDM_SUM, vectors, sched, rc, &mx);
+    return SumSsdmAllreduceResult{std::vector<DenseVector>(sched.workers, r.first),
+                                  std::move(r.second), std::move(mx)};
 }
 
 }  // namespace marsit::gpu

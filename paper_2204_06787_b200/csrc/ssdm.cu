@@ -452,7 +452,9 @@ marsit_status ssdm_allreduce_impl(marsit_ctx* ctx, int mode, uint64_t round, uin
         return fail(MARSIT_EPARAM, "ssdm mode must be cascading (0) or sum (1)");
     if (!d_vectors || !d_estimate) return fail(MARSIT_EPARAM, "null argument");
     const HostSchedule& hs = ctx->sched;
-    if (hs.topology != 0)
+    // ring schedules (built, or explicit tables whose reduce phase is one
+    // linear chain per segment — checked below); torus: as the reference
+    if (hs.topology == 1)
         return fail(MARSIT_EUNSUPPORTED, mode == MARSIT_SSDM_CASCADING
                                              ? "cascading_allreduce: only ring schedules are supported"
                                              : "sum_ssdm_allreduce: only ring schedules are supported");

@@ -12,6 +12,7 @@
 
 #include <marsit_b200/drop_in.hpp>
 
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -96,8 +97,63 @@ static void run_allreduce(const char* tag, const Schedule& sched, size_t L) {
     std::printf("allreduce %-23s L=%zu %s\n", tag, L, failures ? "" : "ok");
 }
 
+static void run_dense(const char* tag, const Schedule& sched, size_t D, int kind) {
+    auto v = inputs(sched.workers, D, 5, 1, kind);
+    DenseAllreduceResult a = marsit::allreduce_dense(v, sched);
+    DenseAllreduceResult b = marsit::gpu::allreduce_dense(v, sched);
+    for (uint32_t w = 0; w < sched.workers; ++w) expect(same(a.per_worker[w], b.per_worker[w]), "mean", tag);
+    expect(a.bits.per_worker == b.bits.per_worker && a.bits.total == b.bits.total, "dense bits", tag);
+    std::printf("dense %-27s D=%zu %s\n", tag, D, failures ? "" : "ok");
+}
+
+// SSDM: bits exact; values exact for dyadic inputs in the sum variant (every
+// norm is a first compression of exact data), else within 1e-9 relative.
+static void run_ssdm(const char* tag, const Schedule& sched, size_t D, int kind) {
+    auto v = inputs(sched.workers, D, 9, 2, kind);
+    RoundContext rc{2026, 3};
+    for (int mode = 0; mode < 2; ++mode) {
+        std::vector<DenseVector> ea, eb;
+        BitsAccount ba(sched.workers), bb(sched.workers);
+        if (mode == 0) {
+            auto a = marsit::cascading_allreduce(v, sched, rc);
+            auto b = marsit::gpu::cascading_allreduce(v, sched, rc);
+            ea = a.per_worker; eb = b.per_worker; ba = a.bits; bb = b.bits;
+        } else {
+            auto a = marsit::sum_ssdm_allreduce(v, sched, rc);
+            auto b = marsit::gpu::sum_ssdm_allreduce(v, sched, rc);
+            ea = a.per_worker; eb = b.per_worker; ba = a.bits; bb = b.bits;
+            expect(a.max_abs_per_step == b.max_abs_per_step, "max_abs_per_step", tag);
+        }
+        bool ok = true;
+        for (size_t j = 0; j < D; ++j) {
+            const double x = ea[0][j], y = eb[0][j];
+            if (mode == 1 && kind == 0) ok &= std::memcmp(&x, &y, 8) == 0;
+            else ok &= std::signbit(x) == std::signbit(y) && std::fabs(x - y) <= 1e-9 * std::fabs(x);
+        }
+        expect(ok, mode ? "sum-ssdm estimate" : "cascading estimate", tag);
+        expect(ba.per_worker == bb.per_worker && ba.reduce_bits == bb.reduce_bits &&
+                   ba.gather_bits == bb.gather_bits, "ssdm bits", tag);
+    }
+    std::printf("ssdm %-28s D=%zu %s\n", tag, D, failures ? "" : "ok");
+}
+
 int main() {
     try {
+        run_dense("ring4 gaussian", build_ring_schedule(4), 1001, 1);
+        run_dense("torus2x4 zeros", build_torus_schedule(2, 4), 777, 2);
+        run_dense("ring8 dyadic", build_ring_schedule(8), 8192, 0);
+        run_ssdm("ring4 dyadic", build_ring_schedule(4), 4096, 0);
+        run_ssdm("ring5 gaussian", build_ring_schedule(5), 333, 1);
+        {  // torus: unsupported_error like the reference
+            bool threw = false;
+            try {
+                marsit::gpu::cascading_allreduce(inputs(4, 10, 1, 1, 1), build_torus_schedule(2, 2),
+                                                 RoundContext{1, 1});
+            } catch (const unsupported_error&) {
+                threw = true;
+            }
+            expect(threw, "unsupported_error for torus SSDM", "errors");
+        }
         run_case("ring5 dyadic", build_ring_schedule(5), 37, std::nullopt, 0, 4);
         run_case("ring4 C1 dyadic", build_ring_schedule(4), 1000000, std::nullopt, 0, 2);
         run_case("ring8 gaussian", build_ring_schedule(8), 100003, std::nullopt, 1, 3);
