@@ -250,17 +250,23 @@ __global__ void __launch_bounds__(kSsThreads) ssdm_compress_kernel(const SsdmPar
     const uint32_t warp = blockIdx.x * (kSsThreads / 32) + (threadIdx.x >> 5);
     uint32_t* out = p.pk + uint64_t(item) * p.wst;
     const uint32_t q_end = min(p.wst, (warp + 1) * kSsWordsPerWarp);
+    // this item's values: coordinates [0, valid) of the segment are real,
+    // [valid, L) value padding (0)
+    const uint64_t seg0 = uint64_t(s) * p.L;
+    const uint64_t valid = CASCADE ? p.L : (p.D > seg0 ? min(p.L, p.D - seg0) : 0);
+    const double* accs = p.acc + seg0;
+    const SRC* raw = static_cast<const SRC*>(p.vec[w]) + seg0;
     for (uint32_t q0 = warp * kSsWordsPerWarp; q0 < q_end; q0 += 8) {
         double v[8];
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
             const uint64_t j = uint64_t(q0 + b) * 32 + lane;
-            if (j >= p.L)
+            if (j >= valid)
                 v[b] = 0.0;
             else if (CASCADE)
-                v[b] = p.acc[uint64_t(s) * p.L + j];
+                v[b] = accs[j];
             else
-                v[b] = raw_at<SRC>(p, w, s, j);
+                v[b] = double(raw[j]);
         }
         uint64_t z = key + (uint64_t(q0) * 32 + lane + 1) * kGamma;  // draw j = 32 q + lane
 #pragma unroll
@@ -303,32 +309,39 @@ __global__ void ssdm_out_cascade_kernel(const SsdmParams p, T* __restrict__ out)
 // Sum variant estimate: mean of the M decompressed packets, summed in worker
 // order from 0.0, times 1/M (allreduce.hpp:322-336).  A warp per packed word
 // (lanes = coordinates); the packet words of 8 workers are loaded at once.
+// +-norm is the norm with its sign bit set from the packet bit; a zero norm
+// then contributes +-0.0 instead of +0.0, which leaves the sum unchanged (it
+// starts at +0.0, and x + -0.0 == x for every x but -0.0).
 template <typename T>
 __global__ void ssdm_out_sum_kernel(const SsdmParams p, T* __restrict__ out) {
-    __shared__ double s_norm[kSsMaxWorkers];
+    __shared__ unsigned long long s_norm[kSsMaxWorkers];  // bit patterns
     const double inv_m = 1.0 / double(p.M);
     const uint32_t s = blockIdx.y;
-    for (uint32_t w = threadIdx.x; w < p.M; w += blockDim.x) s_norm[w] = p.norms[w * p.S + s];
+    for (uint32_t w = threadIdx.x; w < p.M; w += blockDim.x)
+        s_norm[w] = __double_as_longlong(p.norms[w * p.S + s]);
     __syncthreads();
     const uint64_t wps = ceil_div_d(p.L, 32);
+    const uint64_t stride = uint64_t(p.S) * p.wst;  // worker w's row of segment s
     const int lane = threadIdx.x & 31;
     const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x / 32);
+    const uint64_t seg0 = uint64_t(s) * p.L;
+    const uint64_t valid = p.D > seg0 ? min(p.L, p.D - seg0) : 0;
     for (uint64_t q = blockIdx.x * uint64_t(blockDim.x / 32) + (threadIdx.x >> 5); q < wps; q += warps) {
-        const uint64_t j = q * 32 + lane, gi = uint64_t(s) * p.L + j;
+        const uint64_t j = q * 32 + lane;
+        const uint32_t* row = p.pk + uint64_t(s) * p.wst + q;
         double a = 0.0;
         for (uint32_t w0 = 0; w0 < p.M; w0 += 8) {
             uint32_t word[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-                word[i] = w0 + i < p.M ? __ldg(p.pk + (uint64_t(w0 + i) * p.S + s) * p.wst + q) : 0u;
+            for (int i = 0; i < 8; ++i) word[i] = w0 + i < p.M ? __ldg(row + (w0 + i) * stride) : 0u;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 if (w0 + i >= p.M) break;
-                const double nrm = s_norm[w0 + i];
-                a = __dadd_rn(a, nrm == 0.0 ? 0.0 : (((word[i] >> lane) & 1u) ? nrm : -nrm));
+                const unsigned long long neg = uint64_t(((word[i] >> lane) & 1u) ^ 1u) << 63;
+                a = __dadd_rn(a, __longlong_as_double(s_norm[w0 + i] | neg));
             }
         }
-        if (j < p.L && gi < p.D) out[gi] = T(__dmul_rn(a, inv_m));
+        if (j < valid) out[seg0 + j] = T(__dmul_rn(a, inv_m));
     }
 }
 
