@@ -159,7 +159,7 @@ __device__ __forceinline__ uint32_t sign_nibble(T a, T b, T c, T d) {
 // (segmentation.hpp:45-49 + sign_vector.hpp:70).
 // ---------------------------------------------------------------------------
 template <typename T, bool VEC>
-__global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 4 : 2) extract_kernel(const StreamParams<T> p) {
+__global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? (VEC ? 4 : 3) : 2) extract_kernel(const StreamParams<T> p) {
     const int lane = threadIdx.x & 31;
     const uint32_t warps = gridDim.x * (kStreamThreads / 32);
     const uint32_t tasks_per_seg = (p.words_proc + kTaskWords - 1) / kTaskWords;
@@ -225,22 +225,23 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 4 : 2) extrac
                     p.bits[(uint64_t(s) * p.ml + wl) * p.wst + wi] = v;
             }
         } else {
-#pragma unroll 4
+            // any segment length: lane-contiguous (coalesced) loads, all 32 of a
+            // lane issued before the first is used
+            T gv[kTaskWords], cv[kTaskWords];
+#pragma unroll
             for (int t = 0; t < kTaskWords; ++t) {
                 const uint64_t j = j0 + t * 32 + lane;
                 const uint64_t gi = seg0 + j;
-                bool bit = false;
-                if (j < p.seg_len) {
-                    if (gi < p.dim) {
-                        const T gg = g[gi], cc = c[gi];
-                        const T u = add_rn(gg, cc);
-                        bad |= !(finite(gg) && finite(cc) && finite(u));
-                        bit = u >= T(0);
-                    } else {
-                        bit = true;  // value padding 0.0 packs to 1
-                    }
-                }
-                const uint32_t w = __ballot_sync(kFull, bit);
+                const bool in = j < p.seg_len && gi < p.dim;
+                gv[t] = in ? g[gi] : T(0);  // value padding 0.0 (+ 0.0) packs to 1
+                cv[t] = in ? c[gi] : T(0);
+            }
+#pragma unroll
+            for (int t = 0; t < kTaskWords; ++t) {
+                const uint64_t j = j0 + t * 32 + lane;
+                const T u = add_rn(gv[t], cv[t]);
+                bad |= !(finite(gv[t]) && finite(cv[t]) && finite(u));
+                const uint32_t w = __ballot_sync(kFull, j < p.seg_len && u >= T(0));
                 if (lane == t) word = w;
             }
         }
@@ -340,14 +341,26 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode
                 }
             }
         } else {
-#pragma unroll 4
+            // any segment length: lane-contiguous (coalesced) loads, all issued
+            // before the first is used
+            T gv[kTaskWords], cv[kTaskWords];
+            uint32_t wv[kTaskWords];
+#pragma unroll
+            for (int t = 0; t < kTaskWords; ++t) {
+                const uint64_t j = j0 + t * 32 + lane;
+                const uint64_t gi = seg0 + j;
+                const bool in = j < p.seg_len && gi < p.dim;
+                gv[t] = in ? g[gi] : T(0);
+                cv[t] = in ? c[gi] : T(0);
+                wv[t] = in ? __ldg(aw + t) : 0u;
+            }
+#pragma unroll
             for (int t = 0; t < kTaskWords; ++t) {
                 const uint64_t j = j0 + t * 32 + lane;
                 const uint64_t gi = seg0 + j;
                 if (j < p.seg_len && gi < p.dim) {
-                    const uint32_t word = __ldg(aw + t);
-                    const T gt = ((word >> lane) & 1u) ? eta : -eta;
-                    co[gi] = sub_rn(add_rn(g[gi], c[gi]), gt);
+                    const T gt = ((wv[t] >> lane) & 1u) ? eta : -eta;
+                    co[gi] = sub_rn(add_rn(gv[t], cv[t]), gt);
                     if (upd) upd[gi] = gt;
                     if (xp) xp[gi] = sub_rn(xp[gi], gt);
                 }

@@ -905,6 +905,8 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     ctx->words64 = uint32_t(ceil_div(ctx->L, 64));
     ctx->words_proc = uint32_t(round_up(2ull * ctx->words64, 4));
     ctx->wst = uint32_t(round_up(ctx->words_proc, 32));
+    // vector kernels: every segment's quads 16 B-aligned (L % 4 == 0); other
+    // lengths take the coalesced scalar kernels (all loads issued first)
     ctx->vec_ok = (ctx->L % 4) == 0;
 
     // merge plan, coin budget, tiling
