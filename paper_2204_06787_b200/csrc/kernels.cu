@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? (VEC ? 4 : 3)
             for (int t = 0; t < kTaskWords; ++t) {
                 const uint64_t j = j0 + t * 32 + lane;
                 const T u = add_rn(gv[t], cv[t]);
-                bad |= !(finite(gv[t]) && finite(cv[t]) && finite(u));
+                fin = fma_rn(u, T(0), fin);  // NaN iff some u is inf/NaN (any non-finite g or c)
                 const uint32_t w = __ballot_sync(kFull, j < p.seg_len && u >= T(0));
                 if (lane == t) word = w;
             }
