@@ -227,21 +227,25 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? (VEC ? 4 : 3)
         } else {
             // any segment length: lane-contiguous (coalesced) loads, all 32 of a
             // lane issued before the first is used
+            // element t of this lane is coordinate j0 + 32 t + lane: real below
+            // n_real, value padding (0.0, packs to 1) below n_seg, storage padding above
+            const uint64_t first = j0 + lane;
+            const uint64_t lim = p.dim > seg0 ? (p.dim - seg0 < p.seg_len ? p.dim - seg0 : p.seg_len) : 0;
+            const int n_real = lim > first ? (lim - first > 4096 ? 4096 : int(lim - first)) : 0;
+            const int n_seg = p.seg_len > first ? (p.seg_len - first > 4096 ? 4096 : int(p.seg_len - first)) : 0;
+            const T* gb = g + seg0 + first;
+            const T* cb = c + seg0 + first;
             T gv[kTaskWords], cv[kTaskWords];
 #pragma unroll
             for (int t = 0; t < kTaskWords; ++t) {
-                const uint64_t j = j0 + t * 32 + lane;
-                const uint64_t gi = seg0 + j;
-                const bool in = j < p.seg_len && gi < p.dim;
-                gv[t] = in ? g[gi] : T(0);  // value padding 0.0 (+ 0.0) packs to 1
-                cv[t] = in ? c[gi] : T(0);
+                gv[t] = t * 32 < n_real ? gb[t * 32] : T(0);
+                cv[t] = t * 32 < n_real ? cb[t * 32] : T(0);
             }
 #pragma unroll
             for (int t = 0; t < kTaskWords; ++t) {
-                const uint64_t j = j0 + t * 32 + lane;
                 const T u = add_rn(gv[t], cv[t]);
                 fin = fma_rn(u, T(0), fin);  // NaN iff some u is inf/NaN (any non-finite g or c)
-                const uint32_t w = __ballot_sync(kFull, j < p.seg_len && u >= T(0));
+                const uint32_t w = __ballot_sync(kFull, t * 32 < n_seg && u >= T(0));
                 if (lane == t) word = w;
             }
         }
@@ -343,26 +347,28 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode
         } else {
             // any segment length: lane-contiguous (coalesced) loads, all issued
             // before the first is used
+            // element t of this lane is coordinate j0 + 32 t + lane (real below n_real)
+            const uint64_t first = j0 + lane;
+            const uint64_t lim = p.dim > seg0 ? (p.dim - seg0 < p.seg_len ? p.dim - seg0 : p.seg_len) : 0;
+            const int n_real = lim > first ? (lim - first > 4096 ? 4096 : int(lim - first)) : 0;
+            const uint64_t off = seg0 + first;
             T gv[kTaskWords], cv[kTaskWords];
-            uint32_t wv[kTaskWords];
+            // the task's 16 aggregate words: one load per lane, then broadcast
+            const uint32_t wmine =
+                (lane < kTaskWords && q * kTaskWords + lane < p.words_proc) ? __ldg(aw + lane) : 0u;
 #pragma unroll
             for (int t = 0; t < kTaskWords; ++t) {
-                const uint64_t j = j0 + t * 32 + lane;
-                const uint64_t gi = seg0 + j;
-                const bool in = j < p.seg_len && gi < p.dim;
-                gv[t] = in ? g[gi] : T(0);
-                cv[t] = in ? c[gi] : T(0);
-                wv[t] = in ? __ldg(aw + t) : 0u;
+                gv[t] = t * 32 < n_real ? g[off + t * 32] : T(0);
+                cv[t] = t * 32 < n_real ? c[off + t * 32] : T(0);
             }
 #pragma unroll
             for (int t = 0; t < kTaskWords; ++t) {
-                const uint64_t j = j0 + t * 32 + lane;
-                const uint64_t gi = seg0 + j;
-                if (j < p.seg_len && gi < p.dim) {
-                    const T gt = ((wv[t] >> lane) & 1u) ? eta : -eta;
-                    co[gi] = sub_rn(add_rn(gv[t], cv[t]), gt);
-                    if (upd) upd[gi] = gt;
-                    if (xp) xp[gi] = sub_rn(xp[gi], gt);
+                const uint32_t wv = __shfl_sync(kFull, wmine, t);
+                if (t * 32 < n_real) {
+                    const T gt = ((wv >> lane) & 1u) ? eta : -eta;
+                    co[off + t * 32] = sub_rn(add_rn(gv[t], cv[t]), gt);
+                    if (upd) upd[off + t * 32] = gt;
+                    if (xp) xp[off + t * 32] = sub_rn(xp[off + t * 32], gt);
                 }
             }
         }
