@@ -613,7 +613,6 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
     extern __shared__ uint32_t cslots[];  // [max_slots][WPT][kMergeThreads]
     __shared__ uint32_t s_warp[kMergeThreads / 32];
     __shared__ uint64_t s_acc[kMergeThreads / 32];
-    __shared__ uint64_t s_base;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t T = gridDim.x;  // CTAs in this launch
     const uint32_t sl = p.seg_lo + blockIdx.x / p.part_tiles, lt = blockIdx.x % p.part_tiles;
@@ -631,6 +630,36 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
     const uint32_t kb = p.stage_begin[sl * (p.n_stages + 1) + p.stage];
     const uint32_t nm = p.stage_begin[sl * (p.n_stages + 1) + p.stage + 1] - kb;
     const uint32_t sg = p.s_first + sl;
+    // The stage's merge descriptors and the data-independent part of each
+    // merge's draw base (draws before this round + earlier launch parts +
+    // the continued stream's total, all written by earlier launches) are
+    // staged in shared memory once, so no merge step starts with a dependent
+    // global load (kMaxCachedMerges bounds the cache; longer stages read the
+    // descriptors from global memory).
+    __shared__ DevMerge s_m[kMaxCachedMerges];
+    __shared__ uint64_t s_sbase[kMaxCachedMerges];
+    const bool cached = nm <= kMaxCachedMerges;
+    auto static_base = [&](uint32_t mi, const DevMerge& m) -> uint64_t {
+        const uint32_t nmerges = p.n_merges;
+        uint64_t base = m.base_add;  // draws of this stream before this merge
+        for (uint32_t q = 0; q < p.part; ++q)  // earlier parts (earlier launches)
+            base += __ldcg(p.part_totals + uint64_t(q) * nmerges + mb + mi);
+        for (int32_t src = m.offset_src; src >= 0;) {  // continued stream (earlier stage)
+            const DevMerge& pm = p.merges[mb + src];
+            for (uint32_t q = 0; q < p.n_parts; ++q)
+                base += __ldcg(p.part_totals + uint64_t(q) * nmerges + mb + src);
+            base += pm.base_add;
+            src = pm.offset_src;
+        }
+        return base;
+    };
+    if (cached && tid < nm) {
+        const DevMerge m = p.merges[mb + kb + tid];
+        s_m[tid] = m;
+        s_sbase[tid] = static_base(kb + tid, m);
+    }
+    __syncthreads();
+    auto merge_at = [&](uint32_t k) -> DevMerge { return cached ? s_m[k] : p.merges[mb + kb + k]; };
     // a thread's last words may pass the segment's end (WPT = 12): those are
     // loaded as 0 and never stored
     const bool tail = w0 + WPT > p.words_proc;
@@ -664,7 +693,7 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
     // (ring / torus: the received operand is the running aggregate)
     uint32_t pl[WPT];
     if (nm > 0) {
-        const DevMerge m0 = p.merges[mb + kb];
+        const DevMerge m0 = merge_at(0);
         if ((m0.local_src & 0xC000u) == kSrcLeaf) load_src(m0.local_src, pl);
     }
     uint32_t r[WPT], d[WPT];
@@ -675,7 +704,7 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
         DevMerge m{};
         uint32_t cnt = 0;
         if (live) {
-            m = p.merges[mb + mi];
+            m = merge_at(k);
             load_src(m.recv_src, r);
             if ((m.local_src & 0xC000u) == kSrcLeaf) {
 #pragma unroll
@@ -686,7 +715,7 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
                 for (int j = 0; j < WPT; ++j) d[j] = (r[j] ^ d[j]) & vmask(j);
             }
             if (k + 1 < nm) {
-                const DevMerge mn = p.merges[mb + mi + 1];
+                const DevMerge mn = merge_at(k + 1);
                 if ((mn.local_src & 0xC000u) == kSrcLeaf) load_src(mn.local_src, pl);
             }
 #pragma unroll
@@ -725,30 +754,18 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
         if (lane == 0) s_acc[wid] = acc;
         __syncthreads();
         COOP_T(t2);
-        if (live && tid == 0) {
-            uint64_t pre = 0;
+        // every thread sums the 8 warp partials itself (smem broadcast): no
+        // second block barrier before the coin loads
+        uint64_t pre = 0;
 #pragma unroll
-            for (int w = 0; w < kMergeThreads / 32; ++w) pre += s_acc[w];
-            const uint32_t nmerges = p.n_merges;
-            uint64_t base = m.base_add;  // draws of this stream before this merge
-            for (uint32_t q = 0; q < p.part; ++q)  // earlier parts (earlier launches)
-                base += __ldcg(p.part_totals + uint64_t(q) * nmerges + mb + mi);
-            for (int32_t src = m.offset_src; src >= 0;) {  // continued stream (earlier stage)
-                const DevMerge& pm = p.merges[mb + src];
-                for (uint32_t q = 0; q < p.n_parts; ++q)
-                    base += __ldcg(p.part_totals + uint64_t(q) * nmerges + mb + src);
-                base += pm.base_add;
-                src = pm.offset_src;
-            }
-            s_base = base + pre;
-            // the last tile of the part knows the part's total for this merge
-            if (lt == p.part_tiles - 1 || tile + 1 == p.tiles_per_seg)
-                p.part_totals[uint64_t(p.part) * nmerges + mb + mi] = pre + tile_total;
-        }
-        __syncthreads();
+        for (int w = 0; w < kMergeThreads / 32; ++w) pre += s_acc[w];
         COOP_T(t3);
         if (live) {
-            const uint64_t n0 = s_base + warp_off + (incl - cnt);  // my first coin's draw
+            const uint64_t sbase = cached ? s_sbase[k] : static_base(mi, m);
+            // the last tile of the part knows the part's total for this merge
+            if (tid == 0 && (lt == p.part_tiles - 1 || tile + 1 == p.tiles_per_seg))
+                p.part_totals[uint64_t(p.part) * p.n_merges + mb + mi] = pre + tile_total;
+            const uint64_t n0 = sbase + pre + warp_off + (incl - cnt);  // my first coin's draw
             if (n0 + cnt <= uint64_t(m.coin_words) * 32) {
                 const uint32_t* cw = p.coins + m.coin_off;
                 uint64_t n = n0;
@@ -794,9 +811,9 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
                 }
             }
         }
-        // s_warp / s_base are rewritten next step; slots are read by the
-        // writing thread only
-        __syncthreads();
+        // no block barrier here: s_warp / s_acc are rewritten next step only
+        // after the grid barrier, and slots / global nodes are read back by
+        // the thread that wrote them
         COOP_T(t4);
         COOP_ADD(0, t1 - t0);
         COOP_ADD(1, t2 - t1);

@@ -9,6 +9,7 @@ namespace marsit_b200 {
 
 constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ull;  // rng.hpp:64
 constexpr uint32_t kMaxLocalWorkers = 64;           // workers resident on one rank
+constexpr int kMaxCachedMerges = 32;                // merge descriptors staged in smem per stage
 constexpr int kMergeThreads = 256;                   // 8 warps; a warp tile is 32 x WPT packed
                                                      // words, WPT in {1, 2} chosen per context
 constexpr int kStreamThreads = 256;                  // sign_extract / decode
