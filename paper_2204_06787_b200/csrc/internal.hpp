@@ -280,7 +280,9 @@ struct marsit_ctx {
     void* dense_mean = nullptr;  // [S*L] of dtype (G > 1)
     marsit_b200::DenseOp* d_dense_ops = nullptr;
     uint16_t* d_dense_final = nullptr;
-    uint16_t* d_dense_chain = nullptr;  // ring plans: [s_own][M] chain leaf order
+    uint16_t* d_dense_chain = nullptr;  // chain-of-chains plans: [s_own][M] leaf order
+    uint64_t* d_dense_groups = nullptr; // [s_own] group-end bits of that order
+    bool dense_multi = false;           // more than one group in some segment
     uint32_t dense_n_ops = 0;
     // coin precompute on the aux stream; two buffers: this round's and the
     // next round's, computed speculatively for (seed, t + 1) during the decode

@@ -1031,14 +1031,17 @@ __global__ void __launch_bounds__(kDenseThreads) dense_reduce_kernel(const Dense
     if (bad) atomicOr(p.err, 1);
 }
 
-// Ring plans: every owned segment's reduction is one linear chain,
-// v_0 = u[c_1] + u[c_0], v_k = u[c_{k+1}] + v_{k-1} (the receiver's state plus
-// the received partial, allreduce.hpp:114-116), so the leaves are loaded in
-// chain order straight into registers (static indices) — no shared-memory
-// staging — 16 loads in flight per group of 8 workers.  MODE 0: leaves
+// Chain-of-chains plans (ring: one chain; torus: one chain per row, then a
+// chain over the row results): the leaves of a segment are visited in
+// `chain` order; within a group v_0 = u[c_0], v_k = u[c_k] + v_{k-1} (the
+// receiver's state plus the received partial, allreduce.hpp:114-116, IEEE
+// addition being commutative), and where bit k of `chain_groups` is set the
+// group's value is folded into the outer chain the same way.  Leaves are
+// loaded in chain order straight into registers (static indices) — no
+// shared-memory staging — 16 loads in flight per group of 8 workers.  MODE 0: leaves
 // g + c (one GPU), with the compensation reset fused; 1: exchanged u buffer;
 // 2: peers' u buffers (P2P).
-template <typename T, int MODE>
+template <typename T, int MODE, bool MULTI>
 __global__ void __launch_bounds__(256) dense_chain_kernel(const DenseParams<T> p) {
     const uint64_t n = uint64_t(p.n_seg) * p.seg_len;
     bool bad = false;
@@ -1049,7 +1052,9 @@ __global__ void __launch_bounds__(256) dense_chain_kernel(const DenseParams<T> p
         const uint64_t j = uint64_t(p.s_first + sl) * p.seg_len + o;  // global coordinate
         if (j >= p.dim) continue;  // value padding never reaches the output
         const uint16_t* ch = p.chain + uint64_t(sl) * p.workers;
-        double acc = 0.0;
+        const uint64_t gm = MULTI ? p.chain_groups[sl] : (1ull << (p.workers - 1));
+        double acc = 0.0, out = 0.0;
+        bool first_in = true, first_out = true;
         for (uint32_t k0 = 0; k0 < p.workers; k0 += 8) {
             T u[8];
             if (MODE == 0) {
@@ -1087,18 +1092,25 @@ __global__ void __launch_bounds__(256) dense_chain_kernel(const DenseParams<T> p
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 if (k0 + k >= p.workers) break;
-                acc = (k0 + k == 0) ? double(u[k]) : __dadd_rn(double(u[k]), acc);
+                acc = first_in ? double(u[k]) : __dadd_rn(double(u[k]), acc);
                 bad |= !isfinite(acc);
+                first_in = false;
+                if ((gm >> (k0 + k)) & 1) {  // a group's chain ends: fold into the outer chain
+                    out = first_out ? acc : __dadd_rn(acc, out);
+                    bad |= !isfinite(out);
+                    first_out = false;
+                    first_in = true;
+                }
             }
         }
-        p.mean[j] = T(__dmul_rn(acc, p.inv_m));
+        p.mean[j] = T(__dmul_rn(out, p.inv_m));
     }
     if (bad) atomicOr(p.err, 1);
 }
 
 // dense_chain_kernel, one-GPU leaves, 4 consecutive coordinates per thread
 // (16-byte loads; needs L and D multiples of 4 and aligned g, c, c', mean).
-template <typename T>
+template <typename T, bool MULTI>
 __global__ void __launch_bounds__(256) dense_chain4_kernel(const DenseParams<T> p) {
     const uint64_t n4 = uint64_t(p.n_seg) * p.seg_len / 4;
     bool bad = false;
@@ -1110,7 +1122,9 @@ __global__ void __launch_bounds__(256) dense_chain4_kernel(const DenseParams<T> 
         const uint64_t j = uint64_t(p.s_first + sl) * p.seg_len + o;
         if (j >= p.dim) continue;
         const uint16_t* ch = p.chain + uint64_t(sl) * p.workers;
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        const uint64_t gm = MULTI ? p.chain_groups[sl] : (1ull << (p.workers - 1));
+        double acc[4] = {0.0, 0.0, 0.0, 0.0}, out[4] = {0.0, 0.0, 0.0, 0.0};
+        bool first_in = true, first_out = true;
         for (uint32_t k0 = 0; k0 < p.workers; k0 += 8) {
             Quad<T> gq[8], cq[8];
 #pragma unroll
@@ -1132,9 +1146,19 @@ __global__ void __launch_bounds__(256) dense_chain4_kernel(const DenseParams<T> 
                 for (int e = 0; e < 4; ++e) {
                     const T u = add_rn(gq[k].v[e], cq[k].v[e]);
                     bad |= !(finite(gq[k].v[e]) && finite(cq[k].v[e]) && finite(u));
-                    acc[e] = (k0 + k == 0) ? double(u) : __dadd_rn(double(u), acc[e]);
+                    acc[e] = first_in ? double(u) : __dadd_rn(double(u), acc[e]);
                     bad |= !isfinite(acc[e]);
                     zero.v[e] = T(0);
+                }
+                first_in = false;
+                if ((gm >> (k0 + k)) & 1) {  // a group's chain ends: fold into the outer chain
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        out[e] = first_out ? acc[e] : __dadd_rn(acc[e], out[e]);
+                        bad |= !isfinite(out[e]);
+                    }
+                    first_out = false;
+                    first_in = true;
                 }
                 T* z = p.c_zero[ch[k0 + k]];
                 if (z) store4(z + j, zero);  // after the read (c may alias)
@@ -1142,7 +1166,68 @@ __global__ void __launch_bounds__(256) dense_chain4_kernel(const DenseParams<T> 
         }
         Quad<T> m;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) m.v[e] = T(__dmul_rn(acc[e], p.inv_m));
+        for (int e = 0; e < 4; ++e) m.v[e] = T(__dmul_rn(out[e], p.inv_m));
+        store4(p.mean + j, m);
+    }
+    if (bad) atomicOr(p.err, 1);
+}
+
+// General reduction DAG (torus plans), one-GPU leaves, 4 consecutive
+// coordinates per thread with 16-byte loads (same eligibility as
+// dense_chain4_kernel); node values in shared memory as
+// [node][coordinate of the quad][kDenseThreads] doubles (conflict-free).
+template <typename T>
+__global__ void __launch_bounds__(kDenseThreads) dense_dag4_kernel(const DenseParams<T> p) {
+    extern __shared__ double dval[];  // [workers + n_ops][4][kDenseThreads]
+    const int tid = threadIdx.x;
+    const uint64_t n4 = uint64_t(p.n_seg) * p.seg_len / 4;
+    bool bad = false;
+    auto at = [&](uint32_t node, int e) -> double& { return dval[(node * 4 + e) * kDenseThreads + tid]; };
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + tid; i < n4;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i0 = i * 4;
+        const uint32_t sl = uint32_t(i0 / p.seg_len);
+        const uint64_t o = i0 - uint64_t(sl) * p.seg_len;
+        const uint64_t j = uint64_t(p.s_first + sl) * p.seg_len + o;
+        if (j >= p.dim) continue;  // value padding never reaches the output
+        for (uint32_t w0 = 0; w0 < p.workers; w0 += 8) {
+            Quad<T> gq[8], cq[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (w0 + k < p.workers) {
+                    gq[k] = load4(p.src[2 * (w0 + k)] + j);
+                    cq[k] = load4_rw(p.src[2 * (w0 + k) + 1] + j);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (w0 + k >= p.workers) break;
+                Quad<T> zero;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const T u = add_rn(gq[k].v[e], cq[k].v[e]);
+                    bad |= !(finite(gq[k].v[e]) && finite(cq[k].v[e]) && finite(u));
+                    at(w0 + k, e) = double(u);
+                    zero.v[e] = T(0);
+                }
+                T* z = p.c_zero[w0 + k];
+                if (z) store4(z + j, zero);  // after the read (c may alias)
+            }
+        }
+        const DenseOp* ops = p.ops + uint64_t(sl) * p.n_ops;
+        for (uint32_t k = 0; k < p.n_ops; ++k) {
+            const DenseOp op = ops[k];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const double v = __dadd_rn(at(op.a, e), at(op.b, e));
+                bad |= !isfinite(v);
+                at(p.workers + k, e) = v;
+            }
+        }
+        const uint32_t fin = p.final_node[sl];
+        Quad<T> m;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) m.v[e] = T(__dmul_rn(at(fin, e), p.inv_m));
         store4(p.mean + j, m);
     }
     if (bad) atomicOr(p.err, 1);
@@ -1306,15 +1391,39 @@ cudaError_t launch_sub_update(T* const* x, uint32_t ml, const T* v, uint64_t dim
 template <typename T>
 cudaError_t launch_dense_reduce(const DenseParams<T>& p, int grid, cudaStream_t st) {
     if (p.chain) {
-        if (p.mode == 0 && p.vec4)
-            dense_chain4_kernel<T><<<grid, 256, 0, st>>>(p);
-        else if (p.mode == 0)
-            dense_chain_kernel<T, 0><<<grid, 256, 0, st>>>(p);
-        else if (p.mode == 1)
-            dense_chain_kernel<T, 1><<<grid, 256, 0, st>>>(p);
-        else
-            dense_chain_kernel<T, 2><<<grid, 256, 0, st>>>(p);
+        if (p.chain_multi) {
+            if (p.mode == 0 && p.vec4)
+                dense_chain4_kernel<T, true><<<grid, 256, 0, st>>>(p);
+            else if (p.mode == 0)
+                dense_chain_kernel<T, 0, true><<<grid, 256, 0, st>>>(p);
+            else if (p.mode == 1)
+                dense_chain_kernel<T, 1, true><<<grid, 256, 0, st>>>(p);
+            else
+                dense_chain_kernel<T, 2, true><<<grid, 256, 0, st>>>(p);
+        } else {
+            if (p.mode == 0 && p.vec4)
+                dense_chain4_kernel<T, false><<<grid, 256, 0, st>>>(p);
+            else if (p.mode == 0)
+                dense_chain_kernel<T, 0, false><<<grid, 256, 0, st>>>(p);
+            else if (p.mode == 1)
+                dense_chain_kernel<T, 1, false><<<grid, 256, 0, st>>>(p);
+            else
+                dense_chain_kernel<T, 2, false><<<grid, 256, 0, st>>>(p);
+        }
         return cudaGetLastError();
+    }
+    if (p.mode == 0 && p.vec4) {
+        const size_t smem4 = size_t(p.workers + p.n_ops) * 4 * kDenseThreads * sizeof(double);
+        if (smem4 <= 200 * 1024) {
+            if (smem4 > 48 * 1024) {
+                cudaError_t e = cudaFuncSetAttribute(dense_dag4_kernel<T>,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     int(smem4));
+                if (e != cudaSuccess) return e;
+            }
+            dense_dag4_kernel<T><<<grid * 2, kDenseThreads, smem4, st>>>(p);
+            return cudaGetLastError();
+        }
     }
     const size_t smem = size_t(p.workers + p.n_ops) * kDenseThreads * sizeof(double);
     if (smem > 48 * 1024) {
@@ -1384,14 +1493,24 @@ cudaError_t preload_kernels() {
             reinterpret_cast<const void*>(dense_leaf_kernel<double>),
             reinterpret_cast<const void*>(dense_reduce_kernel<float>),
             reinterpret_cast<const void*>(dense_reduce_kernel<double>),
-            reinterpret_cast<const void*>(dense_chain_kernel<float, 0>),
-            reinterpret_cast<const void*>(dense_chain_kernel<float, 1>),
-            reinterpret_cast<const void*>(dense_chain_kernel<float, 2>),
-            reinterpret_cast<const void*>(dense_chain_kernel<double, 0>),
-            reinterpret_cast<const void*>(dense_chain_kernel<double, 1>),
-            reinterpret_cast<const void*>(dense_chain_kernel<double, 2>),
-            reinterpret_cast<const void*>(dense_chain4_kernel<float>),
-            reinterpret_cast<const void*>(dense_chain4_kernel<double>),
+            reinterpret_cast<const void*>(dense_chain_kernel<float, 0, false>),
+            reinterpret_cast<const void*>(dense_chain_kernel<float, 1, false>),
+            reinterpret_cast<const void*>(dense_chain_kernel<float, 2, false>),
+            reinterpret_cast<const void*>(dense_chain4_kernel<float, false>),
+            reinterpret_cast<const void*>(dense_chain_kernel<double, 0, false>),
+            reinterpret_cast<const void*>(dense_chain_kernel<double, 1, false>),
+            reinterpret_cast<const void*>(dense_chain_kernel<double, 2, false>),
+            reinterpret_cast<const void*>(dense_chain4_kernel<double, false>),
+            reinterpret_cast<const void*>(dense_chain_kernel<float, 0, true>),
+            reinterpret_cast<const void*>(dense_chain_kernel<float, 1, true>),
+            reinterpret_cast<const void*>(dense_chain_kernel<float, 2, true>),
+            reinterpret_cast<const void*>(dense_chain4_kernel<float, true>),
+            reinterpret_cast<const void*>(dense_chain_kernel<double, 0, true>),
+            reinterpret_cast<const void*>(dense_chain_kernel<double, 1, true>),
+            reinterpret_cast<const void*>(dense_chain_kernel<double, 2, true>),
+            reinterpret_cast<const void*>(dense_chain4_kernel<double, true>),
+            reinterpret_cast<const void*>(dense_dag4_kernel<float>),
+            reinterpret_cast<const void*>(dense_dag4_kernel<double>),
             reinterpret_cast<const void*>(sub_update_kernel<float>),
             reinterpret_cast<const void*>(sub_update_kernel<double>),
         };

@@ -137,8 +137,10 @@ struct DenseParams {
     const T* u_buf;                      // mode 1: [G][s_own][ml][L] u values
     const T* const* u_peers;             // mode 2 (P2P): rank q's own [S][ml][L] u buffer
     bool vec4;                           // mode 0 chain: 16-byte aligned quads throughout
-    const uint16_t* chain;               // ring plans: [n_seg][workers] leaf order of the
-                                         // linear reduction chain (null: general DAG)
+    const uint16_t* chain;               // chain-of-chains plans: [n_seg][workers] leaf order
+                                         // (null: general DAG)
+    const uint64_t* chain_groups;        // [n_seg]: bit k set = a group chain ends at leaf k
+    bool chain_multi;                    // some segment has more than one group (torus)
     T* c_zero[kMaxLocalWorkers];         // compensation reset c' = 0 fused into the pass
                                          // that reads g, c (sync.hpp:83-85); may alias c
     const DenseOp* ops;                  // [n_seg][n_ops]

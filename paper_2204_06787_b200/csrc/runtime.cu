@@ -16,6 +16,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -137,7 +138,7 @@ marsit_ctx::~marsit_ctx() {
     if (device >= 0) cudaSetDevice(device);
     for (void* p : {(void*)bits, (void*)recv, (void*)agg, (void*)err, dense_send, dense_recv,
                     dense_mean, (void*)d_dense_ops, (void*)d_dense_final, (void*)d_metrics,
-                    (void*)d_dense_chain,
+                    (void*)d_dense_chain, (void*)d_dense_groups,
                     (void*)flags, (void*)d_peer_tables})
         if (p) cudaFree(p);
     for (auto& tp : pending) {
@@ -478,6 +479,8 @@ marsit_status dense_phase(marsit_ctx* ctx, int phase, const void* const* g, cons
     if (s) return s;
     DenseParams<T> p{};
     p.chain = ctx->d_dense_chain;
+    p.chain_groups = ctx->d_dense_groups;
+    p.chain_multi = ctx->dense_multi;
     p.ops = ctx->d_dense_ops;
     p.final_node = ctx->d_dense_final;
     p.n_ops = ctx->dense_n_ops;
@@ -584,6 +587,61 @@ marsit_status dense_phase_any(marsit_ctx* ctx, int phase, const void* const* g,
                               void* mean, cudaStream_t st) {
     if (ctx->dtype == MARSIT_F32) return dense_phase<float>(ctx, phase, g, c, c_out, params, mean, st);
     return dense_phase<double>(ctx, phase, g, c, c_out, params, mean, st);
+}
+
+// Dense reduction tree of one segment (node < M: leaf; else op node - M)
+// as groups of leaves: value = fold(fold(G_1), fold(G_2), ...) with
+// fold(x_1, ..., x_n) = (((x_1 + x_2) + x_3) ... + x_n).  Returns false when
+// the tree has another shape.  The order of the two operands of one add is
+// immaterial (IEEE addition is commutative); the tree shape is reproduced
+// exactly.
+static bool chain_of_chains(const DenseOp* ops, uint32_t M, uint32_t fin,
+                            std::vector<uint16_t>& order, uint64_t& group_ends) {
+    auto leaf = [&](uint32_t n) { return n < M; };
+    // is_chain / flatten: a left-deep chain whose every add takes one leaf
+    std::function<bool(uint32_t, std::vector<uint16_t>*)> flat = [&](uint32_t n,
+                                                                    std::vector<uint16_t>* out) {
+        if (leaf(n)) {
+            if (out) out->push_back(uint16_t(n));
+            return true;
+        }
+        const DenseOp& o = ops[n - M];
+        if (leaf(o.b) && flat(o.a, nullptr)) return flat(o.a, out) && (out ? (out->push_back(o.b), true) : true);
+        if (leaf(o.a) && flat(o.b, nullptr)) return flat(o.b, out) && (out ? (out->push_back(o.a), true) : true);
+        return false;
+    };
+    std::vector<std::vector<uint16_t>> grp;
+    std::function<bool(uint32_t)> decompose = [&](uint32_t n) -> bool {
+        if (flat(n, nullptr)) {
+            grp.emplace_back();
+            return flat(n, &grp.back());
+        }
+        const DenseOp& o = ops[n - M];
+        for (const auto& [prefix, group] : {std::pair<uint32_t, uint32_t>{o.a, o.b}, {o.b, o.a}}) {
+            if (flat(group, nullptr) && decompose(prefix)) {
+                grp.emplace_back();
+                return flat(group, &grp.back());
+            }
+        }
+        return false;
+    };
+    order.clear();
+    group_ends = 0;
+    if (M > 64 || !decompose(fin)) return false;
+    std::vector<bool> seen(M, false);
+    for (const auto& g : grp)
+        for (uint16_t w : g) {
+            if (seen[w]) return false;  // every leaf exactly once
+            seen[w] = true;
+            order.push_back(w);
+        }
+    if (order.size() != M) return false;
+    uint32_t k = 0;
+    for (const auto& g : grp) {
+        k += uint32_t(g.size());
+        group_ends |= 1ull << (k - 1);
+    }
+    return true;
 }
 
 // Coin precompute budget per merge: frac * L draws per use of its (receiver,
@@ -1015,22 +1073,28 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
             fin[sl] = uint16_t(sp.final_node);
         }
         ctx->dense_n_ops = n_ops;
-        // linear chains (ring): v_0 = leaf a_0 + leaf b_0, v_k = leaf a_k + v_{k-1}
-        bool chain = n_ops + 1 == ctx->M && env_int("MARSIT_DENSE_DAG", 0) == 0;
+        // Chain-of-chains form (ring: one chain; torus: row chains, then a
+        // chain over the row results): the register kernels evaluate it;
+        // anything else keeps the general DAG kernels.
+        bool chain = n_ops + 1 == ctx->M && env_int("MARSIT_DENSE_DAG", 0) == 0 && ctx->M <= 64;
         std::vector<uint16_t> order(size_t(ctx->s_own) * ctx->M);
+        std::vector<uint64_t> groups(ctx->s_own);
         for (uint32_t sl = 0; sl < ctx->s_own && chain; ++sl) {
-            const DenseOp* o = &ops[size_t(sl) * n_ops];
-            chain = o[0].a < ctx->M && o[0].b < ctx->M && fin[sl] == ctx->M + n_ops - 1;
-            order[size_t(sl) * ctx->M] = o[0].b;
-            order[size_t(sl) * ctx->M + 1] = o[0].a;
-            for (uint32_t k = 1; k < n_ops && chain; ++k) {
-                chain = o[k].a < ctx->M && o[k].b == ctx->M + k - 1;
-                order[size_t(sl) * ctx->M + k + 1] = o[k].a;
+            std::vector<uint16_t> ord;
+            uint64_t gm = 0;
+            chain = chain_of_chains(&ops[size_t(sl) * n_ops], ctx->M, fin[sl], ord, gm);
+            if (chain) {
+                std::copy(ord.begin(), ord.end(), order.begin() + size_t(sl) * ctx->M);
+                groups[sl] = gm;
+                ctx->dense_multi |= gm != (1ull << (ctx->M - 1));
             }
         }
         if (chain && n_ops > 0) {
             CUDA_TRY(cudaMalloc(&ctx->d_dense_chain, sizeof(uint16_t) * order.size()));
             CUDA_TRY(cudaMemcpy(ctx->d_dense_chain, order.data(), sizeof(uint16_t) * order.size(),
+                                cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMalloc(&ctx->d_dense_groups, sizeof(uint64_t) * groups.size()));
+            CUDA_TRY(cudaMemcpy(ctx->d_dense_groups, groups.data(), sizeof(uint64_t) * groups.size(),
                                 cudaMemcpyHostToDevice));
         }
         CUDA_TRY(cudaMalloc(&ctx->d_dense_ops, sizeof(DenseOp) * ops.size()));

@@ -360,13 +360,17 @@ def test_merge_tilings_bit_exact(wpt, topo, a, b, D, monkeypatch):
 
 
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
-@pytest.mark.parametrize("M,D", [(8, 8192), (4, 1_000_000), (8, 8196)])
-def test_dense_round_vector_path_vs_oracle(dtype, M, D):
-    """Dense rounds on ring plans whose L and D are multiples of 4 take the
-    16-byte chain kernel (and a ragged D the scalar one): exact vs the oracle,
-    compensation reset to 0."""
-    sched = mb.build_ring_schedule(M)
-    T = O.schedule("ring", M)
+@pytest.mark.parametrize("topo,a,b,D", [("ring", 8, 0, 8192), ("ring", 4, 0, 1_000_000),
+                                        ("ring", 8, 0, 8196), ("torus", 2, 4, 8192),
+                                        ("torus", 2, 4, 60_224), ("torus", 3, 3, 36_036),
+                                        ("torus", 2, 4, 8196), ("torus", 2, 2, 1003)])
+def test_dense_round_vector_path_vs_oracle(dtype, topo, a, b, D):
+    """Dense rounds whose L and D are multiples of 4 take the 16-byte kernels
+    (ring: register chain; torus: the reduction DAG in shared memory), ragged
+    sizes the scalar ones: exact vs the oracle, compensation reset to 0."""
+    sched = sched_of(topo, a, b)
+    T = O.schedule(topo, a, b)
+    M = sched.workers
     rng = np.random.default_rng(D + M)
     if dtype == torch.float64:
         g = rng.standard_normal((M, D))
