@@ -16,7 +16,6 @@
 #include <nccl.h>
 
 #include <algorithm>
-#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -597,51 +596,76 @@ marsit_status dense_phase_any(marsit_ctx* ctx, int phase, const void* const* g,
 // exactly.
 static bool chain_of_chains(const DenseOp* ops, uint32_t M, uint32_t fin,
                             std::vector<uint16_t>& order, uint64_t& group_ends) {
-    auto leaf = [&](uint32_t n) { return n < M; };
-    // is_chain / flatten: a left-deep chain whose every add takes one leaf
-    std::function<bool(uint32_t, std::vector<uint16_t>*)> flat = [&](uint32_t n,
-                                                                    std::vector<uint16_t>* out) {
-        if (leaf(n)) {
-            if (out) out->push_back(uint16_t(n));
-            return true;
-        }
-        const DenseOp& o = ops[n - M];
-        if (leaf(o.b) && flat(o.a, nullptr)) return flat(o.a, out) && (out ? (out->push_back(o.b), true) : true);
-        if (leaf(o.a) && flat(o.b, nullptr)) return flat(o.b, out) && (out ? (out->push_back(o.a), true) : true);
-        return false;
-    };
-    std::vector<std::vector<uint16_t>> grp;
-    std::function<bool(uint32_t)> decompose = [&](uint32_t n) -> bool {
-        if (flat(n, nullptr)) {
-            grp.emplace_back();
-            return flat(n, &grp.back());
-        }
-        const DenseOp& o = ops[n - M];
-        for (const auto& [prefix, group] : {std::pair<uint32_t, uint32_t>{o.a, o.b}, {o.b, o.a}}) {
-            if (flat(group, nullptr) && decompose(prefix)) {
-                grp.emplace_back();
-                return flat(group, &grp.back());
-            }
-        }
-        return false;
-    };
     order.clear();
     group_ends = 0;
-    if (M > 64 || !decompose(fin)) return false;
-    std::vector<bool> seen(M, false);
-    for (const auto& g : grp)
-        for (uint16_t w : g) {
-            if (seen[w]) return false;  // every leaf exactly once
-            seen[w] = true;
-            order.push_back(w);
+    if (M > 64 || fin < M) return false;
+    const uint32_t n_nodes = fin + 1;  // ops are in topological order: fin is the last
+    auto leaf = [&](uint32_t n) { return n < M; };
+    // chain[n]: n is a left-deep chain whose every add takes one leaf
+    std::vector<uint8_t> chain(n_nodes, 0);
+    for (uint32_t n = 0; n < n_nodes; ++n) {
+        if (leaf(n)) {
+            chain[n] = 1;
+            continue;
         }
-    if (order.size() != M) return false;
+        const DenseOp& o = ops[n - M];
+        if (o.a >= n || o.b >= n) return false;
+        chain[n] = (leaf(o.b) && chain[o.a]) || (leaf(o.a) && chain[o.b]);
+    }
+    auto flatten = [&](uint32_t n, std::vector<uint16_t>& out) {
+        std::vector<uint16_t> rev;
+        while (!leaf(n)) {
+            const DenseOp& o = ops[n - M];
+            if (leaf(o.b) && chain[o.a]) {
+                rev.push_back(o.b);
+                n = o.a;
+            } else {
+                rev.push_back(o.a);
+                n = o.b;
+            }
+        }
+        rev.push_back(uint16_t(n));
+        out.insert(out.end(), rev.rbegin(), rev.rend());
+    };
+    // dec[n]: n = fold over groups; the prefix operand of each outer add is
+    // itself decomposable and the other operand is one group (a chain)
+    std::vector<int8_t> dec(n_nodes, -1);
+    std::vector<uint32_t> pre(n_nodes, 0), grp_of(n_nodes, 0);
+    for (uint32_t n = 0; n < n_nodes; ++n) {
+        if (chain[n]) {
+            dec[n] = 1;
+            pre[n] = ~0u;  // a single group
+            continue;
+        }
+        const DenseOp& o = ops[n - M];
+        dec[n] = 0;
+        if (chain[o.b] && dec[o.a] == 1) {
+            dec[n] = 1, pre[n] = o.a, grp_of[n] = o.b;
+        } else if (chain[o.a] && dec[o.b] == 1) {
+            dec[n] = 1, pre[n] = o.b, grp_of[n] = o.a;
+        }
+    }
+    if (dec[fin] != 1) return false;
+    std::vector<uint32_t> groups;  // group roots, last first
+    uint32_t n = fin;
+    while (pre[n] != ~0u) {
+        groups.push_back(grp_of[n]);
+        n = pre[n];
+    }
+    groups.push_back(n);
+    std::vector<bool> seen(M, false);
     uint32_t k = 0;
-    for (const auto& g : grp) {
-        k += uint32_t(g.size());
+    for (auto it = groups.rbegin(); it != groups.rend(); ++it) {
+        const size_t before = order.size();
+        flatten(*it, order);
+        for (size_t i = before; i < order.size(); ++i) {
+            if (seen[order[i]]) return false;  // every leaf exactly once
+            seen[order[i]] = true;
+        }
+        k += uint32_t(order.size() - before);
         group_ends |= 1ull << (k - 1);
     }
-    return true;
+    return order.size() == M;
 }
 
 // Coin precompute budget per merge: frac * L draws per use of its (receiver,

@@ -388,3 +388,42 @@ def test_dense_round_vector_path_vs_oracle(dtype, topo, a, b, D):
     assert np.array_equal(mean.double().cpu().numpy(), want)
     assert all(bool((c == 0).all()) for c in comp)
     ctx.check()
+
+
+@pytest.mark.parametrize("topo,a,b,D,period", [
+    ("ring", 33, 0, 40_009, None),    # 32 merges per segment: descriptor cache limit
+    ("ring", 64, 0, 70_001, 2),       # 63 merges: descriptors read from global memory
+    ("torus", 4, 8, 50_021, 2),
+    ("torus", 8, 8, 64 * 1024 + 5, None),
+])
+def test_large_worker_counts_vs_oracle(topo, a, b, D, period):
+    """Many workers on one context (up to kMaxLocalWorkers = 64): long merge
+    chains (more merges per stage than the shared-memory descriptor cache
+    holds) and wide dense reduction trees, exact vs the oracle over rounds
+    including dense ones."""
+    sched = sched_of(topo, a, b)
+    T = O.schedule(topo, a, b)
+    W, seed = sched.workers, 4242
+    ctx = mb.Context(D, sched, torch.float32, 0)
+    comp_o = np.zeros((W, D))
+    comp = [torch.zeros(D, device=DEV) for _ in range(W)]
+    for t in (1, 2, 3):
+        g = np.stack([O.gen_dyadic(seed, w, t, D) for w in range(W)])
+        r = O.marsit_round(T, t, period, ETA, g, comp_o, seed)
+        assert r.status == 0
+        gd = [torch.tensor(x, dtype=torch.float32, device=DEV) for x in g]
+        if r.full_precision:
+            mean = torch.empty(D, device=DEV)
+            ctx.dense_round(t, gd, comp, mean)
+            got_update = mean
+        else:
+            agg = torch.empty((D + 63) // 64, dtype=torch.int64, device=DEV)
+            upd = torch.empty(D, device=DEV)
+            ctx.sign_round(t, ETA, seed, gd, comp, agg_bits=agg, update=upd)
+            assert u64(agg).tolist() == r.agg_bits.tolist(), (topo, t)
+            got_update = upd
+        torch.cuda.synchronize()
+        assert np.array_equal(got_update.double().cpu().numpy(), r.update), (topo, t)
+        assert np.array_equal(np.stack([c.double().cpu().numpy() for c in comp]), r.comp)
+        comp_o = r.comp
+    ctx.check()
