@@ -827,18 +827,10 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
 // Coin precompute: blockIdx.y = merge, warps stride over the merge's words;
 // lane l draws n = 32*w + l and the warp ballot is coin word w.
 // ---------------------------------------------------------------------------
-// Coin of draw z: (mix64(z) < th) evaluated on the high word only (exact
-// unless the high words tie, probability 2^-32, which takes the full path).
-// The first xor-shift stays on the ALU pipe, the second goes through the
-// FMA pipe, and only the high word of the last product is formed.
-__device__ __forceinline__ bool coin_hi(uint64_t z, uint64_t th) {
-    const uint32_t xh = mix64_hi(z);
-    const uint32_t thh = uint32_t(th >> 32);
-    bool c = xh < thh;
-    if (xh == thh) c = mix64(z) < th;
-    return c;
-}
-
+// Coin of draw z: mix64(z) < th, decided on the high word of mix64 (exact
+// unless it equals th's high word, probability 2^-32).  mix64_hi sends the
+// first xor-shift to the ALU pipe and the second through the FMA pipe, and
+// forms only the high word of the last product.
 __global__ void __launch_bounds__(256) coins_kernel(const DevMerge* __restrict__ merges,
                                                     uint64_t seed, uint64_t round,
                                                     uint32_t* __restrict__ coins) {
@@ -854,13 +846,32 @@ __global__ void __launch_bounds__(256) coins_kernel(const DevMerge* __restrict__
         // independent draw streams for ILP), then both are stored coalesced
         uint64_t za = key + (uint64_t(c) * 2048 + uint64_t(lane) * 32 + 1) * kGamma;
         uint64_t zb = za + 1024 * kGamma;
+        // the high word decides unless it equals th's (probability 2^-32 per
+        // draw): ties only raise a flag, and a word that saw one is redrawn
+        // with the full compare (no per-draw branch)
+        const uint32_t thh = uint32_t(th >> 32);
+        const uint64_t za0 = za, zb0 = zb;
         uint32_t wa = 0, wb = 0;
+        bool tie = false;
 #pragma unroll 8
         for (int i = 0; i < 32; ++i) {
-            if (coin_hi(za, th)) wa |= 1u << i;
-            if (coin_hi(zb, th)) wb |= 1u << i;
+            const uint32_t xa = mix64_hi(za), xb = mix64_hi(zb);
+            wa |= uint32_t(xa < thh) << i;
+            wb |= uint32_t(xb < thh) << i;
+            tie |= (xa == thh) | (xb == thh);
             za += kGamma;
             zb += kGamma;
+        }
+        if (tie) {
+            za = za0;
+            zb = zb0;
+            wa = wb = 0;
+            for (int i = 0; i < 32; ++i) {
+                if (mix64(za) < th) wa |= 1u << i;
+                if (mix64(zb) < th) wb |= 1u << i;
+                za += kGamma;
+                zb += kGamma;
+            }
         }
         __stcg(out + uint64_t(c) * 64 + lane, wa);
         __stcg(out + uint64_t(c) * 64 + 32 + lane, wb);
