@@ -271,8 +271,12 @@ __device__ __forceinline__ const uint32_t* agg_row(const StreamParams<T>& p, uin
     return base + uint64_t(s) * p.wst;
 }
 
-template <typename T, bool VEC>
-__global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode_kernel(const StreamParams<T> p) {
+// XU: the replica update x -= g_t is fused (its quads are loaded with g and c,
+// so the read-modify-write of x is not a dependent round trip per sub-chunk)
+template <typename T, bool VEC, bool XU>
+__global__ void __launch_bounds__(kStreamThreads,
+                                  (sizeof(T) == 4 && !XU) ? 3 : ((sizeof(T) == 8 && XU) ? 1 : 2))
+    decode_kernel(const StreamParams<T> p) {
     const int lane = threadIdx.x & 31;
     const uint32_t warps = gridDim.x * (kStreamThreads / 32);
     const uint32_t tasks_per_seg = (p.words_proc + kTaskWords - 1) / kTaskWords;
@@ -293,7 +297,7 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode
         const uint64_t j0 = uint64_t(q) * (kTaskWords * 32);
         const uint32_t* aw = agg_row(p, s) + q * kTaskWords;
         if (VEC) {
-            Quad<T> gv[4], cv[4];
+            Quad<T> gv[4], cv[4], xv[XU ? 4 : 1];
             uint32_t nib[4];
 #pragma unroll
             for (int sub = 0; sub < 4; ++sub) {
@@ -305,6 +309,7 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode
                 if (j < p.seg_len && gi + 3 < p.dim) {
                     gv[sub] = load4(g + gi);
                     cv[sub] = load4_rw(c + gi);
+                    if (XU && xp) xv[XU ? sub : 0] = load4_rw(xp + gi);
                 } else {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
@@ -328,11 +333,11 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode
                 if (j < p.seg_len && gi + 3 < p.dim) {
                     store4(co + gi, out);
                     if (upd) store4(upd + gi, up);
-                    if (xp) {
-                        Quad<T> xv = load4_rw(xp + gi);
+                    if (XU && xp) {
+                        Quad<T>& xq = xv[XU ? sub : 0];
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) xv.v[k] = sub_rn(xv.v[k], up.v[k]);
-                        store4(xp + gi, xv);
+                        for (int k = 0; k < 4; ++k) xq.v[k] = sub_rn(xq.v[k], up.v[k]);
+                        store4(xp + gi, xq);
                     }
                 } else {
 #pragma unroll
@@ -340,7 +345,7 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode
                         if ((j + k < p.seg_len) && (gi + k < p.dim)) {
                             co[gi + k] = out.v[k];
                             if (upd) upd[gi + k] = up.v[k];
-                            if (xp) xp[gi + k] = sub_rn(xp[gi + k], up.v[k]);
+                            if (XU && xp) xp[gi + k] = sub_rn(xp[gi + k], up.v[k]);
                         }
                 }
             }
@@ -352,7 +357,7 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode
             const uint64_t lim = p.dim > seg0 ? (p.dim - seg0 < p.seg_len ? p.dim - seg0 : p.seg_len) : 0;
             const int n_real = lim > first ? (lim - first > 4096 ? 4096 : int(lim - first)) : 0;
             const uint64_t off = seg0 + first;
-            T gv[kTaskWords], cv[kTaskWords];
+            T gv[kTaskWords], cv[kTaskWords], xv[XU ? kTaskWords : 1];
             // the task's 16 aggregate words: one load per lane, then broadcast
             const uint32_t wmine =
                 (lane < kTaskWords && q * kTaskWords + lane < p.words_proc) ? __ldg(aw + lane) : 0u;
@@ -360,6 +365,7 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode
             for (int t = 0; t < kTaskWords; ++t) {
                 gv[t] = t * 32 < n_real ? g[off + t * 32] : T(0);
                 cv[t] = t * 32 < n_real ? c[off + t * 32] : T(0);
+                if (XU) xv[XU ? t : 0] = (xp && t * 32 < n_real) ? xp[off + t * 32] : T(0);
             }
 #pragma unroll
             for (int t = 0; t < kTaskWords; ++t) {
@@ -368,7 +374,7 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? 3 : 2) decode
                     const T gt = ((wv >> lane) & 1u) ? eta : -eta;
                     co[off + t * 32] = sub_rn(add_rn(gv[t], cv[t]), gt);
                     if (upd) upd[off + t * 32] = gt;
-                    if (xp) xp[off + t * 32] = sub_rn(xp[off + t * 32], gt);
+                    if (XU && xp) xp[off + t * 32] = sub_rn(xv[XU ? t : 0], gt);
                 }
             }
         }
@@ -1265,10 +1271,19 @@ cudaError_t launch_decode(const StreamParams<T>& p, bool vec, int grid, cudaStre
             decode_stats_kernel<T, true><<<grid, kStreamThreads, 0, st>>>(p);
         else
             decode_stats_kernel<T, false><<<grid, kStreamThreads, 0, st>>>(p);
-    } else if (vec)
-        decode_kernel<T, true><<<grid, kStreamThreads, 0, st>>>(p);
-    else
-        decode_kernel<T, false><<<grid, kStreamThreads, 0, st>>>(p);
+    } else {
+        bool xu = false;
+        for (uint32_t w = 0; w < p.ml; ++w) xu |= p.x[w] != nullptr;
+        if (xu) {
+            if (vec)
+                decode_kernel<T, true, true><<<grid, kStreamThreads, 0, st>>>(p);
+            else
+                decode_kernel<T, false, true><<<grid, kStreamThreads, 0, st>>>(p);
+        } else if (vec)
+            decode_kernel<T, true, false><<<grid, kStreamThreads, 0, st>>>(p);
+        else
+            decode_kernel<T, false, false><<<grid, kStreamThreads, 0, st>>>(p);
+    }
     return cudaGetLastError();
 }
 
@@ -1333,7 +1348,7 @@ cudaError_t stream_occupancy(bool f64, int* extract_blocks, int* decode_blocks) 
                                                           kStreamThreads, 0);
         if (e == cudaSuccess)
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(decode_blocks,
-                                                              decode_kernel<double, true>,
+                                                              decode_kernel<double, true, false>,
                                                               kStreamThreads, 0);
     } else {
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(extract_blocks,
@@ -1341,7 +1356,7 @@ cudaError_t stream_occupancy(bool f64, int* extract_blocks, int* decode_blocks) 
                                                           kStreamThreads, 0);
         if (e == cudaSuccess)
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(decode_blocks,
-                                                              decode_kernel<float, true>,
+                                                              decode_kernel<float, true, false>,
                                                               kStreamThreads, 0);
     }
     return e;
@@ -1483,10 +1498,14 @@ cudaError_t preload_kernels() {
             reinterpret_cast<const void*>(extract_kernel<float, false>),
             reinterpret_cast<const void*>(extract_kernel<double, true>),
             reinterpret_cast<const void*>(extract_kernel<double, false>),
-            reinterpret_cast<const void*>(decode_kernel<float, true>),
-            reinterpret_cast<const void*>(decode_kernel<float, false>),
-            reinterpret_cast<const void*>(decode_kernel<double, true>),
-            reinterpret_cast<const void*>(decode_kernel<double, false>),
+            reinterpret_cast<const void*>(decode_kernel<float, true, false>),
+            reinterpret_cast<const void*>(decode_kernel<float, false, false>),
+            reinterpret_cast<const void*>(decode_kernel<double, true, false>),
+            reinterpret_cast<const void*>(decode_kernel<double, false, false>),
+            reinterpret_cast<const void*>(decode_kernel<float, true, true>),
+            reinterpret_cast<const void*>(decode_kernel<float, false, true>),
+            reinterpret_cast<const void*>(decode_kernel<double, true, true>),
+            reinterpret_cast<const void*>(decode_kernel<double, false, true>),
             reinterpret_cast<const void*>(decode_stats_kernel<float, true>),
             reinterpret_cast<const void*>(decode_stats_kernel<float, false>),
             reinterpret_cast<const void*>(decode_stats_kernel<double, true>),
