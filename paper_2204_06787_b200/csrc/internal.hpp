@@ -262,6 +262,9 @@ struct marsit_ctx {
     uint32_t M = 0, S = 0, G = 1, rank = 0, ml = 0, s_own = 0, s_first = 0;
     uint32_t words64 = 0, words_proc = 0, wst = 0;
     int sm_count = 148;
+    // K1/K4 task order (StreamParams::reverse); MARSIT_L2_REUSE=0 disables
+    bool l2_reuse = marsit_b200::env_int("MARSIT_L2_REUSE", 1) != 0;
+    uint32_t task_dir = 0;
     bool vec_ok = false;
     marsit_b200::HostSchedule sched;
     marsit_b200::Plan plan;

@@ -168,8 +168,10 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? (VEC ? 4 : 3)
     T fin = T(0);  // stays 0 unless some u = g + c is not finite
     for (uint64_t task = blockIdx.x * (kStreamThreads / 32) + (threadIdx.x >> 5); task < n_tasks;
          task += warps) {
-        const uint32_t q = uint32_t(task % tasks_per_seg);
-        const uint64_t rest = task / tasks_per_seg;
+        // p.reverse: walk the tasks from the end (see StreamParams::reverse)
+        const uint64_t tk = p.reverse ? n_tasks - 1 - task : task;
+        const uint32_t q = uint32_t(tk % tasks_per_seg);
+        const uint64_t rest = tk / tasks_per_seg;
         const uint32_t s = p.seg0 + uint32_t(rest % p.n_proc);
         const uint32_t wl = uint32_t(rest / p.n_proc);
         const T* __restrict__ g = p.g[wl];
@@ -284,8 +286,10 @@ __global__ void __launch_bounds__(kStreamThreads,
     const T eta = p.eta;
     for (uint64_t task = blockIdx.x * (kStreamThreads / 32) + (threadIdx.x >> 5); task < n_tasks;
          task += warps) {
-        const uint32_t q = uint32_t(task % tasks_per_seg);
-        const uint64_t rest = task / tasks_per_seg;
+        // p.reverse: walk the tasks from the end (see StreamParams::reverse)
+        const uint64_t tk = p.reverse ? n_tasks - 1 - task : task;
+        const uint32_t q = uint32_t(tk % tasks_per_seg);
+        const uint64_t rest = tk / tasks_per_seg;
         const uint32_t s = p.seg0 + uint32_t(rest % p.n_proc);
         const uint32_t wl = uint32_t(rest / p.n_proc);
         const T* __restrict__ g = p.g[wl];

@@ -77,6 +77,11 @@ struct StreamParams {
     uint32_t seg0, n_proc;       // this launch: segments [seg0, seg0 + n_proc)
     uint64_t dim, seg_len;       // D, L
     uint32_t words_proc, wst;
+    // walk the warp tasks from the last to the first: the decode walks them
+    // opposite to the same round's extract, so it starts on the coordinates
+    // the extract read last (still in L2 across the merge); the direction
+    // alternates by round so consecutive rounds never share a cache warm-up
+    uint32_t reverse;
     uint32_t* bits;              // extract output: [S][ml][wst]
     const uint32_t* agg;         // decode input: [S][wst]
     // P2P transport: segment s is read from its owner's buffer agg_peers[s / s_own]

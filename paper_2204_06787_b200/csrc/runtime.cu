@@ -240,12 +240,15 @@ marsit_status run_extract(marsit_ctx* ctx, const void* const* g, const void* con
     marsit_status s = ctx->begin_phase(st, &ev);
     if (s) return s;
     const bool vec = vec_ok_ptrs(ctx, g, c);
-    if (ctx->dtype == MARSIT_F32)
-        CUDA_TRY(launch_extract(stream_params<float>(ctx, g, c, nullptr, nullptr, 0.0), vec,
-                                ctx->extract_grid, st));
-    else
-        CUDA_TRY(launch_extract(stream_params<double>(ctx, g, c, nullptr, nullptr, 0.0), vec,
-                                ctx->extract_grid, st));
+    if (ctx->dtype == MARSIT_F32) {
+        auto p = stream_params<float>(ctx, g, c, nullptr, nullptr, 0.0);
+        p.reverse = ctx->task_dir;
+        CUDA_TRY(launch_extract(p, vec, ctx->extract_grid, st));
+    } else {
+        auto p = stream_params<double>(ctx, g, c, nullptr, nullptr, 0.0);
+        p.reverse = ctx->task_dir;
+        CUDA_TRY(launch_extract(p, vec, ctx->extract_grid, st));
+    }
     return ctx->end_phase(kPhExtract, st, ev, 1);
 }
 
@@ -429,6 +432,7 @@ marsit_status run_decode(marsit_ctx* ctx, const void* const* g, const void* cons
         p.n_workers = ctx->M;
         p.agg_peers = p2p_table(ctx, 1);
         p.s_own = ctx->s_own;
+        p.reverse = ctx->l2_reuse ? ctx->task_dir ^ 1u : 0u;
         CUDA_TRY(launch_decode(p, vec, ctx->decode_grid, st));
     } else {
         auto p = stream_params<double>(ctx, g, c, c_out, update, eta, params);
@@ -438,6 +442,7 @@ marsit_status run_decode(marsit_ctx* ctx, const void* const* g, const void* cons
         p.n_workers = ctx->M;
         p.agg_peers = p2p_table(ctx, 1);
         p.s_own = ctx->s_own;
+        p.reverse = ctx->l2_reuse ? ctx->task_dir ^ 1u : 0u;
         CUDA_TRY(launch_decode(p, vec, ctx->decode_grid, st));
     }
     return ctx->end_phase(kPhDecode, st, ev, 1);
@@ -711,6 +716,7 @@ marsit_status sign_phase(marsit_ctx* ctx, int phase, uint64_t t, double eta_s, u
     marsit_status s = MARSIT_OK;
     if (phase == 0) {
         if (ctx->p2p) ++ctx->epoch;
+        ctx->task_dir = ctx->l2_reuse ? uint32_t(t & 1) : 0;
         if ((s = run_coins(ctx, seed, t, st))) return s;
         if ((s = run_extract(ctx, d_grads, d_comp, st))) return s;
         return p2p_signal(ctx, 0, st);  // my packed signs are ready
