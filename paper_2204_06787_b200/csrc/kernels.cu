@@ -393,6 +393,16 @@ __global__ void __launch_bounds__(kStreamThreads,
 // HBM traffic.  matches += [aggregate bit == (sum / M >= 0)] over the D
 // coordinates.  Needs every worker of the job local (p.ml == M).
 // ---------------------------------------------------------------------------
+// (sum / M >= 0) of the worker-order fp64 sum of u (trainer.hpp:249): for
+// fp32 u a negative sum is at most -2^-149 and sum / M cannot round to -0,
+// so the sign of the sum decides without the division; fp64 u can be
+// subnormal, so a negative sum still takes the literal division.
+template <typename T>
+__device__ __forceinline__ bool mean_nonneg(double sum, double m) {
+    if (sum >= 0.0) return true;
+    return sizeof(T) == 8 && __ddiv_rn(sum, m) >= 0.0;
+}
+
 template <typename T>
 __device__ __forceinline__ void decode_one(const StreamParams<T>& p, uint32_t wl, uint64_t gi,
                                            T gt, T& u) {
@@ -487,7 +497,7 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 80 : 128) decode_stats_kernel(const
                 for (int h = 0; h < 2; ++h)
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
-                        matches += (((nib[h] >> k) & 1u) != 0) == (__ddiv_rn(sum[h][k], wm) >= 0.0);
+                        matches += (((nib[h] >> k) & 1u) != 0) == mean_nonneg<T>(sum[h][k], wm);
             }
         } else {
             // ragged task (segment / vector tail or unaligned buffers): per coordinate
@@ -504,7 +514,7 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 80 : 128) decode_stats_kernel(const
                         decode_one(p, wl, gi, gt, u);
                         sum = __dadd_rn(sum, double(u));
                     }
-                    matches += (bit != 0) == (__ddiv_rn(sum, wm) >= 0.0);
+                    matches += (bit != 0) == mean_nonneg<T>(sum, wm);
                 }
             }
         }

@@ -34,6 +34,9 @@ def gen(recipe, seed, w, t, D):
     ("ring", 4, 0, 65_536, 1, torch.float32),
     ("torus", 2, 4, 60_211, 1, torch.float64),
     ("ring", 5, 0, 37, 0, torch.float64),
+    ("ring", 2, 0, 4_099, 0, torch.float32),
+    ("ring", 8, 0, 262_144, 1, torch.float32),    # aligned quads
+    ("ring", 16, 0, 50_001, 0, torch.float32),
 ])
 def test_metrics_match_oracle_over_rounds(topo, a, b, D, recipe, dtype):
     sched, T = sched_pair(topo, a, b)
