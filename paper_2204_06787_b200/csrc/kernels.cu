@@ -559,33 +559,30 @@ __device__ __forceinline__ uint32_t shl_fma(uint32_t x, uint32_t s) { return x *
 // Parallel bit deposit (PDEP): the low popcount(m) bits of x are placed,
 // in order, at the set bits of m.  Branch-free "expand" of Hacker's Delight
 // §7-6 (five parallel-suffix rounds); left shifts are written as multiplies
-// so they can issue on the FMA pipe next to the ALU-pipe logic ops.
-__device__ __forceinline__ uint32_t deposit32(uint32_t m, uint32_t x) {
-    const uint32_t m0 = m;
+// so they can issue on the FMA pipe next to the ALU-pipe logic ops.  Split
+// in two: the five shift masks depend only on m (the disagreement word,
+// known before the grid barrier, so they are formed while the other tiles
+// arrive), the moves of x need the coin window (known after it).
+__device__ __forceinline__ void expand_masks(uint32_t m, uint32_t (&mv)[5]) {
     uint32_t mk = ~m << 1;
-    uint32_t mv0, mv1, mv2, mv3, mv4;
-#define MARSIT_EXPAND_ROUND(I, MV)                        \
-    {                                                     \
-        uint32_t mp = mk ^ shl_fma(mk, 1);                \
-        mp ^= shl_fma(mp, 2);                             \
-        mp ^= shl_fma(mp, 4);                             \
-        mp ^= shl_fma(mp, 8);                             \
-        mp ^= shl_fma(mp, 16);                            \
-        MV = mp & m;                                      \
-        m = (m ^ MV) | (MV >> (1 << I));                  \
-        mk &= ~mp;                                        \
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        uint32_t mp = mk ^ shl_fma(mk, 1);
+        mp ^= shl_fma(mp, 2);
+        mp ^= shl_fma(mp, 4);
+        mp ^= shl_fma(mp, 8);
+        mp ^= shl_fma(mp, 16);
+        mv[i] = mp & m;
+        m = (m ^ mv[i]) | (mv[i] >> (1 << i));
+        mk &= ~mp;
     }
-    MARSIT_EXPAND_ROUND(0, mv0)
-    MARSIT_EXPAND_ROUND(1, mv1)
-    MARSIT_EXPAND_ROUND(2, mv2)
-    MARSIT_EXPAND_ROUND(3, mv3)
-    MARSIT_EXPAND_ROUND(4, mv4)
-#undef MARSIT_EXPAND_ROUND
-    x = (x & ~mv4) | (shl_fma(x, 16) & mv4);
-    x = (x & ~mv3) | (shl_fma(x, 8) & mv3);
-    x = (x & ~mv2) | (shl_fma(x, 4) & mv2);
-    x = (x & ~mv1) | (shl_fma(x, 2) & mv1);
-    x = (x & ~mv0) | (shl_fma(x, 1) & mv0);
+}
+__device__ __forceinline__ uint32_t expand_apply(uint32_t x, const uint32_t (&mv)[5], uint32_t m0) {
+    x = (x & ~mv[4]) | (shl_fma(x, 16) & mv[4]);
+    x = (x & ~mv[3]) | (shl_fma(x, 8) & mv[3]);
+    x = (x & ~mv[2]) | (shl_fma(x, 4) & mv[2]);
+    x = (x & ~mv[1]) | (shl_fma(x, 2) & mv[1]);
+    x = (x & ~mv[0]) | (shl_fma(x, 1) & mv[0]);
     return x & m0;
 }
 
@@ -630,7 +627,9 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
     merge_coop_kernel(const CoopParams p) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
-    extern __shared__ uint32_t cslots[];  // [max_slots][WPT][kMergeThreads]
+    extern __shared__ uint32_t cslots[];  // [max_slots][WPT][kMergeThreads], then the
+                                          // deposit masks [WPT][5][kMergeThreads]
+    uint32_t* cmask = cslots + size_t(p.max_slots) * WPT * kMergeThreads;
     __shared__ uint32_t s_warp[kMergeThreads / 32];
     __shared__ uint64_t s_acc[kMergeThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -762,7 +761,19 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
         if (tid == 0) __stcg(reinterpret_cast<unsigned long long*>(flags + blockIdx.x),
                              (unsigned long long)tile_total);
         COOP_T(t1);
-        grid.sync();
+        // split grid barrier: the deposit masks of r ^ l are formed while the
+        // other tiles arrive (they need d only, not the draw base)
+        auto token = grid.barrier_arrive();
+        if (live) {
+#pragma unroll
+            for (int j = 0; j < WPT; ++j) {
+                uint32_t mv[5];
+                expand_masks(d[j], mv);
+#pragma unroll
+                for (int i = 0; i < 5; ++i) cmask[(j * 5 + i) * kMergeThreads + tid] = mv[i];
+            }
+        }
+        grid.barrier_wait(std::move(token));
         // exclusive draw offset: the counts of this segment's earlier tiles in
         // this launch, read block-wide (all loads in flight at once)
         const uint32_t seg_base = blockIdx.x - lt;
@@ -800,7 +811,10 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
                         const uint32_t c1 = (sh + pc > 32) ? __ldg(cw + wi + 1) : 0u;
                         window = __funnelshift_r(c0, c1, sh);
                     }
-                    r[j] = (r[j] ^ (d[j] & ~deposit32(d[j], window))) & vmask(j);
+                    uint32_t mv[5];
+#pragma unroll
+                    for (int i = 0; i < 5; ++i) mv[i] = cmask[(j * 5 + i) * kMergeThreads + tid];
+                    r[j] = (r[j] ^ (d[j] & ~expand_apply(window, mv, d[j]))) & vmask(j);
                     n += pc;
                 }
             } else {
