@@ -300,6 +300,7 @@ struct marsit_ctx {
     } coin_tag[2];
     int cur_coin = 0;
     bool coin_prefetch = true;
+    bool coin_prefetch_at_extract = false;
     bool coins_pending = false;
     uint64_t coin_total_words = 0;
     // single GPU: per-segment merges (aux) pipelined with per-segment decodes

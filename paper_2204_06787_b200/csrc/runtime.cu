@@ -718,13 +718,16 @@ marsit_status sign_phase(marsit_ctx* ctx, int phase, uint64_t t, double eta_s, u
         if (ctx->p2p) ++ctx->epoch;
         ctx->task_dir = ctx->l2_reuse ? uint32_t(t & 1) : 0;
         if ((s = run_coins(ctx, seed, t, st))) return s;
+        // MARSIT_COIN_PREFETCH_AT=1: the next round's coins run underneath
+        // this extract instead of this round's decode
+        if (ctx->coin_prefetch_at_extract && (s = prefetch_coins(ctx, seed, t, st))) return s;
         if ((s = run_extract(ctx, d_grads, d_comp, st))) return s;
         return p2p_signal(ctx, 0, st);  // my packed signs are ready
     }
     if (phase == 1) {
         if ((s = p2p_wait(ctx, 0, st))) return s;  // every rank's packed signs
         if ((s = run_merge(ctx, seed, t, st))) return s;
-        if ((s = prefetch_coins(ctx, seed, t, st))) return s;
+        if (!ctx->coin_prefetch_at_extract && (s = prefetch_coins(ctx, seed, t, st))) return s;
         return p2p_signal(ctx, 1, st);  // my owned aggregates are ready
     }
     if ((s = p2p_wait(ctx, 1, st))) return s;  // every owner's aggregates
@@ -1051,6 +1054,7 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
             CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_coin_done[b], cudaEventDisableTiming));
         }
     ctx->coin_prefetch = env_int("MARSIT_COIN_PREFETCH", 1) != 0;
+    ctx->coin_prefetch_at_extract = env_int("MARSIT_COIN_PREFETCH_AT", 0) != 0;
     if (ctx->pipeline) {
         CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_extract, cudaEventDisableTiming));
         ctx->ev_merge.resize(ctx->S);
