@@ -82,6 +82,7 @@ struct MergeRunner {
     uint32_t* gnodes = nullptr;
     uint64_t* flags = nullptr;  // [kmax][seg_per_launch * part_tiles]
     uint64_t* part_totals = nullptr;
+    uint64_t* coin_end = nullptr;  // [n_merges] last round's end draw index per merge (~0: none)
     const uint32_t* const* peer_bits = nullptr;  // P2P transport: device table [G]
 
     MergeRunner() = default;
@@ -89,7 +90,7 @@ struct MergeRunner {
     MergeRunner& operator=(const MergeRunner&) = delete;
     ~MergeRunner() {
         for (void* p : {(void*)d_merges, (void*)d_seg_begin, (void*)d_stage_begin, (void*)gnodes,
-                        (void*)flags, (void*)part_totals})
+                        (void*)flags, (void*)part_totals, (void*)coin_end})
             if (p) cudaFree(p);
     }
 
@@ -179,6 +180,8 @@ struct MergeRunner {
         CUDA_TRY(cudaMemset(flags, 0, sizeof(uint64_t) * nflags));
         CUDA_TRY(cudaMalloc(&part_totals, sizeof(uint64_t) * size_t(n_parts) * nm));
         CUDA_TRY(cudaMemset(part_totals, 0, sizeof(uint64_t) * size_t(n_parts) * nm));
+        CUDA_TRY(cudaMalloc(&coin_end, sizeof(uint64_t) * nm));
+        CUDA_TRY(cudaMemset(coin_end, 0xFF, sizeof(uint64_t) * nm));  // no history yet
         return MARSIT_OK;
     }
 
@@ -186,7 +189,7 @@ struct MergeRunner {
     // per launch; more segments run as consecutive launches).
     marsit_status run(const uint32_t* leaves, uint32_t* agg, const uint32_t* coins, uint64_t seed,
                       uint64_t round, cudaStream_t st, uint64_t* n_launch, uint32_t seg_lo = 0,
-                      uint32_t seg_cnt = ~0u) {
+                      uint32_t seg_cnt = ~0u, const uint32_t* coin_valid = nullptr) {
         if (seg_cnt == ~0u) seg_cnt = n_seg - seg_lo;
         CoopParams c{};
         c.merges = d_merges;
@@ -215,6 +218,8 @@ struct MergeRunner {
         c.part_totals = part_totals;
         c.seed = seed;
         c.round = round;
+        c.coin_valid = coins ? coin_valid : nullptr;
+        c.coin_end = coin_end;
         for (uint32_t s0 = seg_lo; s0 < seg_lo + seg_cnt; s0 += seg_per_launch) {
             c.seg_lo = s0;
             c.seg_cnt = std::min(seg_per_launch, seg_lo + seg_cnt - s0);
@@ -293,6 +298,7 @@ struct marsit_ctx {
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr;
     uint32_t* coin_buf[2] = {nullptr, nullptr};
+    uint32_t* coin_valid[2] = {nullptr, nullptr};  // [n_merges] words computed per merge
     cudaEvent_t ev_coin_done[2] = {nullptr, nullptr};
     struct CoinTag {
         bool valid = false;

@@ -657,6 +657,7 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
     // descriptors from global memory).
     __shared__ DevMerge s_m[kMaxCachedMerges];
     __shared__ uint64_t s_sbase[kMaxCachedMerges];
+    __shared__ uint32_t s_valid[kMaxCachedMerges];
     const bool cached = nm <= kMaxCachedMerges;
     auto static_base = [&](uint32_t mi, const DevMerge& m) -> uint64_t {
         const uint32_t nmerges = p.n_merges;
@@ -676,6 +677,7 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
         const DevMerge m = p.merges[mb + kb + tid];
         s_m[tid] = m;
         s_sbase[tid] = static_base(kb + tid, m);
+        s_valid[tid] = p.coin_valid ? p.coin_valid[mb + kb + tid] : 0u;
     }
     __syncthreads();
     auto merge_at = [&](uint32_t k) -> DevMerge { return cached ? s_m[k] : p.merges[mb + kb + k]; };
@@ -794,10 +796,15 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
         if (live) {
             const uint64_t sbase = cached ? s_sbase[k] : static_base(mi, m);
             // the last tile of the part knows the part's total for this merge
-            if (tid == 0 && (lt == p.part_tiles - 1 || tile + 1 == p.tiles_per_seg))
+            if (tid == 0 && (lt == p.part_tiles - 1 || tile + 1 == p.tiles_per_seg)) {
                 p.part_totals[uint64_t(p.part) * p.n_merges + mb + mi] = pre + tile_total;
+                if (p.coin_end && p.part + 1 == p.n_parts)  // the stream's end index
+                    p.coin_end[mb + mi] = sbase + pre + tile_total;
+            }
+            const uint32_t valid =
+                cached ? s_valid[k] : (p.coin_valid ? __ldcg(p.coin_valid + mb + mi) : 0u);
             const uint64_t n0 = sbase + pre + warp_off + (incl - cnt);  // my first coin's draw
-            if (n0 + cnt <= uint64_t(m.coin_words) * 32) {
+            if (n0 + cnt <= uint64_t(valid) * 32) {
                 const uint32_t* cw = p.coins + m.coin_off;
                 uint64_t n = n0;
 #pragma unroll
@@ -865,11 +872,23 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
 // unless it equals th's high word, probability 2^-32).  mix64_hi sends the
 // first xor-shift to the ALU pipe and the second through the FMA pipe, and
 // forms only the high word of the last product.
+// Adaptive budget: a merge whose stream ended at draw E last round gets its
+// coins up to E + E/16 + 4096 (capped by its buffer capacity); without a
+// history (E = ~0), coin_default words.  The merge draws anything beyond
+// coin_valid inline, so the budget changes the work, never the bits.
 __global__ void __launch_bounds__(256) coins_kernel(const DevMerge* __restrict__ merges,
                                                     uint64_t seed, uint64_t round,
+                                                    const uint64_t* __restrict__ coin_end,
+                                                    uint32_t* __restrict__ coin_valid,
                                                     uint32_t* __restrict__ coins) {
     const DevMerge m = merges[blockIdx.y];
-    const uint32_t chunks = (m.coin_words + 63) / 64;  // 64 words = 2048 draws per chunk
+    uint64_t want = m.coin_default;
+    const uint64_t e = coin_end ? coin_end[blockIdx.y] : ~0ull;
+    if (e != ~0ull) want = (e + e / 16 + 4096 + 31) / 32;
+    const uint32_t words = uint32_t(want < m.coin_words ? want : m.coin_words);
+    const uint32_t chunks = (words + 63) / 64;  // 64 words = 2048 draws per chunk
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        coin_valid[blockIdx.y] = chunks * 64 < m.coin_words ? chunks * 64 : m.coin_words;
     if (chunks == 0) return;
     const int lane = threadIdx.x & 31;
     const uint64_t key = m.key_mode ? m.key : stream_key(seed, 5, m.receiver, round, m.segment);
@@ -1392,9 +1411,11 @@ cudaError_t stream_occupancy(bool f64, int* extract_blocks, int* decode_blocks) 
 
 
 cudaError_t launch_coins(const DevMerge* merges, uint32_t n_merges, uint64_t seed, uint64_t round,
+                         const uint64_t* coin_end, uint32_t* coin_valid,
                          uint32_t* coins, int grid_x, cudaStream_t st) {
     if (n_merges == 0) return cudaSuccess;
-    coins_kernel<<<dim3(grid_x, n_merges), 256, 0, st>>>(merges, seed, round, coins);
+    coins_kernel<<<dim3(grid_x, n_merges), 256, 0, st>>>(merges, seed, round, coin_end, coin_valid,
+                                                        coins);
     return cudaGetLastError();
 }
 

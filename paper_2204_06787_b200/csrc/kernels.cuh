@@ -34,10 +34,12 @@ struct DevMerge {
     uint8_t key_mode;    // 0: derive key from (seed, round); 1: explicit `key`
     uint8_t pad_;
     uint32_t segment;    // global segment id (stream key)
-    uint32_t coin_words; // precomputed coin bits of this merge: draws [0, 32*coin_words)
+    uint32_t coin_words; // coin-buffer capacity of this merge: draws [0, 32*coin_words)
     uint64_t coin_off;   // u32-word offset of those bits in the coin buffer
+    uint32_t coin_default;  // words precomputed while the merge has no history
+    uint32_t pad2_;
 };
-static_assert(sizeof(DevMerge) == 56, "DevMerge layout");
+static_assert(sizeof(DevMerge) == 64, "DevMerge layout");
 
 
 // Cooperative merge (kernels.cu, K2): the tiles of one launch are
@@ -64,6 +66,11 @@ struct CoopParams {
     uint64_t* flags;              // [k_steps][CTAs] popcount of each tile
     uint64_t* part_totals;        // [n_parts][n_merges] draws consumed per (part, merge)
     uint64_t seed, round;
+    // adaptive coin budget: words the coin kernel computed per merge (this
+    // buffer), and the draw index each merge ended at (written by its last
+    // tile; the next round's coin kernel sizes its work from it)
+    const uint32_t* coin_valid;
+    uint64_t* coin_end;
 };
 cudaError_t launch_merge_coop(const CoopParams& p, int wpt, size_t smem, cudaStream_t st);
 cudaError_t merge_coop_occupancy(int wpt, size_t smem, int* blocks_per_sm);
@@ -107,6 +114,7 @@ cudaError_t stream_occupancy(bool f64, int* extract_blocks, int* decode_blocks);
 // (mix(key_m + (n+1)γ) < thresh11_m) for n < 32 * coin_words.  Data
 // independent, so it runs concurrently with the HBM-bound extract.
 cudaError_t launch_coins(const DevMerge* merges, uint32_t n_merges, uint64_t seed, uint64_t round,
+                         const uint64_t* coin_end, uint32_t* coin_valid,
                          uint32_t* coins, int grid_x, cudaStream_t st);
 cudaError_t launch_export_bits(const uint32_t* agg, uint32_t wst, uint64_t dim, uint64_t seg_len,
                                uint32_t* out_u32, cudaStream_t st,

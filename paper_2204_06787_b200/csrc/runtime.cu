@@ -151,6 +151,7 @@ marsit_ctx::~marsit_ctx() {
     for (int b = 0; b < 2; ++b) {
         if (ev_coin_done[b]) cudaEventDestroy(ev_coin_done[b]);
         if (coin_buf[b]) cudaFree(coin_buf[b]);
+        if (coin_valid[b]) cudaFree(coin_valid[b]);
     }
     if (aux) cudaStreamDestroy(aux);
     if (comm && owns_comm) ncclCommDestroy(comm);
@@ -279,7 +280,8 @@ marsit_status launch_coin_buffer(marsit_ctx* ctx, int b, uint64_t seed, uint64_t
     marsit_status s = ctx->begin_phase(ctx->aux, &ev);
     if (s) return s;
     CUDA_TRY(launch_coins(ctx->merge.d_merges, ctx->merge.dp.n_merges, seed, round,
-                          ctx->coin_buf[b], ctx->coin_grid_x, ctx->aux));
+                          ctx->merge.coin_end, ctx->coin_valid[b], ctx->coin_buf[b],
+                          ctx->coin_grid_x, ctx->aux));
     if ((s = ctx->end_phase(kPhCoins, ctx->aux, ev, 1))) return s;
     CUDA_TRY(cudaEventRecord(ctx->ev_coin_done[b], ctx->aux));
     ctx->coin_tag[b] = {true, seed, round};
@@ -392,7 +394,8 @@ marsit_status run_merge(marsit_ctx* ctx, uint64_t seed, uint64_t round, cudaStre
     if (s) return s;
     uint64_t n = 0;
     if ((s = ctx->merge.run(ctx->G == 1 ? ctx->bits : ctx->recv, ctx->agg,
-                            ctx->coin_buf[ctx->cur_coin], seed, round, st, &n)))
+                            ctx->coin_buf[ctx->cur_coin], seed, round, st, &n, 0, ~0u,
+                            ctx->coin_valid[ctx->cur_coin])))
         return s;
     return ctx->end_phase(kPhMerge, st, ev, n);
 }
@@ -687,9 +690,12 @@ void assign_coin_budget(DevicePlan& dp, uint32_t n_seg, uint64_t L, double frac,
             DevMerge& d = dp.merges[k];
             uint32_t depth = 0;
             for (int32_t src = d.offset_src; src >= 0; src = dp.merges[mb + src].offset_src) ++depth;
+            // capacity: every draw the stream can make (the coin kernel
+            // computes only what the last round's draw count calls for)
             const double want = frac * double(L) * (depth + 1);
-            uint64_t words = frac > 0 ? ceil_div(uint64_t(want) + 1, 32) : 0;
-            words = std::min<uint64_t>(words, ceil_div(L * (depth + 1), 32));
+            const uint64_t cap = frac > 0 ? ceil_div(L * (depth + 1), 32) : 0;
+            uint64_t words = cap;
+            d.coin_default = uint32_t(std::min<uint64_t>(cap, ceil_div(uint64_t(want) + 1, 32)));
             d.coin_words = uint32_t(words);
             d.coin_off = off;
             off += round_up(words, 64);  // whole 64-word chunks (coins_kernel)
@@ -780,7 +786,7 @@ marsit_status sign_round_impl(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_
             if ((s = ctx->begin_phase(ctx->aux, &ev))) return s;
             uint64_t nl = 0;
             if ((s = ctx->merge.run(ctx->bits, ctx->agg, ctx->coin_buf[ctx->cur_coin], seed, t,
-                                    ctx->aux, &nl, sg, 1)))
+                                    ctx->aux, &nl, sg, 1, ctx->coin_valid[ctx->cur_coin])))
                 return s;
             if ((s = ctx->end_phase(kPhMerge, ctx->aux, ev, nl))) return s;
             CUDA_TRY(cudaEventRecord(ctx->ev_merge[sg], ctx->aux));
@@ -790,7 +796,8 @@ marsit_status sign_round_impl(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_
             cudaEvent_t ev;
             if ((s = ctx->begin_phase(ctx->aux, &ev))) return s;
             CUDA_TRY(launch_coins(ctx->merge.d_merges, ctx->merge.dp.n_merges, seed, t + 1,
-                                  ctx->coin_buf[b], ctx->coin_grid_x, ctx->aux));
+                                  ctx->merge.coin_end, ctx->coin_valid[b], ctx->coin_buf[b],
+                                  ctx->coin_grid_x, ctx->aux));
             if ((s = ctx->end_phase(kPhCoins, ctx->aux, ev, 1))) return s;
             CUDA_TRY(cudaEventRecord(ctx->ev_coin_done[b], ctx->aux));
             ctx->coin_tag[b] = {true, seed, t + 1};
@@ -1050,6 +1057,8 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
     if (ctx->coin_total_words)
         for (int b = 0; b < 2; ++b) {
+            CUDA_TRY(cudaMalloc(&ctx->coin_valid[b], sizeof(uint32_t) * std::max<uint32_t>(mr.dp.n_merges, 1)));
+            CUDA_TRY(cudaMemset(ctx->coin_valid[b], 0, sizeof(uint32_t) * std::max<uint32_t>(mr.dp.n_merges, 1)));
             CUDA_TRY(cudaMalloc(&ctx->coin_buf[b], sizeof(uint32_t) * ctx->coin_total_words));
             CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_coin_done[b], cudaEventDisableTiming));
         }
