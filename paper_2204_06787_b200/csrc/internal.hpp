@@ -58,7 +58,21 @@ inline bool have_device() {
 struct DevicePlan {
     std::vector<DevMerge> merges;
     std::vector<uint32_t> seg_begin, stage_begin;
+    // [n_seg][n_stages][kMaxLanes+1] merge offsets (within the segment) of
+    // each lane; n_lanes[stage] = lanes of the stage (max over segments)
+    std::vector<uint32_t> lane_begin, n_lanes;
     uint32_t max_slots = 0, gmax = 0, n_stages = 1, n_merges = 0;
+    // one lane per stage (plans built without the lane analysis)
+    void single_lanes() {
+        const size_t n_seg = seg_begin.size();
+        lane_begin.assign(n_seg * n_stages * (kMaxLanes + 1), 0);
+        n_lanes.assign(n_stages, 1);
+        for (size_t sl = 0; sl < n_seg; ++sl)
+            for (uint32_t st = 0; st < n_stages; ++st)
+                for (uint32_t ln = 0; ln <= kMaxLanes; ++ln)
+                    lane_begin[(sl * n_stages + st) * (kMaxLanes + 1) + ln] =
+                        stage_begin[sl * (n_stages + 1) + st + (ln > 0 ? 1 : 0)];
+    }
 };
 
 // Lower the owned segments' merge DAGs into the device plan (runtime.cu).
@@ -78,7 +92,8 @@ struct MergeRunner {
     std::vector<uint32_t> k_steps;  // per stage: max merges over segments
     DevMerge* d_merges = nullptr;
     uint32_t* d_seg_begin = nullptr;
-    uint32_t* d_stage_begin = nullptr;
+    uint32_t* d_stage_begin = nullptr;  // the lane table (DevicePlan::lane_begin)
+    uint32_t lanes_max = 1;
     uint32_t* gnodes = nullptr;
     uint64_t* flags = nullptr;  // [kmax][seg_per_launch * part_tiles]
     uint64_t* part_totals = nullptr;
@@ -96,14 +111,34 @@ struct MergeRunner {
 
     // seg_launch: owned segments per launch (1: per-segment pipeline);
     // cta_limit: CTAs per SM left to the merge (0: all it can get).
+    // Lanes (independent chains side by side) halve the barrier steps of a
+    // torus stage but multiply the tiles of a launch; when that costs extra
+    // launches (one GPU, many segments: the tiles no longer fit one
+    // co-resident grid) the stages run as single lanes instead.
     marsit_status configure(int sm_count, uint32_t seg_launch = 0, int cta_limit = 0) {
+        marsit_status s = configure_once(sm_count, seg_launch, cta_limit);
+        if (s || lanes_max == 1 || n_parts == 1) return s;
+        const uint32_t parts_lanes = n_parts;
+        DevicePlan keep = dp;
+        dp.single_lanes();
+        if ((s = configure_once(sm_count, seg_launch, cta_limit))) return s;
+        if (n_parts < parts_lanes) return MARSIT_OK;
+        dp = keep;
+        return configure_once(sm_count, seg_launch, cta_limit);
+    }
+
+    marsit_status configure_once(int sm_count, uint32_t seg_launch, int cta_limit) {
         seg_per_launch = seg_launch ? seg_launch : n_seg;
         k_steps.assign(dp.n_stages, 0);
+        lanes_max = 1;
+        for (uint32_t st = 0; st < dp.n_stages; ++st) lanes_max = std::max(lanes_max, dp.n_lanes[st]);
         for (uint32_t sl = 0; sl < n_seg; ++sl)
             for (uint32_t st = 0; st < dp.n_stages; ++st) {
-                const uint32_t* sb = &dp.stage_begin[size_t(sl) * (dp.n_stages + 1)];
-                k_steps[st] = std::max(k_steps[st], sb[st + 1] - sb[st]);
+                const uint32_t* lb = &dp.lane_begin[(size_t(sl) * dp.n_stages + st) * (kMaxLanes + 1)];
+                for (uint32_t ln = 0; ln < kMaxLanes; ++ln)
+                    k_steps[st] = std::max(k_steps[st], lb[ln + 1] - lb[ln]);
             }
+        const uint64_t vsegs = uint64_t(seg_per_launch) * lanes_max;  // tile sets per launch
         // Tiling (measured on B200, tools/sweep_merge_balance.sh, merge alone):
         // fewest launches ("parts") first, then the lowest estimated step cost
         //   cost = WPT * (k + 1) + 6 * [k >= 3],   k = CTAs on the busiest SM.
@@ -129,20 +164,20 @@ struct MergeRunner {
             const uint64_t gran = std::max(w, 4);  // a thread's words never straddle tiles
             const uint64_t tps_min = ceil_div(words_proc, tw_max);
             uint64_t tps = tps_min, tw = round_up(ceil_div(words_proc, tps), gran);
-            if (balance > 0 && balance <= occ && (uint64_t(balance) * sm_count) % seg_per_launch == 0) {
+            if (balance > 0 && balance <= occ && (uint64_t(balance) * sm_count) % vsegs == 0) {
                 // exactly `balance` CTAs on every SM; trailing tiles may be
                 // empty: they only take part in the barriers
-                const uint64_t t = uint64_t(balance) * sm_count / seg_per_launch;
+                const uint64_t t = uint64_t(balance) * sm_count / vsegs;
                 const uint64_t tww = round_up(ceil_div(words_proc, t), gran);
                 if (t >= tps_min && tww <= tw_max) {
                     tps = t;
                     tw = tww;
                 }
             }
-            const uint64_t pt = std::min<uint64_t>(tps, cap / seg_per_launch);
+            const uint64_t pt = std::min<uint64_t>(tps, cap / vsegs);
             if (pt == 0) continue;
             const uint64_t parts = ceil_div(tps, pt);
-            const uint64_t ctas = pt * seg_per_launch;
+            const uint64_t ctas = pt * vsegs;
             const uint64_t k = ceil_div(ctas, uint64_t(sm_count));
             const uint64_t cost = uint64_t(w) * (k + 1) + (k >= 3 ? 6 : 0);
             if (parts < best_parts || (parts == best_parts && cost < best_cost)) {
@@ -168,14 +203,14 @@ struct MergeRunner {
         CUDA_TRY(cudaMalloc(&d_seg_begin, sizeof(uint32_t) * dp.seg_begin.size()));
         CUDA_TRY(cudaMemcpy(d_seg_begin, dp.seg_begin.data(), sizeof(uint32_t) * dp.seg_begin.size(),
                             cudaMemcpyHostToDevice));
-        CUDA_TRY(cudaMalloc(&d_stage_begin, sizeof(uint32_t) * dp.stage_begin.size()));
-        CUDA_TRY(cudaMemcpy(d_stage_begin, dp.stage_begin.data(),
-                            sizeof(uint32_t) * dp.stage_begin.size(), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMalloc(&d_stage_begin, sizeof(uint32_t) * dp.lane_begin.size()));
+        CUDA_TRY(cudaMemcpy(d_stage_begin, dp.lane_begin.data(),
+                            sizeof(uint32_t) * dp.lane_begin.size(), cudaMemcpyHostToDevice));
         const uint32_t gmax = std::max<uint32_t>(dp.gmax, 1);
         CUDA_TRY(cudaMalloc(&gnodes, sizeof(uint32_t) * size_t(n_seg) * gmax * wst));
         uint32_t kmax = 1;
         for (uint32_t k : k_steps) kmax = std::max(kmax, k);
-        const size_t nflags = size_t(kmax) * seg_per_launch * part_tiles;
+        const size_t nflags = size_t(kmax) * seg_per_launch * lanes_max * part_tiles;
         CUDA_TRY(cudaMalloc(&flags, sizeof(uint64_t) * nflags));
         CUDA_TRY(cudaMemset(flags, 0, sizeof(uint64_t) * nflags));
         CUDA_TRY(cudaMalloc(&part_totals, sizeof(uint64_t) * size_t(n_parts) * nm));
@@ -194,7 +229,7 @@ struct MergeRunner {
         CoopParams c{};
         c.merges = d_merges;
         c.seg_begin = d_seg_begin;
-        c.stage_begin = d_stage_begin;
+        c.lane_begin = d_stage_begin;
         c.n_stages = dp.n_stages;
         c.n_seg = n_seg;
         c.s_first = s_first;
@@ -227,6 +262,7 @@ struct MergeRunner {
                 if (k_steps[stage] == 0) continue;
                 c.stage = stage;
                 c.k_steps = k_steps[stage];
+                c.n_lanes = dp.n_lanes[stage];
                 for (uint32_t part = 0; part < n_parts; ++part) {
                     c.part = part;
                     c.part_tile0 = part * part_tiles;

@@ -634,7 +634,8 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
     __shared__ uint64_t s_acc[kMergeThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t T = gridDim.x;  // CTAs in this launch
-    const uint32_t sl = p.seg_lo + blockIdx.x / p.part_tiles, lt = blockIdx.x % p.part_tiles;
+    const uint32_t vs = blockIdx.x / p.part_tiles, lt = blockIdx.x % p.part_tiles;
+    const uint32_t sl = p.seg_lo + vs / p.n_lanes, chain = vs % p.n_lanes;
     const uint32_t tile = p.part_tile0 + lt;
     // a tile is tile_words (<= 256 * WPT, multiple of 4) consecutive words
     const uint32_t w0 = tile * p.tile_words + tid * WPT;
@@ -646,8 +647,9 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
         return rem >= 32 ? kFull : (rem <= 0 ? 0u : ((1u << rem) - 1u));
     };
     const uint32_t mb = p.seg_begin[sl];
-    const uint32_t kb = p.stage_begin[sl * (p.n_stages + 1) + p.stage];
-    const uint32_t nm = p.stage_begin[sl * (p.n_stages + 1) + p.stage + 1] - kb;
+    const uint32_t* lb = p.lane_begin + (size_t(sl) * p.n_stages + p.stage) * (kMaxLanes + 1) + chain;
+    const uint32_t kb = lb[0];
+    const uint32_t nm = lb[1] - kb;
     const uint32_t sg = p.s_first + sl;
     // The stage's merge descriptors and the data-independent part of each
     // merge's draw base (draws before this round + earlier launch parts +
@@ -1351,7 +1353,7 @@ static cudaError_t coop_launch_t(const CoopParams& p, size_t smem, cudaStream_t 
     CoopParams q = p;
     void* args[] = {&q};
     return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(merge_coop_kernel<WPT>),
-                                       dim3(p.seg_cnt * p.part_tiles), dim3(kMergeThreads), args,
+                                       dim3(p.seg_cnt * p.n_lanes * p.part_tiles), dim3(kMergeThreads), args,
                                        smem, st);
 }
 

@@ -10,7 +10,8 @@ namespace marsit_b200 {
 constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ull;  // rng.hpp:64
 constexpr uint32_t kMaxLocalWorkers = 64;           // workers resident on one rank
 constexpr int kMaxCachedMerges = 32;                // merge descriptors staged in smem per stage
-constexpr int kMergeThreads = 256;                   // 8 warps; a warp tile is 32 x WPT packed
+constexpr int kMergeThreads = 256;
+constexpr uint32_t kMaxLanes = 8;                   // independent chains per stage run side by side                   // 8 warps; a warp tile is 32 x WPT packed
                                                      // words, WPT in {1, 2} chosen per context
 constexpr int kStreamThreads = 256;                  // sign_extract / decode
 constexpr int kTaskWords = 16;                       // u32 words per warp task (512 elements)
@@ -47,8 +48,12 @@ static_assert(sizeof(DevMerge) == 64, "DevMerge layout");
 struct CoopParams {
     const DevMerge* merges;       // owned segments' merges, stage-sorted per segment
     const uint32_t* seg_begin;    // [n_seg] first merge of each owned segment
-    const uint32_t* stage_begin;  // [n_seg][n_stages+1] merge ranges per stage
-    uint32_t n_stages, stage, k_steps;  // k_steps: max merges of this stage over segments
+    // merge ranges per (segment, stage, lane): [n_seg][n_stages][kMaxLanes+1];
+    // a lane is an independent chain of the stage (torus: one per row), run
+    // by its own tiles, so independent chains share the grid barriers
+    const uint32_t* lane_begin;
+    uint32_t n_stages, stage, k_steps;  // k_steps: max merges of a lane of this stage
+    uint32_t n_lanes;             // lanes of this stage (grid = seg_cnt x n_lanes x part_tiles)
     uint32_t n_seg, s_first, tiles_per_seg, words_proc, wst, ml, max_slots;
     uint32_t tile_words;          // words per tile (<= 256 * WPT, multiple of max(WPT, 4))
     uint32_t part, n_parts, part_tile0, part_tiles;  // tiles of each segment in this launch

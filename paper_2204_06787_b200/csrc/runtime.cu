@@ -16,6 +16,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -50,14 +51,41 @@ marsit_status lower_plan(const Plan& plan, uint32_t s_first, uint32_t n_seg, Dev
     dp.n_stages = plan.n_stages;
     dp.seg_begin.resize(n_seg);
     dp.stage_begin.assign(size_t(n_seg) * (plan.n_stages + 1), 0);
+    dp.lane_begin.assign(size_t(n_seg) * plan.n_stages * (kMaxLanes + 1), 0);
+    dp.n_lanes.assign(plan.n_stages, 1);
+    const bool lanes = env_int("MARSIT_MERGE_LANES", 1) != 0;
     for (uint32_t sl = 0; sl < n_seg; ++sl) {
         const SegmentPlan& sp = plan.seg[s_first + sl];
         const size_t n = sp.merges.size();
         if (sp.final_node < W) return fail(MARSIT_EUNSUPPORTED, "schedule performs no reduction");
+        // lanes: the connected components of each stage's same-stage
+        // dependencies (torus: one row chain each), numbered by first
+        // appearance; MARSIT_MERGE_LANES=0 keeps one lane per stage
+        std::vector<uint32_t> root(n), lane(n, 0);
+        for (size_t k = 0; k < n; ++k) root[k] = uint32_t(k);
+        std::function<uint32_t(uint32_t)> find = [&](uint32_t x) {
+            return root[x] == x ? x : (root[x] = find(root[x]));
+        };
+        for (size_t k = 0; k < n; ++k)
+            for (uint32_t in : {sp.merges[k].recv_node, sp.merges[k].local_node})
+                if (in >= W && sp.merges[in - W].stage == sp.merges[k].stage)
+                    root[find(uint32_t(k))] = find(in - W);
+        if (lanes) {
+            std::vector<int> lane_of_root(n, -1);
+            std::vector<uint32_t> next_lane(plan.n_stages, 0);
+            for (size_t k = 0; k < n; ++k) {
+                const uint32_t rt = find(uint32_t(k));
+                if (lane_of_root[rt] < 0)
+                    lane_of_root[rt] = int(std::min(next_lane[sp.merges[k].stage]++, kMaxLanes - 1));
+                lane[k] = uint32_t(lane_of_root[rt]);
+            }
+        }
         std::vector<uint32_t> order(n);
         for (size_t k = 0; k < n; ++k) order[k] = uint32_t(k);
         std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
-            return sp.merges[a].stage < sp.merges[b].stage;
+            if (sp.merges[a].stage != sp.merges[b].stage)
+                return sp.merges[a].stage < sp.merges[b].stage;
+            return lane[a] < lane[b];
         });
         std::vector<uint32_t> pos(n);  // schedule index -> execution index
         for (size_t e = 0; e < n; ++e) pos[order[e]] = uint32_t(e);
@@ -124,6 +152,17 @@ marsit_status lower_plan(const Plan& plan, uint32_t s_first, uint32_t n_seg, Dev
                 if (sp.merges[order[e]].stage < st) ++c;
             dp.stage_begin[size_t(sl) * (plan.n_stages + 1) + st] = c;
         }
+        for (uint32_t st = 0; st < plan.n_stages; ++st)
+            for (uint32_t ln = 0; ln <= kMaxLanes; ++ln) {
+                uint32_t c = 0, used = 0;
+                for (size_t e = 0; e < n; ++e) {
+                    const MergeNode& m = sp.merges[order[e]];
+                    if (m.stage < st || (m.stage == st && lane[order[e]] < ln)) ++c;
+                    if (m.stage == st) used = std::max(used, lane[order[e]] + 1);
+                }
+                dp.lane_begin[(size_t(sl) * plan.n_stages + st) * (kMaxLanes + 1) + ln] = c;
+                dp.n_lanes[st] = std::max(dp.n_lanes[st], used);
+            }
         if (slot_busy.size() > 64 || gnext > 0x3FFF)
             return fail(MARSIT_EUNSUPPORTED, "merge plan too large");
     }
@@ -1335,6 +1374,7 @@ marsit_status marsit_merge_signs(const uint64_t* d_recv, uint32_t c_recv, const 
     mr.dp.seg_begin = {0};
     mr.dp.stage_begin = {0, 1};
     mr.dp.n_stages = 1;
+    mr.dp.single_lanes();
     mr.dp.n_merges = 1;
     marsit_status s;
     if ((s = mr.configure(sm)) || (s = mr.upload())) return s;

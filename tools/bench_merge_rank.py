@@ -35,14 +35,18 @@ class _H:
 recv = torch.as_tensor(_H(), device="cuda")
 recv.copy_(torch.randint(-2**62, 2**62, recv.shape, device="cuda"))
 D = args.dim
-g = [torch.empty(D, device="cuda") for _ in range(ml)]
+g = [torch.zeros(D, device="cuda") for _ in range(ml)]
 c = [torch.zeros(D, device="cuda") for _ in range(ml)]
+# phase 0 first every round: it computes the round's coins (adaptive budget:
+# the coin kernel sizes each merge's coins from the previous merge)
 for t in range(1, 4):
+    ctx.round_phase(0, t, None, 2 ** -10, 7, g, c)
     ctx.round_phase(1, t, None, 2 ** -10, 7, g, c)
 torch.cuda.synchronize()
 ctx.set_timing(True)
 ctx.timing(reset=True)
 for t in range(4, 4 + args.iters):
+    ctx.round_phase(0, t, None, 2 ** -10, 7, g, c)
     ctx.round_phase(1, t, None, 2 ** -10, 7, g, c)
 torch.cuda.synchronize()
 ms, n = ctx.timing(reset=True)["merge"]

@@ -15,11 +15,13 @@ def run(G, D):
     recv = torch.as_tensor(_H(), device="cuda")
     recv.copy_(torch.randint(-2**62, 2**62, recv.shape, device="cuda"))
     ml = 8 // G
-    g = [torch.empty(D, device="cuda") for _ in range(ml)]
+    g = [torch.zeros(D, device="cuda") for _ in range(ml)]
     c = [torch.zeros(D, device="cuda") for _ in range(ml)]
-    for t in range(1, 4): ctx.round_phase(1, t, None, 2**-10, 7, g, c)
+    for t in range(1, 4):
+        ctx.round_phase(0, t, None, 2**-10, 7, g, c); ctx.round_phase(1, t, None, 2**-10, 7, g, c)
     torch.cuda.synchronize(); L.marsit_debug_coop_prof(buf, 1)
-    for t in range(4, 14): ctx.round_phase(1, t, None, 2**-10, 7, g, c)
+    for t in range(4, 14):
+        ctx.round_phase(0, t, None, 2**-10, 7, g, c); ctx.round_phase(1, t, None, 2**-10, 7, g, c)
     torch.cuda.synchronize(); L.marsit_debug_coop_prof(buf, 1)
     n = buf[4]
     print(f"G={G} D={D}: steps {n}  avg ns: load+scan {buf[0]/n:.0f}  grid.sync {buf[1]/n:.0f}  "
