@@ -319,6 +319,7 @@ struct marsit_ctx {
     int stream_grid = 0;   // generic grid-stride kernels
     int extract_grid = 0;  // persistent, one wave of resident CTAs
     int decode_grid = 0;
+    int stats_grid = 0;   // decode with the fused matching count (metrics on)
     // dense round scratch
     void* dense_send = nullptr;  // [G][s_own][ml][L] of dtype
     void* dense_recv = nullptr;
