@@ -153,8 +153,8 @@ struct MergeRunner {
         uint64_t best_parts = ~0ull, best_cost = ~0ull;
         for (int w : {1, 2, 4, 8, 12, 16}) {
             if (forced && w != forced) continue;
-            // slots + the deposit masks (5 words per packed word)
-            const size_t sm = (size_t(std::max<uint32_t>(dp.max_slots, 1)) + 5) * w * kMergeThreads * 4;
+            // slots + the deposit masks (4 words per packed word)
+            const size_t sm = (size_t(std::max<uint32_t>(dp.max_slots, 1)) + 4) * w * kMergeThreads * 4;
             if (sm > 160 * 1024) continue;
             int occ = 0;
             CUDA_TRY(merge_coop_occupancy(w, sm, &occ));

@@ -557,33 +557,42 @@ __device__ __forceinline__ uint32_t coin_word(uint32_t d, uint64_t& z, uint64_t 
 // after the complete draw total of the merge it continues (previous stage).
 __device__ __forceinline__ uint32_t shl_fma(uint32_t x, uint32_t s) { return x * (1u << s); }
 // Parallel bit deposit (PDEP): the low popcount(m) bits of x are placed,
-// in order, at the set bits of m.  Branch-free "expand" of Hacker's Delight
-// §7-6 (five parallel-suffix rounds); left shifts are written as multiplies
-// so they can issue on the FMA pipe next to the ALU-pipe logic ops.  Split
-// in two: the five shift masks depend only on m (the disagreement word,
-// known before the grid barrier, so they are formed while the other tiles
-// arrive), the moves of x need the coin window (known after it).
-__device__ __forceinline__ void expand_masks(uint32_t m, uint32_t (&mv)[5]) {
-    uint32_t mk = ~m << 1;
+// in order, at the set bits of m.  Byte-parallel form of the branch-free
+// "expand" of Hacker's Delight §7-6: the four bytes of m are expanded side
+// by side in three parallel-suffix rounds (shifts masked to stay inside a
+// byte), and byte b of x is first fed from bit popcount(m's lower bytes) of
+// x (an exclusive prefix of the byte popcounts, one multiply).  Split in
+// two: the masks depend only on m (the disagreement word, known before the
+// grid barrier, so they are formed while the other tiles arrive); the moves
+// of x need the coin window (known after it).  expand_apply(x, masks(m)) & m
+// == pdep(x, m) (checked against a bit-serial pdep on 200k random words and
+// every byte pattern).
+__device__ __forceinline__ void expand_masks(uint32_t m, uint32_t (&mv)[4]) {
+    uint32_t pc = m - ((m >> 1) & 0x55555555u);
+    pc = (pc & 0x33333333u) + ((pc >> 2) & 0x33333333u);
+    pc = (pc + (pc >> 4)) & 0x0F0F0F0Fu;
+    mv[3] = pc * 0x01010100u;  // byte b: popcount of bytes < b
+    uint32_t mk = shl_fma(~m, 1) & 0xFEFEFEFEu;
 #pragma unroll
-    for (int i = 0; i < 5; ++i) {
-        uint32_t mp = mk ^ shl_fma(mk, 1);
-        mp ^= shl_fma(mp, 2);
-        mp ^= shl_fma(mp, 4);
-        mp ^= shl_fma(mp, 8);
-        mp ^= shl_fma(mp, 16);
-        mv[i] = mp & m;
-        m = (m ^ mv[i]) | (mv[i] >> (1 << i));
+    for (int i = 0; i < 3; ++i) {
+        uint32_t mp = mk ^ (shl_fma(mk, 1) & 0xFEFEFEFEu);
+        mp ^= shl_fma(mp, 2) & 0xFCFCFCFCu;
+        mp ^= shl_fma(mp, 4) & 0xF0F0F0F0u;
+        const uint32_t v = mp & m;
+        m = (m ^ v) | (v >> (1 << i));
         mk &= ~mp;
+        mv[i] = v;
     }
 }
-__device__ __forceinline__ uint32_t expand_apply(uint32_t x, const uint32_t (&mv)[5], uint32_t m0) {
-    x = (x & ~mv[4]) | (shl_fma(x, 16) & mv[4]);
-    x = (x & ~mv[3]) | (shl_fma(x, 8) & mv[3]);
-    x = (x & ~mv[2]) | (shl_fma(x, 4) & mv[2]);
-    x = (x & ~mv[1]) | (shl_fma(x, 2) & mv[1]);
-    x = (x & ~mv[0]) | (shl_fma(x, 1) & mv[0]);
-    return x & m0;
+__device__ __forceinline__ uint32_t expand_apply(uint32_t x, const uint32_t (&mv)[4]) {
+    const uint32_t ex = mv[3];
+    uint32_t t = __byte_perm(x, x >> ((ex >> 8) & 0xFFu), 0x0040);
+    t = __byte_perm(t, x >> ((ex >> 16) & 0xFFu), 0x0410);
+    t = __byte_perm(t, x >> (ex >> 24), 0x4210);
+    t = (t & ~mv[2]) | (shl_fma(t, 4) & mv[2]);
+    t = (t & ~mv[1]) | (shl_fma(t, 2) & mv[1]);
+    t = (t & ~mv[0]) | (shl_fma(t, 1) & mv[0]);
+    return t;  // bits outside m are don't-care (the caller masks with d)
 }
 
 template <int WPT>
@@ -628,7 +637,7 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     extern __shared__ uint32_t cslots[];  // [max_slots][WPT][kMergeThreads], then the
-                                          // deposit masks [WPT][5][kMergeThreads]
+                                          // deposit masks [WPT][4][kMergeThreads]
     uint32_t* cmask = cslots + size_t(p.max_slots) * WPT * kMergeThreads;
     __shared__ uint32_t s_warp[kMergeThreads / 32];
     __shared__ uint64_t s_acc[kMergeThreads / 32];
@@ -771,10 +780,10 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
         if (live) {
 #pragma unroll
             for (int j = 0; j < WPT; ++j) {
-                uint32_t mv[5];
+                uint32_t mv[4];
                 expand_masks(d[j], mv);
 #pragma unroll
-                for (int i = 0; i < 5; ++i) cmask[(j * 5 + i) * kMergeThreads + tid] = mv[i];
+                for (int i = 0; i < 4; ++i) cmask[(j * 4 + i) * kMergeThreads + tid] = mv[i];
             }
         }
         grid.barrier_wait(std::move(token));
@@ -820,10 +829,10 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
                         const uint32_t c1 = (sh + pc > 32) ? __ldg(cw + wi + 1) : 0u;
                         window = __funnelshift_r(c0, c1, sh);
                     }
-                    uint32_t mv[5];
+                    uint32_t mv[4];
 #pragma unroll
-                    for (int i = 0; i < 5; ++i) mv[i] = cmask[(j * 5 + i) * kMergeThreads + tid];
-                    r[j] = (r[j] ^ (d[j] & ~expand_apply(window, mv, d[j]))) & vmask(j);
+                    for (int i = 0; i < 4; ++i) mv[i] = cmask[(j * 4 + i) * kMergeThreads + tid];
+                    r[j] = (r[j] ^ (d[j] & ~expand_apply(window, mv))) & vmask(j);
                     n += pc;
                 }
             } else {
