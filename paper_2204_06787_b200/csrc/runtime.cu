@@ -1125,8 +1125,10 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
         // (tools/sweep_stream_ctas.sh, tools/ab_extract_ctas.sh).
         int ob_extract = 0, ob_decode = 0;
         CUDA_TRY(stream_occupancy(ctx->dtype == MARSIT_F64, &ob_extract, &ob_decode));
+        // fp64: one decode CTA per SM leaves the coin prefetch room (C3 fp64
+        // round 1420 -> 1334 us; at 2 the coins starve underneath the decode)
         const int want_e = env_int("MARSIT_EXTRACT_CTAS", 3);
-        const int want_d = env_int("MARSIT_DECODE_CTAS", 2);
+        const int want_d = env_int("MARSIT_DECODE_CTAS", ctx->dtype == MARSIT_F64 ? 1 : 2);
         ctx->extract_grid = std::max(1, std::min(ob_extract, want_e)) * ctx->sm_count;
         ctx->decode_grid = std::max(1, std::min(ob_decode, want_d)) * ctx->sm_count;
         // metrics on: the worker-inner decode keeps fewer loads in flight per
