@@ -4,6 +4,8 @@ thousand incl. D < M and 64-bit word boundaries, fp64 Gaussian inputs with
 zeros / -0.0 / subnormals, fp32 dyadic (fp32-exact) inputs, dense cadence,
 compensation carried over 3 rounds.  Bit-exact: aggregate bits, update and
 compensation."""
+import os
+
 import numpy as np
 import pytest
 
@@ -48,7 +50,8 @@ def inputs(rng, f64, M, D, seed, t):
     return g
 
 
-@pytest.mark.parametrize("case", range(32))
+# MARSIT_FUZZ_CASES widens the sweep (e.g. 1000 for a soak run on the GPU box)
+@pytest.mark.parametrize("case", range(int(os.environ.get("MARSIT_FUZZ_CASES", "32"))))
 def test_fuzz_rounds_vs_oracle(case):
     rng, topo, a, b, M, D, f64, period, eta = draw_case(7000 + case)
     sched = mb.build_ring_schedule(a) if topo == "ring" else mb.build_torus_schedule(a, b)
