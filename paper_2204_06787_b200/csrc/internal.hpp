@@ -98,6 +98,8 @@ struct MergeRunner {
     uint64_t* flags = nullptr;  // [kmax][seg_per_launch * part_tiles]
     uint64_t* part_totals = nullptr;
     uint64_t* coin_end = nullptr;  // [n_merges] last round's end draw index per merge (~0: none)
+    unsigned* seg_bars = nullptr;  // per-(segment, lane) barrier words (MARSIT_SEG_BARRIER)
+    bool seg_barrier = env_int("MARSIT_SEG_BARRIER", 1) != 0;
     const uint32_t* const* peer_bits = nullptr;  // P2P transport: device table [G]
 
     MergeRunner() = default;
@@ -105,7 +107,7 @@ struct MergeRunner {
     MergeRunner& operator=(const MergeRunner&) = delete;
     ~MergeRunner() {
         for (void* p : {(void*)d_merges, (void*)d_seg_begin, (void*)d_stage_begin, (void*)gnodes,
-                        (void*)flags, (void*)part_totals, (void*)coin_end})
+                        (void*)flags, (void*)part_totals, (void*)coin_end, (void*)seg_bars})
             if (p) cudaFree(p);
     }
 
@@ -215,6 +217,8 @@ struct MergeRunner {
         CUDA_TRY(cudaMemset(flags, 0, sizeof(uint64_t) * nflags));
         CUDA_TRY(cudaMalloc(&part_totals, sizeof(uint64_t) * size_t(n_parts) * nm));
         CUDA_TRY(cudaMemset(part_totals, 0, sizeof(uint64_t) * size_t(n_parts) * nm));
+        CUDA_TRY(cudaMalloc(&seg_bars, sizeof(unsigned) * size_t(seg_per_launch) * lanes_max));
+        CUDA_TRY(cudaMemset(seg_bars, 0, sizeof(unsigned) * size_t(seg_per_launch) * lanes_max));
         CUDA_TRY(cudaMalloc(&coin_end, sizeof(uint64_t) * nm));
         CUDA_TRY(cudaMemset(coin_end, 0xFF, sizeof(uint64_t) * nm));  // no history yet
         return MARSIT_OK;
@@ -255,6 +259,7 @@ struct MergeRunner {
         c.round = round;
         c.coin_valid = coins ? coin_valid : nullptr;
         c.coin_end = coin_end;
+        c.seg_bars = seg_barrier ? seg_bars : nullptr;
         for (uint32_t s0 = seg_lo; s0 < seg_lo + seg_cnt; s0 += seg_per_launch) {
             c.seg_lo = s0;
             c.seg_cnt = std::min(seg_per_launch, seg_lo + seg_cnt - s0);

@@ -631,6 +631,29 @@ __device__ __forceinline__ uint64_t gtime_ns() {
 #define COOP_ADD(i, x)
 #endif
 
+// Barrier over the n co-resident CTAs of one segment (the sense-reversing
+// counter of cooperative groups' grid barrier on a per-segment word: the
+// master adds 2^31 - (n - 1), the others 1, so every barrier flips bit 31
+// and leaves the low bits at 0 for the next one).
+__device__ __forceinline__ unsigned seg_barrier_arrive(unsigned* bar, bool master, unsigned n) {
+    __syncthreads();
+    unsigned old = 0;
+    if (threadIdx.x == 0) {
+        const unsigned nb = master ? 0x80000000u - (n - 1) : 1u;
+        asm volatile("atom.add.release.gpu.u32 %0,[%1],%2;" : "=r"(old) : "l"(bar), "r"(nb) : "memory");
+    }
+    return old;
+}
+__device__ __forceinline__ void seg_barrier_wait(unsigned* bar, unsigned old) {
+    if (threadIdx.x == 0) {
+        unsigned cur;
+        do {
+            asm volatile("ld.acquire.gpu.u32 %0,[%1];" : "=r"(cur) : "l"(bar) : "memory");
+        } while (((old ^ cur) & 0x80000000u) == 0);
+    }
+    __syncthreads();
+}
+
 template <int WPT>
 __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 : 4))
     merge_coop_kernel(const CoopParams p) {
@@ -774,9 +797,16 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
         if (tid == 0) __stcg(reinterpret_cast<unsigned long long*>(flags + blockIdx.x),
                              (unsigned long long)tile_total);
         COOP_T(t1);
-        // split grid barrier: the deposit masks of r ^ l are formed while the
-        // other tiles arrive (they need d only, not the draw base)
-        auto token = grid.barrier_arrive();
+        // split barrier: the deposit masks of r ^ l are formed while the
+        // other tiles arrive (they need d only, not the draw base).  With
+        // p.seg_bars the barrier spans only this segment's tiles (its own
+        // counter; the prefix never reads another segment's counts).
+        unsigned seg_tok = 0;
+        cg::grid_group::arrival_token token{};
+        if (p.seg_bars)
+            seg_tok = seg_barrier_arrive(p.seg_bars + blockIdx.x / p.part_tiles, lt == 0, p.part_tiles);
+        else
+            token = grid.barrier_arrive();
         if (live) {
 #pragma unroll
             for (int j = 0; j < WPT; ++j) {
@@ -786,7 +816,10 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
                 for (int i = 0; i < 4; ++i) cmask[(j * 4 + i) * kMergeThreads + tid] = mv[i];
             }
         }
-        grid.barrier_wait(std::move(token));
+        if (p.seg_bars)
+            seg_barrier_wait(p.seg_bars + blockIdx.x / p.part_tiles, seg_tok);
+        else
+            grid.barrier_wait(std::move(token));
         // exclusive draw offset: the counts of this segment's earlier tiles in
         // this launch, read block-wide (all loads in flight at once)
         const uint32_t seg_base = blockIdx.x - lt;

@@ -76,6 +76,7 @@ struct CoopParams {
     // tile; the next round's coin kernel sizes its work from it)
     const uint32_t* coin_valid;
     uint64_t* coin_end;
+    unsigned* seg_bars;           // per-segment barrier counters [seg_cnt x n_lanes] or null (grid barrier)
 };
 cudaError_t launch_merge_coop(const CoopParams& p, int wpt, size_t smem, cudaStream_t st);
 cudaError_t merge_coop_occupancy(int wpt, size_t smem, int* blocks_per_sm);
