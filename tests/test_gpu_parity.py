@@ -427,3 +427,37 @@ def test_large_worker_counts_vs_oracle(topo, a, b, D, period):
         assert np.array_equal(np.stack([c.double().cpu().numpy() for c in comp]), r.comp)
         comp_o = r.comp
     ctx.check()
+
+
+@pytest.mark.parametrize("frac", ["0.53", "0.2"])
+def test_adaptive_coin_budget_over_rounds_vs_oracle(frac, monkeypatch):
+    """Error feedback with a fixed Gaussian gradient drives the disagreement
+    rate above 1/2 over rounds; the coin kernel sizes each merge's coins from
+    the previous round's end index (first round: MARSIT_COIN_FRAC), and every
+    draw beyond them is taken inline — bit-exact against the oracle either
+    way, for 8 rounds (fp64, ring 8 and torus 2x4, ragged L)."""
+    monkeypatch.setenv("MARSIT_COIN_FRAC", frac)
+    for topo, a, b in (("ring", 8, 0), ("torus", 2, 4)):
+        D = 300_007
+        sched = sched_of(topo, a, b)
+        T = O.schedule(topo, a, b)
+        W, seed = sched.workers, 31
+        rng = np.random.default_rng(5)
+        g = rng.standard_normal((W, D)) * 1e-3
+        gd = [torch.tensor(x, dtype=torch.float64, device=DEV) for x in g]
+        ctx = mb.Context(D, sched, torch.float64, 0)
+        comp = [torch.zeros(D, dtype=torch.float64, device=DEV) for _ in range(W)]
+        comp_o = np.zeros((W, D))
+        ctx.set_metrics(True)
+        rates = []
+        for t in range(1, 9):
+            agg = torch.empty((D + 63) // 64, dtype=torch.int64, device=DEV)
+            ctx.sign_round(t, ETA, seed, gd, comp, agg_bits=agg)
+            rates.append(ctx.metrics().disagreement_rate)
+            r = O.marsit_round(T, t, None, ETA, g, comp_o, seed)
+            assert u64(agg).tolist() == r.agg_bits.tolist(), (topo, t)
+            got = np.stack([c.cpu().numpy() for c in comp])
+            assert np.array_equal(got, r.comp), (topo, t)
+            comp_o = r.comp
+        assert max(rates) > 0.5  # the drift the adaptive budget follows
+        ctx.check()
