@@ -1127,7 +1127,10 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
         CUDA_TRY(stream_occupancy(ctx->dtype == MARSIT_F64, &ob_extract, &ob_decode));
         // fp64: one decode CTA per SM leaves the coin prefetch room (C3 fp64
         // round 1420 -> 1334 us; at 2 the coins starve underneath the decode)
-        const int want_e = env_int("MARSIT_EXTRACT_CTAS", 3);
+        // short extracts (a G = 8 rank reads 205 MB) lose less to their tail
+        // with 4 CTAs/SM (34.0 -> 32.5 us); long ones run best at 3
+        const uint64_t ext_bytes = uint64_t(ctx->ml) * ctx->D * ctx->esize * 2;
+        const int want_e = env_int("MARSIT_EXTRACT_CTAS", ext_bytes < (512ull << 20) ? 4 : 3);
         const int want_d = env_int("MARSIT_DECODE_CTAS", ctx->dtype == MARSIT_F64 ? 1 : 2);
         ctx->extract_grid = std::max(1, std::min(ob_extract, want_e)) * ctx->sm_count;
         ctx->decode_grid = std::max(1, std::min(ob_decode, want_d)) * ctx->sm_count;
