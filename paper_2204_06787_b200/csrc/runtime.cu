@@ -405,7 +405,11 @@ marsit_status run_coins(marsit_ctx* ctx, uint64_t seed, uint64_t round, cudaStre
         if (ctx->coin_tag[b].valid && ctx->coin_tag[b].seed == seed &&
             ctx->coin_tag[b].round == round) {
             ctx->cur_coin = b;
-            ctx->coins_pending = true;
+            // prefetched underneath the last decode: wait for it here, before
+            // the extract, so the extract and the merge stay adjacent in the
+            // stream (programmatic dependent launch of the merge)
+            CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_coin_done[b], 0));
+            ctx->coins_pending = false;
             return MARSIT_OK;
         }
     const int b = 1 - ctx->cur_coin;
