@@ -449,7 +449,8 @@ def run_ours(args):
             "unit": "Gelem/s",
             "n_gpus": world,
             "steps": args.steps,
-            "warmup": n_warm,
+            "warmup": n_warm,  # untimed steps actually run: >= max(W, 3) and >= --min-busy-s of work
+            "warmup_requested": args.warmup,
             "ms_per_step": ms,
             "higher_is_better": True,
             "scaling": "strong",
