@@ -140,3 +140,20 @@ def test_dropin_binary_fails_loudly_without_gpu():
         pytest.skip("a device is present")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=60)
     assert r.returncode != 0 and "no CUDA device" in r.stdout
+
+
+def test_plain_c_program_builds_and_fails_loudly_without_gpu():
+    """tools/sign_round_c.c uses the C-ABI from plain C (gcc -std=c11, no C++
+    or torch in the translation unit); without a device it must stop with
+    the library's no-CPU-path error."""
+    import subprocess
+    r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tools"), "sign_round_c"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    exe = os.path.join(ROOT, "build", "sign_round_c")
+    assert os.path.exists(exe)
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a device is present (the GPU suite runs it)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+    assert r.returncode != 0 and "no CUDA device" in r.stderr

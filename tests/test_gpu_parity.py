@@ -461,3 +461,18 @@ def test_adaptive_coin_budget_over_rounds_vs_oracle(frac, monkeypatch):
             comp_o = r.comp
         assert max(rates) > 0.5  # the drift the adaptive budget follows
         ctx.check()
+
+
+def test_plain_c_program_round_trip():
+    """build/sign_round_c (the C-ABI from plain C) runs 6 rounds, dense every
+    4th, and checks c' = (g + c) - g_t bit for bit after every sign round."""
+    import os
+    import subprocess
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "build", "sign_round_c")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tools"), "sign_round_c"], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "identity held exactly" in r.stdout
+    assert r.stdout.count("dense") == 2 and r.stdout.count(" sign ") == 4
