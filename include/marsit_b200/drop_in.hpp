@@ -30,6 +30,12 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
+#include <cstring>
+#include <bit>
+#include <exception>
+#include <optional>
+#include <thread>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -38,6 +44,14 @@
 #include <vector>
 
 #include "../marsit_b200.h"
+
+#ifdef MARSIT_DROPIN_PROFILE
+#include <chrono>
+#include <cstdio>
+#define MARSIT_DROPIN_T(v) const auto v = std::chrono::steady_clock::now()
+#else
+#define MARSIT_DROPIN_T(v)
+#endif
 
 namespace marsit::gpu {
 
@@ -70,6 +84,114 @@ struct DeviceBuffer {
     DeviceBuffer(const DeviceBuffer&) = delete;
     DeviceBuffer& operator=(const DeviceBuffer&) = delete;
 };
+
+// Grow-only device scratch reused across calls (per host thread): the
+// value-semantics entry points stage their inputs here instead of allocating
+// (and synchronously freeing) device memory on every call.
+inline void* scratch(int slot, size_t bytes) {
+    struct Pool {
+        void* p[8] = {};
+        size_t n[8] = {};
+        ~Pool() {
+            for (void* q : p)
+                if (q) cudaFree(q);
+        }
+    };
+    thread_local Pool pool;
+    if (pool.n[slot] < bytes) {
+        if (pool.p[slot]) cuda_check(cudaFree(pool.p[slot]), "cudaFree");
+        pool.p[slot] = nullptr;
+        pool.n[slot] = 0;
+        cuda_check(cudaMalloc(&pool.p[slot], bytes ? bytes : 1), "cudaMalloc");
+        pool.n[slot] = bytes;
+    }
+    return pool.p[slot];
+}
+
+// Pinned double-buffered staging per worker slot (process-wide, grow-only):
+// a host thread copies a pageable vector chunk by chunk into pinned memory
+// while the previous chunk's DMA runs on its own stream.
+struct Staging {
+    static constexpr size_t kChunk = size_t(16) << 20;  // bytes per buffer
+    void* buf[2] = {nullptr, nullptr};
+    cudaStream_t st = nullptr;
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    Staging() {
+        for (int b = 0; b < 2; ++b) {
+            cuda_check(cudaHostAlloc(&buf[b], kChunk, cudaHostAllocDefault), "cudaHostAlloc");
+            cuda_check(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming), "cudaEventCreate");
+        }
+        cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    }
+    // host (pageable) -> device, pipelined through the two pinned buffers
+    void to_device(void* dst, const void* src, size_t bytes) {
+        int b = 0;
+        for (size_t off = 0; off < bytes; off += kChunk, b ^= 1) {
+            const size_t n = std::min(kChunk, bytes - off);
+            cuda_check(cudaEventSynchronize(done[b]), "staging");  // buffer b free again
+            std::memcpy(buf[b], static_cast<const char*>(src) + off, n);
+            cuda_check(cudaMemcpyAsync(static_cast<char*>(dst) + off, buf[b], n,
+                                       cudaMemcpyHostToDevice, st), "H2D");
+            cuda_check(cudaEventRecord(done[b], st), "staging");
+        }
+        cuda_check(cudaStreamSynchronize(st), "H2D");
+    }
+    // device -> freshly allocated host vector (written once, no zero fill)
+    std::vector<double> to_host(const void* src, size_t count) {
+        std::vector<double> out;
+        out.reserve(count);
+        const size_t bytes = count * sizeof(double);
+        const size_t n0 = std::min(kChunk, bytes);
+        cuda_check(cudaMemcpyAsync(buf[0], src, n0, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaEventRecord(done[0], st), "staging");
+        int b = 0;
+        for (size_t off = 0; off < bytes; off += kChunk, b ^= 1) {
+            const size_t n = std::min(kChunk, bytes - off);
+            if (off + n < bytes) {  // the next chunk's DMA under this chunk's copy-out
+                const size_t n1 = std::min(kChunk, bytes - off - n);
+                cuda_check(cudaMemcpyAsync(buf[b ^ 1], static_cast<const char*>(src) + off + n, n1,
+                                           cudaMemcpyDeviceToHost, st), "D2H");
+                cuda_check(cudaEventRecord(done[b ^ 1], st), "staging");
+            }
+            cuda_check(cudaEventSynchronize(done[b]), "staging");
+            const double* p = static_cast<const double*>(buf[b]);
+            out.insert(out.end(), p, p + n / sizeof(double));
+        }
+        return out;
+    }
+};
+inline Staging& staging(uint32_t slot) {
+    static std::mutex mu;
+    static std::map<uint32_t, std::unique_ptr<Staging>> pool;
+    std::lock_guard<std::mutex> lock(mu);
+    auto& p = pool[slot];
+    if (!p) p = std::make_unique<Staging>();
+    return *p;
+}
+
+// Run f(i) for i in [0, n) on n host threads (the per-worker staging: the
+// pageable copies, the page faults of fresh result vectors and DenseVector's
+// finiteness scan all scale with threads).
+template <class F>
+inline void parallel_for(uint32_t n, F&& f) {
+    if (n <= 1) {
+        if (n == 1) f(0u);
+        return;
+    }
+    std::vector<std::thread> th;
+    std::vector<std::exception_ptr> err(n);
+    for (uint32_t i = 0; i < n; ++i)
+        th.emplace_back([&, i] {
+            try {
+                f(i);
+            } catch (...) {
+                err[i] = std::current_exception();
+            }
+        });
+    for (auto& t : th) t.join();
+    for (auto& e : err)
+        if (e) std::rethrow_exception(e);
+}
 
 // marsit::Schedule (schedule.hpp:31-55) -> flat tables -> marsit_schedule.
 struct ScheduleHandle {
@@ -160,41 +282,58 @@ inline MarsitRoundResult marsit_round(std::uint64_t t, const SyncConfig& cfg,
     marsit_ctx* ctx = detail::context_for(dim, sched);
     const uint32_t W = sched.workers;
     const size_t bytes = dim * sizeof(double);
-    detail::DeviceBuffer dg(W * bytes), dc(W * bytes), dout(W * bytes), dupd(bytes),
-        dagg(((dim + 63) / 64) * 8);
+    struct Buf {
+        void* p;
+    };
+    const Buf dg{detail::scratch(0, W * bytes)}, dc{detail::scratch(1, W * bytes)},
+        dout{detail::scratch(2, W * bytes)}, dupd{detail::scratch(3, bytes)},
+        dagg{detail::scratch(4, ((dim + 63) / 64) * 8)};
     std::vector<const void*> gp(W), cp(W);
     std::vector<void*> op(W);
     for (uint32_t w = 0; w < W; ++w) {
-        char* g = static_cast<char*>(dg.p) + w * bytes;
-        char* c = static_cast<char*>(dc.p) + w * bytes;
-        detail::cuda_check(cudaMemcpy(g, scaled_grads[w].values().data(), bytes, cudaMemcpyHostToDevice), "H2D");
-        detail::cuda_check(cudaMemcpy(c, comp[w].c.values().data(), bytes, cudaMemcpyHostToDevice), "H2D");
-        gp[w] = g;
-        cp[w] = c;
+        gp[w] = static_cast<char*>(dg.p) + w * bytes;
+        cp[w] = static_cast<char*>(dc.p) + w * bytes;
         op[w] = static_cast<char*>(dout.p) + w * bytes;
     }
+    MARSIT_DROPIN_T(t0);
+    detail::parallel_for(W, [&](uint32_t w) {  // one host thread and pinned pipeline per worker
+        detail::Staging& sg = detail::staging(w);
+        sg.to_device(const_cast<void*>(gp[w]), scaled_grads[w].values().data(), bytes);
+        sg.to_device(const_cast<void*>(cp[w]), comp[w].c.values().data(), bytes);
+    });
+    MARSIT_DROPIN_T(t1);
     const std::uint64_t period = cfg.full_precision_period ? *cfg.full_precision_period : 0;
     int full = 0;
     detail::check(::marsit_round(ctx, t, period, cfg.eta_s, global_seed, gp.data(), cp.data(),
                                  op.data(), static_cast<uint64_t*>(dagg.p), dupd.p, &full, nullptr));
     detail::check(marsit_ctx_check(ctx, nullptr));  // DenseVector finiteness (sync)
+    MARSIT_DROPIN_T(t2);
     std::vector<double> upd(dim);
     detail::cuda_check(cudaMemcpy(upd.data(), dupd.p, bytes, cudaMemcpyDeviceToHost), "D2H");
     MarsitRoundResult out{DenseVector(std::move(upd)), {}, detail::bits_account(ctx, W, full != 0),
                           full != 0, std::nullopt};
-    for (uint32_t w = 0; w < W; ++w) {
-        std::vector<double> c(dim);
-        detail::cuda_check(cudaMemcpy(c.data(), op[w], bytes, cudaMemcpyDeviceToHost), "D2H");
-        out.compensation.push_back(CompensationState{DenseVector(std::move(c))});
-    }
+    std::vector<std::optional<CompensationState>> cs(W);
+    detail::parallel_for(W, [&](uint32_t w) {
+        cs[w].emplace(CompensationState{DenseVector(detail::staging(w).to_host(op[w], dim))});
+    });
+    out.compensation.reserve(W);
+    for (auto& c : cs) out.compensation.push_back(std::move(*c));
+    MARSIT_DROPIN_T(t3);
     if (!full) {
         PackedSignVector bits = PackedSignVector::zeros(dim);
         std::vector<std::uint64_t> words((dim + 63) / 64);
         detail::cuda_check(cudaMemcpy(words.data(), dagg.p, words.size() * 8, cudaMemcpyDeviceToHost), "D2H");
-        for (size_t j = 0; j < dim; ++j)
-            if ((words[j >> 6] >> (j & 63)) & 1u) bits.set_bit(j, true);
+        for (size_t k = 0; k < words.size(); ++k)  // set bits only (the type has no word setter)
+            for (std::uint64_t x = words[k]; x; x &= x - 1)
+                bits.set_bit(k * 64 + static_cast<size_t>(std::countr_zero(x)), true);
         out.aggregate_bits = std::move(bits);
     }
+    MARSIT_DROPIN_T(t4);
+#ifdef MARSIT_DROPIN_PROFILE
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "drop-in: stage-in %.1f  round %.1f  results %.1f  bits %.1f ms\n",
+                 ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4));
+#endif
     return out;
 }
 

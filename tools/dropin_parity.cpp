@@ -13,7 +13,9 @@
 #include <marsit_b200/drop_in.hpp>
 
 #include <cmath>
+#include <chrono>
 #include <cstdio>
+#include <string>
 #include <cstring>
 #include <vector>
 
@@ -137,7 +139,40 @@ static void run_ssdm(const char* tag, const Schedule& sched, size_t D, int kind)
     std::printf("ssdm %-28s D=%zu %s\n", tag, D, failures ? "" : "ok");
 }
 
-int main() {
+// --time D: wall time of one marsit_round through the reference's own API
+// (host DenseVectors in, MarsitRoundResult out) — the reference's CPU round vs
+// marsit::gpu::marsit_round (staging, device round, read-back) — ring 8, fp64
+// Gaussian gradients, compensation carried over 3 timed rounds.
+static int time_rounds(size_t D) {
+    const Schedule sched = build_ring_schedule(8);
+    const auto g = inputs(8, D, 7, 1, 1);
+    std::vector<CompensationState> c_ref(8, CompensationState{DenseVector::zeros(D)}), c_gpu = c_ref;
+    const SyncConfig cfg{std::nullopt, 0x1.0p-10};
+    auto wall = [](auto&& fn) {
+        const auto t0 = std::chrono::steady_clock::now();
+        fn();
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    };
+    marsit::gpu::marsit_round(1, cfg, g, c_gpu, sched, 5);  // context + scratch warm-up
+    c_gpu = c_ref;
+    for (uint64_t t = 1; t <= 3; ++t) {
+        std::optional<MarsitRoundResult> rr, rg;
+        const double ms_ref = wall([&] { rr.emplace(marsit_round(t, cfg, g, c_ref, sched, 5)); });
+        const double ms_gpu =
+            wall([&] { rg.emplace(marsit::gpu::marsit_round(t, cfg, g, c_gpu, sched, 5)); });
+        const bool same_bits = rr->aggregate_bits == rg->aggregate_bits;
+        c_ref = rr->compensation;
+        c_gpu = rg->compensation;
+        std::printf("D=%zu round %llu: reference %.1f ms, marsit::gpu %.1f ms (%.1fx), bits %s\n", D,
+                    (unsigned long long)t, ms_ref, ms_gpu, ms_ref / ms_gpu,
+                    same_bits ? "identical" : "DIFFER");
+        if (!same_bits) return 1;
+    }
+    return 0;
+}
+
+int main(int argc, char** argv) {
+    if (argc == 3 && std::string(argv[1]) == "--time") return time_rounds(std::stoull(argv[2]));
     try {
         run_dense("ring4 gaussian", build_ring_schedule(4), 1001, 1);
         run_dense("torus2x4 zeros", build_torus_schedule(2, 4), 777, 2);
