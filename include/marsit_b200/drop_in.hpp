@@ -28,6 +28,7 @@
 #include <marsit/sync.hpp>
 
 #include <cuda_runtime.h>
+#include <sys/mman.h>
 
 #include <cstdint>
 #include <algorithm>
@@ -141,6 +142,14 @@ struct Staging {
         std::vector<double> out;
         out.reserve(count);
         const size_t bytes = count * sizeof(double);
+#ifdef MADV_HUGEPAGE
+        {  // fresh pages: ask for transparent huge pages (fewer first-touch faults)
+            const uintptr_t a = reinterpret_cast<uintptr_t>(out.data());
+            const uintptr_t lo = (a + (size_t(2) << 20) - 1) & ~((uintptr_t(2) << 20) - 1);
+            const uintptr_t hi = (a + bytes) & ~((uintptr_t(2) << 20) - 1);
+            if (hi > lo) madvise(reinterpret_cast<void*>(lo), hi - lo, MADV_HUGEPAGE);
+        }
+#endif
         const size_t n0 = std::min(kChunk, bytes);
         cuda_check(cudaMemcpyAsync(buf[0], src, n0, cudaMemcpyDeviceToHost, st), "D2H");
         cuda_check(cudaEventRecord(done[0], st), "staging");
