@@ -305,10 +305,12 @@ inline MarsitRoundResult marsit_round(std::uint64_t t, const SyncConfig& cfg,
         op[w] = static_cast<char*>(dout.p) + w * bytes;
     }
     MARSIT_DROPIN_T(t0);
-    detail::parallel_for(W, [&](uint32_t w) {  // one host thread and pinned pipeline per worker
-        detail::Staging& sg = detail::staging(w);
-        sg.to_device(const_cast<void*>(gp[w]), scaled_grads[w].values().data(), bytes);
-        sg.to_device(const_cast<void*>(cp[w]), comp[w].c.values().data(), bytes);
+    detail::parallel_for(2 * W, [&](uint32_t i) {  // one host thread and pinned pipeline per vector
+        const uint32_t w = i / 2;
+        if (i % 2 == 0)
+            detail::staging(i).to_device(const_cast<void*>(gp[w]), scaled_grads[w].values().data(), bytes);
+        else
+            detail::staging(i).to_device(const_cast<void*>(cp[w]), comp[w].c.values().data(), bytes);
     });
     MARSIT_DROPIN_T(t1);
     const std::uint64_t period = cfg.full_precision_period ? *cfg.full_precision_period : 0;
