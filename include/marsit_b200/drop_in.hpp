@@ -402,19 +402,14 @@ inline void check_vectors(const std::vector<DenseVector>& v, const Schedule& sch
 inline std::vector<const void*> upload(const std::vector<DenseVector>& v, DeviceBuffer& buf) {
     const size_t bytes = v[0].size() * sizeof(double);
     std::vector<const void*> ptrs(v.size());
-    for (size_t w = 0; w < v.size(); ++w) {
-        char* d = static_cast<char*>(buf.p) + w * bytes;
-        cuda_check(cudaMemcpy(d, v[w].values().data(), bytes, cudaMemcpyHostToDevice), "H2D");
-        ptrs[w] = d;
-    }
+    for (size_t w = 0; w < v.size(); ++w) ptrs[w] = static_cast<char*>(buf.p) + w * bytes;
+    parallel_for(uint32_t(v.size()), [&](uint32_t w) {  // pinned pipeline per vector
+        staging(w).to_device(const_cast<void*>(ptrs[w]), v[w].values().data(), bytes);
+    });
     return ptrs;
 }
 
-inline DenseVector download(const void* d, size_t n) {
-    std::vector<double> h(n);
-    cuda_check(cudaMemcpy(h.data(), d, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
-    return DenseVector(std::move(h));
-}
+inline DenseVector download(const void* d, size_t n) { return DenseVector(staging(0).to_host(d, n)); }
 
 }  // namespace detail
 
