@@ -395,6 +395,8 @@ def test_dense_round_vector_path_vs_oracle(dtype, topo, a, b, D):
     ("ring", 64, 0, 70_001, 2),       # 63 merges: descriptors read from global memory
     ("torus", 4, 8, 50_021, 2),
     ("torus", 8, 8, 64 * 1024 + 5, None),
+    ("torus", 16, 2, 30_011, 3),      # 16 row chains: more than kMaxLanes = 8 lanes
+    ("torus", 2, 16, 40_003, None),   # two long row chains side by side
 ])
 def test_large_worker_counts_vs_oracle(topo, a, b, D, period):
     """Many workers on one context (up to kMaxLocalWorkers = 64): long merge
