@@ -1,3 +1,5 @@
+"""C5 (355M, 8 workers) driver step with and without the fused replica update
+for three bucket sizes, and one bucket-sized context's per-phase times."""
 import sys, os, torch
 sys.path.insert(0, os.getcwd())
 import paper_2204_06787_b200 as mb

@@ -1,3 +1,5 @@
+"""Disagreement rate per round under error feedback with a fixed Gaussian
+gradient (C3 size): the drift above 1/2 that the adaptive coin budget follows."""
 import sys, os, torch
 sys.path.insert(0, os.getcwd())
 import paper_2204_06787_b200 as mb

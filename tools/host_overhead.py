@@ -1,3 +1,5 @@
+"""Host enqueue time of one sign round through the Python API at C1 size vs
+the wall time per round once the queue drains (is the small config host-bound?)."""
 import sys, os, time, torch
 sys.path.insert(0, os.getcwd())
 import paper_2204_06787_b200 as mb
