@@ -4,9 +4,13 @@
 Default (N=1): BASELINE config C3 — ring all-reduce of a 25.6M-element fp32
 gradient over M=8 workers (all simulated on the one GPU), with the global
 compensation update, one step = one marsit_round sign round (t >= 1).
-Under torchrun with N ranks the same M=8 workers are split 8/N per GPU
-(strong scaling: total work fixed) and the path exchanges packed segments
-with NCCL.
+With N ranks (torchrun, or `--gpus N` which re-launches itself under
+torchrun) the same M=8 workers are split 8/N per GPU (strong scaling: total
+work fixed); the packed segments move over NVLink peer memory inside the
+merge and decode kernels (--transport p2p, default) or with NCCL
+(--transport nccl).  The N > 1 line carries `parity_vs_g1` (the G-rank
+round against one context holding all M workers), per-rank phase times and
+the NVLink payload.
 
 Metric: sign-allreduce Gelem/s = D / step time (all-reduce algbw convention).
 
@@ -49,6 +53,8 @@ def parse():
     ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
                     help="N > 1: fused over NVLink peer memory (p2p) or NCCL send/recv + all-gather")
     ap.add_argument("--recipe", type=int, default=0, help="0 dyadic (independent), 1 correlated")
+    ap.add_argument("--dtype", choices=["f32", "f64"], default="f32",
+                    help="element type of gradients and compensation (f64: the drop-in's)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--min-busy-s", type=float, default=1.5,
@@ -228,109 +234,196 @@ def _cpu_model():
 
 
 def run_reference(args):
-    """The reference's own CPU path (oracle/_ref) on every host thread: each step
-    is one marsit_round per thread over a bucket of a D/10-coordinate sample."""
+    """The reference's own CPU path (oracle/_ref: its unmodified headers compiled
+    with the Release flags) on the arm's config: each step is ONE stock
+    marsit_round (sync.hpp:60-120) over the full D and all M workers — the
+    reference is single-threaded, so this is 1 host core.  A secondary figure
+    times the same round on all host threads, the D/10 sample split into one
+    contiguous bucket per thread (the only way the reference uses more cores;
+    bucketed semantics, reported as `bucketed_all_threads`)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    D = CONFIGS[args.config][0]
-    sample = max(D // 10, 1000)
-    steps = []
+    D, topo, a, b = CONFIGS[args.config]
+    M = a * (b or 1)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as O
-    _, topo, a, b = CONFIGS[args.config]
+    steps = []
+    secondary = None
     if O.ref_available():
-        cores = host_threads()
-        rb = RefBuckets(args.config, sample, cores)
-        for t in range(1, args.warmup + 1):
-            rb.round(t)
-        for t in range(args.warmup + 1, args.warmup + args.steps + 1):
-            steps.append(rb.round(t))
-        rb.close()
-        kind = "reference"
-        how = (f"{cores} host threads, each running the reference's marsit_round on a "
-               f"contiguous {sample // cores}-coordinate bucket of the sample")
+        R = O.ref()
+        h = R.ref_bench_create(0 if topo == "ring" else 1, a, b, D, SEED)
+        t = 1
+        for _ in range(args.warmup):
+            ms = R.ref_bench_round(h, t)
+            if ms < 0:
+                raise RuntimeError(f"reference round failed: {ms}")
+            t += 1
+        for _ in range(args.steps):
+            ms = R.ref_bench_round(h, t)
+            if ms < 0:
+                raise RuntimeError(f"reference round failed: {ms}")
+            steps.append(ms)
+            t += 1
+        R.ref_bench_destroy(h)
+        kind, cores = "reference", 1
+        how = (f"the reference's own marsit_round over the full D={D}, M={M} workers, one "
+               f"round per step (single-threaded, as the reference is)")
+        if not args.no_cpu_baseline:
+            try:
+                sample = max(D // 10, 1000)
+                threads = host_threads()
+                rb = RefBuckets(args.config, sample, threads)
+                rb.round(1)
+                bt = [rb.round(tt) for tt in range(2, 5)]
+                rb.close()
+                secondary = {"value": sample / (min(bt) * 1e-3) / 1e9, "unit": "Gelem/s",
+                             "cores": threads, "ms_per_round": min(bt),
+                             "sample": f"D={sample} sample split into {threads} contiguous "
+                                       f"buckets, each the reference's marsit_round on its own "
+                                       f"host thread (bucketed semantics, not one round)"}
+            except Exception as e:  # pragma: no cover
+                secondary = {"error": str(e)}
     else:
-        cb = cpu_baseline(args.config, sample, rounds=max(args.steps, 1))
-        steps = [cb["ms_per_round"]]
-        kind, cores, how = "port", 1, "1 thread (C restatement)"
+        cb = cpu_baseline(args.config, max(D // 10, 1000), rounds=max(args.steps, 1))
+        steps = [cb["ms_per_round"] * 10]
+        kind, cores, how = "port", 1, "1 thread (C restatement, D/10 sample x 10)"
     ms = sum(steps) / len(steps)
-    val = sample / (ms * 1e-3) / 1e9
+    val = D / (ms * 1e-3) / 1e9
     line = {"metric": METRIC, "value": val, "unit": "Gelem/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SURVEY §8c dyadic recipe)", "impl": "reference",
-            "config": {"workload": f"{args.config}: {topo} M={a * (b or 1)} D={D} "
-                                   f"(timed on a D={sample} sample)",
-                       "sample_dim": sample},
+            "config": {"workload": f"{args.config}: {topo} all-reduce M={M} workers, D={D}, "
+                                   f"sign round + compensation",
+                       "D": D, "workers": M, "topology": topo, "same_config": kind == "reference"},
             "cpu_baseline": {"value": val, "unit": "Gelem/s", "cores": cores, "kind": kind,
-                             "sample": f"D={sample} (1/10 of D), one step = {how}"},
+                             "sample": f"one step = {how}", "host_cpu": _cpu_model(),
+                             "nproc": os.cpu_count()},
             "e2e": {"value": val, "unit": "Gelem/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    if secondary is not None:
+        line["bucketed_all_threads"] = secondary
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------
+class Comm:
+    """torch.distributed plumbing of the bench (barriers, max over ranks, the
+    warm-up decision, small objects).  NCCL over the ranks' GPUs; gloo with CPU
+    tensors when the ranks share one device (MARSIT_BENCH_DEVICE, tests)."""
+
+    def __init__(self, world, rank, dev, shared):
+        import torch
+        import torch.distributed as dist
+        self.dist, self.world, self.rank = dist, world, rank
+        self.tdev = torch.device("cpu")
+        if world > 1:
+            if shared:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=dev)
+                self.tdev = dev
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device=self.tdev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def bcast(self, v: int) -> int:
+        if self.world == 1:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.int64, device=self.tdev)
+        self.dist.broadcast(t, 0)
+        return int(t.item())
+
+    def gather(self, obj):
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+def _digest(t) -> str:
+    import hashlib
+    return hashlib.blake2b(t.contiguous().view(-1).cpu().numpy().tobytes(), digest_size=16).hexdigest()
+
+
 def run_ours(args):
     import torch
-    import torch.distributed as dist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        args.gpus = world
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    shared = os.environ.get("MARSIT_BENCH_DEVICE") is not None
+    dev_index = int(os.environ["MARSIT_BENCH_DEVICE"]) if shared else local_rank
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    comm = Comm(world, rank, dev, shared)
 
     import paper_2204_06787_b200 as mb
 
     D, topo, a, b = CONFIGS[args.config]
     sched = mb.build_ring_schedule(a) if topo == "ring" else mb.build_torus_schedule(a, b)
-    M = sched.workers
+    M, S = sched.workers, sched.segments
+    dt = torch.float64 if args.dtype == "f64" else torch.float32
+    esize = 8 if dt == torch.float64 else 4
     nccl_id = None
     if world > 1 and args.transport == "nccl":
-        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(mb.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nccl_id = bytes(idt.cpu().tolist())
-    ctx = mb.Context(D, sched, torch.float32, local_rank, nranks=world, rank=rank,
-                     nccl_id=nccl_id, transport=args.transport if world > 1 else None)
+        ids = comm.gather(bytes(mb.nccl_unique_id()) if rank == 0 else None)
+        nccl_id = ids[0]
+    ctx = mb.Context(D, sched, dt, dev_index, nranks=world, rank=rank, nccl_id=nccl_id,
+                     transport=args.transport if world > 1 else None)
+    opened = []
     if world > 1 and args.transport == "p2p":
-        mb.exchange_p2p_buffers(ctx)  # CUDA IPC handles over torch.distributed
+        opened = mb.exchange_p2p_buffers(ctx)  # CUDA IPC handles over torch.distributed
     ml, w0 = ctx.local_workers, ctx.first_worker
-    grads = [torch.empty(D, device=dev) for _ in range(ml)]
+    grads = [torch.empty(D, device=dev, dtype=dt) for _ in range(ml)]
     for i in range(ml):
         mb.fill_recipe(grads[i], args.recipe, SEED, w0 + i, 1)
-    comp = [torch.zeros(D, device=dev) for _ in range(ml)]
+    comp = [torch.zeros(D, device=dev, dtype=dt) for _ in range(ml)]
     stream = torch.cuda.current_stream(dev)
 
     def step(t):
         ctx.sign_round(t, ETA, SEED, grads, comp)
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(dev_index)
     sampler.start()
-    # warm-up: at least W steps and at least min_busy_s of GPU work (clock sampling)
+    # warm-up: at least max(W, 3) steps and at least --min-busy-s of GPU work
+    # (clock sampling); rank 0 decides and every rank runs the same number of
+    # rounds (the lock-step delivery of transport.hpp:27-35: the P2P flag
+    # waits and NCCL collectives pair round by round)
     t = 1
-    t_busy0 = time.time()
     n_warm = 0
-    while n_warm < max(args.warmup, 3) or time.time() - t_busy0 < args.min_busy_s:
-        step(t)
-        t += 1
-        n_warm += 1
-        if n_warm % 20 == 0:
-            torch.cuda.synchronize(dev)
-    torch.cuda.synchronize(dev)
-    barrier()
+    t_busy0 = time.time()
+    chunk = max(args.warmup, 3)
+    while True:
+        for _ in range(chunk):
+            step(t)
+            t += 1
+            n_warm += 1
+        torch.cuda.synchronize(dev)
+        more = int(time.time() - t_busy0 < args.min_busy_s) if rank == 0 else 0
+        if not comm.bcast(more):
+            break
+        chunk = 20
+    ctx.check()
+    comm.barrier()
     torch.cuda.synchronize(dev)
     # headline: K steps, no per-phase instrumentation inside the timed region
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -341,10 +434,9 @@ def run_ours(args):
         t += 1
     e1.record(stream)
     torch.cuda.synchronize(dev)
-    barrier()
-    torch.cuda.synchronize(dev)
     wall1 = time.time()
-    ms = e0.elapsed_time(e1) / args.steps
+    comm.barrier()
+    ms_rank = e0.elapsed_time(e1) / args.steps
     # breakdown: K more steps with CUDA events around every phase on its
     # stream (the roofline's per-launch kernel times)
     ctx.set_timing(True)
@@ -358,16 +450,13 @@ def run_ours(args):
     ctx.check()
     sampler.stop()
     clocks = sampler.summary(wall0, wall1)
-    if world > 1:
-        tm = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-        ms = float(tm.item())
+    ms = comm.max(ms_rank)
 
     # e2e through the public API with host buffers (pinned), copies inside the
     # region: every step uploads its gradients and reads back its aggregate
     # bits.  Two device gradient buffers: step k+1's upload (copy stream)
     # overlaps step k's round (compute stream), as a training loop would.
-    host_g = [torch.empty(D, dtype=torch.float32, pin_memory=True) for _ in range(ml)]
+    host_g = [torch.empty(D, dtype=dt, pin_memory=True) for _ in range(ml)]
     for i in range(ml):
         host_g[i].copy_(grads[i])
     nwords = (D + 63) // 64
@@ -381,25 +470,25 @@ def run_ours(args):
         e.record(stream)
 
     def e2e_upload(k):
-        b = k % 2
+        bb = k % 2
         with torch.cuda.stream(copy_stream):
-            copy_stream.wait_event(ev_used[b])  # the round that read buffer b is done
+            copy_stream.wait_event(ev_used[bb])  # the round that read buffer bb is done
             for i in range(ml):
-                dev_g[b][i].copy_(host_g[i], non_blocking=True)
-            ev_copied[b].record(copy_stream)
+                dev_g[bb][i].copy_(host_g[i], non_blocking=True)
+            ev_copied[bb].record(copy_stream)
 
     def e2e_round(k, t):
-        b = k % 2
-        stream.wait_event(ev_copied[b])
-        ctx.sign_round(t, ETA, SEED, dev_g[b], comp, agg_bits=agg_dev)
-        ev_used[b].record(stream)
+        bb = k % 2
+        stream.wait_event(ev_copied[bb])
+        ctx.sign_round(t, ETA, SEED, dev_g[bb], comp, agg_bits=agg_dev)
+        ev_used[bb].record(stream)
         agg_host.copy_(agg_dev, non_blocking=True)
 
     e2e_upload(0)
     e2e_round(0, t)
     t += 1
     torch.cuda.synchronize(dev)
-    barrier()
+    comm.barrier()
     x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     x0.record(stream)
     ev_used[0].record(stream)
@@ -412,32 +501,67 @@ def run_ours(args):
         t += 1
     x1.record(stream)
     torch.cuda.synchronize(dev)
-    barrier()
-    e2e_ms = x0.elapsed_time(x1) / args.e2e_steps
-    if world > 1:
-        tm = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tm.item())
+    comm.barrier()
+    e2e_ms = comm.max(x0.elapsed_time(x1) / args.e2e_steps)
+    ctx.check()
 
-    # roofline: dominant kernel = decode+compensation (K3/K4), 12.125 B per
-    # worker-element (read g, c; write c'; read 1/8 B of aggregate bits)
+    # N > 1: parity self-check of the G-rank job against one context holding
+    # all M workers (rank 0): the same round from c = 0 on every rank, hashes
+    # of the aggregate bits and of every worker's compensation
+    parity = None
+    if world > 1:
+        T0 = 1 << 20
+        chk = [torch.zeros(D, device=dev, dtype=dt) for _ in range(ml)]
+        agg_chk = torch.empty(nwords, dtype=torch.int64, device=dev)
+        ctx.sign_round(T0, ETA, SEED, grads, chk, agg_bits=agg_chk)
+        torch.cuda.synchronize(dev)
+        ctx.check()
+        mine = {"agg": _digest(agg_chk), "comp": {w0 + i: _digest(chk[i]) for i in range(ml)}}
+        allh = comm.gather(mine)
+        del chk, agg_chk
+        if rank == 0:
+            one = mb.Context(D, sched, dt, dev_index)
+            g1 = [torch.empty(D, device=dev, dtype=dt) for _ in range(M)]
+            for w in range(M):
+                mb.fill_recipe(g1[w], args.recipe, SEED, w, 1)
+            c1 = [torch.zeros(D, device=dev, dtype=dt) for _ in range(M)]
+            a1 = torch.empty(nwords, dtype=torch.int64, device=dev)
+            one.sign_round(T0, ETA, SEED, g1, c1, agg_bits=a1)
+            torch.cuda.synchronize(dev)
+            one.check()
+            ok = all(h["agg"] == _digest(a1) for h in allh)
+            for h in allh:
+                for w, dg in h["comp"].items():
+                    ok &= dg == _digest(c1[int(w)])
+            parity = "bit-exact" if ok else "MISMATCH"
+            del one, g1, c1, a1
+        parity = comm.gather(parity)[0]
+
+    # per-rank phase times (timing pass) and NVLink payload (N > 1)
+    per_rank = comm.gather({k: v[0] / args.steps for k, v in phases.items() if v[1]})
+    L = -(-D // S)
+    seg_bytes = ((2 * -(-L // 64) + 3) // 4 * 4) * 4  # packed words of one segment (u32, x4)
+    s_own = S // world
+    nvl_in = ((M - ml) * s_own + (S - s_own)) * seg_bytes if world > 1 else 0
+
+    # roofline: dominant kernel = decode+compensation (K3/K4), 8 + 4 B (fp32)
+    # per worker-element + 1/8 B of aggregate bits
     hbm, hbm_kind = peaks()
-    # achieved = algorithmic bytes of all launches of the kernel in the timed
-    # region / their summed device time (CUDA events around every launch)
     dec_ms_tot, dec_n = phases.get("decode_comp", (float("nan"), 0))
     ext_ms_tot, ext_n = phases.get("sign_extract", (float("nan"), 0))
-    dec_bytes = ml * D * 12.125 * args.steps   # read g, c; write c'; 1/8 B of bits
-    ext_bytes = ml * D * 8.125 * args.steps    # read g, c; write 1/8 B of bits
+    dec_unit = 3 * esize + 0.125
+    dec_bytes = ml * D * dec_unit * args.steps   # read g, c; write c'; 1/8 B of bits
+    ext_bytes = ml * D * (2 * esize + 0.125) * args.steps  # read g, c; write 1/8 B of bits
     dec_gbs = dec_bytes / (dec_ms_tot * 1e-3) / 1e9
     dec_ms = dec_ms_tot / max(dec_n, 1)
-    ext_ms = ext_ms_tot / max(ext_n, 1)
-    step_bytes = ml * D * 20.25
+    step_unit = 5 * esize + 0.25
+    step_bytes = ml * D * step_unit
     step_gbs = step_bytes / (ms * 1e-3) / 1e9
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f)
-        traffic = tr.get(f"{args.config}_g{world}_decode_bytes")
+        traffic = tr.get(f"{args.config}_g{world}_decode_bytes" + ("_f64" if esize == 8 else ""))
     except Exception:
         pass
     launches = sum(nl for _, nl in phases.values())
@@ -455,7 +579,7 @@ def run_ours(args):
             "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None,
-            "dtype": "f32",
+            "dtype": args.dtype,
             "data": "synthetic (SURVEY §8c dyadic recipe, on-device generation)"
                     if args.recipe == 0 else "synthetic (SURVEY §8d correlated recipe)",
             "config": {"workload": f"{args.config}: {topo} all-reduce M={M} workers "
@@ -464,7 +588,7 @@ def run_ours(args):
                        "parallelism": f"{world} rank(s) x {ml} workers",
                        "transport": (args.transport if world > 1 else "none (1 rank)"),
                        "l2": "inputs (%.1f GB) > L2 (126 MB): no flush needed"
-                             % (2 * ml * D * 4 / 1e9)},
+                             % (2 * ml * D * esize / 1e9)},
             "worker_gelem_s": M * D / (ms * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "kernel": "decode_comp (K3+K4)",
                          "achieved": dec_gbs, "peak": hbm, "unit": "GB/s",
@@ -474,38 +598,74 @@ def run_ours(args):
                          "avg_launch_ms": dec_ms, "launches": int(dec_n)},
             "step_roofline": {"bytes_per_step": step_bytes, "achieved": step_gbs,
                               "frac": step_gbs / hbm,
-                              "note": "20.25 B per worker-element two-pass floor (SURVEY §8d)"},
+                              "note": f"{step_unit} B per worker-element two-pass floor "
+                                      f"(SURVEY §8d), this rank's {ml} workers"},
             "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items() if v[1]},
             "sign_extract_gbs": ext_bytes / (ext_ms_tot * 1e-3) / 1e9,
             "gpu_launches": int(launches),
             "clocks": clocks,
             "e2e": {"value": D / (e2e_ms * 1e-3) / 1e9, "unit": "Gelem/s",
                     "ms_per_step": e2e_ms,
-                    "h2d_bytes_per_step": ml * D * 4,
-                    "d2h_bytes_per_step": nwords * 8,
+                    "h2d_bytes_per_step": ml * D * esize * world,
+                    "d2h_bytes_per_step": nwords * 8 * world,
                     "path": "Context.sign_round (C-ABI marsit_sign_round) with pinned host "
-                            "gradients copied in and aggregate bits copied out every step; "
-                            "double-buffered device gradients: step k+1's upload (copy "
-                            "stream) overlaps step k's round",
-                    "h2d_gbs": ml * D * 4 / (e2e_ms * 1e-3) / 1e9},
+                            "gradients copied in and aggregate bits copied out every step on "
+                            "every rank; double-buffered device gradients: step k+1's upload "
+                            "(copy stream) overlaps step k's round",
+                    "h2d_gbs_per_rank": ml * D * esize / (e2e_ms * 1e-3) / 1e9},
         }
+        if world > 1:
+            line["parity_vs_g1"] = parity
+            line["per_rank_phases_ms"] = per_rank
+            line["nvlink"] = {"bytes_in_per_rank_per_step": nvl_in,
+                              "achieved_gbs": nvl_in / (ms * 1e-3) / 1e9,
+                              "peak_gbs": 770.0, "peak_kind": "measured peer copy "
+                              "(B200_PROFILING.md; 900 nominal)",
+                              "frac": nvl_in / (ms * 1e-3) / 1e9 / 770.0,
+                              "note": "owned segments' leaves from the other ranks + the other "
+                                      "owners' aggregates, packed bits"}
+            if shared:
+                line["note"] = ("ranks shared one GPU (MARSIT_BENCH_DEVICE): functional run, "
+                                "times are not a multi-GPU measurement")
         if world == 1 and not args.no_cpu_baseline:
             try:
                 line["cpu_baseline"] = cpu_baseline(args.config, D // 10)
             except Exception as e:  # pragma: no cover
                 line["cpu_baseline"] = {"value": None, "error": str(e)}
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    comm.barrier()
+    del ctx
+    for ptr in opened:
+        mb._native.lib().marsit_ipc_close(ptr)
+    comm.close()
+
+
+def spawn(args):
+    """`bench.py --gpus N` outside torchrun: re-launch this command as N ranks."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return 0
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        return spawn(args)
+    if int(world or 1) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} does not match WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    run_ours(args)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define MARSIT_B200_ABI_VERSION 1
+#define MARSIT_B200_ABI_VERSION 2
 
 typedef enum marsit_status {
     MARSIT_OK = 0,
@@ -95,11 +95,14 @@ marsit_status marsit_schedule_plan(const marsit_schedule* s, uint32_t segment,
  * ---------------------------------------------------------------------- */
 typedef struct marsit_ctx marsit_ctx;
 
-/* How the packed segments move between ranks (nranks > 1). */
+/* How the packed segments move between ranks (nranks > 1).  The zero value
+ * (the default of a zero-initialised descriptor) is the P2P transport, the
+ * one exercised end to end across processes by the test suite; NCCL is
+ * opt-in (see DESIGN.md section 5 for what has run on hardware). */
 typedef enum marsit_transport {
-    MARSIT_TRANSPORT_NCCL = 0,      /* built in: grouped send/recv + all-gather     */
+    MARSIT_TRANSPORT_P2P = 0,       /* fused over peer memory (marsit_ctx_set_peers) */
     MARSIT_TRANSPORT_EXTERNAL = 1,  /* the caller moves the blocks between phases   */
-    MARSIT_TRANSPORT_P2P = 2        /* fused over peer memory (marsit_ctx_set_peers) */
+    MARSIT_TRANSPORT_NCCL = 2       /* built in: grouped send/recv + all-gather     */
 } marsit_transport;
 
 typedef struct marsit_ctx_desc {
@@ -229,6 +232,29 @@ marsit_status marsit_bits_account(const marsit_ctx* ctx, int dense, uint64_t* pe
  * missing contributions).  Clears the latch. */
 marsit_status marsit_ctx_check(marsit_ctx* ctx, void* stream);
 
+/* Failure handling of multi-rank contexts (P2P, NCCL).  Every round enqueued
+ * on such a context is watched by a host thread: if it has not completed
+ * within the timeout (default 120000 ms, env MARSIT_WAIT_TIMEOUT_MS; 0 =
+ * unbounded), if NCCL reports an asynchronous error (ncclCommGetAsyncError),
+ * or if a peer announced an abort, the context is marked failed — P2P stream
+ * waits are released (this rank's flags and its slots in the peers' flags are
+ * set to the abort value, so the peers fail too instead of hanging), an NCCL
+ * communicator is aborted — and every later call returns the latched status:
+ * MARSIT_EPROTOCOL (a broken wire, protocol_error, errors.hpp:24-29) or
+ * MARSIT_ENCCL.  marsit_ctx_status returns the latched status without
+ * synchronising; marsit_ctx_check returns it after synchronising. */
+marsit_status marsit_ctx_set_wait_timeout(marsit_ctx* ctx, uint64_t timeout_ms);
+marsit_status marsit_ctx_status(const marsit_ctx* ctx);
+
+/* Opt-in data consensus (consensus(), allreduce.hpp:32-43, called by
+ * marsit_round at sync.hpp:101): after its merge every owner hashes its
+ * aggregate segments (64-bit, order-independent XOR of SplitMix64 word
+ * hashes) into a slot that travels with the segment; after the decode every
+ * rank re-hashes all S segments as it reads them and compares.  A mismatch
+ * is latched and reported by marsit_ctx_check as MARSIT_EPROTOCOL
+ * ("consensus").  Off by default (two small kernels per round). */
+marsit_status marsit_ctx_set_consensus(marsit_ctx* ctx, int enable);
+
 /* Per-phase device timing (CUDA events on the launching stream).
  * Phases: 0 sign_extract, 1 exchange, 2 merge, 3 allgather, 4 decode_comp,
  * 5 export, 6 dense, 7 coins (coin precompute, on the context's side stream,
@@ -336,7 +362,7 @@ typedef struct marsit_driver_desc {
     double eta_s;                     /* > 0                                       */
     uint64_t global_seed;
     uint64_t first_round;             /* t of the first step (trainer starts at 0) */
-    marsit_transport transport;       /* nranks > 1: NCCL (default) or P2P         */
+    marsit_transport transport;       /* nranks > 1: P2P (default) or NCCL         */
 } marsit_driver_desc;
 
 marsit_status marsit_driver_create(const marsit_driver_desc* desc, marsit_driver** out);
@@ -364,6 +390,9 @@ marsit_status marsit_driver_p2p_buffers(const marsit_driver* drv, uint32_t bucke
                                         marsit_p2p_buffers* out);
 marsit_status marsit_driver_set_peers(marsit_driver* drv, uint32_t bucket,
                                       const marsit_p2p_buffers* peers, uint32_t nranks);
+/* marsit_ctx_set_wait_timeout / marsit_ctx_set_consensus on every bucket. */
+marsit_status marsit_driver_set_wait_timeout(marsit_driver* drv, uint64_t timeout_ms);
+marsit_status marsit_driver_set_consensus(marsit_driver* drv, int enable);
 /* Round metrics of the last step summed over the buckets (matching over all D
  * coordinates, as trainer.hpp:280-281 records it per round). */
 marsit_status marsit_driver_set_metrics(marsit_driver* drv, int enable);

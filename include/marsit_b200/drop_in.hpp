@@ -19,7 +19,11 @@
 //    (rng.hpp:28-54) and the aggregate are bit-identical;
 //  * errors surface as the reference exception types (errors.hpp:10-42);
 //  * value semantics: nothing is retained between calls except a cached
-//    device context per (D, schedule) (scratch buffers, compiled plan).
+//    device context per (calling thread, D, schedule) (scratch buffers,
+//    compiled plan) and pinned staging buffers per calling thread;
+//  * re-entrant like the reference's pure functions: concurrent calls from
+//    different host threads never share a context, scratch or staging
+//    buffer (the C-ABI allows one host thread per context).
 #pragma once
 
 #include <marsit/allreduce.hpp>
@@ -109,8 +113,8 @@ inline void* scratch(int slot, size_t bytes) {
     return pool.p[slot];
 }
 
-// Pinned double-buffered staging per worker slot (process-wide, grow-only):
-// a host thread copies a pageable vector chunk by chunk into pinned memory
+// Pinned double-buffered staging per (calling thread, worker slot), grow-only:
+// a helper thread copies a pageable vector chunk by chunk into pinned memory
 // while the previous chunk's DMA runs on its own stream.
 struct Staging {
     static constexpr size_t kChunk = size_t(16) << 20;  // bytes per buffer
@@ -169,11 +173,13 @@ struct Staging {
         return out;
     }
 };
-inline Staging& staging(uint32_t slot) {
+// `owner` is the thread that called the entry point (its helper threads use
+// the owner's buffers), so concurrent callers never share a slot.
+inline Staging& staging(std::thread::id owner, uint32_t slot) {
     static std::mutex mu;
-    static std::map<uint32_t, std::unique_ptr<Staging>> pool;
+    static std::map<std::pair<std::thread::id, uint32_t>, std::unique_ptr<Staging>> pool;
     std::lock_guard<std::mutex> lock(mu);
-    auto& p = pool[slot];
+    auto& p = pool[{owner, slot}];
     if (!p) p = std::make_unique<Staging>();
     return *p;
 }
@@ -225,7 +231,9 @@ struct ScheduleHandle {
     ~ScheduleHandle() { marsit_schedule_destroy(s); }
 };
 
-// One cached context per (D, schedule tables); fp64 instantiation.
+// One cached context per (calling thread, D, schedule tables); fp64
+// instantiation.  Thread-local: a context's device scratch (packed signs,
+// aggregate, coin buffers, error latch) serves one round at a time.
 struct CachedCtx {
     std::unique_ptr<ScheduleHandle> sched;
     marsit_ctx* ctx = nullptr;
@@ -246,9 +254,7 @@ inline std::vector<uint32_t> schedule_key(const Schedule& s) {
 }
 
 inline marsit_ctx* context_for(size_t dim, const Schedule& sched) {
-    static std::mutex mu;
-    static std::map<std::pair<size_t, std::vector<uint32_t>>, std::unique_ptr<CachedCtx>> cache;
-    std::lock_guard<std::mutex> lock(mu);
+    thread_local std::map<std::pair<size_t, std::vector<uint32_t>>, std::unique_ptr<CachedCtx>> cache;
     auto key = std::make_pair(dim, schedule_key(sched));
     auto it = cache.find(key);
     if (it != cache.end()) return it->second->ctx;
@@ -305,12 +311,13 @@ inline MarsitRoundResult marsit_round(std::uint64_t t, const SyncConfig& cfg,
         op[w] = static_cast<char*>(dout.p) + w * bytes;
     }
     MARSIT_DROPIN_T(t0);
+    const std::thread::id owner = std::this_thread::get_id();
     detail::parallel_for(2 * W, [&](uint32_t i) {  // one host thread and pinned pipeline per vector
         const uint32_t w = i / 2;
         if (i % 2 == 0)
-            detail::staging(i).to_device(const_cast<void*>(gp[w]), scaled_grads[w].values().data(), bytes);
+            detail::staging(owner, i).to_device(const_cast<void*>(gp[w]), scaled_grads[w].values().data(), bytes);
         else
-            detail::staging(i).to_device(const_cast<void*>(cp[w]), comp[w].c.values().data(), bytes);
+            detail::staging(owner, i).to_device(const_cast<void*>(cp[w]), comp[w].c.values().data(), bytes);
     });
     MARSIT_DROPIN_T(t1);
     const std::uint64_t period = cfg.full_precision_period ? *cfg.full_precision_period : 0;
@@ -325,7 +332,7 @@ inline MarsitRoundResult marsit_round(std::uint64_t t, const SyncConfig& cfg,
                           full != 0, std::nullopt};
     std::vector<std::optional<CompensationState>> cs(W);
     detail::parallel_for(W, [&](uint32_t w) {
-        cs[w].emplace(CompensationState{DenseVector(detail::staging(w).to_host(op[w], dim))});
+        cs[w].emplace(CompensationState{DenseVector(detail::staging(owner, w).to_host(op[w], dim))});
     });
     out.compensation.reserve(W);
     for (auto& c : cs) out.compensation.push_back(std::move(*c));
@@ -348,8 +355,11 @@ inline MarsitRoundResult marsit_round(std::uint64_t t, const SyncConfig& cfg,
     return out;
 }
 
-// allreduce.hpp:148-189, same signature and result (every worker's state
-// is the consensus aggregate, as for ring and torus schedules).
+// allreduce.hpp:148-189, same signature and result for schedules that end in
+// consensus (ring, torus): every worker's state is the consensus aggregate.
+// Schedules whose workers end in different states (e.g. reduce-only tables)
+// raise unsupported_error: the device path materialises one aggregate per
+// segment.
 inline SignAllreduceResult allreduce_sign(const std::vector<std::vector<PackedSignVector>>& signs,
                                           const Schedule& sched, const RoundContext& rc) {
     if (signs.size() != sched.workers) throw parameter_error("allreduce_sign: worker count mismatch");
@@ -403,13 +413,16 @@ inline std::vector<const void*> upload(const std::vector<DenseVector>& v, Device
     const size_t bytes = v[0].size() * sizeof(double);
     std::vector<const void*> ptrs(v.size());
     for (size_t w = 0; w < v.size(); ++w) ptrs[w] = static_cast<char*>(buf.p) + w * bytes;
+    const std::thread::id owner = std::this_thread::get_id();
     parallel_for(uint32_t(v.size()), [&](uint32_t w) {  // pinned pipeline per vector
-        staging(w).to_device(const_cast<void*>(ptrs[w]), v[w].values().data(), bytes);
+        staging(owner, w).to_device(const_cast<void*>(ptrs[w]), v[w].values().data(), bytes);
     });
     return ptrs;
 }
 
-inline DenseVector download(const void* d, size_t n) { return DenseVector(staging(0).to_host(d, n)); }
+inline DenseVector download(const void* d, size_t n) {
+    return DenseVector(staging(std::this_thread::get_id(), 0).to_host(d, n));
+}
 
 }  // namespace detail
 

@@ -139,6 +139,9 @@ def ref():
         R.ref_ssdm_allreduce.argtypes = [C.c_int, C.c_int, C.c_uint32, C.c_uint32, C.c_size_t,
                                          _f64p, C.c_uint64, C.c_uint64, _f64p, _u64p,
                                          C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), _i64p]
+        R.ref_matching.restype = C.c_int
+        R.ref_matching.argtypes = [_u64p, C.c_size_t, C.c_uint32, _f64p, _f64p,
+                                   C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
         R.ref_bench_create.restype = C.c_void_p
         R.ref_bench_create.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_size_t, C.c_uint64]
         R.ref_bench_round.restype = C.c_double
@@ -332,6 +335,38 @@ def matching_count(agg_bits: np.ndarray, grads: np.ndarray, comp: np.ndarray) ->
     bits = np.unpackbits(np.ascontiguousarray(agg_bits, "<u8").view(np.uint8),
                          bitorder="little")[:dim].astype(bool)
     return int(np.count_nonzero(bits == (mean >= 0.0)))
+
+
+def gen_metrics_inputs(seed: int, workers: int, dim: int):
+    """fp32-valued (g, c) for the matching-rate fixtures: Gaussian values
+    rounded to fp32, plus every 7th coordinate a cancellation case where
+    fp32(g + c) loses the bits that decide the sign of the fp64 mean
+    (worker 0: 1 + 2^-30, worker 1: -1 - 2^-29, the rest 0), so a mean formed
+    from fp32-rounded u differs from trainer.hpp:241-251's fp64 add(g, c)."""
+    rs = np.random.RandomState(seed)
+    g = rs.standard_normal((workers, dim)).astype(np.float32).astype(np.float64) * 1e-3
+    c = rs.standard_normal((workers, dim)).astype(np.float32).astype(np.float64) * 1e-3
+    g = g.astype(np.float32).astype(np.float64)
+    c = c.astype(np.float32).astype(np.float64)
+    idx = np.arange(0, dim, 7)
+    g[:, idx] = 0.0
+    c[:, idx] = 0.0
+    g[0, idx], c[0, idx] = 1.0, 2.0 ** -30
+    g[1, idx], c[1, idx] = -1.0, -(2.0 ** -29)
+    return g, c
+
+
+def ref_matching(agg_bits: np.ndarray, grads: np.ndarray, comp: np.ndarray):
+    """The REAL reference's matching figure (oracle/_ref: analysis.hpp:244-253
+    on trainer.hpp:241-251's mean): (rate, count)."""
+    grads = np.ascontiguousarray(grads, np.float64)
+    comp = np.ascontiguousarray(comp, np.float64)
+    W, dim = grads.shape
+    words = np.ascontiguousarray(agg_bits, np.uint64)
+    rate, cnt = C.c_double(), C.c_uint64()
+    rc = ref().ref_matching(words, dim, W, grads.ravel(), comp.ravel(), C.byref(rate), C.byref(cnt))
+    assert rc == 0, rc
+    return rate.value, cnt.value
 
 
 # ----------------------------------------------------------------------------

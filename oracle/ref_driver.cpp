@@ -11,6 +11,7 @@
 // 3 protocol_error, 4 unsupported_error, 9 other exception.
 
 #include <marsit/allreduce.hpp>
+#include <marsit/analysis.hpp>
 #include <marsit/merge.hpp>
 #include <marsit/rng.hpp>
 #include <marsit/schedule.hpp>
@@ -18,6 +19,7 @@
 #include <marsit/sync.hpp>
 
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -178,6 +180,27 @@ int ref_marsit_round(std::uint64_t t, int has_period, std::uint64_t period, doub
             bits_per_worker[w] = res.bits.per_worker[w];
         *reduce_bits = res.bits.reduce_bits;
         *gather_bits = res.bits.gather_bits;
+    });
+}
+
+// The trainer's per-round matching figure: matching_rate (analysis.hpp:244-253)
+// of the aggregate bits against the mean of u_w = add(g_w, c_w) summed in
+// worker order and divided by W (trainer.hpp:241-251).  *matches receives
+// the count (rate * dim, exact for dim < 2^53).
+int ref_matching(const std::uint64_t* agg_words, std::size_t dim, std::uint32_t workers,
+                 const double* grads, const double* comp, double* rate, std::uint64_t* matches) {
+    return guarded([&] {
+        std::vector<double> mean(dim, 0.0);
+        for (std::uint32_t w = 0; w < workers; ++w) {
+            const DenseVector g(std::vector<double>(grads + w * dim, grads + (w + 1) * dim));
+            const DenseVector c(std::vector<double>(comp + w * dim, comp + (w + 1) * dim));
+            const DenseVector u = add(g, c);
+            for (std::size_t j = 0; j < dim; ++j) mean[j] += u[j];
+        }
+        for (double& v : mean) v /= static_cast<double>(workers);
+        const double r = matching_rate(from_words(agg_words, dim), DenseVector(std::move(mean)));
+        *rate = r;
+        *matches = static_cast<std::uint64_t>(std::llround(r * static_cast<double>(dim)));
     });
 }
 

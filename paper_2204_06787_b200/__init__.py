@@ -248,13 +248,14 @@ class Context:
     def __init__(self, dim: int, schedule: Schedule, dtype=None, device: int = 0,
                  nranks: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
                  external_transport: bool = False, transport: Optional[str] = None):
-        """transport: "nccl" (default for nranks > 1), "external" (the caller
-        moves blocks between marsit_round_phase calls) or "p2p" (fused over
-        peer memory; call set_peers before the first round)."""
+        """transport (nranks > 1): "p2p" (default: fused over peer memory; call
+        set_peers / exchange_p2p_buffers before the first round), "nccl"
+        (grouped send/recv + all-gather; needs nccl_id) or "external" (the
+        caller moves blocks between marsit_round_phase calls)."""
         import torch
         dtype = dtype or torch.float32
         if transport is None:
-            transport = "external" if external_transport else "nccl"
+            transport = "external" if external_transport else ("nccl" if nccl_id else "p2p")
         self.transport = transport
         self.dim, self.schedule, self.device = int(dim), schedule, int(device)
         self.dtype = dtype
@@ -266,7 +267,7 @@ class Context:
         desc.device = self.device
         desc.nranks = nranks
         desc.rank = rank
-        desc.transport = {"nccl": 0, "external": 1, "p2p": 2}[transport]
+        desc.transport = {"p2p": 0, "external": 1, "nccl": 2}[transport]
         self._id_buf = None
         if nccl_id is not None:
             self._id_buf = C.create_string_buffer(bytes(nccl_id), 128)
@@ -350,6 +351,21 @@ class Context:
 
     def set_timing(self, on: bool):
         _check(N.lib().marsit_ctx_set_timing(self._h, int(on)))
+
+    def set_wait_timeout(self, ms: int):
+        """Bound on how long a round may wait for its peers / NCCL before the
+        context fails with ProtocolError / NcclError (0 = unbounded)."""
+        _check(N.lib().marsit_ctx_set_wait_timeout(self._h, int(ms)))
+
+    def set_consensus(self, on: bool):
+        """Opt-in data consensus (allreduce.hpp:32-43): every rank checks the
+        aggregate it read against its owners' hashes; check() raises
+        ProtocolError on a mismatch."""
+        _check(N.lib().marsit_ctx_set_consensus(self._h, int(on)))
+
+    def status(self):
+        """Raise the latched failure of the context, if any (no synchronisation)."""
+        _check(N.lib().marsit_ctx_status(self._h))
 
     def set_metrics(self, on: bool):
         """Fused on-device round metrics (matching count in the decode,
@@ -641,9 +657,9 @@ class Driver:
     def __init__(self, dim: int, schedule: Schedule, *, eta_s: float, global_seed: int,
                  period: Optional[int] = None, bucket_elems: int = 0, dtype=None,
                  device: int = 0, first_round: int = 0, nranks: int = 1, rank: int = 0,
-                 nccl_id: Optional[bytes] = None, transport: str = "nccl"):
-        """transport (nranks > 1): "nccl", or "p2p" (then exchange every
-        bucket's buffers with set_peers / exchange_p2p_buffers first)."""
+                 nccl_id: Optional[bytes] = None, transport: str = "p2p"):
+        """transport (nranks > 1): "p2p" (default; exchange every bucket's
+        buffers with set_peers / exchange_p2p_buffers first) or "nccl"."""
         import torch
         dtype = dtype or torch.float32
         if period == 0:
@@ -665,7 +681,7 @@ class Driver:
         d.eta_s = float(eta_s)
         d.global_seed = global_seed
         d.first_round = first_round
-        d.transport = {"nccl": 0, "p2p": 2}[transport]
+        d.transport = {"p2p": 0, "nccl": 2}[transport]
         out = C.c_void_p()
         _check(N.lib().marsit_driver_create(C.byref(d), C.byref(out)))
         self._h = out
@@ -722,6 +738,12 @@ class Driver:
 
     def set_metrics(self, on: bool):
         _check(N.lib().marsit_driver_set_metrics(self._h, int(on)))
+
+    def set_wait_timeout(self, ms: int):
+        _check(N.lib().marsit_driver_set_wait_timeout(self._h, int(ms)))
+
+    def set_consensus(self, on: bool):
+        _check(N.lib().marsit_driver_set_consensus(self._h, int(on)))
 
     def metrics(self) -> "RoundMetrics":
         """Last step's metrics summed over the buckets (trainer.hpp:278-281)."""

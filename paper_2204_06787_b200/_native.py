@@ -92,6 +92,11 @@ SIGNATURES = {
                                    C.POINTER(_u64)]),
     "marsit_ctx_check": (_i32, [_vp, _vp]),
     "marsit_ctx_set_timing": (_i32, [_vp, _i32]),
+    "marsit_ctx_set_wait_timeout": (_i32, [_vp, _u64]),
+    "marsit_ctx_set_consensus": (_i32, [_vp, _i32]),
+    "marsit_ctx_status": (_i32, [_vp]),
+    "marsit_driver_set_wait_timeout": (_i32, [_vp, _u64]),
+    "marsit_driver_set_consensus": (_i32, [_vp, _i32]),
     "marsit_ctx_set_metrics": (_i32, [_vp, _i32]),
     "marsit_ctx_p2p_buffers": (_i32, [_vp, C.POINTER(P2PBuffers)]),
     "marsit_ctx_set_peers": (_i32, [_vp, C.POINTER(P2PBuffers), _u32]),

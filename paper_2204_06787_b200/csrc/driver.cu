@@ -107,8 +107,8 @@ marsit_status marsit_driver_create(const marsit_driver_desc* desc, marsit_driver
         cd.nranks = desc->nranks;
         cd.rank = desc->rank;
         cd.nccl_id = desc->nccl_id;
-        cd.transport = desc->transport == MARSIT_TRANSPORT_P2P ? MARSIT_TRANSPORT_P2P
-                                                               : MARSIT_TRANSPORT_NCCL;
+        cd.transport = desc->transport == MARSIT_TRANSPORT_NCCL ? MARSIT_TRANSPORT_NCCL
+                                                                : MARSIT_TRANSPORT_P2P;
         // one NCCL communicator for all buckets (a unique id initialises one comm)
         marsit_status s = ctx_create_internal(
             &cd, drv->buckets.empty() ? nullptr : drv->buckets[0].ctx->comm, &b.ctx);
@@ -196,6 +196,22 @@ marsit_status marsit_driver_set_peers(marsit_driver* drv, uint32_t bucket,
     if (!drv) return fail(MARSIT_EPARAM, "driver is null");
     if (bucket >= drv->buckets.size()) return fail(MARSIT_EPARAM, "bucket out of range");
     return marsit_ctx_set_peers(drv->buckets[bucket].ctx, peers, nranks);
+}
+
+marsit_status marsit_driver_set_wait_timeout(marsit_driver* drv, uint64_t timeout_ms) {
+    if (!drv) return fail(MARSIT_EPARAM, "driver is null");
+    marsit_status s;
+    for (auto& b : drv->buckets)
+        if ((s = marsit_ctx_set_wait_timeout(b.ctx, timeout_ms))) return s;
+    return MARSIT_OK;
+}
+
+marsit_status marsit_driver_set_consensus(marsit_driver* drv, int enable) {
+    if (!drv) return fail(MARSIT_EPARAM, "driver is null");
+    marsit_status s;
+    for (auto& b : drv->buckets)
+        if ((s = marsit_ctx_set_consensus(b.ctx, enable))) return s;
+    return MARSIT_OK;
 }
 
 marsit_status marsit_driver_set_metrics(marsit_driver* drv, int enable) {
@@ -323,18 +339,27 @@ marsit_status marsit_read_params_checkpoint(const char* path, void* d_params, ui
     if (!path || !d_params) return fail(MARSIT_EPARAM, "bad argument");
     std::ifstream f(path, std::ios::binary);
     if (!f) return fail(MARSIT_EPARAM, std::string("cannot open ") + path);
-    char magic[12];
-    uint32_t version = 0;
-    uint64_t n = 0;
-    f.read(magic, 12);
-    f.read(reinterpret_cast<char*>(&version), 4);
-    f.read(reinterpret_cast<char*>(&n), 8);
+    // read_checkpoint (checkpoint.hpp:65-91): explicit little-endian header
+    // fields and an exact file size of 24 + 8 * dim ("size mismatch")
+    f.seekg(0, std::ios::end);
+    const std::streamoff size = f.tellg();
+    f.seekg(0, std::ios::beg);
+    unsigned char hdr[24];
+    if (size < 24 || !f.read(reinterpret_cast<char*>(hdr), 24))
+        return fail(MARSIT_EPARAM, "read_checkpoint: truncated header");
+    auto le = [&](int off, int bytes) {
+        uint64_t v = 0;
+        for (int i = 0; i < bytes; ++i) v |= uint64_t(hdr[off + i]) << (8 * i);
+        return v;
+    };
     const char want[12] = {'m', 'a', 'r', 's', 'i', 't', '-', 'c', 'k', 'p', 't', '\0'};
-    if (!f || std::memcmp(magic, want, 12) != 0) return fail(MARSIT_EPARAM, "not a marsit checkpoint");
-    if (version != 1) return fail(MARSIT_EUNSUPPORTED, "unsupported checkpoint version");
+    if (std::memcmp(hdr, want, 12) != 0) return fail(MARSIT_EPARAM, "read_checkpoint: bad magic");
+    if (le(12, 4) != 1) return fail(MARSIT_EUNSUPPORTED, "read_checkpoint: unsupported version");
+    const uint64_t n = le(16, 8);
+    if (uint64_t(size) != 24 + n * 8) return fail(MARSIT_EPARAM, "read_checkpoint: size mismatch");
     if (n != dim) return fail(MARSIT_EPARAM, "checkpoint dimension mismatch");
     std::vector<double> v(dim);
-    f.read(reinterpret_cast<char*>(v.data()), std::streamsize(dim * 8));
+    f.read(reinterpret_cast<char*>(v.data()), std::streamsize(dim * 8));  // LE hosts (x86-64, aarch64)
     if (!f) return fail(MARSIT_EPARAM, "truncated checkpoint");
     for (double x : v)
         if (!std::isfinite(x)) return fail(MARSIT_ENONFINITE, "DenseVector: non-finite entry");

@@ -6,10 +6,16 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <memory>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/marsit_b200.h"
@@ -62,6 +68,11 @@ struct DevicePlan {
     // each lane; n_lanes[stage] = lanes of the stage (max over segments)
     std::vector<uint32_t> lane_begin, n_lanes;
     uint32_t max_slots = 0, gmax = 0, n_stages = 1, n_merges = 0;
+    // cluster plans (lower_cluster_plan): per owned segment the merges in
+    // level order; lvl_begin holds each segment's level offsets (n_levels + 1
+    // entries starting at lvl_start[sl]); seg_begin has n_seg + 1 entries
+    std::vector<uint32_t> lvl_start, lvl_begin;
+    uint32_t level_width = 1;  // most merges in one level
     // one lane per stage (plans built without the lane analysis)
     void single_lanes() {
         const size_t n_seg = seg_begin.size();
@@ -77,13 +88,15 @@ struct DevicePlan {
 
 // Lower the owned segments' merge DAGs into the device plan (runtime.cu).
 marsit_status lower_plan(const Plan& plan, uint32_t s_first, uint32_t n_seg, DevicePlan& dp);
+// The same for the cluster merge: levels of independent merges, shared-memory slots.
+marsit_status lower_cluster_plan(const Plan& plan, uint32_t s_first, uint32_t n_seg, DevicePlan& dp);
 
 // The cooperative merge of a set of owned segments (K2).  Chooses the words
 // per thread and splits each segment's tiles into parts so that one launch's
 // tiles are co-resident; launches stage x part.
 struct MergeRunner {
     DevicePlan dp;
-    uint32_t n_seg = 0, s_first = 0, words_proc = 0, wst = 0, ml = 0;
+    uint32_t n_seg = 0, s_first = 0, words_proc = 0, wst = 0, ml = 0, agg_stride = 0;
     uint64_t L = 0;
     int wpt = 1;
     size_t smem = 0;
@@ -101,13 +114,19 @@ struct MergeRunner {
     unsigned* seg_bars = nullptr;  // per-(segment, lane) barrier words (MARSIT_SEG_BARRIER)
     bool seg_barrier = env_int("MARSIT_SEG_BARRIER", 1) != 0;
     const uint32_t* const* peer_bits = nullptr;  // P2P transport: device table [G]
+    // cluster merge (default; MARSIT_MERGE_COOP=1: the cooperative kernel)
+    bool cluster = env_int("MARSIT_MERGE_COOP", 0) == 0;
+    uint32_t csize = 16, tile_groups = 0, nsub = 1;
+    uint32_t* d_lvl_start = nullptr;
+    uint32_t* d_lvl_begin = nullptr;
 
     MergeRunner() = default;
     MergeRunner(const MergeRunner&) = delete;
     MergeRunner& operator=(const MergeRunner&) = delete;
     ~MergeRunner() {
         for (void* p : {(void*)d_merges, (void*)d_seg_begin, (void*)d_stage_begin, (void*)gnodes,
-                        (void*)flags, (void*)part_totals, (void*)coin_end, (void*)seg_bars})
+                        (void*)flags, (void*)part_totals, (void*)coin_end, (void*)seg_bars,
+                        (void*)d_lvl_start, (void*)d_lvl_begin})
             if (p) cudaFree(p);
     }
 
@@ -118,6 +137,7 @@ struct MergeRunner {
     // launches (one GPU, many segments: the tiles no longer fit one
     // co-resident grid) the stages run as single lanes instead.
     marsit_status configure(int sm_count, uint32_t seg_launch = 0, int cta_limit = 0) {
+        if (cluster) return configure_cluster(seg_launch ? seg_launch : n_seg);
         marsit_status s = configure_once(sm_count, seg_launch, cta_limit);
         if (s || lanes_max == 1 || n_parts == 1) return s;
         const uint32_t parts_lanes = n_parts;
@@ -127,6 +147,48 @@ struct MergeRunner {
         if (n_parts < parts_lanes) return MARSIT_OK;
         dp = keep;
         return configure_once(sm_count, seg_launch, cta_limit);
+    }
+
+    // Cluster size and groups per thread: fewest waves of resident clusters
+    // for the segments of one launch, then the smallest CTA tile (the
+    // per-level deposit work of a CTA), + a fixed per-level sync cost.
+    // MARSIT_MERGE_CSIZE forces the CTAs per cluster.
+    marsit_status configure_cluster(uint32_t seg_launch) {
+        seg_per_launch = seg_launch;
+        n_parts = 1;
+        const uint32_t total_groups = words_proc / 4;
+        const int forced = env_int("MARSIT_MERGE_CSIZE", 0);
+        uint64_t best = ~0ull;
+        const uint32_t nl = dp.level_width;
+        for (uint32_t cs : {16u, 14u, 12u, 10u, 8u, 6u, 4u, 2u, 1u}) {
+            if (forced && cs != uint32_t(forced)) continue;
+            const uint32_t tg = uint32_t(ceil_div(total_groups, cs));
+            uint32_t ns = 0;
+            for (uint32_t c : {1u, 2u, 4u, 8u, 16u})
+                if (uint64_t(c) * kClusterThreads >= tg && (nl == 1 || c <= 8)) {
+                    ns = c;
+                    break;
+                }
+            if (!ns) continue;
+            const size_t sm = size_t(std::max<uint32_t>(dp.max_slots, 1)) * tg * 16;
+            if (sm > 200 * 1024) continue;
+            int occ = 0;
+            if (merge_cluster_occupancy(int(ns), int(nl), cs, sm, &occ) != cudaSuccess || occ <= 0) {
+                cudaGetLastError();
+                continue;
+            }
+            const uint64_t waves = ceil_div(seg_per_launch, uint64_t(occ));
+            const uint64_t cost = waves * (uint64_t(tg) + 400);
+            if (cost < best) {
+                best = cost;
+                csize = cs;
+                tile_groups = tg;
+                nsub = ns;
+                smem = sm;
+            }
+        }
+        if (best == ~0ull) return fail(MARSIT_EUNSUPPORTED, "merge clusters do not fit the device");
+        return MARSIT_OK;
     }
 
     marsit_status configure_once(int sm_count, uint32_t seg_launch, int cta_limit) {
@@ -202,6 +264,22 @@ struct MergeRunner {
         CUDA_TRY(cudaMalloc(&d_merges, sizeof(DevMerge) * nm));
         CUDA_TRY(cudaMemcpy(d_merges, dp.merges.data(), sizeof(DevMerge) * dp.n_merges,
                             cudaMemcpyHostToDevice));
+        if (cluster) {
+            auto put = [](uint32_t** d, const std::vector<uint32_t>& h) -> cudaError_t {
+                cudaError_t e = cudaMalloc(d, sizeof(uint32_t) * std::max<size_t>(h.size(), 1));
+                if (e == cudaSuccess && !h.empty())
+                    e = cudaMemcpy(*d, h.data(), sizeof(uint32_t) * h.size(), cudaMemcpyHostToDevice);
+                return e;
+            };
+            CUDA_TRY(put(&d_seg_begin, dp.seg_begin));
+            CUDA_TRY(put(&d_lvl_start, dp.lvl_start));
+            CUDA_TRY(put(&d_lvl_begin, dp.lvl_begin));
+            CUDA_TRY(cudaMalloc(&part_totals, sizeof(uint64_t) * nm));
+            CUDA_TRY(cudaMemset(part_totals, 0, sizeof(uint64_t) * nm));
+            CUDA_TRY(cudaMalloc(&coin_end, sizeof(uint64_t) * nm));
+            CUDA_TRY(cudaMemset(coin_end, 0xFF, sizeof(uint64_t) * nm));  // no history yet
+            return MARSIT_OK;
+        }
         CUDA_TRY(cudaMalloc(&d_seg_begin, sizeof(uint32_t) * dp.seg_begin.size()));
         CUDA_TRY(cudaMemcpy(d_seg_begin, dp.seg_begin.data(), sizeof(uint32_t) * dp.seg_begin.size(),
                             cudaMemcpyHostToDevice));
@@ -230,6 +308,37 @@ struct MergeRunner {
                       uint64_t round, cudaStream_t st, uint64_t* n_launch, uint32_t seg_lo = 0,
                       uint32_t seg_cnt = ~0u, const uint32_t* coin_valid = nullptr) {
         if (seg_cnt == ~0u) seg_cnt = n_seg - seg_lo;
+        if (cluster) {
+            ClusterParams c{};
+            c.merges = d_merges;
+            c.seg_begin = d_seg_begin;
+            c.lvl_start = d_lvl_start;
+            c.lvl_begin = d_lvl_begin;
+            c.n_seg = n_seg;
+            c.s_first = s_first;
+            c.seg_lo = seg_lo;
+            c.csize = csize;
+            c.tile_groups = tile_groups;
+            c.words_proc = words_proc;
+            c.wst = wst;
+            c.ml = ml;
+            c.n_slots = dp.max_slots;
+            c.seg_bits = L;
+            c.leaves = leaves;
+            c.peer_bits = peer_bits;
+            c.agg = agg;
+            c.agg_stride = agg_stride ? agg_stride : wst;
+            c.coins = coins;
+            c.coin_valid = coins ? coin_valid : nullptr;
+            c.totals = part_totals;
+            c.coin_end = coin_end;
+            c.seed = seed;
+            c.round = round;
+            if (seg_cnt == 0) return MARSIT_OK;
+            CUDA_TRY(launch_merge_cluster(c, int(nsub), int(dp.level_width), seg_cnt, smem, st));
+            ++*n_launch;
+            return MARSIT_OK;
+        }
         CoopParams c{};
         c.merges = d_merges;
         c.seg_begin = d_seg_begin;
@@ -252,6 +361,7 @@ struct MergeRunner {
         c.gnodes = gnodes;
         c.gmax = std::max<uint32_t>(dp.gmax, 1);
         c.agg = agg;
+        c.agg_stride = agg_stride ? agg_stride : wst;
         c.coins = coins;
         c.flags = flags;
         c.part_totals = part_totals;
@@ -283,6 +393,47 @@ struct MergeRunner {
 struct TimedPair {
     int phase;
     cudaEvent_t a, b;
+};
+
+// Device error latch bits (marsit_ctx::err, reported by marsit_ctx_check).
+constexpr int kErrNonFinite = 1;  // DenseVector finiteness (dense_vector.hpp:25-29)
+constexpr int kErrConsensus = 2;  // an aggregate segment differs from its owner's (allreduce.hpp:32-43)
+
+// P2P flag value that releases every stream wait: written by a watchdog that
+// gave up (into its own flags and into its slot of every peer's flags) so no
+// stream stays blocked; a peer that sees it reports the abort.
+constexpr uint64_t kFlagAbort = ~0ull;
+
+// Bounded waits for multi-rank contexts (P2P epoch flags, NCCL collectives).
+// The round entry points hand every enqueued round to this thread; if a round
+// has not completed after the timeout (or NCCL reports an asynchronous error,
+// or a peer posted kFlagAbort), the context is marked failed: P2P waits are
+// released by writing kFlagAbort into the local flags and the peers' slots,
+// NCCL communicators are aborted, and every later call on the context
+// returns the latched status (EPROTOCOL / ENCCL) instead of hanging — the
+// reference's contract for a broken wire is protocol_error (errors.hpp:24-29).
+struct Watchdog {
+    struct Item {
+        cudaEvent_t ev;
+        std::chrono::steady_clock::time_point t0;
+        uint64_t epoch;
+    };
+    marsit_ctx* ctx = nullptr;
+    std::thread th;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<Item> pending;
+    std::vector<cudaEvent_t> free_events;
+    bool stop = false;
+    cudaStream_t st = nullptr;        // private stream: flag reads and releases
+    cudaEvent_t ev_poll = nullptr;
+    uint64_t* h_flags = nullptr;      // pinned copy of the local flags [2][G]
+
+    explicit Watchdog(marsit_ctx* c);
+    ~Watchdog();
+    marsit_status watch(cudaStream_t s, uint64_t epoch);  // after a round was enqueued on s
+    void loop();
+    void give_up(marsit_status st, const std::string& msg);
 };
 
 
@@ -319,7 +470,8 @@ struct marsit_ctx {
     // device buffers
     uint32_t* bits = nullptr;  // [S][ml][wst]
     uint32_t* recv = nullptr;  // [G][s_own][ml][wst]   (G > 1)
-    uint32_t* agg = nullptr;   // [S][wst]
+    uint32_t* agg = nullptr;   // [S][wsa]: wst words, then the segment's u64 owner hash (consensus)
+    uint32_t wsa = 0;          // aggregate row stride in u32 words (wst + 4)
     int* err = nullptr;
     int stream_grid = 0;   // generic grid-stride kernels
     int extract_grid = 0;  // persistent, one wave of resident CTAs
@@ -375,6 +527,20 @@ struct marsit_ctx {
     unsigned long long* d_metrics = nullptr;  // [0] matches, [1..2] NCCL sum scratch
     bool last_valid = false, last_dense = false, last_matching = false;
     uint64_t last_t = 0;
+    // failure handling: a latched failure (status, message) makes every later
+    // call return it; the watchdog bounds waits on peers / NCCL
+    std::atomic<int> fail_status{0};
+    mutable std::mutex fail_mu;
+    std::string fail_msg;
+    uint64_t wait_timeout_ms = uint64_t(marsit_b200::env_int("MARSIT_WAIT_TIMEOUT_MS", 120000));
+    std::unique_ptr<marsit_b200::Watchdog> watchdog;
+    // opt-in data consensus (allreduce.hpp:32-43): owners hash their aggregate
+    // segments after the merge; after the decode every rank re-hashes all S
+    // segments as it reads them and compares
+    bool consensus = false;
+    unsigned long long* d_verify = nullptr;  // [S] re-hashed segments
+    cudaEvent_t ev_check = nullptr;          // marsit_ctx_check's stream poll
+    uint64_t* h_check = nullptr;             // pinned: error latch, then the P2P flags [2][G]
     // timing
     bool timing = false;
     std::vector<marsit_b200::TimedPair> pending;
@@ -411,5 +577,12 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
                                   marsit_ctx** out);
 // Payload bits of one round (allreduce.hpp:113, 182).
 uint64_t round_bits_total(const marsit_ctx* ctx, bool dense);
+// The latched failure of a context (MARSIT_OK when healthy); sets the
+// thread-local message.
+marsit_status ctx_failed(const marsit_ctx* ctx);
+void ctx_set_failed(marsit_ctx* ctx, marsit_status st, const std::string& msg);
+// Hand the round just enqueued on `st` to the context's watchdog (no-op for
+// single-rank contexts).
+marsit_status watch_round(marsit_ctx* ctx, cudaStream_t st);
 
 }  // namespace marsit_b200

@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kStreamThreads, sizeof(T) == 4 ? (VEC ? 4 : 3)
 template <typename T>
 __device__ __forceinline__ const uint32_t* agg_row(const StreamParams<T>& p, uint32_t s) {
     const uint32_t* base = p.agg_peers ? p.agg_peers[s / p.s_own] : p.agg;
-    return base + uint64_t(s) * p.wst;
+    return base + uint64_t(s) * p.wsa;
 }
 
 // XU: the replica update x -= g_t is fused (its quads are loaded with g and c,
@@ -393,9 +393,10 @@ __global__ void __launch_bounds__(kStreamThreads,
 // HBM traffic.  matches += [aggregate bit == (sum / M >= 0)] over the D
 // coordinates.  Needs every worker of the job local (p.ml == M).
 // ---------------------------------------------------------------------------
-// (sum / M >= 0) of the worker-order fp64 sum of u (trainer.hpp:249): for
-// fp32 u a negative sum is at most -2^-149 and sum / M cannot round to -0,
-// so the sign of the sum decides without the division; fp64 u can be
+// (sum / M >= 0) of the worker-order fp64 sum of u = g + c (trainer.hpp:249):
+// for fp32 inputs every u and hence the exact sum is a multiple of 2^-149, so
+// a negative rounded fp64 sum is at most -2^-149 and sum / M cannot round to
+// -0: the sign of the sum decides without the division; fp64 u can be
 // subnormal, so a negative sum still takes the literal division.
 template <typename T>
 __device__ __forceinline__ bool mean_nonneg(double sum, double m) {
@@ -403,10 +404,18 @@ __device__ __forceinline__ bool mean_nonneg(double sum, double m) {
     return sizeof(T) == 8 && __ddiv_rn(sum, m) >= 0.0;
 }
 
+// u in fp64 as the trainer forms it (add(g, c) on doubles, trainer.hpp:247):
+// for fp32 inputs the exact sum of the two fp32 values, not the fp32-rounded u
+// of the compensation update (the two can differ in the sign of the mean).
+__device__ __forceinline__ double u64_of(float g, float c) { return __dadd_rn(double(g), double(c)); }
+__device__ __forceinline__ double u64_of(double g, double c) { return __dadd_rn(g, c); }
+
 template <typename T>
 __device__ __forceinline__ void decode_one(const StreamParams<T>& p, uint32_t wl, uint64_t gi,
-                                           T gt, T& u) {
-    u = add_rn(p.g[wl][gi], p.c[wl][gi]);
+                                           T gt, double& u64) {
+    const T g = p.g[wl][gi], c = p.c[wl][gi];
+    const T u = add_rn(g, c);
+    u64 = u64_of(g, c);
     p.c_out[wl][gi] = sub_rn(u, gt);
     if (wl == 0 && p.update) p.update[gi] = gt;
     if (p.x[wl]) p.x[wl][gi] = sub_rn(p.x[wl][gi], gt);
@@ -474,7 +483,7 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 80 : 128) decode_stats_kernel(const
                         for (int k = 0; k < 4; ++k) {
                             const T gt = ((nib[h] >> k) & 1u) ? eta : -eta;
                             const T u = add_rn(gv[h].v[k], cv[h].v[k]);
-                            sum[h][k] = __dadd_rn(sum[h][k], double(u));
+                            sum[h][k] = __dadd_rn(sum[h][k], u64_of(gv[h].v[k], cv[h].v[k]));
                             out.v[k] = sub_rn(u, gt);
                             up.v[k] = gt;
                         }
@@ -510,9 +519,9 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 80 : 128) decode_stats_kernel(const
                     const T gt = bit ? eta : -eta;
                     double sum = 0.0;
                     for (uint32_t wl = 0; wl < p.ml; ++wl) {
-                        T u;
+                        double u;
                         decode_one(p, wl, gi, gt, u);
-                        sum = __dadd_rn(sum, double(u));
+                        sum = __dadd_rn(sum, u);
                     }
                     matches += (bit != 0) == mean_nonneg<T>(sum, wm);
                 }
@@ -884,7 +893,7 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
                         cslots[(m.out_slot * WPT + j) * kMergeThreads + tid] = r[j];
                 }
                 if (m.out_global == kFinal) {
-                    uint32_t* dst = p.agg + uint64_t(sg) * p.wst + w0;
+                    uint32_t* dst = p.agg + uint64_t(sg) * p.agg_stride + w0;
 #pragma unroll
                     for (int j = 0; j < WPT; ++j)
                         if (!tail || w0 + j < p.words_proc) dst[j] = r[j];
@@ -905,6 +914,227 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
         COOP_ADD(2, t3 - t2);
         COOP_ADD(3, t4 - t3);
         COOP_ADD(4, 1);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2 (cluster): one thread-block cluster per owned segment runs the whole
+// merge DAG of the segment (see ClusterParams).  Per level of up to NL
+// independent merges:
+//   pass 1  every thread: d = (r ^ l) & valid for its NSUB 4-word groups of
+//           each merge, popcounts, warp scans;
+//           CTA scan of the NL x NSUB columns (two block barriers);
+//           each CTA stores its per-merge totals into slot [its rank] of
+//           every cluster CTA's shared memory (st.shared::cluster), then
+//           barrier.cluster arrive.release / wait.acquire;
+//   prefix  the draw offset of a group = stream base (earlier merges of the
+//           same stream, shared memory) + totals of the lower-ranked CTAs
+//           (local shared memory after the barrier) + the CTA-local prefix;
+//   pass 2  coins of the group's draws (precomputed bitstream, L2) deposited
+//           onto the set bits of d; out = r ^ (d & ~coin) (merge.hpp:44-53):
+//           a shared-memory slot for a later level, or the aggregate.
+// The cluster totals double-buffer by level parity: a CTA overwrites slot
+// [v & 1] of a peer only after the barrier of level v + 1, which the peer
+// passes only after reading level v's values.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 64-bit store into CTA `rank`'s shared memory at the address of `local` (DSMEM)
+__device__ __forceinline__ void st_cluster_u64(void* local, uint32_t rank, unsigned long long v) {
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local));
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    asm volatile("st.shared::cluster.u64 [%0], %1;" :: "r"(ra), "l"(v) : "memory");
+}
+
+template <int NSUB, int NL>
+__global__ void __launch_bounds__(kClusterThreads, 1) merge_cluster_kernel(const ClusterParams p) {
+    extern __shared__ uint4 cl_slots[];  // [n_slots][tile_groups] node values of this CTA's tile
+    constexpr int NCOL = NL * NSUB;
+    constexpr int NW = kClusterThreads / 32;
+    __shared__ uint32_t s_wt[NCOL][NW];    // warp totals per column
+    __shared__ uint32_t s_wpre[NCOL][NW];  // exclusive warp prefix per column
+    __shared__ uint32_t s_ctot[NCOL];      // CTA total per column
+    __shared__ unsigned long long s_all[2][kMaxClusterSize][NL];  // CTA totals of the cluster
+    __shared__ DevMerge s_m[kMaxSegMerges];
+    __shared__ unsigned long long s_tot[kMaxSegMerges];  // cluster-wide draws of each merge
+    __shared__ uint32_t s_valid[kMaxSegMerges];
+    __shared__ uint32_t s_lvl[kMaxSegMerges + 1];
+
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t cr = cluster_ctarank();
+    const uint32_t sl = p.seg_lo + blockIdx.x / p.csize;
+    const uint32_t sg = p.s_first + sl;
+    const uint32_t mb = p.seg_begin[sl], nm = p.seg_begin[sl + 1] - mb;
+    const uint32_t lb0 = p.lvl_start[sl], nlv = p.lvl_start[sl + 1] - lb0 - 1;
+    for (uint32_t i = tid; i < nm; i += kClusterThreads) {
+        s_m[i] = p.merges[mb + i];
+        s_tot[i] = 0;
+        s_valid[i] = p.coin_valid ? p.coin_valid[mb + i] : 0u;
+    }
+    for (uint32_t i = tid; i <= nlv; i += kClusterThreads) s_lvl[i] = p.lvl_begin[lb0 + i];
+    // every CTA of the cluster is running before the first remote store
+    cluster_sync_all();
+
+    const uint32_t total_groups = p.words_proc / 4;
+    const uint32_t g_first = cr * p.tile_groups;
+    // group u of this thread: local index gl = u * kClusterThreads + tid,
+    // segment words [4 g, 4 g + 4) with g = g_first + gl
+    auto group_ok = [&](int u) -> bool {
+        const uint32_t gl = uint32_t(u) * kClusterThreads + tid;
+        return gl < p.tile_groups && g_first + gl < total_groups;
+    };
+    auto vmask = [&](uint32_t word) -> uint32_t {
+        const int64_t rem = int64_t(p.seg_bits) - int64_t(word) * 32;
+        return rem >= 32 ? kFull : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+    };
+    auto load_src = [&](uint16_t src, int u) -> uint4 {
+        const uint32_t idx = src & 0x3FFFu;
+        const uint32_t gl = uint32_t(u) * kClusterThreads + tid;
+        if ((src & 0xC000u) == kSrcSlot) return cl_slots[size_t(idx) * p.tile_groups + gl];
+        const uint32_t g = g_first + gl;
+        if (p.peer_bits) {  // P2P: the source rank's own buffer, over NVLink
+            const uint32_t* row = p.peer_bits[idx / p.ml] + (uint64_t(sg) * p.ml + idx % p.ml) * p.wst;
+            return __ldcg(reinterpret_cast<const uint4*>(row) + g);
+        }
+        const uint32_t* row =
+            p.leaves + (uint64_t((idx / p.ml) * p.n_seg + sl) * p.ml + idx % p.ml) * p.wst;
+        return __ldg(reinterpret_cast<const uint4*>(row) + g);
+    };
+    auto diff = [&](const DevMerge& m, int u, uint32_t (&r)[4], uint32_t (&d)[4]) {
+        const uint4 a = load_src(m.recv_src, u), b = load_src(m.local_src, u);
+        const uint32_t w0 = (g_first + uint32_t(u) * kClusterThreads + tid) * 4;
+        r[0] = a.x, r[1] = a.y, r[2] = a.z, r[3] = a.w;
+        d[0] = (a.x ^ b.x) & vmask(w0);
+        d[1] = (a.y ^ b.y) & vmask(w0 + 1);
+        d[2] = (a.z ^ b.z) & vmask(w0 + 2);
+        d[3] = (a.w ^ b.w) & vmask(w0 + 3);
+    };
+
+    for (uint32_t v = 0; v < nlv; ++v) {
+        const uint32_t k0 = s_lvl[v], nk = s_lvl[v + 1] - k0;
+        // pass 1: counts and warp scans
+        uint32_t ex[NL][NSUB];
+#pragma unroll
+        for (int i = 0; i < NL; ++i)
+#pragma unroll
+            for (int u = 0; u < NSUB; ++u) {
+                uint32_t c = 0;
+                if (uint32_t(i) < nk && group_ok(u)) {
+                    uint32_t r[4], d[4];
+                    diff(s_m[k0 + i], u, r, d);
+                    c = __popc(d[0]) + __popc(d[1]) + __popc(d[2]) + __popc(d[3]);
+                }
+                uint32_t incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                ex[i][u] = incl - c;
+                if (lane == 31) s_wt[i * NSUB + u][wid] = incl;
+            }
+        __syncthreads();
+        if (wid < NCOL) {
+            const uint32_t x = s_wt[wid][lane];
+            uint32_t incl = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += y;
+            }
+            s_wpre[wid][lane] = incl - x;
+            if (lane == 31) s_ctot[wid] = incl;
+        }
+        __syncthreads();
+        // this CTA's per-merge totals into every cluster CTA's slot [v & 1][cr]
+        if (uint32_t(tid) < p.csize) {
+#pragma unroll
+            for (int i = 0; i < NL; ++i) {
+                unsigned long long t = 0;
+#pragma unroll
+                for (int u = 0; u < NSUB; ++u) t += s_ctot[i * NSUB + u];
+                st_cluster_u64(&s_all[v & 1][cr][i], uint32_t(tid), t);
+            }
+        }
+        cluster_sync_all();
+        // pass 2: draw offsets, coins, deposit
+#pragma unroll
+        for (int i = 0; i < NL; ++i) {
+            if (uint32_t(i) >= nk) continue;
+            const uint32_t k = k0 + i;
+            const DevMerge& m = s_m[k];
+            unsigned long long pre = 0, tot = 0;
+            for (uint32_t q = 0; q < p.csize; ++q) {
+                const unsigned long long x = s_all[v & 1][q][i];
+                pre += q < cr ? x : 0ull;
+                tot += x;
+            }
+            // stream base: draws before this round's merges + the earlier
+            // merges of the same (receiver, segment) stream (continuation)
+            uint64_t base = m.base_add;
+            for (int32_t src = m.offset_src; src >= 0; src = s_m[src].offset_src)
+                base += s_tot[src] + s_m[src].base_add;
+            if (tid == 0) {
+                s_tot[k] = tot;  // read by later levels (after their block barriers)
+                if (cr == 0) {
+                    if (p.totals) p.totals[mb + k] = tot;
+                    if (p.coin_end) p.coin_end[mb + k] = base + tot;
+                }
+            }
+            const uint64_t valid_bits = uint64_t(s_valid[k]) * 32;
+            const uint32_t* cw = p.coins ? p.coins + m.coin_off : nullptr;
+            uint64_t col_off = 0;  // totals of this CTA's earlier columns of merge i
+#pragma unroll
+            for (int u = 0; u < NSUB; ++u) {
+                const uint64_t off_u = col_off;
+                col_off += s_ctot[i * NSUB + u];
+                if (!group_ok(u)) continue;
+                uint32_t r[4], d[4];
+                diff(m, u, r, d);
+                const uint32_t cnt = __popc(d[0]) + __popc(d[1]) + __popc(d[2]) + __popc(d[3]);
+                uint64_t n = base + pre + off_u + s_wpre[i * NSUB + u][wid] + ex[i][u];
+                if (cw && n + cnt <= valid_bits) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t pc = __popc(d[j]);
+                        if (pc) {
+                            const uint64_t wi = n >> 5;
+                            const uint32_t sh = uint32_t(n & 31);
+                            const uint32_t c0 = __ldg(cw + wi);
+                            const uint32_t c1 = (sh + pc > 32) ? __ldg(cw + wi + 1) : 0u;
+                            uint32_t mv[4];
+                            expand_masks(d[j], mv);
+                            r[j] ^= d[j] & ~expand_apply(__funnelshift_r(c0, c1, sh), mv);
+                            n += pc;
+                        }
+                    }
+                } else {
+                    // beyond the precomputed budget: draw inline (same stream, same indices)
+                    const uint64_t key = m.key_mode ? m.key : stream_key(p.seed, 5, m.receiver, p.round, sg);
+                    uint64_t z = key + (n + 1) * kGamma;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) r[j] ^= d[j] & ~coin_word(d[j], z, m.thresh11);
+                }
+                const uint4 out = make_uint4(r[0], r[1], r[2], r[3]);
+                const uint32_t gl = uint32_t(u) * kClusterThreads + tid;
+                if (m.out_slot != kNone) cl_slots[size_t(m.out_slot) * p.tile_groups + gl] = out;
+                if (m.out_global == kFinal)
+                    reinterpret_cast<uint4*>(p.agg + uint64_t(sg) * p.agg_stride)[g_first + gl] = out;
+            }
+        }
+        // no block barrier here: slots are read back by the threads that
+        // wrote them, and s_wt / s_wpre / s_ctot are rewritten next level
+        // only after that level's first block barrier... except s_ctot /
+        // s_wpre, which this level still reads above: the next level writes
+        // them after its first __syncthreads, which every thread reaches
+        // only after finishing this pass.
     }
 }
 
@@ -1007,6 +1237,40 @@ __global__ void export_bits_kernel(const uint32_t* __restrict__ agg, uint32_t ws
             }
         }
         out[k] = val;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Consensus hashes (see launch_seg_hash): blockIdx.y = segment, grid-stride
+// over its words, XOR-reduced per warp, one atomic per warp.
+// ---------------------------------------------------------------------------
+__global__ void seg_hash_kernel(const uint32_t* agg, const uint32_t* const* agg_peers,
+                                uint32_t s_own, uint32_t wsa, uint32_t wst, uint32_t words_proc,
+                                uint32_t s0, unsigned long long* out) {
+    const uint32_t s = s0 + blockIdx.y;
+    const uint32_t* row = (agg_peers ? agg_peers[s / s_own] : agg) + uint64_t(s) * wsa;
+    const uint64_t salt = (uint64_t(s) + 1) * kGamma;
+    uint64_t h = 0;
+    for (uint32_t wi = blockIdx.x * blockDim.x + threadIdx.x; wi < words_proc;
+         wi += gridDim.x * blockDim.x)
+        h ^= mix64(((uint64_t(wi) << 32) | __ldcg(row + wi)) + salt);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) h ^= __shfl_xor_sync(kFull, h, o);
+    if ((threadIdx.x & 31) == 0 && h) {
+        unsigned long long* dst =
+            out ? out + s : reinterpret_cast<unsigned long long*>(const_cast<uint32_t*>(row) + wst);
+        atomicXor(dst, (unsigned long long)h);
+    }
+}
+
+__global__ void hash_compare_kernel(const uint32_t* agg, const uint32_t* const* agg_peers,
+                                    uint32_t s_own, uint32_t wsa, uint32_t wst, uint32_t n_seg,
+                                    const unsigned long long* verify, int* err) {
+    for (uint32_t s = threadIdx.x; s < n_seg; s += blockDim.x) {
+        const uint32_t* row = (agg_peers ? agg_peers[s / s_own] : agg) + uint64_t(s) * wsa;
+        const unsigned long long stored =
+            __ldcg(reinterpret_cast<const unsigned long long*>(row + wst));
+        if (stored != verify[s]) atomicOr(err, 2);
     }
 }
 
@@ -1431,6 +1695,80 @@ cudaError_t merge_coop_occupancy(int wpt, size_t smem, int* blocks) {
     }
 }
 
+template <int NSUB, int NL>
+static cudaError_t cluster_attr(size_t smem) {
+    auto k = merge_cluster_kernel<NSUB, NL>;
+    static cudaError_t e = [&] {
+        cudaError_t r = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        return r;
+    }();
+    (void)smem;
+    return e;
+}
+
+template <int NSUB, int NL>
+static cudaError_t cluster_launch_t(const ClusterParams& p, uint32_t clusters, size_t smem,
+                                    cudaStream_t st) {
+    cudaError_t e = cluster_attr<NSUB, NL>(smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(clusters * p.csize);
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, merge_cluster_kernel<NSUB, NL>, p);
+}
+
+template <int NSUB, int NL>
+static cudaError_t cluster_occ_t(uint32_t csize, size_t smem, int* clusters) {
+    cudaError_t e = cluster_attr<NSUB, NL>(smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(csize);
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaOccupancyMaxActiveClusters(clusters, merge_cluster_kernel<NSUB, NL>, &cfg);
+}
+
+#define MARSIT_CLUSTER_DISPATCH(FN, ...)                                 \
+    switch (nl * 100 + nsub) {                                           \
+        case 101: return FN<1, 1>(__VA_ARGS__);                          \
+        case 102: return FN<2, 1>(__VA_ARGS__);                          \
+        case 104: return FN<4, 1>(__VA_ARGS__);                          \
+        case 108: return FN<8, 1>(__VA_ARGS__);                          \
+        case 116: return FN<16, 1>(__VA_ARGS__);                         \
+        case 201: return FN<1, 2>(__VA_ARGS__);                          \
+        case 202: return FN<2, 2>(__VA_ARGS__);                          \
+        case 204: return FN<4, 2>(__VA_ARGS__);                          \
+        case 208: return FN<8, 2>(__VA_ARGS__);                          \
+        default: return cudaErrorInvalidValue;                           \
+    }
+
+cudaError_t launch_merge_cluster(const ClusterParams& p, int nsub, int nl, uint32_t clusters,
+                                 size_t smem, cudaStream_t st) {
+    MARSIT_CLUSTER_DISPATCH(cluster_launch_t, p, clusters, smem, st)
+}
+
+cudaError_t merge_cluster_occupancy(int nsub, int nl, uint32_t csize, size_t smem, int* clusters) {
+    MARSIT_CLUSTER_DISPATCH(cluster_occ_t, csize, smem, clusters)
+}
+
 cudaError_t stream_occupancy(bool f64, int* extract_blocks, int* decode_blocks) {
     cudaError_t e;
     if (f64) {
@@ -1472,6 +1810,24 @@ cudaError_t launch_export_bits(const uint32_t* agg, uint32_t wst, uint64_t dim, 
     if (blocks > 148 * 8) blocks = 148 * 8;
     export_bits_kernel<<<int(blocks), threads, 0, st>>>(agg, wst, dim, seg_len, n_out, out_u32,
                                                         agg_peers, s_own);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_seg_hash(const uint32_t* agg, const uint32_t* const* agg_peers, uint32_t s_own,
+                            uint32_t wsa, uint32_t wst, uint32_t words_proc, uint32_t s0,
+                            uint32_t n_seg, unsigned long long* out, cudaStream_t st) {
+    if (n_seg == 0) return cudaSuccess;
+    uint32_t gx = (words_proc + 256 * 16 - 1) / (256 * 16);
+    gx = gx < 1 ? 1 : (gx > 64 ? 64 : gx);
+    seg_hash_kernel<<<dim3(gx, n_seg), 256, 0, st>>>(agg, agg_peers, s_own, wsa, wst, words_proc, s0,
+                                                     out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hash_compare(const uint32_t* agg, const uint32_t* const* agg_peers,
+                                uint32_t s_own, uint32_t wsa, uint32_t wst, uint32_t n_seg,
+                                const unsigned long long* verify, int* err, cudaStream_t st) {
+    hash_compare_kernel<<<1, 256, 0, st>>>(agg, agg_peers, s_own, wsa, wst, n_seg, verify, err);
     return cudaGetLastError();
 }
 
@@ -1609,9 +1965,20 @@ cudaError_t preload_kernels() {
             reinterpret_cast<const void*>(merge_coop_kernel<8>),
             reinterpret_cast<const void*>(merge_coop_kernel<12>),
             reinterpret_cast<const void*>(merge_coop_kernel<16>),
+            reinterpret_cast<const void*>(merge_cluster_kernel<1, 1>),
+            reinterpret_cast<const void*>(merge_cluster_kernel<2, 1>),
+            reinterpret_cast<const void*>(merge_cluster_kernel<4, 1>),
+            reinterpret_cast<const void*>(merge_cluster_kernel<8, 1>),
+            reinterpret_cast<const void*>(merge_cluster_kernel<16, 1>),
+            reinterpret_cast<const void*>(merge_cluster_kernel<1, 2>),
+            reinterpret_cast<const void*>(merge_cluster_kernel<2, 2>),
+            reinterpret_cast<const void*>(merge_cluster_kernel<4, 2>),
+            reinterpret_cast<const void*>(merge_cluster_kernel<8, 2>),
             reinterpret_cast<const void*>(coins_kernel),
             reinterpret_cast<const void*>(export_bits_kernel),
             reinterpret_cast<const void*>(flag_write_kernel),
+            reinterpret_cast<const void*>(seg_hash_kernel),
+            reinterpret_cast<const void*>(hash_compare_kernel),
             reinterpret_cast<const void*>(dense_leaf_kernel<float>),
             reinterpret_cast<const void*>(dense_leaf_kernel<double>),
             reinterpret_cast<const void*>(dense_reduce_kernel<float>),

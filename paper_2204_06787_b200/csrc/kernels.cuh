@@ -66,7 +66,8 @@ struct CoopParams {
     const uint32_t* const* peer_bits;
     uint32_t* gnodes;             // [n_seg][gmax][wst] nodes crossing stages
     uint32_t gmax;
-    uint32_t* agg;                // [S][wst]
+    uint32_t* agg;                // [S][agg_stride]
+    uint32_t agg_stride;          // u32 words per aggregate row
     const uint32_t* coins;        // precomputed coin bitstreams
     uint64_t* flags;              // [k_steps][CTAs] popcount of each tile
     uint64_t* part_totals;        // [n_parts][n_merges] draws consumed per (part, merge)
@@ -80,6 +81,47 @@ struct CoopParams {
 };
 cudaError_t launch_merge_coop(const CoopParams& p, int wpt, size_t smem, cudaStream_t st);
 cudaError_t merge_coop_occupancy(int wpt, size_t smem, int* blocks_per_sm);
+
+// Cluster merge (kernels.cu, K2): one thread-block cluster of csize CTAs per
+// owned segment runs the segment's whole merge DAG in one launch.  A CTA owns
+// a contiguous tile of tile_groups 4-word groups of the segment; its
+// kClusterThreads threads own groups u * kClusterThreads + tid (NSUB of
+// them).  The merges run level by level (a level = up to NL independent
+// merges); per level: popcount of r ^ l, one CTA scan, each CTA pushes its
+// per-merge totals into every CTA's shared memory (DSMEM) and one cluster
+// barrier gives every CTA its draw offset — no grid-wide barrier, no global
+// flags.  DAG intermediates stay in shared memory (slots); leaves are read
+// from the extract's packed signs (or a peer rank's, P2P); the final node
+// goes to the aggregate.  Clusters never wait on each other, so segments
+// beyond one wave of resident clusters simply run later.
+constexpr int kClusterThreads = 1024;
+constexpr int kMaxClusterSize = 16;  // non-portable cluster size
+constexpr int kMaxLevelMerges = 2;
+constexpr int kMaxSegMerges = 64;    // merges of one segment staged in shared memory
+struct ClusterParams {
+    const DevMerge* merges;       // owned segments' merges, level order per segment
+    const uint32_t* seg_begin;    // [n_seg + 1] first merge of each owned segment
+    const uint32_t* lvl_start;    // [n_seg + 1] first entry of each segment in lvl_begin
+    const uint32_t* lvl_begin;    // per segment: n_levels + 1 merge offsets (within the segment)
+    uint32_t n_seg, s_first, seg_lo;  // this launch: owned segments [seg_lo, seg_lo + clusters)
+    uint32_t csize;               // CTAs per cluster
+    uint32_t tile_groups;         // 4-word groups per CTA tile
+    uint32_t words_proc, wst, ml, n_slots;
+    uint64_t seg_bits;            // L
+    const uint32_t* leaves;       // leaf(w, sl) = leaves + ((w/ml*n_seg + sl)*ml + w%ml)*wst
+    const uint32_t* const* peer_bits;  // P2P: leaf(w, sl) = peer_bits[w/ml] + ((s_first+sl)*ml + w%ml)*wst
+    uint32_t* agg;                // [S][agg_stride]
+    uint32_t agg_stride;
+    const uint32_t* coins;        // precomputed coin bitstreams (null: every draw inline)
+    const uint32_t* coin_valid;   // words computed per merge (null: none)
+    uint64_t* totals;             // [n_merges] draws consumed by each merge
+    uint64_t* coin_end;           // [n_merges] stream index after each merge (adaptive coins)
+    uint64_t seed, round;
+};
+cudaError_t launch_merge_cluster(const ClusterParams& p, int nsub, int nl, uint32_t clusters,
+                                 size_t smem, cudaStream_t st);
+// Concurrently resident clusters of csize CTAs with `smem` dynamic bytes (0 if unsupported).
+cudaError_t merge_cluster_occupancy(int nsub, int nl, uint32_t csize, size_t smem, int* clusters);
 
 template <typename T>
 struct StreamParams {
@@ -96,7 +138,8 @@ struct StreamParams {
     // alternates by round so consecutive rounds never share a cache warm-up
     uint32_t reverse;
     uint32_t* bits;              // extract output: [S][ml][wst]
-    const uint32_t* agg;         // decode input: [S][wst]
+    const uint32_t* agg;         // decode input: [S][wsa]
+    uint32_t wsa;                // aggregate row stride (u32 words)
     // P2P transport: segment s is read from its owner's buffer agg_peers[s / s_own]
     const uint32_t* const* agg_peers;
     uint32_t s_own;
@@ -133,6 +176,21 @@ struct FlagSlots {
     uint32_t n;
 };
 cudaError_t launch_flag_write(const FlagSlots& s, unsigned long long value, cudaStream_t st);
+// Opt-in data consensus (allreduce.hpp:32-43 on the device): the hash of an
+// aggregate segment s is the XOR over its words wi < words_proc of
+// mix64(((u64)wi << 32 | word) + (s + 1) * gamma) (order independent).
+// seg_hash XORs the hashes of segments [s0, s0 + n_seg) into out[s] (out
+// non-null) or into the segment's own hash slot, the u64 after its wst words
+// in the aggregate row (out null; the slot must be zero).  Rows are read from
+// agg_peers[s / s_own] when given, else from agg.  hash_compare latches
+// err |= 2 for every segment whose slot (the owner's hash, as read here)
+// differs from verify[s].
+cudaError_t launch_seg_hash(const uint32_t* agg, const uint32_t* const* agg_peers, uint32_t s_own,
+                            uint32_t wsa, uint32_t wst, uint32_t words_proc, uint32_t s0,
+                            uint32_t n_seg, unsigned long long* out, cudaStream_t st);
+cudaError_t launch_hash_compare(const uint32_t* agg, const uint32_t* const* agg_peers,
+                                uint32_t s_own, uint32_t wsa, uint32_t wst, uint32_t n_seg,
+                                const unsigned long long* verify, int* err, cudaStream_t st);
 // Loads every kernel of the library (instead of lazily at first launch).
 cudaError_t preload_kernels();
 // x_w -= v for the local workers' parameter replicas (dense-round update).

@@ -40,6 +40,183 @@ marsit_status fail(marsit_status st, const std::string& msg) {
     return st;
 }
 
+marsit_status ctx_failed(const marsit_ctx* ctx) {
+    const int st = ctx->fail_status.load();
+    if (!st) return MARSIT_OK;
+    std::lock_guard<std::mutex> lock(ctx->fail_mu);
+    return fail(marsit_status(st), ctx->fail_msg);
+}
+
+void ctx_set_failed(marsit_ctx* ctx, marsit_status st, const std::string& msg) {
+    std::lock_guard<std::mutex> lock(ctx->fail_mu);
+    if (ctx->fail_status.load()) return;  // the first failure wins
+    ctx->fail_msg = msg;
+    ctx->fail_status.store(int(st));
+}
+
+// Wait for everything enqueued on `st` so far by polling an event (never
+// blocking inside the driver: a thread blocked in a synchronous call can hold
+// up the watchdog's own calls that would release the wait).
+cudaError_t poll_stream(cudaStream_t st, cudaEvent_t ev) {
+    cudaError_t e = cudaEventRecord(ev, st);
+    if (e != cudaSuccess) return e;
+    for (;;) {
+        e = cudaEventQuery(ev);
+        if (e != cudaErrorNotReady) return e;
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Watchdog (see internal.hpp)
+// ---------------------------------------------------------------------------
+Watchdog::Watchdog(marsit_ctx* c) : ctx(c) {
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ev_poll, cudaEventDisableTiming);
+    cudaHostAlloc(reinterpret_cast<void**>(&h_flags), 2 * size_t(ctx->G) * sizeof(uint64_t),
+                  cudaHostAllocDefault);
+    th = std::thread([this] { loop(); });
+}
+
+Watchdog::~Watchdog() {
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        stop = true;
+    }
+    cv.notify_all();
+    if (th.joinable()) th.join();
+    for (auto& it : pending) cudaEventDestroy(it.ev);
+    for (auto e : free_events) cudaEventDestroy(e);
+    if (h_flags) cudaFreeHost(h_flags);
+    if (ev_poll) cudaEventDestroy(ev_poll);
+    if (st) cudaStreamDestroy(st);
+}
+
+marsit_status Watchdog::watch(cudaStream_t s, uint64_t epoch) {
+    cudaEvent_t ev = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!free_events.empty()) {
+            ev = free_events.back();
+            free_events.pop_back();
+        }
+    }
+    if (!ev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ev, s));
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        pending.push_back({ev, std::chrono::steady_clock::now(), epoch});
+    }
+    cv.notify_all();
+    return MARSIT_OK;
+}
+
+// Mark the context failed and unblock everything it enqueued: P2P stream
+// waits are released (kFlagAbort in the local flags) and the peers are told
+// (kFlagAbort in this rank's slots of their flags); NCCL is aborted.
+void Watchdog::give_up(marsit_status status, const std::string& msg) {
+    ctx_set_failed(ctx, status, msg);
+    if (ctx->p2p) {
+        const size_t n = 2 * size_t(ctx->G);
+        cudaMemsetAsync(ctx->flags, 0xFF, n * sizeof(uint64_t), st);
+        for (uint32_t q = 0; q < ctx->G && q < ctx->peer_flags.size(); ++q) {
+            if (q == ctx->rank || !ctx->peer_flags[q]) continue;
+            for (int which = 0; which < 2; ++which)
+                cudaMemsetAsync(const_cast<uint64_t*>(ctx->peer_flags[q]) + size_t(which) * ctx->G + ctx->rank,
+                                0xFF, sizeof(uint64_t), st);
+        }
+        poll_stream(st, ev_poll);
+    }
+    if (ctx->comm && ctx->owns_comm) {
+        // frees the communicator and unblocks its kernels; the context only
+        // returns the latched failure from now on
+        ncclCommAbort(ctx->comm);
+        ctx->owns_comm = false;
+    }
+    cudaGetLastError();
+}
+
+void Watchdog::loop() {
+    cudaSetDevice(ctx->device);
+    std::unique_lock<std::mutex> lock(mu);
+    while (!stop) {
+        if (pending.empty()) {
+            cv.wait(lock, [this] { return stop || !pending.empty(); });
+            continue;
+        }
+        Item it = pending.front();
+        lock.unlock();
+        const cudaError_t q = cudaEventQuery(it.ev);
+        bool done = q == cudaSuccess;
+        if (q != cudaSuccess && q != cudaErrorNotReady) {
+            ctx_set_failed(ctx, MARSIT_ECUDA, std::string("round failed: ") + cudaGetErrorString(q));
+            done = true;
+        }
+        if (!done && !ctx->fail_status.load()) {
+            std::string why;
+            marsit_status status = MARSIT_EPROTOCOL;
+            if (ctx->comm) {
+                ncclResult_t ar = ncclSuccess;
+                if (ncclCommGetAsyncError(ctx->comm, &ar) == ncclSuccess && ar != ncclSuccess &&
+                    ar != ncclInProgress) {
+                    status = MARSIT_ENCCL;
+                    why = std::string("NCCL asynchronous error: ") + ncclGetErrorString(ar);
+                }
+            }
+            const auto waited = std::chrono::duration_cast<std::chrono::milliseconds>(
+                                    std::chrono::steady_clock::now() - it.t0).count();
+            if (why.empty() && ctx->p2p) {
+                // which peers are missing (or announced an abort)
+                const size_t n = 2 * size_t(ctx->G);
+                if (cudaMemcpyAsync(h_flags, ctx->flags, n * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                    st) == cudaSuccess &&
+                    poll_stream(st, ev_poll) == cudaSuccess) {
+                    std::string missing;
+                    for (uint32_t r = 0; r < ctx->G; ++r) {
+                        if (r == ctx->rank) continue;
+                        for (int which = 0; which < 2; ++which) {
+                            const uint64_t v = h_flags[size_t(which) * ctx->G + r];
+                            if (v == kFlagAbort)
+                                why = "P2P: peer rank " + std::to_string(r) + " aborted";
+                            else if (v < it.epoch && missing.empty())
+                                missing = "peer rank " + std::to_string(r) + " has not reported " +
+                                          (which ? "its owned aggregates" : "its packed signs") +
+                                          " for epoch " + std::to_string(it.epoch) + " (last " +
+                                          std::to_string(v) + ")";
+                        }
+                    }
+                    if (why.empty() && ctx->wait_timeout_ms && uint64_t(waited) > ctx->wait_timeout_ms)
+                        why = "P2P: round did not complete within " +
+                              std::to_string(ctx->wait_timeout_ms) + " ms" +
+                              (missing.empty() ? std::string() : ": " + missing);
+                }
+                cudaGetLastError();
+            } else if (why.empty() && ctx->wait_timeout_ms && uint64_t(waited) > ctx->wait_timeout_ms) {
+                status = ctx->comm ? MARSIT_ENCCL : MARSIT_EPROTOCOL;
+                why = "round did not complete within " + std::to_string(ctx->wait_timeout_ms) + " ms";
+            }
+            if (!why.empty()) give_up(status, why);
+        }
+        lock.lock();
+        if (done) {
+            pending.pop_front();
+            free_events.push_back(it.ev);
+            continue;
+        }
+        if (ctx->fail_status.load()) {
+            // released: the stream drains; keep the events until they complete
+            cv.wait_for(lock, std::chrono::milliseconds(5));
+            continue;
+        }
+        cv.wait_for(lock, std::chrono::milliseconds(20));
+    }
+}
+
+marsit_status watch_round(marsit_ctx* ctx, cudaStream_t st) {
+    if (!ctx->watchdog) return MARSIT_OK;
+    return ctx->watchdog->watch(st, ctx->epoch);
+}
+
 // Lower the owned segments' merge DAGs: execution order = (stage, schedule
 // order); outputs consumed by a later merge of the same stage get a
 // shared-memory slot (liveness-based reuse, read-before-write within a
@@ -170,12 +347,123 @@ marsit_status lower_plan(const Plan& plan, uint32_t s_first, uint32_t n_seg, Dev
     return MARSIT_OK;
 }
 
+// Cluster plans: one cluster runs a segment's whole DAG, so there are no
+// stages.  Merges are grouped into levels (ASAP over their operands and the
+// stream they continue, at most kMaxLevelMerges per level: a torus's row
+// chains advance side by side); every merge output except the final node
+// lives in a shared-memory slot, reused in place when its only reader is the
+// merge that overwrites it (the ring's running aggregate) or freed after the
+// level of its last reader.
+marsit_status lower_cluster_plan(const Plan& plan, uint32_t s_first, uint32_t n_seg, DevicePlan& dp) {
+    const uint32_t W = plan.workers;
+    dp = DevicePlan{};
+    dp.n_stages = 1;
+    dp.seg_begin.assign(size_t(n_seg) + 1, 0);
+    dp.lvl_start.assign(size_t(n_seg) + 1, 0);
+    for (uint32_t sl = 0; sl < n_seg; ++sl) {
+        const SegmentPlan& sp = plan.seg[s_first + sl];
+        const size_t n = sp.merges.size();
+        if (sp.final_node < W) return fail(MARSIT_EUNSUPPORTED, "schedule performs no reduction");
+        if (n > size_t(kMaxSegMerges))
+            return fail(MARSIT_EUNSUPPORTED, "merge plan too large (more than 64 merges per segment)");
+        std::vector<int> lvl(n, 0);
+        std::vector<uint32_t> width;
+        for (size_t k = 0; k < n; ++k) {  // schedule order is topological
+            const MergeNode& m = sp.merges[k];
+            int L = 0;
+            for (uint32_t in : {m.recv_node, m.local_node})
+                if (in >= W) L = std::max(L, lvl[in - W] + 1);
+            if (m.offset_src >= 0) L = std::max(L, lvl[m.offset_src] + 1);
+            while (size_t(L) < width.size() && width[L] >= uint32_t(kMaxLevelMerges)) ++L;
+            if (size_t(L) >= width.size()) width.resize(L + 1, 0);
+            ++width[L];
+            lvl[k] = L;
+        }
+        std::vector<uint32_t> order(n);
+        for (size_t k = 0; k < n; ++k) order[k] = uint32_t(k);
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return lvl[a] < lvl[b]; });
+        std::vector<uint32_t> pos(n);
+        for (size_t e = 0; e < n; ++e) pos[order[e]] = uint32_t(e);
+        // readers of every merge output: last level, count per level
+        std::vector<int> last(n, -1);
+        for (size_t k = 0; k < n; ++k)
+            for (uint32_t in : {sp.merges[k].recv_node, sp.merges[k].local_node})
+                if (in >= W) last[in - W] = std::max(last[in - W], lvl[k]);
+        auto readers_at = [&](uint32_t node, int level) {
+            int c = 0;
+            for (size_t k = 0; k < n; ++k)
+                if (lvl[k] == level)
+                    for (uint32_t in : {sp.merges[k].recv_node, sp.merges[k].local_node})
+                        c += in == W + node;
+            return c;
+        };
+        std::vector<uint16_t> slot_of(n, kNone);
+        std::vector<int> owner;  // slot -> node holding it (-1 free)
+        dp.seg_begin[sl] = uint32_t(dp.merges.size());
+        dp.lvl_start[sl] = uint32_t(dp.lvl_begin.size());
+        size_t e = 0;
+        for (int v = 0; v < int(width.size()); ++v) {
+            dp.lvl_begin.push_back(uint32_t(e));
+            dp.level_width = std::max(dp.level_width, width[v]);
+            for (; e < n && lvl[order[e]] == v; ++e) {
+                const uint32_t k = order[e];
+                const MergeNode& m = sp.merges[k];
+                DevMerge d{};
+                d.thresh11 = coin_threshold(m.c_recv, m.c_local) << 11;
+                d.receiver = m.receiver;
+                d.segment = s_first + sl;
+                d.key_mode = 0;
+                d.offset_src = m.offset_src < 0 ? int16_t(-1) : int16_t(pos[m.offset_src]);
+                auto encode = [&](uint32_t node) -> uint16_t {
+                    if (node < W) return uint16_t(kSrcLeaf | node);
+                    return uint16_t(kSrcSlot | slot_of[node - W]);
+                };
+                d.recv_src = encode(m.recv_node);
+                d.local_src = encode(m.local_node);
+                d.out_slot = kNone;
+                d.out_global = kNone;
+                if (W + k == sp.final_node) {
+                    d.out_global = kFinal;
+                } else {
+                    uint16_t sl_out = kNone;
+                    for (uint32_t in : {m.recv_node, m.local_node})  // in place
+                        if (sl_out == kNone && in >= W && slot_of[in - W] != kNone &&
+                            last[in - W] == v && readers_at(in - W, v) == 1)
+                            sl_out = slot_of[in - W];
+                    if (sl_out == kNone) {
+                        size_t f = 0;
+                        while (f < owner.size() && owner[f] >= 0) ++f;
+                        if (f == owner.size()) owner.push_back(-1);
+                        sl_out = uint16_t(f);
+                    }
+                    owner[sl_out] = int(k);
+                    slot_of[k] = sl_out;
+                    d.out_slot = sl_out;
+                    dp.max_slots = std::max<uint32_t>(dp.max_slots, uint32_t(owner.size()));
+                }
+                dp.merges.push_back(d);
+            }
+            // slots whose node was last read at this level are free again
+            for (size_t f = 0; f < owner.size(); ++f)
+                if (owner[f] >= 0 && last[owner[f]] <= v) owner[f] = -1;
+        }
+        dp.lvl_begin.push_back(uint32_t(n));
+        if (owner.size() > 0x3FFF) return fail(MARSIT_EUNSUPPORTED, "merge plan too large");
+    }
+    dp.seg_begin[n_seg] = uint32_t(dp.merges.size());
+    dp.lvl_start[n_seg] = uint32_t(dp.lvl_begin.size());
+    dp.n_merges = uint32_t(dp.merges.size());
+    return MARSIT_OK;
+}
+
 }  // namespace marsit_b200
 
 marsit_ctx::~marsit_ctx() {
     if (device >= 0) cudaSetDevice(device);
+    watchdog.reset();  // joins the thread before any buffer it reads goes away
     for (void* p : {(void*)bits, (void*)recv, (void*)agg, (void*)err, dense_send, dense_recv,
                     dense_mean, (void*)d_dense_ops, (void*)d_dense_final, (void*)d_metrics,
+                    (void*)d_verify,
                     (void*)d_dense_chain, (void*)d_dense_groups,
                     (void*)flags, (void*)d_peer_tables})
         if (p) cudaFree(p);
@@ -185,6 +473,8 @@ marsit_ctx::~marsit_ctx() {
     }
     for (auto e : event_pool) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_check) cudaEventDestroy(ev_check);
+    if (h_check) cudaFreeHost(h_check);
     if (ev_extract) cudaEventDestroy(ev_extract);
     for (auto e : ev_merge) cudaEventDestroy(e);
     for (int b = 0; b < 2; ++b) {
@@ -251,6 +541,7 @@ StreamParams<T> stream_params(marsit_ctx* ctx, const void* const* g, const void*
     p.wst = ctx->wst;
     p.bits = ctx->bits;
     p.agg = ctx->agg;
+    p.wsa = ctx->wsa;
     p.update = static_cast<T*>(update);
     p.eta = T(eta);
     p.err = ctx->err;
@@ -448,7 +739,7 @@ marsit_status run_allgather(marsit_ctx* ctx, cudaStream_t st) {
     cudaEvent_t ev;
     marsit_status s = ctx->begin_phase(st, &ev);
     if (s) return s;
-    const size_t block = size_t(ctx->s_own) * ctx->wst;
+    const size_t block = size_t(ctx->s_own) * ctx->wsa;  // rows incl. the consensus hash slots
     NCCL_TRY(ncclAllGather(ctx->agg + ctx->rank * block, ctx->agg, block, ncclUint32, ctx->comm, st));
     return ctx->end_phase(kPhAllgather, st, ev, 0);
 }
@@ -499,7 +790,7 @@ marsit_status run_export(marsit_ctx* ctx, uint64_t* out, cudaStream_t st) {
     cudaEvent_t ev;
     marsit_status s = ctx->begin_phase(st, &ev);
     if (s) return s;
-    CUDA_TRY(launch_export_bits(ctx->agg, ctx->wst, ctx->D, ctx->L,
+    CUDA_TRY(launch_export_bits(ctx->agg, ctx->wsa, ctx->D, ctx->L,
                                 reinterpret_cast<uint32_t*>(out), st, p2p_table(ctx, 1), ctx->s_own));
     return ctx->end_phase(kPhExport, st, ev, 1);
 }
@@ -543,7 +834,6 @@ marsit_status dense_phase(marsit_ctx* ctx, int phase, const void* const* g, cons
     p.inv_m = 1.0 / double(ctx->M);
     p.err = ctx->err;
     uint64_t launches = 0;
-    if (phase == 0 && ctx->p2p) ++ctx->epoch;
     if (phase == 1 && (s = p2p_wait(ctx, 0, st))) return s;
     if (phase == 2 && (s = p2p_wait(ctx, 1, st))) return s;
     if (phase == 0 && ctx->G > 1) {
@@ -602,7 +892,10 @@ marsit_status dense_phase(marsit_ctx* ctx, int phase, const void* const* g, cons
         }
     }
     if ((s = ctx->end_phase(kPhDense, st, ev, launches))) return s;
-    if (phase == 0) return p2p_signal(ctx, 0, st);  // my u blocks are ready
+    if (phase == 0) {
+        if (ctx->p2p) ++ctx->epoch;  // after this rank's phase-0 launches
+        return p2p_signal(ctx, 0, st);  // my u blocks are ready
+    }
     if (phase == 1) return p2p_signal(ctx, 1, st);  // my owned mean block is ready
     return MARSIT_OK;
 }
@@ -753,6 +1046,31 @@ void assign_coin_budget(DevicePlan& dp, uint32_t n_seg, uint64_t L, double frac,
 
 namespace marsit_b200 {
 
+// Opt-in consensus, owner side (after the merge, before the aggregates are
+// published): the hash of every owned segment into its row's hash slot.
+marsit_status consensus_own(marsit_ctx* ctx, cudaStream_t st) {
+    if (!ctx->consensus) return MARSIT_OK;
+    CUDA_TRY(cudaMemset2DAsync(ctx->agg + size_t(ctx->s_first) * ctx->wsa + ctx->wst,
+                               size_t(ctx->wsa) * 4, 0, sizeof(uint64_t), ctx->s_own, st));
+    CUDA_TRY(launch_seg_hash(ctx->agg, nullptr, 1, ctx->wsa, ctx->wst, ctx->words_proc,
+                             ctx->s_first, ctx->s_own, nullptr, st));
+    return MARSIT_OK;
+}
+
+// Reader side (after the decode): every segment re-hashed as this rank reads
+// it and compared with its owner's hash (consensus, allreduce.hpp:32-43).
+marsit_status consensus_verify(marsit_ctx* ctx, cudaStream_t st) {
+    if (!ctx->consensus) return MARSIT_OK;
+    if (!ctx->d_verify) CUDA_TRY(cudaMalloc(&ctx->d_verify, sizeof(unsigned long long) * ctx->S));
+    CUDA_TRY(cudaMemsetAsync(ctx->d_verify, 0, sizeof(unsigned long long) * ctx->S, st));
+    const uint32_t* const* peers = p2p_table(ctx, 1);
+    CUDA_TRY(launch_seg_hash(ctx->agg, peers, ctx->s_own, ctx->wsa, ctx->wst, ctx->words_proc, 0,
+                             ctx->S, ctx->d_verify, st));
+    CUDA_TRY(launch_hash_compare(ctx->agg, peers, ctx->s_own, ctx->wsa, ctx->wst, ctx->S,
+                                 ctx->d_verify, ctx->err, st));
+    return MARSIT_OK;
+}
+
 // Sign round phases around the two exchange points:
 //   0: coins (aux) + extract  ->  [exchange of packed segments]
 //   1: merge of the owned segments (+ next round's coin prefetch)
@@ -764,23 +1082,27 @@ marsit_status sign_phase(marsit_ctx* ctx, int phase, uint64_t t, double eta_s, u
                          void* d_update, cudaStream_t st) {
     marsit_status s = MARSIT_OK;
     if (phase == 0) {
-        if (ctx->p2p) ++ctx->epoch;
         ctx->task_dir = ctx->l2_reuse ? uint32_t(t & 1) : 0;
         if ((s = run_coins(ctx, seed, t, st))) return s;
         // MARSIT_COIN_PREFETCH_AT=1: the next round's coins run underneath
         // this extract instead of this round's decode
         if (ctx->coin_prefetch_at_extract && (s = prefetch_coins(ctx, seed, t, st))) return s;
         if ((s = run_extract(ctx, d_grads, d_comp, st))) return s;
+        // the epoch advances only once this rank's phase-0 work is enqueued:
+        // a failed launch above leaves the peers' view consistent
+        if (ctx->p2p) ++ctx->epoch;
         return p2p_signal(ctx, 0, st);  // my packed signs are ready
     }
     if (phase == 1) {
         if ((s = p2p_wait(ctx, 0, st))) return s;  // every rank's packed signs
         if ((s = run_merge(ctx, seed, t, st))) return s;
+        if ((s = consensus_own(ctx, st))) return s;
         if (!ctx->coin_prefetch_at_extract && (s = prefetch_coins(ctx, seed, t, st))) return s;
         return p2p_signal(ctx, 1, st);  // my owned aggregates are ready
     }
     if ((s = p2p_wait(ctx, 1, st))) return s;  // every owner's aggregates
     if ((s = run_decode(ctx, d_grads, d_comp, d_comp_out, params, d_update, eta_s, st))) return s;
+    if ((s = consensus_verify(ctx, st))) return s;
     return run_export(ctx, d_agg_bits, st);
 }
 
@@ -795,8 +1117,9 @@ marsit_status check_round_args(marsit_ctx* ctx, double eta_s, const void* const*
                                const void* const* d_comp, void* const* d_comp_out,
                                void* const* params, bool sign) {
     if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
-    if (sign && !(eta_s > 0.0)) return fail(MARSIT_EPARAM, "SyncConfig: eta_s must be > 0");
     marsit_status s;
+    if ((s = ctx_failed(ctx))) return s;
+    if (sign && !(eta_s > 0.0)) return fail(MARSIT_EPARAM, "SyncConfig: eta_s must be > 0");
     if ((s = check_ptrs(ctx, d_grads, "grads")) || (s = check_ptrs(ctx, d_comp, "comp")) ||
         (s = check_ptrs(ctx, (const void* const*)d_comp_out, "comp_out")) ||
         (params && (s = check_ptrs(ctx, (const void* const*)params, "params"))))
@@ -861,8 +1184,10 @@ marsit_status sign_round_impl(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_
                         d_update, st)))
         return s;
     if ((s = run_allgather(ctx, st))) return s;
-    return sign_phase(ctx, 2, t, eta_s, seed, d_grads, d_comp, d_comp_out, params, d_agg_bits,
-                      d_update, st);
+    if ((s = sign_phase(ctx, 2, t, eta_s, seed, d_grads, d_comp, d_comp_out, params, d_agg_bits,
+                        d_update, st)))
+        return s;
+    return watch_round(ctx, st);
 }
 
 marsit_status dense_round_any(marsit_ctx* ctx, uint64_t t, const void* const* d_grads,
@@ -879,7 +1204,8 @@ marsit_status dense_round_any(marsit_ctx* ctx, uint64_t t, const void* const* d_
     if ((s = dense_exchange(ctx, st))) return s;
     if ((s = dense_phase_any(ctx, 1, d_grads, d_comp, d_comp_out, params, d_mean, st))) return s;
     if ((s = dense_allgather(ctx, st))) return s;
-    return dense_phase_any(ctx, 2, d_grads, d_comp, d_comp_out, params, d_mean, st);
+    if ((s = dense_phase_any(ctx, 2, d_grads, d_comp, d_comp_out, params, d_mean, st))) return s;
+    return watch_round(ctx, st);
 }
 
 uint64_t round_bits_total(const marsit_ctx* ctx, bool dense) {
@@ -1014,6 +1340,8 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     if (desc->rank >= G) return fail(MARSIT_EPARAM, "rank out of range");
     if (hs.workers / G > kMaxLocalWorkers)
         return fail(MARSIT_EUNSUPPORTED, "too many workers per rank (max 64)");
+    if (G > kMaxLocalWorkers)  // P2P flag writes address G - 1 peers (FlagSlots)
+        return fail(MARSIT_EUNSUPPORTED, "too many ranks (max 64)");
     const bool external = desc->transport == MARSIT_TRANSPORT_EXTERNAL;
     const bool p2p = G > 1 && desc->transport == MARSIT_TRANSPORT_P2P;
     if (desc->transport != MARSIT_TRANSPORT_NCCL && desc->transport != MARSIT_TRANSPORT_EXTERNAL &&
@@ -1046,13 +1374,15 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     ctx->words64 = uint32_t(ceil_div(ctx->L, 64));
     ctx->words_proc = uint32_t(round_up(2ull * ctx->words64, 4));
     ctx->wst = uint32_t(round_up(ctx->words_proc, 32));
+    ctx->wsa = ctx->wst + 4;  // + the segment's u64 consensus hash, rows 16 B aligned
     // vector kernels: every segment's quads 16 B-aligned (L % 4 == 0); other
     // lengths take the coalesced scalar kernels (all loads issued first)
     ctx->vec_ok = (ctx->L % 4) == 0;
 
     // merge plan, coin budget, tiling
     MergeRunner& mr = ctx->merge;
-    marsit_status st = lower_plan(ctx->plan, ctx->s_first, ctx->s_own, mr.dp);
+    marsit_status st = mr.cluster ? lower_cluster_plan(ctx->plan, ctx->s_first, ctx->s_own, mr.dp)
+                                  : lower_plan(ctx->plan, ctx->s_first, ctx->s_own, mr.dp);
     if (st) return st;
     mr.n_seg = ctx->s_own;
     mr.s_first = ctx->s_first;
@@ -1060,6 +1390,7 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     mr.wst = ctx->wst;
     mr.ml = ctx->ml;
     mr.L = ctx->L;
+    mr.agg_stride = ctx->wsa;
     double frac = 0.53;
     if (const char* e = std::getenv("MARSIT_COIN_FRAC")) frac = std::atof(e);
     uint64_t max_words = 0;
@@ -1067,7 +1398,7 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     // single GPU with several segments: per-segment merge launches sized to
     // co-reside with the decode (MARSIT_PIPELINE=0 disables)
     ctx->pipeline = G == 1 && ctx->S >= 2 && env_int("MARSIT_PIPELINE", 0) != 0 &&
-                    desc->transport == MARSIT_TRANSPORT_NCCL;
+                    desc->transport != MARSIT_TRANSPORT_EXTERNAL;
     if (ctx->pipeline) {
         if ((st = mr.configure(ctx->sm_count, 1, env_int("MARSIT_PIPE_MERGE_CTAS", 1)))) return st;
     } else {
@@ -1078,8 +1409,8 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     const size_t wst = ctx->wst;
     CUDA_TRY(cudaMalloc(&ctx->bits, sizeof(uint32_t) * ctx->S * ctx->ml * wst));
     CUDA_TRY(cudaMemset(ctx->bits, 0, sizeof(uint32_t) * ctx->S * ctx->ml * wst));
-    CUDA_TRY(cudaMalloc(&ctx->agg, sizeof(uint32_t) * ctx->S * wst));
-    CUDA_TRY(cudaMemset(ctx->agg, 0, sizeof(uint32_t) * ctx->S * wst));
+    CUDA_TRY(cudaMalloc(&ctx->agg, sizeof(uint32_t) * ctx->S * ctx->wsa));
+    CUDA_TRY(cudaMemset(ctx->agg, 0, sizeof(uint32_t) * ctx->S * ctx->wsa));
     if (G > 1 && !p2p) {
         CUDA_TRY(cudaMalloc(&ctx->recv, sizeof(uint32_t) * ctx->S * ctx->ml * wst));
         CUDA_TRY(cudaMemset(ctx->recv, 0, sizeof(uint32_t) * ctx->S * ctx->ml * wst));
@@ -1094,6 +1425,11 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     }
     CUDA_TRY(cudaMalloc(&ctx->err, sizeof(int)));
     CUDA_TRY(cudaMemset(ctx->err, 0, sizeof(int)));
+    // marsit_ctx_check's pinned read-back (allocated here: cudaHostAlloc may
+    // synchronise the device, which a blocked P2P stream would never allow)
+    CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_check, cudaEventDisableTiming));
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_check),
+                           sizeof(uint64_t) * (1 + 2 * size_t(G)), cudaHostAllocDefault));
 
     // coin buffers, aux stream
     CUDA_TRY(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
@@ -1213,6 +1549,7 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
             std::memcpy(&id, desc->nccl_id, sizeof(id));
             NCCL_TRY(ncclCommInitRank(&ctx->comm, int(G), id, int(desc->rank)));
         }
+        if (ctx->comm) ctx->watchdog = std::make_unique<Watchdog>(ctx.get());
     }
     *out = ctx.release();
     return MARSIT_OK;
@@ -1277,7 +1614,7 @@ marsit_status marsit_ctx_exchange_layout(const marsit_ctx* ctx, int dense,
         out->recv = ctx->G > 1 ? ctx->recv : ctx->bits;
         out->block_bytes = uint64_t(ctx->s_own) * ctx->ml * ctx->wst * 4;
         out->gather = ctx->agg;
-        out->gather_block_bytes = uint64_t(ctx->s_own) * ctx->wst * 4;
+        out->gather_block_bytes = uint64_t(ctx->s_own) * ctx->wsa * 4;  // rows incl. hash slots
     }
     return MARSIT_OK;
 }
@@ -1298,10 +1635,13 @@ marsit_status marsit_round_phase(marsit_ctx* ctx, int phase, uint64_t t, uint64_
     if (phase == 0) note_round(ctx, t, dense);
     if (dense) {
         if (!d_update) return fail(MARSIT_EPARAM, "dense round needs d_update for the mean");
-        return dense_phase_any(ctx, phase, d_grads, d_comp, d_comp_out, nullptr, d_update, st);
+        s = dense_phase_any(ctx, phase, d_grads, d_comp, d_comp_out, nullptr, d_update, st);
+    } else {
+        s = sign_phase(ctx, phase, t, eta_s, seed, d_grads, d_comp, d_comp_out, nullptr,
+                       d_agg_bits, d_update, st);
     }
-    return sign_phase(ctx, phase, t, eta_s, seed, d_grads, d_comp, d_comp_out, nullptr,
-                      d_agg_bits, d_update, st);
+    if (s || phase != 2) return s;
+    return watch_round(ctx, st);
 }
 
 marsit_status marsit_sign_extract(marsit_ctx* ctx, const void* const* d_grads,
@@ -1325,7 +1665,20 @@ marsit_status marsit_allreduce_sign(marsit_ctx* ctx, uint64_t round, uint64_t se
                                     void* stream) {
     if (!ctx || !d_signs || !d_out) return fail(MARSIT_EPARAM, "null argument");
     marsit_status s;
-    if ((s = check_consensus(ctx, false))) return s;
+    if ((s = ctx_failed(ctx))) return s;
+    // every worker's result is the consensus aggregate only for schedules
+    // that end in consensus (ring, torus); the reference returns each
+    // worker's own final state otherwise, which this entry point does not
+    // materialise
+    for (uint32_t sg = 0; sg < ctx->S; ++sg)
+        if (!ctx->plan.seg[sg].consensus)
+            return fail(MARSIT_EUNSUPPORTED,
+                        "allreduce_sign: schedules whose workers do not end in consensus are not "
+                        "supported (use ring / torus or a consensus-reaching table)");
+    if (ctx->G > 1 && !ctx->comm)
+        return fail(MARSIT_EUNSUPPORTED,
+                    "allreduce_sign on a multi-rank context needs the NCCL transport "
+                    "(P2P / external contexts: marsit_round_phase)");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     CUDA_TRY(cudaSetDevice(ctx->device));
     const size_t row = size_t(ctx->words64) * 8;
@@ -1337,7 +1690,7 @@ marsit_status marsit_allreduce_sign(marsit_ctx* ctx, uint64_t round, uint64_t se
     if ((s = run_exchange(ctx, st))) return s;
     if ((s = run_merge(ctx, seed, round, st))) return s;
     if ((s = run_allgather(ctx, st))) return s;
-    CUDA_TRY(cudaMemcpy2DAsync(d_out, row, ctx->agg, size_t(ctx->wst) * 4, row, ctx->S,
+    CUDA_TRY(cudaMemcpy2DAsync(d_out, row, ctx->agg, size_t(ctx->wsa) * 4, row, ctx->S,
                                cudaMemcpyDeviceToDevice, st));
     if (counts)
         for (uint32_t sg = 0; sg < ctx->S; ++sg) counts[sg] = ctx->plan.seg[sg].final_count;
@@ -1383,10 +1736,18 @@ marsit_status marsit_merge_signs(const uint64_t* d_recv, uint32_t c_recv, const 
     m.offset_src = -1;
     m.coin_words = 0;  // inline draws
     mr.dp.merges = {m};
-    mr.dp.seg_begin = {0};
-    mr.dp.stage_begin = {0, 1};
-    mr.dp.n_stages = 1;
-    mr.dp.single_lanes();
+    if (mr.cluster) {
+        mr.dp.seg_begin = {0, 1};
+        mr.dp.lvl_start = {0, 2};
+        mr.dp.lvl_begin = {0, 1};
+        mr.dp.level_width = 1;
+        mr.dp.max_slots = 0;
+    } else {
+        mr.dp.seg_begin = {0};
+        mr.dp.stage_begin = {0, 1};
+        mr.dp.n_stages = 1;
+        mr.dp.single_lanes();
+    }
     mr.dp.n_merges = 1;
     marsit_status s;
     if ((s = mr.configure(sm)) || (s = mr.upload())) return s;
@@ -1438,14 +1799,34 @@ marsit_status marsit_ctx_check(marsit_ctx* ctx, void* stream) {
     if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
     CUDA_TRY(cudaSetDevice(ctx->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    int flag = 0;
-    CUDA_TRY(cudaMemcpyAsync(&flag, ctx->err, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
+    // a stuck peer wait is released by the watchdog (bounded), so this returns
+    // stream-ordered reads into pinned memory, completion by polling (no
+    // legacy-stream or pageable copy that could wait on other streams)
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_check, ctx->err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    const bool read_flags = ctx->p2p && ctx->peers_set;
+    if (read_flags)
+        CUDA_TRY(cudaMemcpyAsync(ctx->h_check + 1, ctx->flags, 2 * sizeof(uint64_t) * ctx->G,
+                                 cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(poll_stream(st, ctx->ev_check));
+    const int flag = *reinterpret_cast<const int*>(ctx->h_check);
     CUDA_TRY(cudaGetLastError());
+    marsit_status s;
+    if (read_flags && !ctx->fail_status.load()) {
+        // a peer whose watchdog gave up released our waits with the abort
+        // value: this rank's round read incomplete data
+        const uint64_t* fl = ctx->h_check + 1;
+        for (uint32_t q = 0; q < ctx->G; ++q)
+            if (q != ctx->rank && (fl[q] == kFlagAbort || fl[ctx->G + q] == kFlagAbort)) {
+                ctx_set_failed(ctx, MARSIT_EPROTOCOL, "P2P: peer rank " + std::to_string(q) + " aborted");
+                break;
+            }
+    }
+    if ((s = ctx_failed(ctx))) return s;
     if (flag) {
         CUDA_TRY(cudaMemsetAsync(ctx->err, 0, sizeof(int), st));
-        CUDA_TRY(cudaStreamSynchronize(st));
-        return fail(MARSIT_ENONFINITE, "DenseVector: non-finite entry");
+        CUDA_TRY(poll_stream(st, ctx->ev_check));
+        if (flag & kErrNonFinite) return fail(MARSIT_ENONFINITE, "DenseVector: non-finite entry");
+        return fail(MARSIT_EPROTOCOL, "consensus: an aggregate segment differs from its owner's");
     }
     return MARSIT_OK;
 }
@@ -1484,6 +1865,7 @@ marsit_status marsit_ctx_set_peers(marsit_ctx* ctx, const marsit_p2p_buffers* pe
                         cudaMemcpyHostToDevice));
     ctx->merge.peer_bits = reinterpret_cast<const uint32_t* const*>(ctx->d_peer_tables);
     ctx->peers_set = true;
+    if (!ctx->watchdog) ctx->watchdog = std::make_unique<Watchdog>(ctx);
     return MARSIT_OK;
 }
 
@@ -1565,6 +1947,23 @@ marsit_status marsit_ctx_metrics(marsit_ctx* ctx, marsit_round_metrics* out, voi
     out->disagreement_rate =
         out->compared_bits ? double(out->disagreements) / double(out->compared_bits) : 0.0;
     return MARSIT_OK;
+}
+
+marsit_status marsit_ctx_set_wait_timeout(marsit_ctx* ctx, uint64_t timeout_ms) {
+    if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
+    ctx->wait_timeout_ms = timeout_ms;
+    return MARSIT_OK;
+}
+
+marsit_status marsit_ctx_set_consensus(marsit_ctx* ctx, int enable) {
+    if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
+    ctx->consensus = enable != 0;
+    return MARSIT_OK;
+}
+
+marsit_status marsit_ctx_status(const marsit_ctx* ctx) {
+    if (!ctx) return fail(MARSIT_EPARAM, "ctx is null");
+    return ctx_failed(ctx);
 }
 
 marsit_status marsit_ctx_set_timing(marsit_ctx* ctx, int enable) {

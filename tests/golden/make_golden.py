@@ -238,6 +238,28 @@ def ssdm_cases():
     return dict(compress=comp, allreduce=allr)
 
 
+def metrics_cases():
+    """The trainer's matching figure (analysis.hpp:244-253 on trainer.hpp:241-251's
+    fp64 mean of add(g, c)) from the REAL reference, on fp32-valued inputs with
+    cancellation coordinates (O.gen_metrics_inputs): one sign round each."""
+    out = []
+    for topo, a, b, D, seed in [("ring", 4, 0, 4_099, 11), ("torus", 2, 4, 60_211, 12),
+                                ("ring", 8, 0, 100_003, 13)]:
+        T = O.schedule(topo, a, b)
+        g, c = O.gen_metrics_inputs(seed, T.workers, D)
+        r = O.marsit_round(T, 1, None, ETA, g, c, 2026, use_ref=True)
+        assert r.status == 0
+        rate, matches = O.ref_matching(r.agg_bits, g, c)
+        # what a mean of fp32-rounded u would give (the pre-fix device figure)
+        u32 = (g.astype(np.float32) + c.astype(np.float32)).astype(np.float64)
+        m32 = O.matching_count(r.agg_bits, u32, np.zeros_like(u32))
+        out.append({"topology": topo, "a": a, "b": b, "dim": D, "seed": seed, "round": 1,
+                    "global_seed": 2026, "inputs_sha256": sha(np.concatenate([g, c])),
+                    "agg_words": wx(r.agg_bits), "matches": int(matches), "rate": float(rate).hex(),
+                    "matches_fp32_mean": int(m32)})
+    return out
+
+
 def schedules():
     out = []
     for topo, a, b in [("ring", 2, 0), ("ring", 3, 0), ("ring", 8, 0), ("torus", 2, 2),
@@ -253,9 +275,10 @@ def main():
     if not O.ref_available():
         O.build()
     assert O.ref_available(), "oracle/_ref/libmarsit_ref.so not built (needs /root/reference)"
-    blobs = dict(anchors=anchors(), streams=streams(), merges=merges(),
-                 allreduce=allreduces(), schedules=schedules(), rounds=round_cases(),
-                 ssdm=ssdm_cases())
+    makers = dict(anchors=anchors, streams=streams, merges=merges, allreduce=allreduces,
+                  schedules=schedules, rounds=round_cases, ssdm=ssdm_cases, metrics=metrics_cases)
+    names = sys.argv[1:] or list(makers)  # e.g. `make_golden.py metrics`
+    blobs = {n: makers[n]() for n in names}
     for name, obj in blobs.items():
         with open(os.path.join(HERE, name + ".json"), "w") as f:
             json.dump(obj, f, separators=(",", ":"))

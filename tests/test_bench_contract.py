@@ -38,3 +38,11 @@ def test_reference_arm_nonzero_rank_is_silent():
                   env={"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert r.returncode == 0, r.stderr
     assert r.stdout.strip() == ""
+
+
+def test_gpus_must_match_world_size():
+    """--gpus N under a launcher with another WORLD_SIZE fails loudly (it used to
+    be silently rewritten)."""
+    r = run_bench("--gpus", "2", env={"WORLD_SIZE": "3", "RANK": "0", "LOCAL_RANK": "0"})
+    assert r.returncode == 2
+    assert "does not match WORLD_SIZE" in r.stderr

@@ -179,3 +179,29 @@ def test_c3_matching_count_full_size(pipeline, monkeypatch):
     # disagreement rate is well below the independent-sign 50 %
     assert m.matching_rate > 0.6 and 0.0 < m.disagreement_rate < 0.5
     assert m.merges == W * (W - 1) and m.compared_bits == m.merges * (D // W)
+
+
+@pytest.mark.parametrize("case", range(3))
+def test_matching_pinned_to_reference_golden(golden, case):
+    """The fused matching count against the REAL reference's figure
+    (analysis.hpp:244-253 on trainer.hpp:241-251's fp64 mean of add(g, c),
+    tests/golden/metrics.json): fp32 Gaussian inputs plus coordinates where
+    the fp32-rounded u = g + c flips the sign of the mean — the device forms
+    the mean from the fp64 sum of the two fp32 values, like the trainer."""
+    c = golden("metrics")[case]
+    sched = (mb.build_ring_schedule(c["a"]) if c["topology"] == "ring"
+             else mb.build_torus_schedule(c["a"], c["b"]))
+    W, D = sched.workers, c["dim"]
+    g, cc = O.gen_metrics_inputs(c["seed"], W, D)
+    ctx = mb.Context(D, sched, torch.float32, 0)
+    ctx.set_metrics(True)
+    gd = [torch.tensor(x, dtype=torch.float32, device=DEV) for x in g]
+    cd = [torch.tensor(x, dtype=torch.float32, device=DEV) for x in cc]
+    out = [torch.empty_like(x) for x in cd]
+    agg = torch.empty((D + 63) // 64, dtype=torch.int64, device=DEV)
+    ctx.sign_round(c["round"], ETA, c["global_seed"], gd, cd, comp_out=out, agg_bits=agg)
+    m = ctx.metrics()
+    want = np.array([int(x, 16) for x in c["agg_words"]], dtype=np.uint64)
+    assert np.array_equal(agg.cpu().numpy().view(np.uint64), want)
+    assert m.has_matching and m.matches == c["matches"]
+    assert float.fromhex(c["rate"]) == m.matching_rate

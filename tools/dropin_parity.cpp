@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <string>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 using namespace marsit;
@@ -139,6 +140,43 @@ static void run_ssdm(const char* tag, const Schedule& sched, size_t D, int kind)
     std::printf("ssdm %-28s D=%zu %s\n", tag, D, failures ? "" : "ok");
 }
 
+// Concurrency: several host threads call marsit::gpu::marsit_round with the
+// same (D, schedule) at once (the reference's round is a pure function, and
+// this file's own CPU baseline calls it from many threads); every result
+// must equal the reference's serial result for that thread's inputs.
+static void run_concurrent(const char* tag, uint32_t n_threads, size_t D) {
+    const Schedule sched = build_ring_schedule(4);
+    const SyncConfig cfg{std::nullopt, 0x1.0p-10};
+    std::vector<std::vector<DenseVector>> g(n_threads);
+    std::vector<MarsitRoundResult> want, got(n_threads, MarsitRoundResult{DenseVector::zeros(1), {}, BitsAccount(4), false, std::nullopt});
+    std::vector<CompensationState> c0(4, CompensationState{DenseVector::zeros(D)});
+    for (uint32_t i = 0; i < n_threads; ++i) {
+        g[i] = inputs(4, D, 100 + i, 1, 1);
+        want.push_back(marsit::marsit_round(1, cfg, g[i], c0, sched, 2026 + i));
+    }
+    std::vector<std::thread> th;
+    std::vector<int> err(n_threads, 0);
+    for (uint32_t i = 0; i < n_threads; ++i)
+        th.emplace_back([&, i] {
+            try {
+                for (int rep = 0; rep < 3; ++rep)
+                    got[i] = marsit::gpu::marsit_round(1, cfg, g[i], c0, sched, 2026 + i);
+            } catch (...) {
+                err[i] = 1;
+            }
+        });
+    for (auto& t : th) t.join();
+    for (uint32_t i = 0; i < n_threads; ++i) {
+        expect(!err[i], "exception in a concurrent call", tag);
+        if (err[i]) continue;
+        expect(same(want[i].global_update, got[i].global_update), "concurrent global_update", tag);
+        for (uint32_t w = 0; w < 4; ++w)
+            expect(same(want[i].compensation[w].c, got[i].compensation[w].c), "concurrent compensation", tag);
+        expect(want[i].aggregate_bits == got[i].aggregate_bits, "concurrent aggregate_bits", tag);
+    }
+    std::printf("concurrent %-22s threads=%u D=%zu %s\n", tag, n_threads, D, failures ? "" : "ok");
+}
+
 // --time D: wall time of one marsit_round through the reference's own API
 // (host DenseVectors in, MarsitRoundResult out) — the reference's CPU round vs
 // marsit::gpu::marsit_round (staging, device round, read-back) — ring 8, fp64
@@ -200,6 +238,20 @@ int main(int argc, char** argv) {
         run_allreduce("ring6", build_ring_schedule(6), 97);
         run_allreduce("torus2x3", build_torus_schedule(2, 3), 1000);
         run_allreduce("torus4x2", build_torus_schedule(4, 2), 65537);
+        run_concurrent("ring4 same D", 6, 20011);
+        {  // a reduce-only table ends without consensus: the reference returns
+           // each worker's own state; the device path reports unsupported_error
+            Schedule red = build_ring_schedule(4);
+            red.steps.resize(3);
+            bool threw = false;
+            std::vector<std::vector<PackedSignVector>> signs(4, std::vector<PackedSignVector>(4, PackedSignVector::zeros(10)));
+            try {
+                marsit::gpu::allreduce_sign(signs, red, RoundContext{1, 1});
+            } catch (const unsupported_error&) {
+                threw = true;
+            }
+            expect(threw, "unsupported_error for a non-consensus schedule", "errors");
+        }
         // error mapping: non-finite u (overflow) raises non_finite_error like the reference
         bool threw = false;
         try {

@@ -45,7 +45,7 @@ int main(void) {
     desc.dtype = MARSIT_F64;
     desc.device = 0;
     desc.nranks = 1;
-    desc.transport = MARSIT_TRANSPORT_NCCL;
+    desc.transport = MARSIT_TRANSPORT_P2P; /* the default; unused with one rank */
     marsit_ctx* ctx = NULL;
     CHECK(marsit_ctx_create(&desc, &ctx));
 
