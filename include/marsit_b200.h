@@ -258,8 +258,10 @@ marsit_status marsit_ctx_set_consensus(marsit_ctx* ctx, int enable);
 /* Per-phase device timing (CUDA events on the launching stream).
  * Phases: 0 sign_extract, 1 exchange, 2 merge, 3 allgather, 4 decode_comp,
  * 5 export, 6 dense, 7 coins (coin precompute, on the context's side stream,
- * overlapping phase 0).  ms[i] accumulates; launches[i] counts kernel launches. */
-#define MARSIT_N_PHASES 8
+ * overlapping phase 0), 8 fused_round (small rounds: extract + merge + decode
+ * in one cluster launch).  ms[i] accumulates; launches[i] counts kernel
+ * launches. */
+#define MARSIT_N_PHASES 9
 marsit_status marsit_ctx_set_timing(marsit_ctx* ctx, int enable);
 marsit_status marsit_ctx_timing(marsit_ctx* ctx, float* ms, uint64_t* launches, int reset);
 

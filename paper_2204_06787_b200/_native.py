@@ -14,9 +14,9 @@ SO_PATH = os.environ.get("MARSIT_SO") or os.path.join(HERE, "libmarsit_b200.so")
 
 # status codes (include/marsit_b200.h)
 OK, EPARAM, ENONFINITE, EPROTOCOL, EUNSUPPORTED, ECUDA, ENCCL = range(7)
-N_PHASES = 8
+N_PHASES = 9
 PHASES = ("sign_extract", "exchange", "merge", "allgather", "decode_comp", "export", "dense",
-          "coins")
+          "coins", "fused_round")
 
 F32, F64 = 0, 1
 

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <chrono>
 #include <condition_variable>
 #include <cstdlib>
@@ -114,9 +115,18 @@ struct MergeRunner {
     unsigned* seg_bars = nullptr;  // per-(segment, lane) barrier words (MARSIT_SEG_BARRIER)
     bool seg_barrier = env_int("MARSIT_SEG_BARRIER", 1) != 0;
     const uint32_t* const* peer_bits = nullptr;  // P2P transport: device table [G]
-    // cluster merge (default; MARSIT_MERGE_COOP=1: the cooperative kernel)
-    bool cluster = env_int("MARSIT_MERGE_COOP", 0) == 0;
-    uint32_t csize = 16, tile_groups = 0, nsub = 1;
+    // MARSIT_MERGE_KERNEL=cluster: the thread-block-cluster merge (one cluster
+    // per segment, DSMEM totals, one launch); default: the cooperative merge,
+    // faster on B200 for every measured configuration
+    bool cluster = [] {
+        const char* e = std::getenv("MARSIT_MERGE_KERNEL");
+        return e && std::strcmp(e, "cluster") == 0;
+    }();
+    uint32_t csize = 16, tile_groups = 0, nsub = 1, stage = 0;
+    // fused small rounds (round_cluster_kernel): extra shared memory per CTA
+    // for every worker's packed tile + the aggregate; 0 = merge only
+    uint32_t fused_arrays = 0;
+    int fused_dtype = -1;  // element type of the fused kernel's occupancy query (0 f32, 1 f64)
     uint32_t* d_lvl_start = nullptr;
     uint32_t* d_lvl_begin = nullptr;
 
@@ -170,21 +180,35 @@ struct MergeRunner {
                     break;
                 }
             if (!ns) continue;
-            const size_t sm = size_t(std::max<uint32_t>(dp.max_slots, 1)) * tg * 16;
-            if (sm > 200 * 1024) continue;
+            // slots, + the level's staged r and d when they fit (pass 2 then
+            // reads shared memory instead of re-loading the operands)
+            const size_t base_sm = size_t(dp.max_slots + fused_arrays) * tg * 16;
+            const size_t stage_sm = size_t(2) * nl * tg * 16;
+            if (base_sm > 200 * 1024) continue;
+            const uint32_t stg = base_sm + stage_sm <= 200 * 1024 && env_int("MARSIT_MERGE_STAGE", 1) ? 1u : 0u;
+            const size_t sm = std::max<size_t>(base_sm + (stg ? stage_sm : 0), 16);
             int occ = 0;
-            if (merge_cluster_occupancy(int(ns), int(nl), cs, sm, &occ) != cudaSuccess || occ <= 0) {
+            if (fused_arrays && ns > 4) continue;  // the fused kernel's instantiations
+            const cudaError_t oe =
+                fused_arrays ? (fused_dtype == 1 ? round_cluster_occupancy<double>(int(ns), int(nl), cs, sm, &occ)
+                                                 : round_cluster_occupancy<float>(int(ns), int(nl), cs, sm, &occ))
+                             : merge_cluster_occupancy(int(ns), int(nl), cs, sm, &occ);
+            if (oe != cudaSuccess || occ <= 0) {
                 cudaGetLastError();
                 continue;
             }
             const uint64_t waves = ceil_div(seg_per_launch, uint64_t(occ));
             const uint64_t cost = waves * (uint64_t(tg) + 400);
+            if (env_int("MARSIT_MERGE_DEBUG", 0))
+                fprintf(stderr, "merge cluster: csize %u groups/CTA %u nsub %u stage %u occ %d waves %llu cost %llu\n",
+                        cs, tg, ns, stg, occ, (unsigned long long)waves, (unsigned long long)cost);
             if (cost < best) {
                 best = cost;
                 csize = cs;
                 tile_groups = tg;
                 nsub = ns;
                 smem = sm;
+                stage = stg;
             }
         }
         if (best == ~0ull) return fail(MARSIT_EUNSUPPORTED, "merge clusters do not fit the device");
@@ -302,6 +326,38 @@ struct MergeRunner {
         return MARSIT_OK;
     }
 
+    ClusterParams cluster_params(const uint32_t* leaves, uint32_t* agg, const uint32_t* coins,
+                                 uint64_t seed, uint64_t round, uint32_t seg_lo,
+                                 const uint32_t* coin_valid) const {
+        ClusterParams c{};
+        c.merges = d_merges;
+        c.seg_begin = d_seg_begin;
+        c.lvl_start = d_lvl_start;
+        c.lvl_begin = d_lvl_begin;
+        c.n_seg = n_seg;
+        c.s_first = s_first;
+        c.seg_lo = seg_lo;
+        c.csize = csize;
+        c.tile_groups = tile_groups;
+        c.words_proc = words_proc;
+        c.wst = wst;
+        c.ml = ml;
+        c.n_slots = dp.max_slots;
+        c.stage = stage;
+        c.seg_bits = L;
+        c.leaves = leaves;
+        c.peer_bits = peer_bits;
+        c.agg = agg;
+        c.agg_stride = agg_stride ? agg_stride : wst;
+        c.coins = coins;
+        c.coin_valid = coins ? coin_valid : nullptr;
+        c.totals = part_totals;
+        c.coin_end = coin_end;
+        c.seed = seed;
+        c.round = round;
+        return c;
+    }
+
     // Merge owned segments [seg_lo, seg_lo + seg_cnt) (seg_cnt <= seg_per_launch
     // per launch; more segments run as consecutive launches).
     marsit_status run(const uint32_t* leaves, uint32_t* agg, const uint32_t* coins, uint64_t seed,
@@ -309,31 +365,7 @@ struct MergeRunner {
                       uint32_t seg_cnt = ~0u, const uint32_t* coin_valid = nullptr) {
         if (seg_cnt == ~0u) seg_cnt = n_seg - seg_lo;
         if (cluster) {
-            ClusterParams c{};
-            c.merges = d_merges;
-            c.seg_begin = d_seg_begin;
-            c.lvl_start = d_lvl_start;
-            c.lvl_begin = d_lvl_begin;
-            c.n_seg = n_seg;
-            c.s_first = s_first;
-            c.seg_lo = seg_lo;
-            c.csize = csize;
-            c.tile_groups = tile_groups;
-            c.words_proc = words_proc;
-            c.wst = wst;
-            c.ml = ml;
-            c.n_slots = dp.max_slots;
-            c.seg_bits = L;
-            c.leaves = leaves;
-            c.peer_bits = peer_bits;
-            c.agg = agg;
-            c.agg_stride = agg_stride ? agg_stride : wst;
-            c.coins = coins;
-            c.coin_valid = coins ? coin_valid : nullptr;
-            c.totals = part_totals;
-            c.coin_end = coin_end;
-            c.seed = seed;
-            c.round = round;
+            const ClusterParams c = cluster_params(leaves, agg, coins, seed, round, seg_lo, coin_valid);
             if (seg_cnt == 0) return MARSIT_OK;
             CUDA_TRY(launch_merge_cluster(c, int(nsub), int(dp.level_width), seg_cnt, smem, st));
             ++*n_launch;
@@ -401,8 +433,10 @@ constexpr int kErrConsensus = 2;  // an aggregate segment differs from its owner
 
 // P2P flag value that releases every stream wait: written by a watchdog that
 // gave up (into its own flags and into its slot of every peer's flags) so no
-// stream stays blocked; a peer that sees it reports the abort.
-constexpr uint64_t kFlagAbort = ~0ull;
+// stream stays blocked; a peer that sees it reports the abort.  The stream
+// waits compare (int64_t)(flag - epoch) >= 0, so the value is the largest
+// positive int64 (all-ones would read as -1).
+constexpr uint64_t kFlagAbort = 0x7FFFFFFFFFFFFFFFull;
 
 // Bounded waits for multi-rank contexts (P2P epoch flags, NCCL collectives).
 // The round entry points hand every enqueued round to this thread; if a round
@@ -428,6 +462,7 @@ struct Watchdog {
     cudaStream_t st = nullptr;        // private stream: flag reads and releases
     cudaEvent_t ev_poll = nullptr;
     uint64_t* h_flags = nullptr;      // pinned copy of the local flags [2][G]
+    uint64_t* h_abort = nullptr;      // pinned [2][G] x kFlagAbort (the release values)
 
     explicit Watchdog(marsit_ctx* c);
     ~Watchdog();
@@ -460,6 +495,7 @@ struct marsit_ctx {
     uint32_t M = 0, S = 0, G = 1, rank = 0, ml = 0, s_own = 0, s_first = 0;
     uint32_t words64 = 0, words_proc = 0, wst = 0;
     int sm_count = 148;
+    bool fused = false;  // small rounds: one round_cluster_kernel launch (runtime.cu fused_round)
     // K1/K4 task order (StreamParams::reverse); MARSIT_L2_REUSE=0 disables
     bool l2_reuse = marsit_b200::env_int("MARSIT_L2_REUSE", 1) != 0;
     uint32_t task_dir = 0;

@@ -953,16 +953,23 @@ __device__ __forceinline__ void st_cluster_u64(void* local, uint32_t rank, unsig
     asm volatile("st.shared::cluster.u64 [%0], %1;" :: "r"(ra), "l"(v) : "memory");
 }
 
-template <int NSUB, int NL>
-__global__ void __launch_bounds__(kClusterThreads, 1) merge_cluster_kernel(const ClusterParams p) {
-    extern __shared__ uint4 cl_slots[];  // [n_slots][tile_groups] node values of this CTA's tile
+// The level loop of the cluster merge, shared by merge_cluster_kernel (leaves
+// in global memory: the extract's packed signs or a peer's) and the fused
+// small-round kernel (SMEM_LEAVES: every worker's packed tile in shared memory,
+// leaf w at leaf_smem + w * tile_groups; the final node also to agg_smem).
+// cl_slots: [n_slots][tile_groups] node values of this CTA's tile, then
+// (p.stage) [NL][2][tile_groups] the level's r and d staged by pass 1.
+template <int NSUB, int NL, bool SMEM_LEAVES>
+__device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, uint4* cl_slots,
+                                                     const uint4* leaf_smem, uint4* agg_smem) {
     constexpr int NCOL = NL * NSUB;
     constexpr int NW = kClusterThreads / 32;
     __shared__ uint32_t s_wt[NCOL][NW];    // warp totals per column
     __shared__ uint32_t s_wpre[NCOL][NW];  // exclusive warp prefix per column
     __shared__ uint32_t s_ctot[NCOL];      // CTA total per column
-    __shared__ unsigned long long s_all[2][kMaxClusterSize][NL];  // CTA totals of the cluster
+    __shared__ unsigned long long s_all[2][NL][kMaxClusterSize];  // CTA totals of the cluster
     __shared__ DevMerge s_m[kMaxSegMerges];
+    __shared__ const uint4* s_row[kMaxSegMerges][2];  // leaf operand rows (recv, local) or null
     __shared__ unsigned long long s_tot[kMaxSegMerges];  // cluster-wide draws of each merge
     __shared__ uint32_t s_valid[kMaxSegMerges];
     __shared__ uint32_t s_lvl[kMaxSegMerges + 1];
@@ -973,63 +980,83 @@ __global__ void __launch_bounds__(kClusterThreads, 1) merge_cluster_kernel(const
     const uint32_t sg = p.s_first + sl;
     const uint32_t mb = p.seg_begin[sl], nm = p.seg_begin[sl + 1] - mb;
     const uint32_t lb0 = p.lvl_start[sl], nlv = p.lvl_start[sl + 1] - lb0 - 1;
+    const uint32_t g_first = cr * p.tile_groups;
     for (uint32_t i = tid; i < nm; i += kClusterThreads) {
-        s_m[i] = p.merges[mb + i];
+        const DevMerge m = p.merges[mb + i];
+        s_m[i] = m;
         s_tot[i] = 0;
         s_valid[i] = p.coin_valid ? p.coin_valid[mb + i] : 0u;
+        // leaf rows resolved once (P2P: the source rank's buffer, over NVLink)
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+            const uint16_t src = o ? m.local_src : m.recv_src;
+            const uint32_t w = src & 0x3FFFu;
+            const uint4* row = nullptr;
+            if ((src & 0xC000u) == kSrcLeaf) {
+                if (SMEM_LEAVES)
+                    row = leaf_smem + size_t(w) * p.tile_groups;
+                else
+                    row = reinterpret_cast<const uint4*>(
+                              p.peer_bits ? p.peer_bits[w / p.ml] + (uint64_t(sg) * p.ml + w % p.ml) * p.wst
+                                          : p.leaves + (uint64_t((w / p.ml) * p.n_seg + sl) * p.ml + w % p.ml) * p.wst) +
+                          g_first;
+            }
+            s_row[i][o] = row;
+        }
     }
     for (uint32_t i = tid; i <= nlv; i += kClusterThreads) s_lvl[i] = p.lvl_begin[lb0 + i];
     // every CTA of the cluster is running before the first remote store
     cluster_sync_all();
 
     const uint32_t total_groups = p.words_proc / 4;
-    const uint32_t g_first = cr * p.tile_groups;
-    // group u of this thread: local index gl = u * kClusterThreads + tid,
-    // segment words [4 g, 4 g + 4) with g = g_first + gl
-    auto group_ok = [&](int u) -> bool {
-        const uint32_t gl = uint32_t(u) * kClusterThreads + tid;
-        return gl < p.tile_groups && g_first + gl < total_groups;
+    // groups of this CTA's tile that exist; those entirely below L need no mask
+    const uint32_t n_here = total_groups > g_first ? min(p.tile_groups, total_groups - g_first) : 0u;
+    const uint64_t full_groups = p.seg_bits / 128;  // groups whose 128 bits are all < L
+    const bool peer = p.peer_bits != nullptr;
+    uint4* const stage = cl_slots + size_t(p.n_slots) * p.tile_groups;  // valid when p.stage
+    auto load_src = [&](uint32_t k, int o, uint32_t gl) -> uint4 {
+        const uint4* row = s_row[k][o];
+        if (SMEM_LEAVES && row) return row[gl];
+        if (row) return peer ? __ldcg(row + gl) : __ldg(row + gl);
+        const uint16_t src = o ? s_m[k].local_src : s_m[k].recv_src;
+        return cl_slots[size_t(src & 0x3FFFu) * p.tile_groups + gl];
     };
-    auto vmask = [&](uint32_t word) -> uint32_t {
-        const int64_t rem = int64_t(p.seg_bits) - int64_t(word) * 32;
-        return rem >= 32 ? kFull : (rem <= 0 ? 0u : ((1u << rem) - 1u));
-    };
-    auto load_src = [&](uint16_t src, int u) -> uint4 {
-        const uint32_t idx = src & 0x3FFFu;
-        const uint32_t gl = uint32_t(u) * kClusterThreads + tid;
-        if ((src & 0xC000u) == kSrcSlot) return cl_slots[size_t(idx) * p.tile_groups + gl];
-        const uint32_t g = g_first + gl;
-        if (p.peer_bits) {  // P2P: the source rank's own buffer, over NVLink
-            const uint32_t* row = p.peer_bits[idx / p.ml] + (uint64_t(sg) * p.ml + idx % p.ml) * p.wst;
-            return __ldcg(reinterpret_cast<const uint4*>(row) + g);
+    // r (received operand) and d = (r ^ l) & valid of local group gl of merge k
+    auto diff = [&](uint32_t k, uint32_t gl, uint4& r, uint4& d) {
+        r = load_src(k, 0, gl);
+        const uint4 b = load_src(k, 1, gl);
+        d = make_uint4(r.x ^ b.x, r.y ^ b.y, r.z ^ b.z, r.w ^ b.w);
+        const uint64_t g = uint64_t(g_first) + gl;
+        if (g >= full_groups) {  // the segment's last bits: storage padding is 0
+            uint32_t mk[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t rem = int64_t(p.seg_bits) - int64_t(g * 4 + j) * 32;
+                mk[j] = rem >= 32 ? kFull : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+            }
+            d.x &= mk[0], d.y &= mk[1], d.z &= mk[2], d.w &= mk[3];
         }
-        const uint32_t* row =
-            p.leaves + (uint64_t((idx / p.ml) * p.n_seg + sl) * p.ml + idx % p.ml) * p.wst;
-        return __ldg(reinterpret_cast<const uint4*>(row) + g);
     };
-    auto diff = [&](const DevMerge& m, int u, uint32_t (&r)[4], uint32_t (&d)[4]) {
-        const uint4 a = load_src(m.recv_src, u), b = load_src(m.local_src, u);
-        const uint32_t w0 = (g_first + uint32_t(u) * kClusterThreads + tid) * 4;
-        r[0] = a.x, r[1] = a.y, r[2] = a.z, r[3] = a.w;
-        d[0] = (a.x ^ b.x) & vmask(w0);
-        d[1] = (a.y ^ b.y) & vmask(w0 + 1);
-        d[2] = (a.z ^ b.z) & vmask(w0 + 2);
-        d[3] = (a.w ^ b.w) & vmask(w0 + 3);
-    };
+    auto popc4 = [](const uint4& d) { return __popc(d.x) + __popc(d.y) + __popc(d.z) + __popc(d.w); };
 
     for (uint32_t v = 0; v < nlv; ++v) {
         const uint32_t k0 = s_lvl[v], nk = s_lvl[v + 1] - k0;
-        // pass 1: counts and warp scans
+        // pass 1: d, counts and warp scans (r and d staged for pass 2)
         uint32_t ex[NL][NSUB];
 #pragma unroll
         for (int i = 0; i < NL; ++i)
 #pragma unroll
             for (int u = 0; u < NSUB; ++u) {
+                const uint32_t gl = uint32_t(u) * kClusterThreads + tid;
                 uint32_t c = 0;
-                if (uint32_t(i) < nk && group_ok(u)) {
-                    uint32_t r[4], d[4];
-                    diff(s_m[k0 + i], u, r, d);
-                    c = __popc(d[0]) + __popc(d[1]) + __popc(d[2]) + __popc(d[3]);
+                if (uint32_t(i) < nk && gl < n_here) {
+                    uint4 r, d;
+                    diff(k0 + i, gl, r, d);
+                    c = popc4(d);
+                    if (p.stage) {
+                        stage[(i * 2) * p.tile_groups + gl] = r;
+                        stage[(i * 2 + 1) * p.tile_groups + gl] = d;
+                    }
                 }
                 uint32_t incl = c;
 #pragma unroll
@@ -1053,14 +1080,14 @@ __global__ void __launch_bounds__(kClusterThreads, 1) merge_cluster_kernel(const
             if (lane == 31) s_ctot[wid] = incl;
         }
         __syncthreads();
-        // this CTA's per-merge totals into every cluster CTA's slot [v & 1][cr]
+        // this CTA's per-merge totals into every cluster CTA's slot [v & 1][i][cr]
         if (uint32_t(tid) < p.csize) {
 #pragma unroll
             for (int i = 0; i < NL; ++i) {
                 unsigned long long t = 0;
 #pragma unroll
                 for (int u = 0; u < NSUB; ++u) t += s_ctot[i * NSUB + u];
-                st_cluster_u64(&s_all[v & 1][cr][i], uint32_t(tid), t);
+                st_cluster_u64(&s_all[v & 1][i][cr], uint32_t(tid), t);
             }
         }
         cluster_sync_all();
@@ -1070,11 +1097,14 @@ __global__ void __launch_bounds__(kClusterThreads, 1) merge_cluster_kernel(const
             if (uint32_t(i) >= nk) continue;
             const uint32_t k = k0 + i;
             const DevMerge& m = s_m[k];
-            unsigned long long pre = 0, tot = 0;
-            for (uint32_t q = 0; q < p.csize; ++q) {
-                const unsigned long long x = s_all[v & 1][q][i];
-                pre += q < cr ? x : 0ull;
-                tot += x;
+            // lower-ranked CTAs' totals (the tile's draw offset) and the
+            // cluster total: lane q holds CTA q's total, warp reductions
+            const unsigned long long x = uint32_t(lane) < p.csize ? s_all[v & 1][i][lane] : 0ull;
+            unsigned long long pre = uint32_t(lane) < cr ? x : 0ull, tot = x;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                pre += __shfl_xor_sync(kFull, pre, o);
+                tot += __shfl_xor_sync(kFull, tot, o);
             }
             // stream base: draws before this round's merges + the earlier
             // merges of the same (receiver, segment) stream (continuation)
@@ -1090,51 +1120,226 @@ __global__ void __launch_bounds__(kClusterThreads, 1) merge_cluster_kernel(const
             }
             const uint64_t valid_bits = uint64_t(s_valid[k]) * 32;
             const uint32_t* cw = p.coins ? p.coins + m.coin_off : nullptr;
-            uint64_t col_off = 0;  // totals of this CTA's earlier columns of merge i
+            uint64_t off = base + pre;  // + this CTA's earlier columns of merge i
+            // two groups per batch: their operand and coin loads are issued
+            // together (one round trip each) before the deposit ALU work
 #pragma unroll
-            for (int u = 0; u < NSUB; ++u) {
-                const uint64_t off_u = col_off;
-                col_off += s_ctot[i * NSUB + u];
-                if (!group_ok(u)) continue;
-                uint32_t r[4], d[4];
-                diff(m, u, r, d);
-                const uint32_t cnt = __popc(d[0]) + __popc(d[1]) + __popc(d[2]) + __popc(d[3]);
-                uint64_t n = base + pre + off_u + s_wpre[i * NSUB + u][wid] + ex[i][u];
-                if (cw && n + cnt <= valid_bits) {
+            for (int u0 = 0; u0 < NSUB; u0 += 2) {
+                uint4 r[2], d[2];
+                uint64_t n0[2];
+                bool live[2], fast[2];
+                uint32_t win[2][5];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const uint32_t pc = __popc(d[j]);
-                        if (pc) {
-                            const uint64_t wi = n >> 5;
-                            const uint32_t sh = uint32_t(n & 31);
-                            const uint32_t c0 = __ldg(cw + wi);
-                            const uint32_t c1 = (sh + pc > 32) ? __ldg(cw + wi + 1) : 0u;
-                            uint32_t mv[4];
-                            expand_masks(d[j], mv);
-                            r[j] ^= d[j] & ~expand_apply(__funnelshift_r(c0, c1, sh), mv);
-                            n += pc;
-                        }
+                for (int h = 0; h < 2; ++h) {
+                    const int u = u0 + h;
+                    const uint32_t gl = uint32_t(u) * kClusterThreads + tid;
+                    live[h] = u < NSUB && gl < n_here;
+                    fast[h] = false;
+                    if (u < NSUB) {
+                        n0[h] = off + s_wpre[i * NSUB + u][wid] + ex[i][u];
+                        off += s_ctot[i * NSUB + u];
                     }
-                } else {
-                    // beyond the precomputed budget: draw inline (same stream, same indices)
-                    const uint64_t key = m.key_mode ? m.key : stream_key(p.seed, 5, m.receiver, p.round, sg);
-                    uint64_t z = key + (n + 1) * kGamma;
+                    if (!live[h]) continue;
+                    if (p.stage) {
+                        r[h] = stage[(i * 2) * p.tile_groups + gl];
+                        d[h] = stage[(i * 2 + 1) * p.tile_groups + gl];
+                    } else {
+                        diff(k, gl, r[h], d[h]);
+                    }
+                    fast[h] = cw && n0[h] + popc4(d[h]) <= valid_bits;
+                    if (fast[h]) {
+                        const uint32_t* c = cw + (n0[h] >> 5);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) r[j] ^= d[j] & ~coin_word(d[j], z, m.thresh11);
+                        for (int q = 0; q < 5; ++q) win[h][q] = __ldg(c + q);
+                    }
                 }
-                const uint4 out = make_uint4(r[0], r[1], r[2], r[3]);
-                const uint32_t gl = uint32_t(u) * kClusterThreads + tid;
-                if (m.out_slot != kNone) cl_slots[size_t(m.out_slot) * p.tile_groups + gl] = out;
-                if (m.out_global == kFinal)
-                    reinterpret_cast<uint4*>(p.agg + uint64_t(sg) * p.agg_stride)[g_first + gl] = out;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (!live[h]) continue;
+                    uint32_t rr[4] = {r[h].x, r[h].y, r[h].z, r[h].w};
+                    const uint32_t dd[4] = {d[h].x, d[h].y, d[h].z, d[h].w};
+                    if (fast[h]) {
+                        // sliding 64-bit window over the 5 coin words: word j's
+                        // coins start o bits into (lo, hi); at most one advance
+                        // per word (popc <= 32)
+                        uint32_t lo = win[h][0], hi = win[h][1], o = uint32_t(n0[h] & 31), a = 0;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            uint32_t mv[4];
+                            expand_masks(dd[j], mv);
+                            rr[j] ^= dd[j] & ~expand_apply(__funnelshift_r(lo, hi, o), mv);
+                            o += __popc(dd[j]);
+                            if (j < 3) {
+                                // (lo, hi) = (win[a], win[a + 1]) after a advances
+                                const bool adv = o >= 32;
+                                uint32_t nx = win[h][2];
+                                if (j >= 1) nx = a >= 1 ? win[h][3] : nx;
+                                if (j >= 2) nx = a >= 2 ? win[h][4] : nx;
+                                lo = adv ? hi : lo;
+                                hi = adv ? nx : hi;
+                                o -= adv ? 32u : 0u;
+                                a += adv ? 1u : 0u;
+                            }
+                        }
+                    } else {
+                        // beyond the precomputed budget: draw inline (same stream, same indices)
+                        const uint64_t key =
+                            m.key_mode ? m.key : stream_key(p.seed, 5, m.receiver, p.round, sg);
+                        uint64_t z = key + (n0[h] + 1) * kGamma;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) rr[j] ^= dd[j] & ~coin_word(dd[j], z, m.thresh11);
+                    }
+                    const uint4 out = make_uint4(rr[0], rr[1], rr[2], rr[3]);
+                    const uint32_t gl = uint32_t(u0 + h) * kClusterThreads + tid;
+                    if (m.out_slot != kNone) cl_slots[size_t(m.out_slot) * p.tile_groups + gl] = out;
+                    if (m.out_global == kFinal) {
+                        reinterpret_cast<uint4*>(p.agg + uint64_t(sg) * p.agg_stride)[g_first + gl] = out;
+                        if (SMEM_LEAVES) agg_smem[gl] = out;
+                    }
+                }
             }
         }
-        // no block barrier here: slots are read back by the threads that
-        // wrote them, and s_wt / s_wpre / s_ctot are rewritten next level
-        // only after that level's first block barrier... except s_ctot /
-        // s_wpre, which this level still reads above: the next level writes
-        // them after its first __syncthreads, which every thread reaches
-        // only after finishing this pass.
+        // no block barrier here: slots and the staging are read back by the
+        // threads that wrote them; s_wt / s_wpre / s_ctot are rewritten by
+        // the next level only after its first block barrier, which every
+        // thread reaches after finishing this pass
+    }
+}
+
+template <int NSUB, int NL>
+__global__ void __launch_bounds__(kClusterThreads, 1) merge_cluster_kernel(const ClusterParams p) {
+    extern __shared__ uint4 cl_dyn[];
+    cluster_merge_levels<NSUB, NL, false>(p, cl_dyn, nullptr, nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// Fused small round (see FusedParams): K1 -> K2 -> K3/K4 of one segment per
+// cluster in one launch.  A "task" is one worker's 128 coordinates of one
+// 4-word group of this CTA's tile; a warp takes one task per step: lane l
+// holds coordinates 4l..4l+3 (one 16-byte quad of g and of c), the four sign
+// nibbles of a word meet by OR-shuffles over 8 lanes (as in K1), and the
+// decode reads the group's aggregate words from shared memory.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ bool quad_real(uint64_t j, uint64_t seg_len, uint64_t gi, uint64_t dim) {
+    return j + 3 < seg_len && gi + 3 < dim;
+}
+
+template <typename T, int NSUB, int NL>
+__global__ void __launch_bounds__(kClusterThreads, 1)
+    round_cluster_kernel(const ClusterParams p, const FusedParams<T> f) {
+    extern __shared__ uint4 fz_dyn[];  // [workers][tg] leaves, [tg] aggregate, then the merge's slots / staging
+    const uint32_t tg = p.tile_groups;
+    uint4* leaf = fz_dyn;
+    uint4* aggs = leaf + size_t(f.workers) * tg;
+    uint4* slots = aggs + tg;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t cr = cluster_ctarank();
+    const uint32_t sl = p.seg_lo + blockIdx.x / p.csize;
+    const uint32_t g_first = cr * tg;
+    const uint32_t total_groups = p.words_proc / 4;
+    const uint32_t n_here = total_groups > g_first ? min(tg, total_groups - g_first) : 0u;
+    const uint64_t seg0 = uint64_t(sl) * p.seg_bits;  // first coordinate of the segment (G == 1)
+    constexpr int B = 2;  // groups per warp step: 2B quad loads in flight per lane
+    constexpr uint32_t NWARP = kClusterThreads / 32;
+    // K1: u = g + c, sign nibbles -> packed words in shared memory
+    T fin = T(0);
+    for (uint32_t w = 0; w < f.workers; ++w) {
+        const T* __restrict__ gw = f.g[w];
+        const T* __restrict__ cw = f.c[w];
+        for (uint32_t gl0 = wid; gl0 < n_here; gl0 += NWARP * B) {
+            Quad<T> gv[B], cv[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const uint32_t gl = gl0 + b * NWARP;
+                const uint64_t j = uint64_t(g_first + gl) * 128 + lane * 4;
+                const uint64_t gi = seg0 + j;
+                if (gl < n_here && quad_real<T>(j, p.seg_bits, gi, f.dim)) {
+                    gv[b] = load4(gw + gi);
+                    cv[b] = load4(cw + gi);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const bool in = gl < n_here && j + k < p.seg_bits && gi + k < f.dim;
+                        gv[b].v[k] = in ? gw[gi + k] : T(0);
+                        cv[b].v[k] = in ? cw[gi + k] : T(0);
+                    }
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const uint32_t gl = gl0 + b * NWARP;
+                if (gl >= n_here) break;
+                const uint64_t j = uint64_t(g_first + gl) * 128 + lane * 4;
+                T u[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    u[k] = add_rn(add_rn(gv[b].v[k], cv[b].v[k]), T(0));  // -0.0 -> +0.0 (sign_vector.hpp:70)
+                    fin = fma_rn(u[k], T(0), fin);
+                }
+                uint32_t nib = sign_nibble(u[0], u[1], u[2], u[3]);
+                const uint64_t valid = j >= p.seg_bits ? 0 : p.seg_bits - j;  // storage padding -> 0
+                if (valid < 4) nib &= (1u << valid) - 1u;
+                uint32_t v = nib << ((lane & 7) * 4);
+                v |= __shfl_xor_sync(kFull, v, 1);
+                v |= __shfl_xor_sync(kFull, v, 2);
+                v |= __shfl_xor_sync(kFull, v, 4);
+                if ((lane & 7) == 0) reinterpret_cast<uint32_t*>(leaf + size_t(w) * tg + gl)[lane >> 3] = v;
+            }
+        }
+    }
+    if (__any_sync(kFull, !(fin == fin)) && lane == 0) atomicOr(f.err, 1);
+    __syncthreads();
+    // K2: the segment's merge DAG (cluster-wide draw offsets via DSMEM)
+    cluster_merge_levels<NSUB, NL, true>(p, slots, leaf, aggs);
+    __syncthreads();
+    // K3/K4: g_t = +-eta from the aggregate, c' = (g + c) - g_t
+    for (uint32_t w = 0; w < f.workers; ++w) {
+        const T* __restrict__ gw = f.g[w];
+        const T* cw = f.c[w];  // may alias c_out (in place)
+        T* co = f.c_out[w];
+        T* upd = w == 0 ? f.update : nullptr;
+        for (uint32_t gl0 = wid; gl0 < n_here; gl0 += NWARP * B) {
+            Quad<T> gv[B], cv[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const uint32_t gl = gl0 + b * NWARP;
+                const uint64_t j = uint64_t(g_first + gl) * 128 + lane * 4;
+                const uint64_t gi = seg0 + j;
+                if (gl < n_here && quad_real<T>(j, p.seg_bits, gi, f.dim)) {
+                    gv[b] = load4(gw + gi);
+                    cv[b] = load4_rw(cw + gi);
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const uint32_t gl = gl0 + b * NWARP;
+                if (gl >= n_here) break;
+                const uint64_t j = uint64_t(g_first + gl) * 128 + lane * 4;
+                const uint64_t gi = seg0 + j;
+                const uint32_t word = reinterpret_cast<const uint32_t*>(aggs + gl)[lane >> 3];
+                const uint32_t nib = (word >> ((lane & 7) * 4)) & 0xFu;
+                if (quad_real<T>(j, p.seg_bits, gi, f.dim)) {
+                    Quad<T> out, up;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const T gt = ((nib >> k) & 1u) ? f.eta : -f.eta;
+                        out.v[k] = sub_rn(add_rn(gv[b].v[k], cv[b].v[k]), gt);
+                        up.v[k] = gt;
+                    }
+                    store4(co + gi, out);
+                    if (upd) store4(upd + gi, up);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (j + k < p.seg_bits && gi + k < f.dim) {
+                            const T gt = ((nib >> k) & 1u) ? f.eta : -f.eta;
+                            co[gi + k] = sub_rn(add_rn(gw[gi + k], cw[gi + k]), gt);
+                            if (upd) upd[gi + k] = gt;
+                        }
+                }
+            }
+        }
     }
 }
 
@@ -1760,6 +1965,78 @@ static cudaError_t cluster_occ_t(uint32_t csize, size_t smem, int* clusters) {
         default: return cudaErrorInvalidValue;                           \
     }
 
+template <typename T, int NSUB, int NL>
+static cudaError_t fused_attr() {
+    auto k = round_cluster_kernel<T, NSUB, NL>;
+    static cudaError_t e = [&] {
+        cudaError_t r = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        return r;
+    }();
+    return e;
+}
+
+template <typename T, int NSUB, int NL>
+static cudaError_t fused_launch_t(const ClusterParams& p, const FusedParams<T>& f, uint32_t clusters,
+                                  size_t smem, cudaStream_t st) {
+    cudaError_t e = fused_attr<T, NSUB, NL>();
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(clusters * p.csize);
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, round_cluster_kernel<T, NSUB, NL>, p, f);
+}
+
+template <typename T, int NSUB, int NL>
+static cudaError_t fused_occ_t(uint32_t csize, size_t smem, int* clusters) {
+    cudaError_t e = fused_attr<T, NSUB, NL>();
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(csize);
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaOccupancyMaxActiveClusters(clusters, round_cluster_kernel<T, NSUB, NL>, &cfg);
+}
+
+#define MARSIT_FUSED_DISPATCH(FN, ...)                                   \
+    switch (nl * 100 + nsub) {                                           \
+        case 101: return FN<T, 1, 1>(__VA_ARGS__);                       \
+        case 102: return FN<T, 2, 1>(__VA_ARGS__);                       \
+        case 104: return FN<T, 4, 1>(__VA_ARGS__);                       \
+        case 201: return FN<T, 1, 2>(__VA_ARGS__);                       \
+        case 202: return FN<T, 2, 2>(__VA_ARGS__);                       \
+        case 204: return FN<T, 4, 2>(__VA_ARGS__);                       \
+        default: return cudaErrorInvalidValue;                           \
+    }
+
+template <typename T>
+cudaError_t launch_round_cluster(const ClusterParams& p, const FusedParams<T>& f, int nsub, int nl,
+                                 uint32_t clusters, size_t smem, cudaStream_t st) {
+    MARSIT_FUSED_DISPATCH(fused_launch_t, p, f, clusters, smem, st)
+}
+
+template <typename T>
+cudaError_t round_cluster_occupancy(int nsub, int nl, uint32_t csize, size_t smem, int* clusters) {
+    MARSIT_FUSED_DISPATCH(fused_occ_t, csize, smem, clusters)
+}
+
 cudaError_t launch_merge_cluster(const ClusterParams& p, int nsub, int nl, uint32_t clusters,
                                  size_t smem, cudaStream_t st) {
     MARSIT_CLUSTER_DISPATCH(cluster_launch_t, p, clusters, smem, st)
@@ -1974,6 +2251,18 @@ cudaError_t preload_kernels() {
             reinterpret_cast<const void*>(merge_cluster_kernel<2, 2>),
             reinterpret_cast<const void*>(merge_cluster_kernel<4, 2>),
             reinterpret_cast<const void*>(merge_cluster_kernel<8, 2>),
+            reinterpret_cast<const void*>(round_cluster_kernel<float, 1, 1>),
+            reinterpret_cast<const void*>(round_cluster_kernel<float, 2, 1>),
+            reinterpret_cast<const void*>(round_cluster_kernel<float, 4, 1>),
+            reinterpret_cast<const void*>(round_cluster_kernel<float, 1, 2>),
+            reinterpret_cast<const void*>(round_cluster_kernel<float, 2, 2>),
+            reinterpret_cast<const void*>(round_cluster_kernel<float, 4, 2>),
+            reinterpret_cast<const void*>(round_cluster_kernel<double, 1, 1>),
+            reinterpret_cast<const void*>(round_cluster_kernel<double, 2, 1>),
+            reinterpret_cast<const void*>(round_cluster_kernel<double, 4, 1>),
+            reinterpret_cast<const void*>(round_cluster_kernel<double, 1, 2>),
+            reinterpret_cast<const void*>(round_cluster_kernel<double, 2, 2>),
+            reinterpret_cast<const void*>(round_cluster_kernel<double, 4, 2>),
             reinterpret_cast<const void*>(coins_kernel),
             reinterpret_cast<const void*>(export_bits_kernel),
             reinterpret_cast<const void*>(flag_write_kernel),
@@ -2023,6 +2312,9 @@ cudaError_t preload_kernels() {
     template cudaError_t launch_dense_reduce<T>(const DenseParams<T>&, int, cudaStream_t);      \
     template cudaError_t launch_sub_update<T>(T* const*, uint32_t, const T*, uint64_t, int,     \
                                               cudaStream_t);                                    \
+    template cudaError_t launch_round_cluster<T>(const ClusterParams&, const FusedParams<T>&, int,  \
+                                                 int, uint32_t, size_t, cudaStream_t);          \
+    template cudaError_t round_cluster_occupancy<T>(int, int, uint32_t, size_t, int*);          \
     template cudaError_t launch_dense_leaf<T>(const T* const*, const T* const*, uint32_t,       \
                                               uint64_t, uint64_t, uint32_t, uint32_t, T*, int*,  \
                                               int, cudaStream_t, T* const*);

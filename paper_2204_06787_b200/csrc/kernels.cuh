@@ -107,6 +107,7 @@ struct ClusterParams {
     uint32_t csize;               // CTAs per cluster
     uint32_t tile_groups;         // 4-word groups per CTA tile
     uint32_t words_proc, wst, ml, n_slots;
+    uint32_t stage;               // 1: pass 1 stages r and d in shared memory for pass 2
     uint64_t seg_bits;            // L
     const uint32_t* leaves;       // leaf(w, sl) = leaves + ((w/ml*n_seg + sl)*ml + w%ml)*wst
     const uint32_t* const* peer_bits;  // P2P: leaf(w, sl) = peer_bits[w/ml] + ((s_first+sl)*ml + w%ml)*wst
@@ -120,6 +121,30 @@ struct ClusterParams {
 };
 cudaError_t launch_merge_cluster(const ClusterParams& p, int nsub, int nl, uint32_t clusters,
                                  size_t smem, cudaStream_t st);
+
+// Fused small round (one launch, G == 1): one cluster per segment extracts
+// its tile of every worker into shared memory (K1), runs the segment's merge
+// DAG with the cluster merge's level loop (K2), and decodes + updates the
+// compensation of its tile (K3/K4; the re-read of g and c is L2-resident at
+// these sizes).  Needs every worker local, M <= kFusedMaxWorkers, 16-byte
+// aligned quads (L % 4 == 0).
+constexpr uint32_t kFusedMaxWorkers = 16;
+template <typename T>
+struct FusedParams {
+    const T* g[kFusedMaxWorkers];
+    const T* c[kFusedMaxWorkers];
+    T* c_out[kFusedMaxWorkers];
+    uint32_t workers;
+    uint64_t dim;
+    T eta;
+    T* update;   // optional g_t
+    int* err;    // non-finite latch
+};
+template <typename T>
+cudaError_t launch_round_cluster(const ClusterParams& p, const FusedParams<T>& f, int nsub, int nl,
+                                 uint32_t clusters, size_t smem, cudaStream_t st);
+template <typename T>
+cudaError_t round_cluster_occupancy(int nsub, int nl, uint32_t csize, size_t smem, int* clusters);
 // Concurrently resident clusters of csize CTAs with `smem` dynamic bytes (0 if unsupported).
 cudaError_t merge_cluster_occupancy(int nsub, int nl, uint32_t csize, size_t smem, int* clusters);
 

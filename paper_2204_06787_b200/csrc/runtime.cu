@@ -75,6 +75,10 @@ Watchdog::Watchdog(marsit_ctx* c) : ctx(c) {
     cudaEventCreateWithFlags(&ev_poll, cudaEventDisableTiming);
     cudaHostAlloc(reinterpret_cast<void**>(&h_flags), 2 * size_t(ctx->G) * sizeof(uint64_t),
                   cudaHostAllocDefault);
+    cudaHostAlloc(reinterpret_cast<void**>(&h_abort), 2 * size_t(ctx->G) * sizeof(uint64_t),
+                  cudaHostAllocDefault);
+    if (h_abort)
+        for (size_t i = 0; i < 2 * size_t(ctx->G); ++i) h_abort[i] = kFlagAbort;
     th = std::thread([this] { loop(); });
 }
 
@@ -88,6 +92,7 @@ Watchdog::~Watchdog() {
     for (auto& it : pending) cudaEventDestroy(it.ev);
     for (auto e : free_events) cudaEventDestroy(e);
     if (h_flags) cudaFreeHost(h_flags);
+    if (h_abort) cudaFreeHost(h_abort);
     if (ev_poll) cudaEventDestroy(ev_poll);
     if (st) cudaStreamDestroy(st);
 }
@@ -116,14 +121,14 @@ marsit_status Watchdog::watch(cudaStream_t s, uint64_t epoch) {
 // (kFlagAbort in this rank's slots of their flags); NCCL is aborted.
 void Watchdog::give_up(marsit_status status, const std::string& msg) {
     ctx_set_failed(ctx, status, msg);
-    if (ctx->p2p) {
+    if (ctx->p2p && h_abort) {
         const size_t n = 2 * size_t(ctx->G);
-        cudaMemsetAsync(ctx->flags, 0xFF, n * sizeof(uint64_t), st);
+        cudaMemcpyAsync(ctx->flags, h_abort, n * sizeof(uint64_t), cudaMemcpyHostToDevice, st);
         for (uint32_t q = 0; q < ctx->G && q < ctx->peer_flags.size(); ++q) {
             if (q == ctx->rank || !ctx->peer_flags[q]) continue;
             for (int which = 0; which < 2; ++which)
-                cudaMemsetAsync(const_cast<uint64_t*>(ctx->peer_flags[q]) + size_t(which) * ctx->G + ctx->rank,
-                                0xFF, sizeof(uint64_t), st);
+                cudaMemcpyAsync(const_cast<uint64_t*>(ctx->peer_flags[q]) + size_t(which) * ctx->G + ctx->rank,
+                                h_abort, sizeof(uint64_t), cudaMemcpyHostToDevice, st);
         }
         poll_stream(st, ev_poll);
     }
@@ -518,7 +523,7 @@ marsit_status marsit_ctx::end_phase(int phase, cudaStream_t st, cudaEvent_t a, u
 namespace {
 
 enum Phase { kPhExtract = 0, kPhExchange, kPhMerge, kPhAllgather, kPhDecode, kPhExport, kPhDense,
-             kPhCoins };
+             kPhCoins, kPhFused };
 
 template <typename T>
 StreamParams<T> stream_params(marsit_ctx* ctx, const void* const* g, const void* const* c,
@@ -696,11 +701,10 @@ marsit_status run_coins(marsit_ctx* ctx, uint64_t seed, uint64_t round, cudaStre
         if (ctx->coin_tag[b].valid && ctx->coin_tag[b].seed == seed &&
             ctx->coin_tag[b].round == round) {
             ctx->cur_coin = b;
-            // prefetched underneath the last decode: wait for it here, before
-            // the extract, so the extract and the merge stay adjacent in the
-            // stream (programmatic dependent launch of the merge)
-            CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_coin_done[b], 0));
-            ctx->coins_pending = false;
+            // prefetched underneath the last decode: only the merge needs the
+            // coins, so the extract may overlap the tail of the prefetch (small
+            // rounds: the coin kernel outlasts the decode); run_merge waits
+            ctx->coins_pending = true;
             return MARSIT_OK;
         }
     const int b = 1 - ctx->cur_coin;
@@ -1129,6 +1133,51 @@ marsit_status check_round_args(marsit_ctx* ctx, double eta_s, const void* const*
     return MARSIT_OK;
 }
 
+// Small rounds on one GPU (ctx->fused): extract, merge and decode of a
+// segment in one cluster launch (round_cluster_kernel), the coins of the next
+// round prefetched underneath as usual.
+template <typename T>
+marsit_status fused_round(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_t seed,
+                          const void* const* g, const void* const* c, void* const* c_out,
+                          uint64_t* d_agg_bits, void* d_update, cudaStream_t st) {
+    marsit_status s;
+    if ((s = run_coins(ctx, seed, t, st))) return s;
+    if (ctx->coins_pending) {
+        CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_coin_done[ctx->cur_coin], 0));
+        ctx->coins_pending = false;
+    }
+    // the next round's coins run beside this round's clusters (the other
+    // buffer; their budget reads the draw ends of the round before, which
+    // only sizes the work, never the bits)
+    if ((s = prefetch_coins(ctx, seed, t, st))) return s;
+    cudaEvent_t ev;
+    if ((s = ctx->begin_phase(st, &ev))) return s;
+    FusedParams<T> f{};
+    for (uint32_t w = 0; w < ctx->M; ++w) {
+        f.g[w] = static_cast<const T*>(g[w]);
+        f.c[w] = static_cast<const T*>(c[w]);
+        f.c_out[w] = static_cast<T*>(c_out[w]);
+    }
+    f.workers = ctx->M;
+    f.dim = ctx->D;
+    f.eta = T(eta_s);
+    f.update = static_cast<T*>(d_update);
+    f.err = ctx->err;
+    const MergeRunner& mr = ctx->merge;
+    const ClusterParams p = mr.cluster_params(nullptr, ctx->agg, ctx->coin_buf[ctx->cur_coin], seed, t, 0,
+                                              ctx->coin_valid[ctx->cur_coin]);
+    CUDA_TRY(launch_round_cluster<T>(p, f, int(mr.nsub), int(mr.dp.level_width), ctx->S, mr.smem, st));
+    if ((s = ctx->end_phase(kPhFused, st, ev, 1))) return s;
+    return run_export(ctx, d_agg_bits, st);
+}
+
+bool fused_eligible(const marsit_ctx* ctx, const void* const* g, const void* const* c,
+                    void* const* c_out, void* const* params, void* update) {
+    return ctx->fused && !ctx->metrics && !params && !ctx->pipeline &&
+           vec_ok_ptrs(ctx, g, c) && vec_ok_ptrs(ctx, (const void* const*)c_out, c) &&
+           (!update || aligned16(update));
+}
+
 marsit_status sign_round_impl(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_t seed,
                               const void* const* d_grads, const void* const* d_comp,
                               void* const* d_comp_out, void* const* params, uint64_t* d_agg_bits,
@@ -1139,6 +1188,10 @@ marsit_status sign_round_impl(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_
         return fail(MARSIT_EUNSUPPORTED, "external-transport context: use marsit_round_phase");
     if (ctx->p2p && !ctx->peers_set) return fail(MARSIT_EPARAM, "P2P transport: call marsit_ctx_set_peers");
     note_round(ctx, t, false);
+    if (fused_eligible(ctx, d_grads, d_comp, d_comp_out, params, d_update))
+        return ctx->dtype == MARSIT_F32
+                   ? fused_round<float>(ctx, t, eta_s, seed, d_grads, d_comp, d_comp_out, d_agg_bits, d_update, st)
+                   : fused_round<double>(ctx, t, eta_s, seed, d_grads, d_comp, d_comp_out, d_agg_bits, d_update, st);
     if (ctx->pipeline) {
         // st : coins? E ............ D0 D1 ... D(S-1)   (D_s waits M_s)
         // aux:           M0 M1 ... M(S-1) coins(t+1)      (after E)
@@ -1381,6 +1434,17 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
 
     // merge plan, coin budget, tiling
     MergeRunner& mr = ctx->merge;
+    // small one-GPU rounds run fused (one cluster launch: extract, merge,
+    // decode; the decode's re-read of g and c stays in L2): every worker
+    // local, L % 4 == 0, the inputs well inside L2 (MARSIT_FUSED=0 disables)
+    ctx->fused = G == 1 && hs.workers <= kFusedMaxWorkers && ctx->vec_ok &&
+                 uint64_t(hs.workers) * ctx->D * ctx->esize * 2 <= (96ull << 20) &&
+                 env_int("MARSIT_FUSED", 1) != 0;
+    if (ctx->fused) {
+        mr.cluster = true;
+        mr.fused_arrays = hs.workers + 1;
+        mr.fused_dtype = desc->dtype == MARSIT_F64 ? 1 : 0;
+    }
     marsit_status st = mr.cluster ? lower_cluster_plan(ctx->plan, ctx->s_first, ctx->s_own, mr.dp)
                                   : lower_plan(ctx->plan, ctx->s_first, ctx->s_own, mr.dp);
     if (st) return st;
@@ -1402,7 +1466,13 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     if (ctx->pipeline) {
         if ((st = mr.configure(ctx->sm_count, 1, env_int("MARSIT_PIPE_MERGE_CTAS", 1)))) return st;
     } else {
-        if ((st = mr.configure(ctx->sm_count))) return st;
+        st = mr.configure(ctx->sm_count);
+        if (st && ctx->fused) {  // the fused tiles do not fit: merge-only clusters
+            ctx->fused = false;
+            mr.fused_arrays = 0;
+            st = mr.configure(ctx->sm_count);
+        }
+        if (st) return st;
     }
     if ((st = mr.upload())) return st;
 
@@ -1438,7 +1508,9 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
         for (int b = 0; b < 2; ++b) {
             CUDA_TRY(cudaMalloc(&ctx->coin_valid[b], sizeof(uint32_t) * std::max<uint32_t>(mr.dp.n_merges, 1)));
             CUDA_TRY(cudaMemset(ctx->coin_valid[b], 0, sizeof(uint32_t) * std::max<uint32_t>(mr.dp.n_merges, 1)));
-            CUDA_TRY(cudaMalloc(&ctx->coin_buf[b], sizeof(uint32_t) * ctx->coin_total_words));
+            // + slack: a merge group reads its 5-word coin window whole
+            CUDA_TRY(cudaMalloc(&ctx->coin_buf[b], sizeof(uint32_t) * (ctx->coin_total_words + 16)));
+            CUDA_TRY(cudaMemset(ctx->coin_buf[b], 0, sizeof(uint32_t) * (ctx->coin_total_words + 16)));
             CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_coin_done[b], cudaEventDisableTiming));
         }
     ctx->coin_prefetch = env_int("MARSIT_COIN_PREFETCH", 1) != 0;
