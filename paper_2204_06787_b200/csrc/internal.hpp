@@ -115,6 +115,7 @@ struct MergeRunner {
     unsigned* seg_bars = nullptr;  // per-(segment, lane) barrier words (MARSIT_SEG_BARRIER)
     bool seg_barrier = env_int("MARSIT_SEG_BARRIER", 1) != 0;
     const uint32_t* const* peer_bits = nullptr;  // P2P transport: device table [G]
+    int* err = nullptr;                          // the context's error latch (checked builds)
     // MARSIT_MERGE_KERNEL=cluster: the thread-block-cluster merge (one cluster
     // per segment, DSMEM totals, one launch); default: the cooperative merge,
     // faster on B200 for every measured configuration
@@ -355,6 +356,7 @@ struct MergeRunner {
         c.coin_end = coin_end;
         c.seed = seed;
         c.round = round;
+        c.err = err;
         return c;
     }
 
@@ -402,6 +404,7 @@ struct MergeRunner {
         c.coin_valid = coins ? coin_valid : nullptr;
         c.coin_end = coin_end;
         c.seg_bars = seg_barrier ? seg_bars : nullptr;
+        c.err = err;
         for (uint32_t s0 = seg_lo; s0 < seg_lo + seg_cnt; s0 += seg_per_launch) {
             c.seg_lo = s0;
             c.seg_cnt = std::min(seg_per_launch, seg_lo + seg_cnt - s0);
@@ -430,6 +433,7 @@ struct TimedPair {
 // Device error latch bits (marsit_ctx::err, reported by marsit_ctx_check).
 constexpr int kErrNonFinite = 1;  // DenseVector finiteness (dense_vector.hpp:25-29)
 constexpr int kErrConsensus = 2;  // an aggregate segment differs from its owner's (allreduce.hpp:32-43)
+constexpr int kErrBounds = 8;     // checked builds (MARSIT_CHECKED): an index failed its bound
 
 // P2P flag value that releases every stream wait: written by a watchdog that
 // gave up (into its own flags and into its slot of every peer's flags) so no

@@ -51,6 +51,25 @@ __device__ __forceinline__ uint64_t mix64f(uint64_t z) {
 }
 
 // ---------------------------------------------------------------------------
+// Checked builds (MARSIT_CHECKED, tools/gpu/checked.sh; compute-sanitizer is
+// closed on this GPU pool): jitter() sleeps a pseudo-random time at the
+// synchronisation points of the merge kernels so that any missing ordering
+// shows up as a result that differs from the oracle; BOUNDS(cond, err) latches
+// err |= 8 (reported by marsit_ctx_check) instead of making an access whose
+// index failed its bound.  Both compile to nothing in the product build.
+// ---------------------------------------------------------------------------
+#ifdef MARSIT_CHECKED
+__device__ __forceinline__ void jitter(uint32_t a) {
+    const uint64_t h = mix64((uint64_t(blockIdx.x) << 40) ^ (uint64_t(a) << 20) ^ uint64_t(clock64()));
+    if ((h & 3u) == 0) __nanosleep(uint32_t(h >> 8) & 4095u);
+}
+#define MARSIT_BOUNDS_OK(cond, errp) ((cond) ? true : (((errp) ? atomicOr((errp), 8) : 0), false))
+#else
+__device__ __forceinline__ void jitter(uint32_t) {}
+#define MARSIT_BOUNDS_OK(cond, errp) true
+#endif
+
+// ---------------------------------------------------------------------------
 // Memory helpers
 // ---------------------------------------------------------------------------
 // Streaming 128-bit loads that do not allocate in L1 (each byte is read once).
@@ -812,6 +831,7 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
         // counter; the prefix never reads another segment's counts).
         unsigned seg_tok = 0;
         cg::grid_group::arrival_token token{};
+        jitter(2 * k);
         if (p.seg_bars)
             seg_tok = seg_barrier_arrive(p.seg_bars + blockIdx.x / p.part_tiles, lt == 0, p.part_tiles);
         else
@@ -829,6 +849,7 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
             seg_barrier_wait(p.seg_bars + blockIdx.x / p.part_tiles, seg_tok);
         else
             grid.barrier_wait(std::move(token));
+        jitter(2 * k + 1);
         // exclusive draw offset: the counts of this segment's earlier tiles in
         // this launch, read block-wide (all loads in flight at once)
         const uint32_t seg_base = blockIdx.x - lt;
@@ -867,6 +888,7 @@ __global__ void __launch_bounds__(kMergeThreads, WPT >= 12 ? 2 : (WPT >= 8 ? 3 :
                     if (pc) {
                         const uint64_t wi = n >> 5;
                         const uint32_t sh = uint32_t(n & 31);
+                        if (!MARSIT_BOUNDS_OK(wi + 1 < uint64_t(m.coin_words) + 16, p.err)) break;
                         const uint32_t c0 = __ldg(cw + wi);
                         const uint32_t c1 = (sh + pc > 32) ? __ldg(cw + wi + 1) : 0u;
                         window = __funnelshift_r(c0, c1, sh);
@@ -1090,7 +1112,9 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, uin
                 st_cluster_u64(&s_all[v & 1][i][cr], uint32_t(tid), t);
             }
         }
+        jitter(2 * v);
         cluster_sync_all();
+        jitter(2 * v + 1);
         // pass 2: draw offsets, coins, deposit
 #pragma unroll
         for (int i = 0; i < NL; ++i) {
@@ -1147,6 +1171,8 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, uin
                         diff(k, gl, r[h], d[h]);
                     }
                     fast[h] = cw && n0[h] + popc4(d[h]) <= valid_bits;
+                    if (fast[h] && !MARSIT_BOUNDS_OK((n0[h] >> 5) + 5 <= uint64_t(m.coin_words) + 16, p.err))
+                        fast[h] = live[h] = false;
                     if (fast[h]) {
                         const uint32_t* c = cw + (n0[h] >> 5);
 #pragma unroll

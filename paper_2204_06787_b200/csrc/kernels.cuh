@@ -78,6 +78,7 @@ struct CoopParams {
     const uint32_t* coin_valid;
     uint64_t* coin_end;
     unsigned* seg_bars;           // per-segment barrier counters [seg_cnt x n_lanes] or null (grid barrier)
+    int* err;                     // checked builds: bounds latch (bit 3)
 };
 cudaError_t launch_merge_coop(const CoopParams& p, int wpt, size_t smem, cudaStream_t st);
 cudaError_t merge_coop_occupancy(int wpt, size_t smem, int* blocks_per_sm);
@@ -118,6 +119,7 @@ struct ClusterParams {
     uint64_t* totals;             // [n_merges] draws consumed by each merge
     uint64_t* coin_end;           // [n_merges] stream index after each merge (adaptive coins)
     uint64_t seed, round;
+    int* err;                     // checked builds: bounds latch (bit 3)
 };
 cudaError_t launch_merge_cluster(const ClusterParams& p, int nsub, int nl, uint32_t clusters,
                                  size_t smem, cudaStream_t st);

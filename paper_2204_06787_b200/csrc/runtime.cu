@@ -1495,6 +1495,7 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     }
     CUDA_TRY(cudaMalloc(&ctx->err, sizeof(int)));
     CUDA_TRY(cudaMemset(ctx->err, 0, sizeof(int)));
+    mr.err = ctx->err;
     // marsit_ctx_check's pinned read-back (allocated here: cudaHostAlloc may
     // synchronise the device, which a blocked P2P stream would never allow)
     CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_check, cudaEventDisableTiming));
@@ -1897,6 +1898,7 @@ marsit_status marsit_ctx_check(marsit_ctx* ctx, void* stream) {
     if (flag) {
         CUDA_TRY(cudaMemsetAsync(ctx->err, 0, sizeof(int), st));
         CUDA_TRY(poll_stream(st, ctx->ev_check));
+        if (flag & kErrBounds) return fail(MARSIT_ECUDA, "checked build: a device index failed its bound");
         if (flag & kErrNonFinite) return fail(MARSIT_ENONFINITE, "DenseVector: non-finite entry");
         return fail(MARSIT_EPROTOCOL, "consensus: an aggregate segment differs from its owner's");
     }

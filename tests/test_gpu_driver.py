@@ -142,6 +142,12 @@ def test_params_checkpoint_uses_reference_format():
         assert torch.equal(x, y)
         with pytest.raises(mb.ParameterError):
             mb.read_params_checkpoint(path, torch.empty(1000, dtype=torch.float64, device=DEV))
+        # read_checkpoint rejects a file whose size is not 24 + 8 D (checkpoint.hpp:84)
+        for bad in (blob + b"\0", blob[:-1], blob[:20]):
+            with open(path, "wb") as f:
+                f.write(bad)
+            with pytest.raises(mb.ParameterError):
+                mb.read_params_checkpoint(path, y)
 
 
 @pytest.mark.slow
