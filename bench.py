@@ -550,9 +550,15 @@ def run_ours(args):
     dec_ms_tot, dec_n = phases.get("decode_comp", (float("nan"), 0))
     ext_ms_tot, ext_n = phases.get("sign_extract", (float("nan"), 0))
     dec_unit = 3 * esize + 0.125
+    dec_kernel = "decode_comp (K3+K4)"
+    fused = not dec_n and phases.get("fused_round", (0.0, 0))[1] > 0
+    if fused:  # small rounds run as one launch (extract + merge + decode per cluster)
+        dec_ms_tot, dec_n = phases["fused_round"]
+        dec_unit = 5 * esize + 0.25
+        dec_kernel = "fused_round (K1+K2+K3/K4, one cluster launch; the re-read of g, c hits L2)"
     dec_bytes = ml * D * dec_unit * args.steps   # read g, c; write c'; 1/8 B of bits
     ext_bytes = ml * D * (2 * esize + 0.125) * args.steps  # read g, c; write 1/8 B of bits
-    dec_gbs = dec_bytes / (dec_ms_tot * 1e-3) / 1e9
+    dec_gbs = dec_bytes / (dec_ms_tot * 1e-3) / 1e9 if dec_ms_tot == dec_ms_tot and dec_ms_tot else 0.0
     dec_ms = dec_ms_tot / max(dec_n, 1)
     step_unit = 5 * esize + 0.25
     step_bytes = ml * D * step_unit
@@ -590,7 +596,7 @@ def run_ours(args):
                        "l2": "inputs (%.1f GB) > L2 (126 MB): no flush needed"
                              % (2 * ml * D * esize / 1e9)},
             "worker_gelem_s": M * D / (ms * 1e-3) / 1e9,
-            "roofline": {"bound": "hbm", "kernel": "decode_comp (K3+K4)",
+            "roofline": {"bound": "hbm", "kernel": dec_kernel,
                          "achieved": dec_gbs, "peak": hbm, "unit": "GB/s",
                          "frac": dec_gbs / hbm, "traffic": traffic,
                          "peak_kind": hbm_kind,
@@ -601,7 +607,7 @@ def run_ours(args):
                               "note": f"{step_unit} B per worker-element two-pass floor "
                                       f"(SURVEY §8d), this rank's {ml} workers"},
             "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items() if v[1]},
-            "sign_extract_gbs": ext_bytes / (ext_ms_tot * 1e-3) / 1e9,
+            "sign_extract_gbs": (ext_bytes / (ext_ms_tot * 1e-3) / 1e9) if ext_n else None,
             "gpu_launches": int(launches),
             "clocks": clocks,
             "e2e": {"value": D / (e2e_ms * 1e-3) / 1e9, "unit": "Gelem/s",
