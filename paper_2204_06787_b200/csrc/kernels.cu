@@ -643,7 +643,7 @@ __device__ __forceinline__ void load_words(const uint32_t* p, uint32_t (&v)[WPT]
     }
 }
 
-#ifdef MARSIT_COOP_PROF
+#if defined(MARSIT_COOP_PROF) || defined(MARSIT_FUSED_PROF)
 }  // namespace
 __device__ unsigned long long g_coop_prof[8];
 namespace {
@@ -981,20 +981,27 @@ __device__ __forceinline__ void st_cluster_u64(void* local, uint32_t rank, unsig
 // leaf w at leaf_smem + w * tile_groups; the final node also to agg_smem).
 // cl_slots: [n_slots][tile_groups] node values of this CTA's tile, then
 // (p.stage) [NL][2][tile_groups] the level's r and d staged by pass 1.
+// Static shared state of the cluster merge of one CTA.
+template <int NSUB, int NL>
+struct ClusterMergeShared {
+    uint32_t wt[NL * NSUB][kClusterThreads / 32];    // warp totals per column
+    uint32_t wpre[NL * NSUB][kClusterThreads / 32];  // exclusive warp prefix per column
+    uint32_t ctot[NL * NSUB];                        // CTA total per column
+    unsigned long long all[2][NL][kMaxClusterSize];  // CTA totals of the cluster (DSMEM)
+    DevMerge m[kMaxSegMerges];
+    const uint4* row[kMaxSegMerges][2];              // leaf operand rows (recv, local) or null
+    unsigned long long tot[kMaxSegMerges];           // cluster-wide draws of each merge
+    uint32_t valid[kMaxSegMerges];
+    uint32_t lvl[kMaxSegMerges + 1];
+};
+
+// Prologue: stage the segment's merge descriptors, leaf rows and level table.
+// The caller then needs one cluster barrier (every CTA of the cluster runs
+// before the first remote store; it also publishes the staging to the CTA).
+// The fused kernel stages before its extract and has that barrier after it.
 template <int NSUB, int NL, bool SMEM_LEAVES>
-__device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, uint4* cl_slots,
-                                                     const uint4* leaf_smem, uint4* agg_smem) {
-    constexpr int NCOL = NL * NSUB;
-    constexpr int NW = kClusterThreads / 32;
-    __shared__ uint32_t s_wt[NCOL][NW];    // warp totals per column
-    __shared__ uint32_t s_wpre[NCOL][NW];  // exclusive warp prefix per column
-    __shared__ uint32_t s_ctot[NCOL];      // CTA total per column
-    __shared__ unsigned long long s_all[2][NL][kMaxClusterSize];  // CTA totals of the cluster
-    __shared__ DevMerge s_m[kMaxSegMerges];
-    __shared__ const uint4* s_row[kMaxSegMerges][2];  // leaf operand rows (recv, local) or null
-    __shared__ unsigned long long s_tot[kMaxSegMerges];  // cluster-wide draws of each merge
-    __shared__ uint32_t s_valid[kMaxSegMerges];
-    __shared__ uint32_t s_lvl[kMaxSegMerges + 1];
+__device__ __forceinline__ void cluster_merge_prologue(const ClusterParams& p, ClusterMergeShared<NSUB, NL>& sh,
+                                                       const uint4* leaf_smem) {
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t cr = cluster_ctarank();
@@ -1005,9 +1012,9 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, uin
     const uint32_t g_first = cr * p.tile_groups;
     for (uint32_t i = tid; i < nm; i += kClusterThreads) {
         const DevMerge m = p.merges[mb + i];
-        s_m[i] = m;
-        s_tot[i] = 0;
-        s_valid[i] = p.coin_valid ? p.coin_valid[mb + i] : 0u;
+        sh.m[i] = m;
+        sh.tot[i] = 0;
+        sh.valid[i] = p.coin_valid ? p.coin_valid[mb + i] : 0u;
         // leaf rows resolved once (P2P: the source rank's buffer, over NVLink)
 #pragma unroll
         for (int o = 0; o < 2; ++o) {
@@ -1023,12 +1030,24 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, uin
                                           : p.leaves + (uint64_t((w / p.ml) * p.n_seg + sl) * p.ml + w % p.ml) * p.wst) +
                           g_first;
             }
-            s_row[i][o] = row;
+            sh.row[i][o] = row;
         }
     }
-    for (uint32_t i = tid; i <= nlv; i += kClusterThreads) s_lvl[i] = p.lvl_begin[lb0 + i];
-    // every CTA of the cluster is running before the first remote store
-    cluster_sync_all();
+    for (uint32_t i = tid; i <= nlv; i += kClusterThreads) sh.lvl[i] = p.lvl_begin[lb0 + i];
+}
+
+// The level loop (after cluster_merge_prologue).
+template <int NSUB, int NL, bool SMEM_LEAVES>
+__device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, ClusterMergeShared<NSUB, NL>& sh,
+                                                     uint4* cl_slots, const uint4* leaf_smem, uint4* agg_smem) {
+    constexpr int NCOL = NL * NSUB;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t cr = cluster_ctarank();
+    const uint32_t sl = p.seg_lo + blockIdx.x / p.csize;
+    const uint32_t sg = p.s_first + sl;
+    const uint32_t mb = p.seg_begin[sl];
+    const uint32_t lb0 = p.lvl_start[sl], nlv = p.lvl_start[sl + 1] - lb0 - 1;
+    const uint32_t g_first = cr * p.tile_groups;
 
     const uint32_t total_groups = p.words_proc / 4;
     // groups of this CTA's tile that exist; those entirely below L need no mask
@@ -1037,10 +1056,10 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, uin
     const bool peer = p.peer_bits != nullptr;
     uint4* const stage = cl_slots + size_t(p.n_slots) * p.tile_groups;  // valid when p.stage
     auto load_src = [&](uint32_t k, int o, uint32_t gl) -> uint4 {
-        const uint4* row = s_row[k][o];
+        const uint4* row = sh.row[k][o];
         if (SMEM_LEAVES && row) return row[gl];
         if (row) return peer ? __ldcg(row + gl) : __ldg(row + gl);
-        const uint16_t src = o ? s_m[k].local_src : s_m[k].recv_src;
+        const uint16_t src = o ? sh.m[k].local_src : sh.m[k].recv_src;
         return cl_slots[size_t(src & 0x3FFFu) * p.tile_groups + gl];
     };
     // r (received operand) and d = (r ^ l) & valid of local group gl of merge k
@@ -1062,7 +1081,10 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, uin
     auto popc4 = [](const uint4& d) { return __popc(d.x) + __popc(d.y) + __popc(d.z) + __popc(d.w); };
 
     for (uint32_t v = 0; v < nlv; ++v) {
-        const uint32_t k0 = s_lvl[v], nk = s_lvl[v + 1] - k0;
+#ifdef MARSIT_FUSED_PROF
+        const uint64_t lv_t0 = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0;
+#endif
+        const uint32_t k0 = sh.lvl[v], nk = sh.lvl[v + 1] - k0;
         // pass 1: d, counts and warp scans (r and d staged for pass 2)
         uint32_t ex[NL][NSUB];
 #pragma unroll
@@ -1087,19 +1109,19 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, uin
                     if (lane >= o) incl += y;
                 }
                 ex[i][u] = incl - c;
-                if (lane == 31) s_wt[i * NSUB + u][wid] = incl;
+                if (lane == 31) sh.wt[i * NSUB + u][wid] = incl;
             }
         __syncthreads();
         if (wid < NCOL) {
-            const uint32_t x = s_wt[wid][lane];
+            const uint32_t x = sh.wt[wid][lane];
             uint32_t incl = x;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(kFull, incl, o);
                 if (lane >= o) incl += y;
             }
-            s_wpre[wid][lane] = incl - x;
-            if (lane == 31) s_ctot[wid] = incl;
+            sh.wpre[wid][lane] = incl - x;
+            if (lane == 31) sh.ctot[wid] = incl;
         }
         __syncthreads();
         // this CTA's per-merge totals into every cluster CTA's slot [v & 1][i][cr]
@@ -1108,22 +1130,28 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, uin
             for (int i = 0; i < NL; ++i) {
                 unsigned long long t = 0;
 #pragma unroll
-                for (int u = 0; u < NSUB; ++u) t += s_ctot[i * NSUB + u];
-                st_cluster_u64(&s_all[v & 1][i][cr], uint32_t(tid), t);
+                for (int u = 0; u < NSUB; ++u) t += sh.ctot[i * NSUB + u];
+                st_cluster_u64(&sh.all[v & 1][i][cr], uint32_t(tid), t);
             }
         }
         jitter(2 * v);
+#ifdef MARSIT_FUSED_PROF
+        const uint64_t lv_t1 = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0;
+#endif
         cluster_sync_all();
         jitter(2 * v + 1);
+#ifdef MARSIT_FUSED_PROF
+        const uint64_t lv_t2 = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0;
+#endif
         // pass 2: draw offsets, coins, deposit
 #pragma unroll
         for (int i = 0; i < NL; ++i) {
             if (uint32_t(i) >= nk) continue;
             const uint32_t k = k0 + i;
-            const DevMerge& m = s_m[k];
+            const DevMerge& m = sh.m[k];
             // lower-ranked CTAs' totals (the tile's draw offset) and the
             // cluster total: lane q holds CTA q's total, warp reductions
-            const unsigned long long x = uint32_t(lane) < p.csize ? s_all[v & 1][i][lane] : 0ull;
+            const unsigned long long x = uint32_t(lane) < p.csize ? sh.all[v & 1][i][lane] : 0ull;
             unsigned long long pre = uint32_t(lane) < cr ? x : 0ull, tot = x;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
@@ -1133,16 +1161,16 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, uin
             // stream base: draws before this round's merges + the earlier
             // merges of the same (receiver, segment) stream (continuation)
             uint64_t base = m.base_add;
-            for (int32_t src = m.offset_src; src >= 0; src = s_m[src].offset_src)
-                base += s_tot[src] + s_m[src].base_add;
+            for (int32_t src = m.offset_src; src >= 0; src = sh.m[src].offset_src)
+                base += sh.tot[src] + sh.m[src].base_add;
             if (tid == 0) {
-                s_tot[k] = tot;  // read by later levels (after their block barriers)
+                sh.tot[k] = tot;  // read by later levels (after their block barriers)
                 if (cr == 0) {
                     if (p.totals) p.totals[mb + k] = tot;
                     if (p.coin_end) p.coin_end[mb + k] = base + tot;
                 }
             }
-            const uint64_t valid_bits = uint64_t(s_valid[k]) * 32;
+            const uint64_t valid_bits = uint64_t(sh.valid[k]) * 32;
             const uint32_t* cw = p.coins ? p.coins + m.coin_off : nullptr;
             uint64_t off = base + pre;  // + this CTA's earlier columns of merge i
             // two groups per batch: their operand and coin loads are issued
@@ -1160,8 +1188,8 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, uin
                     live[h] = u < NSUB && gl < n_here;
                     fast[h] = false;
                     if (u < NSUB) {
-                        n0[h] = off + s_wpre[i * NSUB + u][wid] + ex[i][u];
-                        off += s_ctot[i * NSUB + u];
+                        n0[h] = off + sh.wpre[i * NSUB + u][wid] + ex[i][u];
+                        off += sh.ctot[i * NSUB + u];
                     }
                     if (!live[h]) continue;
                     if (p.stage) {
@@ -1226,16 +1254,28 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, uin
             }
         }
         // no block barrier here: slots and the staging are read back by the
-        // threads that wrote them; s_wt / s_wpre / s_ctot are rewritten by
+        // threads that wrote them; sh.wt / sh.wpre / sh.ctot are rewritten by
         // the next level only after its first block barrier, which every
         // thread reaches after finishing this pass
+#ifdef MARSIT_FUSED_PROF
+        if (threadIdx.x == 0 && blockIdx.x == 0) {
+            const uint64_t lv_t3 = gtime_ns();
+            atomicAdd(&g_coop_prof[4], (unsigned long long)(lv_t1 - lv_t0));
+            atomicAdd(&g_coop_prof[5], (unsigned long long)(lv_t2 - lv_t1));
+            atomicAdd(&g_coop_prof[6], (unsigned long long)(lv_t3 - lv_t2));
+            atomicAdd(&g_coop_prof[7], 1ull);
+        }
+#endif
     }
 }
 
 template <int NSUB, int NL>
 __global__ void __launch_bounds__(kClusterThreads, 1) merge_cluster_kernel(const ClusterParams p) {
     extern __shared__ uint4 cl_dyn[];
-    cluster_merge_levels<NSUB, NL, false>(p, cl_dyn, nullptr, nullptr);
+    __shared__ ClusterMergeShared<NSUB, NL> sh;
+    cluster_merge_prologue<NSUB, NL, false>(p, sh, nullptr);
+    cluster_sync_all();
+    cluster_merge_levels<NSUB, NL, false>(p, sh, cl_dyn, nullptr, nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -1254,20 +1294,26 @@ __device__ __forceinline__ bool quad_real(uint64_t j, uint64_t seg_len, uint64_t
 template <typename T, int NSUB, int NL>
 __global__ void __launch_bounds__(kClusterThreads, 1)
     round_cluster_kernel(const ClusterParams p, const FusedParams<T> f) {
+#ifdef MARSIT_FUSED_PROF
+    const uint64_t fp_t0 = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0;
+#endif
     extern __shared__ uint4 fz_dyn[];  // [workers][tg] leaves, [tg] aggregate, then the merge's slots / staging
+    __shared__ ClusterMergeShared<NSUB, NL> sh;
     const uint32_t tg = p.tile_groups;
     uint4* leaf = fz_dyn;
     uint4* aggs = leaf + size_t(f.workers) * tg;
     uint4* slots = aggs + tg;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr uint32_t NWARP = kClusterThreads / 32;
     const uint32_t cr = cluster_ctarank();
     const uint32_t sl = p.seg_lo + blockIdx.x / p.csize;
     const uint32_t g_first = cr * tg;
     const uint32_t total_groups = p.words_proc / 4;
     const uint32_t n_here = total_groups > g_first ? min(tg, total_groups - g_first) : 0u;
     const uint64_t seg0 = uint64_t(sl) * p.seg_bits;  // first coordinate of the segment (G == 1)
+    // the merge's descriptors, loaded under the extract's streaming
+    cluster_merge_prologue<NSUB, NL, true>(p, sh, leaf);
     constexpr int B = 2;  // groups per warp step: 2B quad loads in flight per lane
-    constexpr uint32_t NWARP = kClusterThreads / 32;
     // K1: u = g + c, sign nibbles -> packed words in shared memory
     T fin = T(0);
     for (uint32_t w = 0; w < f.workers; ++w) {
@@ -1315,10 +1361,16 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
         }
     }
     if (__any_sync(kFull, !(fin == fin)) && lane == 0) atomicOr(f.err, 1);
-    __syncthreads();
+    cluster_sync_all();  // the tiles' leaves and the staged descriptors complete; cluster running
     // K2: the segment's merge DAG (cluster-wide draw offsets via DSMEM)
-    cluster_merge_levels<NSUB, NL, true>(p, slots, leaf, aggs);
+#ifdef MARSIT_FUSED_PROF
+    const uint64_t fp_t1 = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0;
+#endif
+    cluster_merge_levels<NSUB, NL, true>(p, sh, slots, leaf, aggs);
     __syncthreads();
+#ifdef MARSIT_FUSED_PROF
+    const uint64_t fp_t2 = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0;
+#endif
     // K3/K4: g_t = +-eta from the aggregate, c' = (g + c) - g_t
     for (uint32_t w = 0; w < f.workers; ++w) {
         const T* __restrict__ gw = f.g[w];
@@ -1367,6 +1419,15 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
             }
         }
     }
+#ifdef MARSIT_FUSED_PROF
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const uint64_t fp_t3 = gtime_ns();
+        atomicAdd(&g_coop_prof[0], (unsigned long long)(fp_t1 - fp_t0));
+        atomicAdd(&g_coop_prof[1], (unsigned long long)(fp_t2 - fp_t1));
+        atomicAdd(&g_coop_prof[2], (unsigned long long)(fp_t3 - fp_t2));
+        atomicAdd(&g_coop_prof[3], 1ull);
+    }
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -1996,8 +2057,12 @@ static cudaError_t fused_attr() {
     auto k = round_cluster_kernel<T, NSUB, NL>;
     static cudaError_t e = [&] {
         cudaError_t r = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncAttributes fa{};
+        if (r == cudaSuccess) r = cudaFuncGetAttributes(&fa, k);
+        // the opt-in maximum per CTA (227 KB on sm_100) less the static shared memory
         if (r == cudaSuccess)
-            r = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            r = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(232448 - fa.sharedSizeBytes));
         return r;
     }();
     return e;
@@ -2349,7 +2414,7 @@ MARSIT_INSTANTIATE(double)
 
 }  // namespace marsit_b200
 
-#ifdef MARSIT_COOP_PROF
+#if defined(MARSIT_COOP_PROF) || defined(MARSIT_FUSED_PROF)
 extern "C" void marsit_debug_coop_prof(unsigned long long* out, int reset) {
     cudaMemcpyFromSymbol(out, marsit_b200::g_coop_prof, sizeof(marsit_b200::g_coop_prof));
     if (reset) {

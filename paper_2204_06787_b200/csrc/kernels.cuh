@@ -131,6 +131,7 @@ cudaError_t launch_merge_cluster(const ClusterParams& p, int nsub, int nl, uint3
 // these sizes).  Needs every worker local, M <= kFusedMaxWorkers, 16-byte
 // aligned quads (L % 4 == 0).
 constexpr uint32_t kFusedMaxWorkers = 16;
+
 template <typename T>
 struct FusedParams {
     const T* g[kFusedMaxWorkers];
