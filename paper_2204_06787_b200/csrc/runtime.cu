@@ -25,6 +25,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.hpp"
 
 using namespace marsit_b200;
@@ -39,6 +41,22 @@ marsit_status fail(marsit_status st, const std::string& msg) {
     g_last_error = msg;
     return st;
 }
+
+// NVTX ranges around the host enqueue of each phase (MARSIT_NVTX=1; for
+// profilers' range filters, e.g. ncu --nvtx --nvtx-include "marsit.merge/").
+struct NvtxRange {
+    bool on;
+    explicit NvtxRange(const char* name) : on(nvtx_enabled()) {
+        if (on) nvtxRangePushA(name);
+    }
+    ~NvtxRange() {
+        if (on) nvtxRangePop();
+    }
+    static bool nvtx_enabled() {
+        static const bool e = env_int("MARSIT_NVTX", 0) != 0;
+        return e;
+    }
+};
 
 marsit_status ctx_failed(const marsit_ctx* ctx) {
     const int st = ctx->fail_status.load();
@@ -819,6 +837,7 @@ marsit_status check_consensus(const marsit_ctx* ctx, bool need_full_count) {
 template <typename T>
 marsit_status dense_phase(marsit_ctx* ctx, int phase, const void* const* g, const void* const* c,
                           void* const* c_out, void* const* params, void* mean, cudaStream_t st) {
+    NvtxRange range(phase == 0 ? "marsit.dense.leaf" : phase == 1 ? "marsit.dense.sum" : "marsit.dense.out");
     cudaEvent_t ev;
     marsit_status s = ctx->begin_phase(st, &ev);
     if (s) return s;
@@ -1085,6 +1104,7 @@ marsit_status sign_phase(marsit_ctx* ctx, int phase, uint64_t t, double eta_s, u
                          void* const* d_comp_out, void* const* params, uint64_t* d_agg_bits,
                          void* d_update, cudaStream_t st) {
     marsit_status s = MARSIT_OK;
+    NvtxRange range(phase == 0 ? "marsit.extract" : phase == 1 ? "marsit.merge" : "marsit.decode");
     if (phase == 0) {
         ctx->task_dir = ctx->l2_reuse ? uint32_t(t & 1) : 0;
         if ((s = run_coins(ctx, seed, t, st))) return s;
@@ -1141,6 +1161,7 @@ marsit_status fused_round(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_t se
                           const void* const* g, const void* const* c, void* const* c_out,
                           uint64_t* d_agg_bits, void* d_update, cudaStream_t st) {
     marsit_status s;
+    NvtxRange range("marsit.fused_round");
     if ((s = run_coins(ctx, seed, t, st))) return s;
     if (ctx->coins_pending) {
         CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_coin_done[ctx->cur_coin], 0));
