@@ -359,6 +359,27 @@ class Comm:
             self.dist.destroy_process_group()
 
 
+def warm_up(comm, step, sync, warmup: int, min_busy_s: float) -> int:
+    """Untimed rounds 1..n: at least max(W, 3) and at least min_busy_s of GPU
+    work (clock sampling).  Rank 0 decides after every chunk whether to go on
+    and broadcasts it, so every rank runs the same number of rounds — the
+    lock-step delivery of transport.hpp:27-35 (P2P flag waits and NCCL
+    collectives pair round by round; a rank that ran ahead would wait for
+    flags its peers never write).  Returns n."""
+    n = 0
+    t0 = time.time()
+    chunk = max(warmup, 3)
+    while True:
+        for _ in range(chunk):
+            n += 1
+            step(n)
+        sync()
+        more = int(time.time() - t0 < min_busy_s) if comm.rank == 0 else 0
+        if not comm.bcast(more):
+            return n
+        chunk = 20
+
+
 def _digest(t) -> str:
     import hashlib
     return hashlib.blake2b(t.contiguous().view(-1).cpu().numpy().tobytes(), digest_size=16).hexdigest()
@@ -404,24 +425,8 @@ def run_ours(args):
 
     sampler = ClockSampler(dev_index)
     sampler.start()
-    # warm-up: at least max(W, 3) steps and at least --min-busy-s of GPU work
-    # (clock sampling); rank 0 decides and every rank runs the same number of
-    # rounds (the lock-step delivery of transport.hpp:27-35: the P2P flag
-    # waits and NCCL collectives pair round by round)
-    t = 1
-    n_warm = 0
-    t_busy0 = time.time()
-    chunk = max(args.warmup, 3)
-    while True:
-        for _ in range(chunk):
-            step(t)
-            t += 1
-            n_warm += 1
-        torch.cuda.synchronize(dev)
-        more = int(time.time() - t_busy0 < args.min_busy_s) if rank == 0 else 0
-        if not comm.bcast(more):
-            break
-        chunk = 20
+    n_warm = warm_up(comm, step, lambda: torch.cuda.synchronize(dev), args.warmup, args.min_busy_s)
+    t = 1 + n_warm
     ctx.check()
     comm.barrier()
     torch.cuda.synchronize(dev)
