@@ -125,7 +125,11 @@ marsit_status Watchdog::watch(cudaStream_t s, uint64_t epoch) {
         }
     }
     if (!ev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventRecord(ev, s));
+    if (cudaEventRecord(ev, s) != cudaSuccess) {
+        std::lock_guard<std::mutex> lock(mu);
+        free_events.push_back(ev);
+        return fail(MARSIT_ECUDA, std::string("watchdog event: ") + cudaGetErrorString(cudaGetLastError()));
+    }
     {
         std::lock_guard<std::mutex> lock(mu);
         pending.push_back({ev, std::chrono::steady_clock::now(), epoch});
@@ -1901,7 +1905,12 @@ marsit_status marsit_ctx_check(marsit_ctx* ctx, void* stream) {
     if (read_flags)
         CUDA_TRY(cudaMemcpyAsync(ctx->h_check + 1, ctx->flags, 2 * sizeof(uint64_t) * ctx->G,
                                  cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(poll_stream(st, ctx->ev_check));
+    if (ctx->watchdog) {
+        CUDA_TRY(poll_stream(st, ctx->ev_check));
+    } else {  // nothing has to release this stream: a blocking wait is fine
+        CUDA_TRY(cudaEventRecord(ctx->ev_check, st));
+        CUDA_TRY(cudaEventSynchronize(ctx->ev_check));
+    }
     const int flag = *reinterpret_cast<const int*>(ctx->h_check);
     CUDA_TRY(cudaGetLastError());
     marsit_status s;
