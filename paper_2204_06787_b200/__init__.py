@@ -401,15 +401,21 @@ class Context:
         return list(counts)
 
 
-_CTX_CACHE = {}
+_TLS = __import__("threading").local()
 
 
 def _context_for(dim, sched, dtype, device) -> Context:
+    """One cached context per (thread, D, schedule, dtype, device): a context's
+    device scratch serves one round at a time, and ctypes releases the GIL
+    during the calls, so threads never share one (like the C++ drop-in)."""
+    cache = getattr(_TLS, "ctx_cache", None)
+    if cache is None:
+        cache = _TLS.ctx_cache = {}
     key = (dim, id(sched), dtype, device)
-    ctx = _CTX_CACHE.get(key)
+    ctx = cache.get(key)
     if ctx is None or ctx.schedule is not sched:
         ctx = Context(dim, sched, dtype, device)
-        _CTX_CACHE[key] = ctx
+        cache[key] = ctx
     return ctx
 
 
