@@ -287,6 +287,11 @@ marsit_status marsit_driver_load(marsit_driver* drv, const char* path, void* str
     CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
     std::ifstream f(path, std::ios::binary);
     if (!f) return fail(MARSIT_EPARAM, std::string("cannot open ") + path);
+    f.seekg(0, std::ios::end);
+    const std::streamoff size = f.tellg();
+    f.seekg(0, std::ios::beg);
+    if (uint64_t(size) != sizeof(StateHeader) + uint64_t(drv->ml) * drv->D * drv->esize)
+        return fail(MARSIT_EPARAM, "sync state file size does not match this driver");
     StateHeader h{};
     f.read(reinterpret_cast<char*>(&h), sizeof(h));
     if (!f || std::memcmp(h.magic, kStateMagic, sizeof(h.magic)) != 0)

@@ -124,6 +124,13 @@ def test_driver_checkpoint_resume_is_bit_identical():
         c = mb.Driver(D, sched, **{**kw, "global_seed": 8})
         with pytest.raises(mb.ParameterError):
             c.load(path)
+        # so is a truncated file or one with trailing bytes
+        blob = open(path, "rb").read()
+        for bad in (blob[:-4], blob + b"\0"):
+            with open(path, "wb") as f:
+                f.write(bad)
+            with pytest.raises(mb.ParameterError):
+                b.load(path)
 
 
 def test_params_checkpoint_uses_reference_format():
