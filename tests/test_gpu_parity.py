@@ -556,3 +556,43 @@ def test_fused_small_round_vs_oracle(dtype, topo, a, b, D, monkeypatch):
     esize = 4 if dtype == torch.float32 else 8
     if W <= 16 and W * D * esize * 2 <= 96 << 20:
         assert ctx.timing()["fused_round"][1] > 0  # the fused kernel ran
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_fused_round_zeros_negzero_subnormals_vs_oracle(dtype):
+    """The fused small round (L % 4 == 0: D = 10,000, M = 5) on exact zeros,
+    -0.0 + -0.0 (packs to 1, sign_vector.hpp:70), fp32 subnormals and their
+    negatives: aggregate, g_t and compensation exactly the oracle's."""
+    rng = np.random.default_rng(5)
+    W, D, seed = 5, 10_000, 17
+    sched = mb.build_ring_schedule(W)
+    T = O.schedule("ring", W)
+    g = rng.standard_normal((W, D)).astype(np.float32) * np.float32(1e-3)
+    c = rng.standard_normal((W, D)).astype(np.float32) * np.float32(1e-3)
+    g[:, ::5] = 0.0
+    g[:, 1::5] = -0.0
+    c[:, ::5] = 0.0
+    c[:, 1::5] = -0.0
+    g[:, 2::5] = np.float32(1e-45)
+    c[:, 2::5] = 0.0
+    g[:, 3::5] = np.float32(-1e-45)
+    c[:, 3::5] = 0.0
+    g64, c64 = g.astype(np.float64), c.astype(np.float64)
+    ctx = mb.Context(D, sched, dtype, 0)
+    ctx.set_timing(True)
+    comp = [torch.tensor(x, dtype=dtype, device=DEV) for x in c64]
+    agg = torch.empty((D + 63) // 64, dtype=torch.int64, device=DEV)
+    upd = torch.empty(D, dtype=dtype, device=DEV)
+    ctx.sign_round(1, ETA, seed, [torch.tensor(x, dtype=dtype, device=DEV) for x in g64], comp,
+                   agg_bits=agg, update=upd)
+    ctx.check()
+    r = O.marsit_round(T, 1, None, ETA, g64, c64, seed)
+    assert u64(agg).tolist() == r.agg_bits.tolist()
+    assert np.array_equal(upd.double().cpu().numpy(), r.update)
+    got = np.stack([x.double().cpu().numpy() for x in comp])
+    if dtype == torch.float64:
+        assert np.array_equal(got, r.comp)
+    else:  # fp32 arithmetic: 1e-6 relative to the operands of c' = (g + c) - g_t
+        bound = 1e-6 * (np.abs(r.comp) + np.abs(g64) + np.abs(c64) + ETA)
+        assert np.all(np.abs(got - r.comp) <= bound)
+    assert ctx.timing()["fused_round"][1] == 1
