@@ -1109,12 +1109,17 @@ marsit_status sign_phase(marsit_ctx* ctx, int phase, uint64_t t, double eta_s, u
                          void* d_update, cudaStream_t st) {
     marsit_status s = MARSIT_OK;
     NvtxRange range(phase == 0 ? "marsit.extract" : phase == 1 ? "marsit.merge" : "marsit.decode");
+    // where the next round's coins run: underneath the decode by default;
+    // underneath the extract when the metrics decode runs (its 3 CTAs/SM fill
+    // the register file, so coins queued behind it would land on the next
+    // round's extract instead: C3 metrics round 809 -> see DESIGN §11)
+    const bool coins_at_extract = ctx->coin_prefetch_at_extract || (ctx->metrics && ctx->ml == ctx->M);
     if (phase == 0) {
         ctx->task_dir = ctx->l2_reuse ? uint32_t(t & 1) : 0;
         if ((s = run_coins(ctx, seed, t, st))) return s;
         // MARSIT_COIN_PREFETCH_AT=1: the next round's coins run underneath
         // this extract instead of this round's decode
-        if (ctx->coin_prefetch_at_extract && (s = prefetch_coins(ctx, seed, t, st))) return s;
+        if (coins_at_extract && (s = prefetch_coins(ctx, seed, t, st))) return s;
         if ((s = run_extract(ctx, d_grads, d_comp, st))) return s;
         // the epoch advances only once this rank's phase-0 work is enqueued:
         // a failed launch above leaves the peers' view consistent
@@ -1125,7 +1130,7 @@ marsit_status sign_phase(marsit_ctx* ctx, int phase, uint64_t t, double eta_s, u
         if ((s = p2p_wait(ctx, 0, st))) return s;  // every rank's packed signs
         if ((s = run_merge(ctx, seed, t, st))) return s;
         if ((s = consensus_own(ctx, st))) return s;
-        if (!ctx->coin_prefetch_at_extract && (s = prefetch_coins(ctx, seed, t, st))) return s;
+        if (!coins_at_extract && (s = prefetch_coins(ctx, seed, t, st))) return s;
         return p2p_signal(ctx, 1, st);  // my owned aggregates are ready
     }
     if ((s = p2p_wait(ctx, 1, st))) return s;  // every owner's aggregates

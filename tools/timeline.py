@@ -22,6 +22,8 @@ args = ap.parse_args()
 D, M = args.dim, args.workers
 sched = mb.build_ring_schedule(M)
 ctx = mb.Context(D, sched, torch.float32, 0)
+if os.environ.get("TL_METRICS"):
+    ctx.set_metrics(True)
 g = [torch.empty(D, device="cuda") for _ in range(M)]
 for w in range(M):
     mb.fill_recipe(g[w], 0, 2026, w, 1)
