@@ -121,8 +121,16 @@ struct MergeRunner {
     // faster on B200 for every measured configuration
     bool cluster = [] {
         const char* e = std::getenv("MARSIT_MERGE_KERNEL");
-        return e && std::strcmp(e, "cluster") == 0;
+        return e && (std::strcmp(e, "cluster") == 0 || std::strcmp(e, "grid") == 0);
     }();
+    // MARSIT_MERGE_KERNEL=grid: the same level loop over any number of
+    // co-resident 1024-thread CTAs per segment (cooperative launch, global
+    // totals + per-segment barrier; K2g); uses the cluster plan
+    bool grid = [] {
+        const char* e = std::getenv("MARSIT_MERGE_KERNEL");
+        return e && std::strcmp(e, "grid") == 0;
+    }();
+    unsigned long long* xch = nullptr;  // grid mode: [2][seg_per_launch][csize][level_width]
     uint32_t csize = 16, tile_groups = 0, nsub = 1, stage = 0;
     size_t merge_smem = 0;  // merge_cluster_kernel's dynamic shared memory (smem minus the fused ring)
     // fused small rounds (round_cluster_kernel): extra shared memory per CTA
@@ -138,7 +146,7 @@ struct MergeRunner {
     ~MergeRunner() {
         for (void* p : {(void*)d_merges, (void*)d_seg_begin, (void*)d_stage_begin, (void*)gnodes,
                         (void*)flags, (void*)part_totals, (void*)coin_end, (void*)seg_bars,
-                        (void*)d_lvl_start, (void*)d_lvl_begin})
+                        (void*)d_lvl_start, (void*)d_lvl_begin, (void*)xch})
             if (p) cudaFree(p);
     }
 
@@ -149,6 +157,8 @@ struct MergeRunner {
     // launches (one GPU, many segments: the tiles no longer fit one
     // co-resident grid) the stages run as single lanes instead.
     marsit_status configure(int sm_count, uint32_t seg_launch = 0, int cta_limit = 0) {
+        if (grid && !fused_arrays) return configure_grid(sm_count, seg_launch ? seg_launch : n_seg);
+        grid = false;
         if (cluster) return configure_cluster(seg_launch ? seg_launch : n_seg);
         marsit_status s = configure_once(sm_count, seg_launch, cta_limit);
         if (s || lanes_max == 1 || n_parts == 1) return s;
@@ -218,6 +228,44 @@ struct MergeRunner {
             }
         }
         if (best == ~0ull) return fail(MARSIT_EUNSUPPORTED, "merge clusters do not fit the device");
+        return MARSIT_OK;
+    }
+
+    // Grid mode: every SM hosts one 1024-thread CTA; the segments of a
+    // launch share the SMs evenly (csize tiles each); the smallest groups per
+    // thread that cover a tile; r / d staging when the shared memory allows.
+    marsit_status configure_grid(int sm_count, uint32_t seg_launch) {
+        n_parts = 1;
+        const uint32_t nl = dp.level_width;
+        const uint32_t total_groups = words_proc / 4;
+        int occ = 0;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            seg_per_launch = std::min<uint32_t>(seg_launch, uint32_t(sm_count) * std::max(occ, 1));
+            const uint32_t cs = std::max<uint32_t>(1, uint32_t(sm_count) * std::max(occ, 1) / seg_per_launch);
+            const uint32_t forced = uint32_t(env_int("MARSIT_MERGE_CSIZE", 0));
+            csize = forced ? forced : cs;
+            tile_groups = uint32_t(ceil_div(total_groups, csize));
+            nsub = 0;
+            for (uint32_t c : {1u, 2u, 4u, 8u, 16u})
+                if (uint64_t(c) * kClusterThreads >= tile_groups && (nl == 1 || c <= 8)) {
+                    nsub = c;
+                    break;
+                }
+            if (!nsub) return fail(MARSIT_EUNSUPPORTED, "merge tiles too large for the grid merge");
+            const size_t base_sm = size_t(dp.max_slots) * tile_groups * 16;
+            const size_t stage_sm = size_t(2) * nl * tile_groups * 16;
+            stage = base_sm + stage_sm <= 200 * 1024 && env_int("MARSIT_MERGE_STAGE", 1) ? 1u : 0u;
+            smem = merge_smem = std::max<size_t>(base_sm + (stage ? stage_sm : 0), 16);
+            if (smem > 200 * 1024) return fail(MARSIT_EUNSUPPORTED, "merge tiles do not fit shared memory");
+            CUDA_TRY(merge_grid_occupancy(int(nsub), int(nl), smem, &occ));
+            if (occ <= 0) return fail(MARSIT_EUNSUPPORTED, "grid merge does not fit an SM");
+            if (uint64_t(seg_per_launch) * csize <= uint64_t(occ) * sm_count) break;
+        }
+        if (uint64_t(seg_per_launch) * csize > uint64_t(occ) * sm_count)
+            return fail(MARSIT_EUNSUPPORTED, "grid merge CTAs are not co-resident");
+        if (env_int("MARSIT_MERGE_DEBUG", 0))
+            fprintf(stderr, "merge grid: %u segments x %u CTAs, groups/CTA %u nsub %u stage %u\n",
+                    seg_per_launch, csize, tile_groups, nsub, stage);
         return MARSIT_OK;
     }
 
@@ -308,6 +356,12 @@ struct MergeRunner {
             CUDA_TRY(cudaMemset(part_totals, 0, sizeof(uint64_t) * nm));
             CUDA_TRY(cudaMalloc(&coin_end, sizeof(uint64_t) * nm));
             CUDA_TRY(cudaMemset(coin_end, 0xFF, sizeof(uint64_t) * nm));  // no history yet
+            if (grid) {
+                const size_t nx = size_t(2) * seg_per_launch * csize * dp.level_width;
+                CUDA_TRY(cudaMalloc(&xch, sizeof(unsigned long long) * nx));
+                CUDA_TRY(cudaMalloc(&seg_bars, sizeof(unsigned) * seg_per_launch));
+                CUDA_TRY(cudaMemset(seg_bars, 0, sizeof(unsigned) * seg_per_launch));
+            }
             return MARSIT_OK;
         }
         CUDA_TRY(cudaMalloc(&d_seg_begin, sizeof(uint32_t) * dp.seg_begin.size()));
@@ -362,6 +416,8 @@ struct MergeRunner {
         c.seed = seed;
         c.round = round;
         c.err = err;
+        c.xch = xch;
+        c.seg_bars = seg_bars;
         return c;
     }
 
@@ -372,8 +428,17 @@ struct MergeRunner {
                       uint32_t seg_cnt = ~0u, const uint32_t* coin_valid = nullptr) {
         if (seg_cnt == ~0u) seg_cnt = n_seg - seg_lo;
         if (cluster) {
-            const ClusterParams c = cluster_params(leaves, agg, coins, seed, round, seg_lo, coin_valid);
             if (seg_cnt == 0) return MARSIT_OK;
+            if (grid) {  // launches of at most seg_per_launch co-resident segments
+                for (uint32_t s0 = seg_lo; s0 < seg_lo + seg_cnt; s0 += seg_per_launch) {
+                    const ClusterParams c = cluster_params(leaves, agg, coins, seed, round, s0, coin_valid);
+                    CUDA_TRY(launch_merge_grid(c, int(nsub), int(dp.level_width),
+                                               std::min(seg_per_launch, seg_lo + seg_cnt - s0), smem, st));
+                    ++*n_launch;
+                }
+                return MARSIT_OK;
+            }
+            const ClusterParams c = cluster_params(leaves, agg, coins, seed, round, seg_lo, coin_valid);
             CUDA_TRY(launch_merge_cluster(c, int(nsub), int(dp.level_width), seg_cnt, merge_smem, st));
             ++*n_launch;
             return MARSIT_OK;

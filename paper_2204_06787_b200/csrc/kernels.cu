@@ -999,12 +999,12 @@ struct ClusterMergeShared {
 // The caller then needs one cluster barrier (every CTA of the cluster runs
 // before the first remote store; it also publishes the staging to the CTA).
 // The fused kernel stages before its extract and has that barrier after it.
-template <int NSUB, int NL, bool SMEM_LEAVES>
+template <int NSUB, int NL, bool SMEM_LEAVES, bool GRID = false>
 __device__ __forceinline__ void cluster_merge_prologue(const ClusterParams& p, ClusterMergeShared<NSUB, NL>& sh,
                                                        const uint4* leaf_smem) {
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t cr = cluster_ctarank();
+    const uint32_t cr = GRID ? blockIdx.x % p.csize : cluster_ctarank();
     const uint32_t sl = p.seg_lo + blockIdx.x / p.csize;
     const uint32_t sg = p.s_first + sl;
     const uint32_t mb = p.seg_begin[sl], nm = p.seg_begin[sl + 1] - mb;
@@ -1037,12 +1037,13 @@ __device__ __forceinline__ void cluster_merge_prologue(const ClusterParams& p, C
 }
 
 // The level loop (after cluster_merge_prologue).
-template <int NSUB, int NL, bool SMEM_LEAVES>
+template <int NSUB, int NL, bool SMEM_LEAVES, bool GRID = false>
 __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, ClusterMergeShared<NSUB, NL>& sh,
                                                      uint4* cl_slots, const uint4* leaf_smem, uint4* agg_smem) {
     constexpr int NCOL = NL * NSUB;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t cr = cluster_ctarank();
+    const uint32_t cr = GRID ? blockIdx.x % p.csize : cluster_ctarank();
+    const uint32_t seg_in_launch = blockIdx.x / p.csize;
     const uint32_t sl = p.seg_lo + blockIdx.x / p.csize;
     const uint32_t sg = p.s_first + sl;
     const uint32_t mb = p.seg_begin[sl];
@@ -1124,8 +1125,18 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
             if (lane == 31) sh.ctot[wid] = incl;
         }
         __syncthreads();
-        // this CTA's per-merge totals into every cluster CTA's slot [v & 1][i][cr]
-        if (uint32_t(tid) < p.csize) {
+        // this CTA's per-merge totals: cluster mode into every cluster CTA's
+        // slot [v & 1][i][cr] (DSMEM); grid mode into global memory
+        unsigned long long* const xch =
+            GRID ? p.xch + (size_t(v & 1) * (gridDim.x / p.csize) + seg_in_launch) * p.csize * NL : nullptr;
+        if (GRID) {
+            if (tid < NL) {
+                unsigned long long t = 0;
+#pragma unroll
+                for (int u = 0; u < NSUB; ++u) t += sh.ctot[tid * NSUB + u];
+                __stcg(xch + size_t(cr) * NL + tid, t);
+            }
+        } else if (uint32_t(tid) < p.csize) {
 #pragma unroll
             for (int i = 0; i < NL; ++i) {
                 unsigned long long t = 0;
@@ -1138,7 +1149,12 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
 #ifdef MARSIT_FUSED_PROF
         const uint64_t lv_t1 = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0;
 #endif
-        cluster_sync_all();
+        if (GRID) {  // one barrier over the segment's CTAs (release / acquire)
+            const unsigned tok = seg_barrier_arrive(p.seg_bars + seg_in_launch, cr == 0, p.csize);
+            seg_barrier_wait(p.seg_bars + seg_in_launch, tok);
+        } else {
+            cluster_sync_all();
+        }
         jitter(2 * v + 1);
 #ifdef MARSIT_FUSED_PROF
         const uint64_t lv_t2 = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0;
@@ -1151,8 +1167,18 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
             const DevMerge& m = sh.m[k];
             // lower-ranked CTAs' totals (the tile's draw offset) and the
             // cluster total: lane q holds CTA q's total, warp reductions
-            const unsigned long long x = uint32_t(lane) < p.csize ? sh.all[v & 1][i][lane] : 0ull;
-            unsigned long long pre = uint32_t(lane) < cr ? x : 0ull, tot = x;
+            unsigned long long pre = 0, tot = 0;
+            if (GRID) {
+                for (uint32_t q = lane; q < p.csize; q += 32) {
+                    const unsigned long long x = __ldcg(xch + size_t(q) * NL + i);
+                    pre += q < cr ? x : 0ull;
+                    tot += x;
+                }
+            } else {
+                const unsigned long long x = uint32_t(lane) < p.csize ? sh.all[v & 1][i][lane] : 0ull;
+                pre = uint32_t(lane) < cr ? x : 0ull;
+                tot = x;
+            }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 pre += __shfl_xor_sync(kFull, pre, o);
@@ -1276,6 +1302,18 @@ __global__ void __launch_bounds__(kClusterThreads, 1) merge_cluster_kernel(const
     cluster_merge_prologue<NSUB, NL, false>(p, sh, nullptr);
     cluster_sync_all();
     cluster_merge_levels<NSUB, NL, false>(p, sh, cl_dyn, nullptr, nullptr);
+}
+
+// K2g: the level loop over csize co-resident CTAs per segment, cross-CTA
+// totals through global memory and one release/acquire barrier per segment
+// and level (cooperative launch).
+template <int NSUB, int NL>
+__global__ void __launch_bounds__(kClusterThreads, 1) merge_grid_kernel(const ClusterParams p) {
+    extern __shared__ uint4 gr_dyn[];
+    __shared__ ClusterMergeShared<NSUB, NL> sh;
+    cluster_merge_prologue<NSUB, NL, false, true>(p, sh, nullptr);
+    __syncthreads();
+    cluster_merge_levels<NSUB, NL, false, true>(p, sh, gr_dyn, nullptr, nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -2128,6 +2166,47 @@ cudaError_t round_cluster_occupancy(int nsub, int nl, uint32_t csize, size_t sme
     MARSIT_FUSED_DISPATCH(fused_occ_t, csize, smem, clusters)
 }
 
+template <int NSUB, int NL>
+static cudaError_t grid_attr() {
+    static cudaError_t e = cudaFuncSetAttribute(merge_grid_kernel<NSUB, NL>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    return e;
+}
+
+template <int NSUB, int NL>
+static cudaError_t grid_launch_t(const ClusterParams& p, uint32_t segments, size_t smem, cudaStream_t st) {
+    cudaError_t e = grid_attr<NSUB, NL>();
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(segments * p.csize);
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, merge_grid_kernel<NSUB, NL>, p);
+}
+
+template <int NSUB, int NL>
+static cudaError_t grid_occ_t(size_t smem, int* blocks) {
+    cudaError_t e = grid_attr<NSUB, NL>();
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_grid_kernel<NSUB, NL>, kClusterThreads,
+                                                         smem);
+}
+
+cudaError_t launch_merge_grid(const ClusterParams& p, int nsub, int nl, uint32_t segments, size_t smem,
+                              cudaStream_t st) {
+    MARSIT_CLUSTER_DISPATCH(grid_launch_t, p, segments, smem, st)
+}
+
+cudaError_t merge_grid_occupancy(int nsub, int nl, size_t smem, int* blocks) {
+    MARSIT_CLUSTER_DISPATCH(grid_occ_t, smem, blocks)
+}
+
 cudaError_t launch_merge_cluster(const ClusterParams& p, int nsub, int nl, uint32_t clusters,
                                  size_t smem, cudaStream_t st) {
     MARSIT_CLUSTER_DISPATCH(cluster_launch_t, p, clusters, smem, st)
@@ -2333,6 +2412,15 @@ cudaError_t preload_kernels() {
             reinterpret_cast<const void*>(merge_coop_kernel<8>),
             reinterpret_cast<const void*>(merge_coop_kernel<12>),
             reinterpret_cast<const void*>(merge_coop_kernel<16>),
+            reinterpret_cast<const void*>(merge_grid_kernel<1, 1>),
+            reinterpret_cast<const void*>(merge_grid_kernel<2, 1>),
+            reinterpret_cast<const void*>(merge_grid_kernel<4, 1>),
+            reinterpret_cast<const void*>(merge_grid_kernel<8, 1>),
+            reinterpret_cast<const void*>(merge_grid_kernel<16, 1>),
+            reinterpret_cast<const void*>(merge_grid_kernel<1, 2>),
+            reinterpret_cast<const void*>(merge_grid_kernel<2, 2>),
+            reinterpret_cast<const void*>(merge_grid_kernel<4, 2>),
+            reinterpret_cast<const void*>(merge_grid_kernel<8, 2>),
             reinterpret_cast<const void*>(merge_cluster_kernel<1, 1>),
             reinterpret_cast<const void*>(merge_cluster_kernel<2, 1>),
             reinterpret_cast<const void*>(merge_cluster_kernel<4, 1>),

@@ -120,6 +120,12 @@ struct ClusterParams {
     uint64_t* coin_end;           // [n_merges] stream index after each merge (adaptive coins)
     uint64_t seed, round;
     int* err;                     // checked builds: bounds latch (bit 3)
+    // grid mode (merge_grid_kernel): csize = CTAs ("tiles") per segment, any
+    // number; the per-merge CTA totals go through global memory, xch
+    // [2][segments of the launch][csize][NL], and one barrier per segment and
+    // level (seg_bars[segment of the launch]) replaces the cluster barrier
+    unsigned long long* xch;
+    unsigned* seg_bars;
 };
 cudaError_t launch_merge_cluster(const ClusterParams& p, int nsub, int nl, uint32_t clusters,
                                  size_t smem, cudaStream_t st);
@@ -150,6 +156,11 @@ template <typename T>
 cudaError_t round_cluster_occupancy(int nsub, int nl, uint32_t csize, size_t smem, int* clusters);
 // Concurrently resident clusters of csize CTAs with `smem` dynamic bytes (0 if unsupported).
 cudaError_t merge_cluster_occupancy(int nsub, int nl, uint32_t csize, size_t smem, int* clusters);
+// K2g: the same level loop over csize co-resident CTAs per segment (any
+// number, cooperative launch of `segments` x csize CTAs of kClusterThreads).
+cudaError_t launch_merge_grid(const ClusterParams& p, int nsub, int nl, uint32_t segments, size_t smem,
+                              cudaStream_t st);
+cudaError_t merge_grid_occupancy(int nsub, int nl, size_t smem, int* blocks_per_sm);
 
 template <typename T>
 struct StreamParams {

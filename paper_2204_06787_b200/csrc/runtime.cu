@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <functional>
+#include <tuple>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1503,6 +1504,38 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
             st = mr.configure(ctx->sm_count);
         }
         if (st) return st;
+        // Segments too large for one co-resident cooperative grid (the
+        // cooperative merge would run as several launch parts, each paying
+        // the whole barrier chain: C2, C4, C5 buckets on one GPU) take the
+        // grid merge K2g: one launch, every stage, shared-memory tiles on
+        // all SMs (C4 157 -> 101 us, C2 129 -> 100 us; it loses where the
+        // cooperative merge fits one part: C3 51 vs 60 us, a G = 8 rank 31 vs
+        // 61 us).  MARSIT_MERGE_KERNEL overrides.
+        if (!mr.cluster && mr.n_parts > 1 && !std::getenv("MARSIT_MERGE_KERNEL")) {
+            DevicePlan coop_plan = mr.dp;
+            const auto coop_cfg = std::make_tuple(mr.wpt, mr.smem, mr.seg_per_launch, mr.tiles_per_seg,
+                                                  mr.part_tiles, mr.n_parts, mr.tile_words, mr.k_steps,
+                                                  mr.lanes_max);
+            mr.cluster = mr.grid = true;
+            DevicePlan gp;
+            marsit_status gs = lower_cluster_plan(ctx->plan, ctx->s_first, ctx->s_own, gp);
+            if (!gs) {
+                mr.dp = gp;
+                uint64_t tw = 0, mw = 0;
+                assign_coin_budget(mr.dp, ctx->s_own, ctx->L, frac, &tw, &mw);
+                gs = mr.configure(ctx->sm_count);
+                if (!gs) {
+                    ctx->coin_total_words = tw;
+                    max_words = mw;
+                }
+            }
+            if (gs) {  // keep the cooperative merge
+                mr.cluster = mr.grid = false;
+                mr.dp = coop_plan;
+                std::tie(mr.wpt, mr.smem, mr.seg_per_launch, mr.tiles_per_seg, mr.part_tiles, mr.n_parts,
+                         mr.tile_words, mr.k_steps, mr.lanes_max) = coop_cfg;
+            }
+        }
     }
     if ((st = mr.upload())) return st;
 

@@ -368,16 +368,20 @@ def test_merge_tilings_bit_exact(wpt, topo, a, b, D, monkeypatch):
     ctx.check()
 
 
-@pytest.mark.parametrize("csize", ["0", "16", "4", "1"])
+@pytest.mark.parametrize("kernel,csize", [("cluster", "0"), ("cluster", "16"), ("cluster", "4"),
+                                          ("cluster", "1"), ("grid", "0"), ("grid", "3"),
+                                          ("grid", "1")])
 @pytest.mark.parametrize("topo,a,b,D", [("ring", 8, 0, 1_000_037), ("torus", 2, 4, 700_001),
                                         ("torus", 3, 3, 36_011), ("ring", 3, 0, 4_001),
                                         ("ring", 16, 0, 250_003)])
-def test_cluster_merge_bit_exact(csize, topo, a, b, D, monkeypatch):
-    """The thread-block-cluster merge (MARSIT_MERGE_KERNEL=cluster: one
-    cluster per segment, levels of up to two independent merges, DSMEM
-    totals) gives the reference's bits for every cluster size, incl. torus
-    continuation streams and ragged segment ends."""
-    monkeypatch.setenv("MARSIT_MERGE_KERNEL", "cluster")
+def test_cluster_merge_bit_exact(kernel, csize, topo, a, b, D, monkeypatch):
+    """The level-loop merges give the reference's bits for every tile count,
+    incl. torus continuation streams and ragged segment ends:
+    MARSIT_MERGE_KERNEL=cluster (one thread-block cluster per segment, DSMEM
+    totals, csize CTAs) and =grid (csize co-resident CTAs per segment,
+    cooperative launch, totals through global memory + a per-segment
+    barrier)."""
+    monkeypatch.setenv("MARSIT_MERGE_KERNEL", kernel)
     monkeypatch.setenv("MARSIT_MERGE_CSIZE", csize)
     sched = sched_of(topo, a, b)
     T = O.schedule(topo, a, b)
@@ -596,3 +600,36 @@ def test_fused_round_zeros_negzero_subnormals_vs_oracle(dtype):
         bound = 1e-6 * (np.abs(r.comp) + np.abs(g64) + np.abs(c64) + ETA)
         assert np.all(np.abs(got - r.comp) <= bound)
     assert ctx.timing()["fused_round"][1] == 1
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("topo,a,b,D", [("torus", 2, 4, 60_200_000), ("ring", 8, 0, 61_000_000)])
+def test_large_segments_grid_merge_equals_cooperative(topo, a, b, D, monkeypatch):
+    """C4 / C2 on one GPU: the segments are too large for one co-resident
+    cooperative grid, so the context picks the grid merge (one launch); its
+    aggregate and compensation equal the cooperative merge's (forced with
+    MARSIT_MERGE_KERNEL=coop) bit for bit over carried rounds."""
+    sched = sched_of(topo, a, b)
+    W, seed = sched.workers, 2026
+    auto = mb.Context(D, sched, torch.float32, 0)
+    auto.set_timing(True)
+    monkeypatch.setenv("MARSIT_MERGE_KERNEL", "coop")
+    coop = mb.Context(D, sched, torch.float32, 0)
+    monkeypatch.delenv("MARSIT_MERGE_KERNEL")
+    g = [torch.empty(D, device=DEV) for _ in range(W)]
+    c1 = [torch.zeros(D, device=DEV) for _ in range(W)]
+    c2 = [torch.zeros(D, device=DEV) for _ in range(W)]
+    a1 = torch.empty((D + 63) // 64, dtype=torch.int64, device=DEV)
+    a2 = torch.empty_like(a1)
+    for t in (1, 2):
+        for w in range(W):
+            mb.fill_recipe(g[w], t % 2, seed, w, t)
+        auto.sign_round(t, ETA, seed, g, c1, agg_bits=a1)
+        coop.sign_round(t, ETA, seed, g, c2, agg_bits=a2)
+        torch.cuda.synchronize()
+        assert torch.equal(a1, a2), t
+        for w in range(W):
+            assert torch.equal(c1[w], c2[w]), (t, w)
+    assert auto.timing()["merge"][1] == 2  # one merge launch per round
+    auto.check()
+    coop.check()

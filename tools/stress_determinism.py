@@ -38,11 +38,13 @@ for i in range(n_cfg):
     T = O.schedule(topo, a, b)
     W = sched.workers
     D = rng.choice([rng.randint(W, 5000), rng.randint(5000, 400_000), rng.randint(400_000, 2_000_000)])
-    kernel = rng.choice(["coop", "cluster"])
+    kernel = rng.choice(["coop", "cluster", "grid"])
     env = {"MARSIT_MERGE_KERNEL": kernel, "MARSIT_COIN_FRAC": rng.choice(["0", "0.2", "0.53", "2"]),
            "MARSIT_FUSED": rng.choice(["0", "1"])}
     if kernel == "cluster":
         env["MARSIT_MERGE_CSIZE"] = rng.choice(["0", "2", "8", "16"])
+    elif kernel == "grid":
+        env["MARSIT_MERGE_CSIZE"] = rng.choice(["0", "0", "5"])
     else:
         env["MARSIT_MERGE_WPT"] = rng.choice(["0", "1", "4", "12"])
     G = rng.choice([g for g in (1, 2, 4) if W % g == 0 and sched.segments % g == 0])
