@@ -1168,11 +1168,20 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
             // lower-ranked CTAs' totals (the tile's draw offset) and the
             // cluster total: lane q holds CTA q's total, warp reductions
             unsigned long long pre = 0, tot = 0;
-            if (GRID) {
-                for (uint32_t q = lane; q < p.csize; q += 32) {
-                    const unsigned long long x = __ldcg(xch + size_t(q) * NL + i);
-                    pre += q < cr ? x : 0ull;
-                    tot += x;
+            if (GRID) {  // all of a lane's loads in flight at once (8 per 256 CTAs)
+                for (uint32_t q0 = 0; q0 < p.csize; q0 += 256) {
+                    unsigned long long x[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const uint32_t q = q0 + k * 32 + lane;
+                        x[k] = q < p.csize ? __ldcg(xch + size_t(q) * NL + i) : 0ull;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const uint32_t q = q0 + k * 32 + lane;
+                        pre += q < cr ? x[k] : 0ull;
+                        tot += x[k];
+                    }
                 }
             } else {
                 const unsigned long long x = uint32_t(lane) < p.csize ? sh.all[v & 1][i][lane] : 0ull;
