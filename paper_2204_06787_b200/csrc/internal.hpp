@@ -186,8 +186,9 @@ struct MergeRunner {
             if (forced && cs != uint32_t(forced)) continue;
             const uint32_t tg = uint32_t(ceil_div(total_groups, cs));
             uint32_t ns = 0;
+            const uint32_t threads = fused_arrays ? uint32_t(kFusedThreads) : uint32_t(kClusterThreads);
             for (uint32_t c : {1u, 2u, 4u, 8u, 16u})
-                if (uint64_t(c) * kClusterThreads >= tg && (nl == 1 || c <= 8)) {
+                if (uint64_t(c) * threads >= tg && (nl == 1 || c <= 8)) {
                     ns = c;
                     break;
                 }

@@ -982,10 +982,10 @@ __device__ __forceinline__ void st_cluster_u64(void* local, uint32_t rank, unsig
 // cl_slots: [n_slots][tile_groups] node values of this CTA's tile, then
 // (p.stage) [NL][2][tile_groups] the level's r and d staged by pass 1.
 // Static shared state of the cluster merge of one CTA.
-template <int NSUB, int NL>
+template <int NSUB, int NL, int NT = kClusterThreads>
 struct ClusterMergeShared {
-    uint32_t wt[NL * NSUB][kClusterThreads / 32];    // warp totals per column
-    uint32_t wpre[NL * NSUB][kClusterThreads / 32];  // exclusive warp prefix per column
+    uint32_t wt[NL * NSUB][NT / 32];    // warp totals per column
+    uint32_t wpre[NL * NSUB][NT / 32];  // exclusive warp prefix per column
     uint32_t ctot[NL * NSUB];                        // CTA total per column
     unsigned long long all[2][NL][kMaxClusterSize];  // CTA totals of the cluster (DSMEM)
     DevMerge m[kMaxSegMerges];
@@ -999,8 +999,9 @@ struct ClusterMergeShared {
 // The caller then needs one cluster barrier (every CTA of the cluster runs
 // before the first remote store; it also publishes the staging to the CTA).
 // The fused kernel stages before its extract and has that barrier after it.
-template <int NSUB, int NL, bool SMEM_LEAVES, bool GRID = false>
-__device__ __forceinline__ void cluster_merge_prologue(const ClusterParams& p, ClusterMergeShared<NSUB, NL>& sh,
+template <int NSUB, int NL, bool SMEM_LEAVES, bool GRID = false, int NT = kClusterThreads>
+__device__ __forceinline__ void cluster_merge_prologue(const ClusterParams& p,
+                                                       ClusterMergeShared<NSUB, NL, NT>& sh,
                                                        const uint4* leaf_smem) {
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1010,7 +1011,7 @@ __device__ __forceinline__ void cluster_merge_prologue(const ClusterParams& p, C
     const uint32_t mb = p.seg_begin[sl], nm = p.seg_begin[sl + 1] - mb;
     const uint32_t lb0 = p.lvl_start[sl], nlv = p.lvl_start[sl + 1] - lb0 - 1;
     const uint32_t g_first = cr * p.tile_groups;
-    for (uint32_t i = tid; i < nm; i += kClusterThreads) {
+    for (uint32_t i = tid; i < nm; i += NT) {
         const DevMerge m = p.merges[mb + i];
         sh.m[i] = m;
         sh.tot[i] = 0;
@@ -1033,12 +1034,12 @@ __device__ __forceinline__ void cluster_merge_prologue(const ClusterParams& p, C
             sh.row[i][o] = row;
         }
     }
-    for (uint32_t i = tid; i <= nlv; i += kClusterThreads) sh.lvl[i] = p.lvl_begin[lb0 + i];
+    for (uint32_t i = tid; i <= nlv; i += NT) sh.lvl[i] = p.lvl_begin[lb0 + i];
 }
 
 // The level loop (after cluster_merge_prologue).
-template <int NSUB, int NL, bool SMEM_LEAVES, bool GRID = false>
-__device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, ClusterMergeShared<NSUB, NL>& sh,
+template <int NSUB, int NL, bool SMEM_LEAVES, bool GRID = false, int NT = kClusterThreads>
+__device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, ClusterMergeShared<NSUB, NL, NT>& sh,
                                                      uint4* cl_slots, const uint4* leaf_smem, uint4* agg_smem) {
     constexpr int NCOL = NL * NSUB;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1092,7 +1093,7 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
         for (int i = 0; i < NL; ++i)
 #pragma unroll
             for (int u = 0; u < NSUB; ++u) {
-                const uint32_t gl = uint32_t(u) * kClusterThreads + tid;
+                const uint32_t gl = uint32_t(u) * NT + tid;
                 uint32_t c = 0;
                 if (uint32_t(i) < nk && gl < n_here) {
                     uint4 r, d;
@@ -1113,15 +1114,15 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
                 if (lane == 31) sh.wt[i * NSUB + u][wid] = incl;
             }
         __syncthreads();
-        if (wid < NCOL) {
-            const uint32_t x = sh.wt[wid][lane];
+        if (wid < NCOL) {  // NT / 32 <= 32 warp totals per column
+            const uint32_t x = lane < NT / 32 ? sh.wt[wid][lane] : 0u;
             uint32_t incl = x;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(kFull, incl, o);
                 if (lane >= o) incl += y;
             }
-            sh.wpre[wid][lane] = incl - x;
+            if (lane < NT / 32) sh.wpre[wid][lane] = incl - x;
             if (lane == 31) sh.ctot[wid] = incl;
         }
         __syncthreads();
@@ -1219,7 +1220,7 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int u = u0 + h;
-                    const uint32_t gl = uint32_t(u) * kClusterThreads + tid;
+                    const uint32_t gl = uint32_t(u) * NT + tid;
                     live[h] = u < NSUB && gl < n_here;
                     fast[h] = false;
                     if (u < NSUB) {
@@ -1279,7 +1280,7 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
                         for (int j = 0; j < 4; ++j) rr[j] ^= dd[j] & ~coin_word(dd[j], z, m.thresh11);
                     }
                     const uint4 out = make_uint4(rr[0], rr[1], rr[2], rr[3]);
-                    const uint32_t gl = uint32_t(u0 + h) * kClusterThreads + tid;
+                    const uint32_t gl = uint32_t(u0 + h) * NT + tid;
                     if (m.out_slot != kNone) cl_slots[size_t(m.out_slot) * p.tile_groups + gl] = out;
                     if (m.out_global == kFinal) {
                         reinterpret_cast<uint4*>(p.agg + uint64_t(sg) * p.agg_stride)[g_first + gl] = out;
@@ -1339,19 +1340,19 @@ __device__ __forceinline__ bool quad_real(uint64_t j, uint64_t seg_len, uint64_t
 }
 
 template <typename T, int NSUB, int NL>
-__global__ void __launch_bounds__(kClusterThreads, 1)
+__global__ void __launch_bounds__(kFusedThreads, 1)
     round_cluster_kernel(const ClusterParams p, const FusedParams<T> f) {
 #ifdef MARSIT_FUSED_PROF
     const uint64_t fp_t0 = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0;
 #endif
     extern __shared__ uint4 fz_dyn[];  // [workers][tg] leaves, [tg] aggregate, then the merge's slots / staging
-    __shared__ ClusterMergeShared<NSUB, NL> sh;
+    __shared__ ClusterMergeShared<NSUB, NL, kFusedThreads> sh;
     const uint32_t tg = p.tile_groups;
     uint4* leaf = fz_dyn;
     uint4* aggs = leaf + size_t(f.workers) * tg;
     uint4* slots = aggs + tg;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    constexpr uint32_t NWARP = kClusterThreads / 32;
+    constexpr uint32_t NWARP = kFusedThreads / 32;
     const uint32_t cr = cluster_ctarank();
     const uint32_t sl = p.seg_lo + blockIdx.x / p.csize;
     const uint32_t g_first = cr * tg;
@@ -1359,8 +1360,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     const uint32_t n_here = total_groups > g_first ? min(tg, total_groups - g_first) : 0u;
     const uint64_t seg0 = uint64_t(sl) * p.seg_bits;  // first coordinate of the segment (G == 1)
     // the merge's descriptors, loaded under the extract's streaming
-    cluster_merge_prologue<NSUB, NL, true>(p, sh, leaf);
-    constexpr int B = 2;  // groups per warp step: 2B quad loads in flight per lane
+    cluster_merge_prologue<NSUB, NL, true, false, kFusedThreads>(p, sh, leaf);
+    constexpr int B = sizeof(T) == 4 ? 4 : 2;  // groups per warp step: 2B quad loads in flight per lane
     // K1: u = g + c, sign nibbles -> packed words in shared memory
     T fin = T(0);
     for (uint32_t w = 0; w < f.workers; ++w) {
@@ -1413,7 +1414,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
 #ifdef MARSIT_FUSED_PROF
     const uint64_t fp_t1 = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0;
 #endif
-    cluster_merge_levels<NSUB, NL, true>(p, sh, slots, leaf, aggs);
+    cluster_merge_levels<NSUB, NL, true, false, kFusedThreads>(p, sh, slots, leaf, aggs);
     __syncthreads();
 #ifdef MARSIT_FUSED_PROF
     const uint64_t fp_t2 = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0;
@@ -2122,7 +2123,7 @@ static cudaError_t fused_launch_t(const ClusterParams& p, const FusedParams<T>& 
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(clusters * p.csize);
-    cfg.blockDim = dim3(kClusterThreads);
+    cfg.blockDim = dim3(kFusedThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -2141,7 +2142,7 @@ static cudaError_t fused_occ_t(uint32_t csize, size_t smem, int* clusters) {
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(csize);
-    cfg.blockDim = dim3(kClusterThreads);
+    cfg.blockDim = dim3(kFusedThreads);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -137,6 +137,9 @@ cudaError_t launch_merge_cluster(const ClusterParams& p, int nsub, int nl, uint3
 // these sizes).  Needs every worker local, M <= kFusedMaxWorkers, 16-byte
 // aligned quads (L % 4 == 0).
 constexpr uint32_t kFusedMaxWorkers = 16;
+// 512 threads per CTA (up to 128 registers each): 8 fp32 (4 fp64) quads of g
+// and of c in flight per lane in the streaming phases
+constexpr int kFusedThreads = 512;
 
 template <typename T>
 struct FusedParams {
