@@ -116,22 +116,26 @@ struct MergeRunner {
     bool seg_barrier = env_int("MARSIT_SEG_BARRIER", 1) != 0;
     const uint32_t* const* peer_bits = nullptr;  // P2P transport: device table [G]
     int* err = nullptr;                          // the context's error latch (checked builds)
-    // MARSIT_MERGE_KERNEL=cluster: the thread-block-cluster merge (one cluster
-    // per segment, DSMEM totals, one launch); default: the cooperative merge,
-    // faster on B200 for every measured configuration
+    // Merge kernel, MARSIT_MERGE_KERNEL:
+    //   grid (default): the level loop over any number of co-resident
+    //     1024-thread CTAs per segment (cooperative launch, tagged global
+    //     totals; K2g) on the cluster plan;
+    //   cluster: the same loop on one thread-block cluster per segment (DSMEM
+    //     totals; K2c);
+    //   coop: the cooperative stage/part merge (K2), also the fallback when
+    //     the grid merge's tiles do not fit.
     bool cluster = [] {
         const char* e = std::getenv("MARSIT_MERGE_KERNEL");
-        return e && (std::strcmp(e, "cluster") == 0 || std::strcmp(e, "grid") == 0);
+        return !e || std::strcmp(e, "cluster") == 0 || std::strcmp(e, "grid") == 0;
     }();
-    // MARSIT_MERGE_KERNEL=grid: the same level loop over any number of
-    // co-resident 1024-thread CTAs per segment (cooperative launch, global
-    // totals + per-segment barrier; K2g); uses the cluster plan
     bool grid = [] {
         const char* e = std::getenv("MARSIT_MERGE_KERNEL");
-        return e && std::strcmp(e, "grid") == 0;
+        return !e || std::strcmp(e, "grid") == 0;
     }();
     unsigned long long* xch = nullptr;  // grid mode: [2][seg_per_launch][csize][level_width]
-    uint32_t csize = 16, tile_groups = 0, nsub = 1, stage = 0;
+    uint32_t xch_epoch = 0;             // grid mode: launches so far (the words' launch tag)
+    uint32_t prefetch = env_int("MARSIT_MERGE_PREFETCH", 1) != 0;  // level loop: next leaves into L1
+    uint32_t csize = 16, tile_groups = 0, nsub = 1, stage = 0, masks = 0;
     size_t merge_smem = 0;  // merge_cluster_kernel's dynamic shared memory (smem minus the fused ring)
     // fused small rounds (round_cluster_kernel): extra shared memory per CTA
     // for every worker's packed tile + the aggregate; 0 = merge only
@@ -202,7 +206,11 @@ struct MergeRunner {
             const size_t cap = fused_arrays ? 212 * 1024 : 200 * 1024;  // fused: 227 KB - static
             if (base_sm + ring > cap) continue;
             const uint32_t stg = base_sm + stage_sm + ring <= cap && env_int("MARSIT_MERGE_STAGE", 1) ? 1u : 0u;
-            const size_t sm = std::max<size_t>(base_sm + (stg ? stage_sm : 0) + ring, 16);
+            // + the deposit masks formed during the level barrier
+            const size_t mask_sm = size_t(4) * nl * tg * 16;
+            const uint32_t msk =
+                stg && base_sm + stage_sm + mask_sm + ring <= cap && env_int("MARSIT_MERGE_MASKS", 1) ? 1u : 0u;
+            const size_t sm = std::max<size_t>(base_sm + (stg ? stage_sm : 0) + (msk ? mask_sm : 0) + ring, 16);
             int occ = 0;
             if (fused_arrays && ns > 4) continue;  // the fused kernel's instantiations
             const cudaError_t oe =
@@ -216,8 +224,8 @@ struct MergeRunner {
             const uint64_t waves = ceil_div(seg_per_launch, uint64_t(occ));
             const uint64_t cost = waves * (uint64_t(tg) + 400);
             if (env_int("MARSIT_MERGE_DEBUG", 0))
-                fprintf(stderr, "merge cluster: csize %u groups/CTA %u nsub %u stage %u occ %d waves %llu cost %llu\n",
-                        cs, tg, ns, stg, occ, (unsigned long long)waves, (unsigned long long)cost);
+                fprintf(stderr, "merge cluster: csize %u groups/CTA %u nsub %u stage %u masks %u occ %d waves %llu cost %llu\n",
+                        cs, tg, ns, stg, msk, occ, (unsigned long long)waves, (unsigned long long)cost);
             if (cost < best) {
                 best = cost;
                 csize = cs;
@@ -226,6 +234,7 @@ struct MergeRunner {
                 smem = sm;
                 merge_smem = sm - ring;
                 stage = stg;
+                masks = msk;
             }
         }
         if (best == ~0ull) return fail(MARSIT_EUNSUPPORTED, "merge clusters do not fit the device");
@@ -241,10 +250,12 @@ struct MergeRunner {
         const uint32_t total_groups = words_proc / 4;
         int occ = 0;
         for (int attempt = 0; attempt < 2; ++attempt) {
-            seg_per_launch = std::min<uint32_t>(seg_launch, uint32_t(sm_count) * std::max(occ, 1));
-            const uint32_t cs = std::max<uint32_t>(1, uint32_t(sm_count) * std::max(occ, 1) / seg_per_launch);
+            // MARSIT_MERGE_CSIZE forces the CTAs per segment (the segments
+            // then run as several launches when they do not fit one)
+            const uint32_t slots = uint32_t(sm_count) * std::max(occ, 1);
             const uint32_t forced = uint32_t(env_int("MARSIT_MERGE_CSIZE", 0));
-            csize = forced ? forced : cs;
+            seg_per_launch = std::min<uint32_t>(seg_launch, forced ? std::max(1u, slots / forced) : slots);
+            csize = forced ? forced : std::max<uint32_t>(1, slots / seg_per_launch);
             tile_groups = uint32_t(ceil_div(total_groups, csize));
             nsub = 0;
             for (uint32_t c : {1u, 2u, 4u, 8u, 16u})
@@ -256,7 +267,9 @@ struct MergeRunner {
             const size_t base_sm = size_t(dp.max_slots) * tile_groups * 16;
             const size_t stage_sm = size_t(2) * nl * tile_groups * 16;
             stage = base_sm + stage_sm <= 200 * 1024 && env_int("MARSIT_MERGE_STAGE", 1) ? 1u : 0u;
-            smem = merge_smem = std::max<size_t>(base_sm + (stage ? stage_sm : 0), 16);
+            const size_t mask_sm = size_t(4) * nl * tile_groups * 16;
+            masks = stage && base_sm + stage_sm + mask_sm <= 200 * 1024 && env_int("MARSIT_MERGE_MASKS", 1) ? 1u : 0u;
+            smem = merge_smem = std::max<size_t>(base_sm + (stage ? stage_sm : 0) + (masks ? mask_sm : 0), 16);
             if (smem > 200 * 1024) return fail(MARSIT_EUNSUPPORTED, "merge tiles do not fit shared memory");
             CUDA_TRY(merge_grid_occupancy(int(nsub), int(nl), smem, &occ));
             if (occ <= 0) return fail(MARSIT_EUNSUPPORTED, "grid merge does not fit an SM");
@@ -265,8 +278,8 @@ struct MergeRunner {
         if (uint64_t(seg_per_launch) * csize > uint64_t(occ) * sm_count)
             return fail(MARSIT_EUNSUPPORTED, "grid merge CTAs are not co-resident");
         if (env_int("MARSIT_MERGE_DEBUG", 0))
-            fprintf(stderr, "merge grid: %u segments x %u CTAs, groups/CTA %u nsub %u stage %u\n",
-                    seg_per_launch, csize, tile_groups, nsub, stage);
+            fprintf(stderr, "merge grid: %u segments x %u CTAs, groups/CTA %u nsub %u stage %u masks %u\n",
+                    seg_per_launch, csize, tile_groups, nsub, stage, masks);
         return MARSIT_OK;
     }
 
@@ -360,8 +373,7 @@ struct MergeRunner {
             if (grid) {
                 const size_t nx = size_t(2) * seg_per_launch * csize * dp.level_width;
                 CUDA_TRY(cudaMalloc(&xch, sizeof(unsigned long long) * nx));
-                CUDA_TRY(cudaMalloc(&seg_bars, sizeof(unsigned) * seg_per_launch));
-                CUDA_TRY(cudaMemset(seg_bars, 0, sizeof(unsigned) * seg_per_launch));
+                CUDA_TRY(cudaMemset(xch, 0, sizeof(unsigned long long) * nx));
             }
             return MARSIT_OK;
         }
@@ -405,6 +417,8 @@ struct MergeRunner {
         c.ml = ml;
         c.n_slots = dp.max_slots;
         c.stage = stage;
+        c.masks = masks;
+        c.prefetch = prefetch;
         c.seg_bits = L;
         c.leaves = leaves;
         c.peer_bits = peer_bits;
@@ -432,7 +446,9 @@ struct MergeRunner {
             if (seg_cnt == 0) return MARSIT_OK;
             if (grid) {  // launches of at most seg_per_launch co-resident segments
                 for (uint32_t s0 = seg_lo; s0 < seg_lo + seg_cnt; s0 += seg_per_launch) {
-                    const ClusterParams c = cluster_params(leaves, agg, coins, seed, round, s0, coin_valid);
+                    ClusterParams c = cluster_params(leaves, agg, coins, seed, round, s0, coin_valid);
+                    if ((++xch_epoch & 0xFFFFFFu) == 0) ++xch_epoch;  // tag 0 = never written
+                    c.xch_tag = xch_epoch;
                     CUDA_TRY(launch_merge_grid(c, int(nsub), int(dp.level_width),
                                                std::min(seg_per_launch, seg_lo + seg_cnt - s0), smem, st));
                     ++*n_launch;

@@ -991,6 +991,7 @@ struct ClusterMergeShared {
     DevMerge m[kMaxSegMerges];
     const uint4* row[kMaxSegMerges][2];              // leaf operand rows (recv, local) or null
     unsigned long long tot[kMaxSegMerges];           // cluster-wide draws of each merge
+    unsigned long long gx[NL][2];                    // grid mode: (lower CTAs', all CTAs') totals
     uint32_t valid[kMaxSegMerges];
     uint32_t lvl[kMaxSegMerges + 1];
 };
@@ -1130,12 +1131,17 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
         // slot [v & 1][i][cr] (DSMEM); grid mode into global memory
         unsigned long long* const xch =
             GRID ? p.xch + (size_t(v & 1) * (gridDim.x / p.csize) + seg_in_launch) * p.csize * NL : nullptr;
+        // grid mode: the total rides in one 64-bit word with the launch's
+        // level tag, so the readers' polls are the barrier (no counter)
+        const uint32_t tag = GRID ? (p.xch_tag << 8) | (v & 0xFFu) : 0u;
         if (GRID) {
             if (tid < NL) {
                 unsigned long long t = 0;
 #pragma unroll
                 for (int u = 0; u < NSUB; ++u) t += sh.ctot[tid * NSUB + u];
-                __stcg(xch + size_t(cr) * NL + tid, t);
+                t |= uint64_t(tag) << 32;
+                asm volatile("st.relaxed.gpu.global.u64 [%0],%1;" ::"l"(xch + size_t(cr) * NL + tid), "l"(t)
+                             : "memory");
             }
         } else if (uint32_t(tid) < p.csize) {
 #pragma unroll
@@ -1150,11 +1156,85 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
 #ifdef MARSIT_FUSED_PROF
         const uint64_t lv_t1 = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0;
 #endif
-        if (GRID) {  // one barrier over the segment's CTAs (release / acquire)
-            const unsigned tok = seg_barrier_arrive(p.seg_bars + seg_in_launch, cr == 0, p.csize);
-            seg_barrier_wait(p.seg_bars + seg_in_launch, tok);
+        // split barrier: arrive, form the deposit masks of the staged d while
+        // the other CTAs arrive (they depend on d only), then wait
+        if (!GRID) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        if (p.masks) {
+            uint4* const mreg = stage + size_t(2 * NL) * p.tile_groups;  // [NL][4 words][tg] x 4 masks
+#pragma unroll
+            for (int i = 0; i < NL; ++i)
+#pragma unroll
+                for (int u = 0; u < NSUB; ++u) {
+                    const uint32_t gl = uint32_t(u) * NT + tid;
+                    if (uint32_t(i) >= nk || gl >= n_here) continue;
+                    const uint4 d = stage[(i * 2 + 1) * p.tile_groups + gl];
+                    const uint32_t dd[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        uint32_t mv[4];
+                        expand_masks(dd[j], mv);
+                        mreg[size_t(i * 4 + j) * p.tile_groups + gl] = make_uint4(mv[0], mv[1], mv[2], mv[3]);
+                    }
+                }
+        }
+        if (!SMEM_LEAVES && !peer && v + 1 < nlv && p.prefetch) {
+            // the next level's local leaf tiles into L1 while the totals arrive
+            const uint32_t k1 = sh.lvl[v + 1], nk1 = sh.lvl[v + 2] - k1;
+#pragma unroll
+            for (int i = 0; i < NL; ++i)
+#pragma unroll
+                for (int u = 0; u < NSUB; ++u) {
+                    const uint32_t gl = uint32_t(u) * NT + tid;
+                    if (uint32_t(i) >= nk1 || gl >= n_here) continue;
+#pragma unroll
+                    for (int o = 0; o < 2; ++o)
+                        if (const uint4* row = sh.row[k1 + i][o])
+                            asm volatile("prefetch.global.L1 [%0];" ::"l"(row + gl));
+                }
+        }
+        if (GRID) {
+            // warp i polls merge i's words of every CTA of the segment (all
+            // of a lane's loads in flight at once, 8 per 256 CTAs) until each
+            // carries this level's tag: the lower CTAs' sum is the tile's
+            // draw offset, the sum over all the merge's total
+            if (wid < NL && uint32_t(wid) < nk) {
+                unsigned long long pre = 0, tot = 0;
+                for (uint32_t q0 = 0; q0 < p.csize; q0 += 256) {
+                    unsigned long long x[8];
+                    for (;;) {
+                        bool ok = true;
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const uint32_t q = q0 + e * 32 + lane;
+                            x[e] = uint64_t(tag) << 32;
+                            if (q < p.csize)
+                                asm volatile("ld.relaxed.gpu.global.u64 %0,[%1];"
+                                             : "=l"(x[e])
+                                             : "l"(xch + size_t(q) * NL + wid)
+                                             : "memory");
+                        }
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) ok &= uint32_t(x[e] >> 32) == tag;
+                        if (__all_sync(kFull, ok)) break;
+                    }
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const uint32_t q = q0 + e * 32 + lane;
+                        const unsigned long long t = x[e] & 0xFFFFFFFFull;
+                        pre += q < cr ? t : 0ull;
+                        tot += t;
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    pre += __shfl_xor_sync(kFull, pre, o);
+                    tot += __shfl_xor_sync(kFull, tot, o);
+                }
+                if (lane == 0) sh.gx[wid][0] = pre, sh.gx[wid][1] = tot;
+            }
+            __syncthreads();
         } else {
-            cluster_sync_all();
+            asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
         }
         jitter(2 * v + 1);
 #ifdef MARSIT_FUSED_PROF
@@ -1169,30 +1249,17 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
             // lower-ranked CTAs' totals (the tile's draw offset) and the
             // cluster total: lane q holds CTA q's total, warp reductions
             unsigned long long pre = 0, tot = 0;
-            if (GRID) {  // all of a lane's loads in flight at once (8 per 256 CTAs)
-                for (uint32_t q0 = 0; q0 < p.csize; q0 += 256) {
-                    unsigned long long x[8];
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const uint32_t q = q0 + k * 32 + lane;
-                        x[k] = q < p.csize ? __ldcg(xch + size_t(q) * NL + i) : 0ull;
-                    }
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const uint32_t q = q0 + k * 32 + lane;
-                        pre += q < cr ? x[k] : 0ull;
-                        tot += x[k];
-                    }
-                }
+            if (GRID) {
+                pre = sh.gx[i][0], tot = sh.gx[i][1];
             } else {
                 const unsigned long long x = uint32_t(lane) < p.csize ? sh.all[v & 1][i][lane] : 0ull;
                 pre = uint32_t(lane) < cr ? x : 0ull;
                 tot = x;
-            }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                pre += __shfl_xor_sync(kFull, pre, o);
-                tot += __shfl_xor_sync(kFull, tot, o);
+                for (int o = 16; o > 0; o >>= 1) {
+                    pre += __shfl_xor_sync(kFull, pre, o);
+                    tot += __shfl_xor_sync(kFull, tot, o);
+                }
             }
             // stream base: draws before this round's merges + the earlier
             // merges of the same (receiver, segment) stream (continuation)
@@ -1253,10 +1320,16 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
                         // coins start o bits into (lo, hi); at most one advance
                         // per word (popc <= 32)
                         uint32_t lo = win[h][0], hi = win[h][1], o = uint32_t(n0[h] & 31), a = 0;
+                        const uint32_t glh = uint32_t(u0 + h) * NT + tid;
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
                             uint32_t mv[4];
-                            expand_masks(dd[j], mv);
+                            if (p.masks) {  // formed during the barrier
+                                const uint4 q = (stage + size_t(2 * NL) * p.tile_groups)[size_t(i * 4 + j) * p.tile_groups + glh];
+                                mv[0] = q.x, mv[1] = q.y, mv[2] = q.z, mv[3] = q.w;
+                            } else {
+                                expand_masks(dd[j], mv);
+                            }
                             rr[j] ^= dd[j] & ~expand_apply(__funnelshift_r(lo, hi, o), mv);
                             o += __popc(dd[j]);
                             if (j < 3) {

@@ -109,6 +109,8 @@ struct ClusterParams {
     uint32_t tile_groups;         // 4-word groups per CTA tile
     uint32_t words_proc, wst, ml, n_slots;
     uint32_t stage;               // 1: pass 1 stages r and d in shared memory for pass 2
+    uint32_t masks;               // 1 (needs stage): the deposit masks of d formed during the
+                                  // barrier, [NL][4][tile_groups] uint4 after the staging
     uint64_t seg_bits;            // L
     const uint32_t* leaves;       // leaf(w, sl) = leaves + ((w/ml*n_seg + sl)*ml + w%ml)*wst
     const uint32_t* const* peer_bits;  // P2P: leaf(w, sl) = peer_bits[w/ml] + ((s_first+sl)*ml + w%ml)*wst
@@ -122,9 +124,12 @@ struct ClusterParams {
     int* err;                     // checked builds: bounds latch (bit 3)
     // grid mode (merge_grid_kernel): csize = CTAs ("tiles") per segment, any
     // number; the per-merge CTA totals go through global memory, xch
-    // [2][segments of the launch][csize][NL], and one barrier per segment and
-    // level (seg_bars[segment of the launch]) replaces the cluster barrier
-    unsigned long long* xch;
+    // [2][segments of the launch][csize][NL]: each word carries its launch
+    // and level tag, and polling all of a segment's words replaces the
+    // cluster barrier
+    unsigned long long* xch;      // word = level tag << 32 | CTA total
+    uint32_t prefetch;            // 1: the next level's local leaf tiles are prefetched into L1
+    uint32_t xch_tag;             // per launch (host counter; the level is the low 8 bits)
     unsigned* seg_bars;
 };
 cudaError_t launch_merge_cluster(const ClusterParams& p, int nsub, int nl, uint32_t clusters,

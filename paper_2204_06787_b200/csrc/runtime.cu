@@ -1471,13 +1471,24 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     ctx->fused = G == 1 && hs.workers <= kFusedMaxWorkers && ctx->vec_ok &&
                  uint64_t(hs.workers) * ctx->D * ctx->esize * 2 <= (96ull << 20) &&
                  env_int("MARSIT_FUSED", 1) != 0;
+    const bool grid_default = mr.grid;
+    const bool kernel_forced = std::getenv("MARSIT_MERGE_KERNEL") != nullptr;
     if (ctx->fused) {
         mr.cluster = true;
         mr.fused_arrays = hs.workers + 1;
         mr.fused_dtype = desc->dtype == MARSIT_F64 ? 1 : 0;
     }
-    marsit_status st = mr.cluster ? lower_cluster_plan(ctx->plan, ctx->s_first, ctx->s_own, mr.dp)
-                                  : lower_plan(ctx->plan, ctx->s_first, ctx->s_own, mr.dp);
+    double frac = 0.53;
+    if (const char* e = std::getenv("MARSIT_COIN_FRAC")) frac = std::atof(e);
+    uint64_t max_words = 0;
+    // lower the plan for the runner's merge kernel and size its coin budget
+    auto lower = [&]() -> marsit_status {
+        marsit_status ls = mr.cluster ? lower_cluster_plan(ctx->plan, ctx->s_first, ctx->s_own, mr.dp)
+                                      : lower_plan(ctx->plan, ctx->s_first, ctx->s_own, mr.dp);
+        if (!ls) assign_coin_budget(mr.dp, ctx->s_own, ctx->L, frac, &ctx->coin_total_words, &max_words);
+        return ls;
+    };
+    marsit_status st = lower();
     if (st) return st;
     mr.n_seg = ctx->s_own;
     mr.s_first = ctx->s_first;
@@ -1486,56 +1497,33 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     mr.ml = ctx->ml;
     mr.L = ctx->L;
     mr.agg_stride = ctx->wsa;
-    double frac = 0.53;
-    if (const char* e = std::getenv("MARSIT_COIN_FRAC")) frac = std::atof(e);
-    uint64_t max_words = 0;
-    assign_coin_budget(mr.dp, ctx->s_own, ctx->L, frac, &ctx->coin_total_words, &max_words);
     // single GPU with several segments: per-segment merge launches sized to
-    // co-reside with the decode (MARSIT_PIPELINE=0 disables)
+    // co-reside with the decode (MARSIT_PIPELINE=1 enables)
     ctx->pipeline = G == 1 && ctx->S >= 2 && env_int("MARSIT_PIPELINE", 0) != 0 &&
                     desc->transport != MARSIT_TRANSPORT_EXTERNAL;
-    if (ctx->pipeline) {
+    if (ctx->pipeline) {  // cooperative merges sized to share the SMs with the decode
+        if (mr.grid && !ctx->fused) {
+            mr.cluster = mr.grid = false;
+            if ((st = lower())) return st;
+        }
         if ((st = mr.configure(ctx->sm_count, 1, env_int("MARSIT_PIPE_MERGE_CTAS", 1)))) return st;
     } else {
         st = mr.configure(ctx->sm_count);
-        if (st && ctx->fused) {  // the fused tiles do not fit: merge-only clusters
+        if (st && ctx->fused) {  // the fused tiles do not fit: the merge kernel alone
             ctx->fused = false;
             mr.fused_arrays = 0;
+            mr.grid = grid_default;
+            st = mr.configure(ctx->sm_count);
+        }
+        // the grid merge's tiles do not fit (very long segments): the
+        // cooperative merge, which runs them as several launch parts
+        if (st && grid_default && mr.grid && !kernel_forced) {
+            cudaGetLastError();
+            mr.cluster = mr.grid = false;
+            if ((st = lower())) return st;
             st = mr.configure(ctx->sm_count);
         }
         if (st) return st;
-        // Segments too large for one co-resident cooperative grid (the
-        // cooperative merge would run as several launch parts, each paying
-        // the whole barrier chain: C2, C4, C5 buckets on one GPU) take the
-        // grid merge K2g: one launch, every stage, shared-memory tiles on
-        // all SMs (C4 157 -> 101 us, C2 129 -> 100 us; it loses where the
-        // cooperative merge fits one part: C3 51 vs 60 us, a G = 8 rank 31 vs
-        // 61 us).  MARSIT_MERGE_KERNEL overrides.
-        if (!mr.cluster && mr.n_parts > 1 && !std::getenv("MARSIT_MERGE_KERNEL")) {
-            DevicePlan coop_plan = mr.dp;
-            const auto coop_cfg = std::make_tuple(mr.wpt, mr.smem, mr.seg_per_launch, mr.tiles_per_seg,
-                                                  mr.part_tiles, mr.n_parts, mr.tile_words, mr.k_steps,
-                                                  mr.lanes_max);
-            mr.cluster = mr.grid = true;
-            DevicePlan gp;
-            marsit_status gs = lower_cluster_plan(ctx->plan, ctx->s_first, ctx->s_own, gp);
-            if (!gs) {
-                mr.dp = gp;
-                uint64_t tw = 0, mw = 0;
-                assign_coin_budget(mr.dp, ctx->s_own, ctx->L, frac, &tw, &mw);
-                gs = mr.configure(ctx->sm_count);
-                if (!gs) {
-                    ctx->coin_total_words = tw;
-                    max_words = mw;
-                }
-            }
-            if (gs) {  // keep the cooperative merge
-                mr.cluster = mr.grid = false;
-                mr.dp = coop_plan;
-                std::tie(mr.wpt, mr.smem, mr.seg_per_launch, mr.tiles_per_seg, mr.part_tiles, mr.n_parts,
-                         mr.tile_words, mr.k_steps, mr.lanes_max) = coop_cfg;
-            }
-        }
     }
     if ((st = mr.upload())) return st;
 

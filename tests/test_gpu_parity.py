@@ -348,7 +348,9 @@ def test_coin_prefetch_speculation_is_safe():
                                         ("ring", 3, 0, 4_001)])
 def test_merge_tilings_bit_exact(wpt, topo, a, b, D, monkeypatch):
     """Every merge tiling (words per thread incl. the 12/16-word tails that
-    pass the segment end, balanced grids) gives the reference's bits."""
+    pass the segment end, balanced grids) of the cooperative merge gives the
+    reference's bits."""
+    monkeypatch.setenv("MARSIT_MERGE_KERNEL", "coop")
     monkeypatch.setenv("MARSIT_MERGE_WPT", str(wpt))
     monkeypatch.setenv("MARSIT_MERGE_BALANCE", "2" if wpt >= 12 else "0")
     sched = sched_of(topo, a, b)
@@ -370,7 +372,7 @@ def test_merge_tilings_bit_exact(wpt, topo, a, b, D, monkeypatch):
 
 @pytest.mark.parametrize("kernel,csize", [("cluster", "0"), ("cluster", "16"), ("cluster", "4"),
                                           ("cluster", "1"), ("grid", "0"), ("grid", "3"),
-                                          ("grid", "1")])
+                                          ("grid", "1"), ("grid", "100"), ("coop", "0")])
 @pytest.mark.parametrize("topo,a,b,D", [("ring", 8, 0, 1_000_037), ("torus", 2, 4, 700_001),
                                         ("torus", 3, 3, 36_011), ("ring", 3, 0, 4_001),
                                         ("ring", 16, 0, 250_003)])
@@ -378,9 +380,9 @@ def test_cluster_merge_bit_exact(kernel, csize, topo, a, b, D, monkeypatch):
     """The level-loop merges give the reference's bits for every tile count,
     incl. torus continuation streams and ragged segment ends:
     MARSIT_MERGE_KERNEL=cluster (one thread-block cluster per segment, DSMEM
-    totals, csize CTAs) and =grid (csize co-resident CTAs per segment,
-    cooperative launch, totals through global memory + a per-segment
-    barrier)."""
+    totals, csize CTAs), =grid (the default: csize co-resident CTAs per
+    segment, cooperative launch, level-tagged totals through global memory)
+    and =coop (the cooperative stage merge)."""
     monkeypatch.setenv("MARSIT_MERGE_KERNEL", kernel)
     monkeypatch.setenv("MARSIT_MERGE_CSIZE", csize)
     sched = sched_of(topo, a, b)
