@@ -1083,6 +1083,23 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
     };
     auto popc4 = [](const uint4& d) { return __popc(d.x) + __popc(d.y) + __popc(d.z) + __popc(d.w); };
 
+    // the next level's local leaf tiles into L1 while this level finishes
+    // (p.prefetch = where: 1 after the masks, 2 before them, 3 after the totals)
+    auto prefetch_next = [&](uint32_t v, uint32_t where) {
+        if (SMEM_LEAVES || peer || v + 1 >= nlv || p.prefetch != where) return;
+        const uint32_t k1 = sh.lvl[v + 1], nk1 = sh.lvl[v + 2] - k1;
+#pragma unroll
+        for (int i = 0; i < NL; ++i)
+#pragma unroll
+            for (int u = 0; u < NSUB; ++u) {
+                const uint32_t gl = uint32_t(u) * NT + tid;
+                if (uint32_t(i) >= nk1 || gl >= n_here) continue;
+#pragma unroll
+                for (int o = 0; o < 2; ++o)
+                    if (const uint4* row = sh.row[k1 + i][o]) asm volatile("prefetch.global.L1 [%0];" ::"l"(row + gl));
+            }
+    };
+
     for (uint32_t v = 0; v < nlv; ++v) {
 #ifdef MARSIT_FUSED_PROF
         const uint64_t lv_t0 = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0;
@@ -1159,6 +1176,7 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
         // split barrier: arrive, form the deposit masks of the staged d while
         // the other CTAs arrive (they depend on d only), then wait
         if (!GRID) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        prefetch_next(v, 2);
         if (p.masks) {
             uint4* const mreg = stage + size_t(2 * NL) * p.tile_groups;  // [NL][4 words][tg] x 4 masks
 #pragma unroll
@@ -1177,21 +1195,7 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
                     }
                 }
         }
-        if (!SMEM_LEAVES && !peer && v + 1 < nlv && p.prefetch) {
-            // the next level's local leaf tiles into L1 while the totals arrive
-            const uint32_t k1 = sh.lvl[v + 1], nk1 = sh.lvl[v + 2] - k1;
-#pragma unroll
-            for (int i = 0; i < NL; ++i)
-#pragma unroll
-                for (int u = 0; u < NSUB; ++u) {
-                    const uint32_t gl = uint32_t(u) * NT + tid;
-                    if (uint32_t(i) >= nk1 || gl >= n_here) continue;
-#pragma unroll
-                    for (int o = 0; o < 2; ++o)
-                        if (const uint4* row = sh.row[k1 + i][o])
-                            asm volatile("prefetch.global.L1 [%0];" ::"l"(row + gl));
-                }
-        }
+        prefetch_next(v, 1);
         if (GRID) {
             // warp i polls merge i's words of every CTA of the segment (all
             // of a lane's loads in flight at once, 8 per 256 CTAs) until each
@@ -1236,6 +1240,7 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
         } else {
             asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
         }
+        prefetch_next(v, 3);
         jitter(2 * v + 1);
 #ifdef MARSIT_FUSED_PROF
         const uint64_t lv_t2 = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0;

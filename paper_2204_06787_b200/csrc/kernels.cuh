@@ -128,7 +128,8 @@ struct ClusterParams {
     // and level tag, and polling all of a segment's words replaces the
     // cluster barrier
     unsigned long long* xch;      // word = level tag << 32 | CTA total
-    uint32_t prefetch;            // 1: the next level's local leaf tiles are prefetched into L1
+    uint32_t prefetch;            // >0: the next level's local leaf tiles are prefetched into L1
+                                  // (1 after the masks, 2 before them, 3 after the totals)
     uint32_t xch_tag;             // per launch (host counter; the level is the low 8 bits)
     unsigned* seg_bars;
 };
