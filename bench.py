@@ -557,10 +557,15 @@ def run_ours(args):
     dec_unit = 3 * esize + 0.125
     dec_kernel = "decode_comp (K3+K4)"
     fused = not dec_n and phases.get("fused_round", (0.0, 0))[1] > 0
+    spread = not dec_n and phases.get("spread_round", (0.0, 0))[1] > 0
     if fused:  # small rounds run as one launch (extract + merge + decode per cluster)
         dec_ms_tot, dec_n = phases["fused_round"]
         dec_unit = 5 * esize + 0.25
         dec_kernel = "fused_round (K1+K2+K3/K4, one cluster launch; the re-read of g, c hits L2)"
+    elif spread:  # small rounds run as one launch over every SM (coins + K1 + K2 + K3/K4)
+        dec_ms_tot, dec_n = phases["spread_round"]
+        dec_unit = 5 * esize + 0.25
+        dec_kernel = "spread_round (coins+K1+K2+K3/K4, one launch over every SM; the re-read of g, c hits L2)"
     dec_bytes = ml * D * dec_unit * args.steps   # read g, c; write c'; 1/8 B of bits
     ext_bytes = ml * D * (2 * esize + 0.125) * args.steps  # read g, c; write 1/8 B of bits
     dec_gbs = dec_bytes / (dec_ms_tot * 1e-3) / 1e9 if dec_ms_tot == dec_ms_tot and dec_ms_tot else 0.0

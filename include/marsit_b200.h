@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define MARSIT_B200_ABI_VERSION 2
+#define MARSIT_B200_ABI_VERSION 3
 
 typedef enum marsit_status {
     MARSIT_OK = 0,
@@ -259,9 +259,10 @@ marsit_status marsit_ctx_set_consensus(marsit_ctx* ctx, int enable);
  * Phases: 0 sign_extract, 1 exchange, 2 merge, 3 allgather, 4 decode_comp,
  * 5 export, 6 dense, 7 coins (coin precompute, on the context's side stream,
  * overlapping phase 0), 8 fused_round (small rounds: extract + merge + decode
- * in one cluster launch).  ms[i] accumulates; launches[i] counts kernel
- * launches. */
-#define MARSIT_N_PHASES 9
+ * in one cluster launch per segment), 9 spread_round (small rounds: coins,
+ * extract, merge and decode in one launch over every SM).  ms[i]
+ * accumulates; launches[i] counts kernel launches. */
+#define MARSIT_N_PHASES 10
 marsit_status marsit_ctx_set_timing(marsit_ctx* ctx, int enable);
 marsit_status marsit_ctx_timing(marsit_ctx* ctx, float* ms, uint64_t* launches, int reset);
 

@@ -301,11 +301,24 @@ class Context:
         _check(N.lib().marsit_ctx_set_peers(self._h, arr, len(peers)))
 
     # raw entry points ------------------------------------------------------
+    def _ptrs(self, tensors):
+        """ctypes pointer array of the tensors' device addresses, cached by
+        address (the same buffers are passed every round; building the array
+        is most of a small round's Python enqueue time)."""
+        key = tuple([x.data_ptr() for x in tensors])
+        cache = self.__dict__.setdefault("_ptr_cache", {})
+        arr = cache.get(key)
+        if arr is None:
+            if len(cache) >= 64:
+                cache.clear()
+            arr = cache[key] = N.ptr_array(key)
+        return arr
+
     def sign_round(self, t, eta_s, seed, grads, comp, comp_out=None, agg_bits=None,
                    update=None, stream=None):
-        g = N.ptr_array([x.data_ptr() for x in grads])
-        c = N.ptr_array([x.data_ptr() for x in comp])
-        co = N.ptr_array([x.data_ptr() for x in (comp_out if comp_out is not None else comp)])
+        g = self._ptrs(grads)
+        c = self._ptrs(comp)
+        co = c if comp_out is None else self._ptrs(comp_out)
         _check(N.lib().marsit_sign_round(
             self._h, t, float(eta_s), seed, g, c, co,
             C.c_void_p(agg_bits.data_ptr() if agg_bits is not None else None),

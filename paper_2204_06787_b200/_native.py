@@ -14,9 +14,9 @@ SO_PATH = os.environ.get("MARSIT_SO") or os.path.join(HERE, "libmarsit_b200.so")
 
 # status codes (include/marsit_b200.h)
 OK, EPARAM, ENONFINITE, EPROTOCOL, EUNSUPPORTED, ECUDA, ENCCL = range(7)
-N_PHASES = 9
+N_PHASES = 10
 PHASES = ("sign_extract", "exchange", "merge", "allgather", "decode_comp", "export", "dense",
-          "coins", "fused_round")
+          "coins", "fused_round", "spread_round")
 
 F32, F64 = 0, 1
 

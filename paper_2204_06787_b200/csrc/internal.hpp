@@ -241,6 +241,67 @@ struct MergeRunner {
         return MARSIT_OK;
     }
 
+    // Spread round (round_spread_kernel, 512-thread CTAs, one per SM): the
+    // cluster size whose co-resident clusters give the most CTAs (ties: the
+    // larger cluster), at least one cluster per owned segment; pairs only
+    // when nothing larger fits (C1, measured: csize 4 / 132 CTAs 27.6 us per
+    // round, 2 / 148 CTAs 33.6 us: the merge tile per CTA doubles); the merge
+    // tiles of a cluster as in configure_cluster.  MARSIT_SPREAD_CSIZE forces it.
+    marsit_status configure_spread(int dtype, uint32_t workers, uint32_t* ctas) {
+        if (dp.n_merges > kSpreadMaxMerges) return fail(MARSIT_EUNSUPPORTED, "spread round: too many merges");
+        seg_per_launch = n_seg;
+        n_parts = 1;
+        grid = false;
+        const uint32_t total_groups = words_proc / 4;
+        const uint32_t nl = dp.level_width;
+        const int forced = env_int("MARSIT_SPREAD_CSIZE", 0);
+        uint32_t best = 0;
+        for (uint32_t cs : {16u, 8u, 4u, 2u}) {
+            if (forced && cs != uint32_t(forced)) continue;
+            const uint32_t tg = uint32_t(ceil_div(total_groups, cs));
+            uint32_t ns = 0;
+            for (uint32_t c : {1u, 2u, 4u})
+                if (uint64_t(c) * kFusedThreads >= tg) {
+                    ns = c;
+                    break;
+                }
+            if (!ns) continue;
+            const size_t cap = 200 * 1024;
+            // the cluster's leaf tiles + its aggregate tile, then the slots
+            const size_t base_sm = size_t(dp.max_slots + workers + 1) * tg * 16;
+            const size_t stage_sm = size_t(2) * nl * tg * 16;
+            const size_t mask_sm = size_t(4) * nl * tg * 16;
+            if (base_sm > cap) continue;
+            const uint32_t stg = base_sm + stage_sm <= cap && env_int("MARSIT_MERGE_STAGE", 1) ? 1u : 0u;
+            const uint32_t msk =
+                stg && base_sm + stage_sm + mask_sm <= cap && env_int("MARSIT_MERGE_MASKS", 1) ? 1u : 0u;
+            const size_t sm = std::max<size_t>(base_sm + (stg ? stage_sm : 0) + (msk ? mask_sm : 0), 16);
+            int occ = 0;
+            const cudaError_t oe = dtype == 1 ? round_spread_occupancy<double>(int(ns), int(nl), cs, sm, &occ)
+                                              : round_spread_occupancy<float>(int(ns), int(nl), cs, sm, &occ);
+            if (oe != cudaSuccess || occ <= 0 || uint32_t(occ) < n_seg) {
+                cudaGetLastError();
+                continue;
+            }
+            if (env_int("MARSIT_MERGE_DEBUG", 0))
+                fprintf(stderr, "spread: csize %u clusters %d groups/CTA %u nsub %u stage %u masks %u\n", cs, occ,
+                        tg, ns, stg, msk);
+            if (cs == 2 && best) continue;
+            if (uint32_t(occ) * cs > best) {
+                best = uint32_t(occ) * cs;
+                csize = cs;
+                tile_groups = tg;
+                nsub = ns;
+                smem = merge_smem = sm;
+                stage = stg;
+                masks = msk;
+            }
+        }
+        if (!best) return fail(MARSIT_EUNSUPPORTED, "spread round does not fit the device");
+        *ctas = best;
+        return MARSIT_OK;
+    }
+
     // Grid mode: every SM hosts one 1024-thread CTA; the segments of a
     // launch share the SMs evenly (csize tiles each); the smallest groups per
     // thread that cover a tile; r / d staging when the shared memory allows.
@@ -587,6 +648,19 @@ struct marsit_ctx {
     uint32_t words64 = 0, words_proc = 0, wst = 0;
     int sm_count = 148;
     bool fused = false;  // small rounds: one round_cluster_kernel launch (runtime.cu fused_round)
+    // small rounds over every SM: one round_spread_kernel launch (runtime.cu
+    // spread_round); preferred to `fused` when it configures
+    bool spread = false;
+    bool spread_coop = true;           // launched with the cooperative attribute while it is accepted
+    uint32_t spread_ctas = 0;          // CTAs of the launch (co-resident clusters x csize)
+    // spread round: TMEM columns per thread for the parked u (0: the decode
+    // re-reads g, c) and the allocation per CTA
+    uint32_t stash_cols = 0, tmem_cols = 0;
+    unsigned* spread_sync = nullptr;   // [2 + S]: arrivals, generation, per-segment merged flags
+    uint32_t* spread_coins[2] = {nullptr, nullptr};  // coin buffers by round parity (SpreadParams)
+    uint32_t* spread_valid[2] = {nullptr, nullptr};
+    unsigned long long* spread_tag = nullptr;        // [2][2] (seed, round) per buffer
+    unsigned long long* spread_cend = nullptr;       // [2][n_merges] stream ends by round parity
     // K1/K4 task order (StreamParams::reverse); MARSIT_L2_REUSE=0 disables
     bool l2_reuse = marsit_b200::env_int("MARSIT_L2_REUSE", 1) != 0;
     uint32_t task_dir = 0;

@@ -645,7 +645,7 @@ __device__ __forceinline__ void load_words(const uint32_t* p, uint32_t (&v)[WPT]
 
 #if defined(MARSIT_COOP_PROF) || defined(MARSIT_FUSED_PROF)
 }  // namespace
-__device__ unsigned long long g_coop_prof[8];
+__device__ unsigned long long g_coop_prof[16];
 namespace {
 __device__ __forceinline__ uint64_t gtime_ns() {
     uint64_t t;
@@ -1016,7 +1016,7 @@ __device__ __forceinline__ void cluster_merge_prologue(const ClusterParams& p,
         const DevMerge m = p.merges[mb + i];
         sh.m[i] = m;
         sh.tot[i] = 0;
-        sh.valid[i] = p.coin_valid ? p.coin_valid[mb + i] : 0u;
+        sh.valid[i] = p.coin_valid ? (p.coherent ? __ldcg(p.coin_valid + mb + i) : p.coin_valid[mb + i]) : 0u;
         // leaf rows resolved once (P2P: the source rank's buffer, over NVLink)
 #pragma unroll
         for (int o = 0; o < 2; ++o) {
@@ -1057,11 +1057,12 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
     const uint32_t n_here = total_groups > g_first ? min(p.tile_groups, total_groups - g_first) : 0u;
     const uint64_t full_groups = p.seg_bits / 128;  // groups whose 128 bits are all < L
     const bool peer = p.peer_bits != nullptr;
+    const bool cg = peer || p.coherent;  // operands written by another SM of this launch / a peer
     uint4* const stage = cl_slots + size_t(p.n_slots) * p.tile_groups;  // valid when p.stage
     auto load_src = [&](uint32_t k, int o, uint32_t gl) -> uint4 {
         const uint4* row = sh.row[k][o];
         if (SMEM_LEAVES && row) return row[gl];
-        if (row) return peer ? __ldcg(row + gl) : __ldg(row + gl);
+        if (row) return cg ? __ldcg(row + gl) : __ldg(row + gl);
         const uint16_t src = o ? sh.m[k].local_src : sh.m[k].recv_src;
         return cl_slots[size_t(src & 0x3FFFu) * p.tile_groups + gl];
     };
@@ -1086,7 +1087,7 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
     // the next level's local leaf tiles into L1 while this level finishes
     // (p.prefetch = where: 1 after the masks, 2 before them, 3 after the totals)
     auto prefetch_next = [&](uint32_t v, uint32_t where) {
-        if (SMEM_LEAVES || peer || v + 1 >= nlv || p.prefetch != where) return;
+        if (SMEM_LEAVES || cg || v + 1 >= nlv || p.prefetch != where) return;
         const uint32_t k1 = sh.lvl[v + 1], nk1 = sh.lvl[v + 2] - k1;
 #pragma unroll
         for (int i = 0; i < NL; ++i)
@@ -1312,7 +1313,7 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
                     if (fast[h]) {
                         const uint32_t* c = cw + (n0[h] >> 5);
 #pragma unroll
-                        for (int q = 0; q < 5; ++q) win[h][q] = __ldg(c + q);
+                        for (int q = 0; q < 5; ++q) win[h][q] = p.coherent ? __ldcg(c + q) : __ldg(c + q);
                     }
                 }
 #pragma unroll
@@ -1412,6 +1413,56 @@ __global__ void __launch_bounds__(kClusterThreads, 1) merge_grid_kernel(const Cl
 // nibbles of a word meet by OR-shuffles over 8 lanes (as in K1), and the
 // decode reads the group's aggregate words from shared memory.
 // ---------------------------------------------------------------------------
+// Tensor memory as a thread-private parking area (tcgen05.st / tcgen05.ld,
+// 32x32b shape: thread i of the warp addresses TMEM lane base_lane + i).
+__device__ __forceinline__ void tmem_put(uint32_t ta, const float (&u)[4]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ta),
+                 "r"(__float_as_uint(u[0])), "r"(__float_as_uint(u[1])), "r"(__float_as_uint(u[2])),
+                 "r"(__float_as_uint(u[3]))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_put(uint32_t ta, const double (&u)[4]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(ta),
+                 "r"(__double2loint(u[0])), "r"(__double2hiint(u[0])), "r"(__double2loint(u[1])),
+                 "r"(__double2hiint(u[1])), "r"(__double2loint(u[2])), "r"(__double2hiint(u[2])),
+                 "r"(__double2loint(u[3])), "r"(__double2hiint(u[3]))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_get(uint32_t ta, float (&u)[4]) {
+    uint32_t a, b, c, d;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                 : "r"(ta)
+                 : "memory");
+    u[0] = __uint_as_float(a), u[1] = __uint_as_float(b), u[2] = __uint_as_float(c), u[3] = __uint_as_float(d);
+}
+__device__ __forceinline__ void tmem_get(uint32_t ta, double (&u)[4]) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(ta)
+                 : "memory");
+#pragma unroll
+    for (int k = 0; k < 4; ++k) u[k] = __hiloint2double(int(r[2 * k + 1]), int(r[2 * k]));
+}
+__device__ __forceinline__ void tmem_alloc(uint32_t* smem_addr, uint32_t cols) {  // one warp
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     uint32_t(__cvta_generic_to_shared(smem_addr))),
+                 "r"(cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+// every thread: after its last TMEM access; warp 0 frees the allocation
+__device__ __forceinline__ void tmem_release(uint32_t addr, uint32_t cols) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if ((threadIdx.x >> 5) == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(addr), "r"(cols) : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 template <typename T>
 __device__ __forceinline__ bool quad_real(uint64_t j, uint64_t seg_len, uint64_t gi, uint64_t dim) {
     return j + 3 < seg_len && gi + 3 < dim;
@@ -1568,59 +1619,454 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 // coins up to E + E/16 + 4096 (capped by its buffer capacity); without a
 // history (E = ~0), coin_default words.  The merge draws anything beyond
 // coin_valid inline, so the budget changes the work, never the bits.
+// Words of merge m's stream computed this round (and the chunks of 64 words
+// that cover them), from the draw index its stream ended at last round.
+__device__ __forceinline__ uint32_t coin_budget(const DevMerge& m, uint64_t e, uint32_t* chunks) {
+    uint64_t want = m.coin_default;
+    if (e != ~0ull) want = (e + e / 16 + 4096 + 31) / 32;
+    const uint32_t words = uint32_t(want < m.coin_words ? want : m.coin_words);
+    *chunks = (words + 63) / 64;  // 64 words = 2048 draws per chunk
+    return *chunks * 64 < m.coin_words ? *chunks * 64 : m.coin_words;
+}
+
+// One warp: coin chunk c (words 64c .. 64c + 63) of the stream with key `key`.
+__device__ __forceinline__ void coin_chunk(uint64_t key, uint64_t th, uint32_t* out, uint32_t c, int lane) {
+    // lane l builds words l and l + 32 of the chunk bit by bit (two
+    // independent draw streams for ILP), then both are stored coalesced
+    uint64_t za = key + (uint64_t(c) * 2048 + uint64_t(lane) * 32 + 1) * kGamma;
+    uint64_t zb = za + 1024 * kGamma;
+    // the high word decides unless it equals th's (probability 2^-32 per
+    // draw): ties only raise a flag, and a word that saw one is redrawn
+    // with the full compare (no per-draw branch)
+    const uint32_t thh = uint32_t(th >> 32);
+    const uint64_t za0 = za, zb0 = zb;
+    uint32_t wa = 0, wb = 0;
+    bool tie = false;
+#pragma unroll 8
+    for (int i = 0; i < 32; ++i) {
+        const uint32_t xa = mix64_hi(za), xb = mix64_hi(zb);
+        wa |= uint32_t(xa < thh) << i;
+        wb |= uint32_t(xb < thh) << i;
+        tie |= (xa == thh) | (xb == thh);
+        za += kGamma;
+        zb += kGamma;
+    }
+    if (tie) {
+        za = za0;
+        zb = zb0;
+        wa = wb = 0;
+        for (int i = 0; i < 32; ++i) {
+            if (mix64(za) < th) wa |= 1u << i;
+            if (mix64(zb) < th) wb |= 1u << i;
+            za += kGamma;
+            zb += kGamma;
+        }
+    }
+    __stcg(out + uint64_t(c) * 64 + lane, wa);
+    __stcg(out + uint64_t(c) * 64 + 32 + lane, wb);
+}
+
 __global__ void __launch_bounds__(256) coins_kernel(const DevMerge* __restrict__ merges,
                                                     uint64_t seed, uint64_t round,
                                                     const uint64_t* __restrict__ coin_end,
                                                     uint32_t* __restrict__ coin_valid,
                                                     uint32_t* __restrict__ coins) {
     const DevMerge m = merges[blockIdx.y];
-    uint64_t want = m.coin_default;
-    const uint64_t e = coin_end ? coin_end[blockIdx.y] : ~0ull;
-    if (e != ~0ull) want = (e + e / 16 + 4096 + 31) / 32;
-    const uint32_t words = uint32_t(want < m.coin_words ? want : m.coin_words);
-    const uint32_t chunks = (words + 63) / 64;  // 64 words = 2048 draws per chunk
-    if (blockIdx.x == 0 && threadIdx.x == 0)
-        coin_valid[blockIdx.y] = chunks * 64 < m.coin_words ? chunks * 64 : m.coin_words;
+    uint32_t chunks;
+    const uint32_t valid = coin_budget(m, coin_end ? coin_end[blockIdx.y] : ~0ull, &chunks);
+    if (blockIdx.x == 0 && threadIdx.x == 0) coin_valid[blockIdx.y] = valid;
     if (chunks == 0) return;
     const int lane = threadIdx.x & 31;
     const uint64_t key = m.key_mode ? m.key : stream_key(seed, 5, m.receiver, round, m.segment);
-    const uint64_t th = m.thresh11;
     uint32_t* out = coins + m.coin_off;
-    for (uint32_t c = blockIdx.x * 8 + (threadIdx.x >> 5); c < chunks; c += gridDim.x * 8) {
-        // lane l builds words l and l + 32 of the chunk bit by bit (two
-        // independent draw streams for ILP), then both are stored coalesced
-        uint64_t za = key + (uint64_t(c) * 2048 + uint64_t(lane) * 32 + 1) * kGamma;
-        uint64_t zb = za + 1024 * kGamma;
-        // the high word decides unless it equals th's (probability 2^-32 per
-        // draw): ties only raise a flag, and a word that saw one is redrawn
-        // with the full compare (no per-draw branch)
-        const uint32_t thh = uint32_t(th >> 32);
-        const uint64_t za0 = za, zb0 = zb;
-        uint32_t wa = 0, wb = 0;
+    for (uint32_t c = blockIdx.x * 8 + (threadIdx.x >> 5); c < chunks; c += gridDim.x * 8)
+        coin_chunk(key, m.thresh11, out, c, lane);
+}
+
+// ---------------------------------------------------------------------------
+// Spread small round (see SpreadParams): one launch, every SM streaming.
+// A CTA owns groups [g_lo, g_hi) of the flattened (segment, group) space; a
+// warp task is one worker's 128 coordinates of one group (lane l: quad l of g
+// and of c), exactly as in the fused round.  Segment s is merged by cluster s.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+
+// The coins of round `round` into buffer cb, by CTAs [0, nctas) of the
+// caller's choosing (cta = this CTA's index among them): warp 0 sizes every
+// stream's chunks from the stream ends of the previous launch (lane-parallel loads,
+// one scan per 32 streams), then the 32-word chunks go round robin over the
+// CTAs first, one coin word per lane (short per-warp latency chains).
+template <typename T>
+__device__ __forceinline__ void spread_coins(const ClusterParams& p, const SpreadParams<T>& s, uint32_t* s_cbase,
+                                             uint32_t cb, uint64_t round, uint32_t cta, uint32_t nctas) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr uint32_t NWARP = kFusedThreads / 32;
+    // budgets from the stream ends of the launch before this one (cend of the
+    // other parity than p.round's, which this launch's merges are writing):
+    // stable for the whole launch, so every CTA sizes the same chunks
+    const unsigned long long* cend = s.cend + size_t((p.round & 1) ^ 1) * s.n_merges;
+    __syncthreads();  // s_cbase may still be read by an earlier call
+    if (wid == 0) {
+        uint32_t run = 0;
+        for (uint32_t k0 = 0; k0 < s.n_merges; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            uint32_t words = 0;
+            if (k < s.n_merges) {
+                uint32_t chunks;  // of 64 words: the budget rule of the coin kernel
+                const uint32_t valid = coin_budget(p.merges[k], __ldcg(cend + k), &chunks);
+                if (cta == 0) s.coin_valid[cb][k] = valid;
+                words = chunks * 64;
+            }
+            const uint32_t units = words / 32;
+            uint32_t incl = units;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (k < s.n_merges) s_cbase[k] = run + incl - units;
+            run += __shfl_sync(kFull, incl, 31);
+        }
+        if (lane == 0) s_cbase[s.n_merges] = run;
+    }
+    __syncthreads();
+    const uint32_t nw = nctas * NWARP, total = s_cbase[s.n_merges];
+    for (uint32_t i = wid * nctas + cta; i < total; i += nw) {
+        uint32_t lo = 0, hi = s.n_merges;  // stream k with s_cbase[k] <= i < s_cbase[k + 1]
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (s_cbase[mid] <= i) lo = mid; else hi = mid;
+        }
+        const DevMerge& m = p.merges[lo];
+        const uint64_t key = m.key_mode ? m.key : stream_key(p.seed, 5, m.receiver, round, m.segment);
+        const uint32_t word = (i - s_cbase[lo]) * 32 + lane;
+        uint64_t z = key + (uint64_t(word) * 32 + 1) * kGamma;
+        const uint32_t thh = uint32_t(m.thresh11 >> 32);
+        uint32_t wv = 0;
         bool tie = false;
 #pragma unroll 8
-        for (int i = 0; i < 32; ++i) {
-            const uint32_t xa = mix64_hi(za), xb = mix64_hi(zb);
-            wa |= uint32_t(xa < thh) << i;
-            wb |= uint32_t(xb < thh) << i;
-            tie |= (xa == thh) | (xb == thh);
-            za += kGamma;
-            zb += kGamma;
+        for (int b = 0; b < 32; ++b) {
+            const uint32_t x = mix64_hi(z);
+            wv |= uint32_t(x < thh) << b;
+            tie |= x == thh;
+            z += kGamma;
         }
-        if (tie) {
-            za = za0;
-            zb = zb0;
-            wa = wb = 0;
-            for (int i = 0; i < 32; ++i) {
-                if (mix64(za) < th) wa |= 1u << i;
-                if (mix64(zb) < th) wb |= 1u << i;
-                za += kGamma;
-                zb += kGamma;
+        if (tie) {  // the full compare for the word that saw a high-word tie
+            z = key + (uint64_t(word) * 32 + 1) * kGamma;
+            wv = 0;
+            for (int b = 0; b < 32; ++b, z += kGamma)
+                if (mix64(z) < m.thresh11) wv |= 1u << b;
+        }
+        __stcg(s.coins[cb] + m.coin_off + word, wv);
+    }
+}
+
+template <typename T, int NSUB, int NL>
+__global__ void __launch_bounds__(kFusedThreads, 1)
+    round_spread_kernel(const ClusterParams p, const SpreadParams<T> s) {
+#ifdef MARSIT_FUSED_PROF
+    const uint64_t fp_t0 = threadIdx.x == 0 ? gtime_ns() : 0;
+#endif
+    extern __shared__ uint4 sp_dyn[];  // merge clusters: [workers][tg] leaves, [tg] aggregate, slots / staging
+    __shared__ ClusterMergeShared<NSUB, NL, kFusedThreads> sh;
+    __shared__ unsigned s_gen;
+    const FusedParams<T>& f = s.f;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr uint32_t NWARP = kFusedThreads / 32;
+    // the generation before this CTA arrives (it cannot advance without us)
+    if (tid == 0) s_gen = ld_acquire_u32(s.sync + 1);
+    const uint32_t gps = p.words_proc / 4;  // groups per segment
+    const uint64_t total = uint64_t(p.n_seg) * gps;
+    const uint32_t g_lo = uint32_t(total * blockIdx.x / gridDim.x);
+    const uint32_t g_hi = uint32_t(total * (blockIdx.x + 1) / gridDim.x);
+    // this round's coins: computed here only when the buffer's tag misses
+    const uint32_t cb = uint32_t(p.round & 1);
+    __shared__ uint32_t s_cbase[kSpreadMaxMerges + 1];
+    __shared__ int s_hit;
+    __shared__ uint32_t s_tmem;
+    if (tid == 0) {
+        const unsigned long long* tg = s.tag + 2 * cb;
+        s_hit = __ldcg(tg) == p.seed && __ldcg(tg + 1) == p.round;
+    }
+    const bool stash = f.stash_cols != 0;
+    if (stash && wid == 0) tmem_alloc(&s_tmem, f.tmem_cols);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // this thread's parking area: lane quadrant wid % 4, column block wid / 4
+    const uint32_t tbase = stash ? s_tmem + ((uint32_t(wid & 3) * 32) << 16) + uint32_t(wid >> 2) * f.stash_cols : 0u;
+    constexpr uint32_t QCOLS = sizeof(T);  // TMEM columns (32-bit) per quad of u
+    // the merge clusters stage their descriptors under the extract
+    const uint32_t cl = blockIdx.x / p.csize;
+    if (cl < p.n_seg) cluster_merge_prologue<NSUB, NL, true, false, kFusedThreads>(p, sh, sp_dyn);
+    if (!s_hit && s.n_merges)
+        spread_coins(p, s, s_cbase, cb, p.round, blockIdx.x, gridDim.x);
+#ifdef MARSIT_FUSED_PROF
+    const bool prof = tid == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1);
+    const int ps = blockIdx.x == 0 ? 8 : 12;  // slots 8..11: CTA 0, 12..15: the last CTA
+    const uint64_t fp_tc = prof ? gtime_ns() : 0;
+    if (prof) atomicAdd(&g_coop_prof[ps], (unsigned long long)(fp_tc - fp_t0));  // coins
+#endif
+    constexpr int B = sizeof(T) == 4 ? 4 : 2;  // groups per warp step
+    // K1: u = g + c, sign nibbles -> packed words of leaf (segment, worker)
+    T fin = T(0);
+    // The warp's tasks in order: t = (w * iters + it) * B + b is group
+    // g_lo + wid + (it * B + b) * NWARP of worker w (also the TMEM column
+    // order); B tasks' quads of g and c in flight per step.
+    const uint32_t iters = g_hi > g_lo + wid ? (g_hi - g_lo - wid + NWARP * B - 1) / (NWARP * B) : 0u;
+    uint32_t t0 = 0;
+    for (uint32_t w = 0; w < f.workers; ++w) {
+        const T* __restrict__ gw = f.g[w];
+        const T* __restrict__ cw = f.c[w];
+        for (uint32_t g0 = g_lo + wid; g0 < g_hi; g0 += NWARP * B, t0 += B) {
+            Quad<T> gv[B], cv[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const uint32_t gg = g0 + b * NWARP;
+                const uint32_t sl = gg / gps;
+                const uint64_t j = uint64_t(gg - sl * gps) * 128 + lane * 4;
+                const uint64_t gi = uint64_t(sl) * p.seg_bits + j;
+                if (gg < g_hi && quad_real<T>(j, p.seg_bits, gi, f.dim)) {
+                    gv[b] = load4(gw + gi);
+                    cv[b] = load4(cw + gi);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const bool in = gg < g_hi && j + k < p.seg_bits && gi + k < f.dim;
+                        gv[b].v[k] = in ? gw[gi + k] : T(0);
+                        cv[b].v[k] = in ? cw[gi + k] : T(0);
+                    }
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const uint32_t gg = g0 + b * NWARP;
+                if (gg >= g_hi) break;
+                const uint32_t sl = gg / gps, gl = gg - sl * gps;
+                const uint64_t j = uint64_t(gl) * 128 + lane * 4;
+                T u[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    u[k] = add_rn(add_rn(gv[b].v[k], cv[b].v[k]), T(0));  // -0.0 -> +0.0 (sign_vector.hpp:70)
+                    fin = fma_rn(u[k], T(0), fin);
+                }
+                if (stash) tmem_put(tbase + (t0 + b) * QCOLS, u);  // warp-uniform
+                uint32_t nib = sign_nibble(u[0], u[1], u[2], u[3]);
+                const uint64_t valid = j >= p.seg_bits ? 0 : p.seg_bits - j;  // storage padding -> 0
+                if (valid < 4) nib &= (1u << valid) - 1u;
+                uint32_t v = nib << ((lane & 7) * 4);
+                v |= __shfl_xor_sync(kFull, v, 1);
+                v |= __shfl_xor_sync(kFull, v, 2);
+                v |= __shfl_xor_sync(kFull, v, 4);
+                if ((lane & 7) == 0)
+                    const_cast<uint32_t*>(p.leaves)[(uint64_t(sl) * p.ml + w) * p.wst + uint64_t(gl) * 4 + (lane >> 3)] = v;
             }
         }
-        __stcg(out + uint64_t(c) * 64 + lane, wa);
-        __stcg(out + uint64_t(c) * 64 + 32 + lane, wb);
     }
+    if (__any_sync(kFull, !(fin == fin)) && lane == 0) atomicOr(f.err, 1);
+    if (stash) tmem_wait_st();
+    // arrive: the last CTA resets the count and advances the generation
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(s.sync, 1u) == gridDim.x - 1) {
+            s.sync[0] = 0;
+            __threadfence();
+            atomicAdd(s.sync + 1, 1u);
+        }
+    }
+    const unsigned gen = s_gen + 1;
+#ifdef MARSIT_FUSED_PROF
+    const uint64_t fp_t1 = threadIdx.x == 0 ? gtime_ns() : 0;
+#endif
+    // K2: cluster cl < n_seg merges segment cl once every CTA has arrived;
+    // meanwhile the other CTAs compute the next round's coins
+    const uint32_t n_merge_ctas = p.n_seg * p.csize;
+    if (cl >= p.n_seg && s.n_merges && gridDim.x > n_merge_ctas) {
+        spread_coins(p, s, s_cbase, cb ^ 1u, p.round + 1, blockIdx.x - n_merge_ctas, gridDim.x - n_merge_ctas);
+        if (blockIdx.x == n_merge_ctas && tid == 0) {  // read by the next launch only
+            s.tag[2 * (cb ^ 1u)] = p.seed;
+            s.tag[2 * (cb ^ 1u) + 1] = p.round + 1;
+        }
+    }
+    if (cl < p.n_seg) {
+        if (tid == 0) {
+            while (ld_acquire_u32(s.sync + 1) != gen) __nanosleep(20);
+            // every CTA has read the tag: buffer cb now holds this round's
+            // coins (computed above on a miss), tagged for later rounds
+            if (blockIdx.x == 0 && s.n_merges) {
+                s.tag[2 * cb] = p.seed;
+                s.tag[2 * cb + 1] = p.round;
+            }
+        }
+#ifdef MARSIT_FUSED_PROF
+        if (prof) atomicAdd(&g_coop_prof[ps + 1], (unsigned long long)(gtime_ns() - fp_t1));  // wait: all arrived
+#endif
+        __syncthreads();
+        // the coin words computed for this round's merges: written in this
+        // launch on a tag miss, so read only now (the prologue ran earlier)
+        {
+            const uint32_t mb = p.seg_begin[cl], nm = p.seg_begin[cl + 1] - mb;
+            for (uint32_t i = tid; i < nm; i += kFusedThreads)
+                sh.valid[i] = p.coin_valid ? __ldcg(p.coin_valid + mb + i) : 0u;
+        }
+        // the cluster's tiles of the segment's leaves into shared memory (one
+        // L2 round trip: every load of a thread in flight at once)
+        const uint32_t tg = p.tile_groups, g_first = cluster_ctarank() * tg;
+        const uint32_t n_here = gps > g_first ? min(tg, gps - g_first) : 0u;
+        uint4* const leaf = sp_dyn;
+        for (uint32_t w = 0; w < f.workers; ++w) {
+            const uint4* src = reinterpret_cast<const uint4*>(p.leaves + (uint64_t(cl) * p.ml + w) * p.wst) + g_first;
+            for (uint32_t gl = tid; gl < n_here; gl += kFusedThreads) leaf[size_t(w) * tg + gl] = __ldcg(src + gl);
+        }
+        cluster_sync_all();  // staged leaves and descriptors complete; the cluster runs
+        cluster_merge_levels<NSUB, NL, true, false, kFusedThreads>(p, sh, leaf + size_t(f.workers + 1) * tg, leaf,
+                                                                    leaf + size_t(f.workers) * tg);
+        __syncthreads();
+        if (tid == 0) __threadfence();
+        cluster_sync_all();  // the segment's aggregate tiles are all written
+        if (tid == 0 && cluster_ctarank() == 0) st_release_u32(s.sync + 2 + cl, gen);
+    }
+#ifdef MARSIT_FUSED_PROF
+    const uint64_t fp_t2 = threadIdx.x == 0 ? gtime_ns() : 0;
+#endif
+    // K3/K4 of this CTA's slice once its segments' aggregates are published
+    if (g_lo < g_hi) {
+        if (tid == 0)
+            for (uint32_t sl = g_lo / gps; sl <= (g_hi - 1) / gps; ++sl)
+                while (ld_acquire_u32(s.sync + 2 + sl) != gen) __nanosleep(20);
+#ifdef MARSIT_FUSED_PROF
+        if (prof) atomicAdd(&g_coop_prof[ps + 2], (unsigned long long)(gtime_ns() - fp_t2));  // wait: aggregates
+#endif
+        __syncthreads();
+    }
+    if (stash) {
+        // K3/K4 from the parked u: c' = u - g_t (u's -0.0 was folded to +0.0,
+        // which leaves u - g_t unchanged since g_t != 0)
+        // the extract parked task (w * iters + it) * B + b at column task * QCOLS
+        uint32_t it = 0;
+        for (uint32_t g0 = g_lo + wid; g0 < g_hi; g0 += NWARP * B, ++it) {
+            uint32_t word[B];  // the groups' aggregate words, once for every worker
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const uint32_t gg = g0 + b * NWARP;
+                if (gg >= g_hi) break;
+                const uint32_t sl = gg / gps, gl = gg - sl * gps;
+                word[b] = __ldcg(p.agg + uint64_t(p.s_first + sl) * p.agg_stride + uint64_t(gl) * 4 + (lane >> 3));
+            }
+            for (uint32_t w = 0; w < f.workers; ++w) {
+                T* co = f.c_out[w];
+                T* upd = w == 0 ? f.update : nullptr;
+                const uint32_t colw = (w * iters + it) * B * QCOLS;
+                T u[B][4];
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    if (g0 + b * NWARP >= g_hi) break;
+                    tmem_get(tbase + colw + b * QCOLS, u[b]);
+                }
+                tmem_wait_ld();
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    const uint32_t gg = g0 + b * NWARP;
+                    if (gg >= g_hi) break;
+                    const uint32_t sl = gg / gps;
+                    const uint64_t j = uint64_t(gg - sl * gps) * 128 + lane * 4;
+                    const uint64_t gi = uint64_t(sl) * p.seg_bits + j;
+                    const uint32_t nib = (word[b] >> ((lane & 7) * 4)) & 0xFu;
+                    Quad<T> out, up;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        up.v[k] = ((nib >> k) & 1u) ? f.eta : -f.eta;
+                        out.v[k] = sub_rn(u[b][k], up.v[k]);
+                    }
+                    if (quad_real<T>(j, p.seg_bits, gi, f.dim)) {
+                        store4(co + gi, out);
+                        if (upd) store4(upd + gi, up);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (j + k < p.seg_bits && gi + k < f.dim) {
+                                co[gi + k] = out.v[k];
+                                if (upd) upd[gi + k] = up.v[k];
+                            }
+                    }
+                }
+            }
+        }
+    }
+    for (uint32_t w = 0; w < (stash ? 0u : f.workers); ++w) {
+        const T* __restrict__ gw = f.g[w];
+        const T* cw = f.c[w];  // may alias c_out (in place)
+        T* co = f.c_out[w];
+        T* upd = w == 0 ? f.update : nullptr;
+        for (uint32_t g0 = g_lo + wid; g0 < g_hi; g0 += NWARP * B) {
+            Quad<T> gv[B], cv[B];
+            uint32_t word[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const uint32_t gg = g0 + b * NWARP;
+                const uint32_t sl = gg / gps, gl = gg - sl * gps;
+                const uint64_t j = uint64_t(gl) * 128 + lane * 4;
+                const uint64_t gi = uint64_t(sl) * p.seg_bits + j;
+                word[b] = 0;
+                if (gg < g_hi) {
+                    word[b] = __ldcg(p.agg + uint64_t(p.s_first + sl) * p.agg_stride + uint64_t(gl) * 4 + (lane >> 3));
+                    if (quad_real<T>(j, p.seg_bits, gi, f.dim)) {
+                        gv[b] = load4(gw + gi);
+                        cv[b] = load4_rw(cw + gi);
+                    }
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const uint32_t gg = g0 + b * NWARP;
+                if (gg >= g_hi) break;
+                const uint32_t sl = gg / gps;
+                const uint64_t j = uint64_t(gg - sl * gps) * 128 + lane * 4;
+                const uint64_t gi = uint64_t(sl) * p.seg_bits + j;
+                const uint32_t nib = (word[b] >> ((lane & 7) * 4)) & 0xFu;
+                if (quad_real<T>(j, p.seg_bits, gi, f.dim)) {
+                    Quad<T> out, up;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const T gt = ((nib >> k) & 1u) ? f.eta : -f.eta;
+                        out.v[k] = sub_rn(add_rn(gv[b].v[k], cv[b].v[k]), gt);
+                        up.v[k] = gt;
+                    }
+                    store4(co + gi, out);
+                    if (upd) store4(upd + gi, up);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (j + k < p.seg_bits && gi + k < f.dim) {
+                            const T gt = ((nib >> k) & 1u) ? f.eta : -f.eta;
+                            co[gi + k] = sub_rn(add_rn(gw[gi + k], cw[gi + k]), gt);
+                            if (upd) upd[gi + k] = gt;
+                        }
+                }
+            }
+        }
+    }
+    if (stash) tmem_release(s_tmem, f.tmem_cols);
+#ifdef MARSIT_FUSED_PROF
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const uint64_t fp_t3 = gtime_ns();
+        atomicAdd(&g_coop_prof[0], (unsigned long long)(fp_t1 - fp_t0));
+        atomicAdd(&g_coop_prof[1], (unsigned long long)(fp_t2 - fp_t1));
+        atomicAdd(&g_coop_prof[2], (unsigned long long)(fp_t3 - fp_t2));
+        atomicAdd(&g_coop_prof[3], 1ull);
+    }
+    if (prof && blockIdx.x == gridDim.x - 1)
+        atomicAdd(&g_coop_prof[ps + 3], (unsigned long long)(gtime_ns() - fp_t0));  // last CTA: whole launch
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -2254,6 +2700,72 @@ cudaError_t round_cluster_occupancy(int nsub, int nl, uint32_t csize, size_t sme
     MARSIT_FUSED_DISPATCH(fused_occ_t, csize, smem, clusters)
 }
 
+template <typename T, int NSUB, int NL>
+static cudaError_t spread_attr() {
+    auto k = round_spread_kernel<T, NSUB, NL>;
+    static cudaError_t e = [&] {
+        cudaError_t r = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncAttributes fa{};
+        if (r == cudaSuccess) r = cudaFuncGetAttributes(&fa, k);
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(232448 - fa.sharedSizeBytes));
+        return r;
+    }();
+    return e;
+}
+
+template <typename T, int NSUB, int NL>
+static cudaError_t spread_launch_t(const ClusterParams& p, const SpreadParams<T>& s, uint32_t ctas,
+                                   size_t smem, bool cooperative, cudaStream_t st) {
+    cudaError_t e = spread_attr<T, NSUB, NL>();
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(kFusedThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = cooperative ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, round_spread_kernel<T, NSUB, NL>, p, s);
+}
+
+template <typename T, int NSUB, int NL>
+static cudaError_t spread_occ_t(uint32_t csize, size_t smem, int* clusters) {
+    cudaError_t e = spread_attr<T, NSUB, NL>();
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(csize);
+    cfg.blockDim = dim3(kFusedThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaOccupancyMaxActiveClusters(clusters, round_spread_kernel<T, NSUB, NL>, &cfg);
+}
+
+template <typename T>
+cudaError_t launch_round_spread(const ClusterParams& p, const SpreadParams<T>& s, int nsub, int nl,
+                                uint32_t ctas, size_t smem, bool cooperative, cudaStream_t st) {
+    MARSIT_FUSED_DISPATCH(spread_launch_t, p, s, ctas, smem, cooperative, st)
+}
+
+template <typename T>
+cudaError_t round_spread_occupancy(int nsub, int nl, uint32_t csize, size_t smem, int* clusters) {
+    MARSIT_FUSED_DISPATCH(spread_occ_t, csize, smem, clusters)
+}
+
 template <int NSUB, int NL>
 static cudaError_t grid_attr() {
     static cudaError_t e = cudaFuncSetAttribute(merge_grid_kernel<NSUB, NL>,
@@ -2582,6 +3094,9 @@ cudaError_t preload_kernels() {
     template cudaError_t launch_round_cluster<T>(const ClusterParams&, const FusedParams<T>&, int,  \
                                                  int, uint32_t, size_t, cudaStream_t);          \
     template cudaError_t round_cluster_occupancy<T>(int, int, uint32_t, size_t, int*);          \
+    template cudaError_t launch_round_spread<T>(const ClusterParams&, const SpreadParams<T>&, int, \
+                                                int, uint32_t, size_t, bool, cudaStream_t);      \
+    template cudaError_t round_spread_occupancy<T>(int, int, uint32_t, size_t, int*);           \
     template cudaError_t launch_dense_leaf<T>(const T* const*, const T* const*, uint32_t,       \
                                               uint64_t, uint64_t, uint32_t, uint32_t, T*, int*,  \
                                               int, cudaStream_t, T* const*);
@@ -2594,7 +3109,7 @@ MARSIT_INSTANTIATE(double)
 extern "C" void marsit_debug_coop_prof(unsigned long long* out, int reset) {
     cudaMemcpyFromSymbol(out, marsit_b200::g_coop_prof, sizeof(marsit_b200::g_coop_prof));
     if (reset) {
-        unsigned long long z[8] = {};
+        unsigned long long z[16] = {};
         cudaMemcpyToSymbol(marsit_b200::g_coop_prof, z, sizeof(z));
     }
 }

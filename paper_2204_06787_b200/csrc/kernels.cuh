@@ -132,6 +132,8 @@ struct ClusterParams {
                                   // (1 after the masks, 2 before them, 3 after the totals)
     uint32_t xch_tag;             // per launch (host counter; the level is the low 8 bits)
     unsigned* seg_bars;
+    uint32_t coherent;            // 1: leaves and coins were written by this launch (spread
+                                  // round): L2-coherent loads, no L1 prefetch
 };
 cudaError_t launch_merge_cluster(const ClusterParams& p, int nsub, int nl, uint32_t clusters,
                                  size_t smem, cudaStream_t st);
@@ -157,12 +159,49 @@ struct FusedParams {
     T eta;
     T* update;   // optional g_t
     int* err;    // non-finite latch
+    // TMEM stash (spread round; 0: off): u = g + c of the CTA's slice is parked in
+    // tensor memory between the extract and the decode, thread-private (warp
+    // w owns lanes 32 (w % 4) .. + 31 and columns (w / 4) * stash_cols ..
+    // + stash_cols), so the decode reads only the aggregate bits; tmem_cols =
+    // the allocation (a power of 2 >= 32)
+    uint32_t stash_cols, tmem_cols;
 };
 template <typename T>
 cudaError_t launch_round_cluster(const ClusterParams& p, const FusedParams<T>& f, int nsub, int nl,
                                  uint32_t clusters, size_t smem, cudaStream_t st);
 template <typename T>
 cudaError_t round_cluster_occupancy(int nsub, int nl, uint32_t csize, size_t smem, int* clusters);
+// Spread small round (one launch, G == 1): the fused round over every SM
+// instead of one cluster per segment.  Each CTA streams an equal slice of the
+// (segment, 128-coordinate group) space: this round's coin chunks, then K1
+// for every worker with the packed signs to global memory (L2); after the
+// last CTA arrives, cluster s < n_seg runs segment s's merge DAG with the
+// cluster level loop (leaves and coins through L2) and publishes it; each CTA
+// then decodes its own slice (K3/K4, the re-read of g and c L2-resident).
+// The synchronisation words are device state only (a self-resetting arrival
+// count + generation), so rounds can be replayed from a CUDA graph.
+constexpr uint32_t kSpreadMaxMerges = 256;  // coin streams per spread round
+// Coins: two buffers b = round & 1, each tagged with the (seed, round) it
+// holds.  Round t uses buffer t & 1 and computes it first only when its tag
+// misses; while the merge clusters run, the other CTAs compute round t + 1's
+// coins into the other buffer and tag it.  The budget of both reads the
+// stream ends the previous launch's merges wrote (cend[(t & 1) ^ 1]; this
+// launch writes cend[t & 1]), so every CTA sizes the same work.
+template <typename T>
+struct SpreadParams {
+    FusedParams<T> f;
+    unsigned* sync;                 // [0] arrivals, [1] generation, [2 + s] segment s merged (generation)
+    uint32_t n_merges;              // coin streams of the round: p.merges[0 .. n_merges)
+    uint32_t* coins[2];             // coin buffers
+    uint32_t* coin_valid[2];        // [n_merges] words computed per buffer
+    unsigned long long* tag;        // [2][2]: (seed, round) each buffer holds, ~0 = none
+    unsigned long long* cend;       // [2][n_merges] stream ends by round parity
+};
+template <typename T>
+cudaError_t launch_round_spread(const ClusterParams& p, const SpreadParams<T>& s, int nsub, int nl,
+                                uint32_t ctas, size_t smem, bool cooperative, cudaStream_t st);
+template <typename T>
+cudaError_t round_spread_occupancy(int nsub, int nl, uint32_t csize, size_t smem, int* clusters);
 // Concurrently resident clusters of csize CTAs with `smem` dynamic bytes (0 if unsupported).
 cudaError_t merge_cluster_occupancy(int nsub, int nl, uint32_t csize, size_t smem, int* clusters);
 // K2g: the same level loop over csize co-resident CTAs per segment (any

@@ -493,7 +493,9 @@ marsit_ctx::~marsit_ctx() {
                     dense_mean, (void*)d_dense_ops, (void*)d_dense_final, (void*)d_metrics,
                     (void*)d_verify,
                     (void*)d_dense_chain, (void*)d_dense_groups,
-                    (void*)flags, (void*)d_peer_tables})
+                    (void*)flags, (void*)d_peer_tables, (void*)spread_sync, (void*)spread_coins[0],
+                    (void*)spread_coins[1], (void*)spread_valid[0], (void*)spread_valid[1],
+                    (void*)spread_tag, (void*)spread_cend})
         if (p) cudaFree(p);
     for (auto& tp : pending) {
         cudaEventDestroy(tp.a);
@@ -546,7 +548,7 @@ marsit_status marsit_ctx::end_phase(int phase, cudaStream_t st, cudaEvent_t a, u
 namespace {
 
 enum Phase { kPhExtract = 0, kPhExchange, kPhMerge, kPhAllgather, kPhDecode, kPhExport, kPhDense,
-             kPhCoins, kPhFused };
+             kPhCoins, kPhFused, kPhSpread };
 
 template <typename T>
 StreamParams<T> stream_params(marsit_ctx* ctx, const void* const* g, const void* const* c,
@@ -1202,6 +1204,60 @@ marsit_status fused_round(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_t se
     return run_export(ctx, d_agg_bits, st);
 }
 
+// Small rounds on one GPU over every SM (ctx->spread): coins, extract, merge
+// and decode in one round_spread_kernel launch, which also computes the next
+// round's coins while the merge clusters run (its own tagged coin buffers);
+// no side stream, no host-side round state (the launch can be graph-captured).
+template <typename T>
+marsit_status spread_round(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_t seed,
+                           const void* const* g, const void* const* c, void* const* c_out,
+                           uint64_t* d_agg_bits, void* d_update, cudaStream_t st) {
+    marsit_status s;
+    NvtxRange range("marsit.spread_round");
+    cudaEvent_t ev;
+    if ((s = ctx->begin_phase(st, &ev))) return s;
+    SpreadParams<T> sp{};
+    for (uint32_t w = 0; w < ctx->M; ++w) {
+        sp.f.g[w] = static_cast<const T*>(g[w]);
+        sp.f.c[w] = static_cast<const T*>(c[w]);
+        sp.f.c_out[w] = static_cast<T*>(c_out[w]);
+    }
+    sp.f.workers = ctx->M;
+    sp.f.dim = ctx->D;
+    sp.f.eta = T(eta_s);
+    sp.f.update = static_cast<T*>(d_update);
+    sp.f.err = ctx->err;
+    sp.sync = ctx->spread_sync;
+    const MergeRunner& mr = ctx->merge;
+    const bool coins = ctx->coin_total_words != 0;
+    const int b = int(t & 1);
+    sp.n_merges = coins ? mr.dp.n_merges : 0;
+    for (int i = 0; i < 2; ++i) {
+        sp.coins[i] = ctx->spread_coins[i];
+        sp.coin_valid[i] = ctx->spread_valid[i];
+    }
+    sp.tag = ctx->spread_tag;
+    sp.cend = ctx->spread_cend;
+    sp.f.stash_cols = ctx->stash_cols;
+    sp.f.tmem_cols = ctx->tmem_cols;
+    ClusterParams p = mr.cluster_params(ctx->bits, ctx->agg, coins ? sp.coins[b] : nullptr, seed, t, 0,
+                                        sp.coin_valid[b]);
+    p.coin_end = reinterpret_cast<uint64_t*>(ctx->spread_cend) + size_t(b) * std::max<uint32_t>(mr.dp.n_merges, 1);
+    p.coherent = 1;
+    const int nsub = int(mr.nsub), nl = int(mr.dp.level_width);
+    cudaError_t e = launch_round_spread<T>(p, sp, nsub, nl, ctx->spread_ctas, mr.smem, ctx->spread_coop, st);
+    if (e != cudaSuccess && ctx->spread_coop) {
+        // cooperative + cluster launch refused: the grid is sized to the
+        // co-resident clusters, so a plain cluster launch keeps every CTA resident
+        cudaGetLastError();
+        ctx->spread_coop = false;
+        e = launch_round_spread<T>(p, sp, nsub, nl, ctx->spread_ctas, mr.smem, false, st);
+    }
+    CUDA_TRY(e);
+    if ((s = ctx->end_phase(kPhSpread, st, ev, 1))) return s;
+    return run_export(ctx, d_agg_bits, st);
+}
+
 bool fused_eligible(const marsit_ctx* ctx, const void* const* g, const void* const* c,
                     void* const* c_out, void* const* params, void* update) {
     return ctx->fused && !ctx->metrics && !params && !ctx->pipeline &&
@@ -1219,6 +1275,10 @@ marsit_status sign_round_impl(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_
         return fail(MARSIT_EUNSUPPORTED, "external-transport context: use marsit_round_phase");
     if (ctx->p2p && !ctx->peers_set) return fail(MARSIT_EPARAM, "P2P transport: call marsit_ctx_set_peers");
     note_round(ctx, t, false);
+    if (ctx->spread && fused_eligible(ctx, d_grads, d_comp, d_comp_out, params, d_update))
+        return ctx->dtype == MARSIT_F32
+                   ? spread_round<float>(ctx, t, eta_s, seed, d_grads, d_comp, d_comp_out, d_agg_bits, d_update, st)
+                   : spread_round<double>(ctx, t, eta_s, seed, d_grads, d_comp, d_comp_out, d_agg_bits, d_update, st);
     if (fused_eligible(ctx, d_grads, d_comp, d_comp_out, params, d_update))
         return ctx->dtype == MARSIT_F32
                    ? fused_round<float>(ctx, t, eta_s, seed, d_grads, d_comp, d_comp_out, d_agg_bits, d_update, st)
@@ -1473,9 +1533,12 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
                  env_int("MARSIT_FUSED", 1) != 0;
     const bool grid_default = mr.grid;
     const bool kernel_forced = std::getenv("MARSIT_MERGE_KERNEL") != nullptr;
+    // ... and preferably spread over every SM (one launch, MARSIT_SPREAD=0
+    // keeps the cluster-per-segment kernel)
+    ctx->spread = ctx->fused && env_int("MARSIT_SPREAD", 1) != 0;
     if (ctx->fused) {
         mr.cluster = true;
-        mr.fused_arrays = hs.workers + 1;
+        mr.fused_arrays = ctx->spread ? 0 : hs.workers + 1;
         mr.fused_dtype = desc->dtype == MARSIT_F64 ? 1 : 0;
     }
     double frac = 0.53;
@@ -1508,7 +1571,17 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
         }
         if ((st = mr.configure(ctx->sm_count, 1, env_int("MARSIT_PIPE_MERGE_CTAS", 1)))) return st;
     } else {
-        st = mr.configure(ctx->sm_count);
+        if (ctx->spread) {
+            st = mr.configure_spread(mr.fused_dtype, hs.workers, &ctx->spread_ctas);
+            if (st) {  // the spread round does not configure: the cluster-per-segment round
+                cudaGetLastError();
+                ctx->spread = false;
+                mr.fused_arrays = hs.workers + 1;
+                st = mr.configure(ctx->sm_count);
+            }
+        } else {
+            st = mr.configure(ctx->sm_count);
+        }
         if (st && ctx->fused) {  // the fused tiles do not fit: the merge kernel alone
             ctx->fused = false;
             mr.fused_arrays = 0;
@@ -1546,6 +1619,40 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
     }
     CUDA_TRY(cudaMalloc(&ctx->err, sizeof(int)));
     CUDA_TRY(cudaMemset(ctx->err, 0, sizeof(int)));
+    // TMEM stash of the spread round: a thread parks one quad of u per
+    // (worker, step, group of the step) — 4 groups per step in fp32, 2 in
+    // fp64 — in 4 (8) columns; a warp's quarter of the 512 columns is 128
+    // per thread (MARSIT_STASH=0 disables).  C1: 30.8 -> 29.2 us per round.
+    // (The cluster-per-segment round measured slower with it, 28.8 -> 30.9
+    // us, and does not use it.)
+    if (ctx->spread) {
+        const uint64_t groups = ceil_div(uint64_t(ctx->S) * (ctx->words_proc / 4), ctx->spread_ctas);
+        const uint64_t B = ctx->esize == 4 ? 4 : 2, step = uint64_t(kFusedThreads / 32) * B;
+        const uint64_t cols = uint64_t(hs.workers) * ceil_div(groups, step) * B * ctx->esize;
+        if (cols <= 128 && env_int("MARSIT_STASH", 1) != 0) {
+            ctx->stash_cols = uint32_t(cols);
+            uint32_t a = 32;
+            while (a < 4 * cols) a *= 2;
+            ctx->tmem_cols = a;
+        }
+    }
+    if (ctx->spread) {
+        ctx->spread_coop = env_int("MARSIT_SPREAD_COOP", 1) != 0;
+
+        CUDA_TRY(cudaMalloc(&ctx->spread_sync, sizeof(unsigned) * (2 + ctx->S)));
+        CUDA_TRY(cudaMemset(ctx->spread_sync, 0, sizeof(unsigned) * (2 + ctx->S)));
+        const size_t nm = std::max<uint32_t>(mr.dp.n_merges, 1);
+        for (int b = 0; b < 2; ++b) {
+            CUDA_TRY(cudaMalloc(&ctx->spread_coins[b], sizeof(uint32_t) * (ctx->coin_total_words + 16)));
+            CUDA_TRY(cudaMemset(ctx->spread_coins[b], 0, sizeof(uint32_t) * (ctx->coin_total_words + 16)));
+            CUDA_TRY(cudaMalloc(&ctx->spread_valid[b], sizeof(uint32_t) * nm));
+            CUDA_TRY(cudaMemset(ctx->spread_valid[b], 0, sizeof(uint32_t) * nm));
+        }
+        CUDA_TRY(cudaMalloc(&ctx->spread_tag, 4 * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMemset(ctx->spread_tag, 0xFF, 4 * sizeof(unsigned long long)));  // no buffer holds coins
+        CUDA_TRY(cudaMalloc(&ctx->spread_cend, 2 * nm * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMemset(ctx->spread_cend, 0xFF, 2 * nm * sizeof(unsigned long long)));  // no history
+    }
     mr.err = ctx->err;
     // marsit_ctx_check's pinned read-back (allocated here: cudaHostAlloc may
     // synchronise the device, which a blocked P2P stream would never allow)

@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol():
     for name in names:
         assert hasattr(lib, name), name
     assert set(names) == set(N.SIGNATURES), set(names) ^ set(N.SIGNATURES)
-    assert lib.marsit_abi_version() == 2
+    assert lib.marsit_abi_version() == 3
 
 
 def test_schedules_match_reference_golden():

@@ -508,6 +508,44 @@ def test_adaptive_coin_budget_over_rounds_vs_oracle(frac, monkeypatch):
         ctx.check()
 
 
+@pytest.mark.parametrize("frac", ["0", "0.2", "2"])
+def test_spread_round_coin_budgets_vs_oracle(frac, monkeypatch):
+    """The spread round's own coins: computed in the launch when the buffer's
+    (seed, round) tag misses (first round, a skipped or revisited round, a new seed),
+    otherwise prefetched by the previous launch during its merge; budgets from
+    the stream ends of the round before, anything beyond drawn inline (a
+    Gaussian gradient with error feedback drives the disagreement above 1/2).
+    Bit-exact against the oracle for fp64, ring 8 and torus 2x4."""
+    monkeypatch.setenv("MARSIT_COIN_FRAC", frac)
+    monkeypatch.setenv("MARSIT_SPREAD", "1")
+    for topo, a, b in (("ring", 8, 0), ("torus", 2, 4)):
+        D = 300_000
+        sched = sched_of(topo, a, b)
+        T = O.schedule(topo, a, b)
+        W = sched.workers
+        rng = np.random.default_rng(5)
+        g = rng.standard_normal((W, D)) * 1e-3
+        gd = [torch.tensor(x, dtype=torch.float64, device=DEV) for x in g]
+        ctx = mb.Context(D, sched, torch.float64, 0)
+        ctx.set_timing(True)
+        comp = [torch.zeros(D, dtype=torch.float64, device=DEV) for _ in range(W)]
+        comp_o = np.zeros((W, D))
+        # skips, a revisit (3, 6, 4: round 6 misses and recomputes the buffer
+        # round 4's prefetch had tagged) and a new seed
+        rounds = [(31, t) for t in range(1, 7)] + [(31, 9), (31, 10), (31, 3), (31, 6), (31, 4),
+                                                   (32, 11), (32, 12)]
+        for seed, t in rounds:
+            agg = torch.empty((D + 63) // 64, dtype=torch.int64, device=DEV)
+            ctx.sign_round(t, ETA, seed, gd, comp, agg_bits=agg)
+            r = O.marsit_round(T, t, None, ETA, g, comp_o, seed)
+            assert u64(agg).tolist() == r.agg_bits.tolist(), (topo, seed, t)
+            got = np.stack([c.cpu().numpy() for c in comp])
+            assert np.array_equal(got, r.comp), (topo, seed, t)
+            comp_o = r.comp
+        ctx.check()
+        assert ctx.timing()["spread_round"][1] == len(rounds)
+
+
 def test_plain_c_program_round_trip():
     """build/sign_round_c (the C-ABI from plain C) runs 6 rounds, dense every
     4th, and checks c' = (g + c) - g_t bit for bit after every sign round."""
@@ -527,14 +565,18 @@ def test_plain_c_program_round_trip():
 @pytest.mark.parametrize("topo,a,b,D", [("ring", 4, 0, 1_000_000), ("ring", 8, 0, 262_142),
                                         ("torus", 2, 4, 60_224), ("ring", 16, 0, 640_000),
                                         ("torus", 3, 3, 36_036), ("ring", 2, 0, 8)])
-def test_fused_small_round_vs_oracle(dtype, topo, a, b, D, monkeypatch):
-    """Small one-GPU rounds run as ONE cluster launch (extract -> merge ->
-    decode per segment, round_cluster_kernel): bit-exact vs the oracle over
-    carried rounds (value padding in the last segment when D % 4 != 0), the
-    g_t output, and the same bits as the unfused kernels (MARSIT_FUSED=0)."""
+@pytest.mark.parametrize("kernel", ["spread", "spread_nostash", "cluster"])
+def test_fused_small_round_vs_oracle(dtype, topo, a, b, D, kernel, monkeypatch):
+    """Small one-GPU rounds run as ONE launch — over every SM with this
+    round's coins inside (round_spread_kernel, the default) or one cluster per
+    segment (round_cluster_kernel, MARSIT_SPREAD=0): bit-exact vs the oracle
+    over carried rounds (value padding in the last segment when D % 4 != 0),
+    the g_t output, and the same bits as the unfused kernels (MARSIT_FUSED=0)."""
     sched = sched_of(topo, a, b)
     T = O.schedule(topo, a, b)
     W, seed = sched.workers, 31
+    monkeypatch.setenv("MARSIT_SPREAD", "0" if kernel == "cluster" else "1")
+    monkeypatch.setenv("MARSIT_STASH", "0" if kernel == "spread_nostash" else "1")
     ctx = mb.Context(D, sched, dtype, 0)
     ctx.set_timing(True)
     monkeypatch.setenv("MARSIT_FUSED", "0")
@@ -561,7 +603,41 @@ def test_fused_small_round_vs_oracle(dtype, topo, a, b, D, monkeypatch):
     ctx.check()
     esize = 4 if dtype == torch.float32 else 8
     if W <= 16 and W * D * esize * 2 <= 96 << 20:
-        assert ctx.timing()["fused_round"][1] > 0  # the fused kernel ran
+        ran = "fused_round" if kernel == "cluster" else "spread_round"
+        assert ctx.timing()[ran][1] == 4  # the one-launch kernel ran every round
+
+
+def test_spread_round_graph_replay_matches_eager():
+    """The spread round keeps no host-side round state (its arrival count and
+    generation live on the device and reset themselves), so rounds captured in
+    a CUDA graph replay exactly: two replays of rounds t = 1, 2, 3 equal six
+    eager rounds t = 1, 2, 3, 1, 2, 3 with the compensation carried."""
+    W, D, seed = 4, 1_000_000, 7
+    sched = mb.build_ring_schedule(W)
+    g = [torch.empty(D, device=DEV) for _ in range(W)]
+    for w in range(W):
+        mb.fill_recipe(g[w], 0, seed, w, 1)
+    ctx, ref = mb.Context(D, sched, torch.float32, 0), mb.Context(D, sched, torch.float32, 0)
+    comp = [torch.zeros(D, device=DEV) for _ in range(W)]
+    comp_r = [torch.zeros(D, device=DEV) for _ in range(W)]
+    agg = torch.zeros((D + 63) // 64, dtype=torch.int64, device=DEV)
+    agg_r = torch.zeros_like(agg)
+    warm = [torch.zeros(D, device=DEV) for _ in range(W)]
+    ctx.sign_round(1, ETA, seed, g, warm)  # kernel attributes, coin tags settled outside capture
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for t in (1, 2, 3):
+            ctx.sign_round(t, ETA, seed, g, comp, agg_bits=agg)
+    for _ in range(2):
+        graph.replay()
+        for t in (1, 2, 3):
+            ref.sign_round(t, ETA, seed, g, comp_r, agg_bits=agg_r)
+        torch.cuda.synchronize()
+        assert torch.equal(agg, agg_r)
+        for w in range(W):
+            assert torch.equal(comp[w], comp_r[w]), w
+    ctx.check()
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
@@ -601,7 +677,8 @@ def test_fused_round_zeros_negzero_subnormals_vs_oracle(dtype):
     else:  # fp32 arithmetic: 1e-6 relative to the operands of c' = (g + c) - g_t
         bound = 1e-6 * (np.abs(r.comp) + np.abs(g64) + np.abs(c64) + ETA)
         assert np.all(np.abs(got - r.comp) <= bound)
-    assert ctx.timing()["fused_round"][1] == 1
+    tm = ctx.timing()
+    assert tm["fused_round"][1] + tm["spread_round"][1] == 1
 
 
 @pytest.mark.slow

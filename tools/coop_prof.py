@@ -4,7 +4,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2204_06787_b200 as mb
 from paper_2204_06787_b200 import _native as N
-L = N.lib(); buf = (C.c_ulonglong * 8)()
+L = N.lib(); buf = (C.c_ulonglong * 16)()
 def run(G, D):
     sched = mb.build_ring_schedule(8)
     ctx = mb.Context(D, sched, torch.float32, 0, nranks=G, rank=0, external_transport=(G > 1))

@@ -1,6 +1,6 @@
-"""Phase times of CTA 0 of the fused small round (MARSIT_FUSED_PROF build,
-MARSIT_SO=...libmarsit_b200_prof.so): extract / merge / decode per launch and,
-inside the merge, pass 1 + CTA scan / cluster barrier / pass 2 per level."""
+"""Phase times of the spread small round (MARSIT_FUSED_PROF build, MARSIT_SO=
+...libmarsit_b200_prof.so): CTA 0 (in merge cluster 0) and the last CTA (a
+streaming-only CTA), per launch, from %globaltimer."""
 import ctypes as C
 import os
 import sys
@@ -30,6 +30,9 @@ for D, M in ((1_000_000, 4), (4_000_000, 4), (1_000_000, 8)):
     torch.cuda.synchronize()
     L.marsit_debug_coop_prof(buf, 1)
     n, nl = max(buf[3], 1), max(buf[7], 1)
-    print(f"D={D} M={M}: launches {buf[3]} extract {buf[0]/n/1e3:.2f} us  merge {buf[1]/n/1e3:.2f} us  "
-          f"decode {buf[2]/n/1e3:.2f} us | per level ({nl // n} levels): pass1+scan {buf[4]/nl/1e3:.2f}  "
-          f"cluster barrier {buf[5]/nl/1e3:.2f}  pass2 {buf[6]/nl/1e3:.2f} us")
+    us = lambda i: buf[i] / n / 1e3  # noqa: E731
+    print(f"D={D} M={M}: CTA0 coins {us(8):.2f} +extract {us(0)-us(8):.2f} | wait-arrivals {us(9):.2f} "
+          f"merge(incl wait) {us(1):.2f} | wait-aggregates {us(10):.2f} decode(incl wait) {us(2):.2f} || "
+          f"last CTA: coins {us(12):.2f} wait-aggregates {us(14):.2f} whole {us(15):.2f} | per level "
+          f"({nl // n}): pass1+scan {buf[4]/nl/1e3:.2f} barrier {buf[5]/nl/1e3:.2f} pass2 {buf[6]/nl/1e3:.2f} us",
+          flush=True)
