@@ -1597,6 +1597,22 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
             st = mr.configure(ctx->sm_count);
         }
         if (st) return st;
+        // one GPU holding many segments: the cooperative merge when it runs
+        // as one launch part (measured, B200: C3 merge 50.8 vs 53.1 us, round
+        // 678-680 vs 687 us); the grid merge stays for a rank's few segments
+        // (G = 2 / 4 / 8: 33.2 / 29.8 / 28.7 vs 40.9 / 34.8 / 30.6 us) and
+        // wherever the cooperative merge needs several parts (C2, C4)
+        if (mr.grid && !ctx->fused && !kernel_forced && G == 1 && ctx->s_own >= 8) {
+            mr.cluster = mr.grid = false;
+            if ((st = lower())) return st;
+            st = mr.configure(ctx->sm_count);
+            if (st || mr.n_parts > 1) {
+                cudaGetLastError();
+                mr.cluster = mr.grid = true;
+                if ((st = lower())) return st;
+                if ((st = mr.configure(ctx->sm_count))) return st;
+            }
+        }
     }
     if ((st = mr.upload())) return st;
 

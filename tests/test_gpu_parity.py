@@ -681,6 +681,39 @@ def test_fused_round_zeros_negzero_subnormals_vs_oracle(dtype):
     assert tm["fused_round"][1] + tm["spread_round"][1] == 1
 
 
+def test_c3_cooperative_default_equals_grid_merge(monkeypatch):
+    """C3 on one GPU (8 segments in one co-resident cooperative launch): the
+    context picks the cooperative merge there (faster by a round's ~8 us) —
+    its results equal the grid merge's (MARSIT_MERGE_KERNEL=grid) bit for bit
+    over carried rounds, one merge launch per round each."""
+    D, seed = 25_600_000, 2026
+    sched = mb.build_ring_schedule(8)
+    W = sched.workers
+    auto = mb.Context(D, sched, torch.float32, 0)
+    auto.set_timing(True)
+    monkeypatch.setenv("MARSIT_MERGE_KERNEL", "grid")
+    grid = mb.Context(D, sched, torch.float32, 0)
+    grid.set_timing(True)
+    monkeypatch.delenv("MARSIT_MERGE_KERNEL")
+    g = [torch.empty(D, device=DEV) for _ in range(W)]
+    c1 = [torch.zeros(D, device=DEV) for _ in range(W)]
+    c2 = [torch.zeros(D, device=DEV) for _ in range(W)]
+    a1 = torch.empty((D + 63) // 64, dtype=torch.int64, device=DEV)
+    a2 = torch.empty_like(a1)
+    for t in (1, 2):
+        for w in range(W):
+            mb.fill_recipe(g[w], t % 2, seed, w, t)
+        auto.sign_round(t, ETA, seed, g, c1, agg_bits=a1)
+        grid.sign_round(t, ETA, seed, g, c2, agg_bits=a2)
+        torch.cuda.synchronize()
+        assert torch.equal(a1, a2), t
+        for w in range(W):
+            assert torch.equal(c1[w], c2[w]), (t, w)
+    assert auto.timing()["merge"][1] == 2 and grid.timing()["merge"][1] == 2
+    auto.check()
+    grid.check()
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("topo,a,b,D", [("torus", 2, 4, 60_200_000), ("ring", 8, 0, 61_000_000)])
 def test_large_segments_grid_merge_equals_cooperative(topo, a, b, D, monkeypatch):
