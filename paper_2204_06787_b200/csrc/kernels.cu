@@ -1792,9 +1792,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     __shared__ uint32_t s_cbase[kSpreadMaxMerges + 1];
     __shared__ int s_hit;
     __shared__ uint32_t s_tmem;
+    // the buffer's tag: loaded now, compared after the extract (a miss
+    // computes the coins then, before this CTA arrives)
+    unsigned long long tag_seed = 0, tag_round = 0;
     if (tid == 0) {
-        const unsigned long long* tg = s.tag + 2 * cb;
-        s_hit = __ldcg(tg) == p.seed && __ldcg(tg + 1) == p.round;
+        tag_seed = __ldcg(s.tag + 2 * cb);
+        tag_round = __ldcg(s.tag + 2 * cb + 1);
     }
     const bool stash = f.stash_cols != 0;
     if (stash && wid == 0) tmem_alloc(&s_tmem, f.tmem_cols);
@@ -1807,13 +1810,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     // the merge clusters stage their descriptors under the extract
     const uint32_t cl = blockIdx.x / p.csize;
     if (cl < p.n_seg) cluster_merge_prologue<NSUB, NL, true, false, kFusedThreads>(p, sh, sp_dyn);
-    if (!s_hit && s.n_merges)
-        spread_coins(p, s, s_cbase, cb, p.round, blockIdx.x, gridDim.x);
 #ifdef MARSIT_FUSED_PROF
     const bool prof = tid == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1);
     const int ps = blockIdx.x == 0 ? 8 : 12;  // slots 8..11: CTA 0, 12..15: the last CTA
     const uint64_t fp_tc = prof ? gtime_ns() : 0;
-    if (prof) atomicAdd(&g_coop_prof[ps], (unsigned long long)(fp_tc - fp_t0));  // coins
+    if (prof) atomicAdd(&g_coop_prof[ps], (unsigned long long)(fp_tc - fp_t0));  // start: TMEM, descriptors
 #endif
     constexpr int B = sizeof(T) == 4 ? 4 : 2;  // groups per warp step
     // K1: u = g + c, sign nibbles -> packed words of leaf (segment, worker)
@@ -1873,6 +1874,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     }
     if (__any_sync(kFull, !(fin == fin)) && lane == 0) atomicOr(f.err, 1);
     if (stash) tmem_wait_st();
+    if (tid == 0) s_hit = tag_seed == p.seed && tag_round == p.round;
+    __syncthreads();
+    if (!s_hit && s.n_merges) spread_coins(p, s, s_cbase, cb, p.round, blockIdx.x, gridDim.x);
     // arrive: the last CTA resets the count and advances the generation
     __syncthreads();
     if (tid == 0) {

@@ -31,8 +31,8 @@ for D, M in ((1_000_000, 4), (4_000_000, 4), (1_000_000, 8)):
     L.marsit_debug_coop_prof(buf, 1)
     n, nl = max(buf[3], 1), max(buf[7], 1)
     us = lambda i: buf[i] / n / 1e3  # noqa: E731
-    print(f"D={D} M={M}: CTA0 coins {us(8):.2f} +extract {us(0)-us(8):.2f} | wait-arrivals {us(9):.2f} "
+    print(f"D={D} M={M}: CTA0 start {us(8):.2f} +extract (+coins on a tag miss) {us(0)-us(8):.2f} | wait-arrivals {us(9):.2f} "
           f"merge(incl wait) {us(1):.2f} | wait-aggregates {us(10):.2f} decode(incl wait) {us(2):.2f} || "
-          f"last CTA: coins {us(12):.2f} wait-aggregates {us(14):.2f} whole {us(15):.2f} | per level "
+          f"last CTA: start {us(12):.2f} wait-aggregates {us(14):.2f} whole {us(15):.2f} | per level "
           f"({nl // n}): pass1+scan {buf[4]/nl/1e3:.2f} barrier {buf[5]/nl/1e3:.2f} pass2 {buf[6]/nl/1e3:.2f} us",
           flush=True)
