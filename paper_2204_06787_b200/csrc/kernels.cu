@@ -1629,27 +1629,37 @@ __device__ __forceinline__ uint32_t coin_budget(const DevMerge& m, uint64_t e, u
     return *chunks * 64 < m.coin_words ? *chunks * 64 : m.coin_words;
 }
 
-// One warp: coin chunk c (words 64c .. 64c + 63) of the stream with key `key`.
-__device__ __forceinline__ void coin_chunk(uint64_t key, uint64_t th, uint32_t* out, uint32_t c, int lane) {
-    // lane l builds words l and l + 32 of the chunk bit by bit (two
-    // independent draw streams for ILP), then both are stored coalesced
-    uint64_t za = key + (uint64_t(c) * 2048 + uint64_t(lane) * 32 + 1) * kGamma;
+// One warp: coin words [w0, w0 + NW) (NW = 32 or 64) of the stream with key
+// `key`: lane l builds word w0 + l (and w0 + 32 + l, a second independent
+// draw stream for ILP) bit by bit, then the words are stored coalesced.  The
+// coin is decided on h2, the high word of mix64's last product (mix64_h2):
+// its final xor-shift only flips bit 0, so h2 < th >> 32 decides unless h2
+// agrees with th's high word above bit 0 (probability 2^-31 per draw) — that
+// only raises a flag, and a word that saw one is redrawn with the full
+// 64-bit compare (no per-draw branch).  (A ballot per word — lane l drawing
+// bit l — measured slower: 151 vs 141 us per C3 coin launch.)
+template <int NW>
+__device__ __forceinline__ void coin_words(uint64_t key, uint64_t th, uint32_t* out, uint64_t w0, int lane) {
+    static_assert(NW == 32 || NW == 64, "coin run of 32 or 64 words");
+    constexpr bool TWO = NW == 64;
+    const uint32_t thh = uint32_t(th >> 32), thh1 = thh >> 1;
+    uint64_t za = key + ((w0 + uint64_t(lane)) * 32 + 1) * kGamma;
     uint64_t zb = za + 1024 * kGamma;
-    // the high word decides unless it equals th's (probability 2^-32 per
-    // draw): ties only raise a flag, and a word that saw one is redrawn
-    // with the full compare (no per-draw branch)
-    const uint32_t thh = uint32_t(th >> 32);
     const uint64_t za0 = za, zb0 = zb;
     uint32_t wa = 0, wb = 0;
     bool tie = false;
 #pragma unroll 8
     for (int i = 0; i < 32; ++i) {
-        const uint32_t xa = mix64_hi(za), xb = mix64_hi(zb);
+        const uint32_t xa = mix64_h2(za);
         wa |= uint32_t(xa < thh) << i;
-        wb |= uint32_t(xb < thh) << i;
-        tie |= (xa == thh) | (xb == thh);
+        tie |= __umulhi(xa, 0x80000000u) == thh1;
         za += kGamma;
-        zb += kGamma;
+        if (TWO) {
+            const uint32_t xb = mix64_h2(zb);
+            wb |= uint32_t(xb < thh) << i;
+            tie |= __umulhi(xb, 0x80000000u) == thh1;
+            zb += kGamma;
+        }
     }
     if (tie) {
         za = za0;
@@ -1657,13 +1667,13 @@ __device__ __forceinline__ void coin_chunk(uint64_t key, uint64_t th, uint32_t* 
         wa = wb = 0;
         for (int i = 0; i < 32; ++i) {
             if (mix64(za) < th) wa |= 1u << i;
-            if (mix64(zb) < th) wb |= 1u << i;
+            if (TWO && mix64(zb) < th) wb |= 1u << i;
             za += kGamma;
             zb += kGamma;
         }
     }
-    __stcg(out + uint64_t(c) * 64 + lane, wa);
-    __stcg(out + uint64_t(c) * 64 + 32 + lane, wb);
+    __stcg(out + w0 + lane, wa);
+    if (TWO) __stcg(out + w0 + 32 + lane, wb);
 }
 
 __global__ void __launch_bounds__(256) coins_kernel(const DevMerge* __restrict__ merges,
@@ -1680,7 +1690,7 @@ __global__ void __launch_bounds__(256) coins_kernel(const DevMerge* __restrict__
     const uint64_t key = m.key_mode ? m.key : stream_key(seed, 5, m.receiver, round, m.segment);
     uint32_t* out = coins + m.coin_off;
     for (uint32_t c = blockIdx.x * 8 + (threadIdx.x >> 5); c < chunks; c += gridDim.x * 8)
-        coin_chunk(key, m.thresh11, out, c, lane);
+        coin_words<64>(key, m.thresh11, out, uint64_t(c) * 64, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -1747,25 +1757,7 @@ __device__ __forceinline__ void spread_coins(const ClusterParams& p, const Sprea
         }
         const DevMerge& m = p.merges[lo];
         const uint64_t key = m.key_mode ? m.key : stream_key(p.seed, 5, m.receiver, round, m.segment);
-        const uint32_t word = (i - s_cbase[lo]) * 32 + lane;
-        uint64_t z = key + (uint64_t(word) * 32 + 1) * kGamma;
-        const uint32_t thh = uint32_t(m.thresh11 >> 32);
-        uint32_t wv = 0;
-        bool tie = false;
-#pragma unroll 8
-        for (int b = 0; b < 32; ++b) {
-            const uint32_t x = mix64_hi(z);
-            wv |= uint32_t(x < thh) << b;
-            tie |= x == thh;
-            z += kGamma;
-        }
-        if (tie) {  // the full compare for the word that saw a high-word tie
-            z = key + (uint64_t(word) * 32 + 1) * kGamma;
-            wv = 0;
-            for (int b = 0; b < 32; ++b, z += kGamma)
-                if (mix64(z) < m.thresh11) wv |= 1u << b;
-        }
-        __stcg(s.coins[cb] + m.coin_off + word, wv);
+        coin_words<32>(key, m.thresh11, s.coins[cb] + m.coin_off, uint64_t(i - s_cbase[lo]) * 32, lane);
     }
 }
 
@@ -3108,6 +3100,21 @@ MARSIT_INSTANTIATE(float)
 MARSIT_INSTANTIATE(double)
 
 }  // namespace marsit_b200
+
+// Test hook (not part of the public header): coin words [0, n_words) of the
+// stream (key, th) through the production coin-word routine, 64 words per warp.
+namespace marsit_b200 {
+namespace {
+__global__ void debug_coin_words_kernel(uint64_t key, uint64_t th, uint32_t n_chunks, uint32_t* out) {
+    const uint32_t c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (c < n_chunks) coin_words<64>(key, th, out, uint64_t(c) * 64, threadIdx.x & 31);
+}
+}  // namespace
+}  // namespace marsit_b200
+extern "C" int marsit_debug_coin_words(uint64_t key, uint64_t th, uint32_t n_chunks, uint32_t* d_out) {
+    marsit_b200::debug_coin_words_kernel<<<(n_chunks + 7) / 8, 256>>>(key, th, n_chunks, d_out);
+    return int(cudaDeviceSynchronize());
+}
 
 #if defined(MARSIT_COOP_PROF) || defined(MARSIT_FUSED_PROF)
 extern "C" void marsit_debug_coop_prof(unsigned long long* out, int reset) {

@@ -41,6 +41,17 @@ __device__ __forceinline__ void xorshr_fma(uint32_t& lo, uint32_t& hi, uint32_t 
     hi ^= mulhi32(hi, m);
     lo = nlo;
 }
+// High word h2 of the last product of mix64(z) (before its final xor-shift):
+// mix64(z) >> 32 == h2 ^ (h2 >> 31), i.e. h2 with bit 0 flipped when its top
+// bit is set, so for a threshold th, mix64(z) < th == (h2 < th >> 32)
+// whenever h2 >> 1 != (th >> 32) >> 1.
+__device__ __forceinline__ uint32_t mix64_h2(uint64_t z) {
+    uint64_t y = z ^ (z >> 30);
+    y *= 0xbf58476d1ce4e5b9ull;
+    uint32_t lo = uint32_t(y), hi = uint32_t(y >> 32);
+    xorshr_fma(lo, hi, 1u << 5);  // >> 27
+    return mulhi32(lo, 0x133111ebu) + lo * 0x94d049bbu + hi * 0x133111ebu;
+}
 // High 32 bits of mix64(z): only the high word of the last product is formed.
 __device__ __forceinline__ uint32_t mix64_hi(uint64_t z) {
     uint64_t y = z ^ (z >> 30);
