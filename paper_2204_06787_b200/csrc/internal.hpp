@@ -582,6 +582,7 @@ struct TimedPair {
 constexpr int kErrNonFinite = 1;  // DenseVector finiteness (dense_vector.hpp:25-29)
 constexpr int kErrConsensus = 2;  // an aggregate segment differs from its owner's (allreduce.hpp:32-43)
 constexpr int kErrBounds = 8;     // checked builds (MARSIT_CHECKED): an index failed its bound
+constexpr int kErrSync = 16;      // spread round: a wait on the other CTAs ran past its bound
 
 // P2P flag value that releases every stream wait: written by a watchdog that
 // gave up (into its own flags and into its slot of every peer's flags) so no

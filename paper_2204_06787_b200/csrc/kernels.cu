@@ -1707,6 +1707,19 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// Spin until *p == v (acquire).  Bounded (~2 s): every CTA of the launch is
+// resident by construction (the grid is the co-resident cluster count), so a
+// timeout means the device was shared beyond that — err |= 16 (reported by
+// marsit_ctx_check) and the launch finishes instead of hanging the GPU.
+__device__ __forceinline__ void wait_eq_u32(const unsigned* p, unsigned v, int* err) {
+    for (uint32_t spin = 0; ld_acquire_u32(p) != v; ++spin) {
+        if (spin == (1u << 22)) {
+            atomicOr(err, 16);
+            return;
+        }
+        __nanosleep(20);
+    }
+}
 
 
 // The coins of round `round` into buffer cb, by CTAs [0, nctas) of the
@@ -1895,7 +1908,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     }
     if (cl < p.n_seg) {
         if (tid == 0) {
-            while (ld_acquire_u32(s.sync + 1) != gen) __nanosleep(20);
+            wait_eq_u32(s.sync + 1, gen, f.err);
             // every CTA has read the tag: buffer cb now holds this round's
             // coins (computed above on a miss), tagged for later rounds
             if (blockIdx.x == 0 && s.n_merges) {
@@ -1938,7 +1951,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     if (g_lo < g_hi) {
         if (tid == 0)
             for (uint32_t sl = g_lo / gps; sl <= (g_hi - 1) / gps; ++sl)
-                while (ld_acquire_u32(s.sync + 2 + sl) != gen) __nanosleep(20);
+                wait_eq_u32(s.sync + 2 + sl, gen, f.err);
 #ifdef MARSIT_FUSED_PROF
         if (prof) atomicAdd(&g_coop_prof[ps + 2], (unsigned long long)(gtime_ns() - fp_t2));  // wait: aggregates
 #endif

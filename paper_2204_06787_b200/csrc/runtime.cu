@@ -2082,6 +2082,8 @@ marsit_status marsit_ctx_check(marsit_ctx* ctx, void* stream) {
         CUDA_TRY(cudaMemsetAsync(ctx->err, 0, sizeof(int), st));
         CUDA_TRY(poll_stream(st, ctx->ev_check));
         if (flag & kErrBounds) return fail(MARSIT_ECUDA, "checked build: a device index failed its bound");
+        if (flag & kErrSync)
+            return fail(MARSIT_ECUDA, "spread round: CTAs were not co-resident (a wait timed out; results invalid)");
         if (flag & kErrNonFinite) return fail(MARSIT_ENONFINITE, "DenseVector: non-finite entry");
         return fail(MARSIT_EPROTOCOL, "consensus: an aggregate segment differs from its owner's");
     }
