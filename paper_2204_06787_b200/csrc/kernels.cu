@@ -1884,6 +1884,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     if (!s_hit && s.n_merges) spread_coins(p, s, s_cbase, cb, p.round, blockIdx.x, gridDim.x);
     // arrive: the last CTA resets the count and advances the generation
     __syncthreads();
+    jitter(100);  // checked builds: random arrival order
     if (tid == 0) {
         __threadfence();
         if (atomicAdd(s.sync, 1u) == gridDim.x - 1) {
@@ -1907,6 +1908,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         }
     }
     if (cl < p.n_seg) {
+        jitter(101);
         if (tid == 0) {
             wait_eq_u32(s.sync + 1, gen, f.err);
             // every CTA has read the tag: buffer cb now holds this round's
@@ -1942,6 +1944,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         __syncthreads();
         if (tid == 0) __threadfence();
         cluster_sync_all();  // the segment's aggregate tiles are all written
+        jitter(102);
         if (tid == 0 && cluster_ctarank() == 0) st_release_u32(s.sync + 2 + cl, gen);
     }
 #ifdef MARSIT_FUSED_PROF
@@ -1949,6 +1952,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 #endif
     // K3/K4 of this CTA's slice once its segments' aggregates are published
     if (g_lo < g_hi) {
+        jitter(103);
         if (tid == 0)
             for (uint32_t sl = g_lo / gps; sl <= (g_hi - 1) / gps; ++sl)
                 wait_eq_u32(s.sync + 2 + sl, gen, f.err);
