@@ -135,6 +135,7 @@ struct MergeRunner {
     unsigned long long* xch = nullptr;  // grid mode: [2][seg_per_launch][csize][level_width]
     uint32_t xch_epoch = 0;             // grid mode: launches so far (the words' launch tag)
     uint32_t prefetch = uint32_t(env_int("MARSIT_MERGE_PREFETCH", 1));  // level loop: next leaves into L1
+    uint32_t coin_l1 = uint32_t(env_int("MARSIT_COIN_L1", 1));         // level loop: likely coin window into L1
     uint32_t csize = 16, tile_groups = 0, nsub = 1, stage = 0, masks = 0;
     size_t merge_smem = 0;  // merge_cluster_kernel's dynamic shared memory (smem minus the fused ring)
     // fused small rounds (round_cluster_kernel): extra shared memory per CTA
@@ -480,6 +481,7 @@ struct MergeRunner {
         c.stage = stage;
         c.masks = masks;
         c.prefetch = prefetch;
+        c.coin_l1 = coin_l1;
         c.seg_bits = L;
         c.leaves = leaves;
         c.peer_bits = peer_bits;

@@ -1171,6 +1171,27 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
             }
         }
         jitter(2 * v);
+        // the coin words this CTA will most likely read in pass 2, into L1
+        // while the other CTAs' totals arrive: the lower CTAs are assumed to
+        // have drawn as many as this one (prefix ~ cr x own), +-slack; a wrong
+        // estimate only wastes the prefetches (p.coin_l1)
+        if (p.coin_l1 && p.coins && !p.coherent) {
+            for (uint32_t i = 0; i < nk; ++i) {
+                const DevMerge& m = sh.m[k0 + i];
+                uint64_t base = m.base_add;
+                for (int32_t src = m.offset_src; src >= 0; src = sh.m[src].offset_src)
+                    base += sh.tot[src] + sh.m[src].base_add;
+                uint64_t own = 0;
+#pragma unroll
+                for (int u = 0; u < NSUB; ++u) own += sh.ctot[i * NSUB + u];
+                const uint64_t est = base + uint64_t(cr) * own, slack = 1024 + (own >> 3);
+                const uint64_t w_lo = (est > slack ? est - slack : 0) >> 5;
+                const uint64_t w_hi = min((est + own + slack) >> 5, uint64_t(sh.valid[k0 + i]));
+                const uint32_t* cw = p.coins + m.coin_off;
+                for (uint64_t line = (w_lo >> 5) + tid; line <= (w_hi >> 5) && w_lo < w_hi; line += NT)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(cw + line * 32));
+            }
+        }
 #ifdef MARSIT_FUSED_PROF
         const uint64_t lv_t1 = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0;
 #endif

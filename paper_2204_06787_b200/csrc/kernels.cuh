@@ -132,6 +132,7 @@ struct ClusterParams {
                                   // (1 after the masks, 2 before them, 3 after the totals)
     uint32_t xch_tag;             // per launch (host counter; the level is the low 8 bits)
     unsigned* seg_bars;
+    uint32_t coin_l1;             // 1: the likely coin window of pass 2 is prefetched into L1
     uint32_t coherent;            // 1: leaves and coins were written by this launch (spread
                                   // round): L2-coherent loads, no L1 prefetch
 };
