@@ -135,7 +135,11 @@ struct MergeRunner {
     unsigned long long* xch = nullptr;  // grid mode: [2][seg_per_launch][csize][level_width]
     uint32_t xch_epoch = 0;             // grid mode: launches so far (the words' launch tag)
     uint32_t prefetch = uint32_t(env_int("MARSIT_MERGE_PREFETCH", 1));  // level loop: next leaves into L1
-    uint32_t coin_l1 = uint32_t(env_int("MARSIT_COIN_L1", 1));         // level loop: likely coin window into L1
+    // level loop, opt-in (MARSIT_COIN_L1=1): the likely coin window of pass 2
+    // prefetched into L1 during the exchange.  Measured: C2 merge 101 -> 98
+    // us, C4 98.6 -> 99.6, G = 8 rank 28.6 -> 30.7, G = 2 34.2 -> 36.4; the
+    // C2 / C4 / C5 rounds unchanged within noise — off by default
+    uint32_t coin_l1 = uint32_t(env_int("MARSIT_COIN_L1", 0) != 0);
     uint32_t csize = 16, tile_groups = 0, nsub = 1, stage = 0, masks = 0;
     size_t merge_smem = 0;  // merge_cluster_kernel's dynamic shared memory (smem minus the fused ring)
     // fused small rounds (round_cluster_kernel): extra shared memory per CTA
