@@ -663,6 +663,11 @@ struct marsit_ctx {
     // spread round: TMEM columns per thread for the parked u (0: the decode
     // re-reads g, c) and the allocation per CTA
     uint32_t stash_cols = 0, tmem_cols = 0;
+    // spread round: the extract's TMA ring (stages of one worker's slice, g
+    // then c, tma_half bytes each; 0 stages = register loads) and the launch's
+    // dynamic shared memory (max of that ring and the merge clusters' tiles)
+    uint32_t tma_stages = 0, tma_half = 0;
+    size_t spread_smem = 0;
     unsigned* spread_sync = nullptr;   // [2 + S]: arrivals, generation, per-segment merged flags
     uint32_t* spread_coins[2] = {nullptr, nullptr};  // coin buffers by round parity (SpreadParams)
     uint32_t* spread_valid[2] = {nullptr, nullptr};

@@ -1847,54 +1847,157 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     T fin = T(0);
     // The warp's tasks in order: t = (w * iters + it) * B + b is group
     // g_lo + wid + (it * B + b) * NWARP of worker w (also the TMEM column
-    // order); B tasks' quads of g and c in flight per step.
+    // order).
     const uint32_t iters = g_hi > g_lo + wid ? (g_hi - g_lo - wid + NWARP * B - 1) / (NWARP * B) : 0u;
-    uint32_t t0 = 0;
-    for (uint32_t w = 0; w < f.workers; ++w) {
-        const T* __restrict__ gw = f.g[w];
-        const T* __restrict__ cw = f.c[w];
-        for (uint32_t g0 = g_lo + wid; g0 < g_hi; g0 += NWARP * B, t0 += B) {
-            Quad<T> gv[B], cv[B];
+    // one quad of worker w, group gg: u, the TMEM stash, the packed nibble
+    auto consume = [&](uint32_t w, uint32_t gg, uint32_t col, const Quad<T>& gv, const Quad<T>& cv) {
+        const uint32_t sl = gg / gps, gl = gg - sl * gps;
+        const uint64_t j = uint64_t(gl) * 128 + lane * 4;
+        T u[4];
 #pragma unroll
-            for (int b = 0; b < B; ++b) {
-                const uint32_t gg = g0 + b * NWARP;
-                const uint32_t sl = gg / gps;
-                const uint64_t j = uint64_t(gg - sl * gps) * 128 + lane * 4;
-                const uint64_t gi = uint64_t(sl) * p.seg_bits + j;
-                if (gg < g_hi && quad_real<T>(j, p.seg_bits, gi, f.dim)) {
-                    gv[b] = load4(gw + gi);
-                    cv[b] = load4(cw + gi);
-                } else {
+        for (int k = 0; k < 4; ++k) {
+            u[k] = add_rn(add_rn(gv.v[k], cv.v[k]), T(0));  // -0.0 -> +0.0 (sign_vector.hpp:70)
+            fin = fma_rn(u[k], T(0), fin);
+        }
+        if (stash) tmem_put(tbase + col, u);  // warp-uniform
+        uint32_t nib = sign_nibble(u[0], u[1], u[2], u[3]);
+        const uint64_t valid = j >= p.seg_bits ? 0 : p.seg_bits - j;  // storage padding -> 0
+        if (valid < 4) nib &= (1u << valid) - 1u;
+        uint32_t v = nib << ((lane & 7) * 4);
+        v |= __shfl_xor_sync(kFull, v, 1);
+        v |= __shfl_xor_sync(kFull, v, 2);
+        v |= __shfl_xor_sync(kFull, v, 4);
+        if ((lane & 7) == 0)
+            const_cast<uint32_t*>(p.leaves)[(uint64_t(sl) * p.ml + w) * p.wst + uint64_t(gl) * 4 + (lane >> 3)] = v;
+    };
+    // a quad that is not whole (segment / vector end): element loads, value padding 0
+    auto edge_quad = [&](uint32_t w, uint64_t j, uint64_t gi, Quad<T>& gv, Quad<T>& cv) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const bool in = gg < g_hi && j + k < p.seg_bits && gi + k < f.dim;
-                        gv[b].v[k] = in ? gw[gi + k] : T(0);
-                        cv[b].v[k] = in ? cw[gi + k] : T(0);
+        for (int k = 0; k < 4; ++k) {
+            const bool in = j + k < p.seg_bits && gi + k < f.dim;
+            gv.v[k] = in ? f.g[w][gi + k] : T(0);
+            cv.v[k] = in ? f.c[w][gi + k] : T(0);
+        }
+    };
+    if (s.tma_stages) {
+        // TMA: one elected thread streams whole workers' slices (g, then c;
+        // one bulk copy per segment piece) into a ring of tma_stages stages
+        // of shared memory, each completing an mbarrier; the warps consume a
+        // stage once its bytes have landed — up to tma_stages x 2 x the
+        // slice in flight per SM, no registers held (the register path keeps
+        // 64 KB per SM in flight, the loaded-latency limit of the extract)
+        __shared__ __align__(8) unsigned long long s_full[kSpreadMaxTmaStages];
+        const uint32_t nst = s.tma_stages;
+        unsigned char* const ring = reinterpret_cast<unsigned char*>(sp_dyn);
+        const uint32_t ring_s = uint32_t(__cvta_generic_to_shared(ring));
+        if (tid == 0) {
+            for (uint32_t q = 0; q < nst; ++q)
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                                 uint32_t(__cvta_generic_to_shared(&s_full[q]))) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        // pieces of the slice: groups [a, b) inside one segment; the whole
+        // quads of each (value / storage padding and partial quads are read
+        // per element by the consumers)
+        auto issue = [&](uint32_t w, uint32_t st) {
+            const uint32_t bar = uint32_t(__cvta_generic_to_shared(&s_full[st]));
+            uint32_t tx = 0;
+            for (int pass = 0; pass < 2; ++pass) {
+                if (pass == 1)
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx) : "memory");
+                for (uint32_t a = g_lo; a < g_hi;) {
+                    const uint32_t sl = a / gps, b = min(g_hi, (sl + 1) * gps);
+                    const uint64_t j0 = uint64_t(a - sl * gps) * 128, seg0 = uint64_t(sl) * p.seg_bits;
+                    uint64_t je = min(uint64_t(b - sl * gps) * 128, p.seg_bits);
+                    je = min(je, f.dim > seg0 ? f.dim - seg0 : uint64_t(0));
+                    const uint64_t n = je > j0 ? (je - j0) & ~3ull : 0;  // whole quads
+                    const uint32_t bytes = uint32_t(n * sizeof(T));
+                    if (bytes) {
+                        if (pass == 0) {
+                            tx += 2 * bytes;
+                        } else {
+                            const uint32_t off = st * 2 * s.tma_half + (a - g_lo) * 128 * uint32_t(sizeof(T));
+                            asm volatile(
+                                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                                ::"r"(ring_s + off), "l"(f.g[w] + seg0 + j0), "r"(bytes), "r"(bar) : "memory");
+                            asm volatile(
+                                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                                ::"r"(ring_s + off + s.tma_half), "l"(f.c[w] + seg0 + j0), "r"(bytes), "r"(bar)
+                                : "memory");
+                        }
                     }
+                    a = b;
                 }
             }
+        };
+        if (tid == 0)
+            for (uint32_t w = 0; w < min(nst, f.workers); ++w) issue(w, w);
+        for (uint32_t w = 0; w < f.workers; ++w) {
+            const uint32_t st = w % nst, par = (w / nst) & 1u;
+            const uint32_t bar = uint32_t(__cvta_generic_to_shared(&s_full[st]));
+            asm volatile(
+                "{\n\t.reg .pred P;\n"
+                "WAIT_%=:\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+                "@!P bra WAIT_%=;\n}" ::"r"(bar), "r"(par) : "memory");
+            const unsigned char* sg = ring + st * 2 * s.tma_half;
+            const unsigned char* sc = sg + s.tma_half;
+            uint32_t t0 = w * iters * B;
+            for (uint32_t g0 = g_lo + wid; g0 < g_hi; g0 += NWARP * B, t0 += B) {
 #pragma unroll
-            for (int b = 0; b < B; ++b) {
-                const uint32_t gg = g0 + b * NWARP;
-                if (gg >= g_hi) break;
-                const uint32_t sl = gg / gps, gl = gg - sl * gps;
-                const uint64_t j = uint64_t(gl) * 128 + lane * 4;
-                T u[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    u[k] = add_rn(add_rn(gv[b].v[k], cv[b].v[k]), T(0));  // -0.0 -> +0.0 (sign_vector.hpp:70)
-                    fin = fma_rn(u[k], T(0), fin);
+                for (int b = 0; b < B; ++b) {
+                    const uint32_t gg = g0 + b * NWARP;
+                    if (gg >= g_hi) break;
+                    const uint32_t sl = gg / gps;
+                    const uint64_t j = uint64_t(gg - sl * gps) * 128 + lane * 4;
+                    const uint64_t gi = uint64_t(sl) * p.seg_bits + j;
+                    Quad<T> gv, cv;
+                    if (quad_real<T>(j, p.seg_bits, gi, f.dim)) {
+                        const uint32_t o = ((gg - g_lo) * 128 + lane * 4) * uint32_t(sizeof(T));
+                        gv = *reinterpret_cast<const Quad<T>*>(sg + o);
+                        cv = *reinterpret_cast<const Quad<T>*>(sc + o);
+                    } else {
+                        edge_quad(w, j, gi, gv, cv);
+                    }
+                    consume(w, gg, (t0 + b) * QCOLS, gv, cv);
                 }
-                if (stash) tmem_put(tbase + (t0 + b) * QCOLS, u);  // warp-uniform
-                uint32_t nib = sign_nibble(u[0], u[1], u[2], u[3]);
-                const uint64_t valid = j >= p.seg_bits ? 0 : p.seg_bits - j;  // storage padding -> 0
-                if (valid < 4) nib &= (1u << valid) - 1u;
-                uint32_t v = nib << ((lane & 7) * 4);
-                v |= __shfl_xor_sync(kFull, v, 1);
-                v |= __shfl_xor_sync(kFull, v, 2);
-                v |= __shfl_xor_sync(kFull, v, 4);
-                if ((lane & 7) == 0)
-                    const_cast<uint32_t*>(p.leaves)[(uint64_t(sl) * p.ml + w) * p.wst + uint64_t(gl) * 4 + (lane >> 3)] = v;
+            }
+            if (w + nst < f.workers) {
+                __syncthreads();  // every warp is done with stage st
+                if (tid == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    issue(w + nst, st);
+                }
+            }
+        }
+        __syncthreads();  // the ring's shared memory is reused by the merge staging
+    } else {
+        uint32_t t0 = 0;
+        for (uint32_t w = 0; w < f.workers; ++w) {
+            const T* __restrict__ gw = f.g[w];
+            const T* __restrict__ cw = f.c[w];
+            for (uint32_t g0 = g_lo + wid; g0 < g_hi; g0 += NWARP * B, t0 += B) {
+                Quad<T> gv[B], cv[B];
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    const uint32_t gg = g0 + b * NWARP;
+                    const uint32_t sl = gg / gps;
+                    const uint64_t j = uint64_t(gg - sl * gps) * 128 + lane * 4;
+                    const uint64_t gi = uint64_t(sl) * p.seg_bits + j;
+                    if (gg < g_hi && quad_real<T>(j, p.seg_bits, gi, f.dim)) {
+                        gv[b] = load4(gw + gi);
+                        cv[b] = load4(cw + gi);
+                    } else if (gg < g_hi) {
+                        edge_quad(w, j, gi, gv[b], cv[b]);
+                    }
+                }
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    const uint32_t gg = g0 + b * NWARP;
+                    if (gg >= g_hi) break;
+                    consume(w, gg, (t0 + b) * QCOLS, gv[b], cv[b]);
+                }
             }
         }
     }

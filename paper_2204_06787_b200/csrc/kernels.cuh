@@ -182,6 +182,7 @@ cudaError_t round_cluster_occupancy(int nsub, int nl, uint32_t csize, size_t sme
 // The synchronisation words are device state only (a self-resetting arrival
 // count + generation), so rounds can be replayed from a CUDA graph.
 constexpr uint32_t kSpreadMaxMerges = 256;  // coin streams per spread round
+constexpr uint32_t kSpreadMaxTmaStages = 4;  // extract ring stages (TMA path)
 // Coins: two buffers b = round & 1, each tagged with the (seed, round) it
 // holds.  Round t uses buffer t & 1 and computes it first only when its tag
 // misses; while the merge clusters run, the other CTAs compute round t + 1's
@@ -197,6 +198,9 @@ struct SpreadParams {
     uint32_t* coin_valid[2];        // [n_merges] words computed per buffer
     unsigned long long* tag;        // [2][2]: (seed, round) each buffer holds, ~0 = none
     unsigned long long* cend;       // [2][n_merges] stream ends by round parity
+    // extract through TMA (0: register loads): stages of one worker's slice,
+    // g then c, tma_half bytes each (the largest slice of any CTA)
+    uint32_t tma_stages, tma_half;
 };
 template <typename T>
 cudaError_t launch_round_spread(const ClusterParams& p, const SpreadParams<T>& s, int nsub, int nl,

@@ -1240,18 +1240,20 @@ marsit_status spread_round(marsit_ctx* ctx, uint64_t t, double eta_s, uint64_t s
     sp.cend = ctx->spread_cend;
     sp.f.stash_cols = ctx->stash_cols;
     sp.f.tmem_cols = ctx->tmem_cols;
+    sp.tma_stages = ctx->tma_stages;
+    sp.tma_half = ctx->tma_half;
     ClusterParams p = mr.cluster_params(ctx->bits, ctx->agg, coins ? sp.coins[b] : nullptr, seed, t, 0,
                                         sp.coin_valid[b]);
     p.coin_end = reinterpret_cast<uint64_t*>(ctx->spread_cend) + size_t(b) * std::max<uint32_t>(mr.dp.n_merges, 1);
     p.coherent = 1;
     const int nsub = int(mr.nsub), nl = int(mr.dp.level_width);
-    cudaError_t e = launch_round_spread<T>(p, sp, nsub, nl, ctx->spread_ctas, mr.smem, ctx->spread_coop, st);
+    cudaError_t e = launch_round_spread<T>(p, sp, nsub, nl, ctx->spread_ctas, ctx->spread_smem, ctx->spread_coop, st);
     if (e != cudaSuccess && ctx->spread_coop) {
         // cooperative + cluster launch refused: the grid is sized to the
         // co-resident clusters, so a plain cluster launch keeps every CTA resident
         cudaGetLastError();
         ctx->spread_coop = false;
-        e = launch_round_spread<T>(p, sp, nsub, nl, ctx->spread_ctas, mr.smem, false, st);
+        e = launch_round_spread<T>(p, sp, nsub, nl, ctx->spread_ctas, ctx->spread_smem, false, st);
     }
     CUDA_TRY(e);
     if ((s = ctx->end_phase(kPhSpread, st, ev, 1))) return s;
@@ -1653,6 +1655,23 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
         }
     }
     if (ctx->spread) {
+        // the extract's TMA ring (opt-in, MARSIT_SPREAD_TMA=1): 3 (else 2)
+        // stages of a worker's slice when they fit next to the static shared
+        // memory.  Measured slower than the register loads (C1 31.9 vs 27.9
+        // us per round from a graph, M = 8 at 1M 54.1 vs 47.1): a stage is
+        // consumed only once all of its bytes have landed
+        ctx->spread_smem = mr.smem;
+        {
+            const uint64_t groups = ceil_div(uint64_t(ctx->S) * (ctx->words_proc / 4), ctx->spread_ctas);
+            const uint64_t half = round_up(groups * 128 * ctx->esize, 16);
+            for (uint32_t nst = std::min<uint32_t>(3, hs.workers); nst >= 2 && env_int("MARSIT_SPREAD_TMA", 0); --nst)
+                if (nst * 2 * half <= 200 * 1024) {
+                    ctx->tma_stages = nst;
+                    ctx->tma_half = uint32_t(half);
+                    ctx->spread_smem = std::max<size_t>(mr.smem, nst * 2 * half);
+                    break;
+                }
+        }
         // the grid is sized to the co-resident clusters, so a plain cluster
         // launch keeps every CTA resident; the cooperative attribute on top
         // (MARSIT_SPREAD_COOP=1) measured no faster and makes Nsight Compute

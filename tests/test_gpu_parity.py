@@ -565,7 +565,7 @@ def test_plain_c_program_round_trip():
 @pytest.mark.parametrize("topo,a,b,D", [("ring", 4, 0, 1_000_000), ("ring", 8, 0, 262_142),
                                         ("torus", 2, 4, 60_224), ("ring", 16, 0, 640_000),
                                         ("torus", 3, 3, 36_036), ("ring", 2, 0, 8)])
-@pytest.mark.parametrize("kernel", ["spread", "spread_nostash", "cluster"])
+@pytest.mark.parametrize("kernel", ["spread", "spread_nostash", "spread_tma", "cluster"])
 def test_fused_small_round_vs_oracle(dtype, topo, a, b, D, kernel, monkeypatch):
     """Small one-GPU rounds run as ONE launch — over every SM with this
     round's coins inside (round_spread_kernel, the default) or one cluster per
@@ -577,6 +577,7 @@ def test_fused_small_round_vs_oracle(dtype, topo, a, b, D, kernel, monkeypatch):
     W, seed = sched.workers, 31
     monkeypatch.setenv("MARSIT_SPREAD", "0" if kernel == "cluster" else "1")
     monkeypatch.setenv("MARSIT_STASH", "0" if kernel == "spread_nostash" else "1")
+    monkeypatch.setenv("MARSIT_SPREAD_TMA", "1" if kernel == "spread_tma" else "0")
     ctx = mb.Context(D, sched, dtype, 0)
     ctx.set_timing(True)
     monkeypatch.setenv("MARSIT_FUSED", "0")
