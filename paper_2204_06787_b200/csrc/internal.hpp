@@ -134,6 +134,7 @@ struct MergeRunner {
     }();
     unsigned long long* xch = nullptr;  // grid mode: [2][seg_per_launch][csize][level_width]
     uint32_t xch_epoch = 0;             // grid mode: launches so far (the words' launch tag)
+    uint32_t grid_nt = kClusterThreads;  // grid mode: threads per CTA (256 / 512 for small tiles)
     uint32_t prefetch = uint32_t(env_int("MARSIT_MERGE_PREFETCH", 1));  // level loop: next leaves into L1
     // level loop, opt-in (MARSIT_COIN_L1=1): the likely coin window of pass 2
     // prefetched into L1 during the exchange.  Measured: C2 merge 101 -> 98
@@ -337,15 +338,30 @@ struct MergeRunner {
             masks = stage && base_sm + stage_sm + mask_sm <= 200 * 1024 && env_int("MARSIT_MERGE_MASKS", 1) ? 1u : 0u;
             smem = merge_smem = std::max<size_t>(base_sm + (stage ? stage_sm : 0) + (masks ? mask_sm : 0), 16);
             if (smem > 200 * 1024) return fail(MARSIT_EUNSUPPORTED, "merge tiles do not fit shared memory");
-            CUDA_TRY(merge_grid_occupancy(int(nsub), int(nl), smem, &occ));
+            CUDA_TRY(merge_grid_occupancy(int(nsub), int(nl), smem, kClusterThreads, &occ));
             if (occ <= 0) return fail(MARSIT_EUNSUPPORTED, "grid merge does not fit an SM");
             if (uint64_t(seg_per_launch) * csize <= uint64_t(occ) * sm_count) break;
         }
         if (uint64_t(seg_per_launch) * csize > uint64_t(occ) * sm_count)
             return fail(MARSIT_EUNSUPPORTED, "grid merge CTAs are not co-resident");
+        // tiles of <= 256 / 512 groups: CTAs of that many threads (one group
+        // per thread; the same grid, so still one CTA per SM): G = 8 rank
+        // merge 28.7 -> 24.8 us, torus 26.6 -> 22.7 us; MARSIT_GRID_SMALL=0
+        // keeps 1024
+        grid_nt = kClusterThreads;
+        for (uint32_t nt : {256u, 512u})
+            if (nsub == 1 && tile_groups <= nt && env_int("MARSIT_GRID_SMALL", 1)) {
+                int occ_s = 0;
+                if (merge_grid_occupancy(1, int(nl), smem, int(nt), &occ_s) == cudaSuccess &&
+                    uint64_t(seg_per_launch) * csize <= uint64_t(occ_s) * sm_count) {
+                    grid_nt = nt;
+                    break;
+                }
+                cudaGetLastError();
+            }
         if (env_int("MARSIT_MERGE_DEBUG", 0))
-            fprintf(stderr, "merge grid: %u segments x %u CTAs, groups/CTA %u nsub %u stage %u masks %u\n",
-                    seg_per_launch, csize, tile_groups, nsub, stage, masks);
+            fprintf(stderr, "merge grid: %u segments x %u CTAs of %u threads, groups/CTA %u nsub %u stage %u masks %u\n",
+                    seg_per_launch, csize, grid_nt, tile_groups, nsub, stage, masks);
         return MARSIT_OK;
     }
 
@@ -486,6 +502,10 @@ struct MergeRunner {
         c.masks = masks;
         c.prefetch = prefetch;
         c.coin_l1 = coin_l1;
+        if (n_seg == 1 && dp.lvl_start.size() >= 2) {
+            c.solo_nm = dp.n_merges;
+            c.solo_nlv = dp.lvl_start[1] - dp.lvl_start[0] - 1;
+        }
         c.seg_bits = L;
         c.leaves = leaves;
         c.peer_bits = peer_bits;
@@ -517,7 +537,7 @@ struct MergeRunner {
                     if ((++xch_epoch & 0xFFFFFFu) == 0) ++xch_epoch;  // tag 0 = never written
                     c.xch_tag = xch_epoch;
                     CUDA_TRY(launch_merge_grid(c, int(nsub), int(dp.level_width),
-                                               std::min(seg_per_launch, seg_lo + seg_cnt - s0), smem, st));
+                                               std::min(seg_per_launch, seg_lo + seg_cnt - s0), smem, int(grid_nt), st));
                     ++*n_launch;
                 }
                 return MARSIT_OK;

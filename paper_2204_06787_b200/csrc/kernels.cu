@@ -1009,8 +1009,11 @@ __device__ __forceinline__ void cluster_merge_prologue(const ClusterParams& p,
     const uint32_t cr = GRID ? blockIdx.x % p.csize : cluster_ctarank();
     const uint32_t sl = p.seg_lo + blockIdx.x / p.csize;
     const uint32_t sg = p.s_first + sl;
-    const uint32_t mb = p.seg_begin[sl], nm = p.seg_begin[sl + 1] - mb;
-    const uint32_t lb0 = p.lvl_start[sl], nlv = p.lvl_start[sl + 1] - lb0 - 1;
+    // one owned segment (a G = S rank): its merge and level ranges come with
+    // the launch, so the descriptor loads below do not wait on these
+    const uint32_t mb = p.solo_nm ? 0u : p.seg_begin[sl], nm = p.solo_nm ? p.solo_nm : p.seg_begin[sl + 1] - mb;
+    const uint32_t lb0 = p.solo_nm ? 0u : p.lvl_start[sl];
+    const uint32_t nlv = p.solo_nm ? p.solo_nlv : p.lvl_start[sl + 1] - lb0 - 1;
     const uint32_t g_first = cr * p.tile_groups;
     for (uint32_t i = tid; i < nm; i += NT) {
         const DevMerge m = p.merges[mb + i];
@@ -1048,8 +1051,9 @@ __device__ __forceinline__ void cluster_merge_levels(const ClusterParams& p, Clu
     const uint32_t seg_in_launch = blockIdx.x / p.csize;
     const uint32_t sl = p.seg_lo + blockIdx.x / p.csize;
     const uint32_t sg = p.s_first + sl;
-    const uint32_t mb = p.seg_begin[sl];
-    const uint32_t lb0 = p.lvl_start[sl], nlv = p.lvl_start[sl + 1] - lb0 - 1;
+    const uint32_t mb = p.solo_nm ? 0u : p.seg_begin[sl];
+    const uint32_t lb0 = p.solo_nm ? 0u : p.lvl_start[sl];
+    const uint32_t nlv = p.solo_nm ? p.solo_nlv : p.lvl_start[sl + 1] - lb0 - 1;
     const uint32_t g_first = cr * p.tile_groups;
 
     const uint32_t total_groups = p.words_proc / 4;
@@ -1417,13 +1421,29 @@ __global__ void __launch_bounds__(kClusterThreads, 1) merge_cluster_kernel(const
 // K2g: the level loop over csize co-resident CTAs per segment, cross-CTA
 // totals through global memory and one release/acquire barrier per segment
 // and level (cooperative launch).
-template <int NSUB, int NL>
-__global__ void __launch_bounds__(kClusterThreads, 1) merge_grid_kernel(const ClusterParams p) {
+// NT = 1024 (NSUB groups per thread), or 256 / 512 for tiles of at most that
+// many groups (a rank's one or two segments over all SMs): 8 or 16 warps at
+// each CTA barrier and scan instead of 32 of which most hold no group.
+template <int NSUB, int NL, int NT = kClusterThreads>
+__global__ void __launch_bounds__(NT, 1) merge_grid_kernel(const ClusterParams p) {
+#ifdef MARSIT_FUSED_PROF
+    const uint64_t gp_t0 = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0;
+#endif
     extern __shared__ uint4 gr_dyn[];
-    __shared__ ClusterMergeShared<NSUB, NL> sh;
-    cluster_merge_prologue<NSUB, NL, false, true>(p, sh, nullptr);
+    __shared__ ClusterMergeShared<NSUB, NL, NT> sh;
+    cluster_merge_prologue<NSUB, NL, false, true, NT>(p, sh, nullptr);
     __syncthreads();
-    cluster_merge_levels<NSUB, NL, false, true>(p, sh, gr_dyn, nullptr, nullptr);
+#ifdef MARSIT_FUSED_PROF
+    const uint64_t gp_t1 = (threadIdx.x == 0 && blockIdx.x == 0) ? gtime_ns() : 0;
+#endif
+    cluster_merge_levels<NSUB, NL, false, true, NT>(p, sh, gr_dyn, nullptr, nullptr);
+#ifdef MARSIT_FUSED_PROF
+    if (threadIdx.x == 0 && blockIdx.x == 0) {  // slots 8-10: prologue, CTA 0's whole launch, launches
+        atomicAdd(&g_coop_prof[8], (unsigned long long)(gp_t1 - gp_t0));
+        atomicAdd(&g_coop_prof[9], (unsigned long long)(gtime_ns() - gp_t0));
+        atomicAdd(&g_coop_prof[10], 1ull);
+    }
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -2903,20 +2923,20 @@ cudaError_t round_spread_occupancy(int nsub, int nl, uint32_t csize, size_t smem
     MARSIT_FUSED_DISPATCH(spread_occ_t, csize, smem, clusters)
 }
 
-template <int NSUB, int NL>
+template <int NSUB, int NL, int NT = kClusterThreads>
 static cudaError_t grid_attr() {
-    static cudaError_t e = cudaFuncSetAttribute(merge_grid_kernel<NSUB, NL>,
+    static cudaError_t e = cudaFuncSetAttribute(merge_grid_kernel<NSUB, NL, NT>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     return e;
 }
 
-template <int NSUB, int NL>
+template <int NSUB, int NL, int NT = kClusterThreads>
 static cudaError_t grid_launch_t(const ClusterParams& p, uint32_t segments, size_t smem, cudaStream_t st) {
-    cudaError_t e = grid_attr<NSUB, NL>();
+    cudaError_t e = grid_attr<NSUB, NL, NT>();
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(segments * p.csize);
-    cfg.blockDim = dim3(kClusterThreads);
+    cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -2924,23 +2944,33 @@ static cudaError_t grid_launch_t(const ClusterParams& p, uint32_t segments, size
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, merge_grid_kernel<NSUB, NL>, p);
+    return cudaLaunchKernelEx(&cfg, merge_grid_kernel<NSUB, NL, NT>, p);
 }
 
-template <int NSUB, int NL>
+template <int NSUB, int NL, int NT = kClusterThreads>
 static cudaError_t grid_occ_t(size_t smem, int* blocks) {
-    cudaError_t e = grid_attr<NSUB, NL>();
+    cudaError_t e = grid_attr<NSUB, NL, NT>();
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_grid_kernel<NSUB, NL>, kClusterThreads,
-                                                         smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, merge_grid_kernel<NSUB, NL, NT>, NT, smem);
 }
 
 cudaError_t launch_merge_grid(const ClusterParams& p, int nsub, int nl, uint32_t segments, size_t smem,
-                              cudaStream_t st) {
+                              int nt, cudaStream_t st) {
+    if (nt == 256 || nt == 512) {
+        if (nsub != 1) return cudaErrorInvalidValue;
+        if (nt == 256)
+            return nl == 1 ? grid_launch_t<1, 1, 256>(p, segments, smem, st) : grid_launch_t<1, 2, 256>(p, segments, smem, st);
+        return nl == 1 ? grid_launch_t<1, 1, 512>(p, segments, smem, st) : grid_launch_t<1, 2, 512>(p, segments, smem, st);
+    }
     MARSIT_CLUSTER_DISPATCH(grid_launch_t, p, segments, smem, st)
 }
 
-cudaError_t merge_grid_occupancy(int nsub, int nl, size_t smem, int* blocks) {
+cudaError_t merge_grid_occupancy(int nsub, int nl, size_t smem, int nt, int* blocks) {
+    if (nt == 256 || nt == 512) {
+        if (nsub != 1) return cudaErrorInvalidValue;
+        if (nt == 256) return nl == 1 ? grid_occ_t<1, 1, 256>(smem, blocks) : grid_occ_t<1, 2, 256>(smem, blocks);
+        return nl == 1 ? grid_occ_t<1, 1, 512>(smem, blocks) : grid_occ_t<1, 2, 512>(smem, blocks);
+    }
     MARSIT_CLUSTER_DISPATCH(grid_occ_t, smem, blocks)
 }
 
@@ -3158,6 +3188,10 @@ cudaError_t preload_kernels() {
             reinterpret_cast<const void*>(merge_grid_kernel<2, 2>),
             reinterpret_cast<const void*>(merge_grid_kernel<4, 2>),
             reinterpret_cast<const void*>(merge_grid_kernel<8, 2>),
+            reinterpret_cast<const void*>(merge_grid_kernel<1, 1, 256>),
+            reinterpret_cast<const void*>(merge_grid_kernel<1, 2, 256>),
+            reinterpret_cast<const void*>(merge_grid_kernel<1, 1, 512>),
+            reinterpret_cast<const void*>(merge_grid_kernel<1, 2, 512>),
             reinterpret_cast<const void*>(merge_cluster_kernel<1, 1>),
             reinterpret_cast<const void*>(merge_cluster_kernel<2, 1>),
             reinterpret_cast<const void*>(merge_cluster_kernel<4, 1>),

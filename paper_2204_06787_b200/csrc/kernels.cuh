@@ -133,6 +133,7 @@ struct ClusterParams {
     uint32_t xch_tag;             // per launch (host counter; the level is the low 8 bits)
     unsigned* seg_bars;
     uint32_t coin_l1;             // 1: the likely coin window of pass 2 is prefetched into L1
+    uint32_t solo_nm, solo_nlv;   // n_seg == 1: the segment's merges and levels (0: read seg_begin / lvl_start)
     uint32_t coherent;            // 1: leaves and coins were written by this launch (spread
                                   // round): L2-coherent loads, no L1 prefetch
 };
@@ -211,9 +212,10 @@ cudaError_t round_spread_occupancy(int nsub, int nl, uint32_t csize, size_t smem
 cudaError_t merge_cluster_occupancy(int nsub, int nl, uint32_t csize, size_t smem, int* clusters);
 // K2g: the same level loop over csize co-resident CTAs per segment (any
 // number, cooperative launch of `segments` x csize CTAs of kClusterThreads).
+// grid merge CTA size: kClusterThreads, or 256 / 512 threads for tiles of at most that many groups
 cudaError_t launch_merge_grid(const ClusterParams& p, int nsub, int nl, uint32_t segments, size_t smem,
-                              cudaStream_t st);
-cudaError_t merge_grid_occupancy(int nsub, int nl, size_t smem, int* blocks_per_sm);
+                              int nt, cudaStream_t st);
+cudaError_t merge_grid_occupancy(int nsub, int nl, size_t smem, int nt, int* blocks_per_sm);
 
 template <typename T>
 struct StreamParams {
