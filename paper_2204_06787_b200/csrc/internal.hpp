@@ -141,6 +141,7 @@ struct MergeRunner {
     // us, C4 98.6 -> 99.6, G = 8 rank 28.6 -> 30.7, G = 2 34.2 -> 36.4; the
     // C2 / C4 / C5 rounds unchanged within noise — off by default
     uint32_t coin_l1 = uint32_t(env_int("MARSIT_COIN_L1", 0) != 0);
+    uint32_t grid_coop = uint32_t(env_int("MARSIT_GRID_COOP", 1) != 0);  // grid merge: cooperative attribute
     uint32_t csize = 16, tile_groups = 0, nsub = 1, stage = 0, masks = 0;
     size_t merge_smem = 0;  // merge_cluster_kernel's dynamic shared memory (smem minus the fused ring)
     // fused small rounds (round_cluster_kernel): extra shared memory per CTA
@@ -502,6 +503,7 @@ struct MergeRunner {
         c.masks = masks;
         c.prefetch = prefetch;
         c.coin_l1 = coin_l1;
+        c.grid_coop = grid_coop;
         if (n_seg == 1 && dp.lvl_start.size() >= 2) {
             c.solo_nm = dp.n_merges;
             c.solo_nlv = dp.lvl_start[1] - dp.lvl_start[0] - 1;

@@ -2943,7 +2943,7 @@ static cudaError_t grid_launch_t(const ClusterParams& p, uint32_t segments, size
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = p.grid_coop ? 1 : 0;  // the grid is the co-resident CTA count either way
     return cudaLaunchKernelEx(&cfg, merge_grid_kernel<NSUB, NL, NT>, p);
 }
 

@@ -134,6 +134,7 @@ struct ClusterParams {
     unsigned* seg_bars;
     uint32_t coin_l1;             // 1: the likely coin window of pass 2 is prefetched into L1
     uint32_t solo_nm, solo_nlv;   // n_seg == 1: the segment's merges and levels (0: read seg_begin / lvl_start)
+    uint32_t grid_coop;           // grid merge: launched with the cooperative attribute
     uint32_t coherent;            // 1: leaves and coins were written by this launch (spread
                                   // round): L2-coherent loads, no L1 prefetch
 };
