@@ -1535,9 +1535,14 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
                  env_int("MARSIT_FUSED", 1) != 0;
     const bool grid_default = mr.grid;
     const bool kernel_forced = std::getenv("MARSIT_MERGE_KERNEL") != nullptr;
-    // ... and preferably spread over every SM (one launch, MARSIT_SPREAD=0
-    // keeps the cluster-per-segment kernel)
-    ctx->spread = ctx->fused && env_int("MARSIT_SPREAD", 1) != 0;
+    // ... and spread over every SM when the merge chain is short (M <= 8:
+    // C1 27.9 vs 28.8-30.9 us, M = 8 at 1M 47.8 vs 58.9 us; at M = 16 the
+    // cluster-per-segment kernel's 16-CTA merge levels win, 70.5 vs 90.8 us).
+    // MARSIT_SPREAD=1 forces the spread round, 0 the cluster-per-segment one
+    {
+        const int sp = env_int("MARSIT_SPREAD", -1);
+        ctx->spread = ctx->fused && (sp > 0 || (sp < 0 && hs.workers <= 8));
+    }
     if (ctx->fused) {
         mr.cluster = true;
         mr.fused_arrays = ctx->spread ? 0 : hs.workers + 1;
