@@ -680,7 +680,7 @@ struct marsit_ctx {
     // small rounds over every SM: one round_spread_kernel launch (runtime.cu
     // spread_round); preferred to `fused` when it configures
     bool spread = false;
-    bool spread_coop = false;          // MARSIT_SPREAD_COOP=1: + the cooperative attribute (while accepted)
+    bool spread_coop = true;           // + the cooperative attribute while accepted (MARSIT_SPREAD_COOP=0: off)
     uint32_t spread_ctas = 0;          // CTAs of the launch (co-resident clusters x csize)
     // spread round: TMEM columns per thread for the parked u (0: the decode
     // re-reads g, c) and the allocation per CTA

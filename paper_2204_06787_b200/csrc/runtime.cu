@@ -1677,11 +1677,13 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
                     break;
                 }
         }
-        // the grid is sized to the co-resident clusters, so a plain cluster
-        // launch keeps every CTA resident; the cooperative attribute on top
-        // (MARSIT_SPREAD_COOP=1) measured no faster and makes Nsight Compute
-        // fail the launch
-        ctx->spread_coop = env_int("MARSIT_SPREAD_COOP", 0) != 0;
+        // the grid is sized to the co-resident clusters; the cooperative
+        // attribute on top (same speed) also makes the driver guarantee that
+        // residency when other kernels share the GPU (two spread contexts on
+        // concurrent streams could otherwise starve each other's CTAs until
+        // the bounded waits give up).  Nsight Compute fails such launches:
+        // profile with MARSIT_SPREAD_COOP=0
+        ctx->spread_coop = env_int("MARSIT_SPREAD_COOP", 1) != 0;
 
         CUDA_TRY(cudaMalloc(&ctx->spread_sync, sizeof(unsigned) * (2 + ctx->S)));
         CUDA_TRY(cudaMemset(ctx->spread_sync, 0, sizeof(unsigned) * (2 + ctx->S)));

@@ -1,6 +1,6 @@
 # ncu of the spread small round at C1 (eager rounds: a graph replay is not profiled)
 cd $GRAFT_REPO_ROOT
-export PYTHONUNBUFFERED=1 SPREAD_NO_GRAPH=1
+export PYTHONUNBUFFERED=1 SPREAD_NO_GRAPH=1 MARSIT_SPREAD_COOP=0  # ncu fails cooperative cluster launches
 O=gpurun_out/prof2
 mkdir -p $O
 timeout 600 ncu --set full --clock-control none --import-source on -k "regex:round_spread_kernel" -s 30 -c 1 \
