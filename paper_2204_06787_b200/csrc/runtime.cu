@@ -1681,9 +1681,12 @@ marsit_status ctx_create_internal(const marsit_ctx_desc* desc, ncclComm_t shared
         // attribute on top (same speed) also makes the driver guarantee that
         // residency when other kernels share the GPU (two spread contexts on
         // concurrent streams could otherwise starve each other's CTAs until
-        // the bounded waits give up).  Nsight Compute fails such launches:
-        // profile with MARSIT_SPREAD_COOP=0
-        ctx->spread_coop = env_int("MARSIT_SPREAD_COOP", 1) != 0;
+        // the bounded waits give up).  Nsight Compute fails such launches, so
+        // under a profiler's injection (or MARSIT_SPREAD_COOP=0) the launch
+        // is a plain cluster launch
+        const bool profiled = std::getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr ||
+                              std::getenv("CUDA_INJECTION64_PATH") != nullptr;
+        ctx->spread_coop = env_int("MARSIT_SPREAD_COOP", profiled ? 0 : 1) != 0;
 
         CUDA_TRY(cudaMalloc(&ctx->spread_sync, sizeof(unsigned) * (2 + ctx->S)));
         CUDA_TRY(cudaMemset(ctx->spread_sync, 0, sizeof(unsigned) * (2 + ctx->S)));
